@@ -1,0 +1,127 @@
+"""Partition / scheduling oracle (TEST INFRASTRUCTURE).
+
+Paper passages followed:
+  * A (weights or KV) is split along M into m x K tile rows; tile row 0 is in
+    host memory, the rest in GPU memory (reading R7: host = the LEADING rows).
+  * each SM reads exactly one tier; the number of host SMs is set by the target
+    ratio, execution-wave alignment and the congestion cap.
+  * Table 1: without multicast a host tile consumed by several SMs crosses the
+    link once per consumer (read amplification); P:L562-564 — with TMA multicast the tile is
+    fetched once per cluster of consumers.
+  * attention KV partitioned along the batch dimension (paper mode).
+
+Interfaces follow SPEC.md partitioner. The B200 row-range rule is the design's own
+("CTA roles"), pinned here as plain integer arithmetic.
+"""
+from __future__ import annotations
+
+import math
+from fractions import Fraction
+
+
+def round_half_up(v) -> int:
+    """floor(v + 1/2) in exact arithmetic."""
+    return math.floor(Fraction(v) + Fraction(1, 2))
+
+
+def partition_op(M: int, tile_m: int, x) -> tuple[int, int]:
+    """(host tile rows, GPU tile rows) for ratio x: host = round_half_up(x * ceil(M/tile_m))."""
+    if tile_m <= 0 or M <= 0:
+        raise ValueError("dims must be positive")
+    if tile_m > M:
+        raise ValueError("tile_m > M")
+    rows = -(-M // tile_m)
+    host = round_half_up(Fraction(x) * rows)
+    host = min(max(host, 0), rows)
+    return host, rows - host
+
+
+def wave_aligned_sms(host_rows: int, share: int) -> int:
+    """Paper wave alignment, reading R9:
+    the largest n <= share such that host_rows mod n == 0 AND ceil(host_rows/n) ==
+    ceil(host_rows/share) (tiles divide evenly without adding a wave — S:L292's example and
+    S:L320's "never increases waves" invariant, which S:L289/S:L325's "largest divisor" alone
+    would violate, e.g. 8 rows / share 3); if no such n exists, keep the share."""
+    if host_rows <= 0:
+        return 0
+    share = max(1, share)
+    waves = -(-host_rows // share)
+    for n in range(share, 0, -1):
+        if host_rows % n == 0 and -(-host_rows // n) == waves:
+            return n
+    return share
+
+
+def assign_sms(host_rows: int, gpu_rows: int, sm_count: int, cap: int | None = None) -> tuple[int, int]:
+    """Paper SM role assignment.
+
+    proportional share = floor(sm_count * host_rows / total_rows), at least 1 when host rows exist
+    and at most sm_count - 1 when GPU rows exist; with congestion control the share is capped
+    at `cap` before wave alignment. Returns (n_sm_host, n_sm_gpu).
+    """
+    total = host_rows + gpu_rows
+    if host_rows == 0:
+        return 0, sm_count
+    if sm_count < 2 and gpu_rows > 0:
+        raise ValueError("need at least one SM per tier")
+    share = (sm_count * host_rows) // total
+    share = max(1, share)
+    if gpu_rows > 0:
+        share = min(share, sm_count - 1)
+    if cap is not None:
+        share = min(share, cap)
+    n_host = wave_aligned_sms(host_rows, share)
+    return n_host, sm_count - n_host
+
+
+def consumers_per_host_row(N: int, tile_n: int) -> int:
+    """Output column blocks that consume every host tile row of a dense GEMM: ceil(N/tile_n) (Table 1)."""
+    return -(-N // tile_n)
+
+
+def fetches_per_row(consumers: int, multicast: bool, cluster_max: int) -> int:
+    """Link fetches of one host tile row: one per consumer without multicast, one per cluster with it."""
+    if not multicast:
+        return consumers
+    return -(-consumers // max(1, cluster_max))
+
+
+def host_traffic(host_bytes: int, N: int, tile_n: int, multicast: bool = False, cluster_max: int = 1) -> int:
+    """Bytes crossing the host link for one GEMM over a host block (Table 1)."""
+    return host_bytes * fetches_per_row(consumers_per_host_row(N, tile_n), multicast, cluster_max)
+
+
+# ----------------------------------------------------------------------------------------------
+# B200 design rules — pure integer arithmetic, pinned bit-exactly against the ABI
+# ----------------------------------------------------------------------------------------------
+
+
+def balanced_ranges(R: int, n: int) -> list[tuple[int, int]]:
+    """Split R rows over n CTAs into contiguous ranges [floor(jR/n), floor((j+1)R/n)):
+    sizes differ by at most one row — row-granular wave alignment."""
+    if n <= 0:
+        return []
+    return [((j * R) // n, ((j + 1) * R) // n) for j in range(n)]
+
+
+def linear_row_ranges(M: int, h: int, n_cta_host: int, n_cta_hbm: int):
+    """Row ownership for dak_linear: host CTAs split rows [0,h), HBM CTAs split [h,M)."""
+    out = []
+    for a, b in balanced_ranges(h, n_cta_host):
+        out.append(("host", a, b))
+    for a, b in balanced_ranges(M - h, n_cta_hbm):
+        out.append(("hbm", h + a, h + b))
+    return out
+
+
+def host_pages_prefix(n_pages: int, ratio, chunk_pages: int) -> int:
+    """Attention page placement (reading in DESIGN.md): the oldest
+    round_half_up(ratio * n_chunks) split-KV chunks of a sequence live on the host."""
+    n_chunks = -(-n_pages // chunk_pages)
+    host_chunks = round_half_up(Fraction(ratio) * n_chunks)
+    return min(n_pages, host_chunks * chunk_pages)
+
+
+def batch_split_host_requests(B: int, ratio) -> int:
+    """Paper attention mode: whole requests on host; round_half_up(ratio * B) of them."""
+    return min(B, max(0, round_half_up(Fraction(ratio) * B)))
