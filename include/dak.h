@@ -1,0 +1,180 @@
+/*
+ * dak.h — C ABI of the B200-native DAK decode hot path (arxiv 2604.26074, "DAK: Direct-Access-
+ * Enabled GPU Memory Offloading with Optimal Efficiency for LLM Inference").
+ *
+ * Citations: P:L<n> = /root/reference/PAPER.md line n (section noted), S:L<n> = SPEC.md line n.
+ *
+ * Conventions (all entry points):
+ *  - Every call returns dak_status (DAK_OK == 0). No exception crosses the ABI. On failure
+ *    dak_last_error() returns a thread-local, human-readable message (valid until the next call
+ *    on the same thread).
+ *  - The CALLER owns every buffer. Op calls never allocate device or host memory; workspace is
+ *    passed in and its size comes from the pure *_workspace_size queries. dak_host_alloc /
+ *    dak_host_free are separate setup helpers for the host tier.
+ *  - Device pointers must be 16-byte aligned (bulk-copy requirement) or the call returns
+ *    DAK_EINVAL. Host-tier pointers must be pinned AND mapped into the device address space
+ *    (cudaHostAlloc(cudaHostAllocMapped|cudaHostAllocPortable), cudaHostRegister(...Mapped) or
+ *    dak_host_alloc); with UVA the host pointer is the device pointer.
+ *  - Op calls are asynchronous on the given stream (a cudaStream_t passed as void*; NULL = the
+ *    legacy default stream). Asynchronous CUDA errors surface at the caller's next sync.
+ *    Op calls contain no host synchronisation and no allocation, so they can be captured in a
+ *    CUDA graph. Calls on distinct streams are thread-safe.
+ *  - bf16 tensors are IEEE bfloat16 bit patterns (uint16). Accumulation is fp32; outputs are
+ *    rounded to bf16 with round-to-nearest-even.
+ */
+#ifndef DAK_H_
+#define DAK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dak_status;
+#define DAK_OK 0
+#define DAK_EINVAL 1        /* bad argument (shape, alignment, mode, NULL)                 */
+#define DAK_ECAPACITY 2     /* required host bytes exceed offloadable bytes / host capacity */
+#define DAK_EUNSUPPORTED 3  /* valid request outside what this build implements            */
+#define DAK_ECUDA 4         /* a CUDA runtime/driver call failed (message has the detail)  */
+#define DAK_ENCCL 5         /* an NCCL call failed                                          */
+
+typedef void* dak_stream_t; /* cudaStream_t */
+
+const char* dak_last_error(void);
+const char* dak_version(void);
+/* Number of SMs of the current device (launch sizing; DAK_ECUDA without a device). */
+dak_status dak_device_sms(int32_t* sms);
+
+/* =============================================================================================
+ * 1. Planner — greedy per-op offload ratios (§3.2; App. A)
+ * ============================================================================================= */
+
+/* Machine model. B_g = hbm_bps; B_h = min(link_bps, host_dram_bps) (P:L216 footnote).
+ * Bandwidths in bytes/s (> 0). host_capacity_bytes < 0 means unlimited. */
+typedef struct {
+  double hbm_bps;
+  double link_bps;
+  double host_dram_bps;
+  int64_t host_capacity_bytes;
+} dak_hw;
+
+#define DAK_OP_LINEAR 0     /* C_i = weight bytes                              (P:L422 fn) */
+#define DAK_OP_ATTENTION 1  /* C_i = KV-cache bytes                            (P:L422 fn) */
+
+/* One offloadable operation. The op's matrix is cut into n_units placement units (linear:
+ * unit_rows output rows; attention: split-KV chunks or whole requests); host units are
+ * the LEADING units. total_bytes = C_i; every unit is unit_bytes except possibly the
+ * last: (n_units-1)*unit_bytes < total_bytes <= n_units*unit_bytes. t_comp_s = T_comp (>= 0). */
+typedef struct {
+  int32_t kind;
+  int32_t reserved;
+  int64_t n_units;
+  int64_t unit_bytes;
+  int64_t total_bytes;
+  double t_comp_s;
+} dak_op;
+
+typedef struct {
+  int64_t host_units;  /* units placed in host memory (leading units)                      */
+  int64_t host_bytes;  /* = host_units*unit_bytes, or total_bytes when all units are host    */
+  double ratio;        /* host_units / n_units (x_i of P:L466)                               */
+  int32_t phase;       /* last greedy phase that gave this op budget: 0 none, 1..3 */
+  int32_t reserved;
+  double latency_s;    /* max(T_comp, (C-y)/B_g, y/B_h) at the planned y   */
+} dak_op_plan;
+
+#define DAK_PLAN_EXACT 0    /* place >= y_req_bytes on host, greedy phases 1->3 (R4)  */
+#define DAK_PLAN_BALANCED 1 /* place max(y_req, sum of memory-bound turning points)  */
+
+/* Three-phase greedy at unit granularity; readings R1, R4-R6 of DESIGN.md.
+ * Deterministic and bit-identical to oracle/planner.py:plan_units (IEEE double, fixed formula
+ * order, no FMA contraction). out: caller array of n_ops. objective_s (nullable): sum of the
+ * per-op latencies (App. A objective).
+ * Errors: DAK_EINVAL (n_ops <= 0, NULL, non-positive bandwidth, inconsistent units, y_req < 0,
+ * bad mode); DAK_ECAPACITY (y_req > sum total_bytes or > host capacity). */
+dak_status dak_plan_ratios(const dak_hw* hw, const dak_op* ops, int32_t n_ops, int64_t y_req_bytes,
+                           int32_t mode, dak_op_plan* out, double* objective_s);
+
+/* =============================================================================================
+ * 2. Host tier memory (SMs stream host data straight into SMEM; no HBM staging)
+ * ============================================================================================= */
+
+/* Pinned, device-mapped, portable host allocation (optionally write-combined). *dev_ptr
+ * receives the device alias (== host pointer under UVA). numa_node >= 0 binds the pages to that
+ * node before pinning (-1: first-touch). */
+dak_status dak_host_alloc(size_t bytes, int32_t write_combined, int32_t numa_node, void** host_ptr, void** dev_ptr);
+dak_status dak_host_free(void* host_ptr);
+
+/* =============================================================================================
+ * 3. Split-source linear: y = act(x W^T + bias) + residual   (§3.1)
+ *    W [M,K] is split along M: rows [0,h) in host memory, rows [h,M) in HBM (R7/R14).
+ * ============================================================================================= */
+
+/* Kernel-native weight layout ("DAK-KC"): a tier block of R rows is stored chunk-major,
+ * [ceil(K/KC)][R][KC] bf16, each row's KC elements forming KC/64 atoms of 128 B whose 16-byte
+ * chunks are XOR-swizzled by (row & 7) (bank-conflict-free ldmatrix / LDS.128). One k-chunk of
+ * any contiguous row range is then ONE contiguous span -> one bulk copy per pipeline stage.
+ * Requirements: K % 64 == 0, KC % 64 == 0, KC <= 2048. */
+size_t dak_linear_packed_bytes(int64_t rows, int64_t K, int32_t kc);
+
+/* Re-layout a row-major block src [rows, K] (bf16) into the DAK-KC layout at dst.
+ * src/dst may be device or mapped-host pointers (the copy runs on the GPU, async on stream). */
+dak_status dak_pack_linear(const void* src, int64_t rows, int64_t K, int32_t kc, void* dst, dak_stream_t stream);
+
+/* Preferred KC for an op (chunk width so one stage of the per-CTA row range is ~16-48 KB). */
+int32_t dak_linear_default_kc(int64_t M, int64_t K, int32_t n_ctas);
+
+#define DAK_ACT_NONE 0
+#define DAK_ACT_RELU 1
+
+typedef struct {
+  int32_t n_cta_host;         /* CTAs that read the host tier (0: auto from calibration)       */
+  int32_t n_cta_hbm;          /* CTAs that read HBM (0: SMs - n_cta_host)                      */
+  int32_t window;             /* congestion window W: max in-flight host stages per CTA*/
+  int32_t stages;             /* SMEM ring depth for HBM CTAs (0: fill shared memory)          */
+  int32_t congestion_control; /* 1: cap host CTAs / window as calibrated          */
+  int32_t pdl;                /* 1: programmatic dependent launch (weights stream before the   */
+                              /*    previous kernel finishes; x/residual read after it)        */
+  int32_t force_path;         /* 0 auto, 1 CUDA-core FMA path, 2 tensor-core (mma.sync) path   */
+  int32_t reserved;
+} dak_launch_cfg;
+
+typedef struct {
+  const void* w_host;   /* DAK-KC packed rows [0,h)   (mapped host; may be NULL when h == 0)  */
+  const void* w_hbm;    /* DAK-KC packed rows [h,M)   (device; may be NULL when h == M)       */
+  int64_t M, K, h;      /* 0 <= h <= M                                                         */
+  int32_t kc;           /* KC used to pack both tiers                                          */
+  int32_t N;            /* batch columns, 1..16                                                */
+  const void* x;        /* [N, K] bf16 row-major, device                                       */
+  void* y;              /* [N, M] bf16 row-major, device                                       */
+  const void* bias;     /* [M] bf16 or NULL                                                    */
+  const void* residual; /* [N, M] bf16 or NULL (added after the activation; may alias y)      */
+  int32_t act;          /* DAK_ACT_*                                                           */
+  int32_t reserved;
+  dak_launch_cfg cfg;
+} dak_linear_args;
+
+/* Launch description (pure query; used by tests and the bench to attribute bytes). */
+typedef struct {
+  int32_t grid, n_cta_host, n_cta_hbm, threads;
+  int32_t stages_hbm, window_host, smem_bytes, path; /* path: 1 FMA, 2 mma.sync               */
+  int64_t rows_per_cta_host_max, rows_per_cta_hbm_max;
+  int64_t hbm_bytes, host_bytes;                      /* algorithmic weight bytes per tier     */
+} dak_linear_launch_info;
+
+dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);
+
+/* Row ownership of CTA `cta` (0 <= cta < grid): tier (0 HBM, 1 host) and [row_begin,row_end)
+ * in global row numbering. Host CTAs split [0,h), HBM CTAs split [h,M), each into contiguous
+ * ranges whose sizes differ by at most one row. Pure query. */
+dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t* tier, int64_t* row_begin, int64_t* row_end);
+
+/* Enqueue the split GEMV / skinny GEMM. */
+dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAK_H_ */

@@ -1,0 +1,58 @@
+"""Build libdak.so (the C-ABI library) in-tree with nvcc for sm_100a.
+
+Usage: python -m paper_2604_26074_b200.build   (also called by __graft_entry__.build()).
+Every translation unit is compiled with -gencode arch=compute_100a,code=sm_100a -lineinfo; the
+planner additionally with -ffp-contract=off (bit-exact double arithmetic, reading R6).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+OUT = os.path.join(PKG, "libdak.so")
+OBJ = os.path.join(ROOT, "build", "obj")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+SOURCES = [
+    ("abi.cpp", []),
+    ("planner.cpp", ["-Xcompiler", "-ffp-contract=off", "-fmad=false"]),
+    ("linear.cu", []),
+]
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("build failed: " + " ".join(cmd))
+    return r.stdout + r.stderr
+
+
+def build(verbose: bool = False) -> str:
+    os.makedirs(OBJ, exist_ok=True)
+    objs = []
+    for src, extra in SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(OBJ, src + ".o")
+        deps = [path, os.path.join(CSRC, "common.h"), os.path.join(ROOT, "include", "dak.h")]
+        if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
+                   "-Xptxas", "-v" if verbose else "-O3", *extra, "-c", path, "-o", obj]
+            if src.endswith(".cpp"):
+                cmd = [NVCC, "-x", "cu", *cmd[1:]] if False else cmd
+            out = _run(cmd)
+            if verbose:
+                sys.stderr.write(out)
+        objs.append(obj)
+    if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
+        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"])
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

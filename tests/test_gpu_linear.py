@@ -1,0 +1,167 @@
+"""GPU parity of dak_linear (split GEMV / skinny GEMM, PAPER §3.1) against the CPU oracle.
+
+All calls go through the C ABI (libdak.so) via the ctypes binding. Tolerance (north star):
+bf16 outputs with fp32 accumulation within 1e-2 relative; integer inputs bit-exact.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import kernels as Kx
+from oracle import planner as P
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def D():
+    from paper_2604_26074_b200 import dak
+    return dak
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+    assert torch.cuda.is_available()
+    return torch
+
+
+def run_linear(D, torch, W, x, h, kc, bias=None, residual=None, act=0, **cfg):
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    M, K = W.shape
+    N = x.shape[0]
+    sl = SplitLinear(D, W, h, kc)
+    xd = to_dev(x)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    bd = to_dev(bias) if bias is not None else None
+    rd = to_dev(residual) if residual is not None else None
+    a = sl.args(xd, y, N, bias=bd, residual=rd, act=act, **cfg)
+    D.linear(a)
+    torch.cuda.synchronize()
+    return from_dev(y), sl, a
+
+
+CASES = [  # (M, K, N, h, kc) — several tiles, ragged row counts, both tiers, both paths
+    (300, 512, 1, 37, 64),
+    (1000, 1024, 3, 0, 128),
+    (777, 2048, 4, 777, 256),
+    (4096, 4096, 1, 32, 512),
+    (513, 256, 8, 100, 64),
+    (1024, 4096, 16, 48, 256),
+    (2000, 1536, 5, 16, 512),
+    (129, 8192, 12, 1, 1024),
+    (5000, 128, 2, 2500, 64),
+]
+
+
+@pytest.mark.parametrize("M,K,N,h,kc", CASES)
+def test_linear_parity(D, torch, M, K, N, h, kc):
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, M + N), bias=True)
+    y, _, _ = run_linear(D, torch, W, x, h, kc, bias=b)
+    ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y), ref)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("N", [1, 4])
+def test_linear_integer_exact(D, torch, path, N):
+    """Integer inputs in [-2, 2]: every partial sum is an exact small integer -> bitwise equal."""
+    M, K = 611, 2048
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, 7), kind="int", bias=True)
+    y, _, _ = run_linear(D, torch, W, x, 40, 256, bias=b, force_path=path)
+    ref = Kx.split_linear(W[:40], W[40:], x, bias_bits=b)
+    assert np.array_equal(Kx.bf16_to_f64(y), ref)
+
+
+@pytest.mark.parametrize("N,kc", [(1, 512), (3, 64), (8, 256), (16, 128)])
+def test_linear_r_invariance_bitwise(D, torch, N, kc):
+    """Outputs are bitwise identical for every split point h and CTA count (fixed KC)."""
+    M, K = 1536, 4096
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, 11))
+    outs = []
+    for h, nh in ((0, 1), (16, 1), (300, 2), (768, 3), (M, 5)):
+        y, _, _ = run_linear(D, torch, W, x, h, kc, n_cta_host=nh)
+        outs.append(y)
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(outs[0]), Kx.linear(W, x))
+
+
+def test_linear_epilogue_relu_residual_inplace(D, torch):
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    M, K, N = 1000, 2048, 8
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, 13), bias=True)
+    res = synth.normal_bf16(np.random.default_rng(3), (N, M))
+    sl = SplitLinear(D, W, 64, 256)
+    xd = to_dev(x)
+    y = to_dev(res)  # residual aliases y (in-place residual add, decoder layer use)
+    D.linear(sl.args(xd, y, N, bias=to_dev(b), residual=y, act=D.ACT_RELU))
+    torch.cuda.synchronize()
+    ref = Kx.linear(W, x, bias_bits=b, act="relu", residual_bits=res)
+    assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_linear_paths_agree(D, torch, path):
+    M, K, N = 2048, 4096, 4
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, 17))
+    y, _, _ = run_linear(D, torch, W, x, 32, 512, force_path=path)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y), Kx.linear(W, x))
+
+
+def test_linear_pdl_chain(D, torch):
+    """A chain y1 = W1 x, y2 = W2 y1, y3 = W3 y2 launched with programmatic dependent launch:
+    weights stream early, the x read waits for the producer kernel (griddepcontrol.wait)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    K = 2048
+    N = 2
+    g = np.random.default_rng(5)
+    Ws = [synth.normal_bf16(g, (K, K), std=1 / np.sqrt(K)) for _ in range(3)]
+    x = synth.normal_bf16(g, (N, K))
+    sls = [SplitLinear(D, W, 32 * (i + 1), 256) for i, W in enumerate(Ws)]
+    bufs = [to_dev(x)] + [torch.empty((N, K), dtype=torch.int16, device="cuda") for _ in range(3)]
+    for rep in range(3):
+        for i in range(3):
+            D.linear(sls[i].args(bufs[i], bufs[i + 1], N, pdl=1))
+    torch.cuda.synchronize()
+    ref = x
+    for W in Ws:
+        r = Kx.linear(W, ref)
+        ref = synth.bf16_bits(r.astype(np.float32))  # bf16 RNE between ops (float32 rounding then bf16)
+    got = from_dev(bufs[3])
+    assert_close(Kx.bf16_to_f64(got), Kx.bf16_to_f64(ref), rtol=2e-2)
+
+
+def test_c1_full_size_at_planner_ratio(D, torch):
+    """BASELINE configs[0]: 4096x4096 bf16 GEMV, N=1, split at the planner's BALANCED ratio
+    (unit 16 rows), in the launch configuration bench.py times; full output compared."""
+    M = K = 4096
+    Bg, Bh = 6555.5e9, 51.5e9
+    plan, _ = D.plan_ratios(dict(hbm_bps=Bg, link_bps=Bh, host_dram_bps=Bh),
+                            [dict(n_units=M // 16, unit_bytes=16 * K * 2, total_bytes=M * K * 2, T=0.0)], 0,
+                            D.PLAN_BALANCED)
+    h = plan[0]["host_units"] * 16
+    assert 16 <= h <= 64
+    W, x, _ = synth.linear_inputs(M, K, 1, seed=synth.seed_for(0, 0))
+    kc = D.default_kc(M, K, 147)
+    y, sl, a = run_linear(D, torch, W, x, h, kc)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y), Kx.linear(W, x))
+    info = D.linear_query(a)
+    assert info["n_cta_host"] >= 1 and info["host_bytes"] == h * K * 2
+
+
+@pytest.mark.parametrize("M,K,N", [(28672, 7168, 8), (7168, 28672, 1), (50272, 7168, 8)])
+def test_opt30b_shapes_sampled(D, torch, M, K, N):
+    """OPT-30B fc1 / fc2 / LM-head shapes (configs[1]) at r ~ r*: sampled rows vs the row-loop oracle."""
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(1, M % 1000))
+    h = 16 * max(1, round(M * 0.0078 / 16))
+    y, _, _ = run_linear(D, torch, W, x, h, D.default_kc(M, K, 147))
+    rows = np.unique(np.concatenate([np.arange(0, 40), np.arange(h - 8, h + 8),
+                                     np.random.default_rng(0).integers(0, M, 200), np.arange(M - 20, M)]))
+    ref = Kx.linear_rowloop(W[rows], x)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y[:, rows]), ref)

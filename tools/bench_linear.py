@@ -1,0 +1,97 @@
+"""Kernel-level timing of dak_linear (development tool; bench.py is the contract harness).
+
+Times a CUDA graph of back-to-back split linears, rotating >= 4 x L2 of distinct HBM weight
+copies (and distinct host copies), and prints algorithmic GB/s per configuration as JSON lines.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_26074_b200 import dak  # noqa: E402
+
+L2 = 132644864
+
+
+def setup(M, K, N, h, kc, copies):
+    hbm = [torch.randn((M - h) * K, device="cuda").to(torch.bfloat16).view(torch.int16) if h < M else None
+           for _ in range(copies)]
+    hosts = []
+    for _ in range(copies if h else 0):
+        hp, dp = dak.host_alloc(max(h * K * 2, 16))
+        hosts.append((hp, dp))
+        src = (torch.randn(h * K, device="cuda") * 0.01).to(torch.bfloat16)
+        dak.pack_linear(src, h, K, kc, dp)
+    x = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    y = torch.empty(N, M, device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    return hbm, hosts, x, y
+
+
+def time_cfg(M, K, N, h, kc, launches=64, reps=10, **cfg):
+    size = M * K * 2
+    copies = max(2, min(64, int(np.ceil(4 * L2 / max(size, 1)))))
+    hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
+    args = []
+    for i in range(launches):
+        a = dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg)
+        args.append(a)
+    info = dak.linear_query(args[0])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for a in args[:4]:
+            dak.linear(a, s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for a in args:
+                dak.linear(a, s)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(reps):
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / launches * 1e-3)
+    t = float(np.median(ts))
+    alg = size + N * K * 2 + N * M * 2
+    for hp, _ in hosts:
+        dak.host_free(hp)
+    del hbm
+    torch.cuda.empty_cache()
+    return dict(M=M, K=K, N=N, h=h, kc=kc, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
+                host_gbs=h * K * 2 / t / 1e9, info={k: info[k] for k in ("grid", "n_cta_host", "stages_hbm", "window_host",
+                                                                        "smem_bytes", "path")}, cfg=cfg)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    a = ap.parse_args()
+    shapes = [(4096, 4096), (7168, 7168), (28672, 7168), (7168, 28672)]
+    Ns = [1, 8] if a.quick else [1, 2, 4, 8, 16]
+    for (M, K) in shapes:
+        kc = dak.default_kc(M, K, 147)
+        for N in Ns:
+            for h in (0, 16 * max(1, round(M * 0.0069 / 16))):
+                r = time_cfg(M, K, N, h, kc)
+                print(json.dumps(r), flush=True)
+    # pdl on / off and stage sweep at C1
+    for pdl in (0, 1):
+        print(json.dumps(time_cfg(4096, 4096, 1, 32, 512, pdl=pdl)), flush=True)
+    for st in (2, 3, 4, 6):
+        print(json.dumps(time_cfg(28672, 7168, 8, 0, 64, stages=st)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
