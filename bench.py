@@ -1,0 +1,322 @@
+"""DAK decode hot-path benchmark (driver contract; see DESIGN.md §7 "Measurement").
+
+Default workload (BASELINE.json configs[1]): OPT-30B decode step, batch 8, context 64 (prompt 32 +
+32 decoded), weights split HBM / pinned host memory at the planner's BALANCED ratios
+(every memory-bound op at its turning point B_l/(B_g+B_l)), one CUDA graph per step
+(P:L637). A step = embed -> 48 x (LN, QKV split-GEMM, KV append, split attention + combine,
+O split-GEMM + residual, LN, FC1 split-GEMM + ReLU, FC2 split-GEMM + residual) -> LN -> LM head.
+
+metric: aggregate GB/s = (weight + KV bytes read from HBM and host per step) / step time.
+Also reported: decode tokens/s, per-tier bytes, roofline of the dominant kernel (dak_linear),
+the CPU oracle baseline, clocks, and an end-to-end number with host buffers.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload c1]
+Under torchrun every rank runs an independent replica (weak scaling, no data-path collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "aggregate GB/s (HBM+host link) vs roofline; decode tokens/s at 1/2/4/8 B200"
+LINK_GBS_DEFAULT = 51.5  # profiles/r01/calib_loadpath.jsonl: SM bulk-copy read of pinned host memory
+
+
+def measured_peaks():
+    hbm, link = None, None
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        pass
+    try:
+        best = 0.0
+        with open(os.path.join(ROOT, "profiles", "r01", "calib_loadpath.jsonl")) as f:
+            for line in f:
+                r = json.loads(line)
+                if r.get("test") in ("host_bulk", "host_tma"):
+                    best = max(best, r.get("host_gbs", 0.0))
+        link = best or None
+    except Exception:
+        pass
+    return (hbm or 6650.0), (link or LINK_GBS_DEFAULT), ("measured" if hbm else "fallback")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int, path: str):
+        self.path = path
+        self.p = None
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["unavailable"])
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return dict(sm_mhz=statistics.median(sm) if sm else None, sm_max_mhz=mx, reasons=sorted(reasons),
+                    samples=len(sm))
+
+
+def dist_setup():
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def reduce_max(v: float, world: int) -> float:
+    if world <= 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU oracle baseline (the oracle as it stands; a bounded sample of the same workload)
+# ------------------------------------------------------------------------------------------------
+def oracle_sample(batch: int, min_seconds: float = 10.0):
+    """OPT-30B layer-0 operators (q/k/v/o, fc1, fc2 as float64 oracle linears at N=batch, plus the
+    layer's decode attention for all 56 heads over the 64-token context), repeated until
+    >= min_seconds of CPU work. Returns (GB/s of algorithmic bytes, seconds, bytes, threads)."""
+    import numpy as np
+    import synth
+    from oracle import kernels as Kx
+    g = np.random.default_rng(synth.seed_for(1, 0))
+    H, F, heads, ctx = 7168, 28672, 56, 64
+    shapes = [(3 * H, H), (H, H), (F, H), (H, F)]
+    mats = [synth.normal_bf16(g, s, 1.0 / np.sqrt(s[1])) for s in shapes]
+    xs = [synth.normal_bf16(g, (batch, s[1])) for s in shapes]
+    q, K, V = synth.kv_inputs([ctx] * batch, heads, 128, heads, seed=synth.seed_for(1, 1))
+    nbytes = sum(m.size * 2 for m in mats) + sum(k.size * 2 * 2 for k in K)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        for W, x in zip(mats, xs):
+            Kx.linear(W, x)
+        Kx.attention_dense(q, K, V)
+        reps += 1
+        if time.perf_counter() - t0 >= min_seconds:
+            break
+    dt = time.perf_counter() - t0
+    threads = int(os.environ.get("OMP_NUM_THREADS", "0")) or os.cpu_count()
+    return nbytes * reps / dt / 1e9, dt, nbytes * reps, threads, reps
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle on bounded samples of the same workload (rank 0 only)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(a.warmup):
+        oracle_sample(a.batch, min_seconds=0.0)
+    gbs = []
+    t_all = 0.0
+    for _ in range(a.steps):
+        v, dt, nb, threads, reps = oracle_sample(a.batch, min_seconds=0.0)
+        gbs.append(v)
+        t_all += dt
+    value = statistics.median(gbs)
+    ms = t_all / a.steps * 1e3
+    sample = "OPT-30B layer 0: q/k/v/o, fc1, fc2 float64 oracle linears at N=%d + decode attention (56 heads, 64 tokens)" % a.batch
+    line = dict(metric=METRIC, value=round(value, 3), unit="GB/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
+                ms_per_step=round(ms, 3), higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f64",
+                data="synthetic", impl="reference",
+                config=dict(workload="opt-30b-decode-b%d-ctx%d (oracle sample)" % (a.batch, a.context), batch=a.batch,
+                            context=a.context),
+                cpu_baseline=dict(value=round(value, 3), unit="GB/s", cores=threads, kind="oracle", sample=sample),
+                e2e=dict(value=round(value, 3), unit="GB/s", h2d_bytes_per_step=0, d2h_bytes_per_step=0),
+                gpu_launches=0)
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="dak", choices=["dak", "reference"])
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--context", type=int, default=64)
+    ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--no-cc", action="store_true")
+    ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layers", type=int, default=48, help="(debug) fewer layers; invalid as a bench number")
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    if a.impl == "reference":
+        return run_reference(a)
+
+    import torch
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import DakOPT, HW, OPT_30B, OPTConfig
+
+    world, rank, local = dist_setup()
+    hbm_gbs, link_gbs, peak_src = measured_peaks()
+    hw = HW(hbm_bps=hbm_gbs * 1e9, link_bps=link_gbs * 1e9)
+    cfg = OPT_30B if a.layers == 48 else OPTConfig(n_layers=a.layers)
+    eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
+                 congestion_control=not a.no_cc, seed=1234 + rank)
+    if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
+        tot = sum(o["total_bytes"] for o in eng.plan_ops)
+        eng.close()
+        eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
+                     congestion_control=not a.no_cc, seed=1234 + rank)
+    nb = eng.bytes_per_step()
+    stream = torch.cuda.Stream()
+    g = eng.capture(stream)
+    for _ in range(a.warmup):
+        g.replay()
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed region: K graph replays (inputs 60 GB >> 126 MB L2: no flush)
+    sampler = ClockSampler(local, os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else "/tmp",
+                                               f"clocks_rank{rank}.csv"))
+    time.sleep(0.3)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(a.steps):
+            g.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    clocks = sampler.stop()
+    t = e0.elapsed_time(e1) / 1e3
+    t_max = reduce_max(t, world)
+    step_s = t_max / a.steps
+    value = nb["total"] * world * a.steps / t_max / 1e9
+    tok_s = a.batch * world * a.steps / t_max
+
+    # ---------------- end to end through the public API with host buffers
+    tok_host = torch.zeros(a.batch, dtype=torch.int32).pin_memory()
+    logits_host = torch.empty(a.batch, cfg.vocab, dtype=torch.bfloat16).pin_memory()
+    barrier(world)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for i in range(a.steps):
+            tok_host.fill_(i % cfg.vocab)
+            eng.tokens.copy_(tok_host, non_blocking=True)
+            g.replay()
+            logits_host.copy_(eng.logits, non_blocking=True)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    te = reduce_max(e0.elapsed_time(e1) / 1e3, world)
+    e2e = dict(value=round(nb["total"] * world * a.steps / te / 1e9, 2), unit="GB/s",
+               tokens_per_s=round(a.batch * world * a.steps / te, 2),
+               h2d_bytes_per_step=tok_host.numel() * 4, d2h_bytes_per_step=logits_host.numel() * 2)
+
+    # ---------------- roofline of the dominant kernel (dak_linear), CUDA events on its stream
+    lin_bytes, lin_time = 0, 0.0
+    evs = []
+    ops = list(eng.linear_ops())
+    xs = torch.zeros(a.batch, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
+    ys = torch.empty(a.batch, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
+    with torch.cuda.stream(stream):
+        for op in ops:
+            la = dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, a.batch, xs, ys,
+                                 cfg=dict(congestion_control=int(not a.no_cc)))
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+            dak.linear(la, stream)
+            s1.record(stream)
+            evs.append((s0, s1, op.M * op.K * 2 + a.batch * (op.K + op.M) * 2))
+    torch.cuda.synchronize()
+    for s0, s1, b in evs:
+        lin_time += s0.elapsed_time(s1) / 1e3
+        lin_bytes += b
+    lin_achieved = lin_bytes / lin_time / 1e9
+    lin_share = lin_time / step_s
+    peak = hbm_gbs + link_gbs
+    roofline = dict(bound="hbm", achieved=round(lin_achieved, 1), peak=round(peak, 1), unit="GB/s",
+                    frac=round(lin_achieved / peak, 4), traffic=None,
+                    kernel="dak_linear (split GEMV/skinny GEMM, all %d launches of a step, per-launch events, no PDL)" % len(ops),
+                    peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json) + measured host link %.1f GB/s" % (peak_src, hbm_gbs, link_gbs),
+                    step_frac=round(value / world / peak, 4),
+                    kernel_time_share_of_step=round(lin_share, 4))
+
+    line = dict(metric=METRIC, value=round(value, 2), unit="GB/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
+                ms_per_step=round(step_s * 1e3, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
+                dtype="bf16", data="synthetic (random-init OPT-30B weights and KV)",
+                config=dict(workload="opt-30b-decode-b%d-ctx%d" % (a.batch, a.context), model_shape="OPT-30B",
+                            batch=a.batch, context=a.context, layers=cfg.n_layers,
+                            plan="BALANCED" if a.ratio is None else "EXACT R=%.4f" % a.ratio,
+                            host_bytes_per_step=nb["host"], hbm_bytes_per_step=nb["hbm"],
+                            host_ratio=round(nb["host"] / nb["total"], 5),
+                            l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
+                            pdl=not a.no_pdl, congestion_control=not a.no_cc,
+                            parallelism="dp%d replicas (weak scaling, no collective)" % world),
+                tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
+                gpu_launches=eng.kernels_per_step() * a.steps)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        v, dt, nbytes, threads, reps = oracle_sample(a.batch)
+        line["cpu_baseline"] = dict(value=round(v, 3), unit="GB/s", cores=threads, kind="oracle",
+                                    sample="OPT-30B layer-0 q/k/v/o/fc1/fc2 float64 oracle linears (N=%d) + 56-head "
+                                           "decode attention over 64 tokens, x%d (%.1f s)" % (a.batch, reps, dt))
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

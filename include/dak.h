@@ -174,6 +174,107 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
 /* Enqueue the split GEMV / skinny GEMM. */
 dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream);
 
+/* =============================================================================================
+ * 4. Split paged GQA decode attention  (P:L631 SplitK_FlashAttn; P:L386 decode attention)
+ *    o[b, h] = softmax(scale * K_b q[b,h]) V_b over the tokens [0, seq_len[b]) of request b,
+ *    kv head g = h / (Hq/Hkv); K_b, V_b gathered through block_table[b]; bit 31 of an entry
+ *    selects the host pool, the low 31 bits index the page in that pool.
+ * ============================================================================================= */
+
+/* KV page layout ("DAK-PG"): a pool is [P][Hkv][page_size][d] bf16; each [page_size][d] block
+ * stores the 16-byte chunk j of token row t at ((j>>3)<<3) | ((j&7) ^ (t&7)). Token slots of a
+ * page beyond seq_len must hold finite values (pools are zero-initialised by their owner). */
+dak_status dak_pack_kv_pages(const void* src, int64_t n_blocks, int32_t page_size, int32_t d, void* dst,
+                             dak_stream_t stream);
+
+typedef struct {
+  const void* q;                /* [B, Hq, d] bf16, device                                      */
+  void* out;                    /* [B, Hq, d] bf16, device                                      */
+  const void* k_hbm;            /* DAK-PG pools in HBM (NULL if no HBM pages)                   */
+  const void* v_hbm;
+  const void* k_host;           /* DAK-PG pools in pinned mapped host memory (NULL if none)     */
+  const void* v_host;
+  const int32_t* block_table;   /* [B, max_pages] device; bit 31 = host tier                   */
+  const int32_t* seq_lens;      /* [B] device, 1 <= seq_len <= max_pages*page_size              */
+  int32_t B, Hq, Hkv, d;        /* d == 128; Hq % Hkv == 0; Hq/Hkv <= 8                         */
+  int32_t page_size;            /* tokens per page, multiple of 16, <= 256                      */
+  int32_t max_pages;            /* block-table row length                                       */
+  int32_t chunk_pages;          /* split-KV chunk (pages); a chunk's tier = its first page's    */
+  float scale;                  /* softmax scale; <= 0 means 1/sqrt(d) (SDPA default)          */
+  void* workspace;              /* device, >= dak_attention_workspace_size bytes                */
+  size_t workspace_bytes;
+  dak_launch_cfg cfg;           /* n_cta_host, n_cta_hbm, window, stages, congestion_control,   */
+                                /* pdl are honoured; force_path is ignored                      */
+  int64_t q_row_stride;         /* elements between requests in q (0: Hq*d; fused QKV: (Hq+2Hkv)*d) */
+} dak_attention_args;
+
+/* Pure query: workspace bytes (split-KV partials: B*Hkv*ceil(max_pages/chunk_pages)*(Hq/Hkv)*(d+1)*4). */
+dak_status dak_attention_workspace_size(const dak_attention_args* args, size_t* bytes);
+
+/* Enqueue split attention + the chunk combine (two kernels on `stream`). */
+dak_status dak_attention(const dak_attention_args* args, dak_stream_t stream);
+
+/* Decode KV write: the K/V rows of the new token of every (request, kv head) go to position
+ * positions[b] of request b (page block_table[b][pos / page_size], row pos % page_size), in the
+ * tier the block-table entry names. k_new, v_new: [B, Hkv*d] bf16 device rows, row_stride
+ * elements apart (0: Hkv*d; rows of a fused QKV output: (Hq+2Hkv)*d). */
+dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_stride, const int32_t* block_table,
+                         const int32_t* positions, int32_t B, int32_t Hkv, int32_t d, int32_t page_size,
+                         int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
+                         dak_stream_t stream);
+
+/* =============================================================================================
+ * 5. Decoder-layer decode step (the split operators as drop-in replacements inside
+ *    the model; whole decode step CUDA-graph captured) and its glue kernels
+ * ============================================================================================= */
+
+/* y[r] = (x[r] - mean) * rsqrt(var + eps) * w + b over `cols`, fp32 statistics (b nullable). */
+dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, int32_t rows, int32_t cols, float eps,
+                         int32_t pdl, dak_stream_t stream);
+
+/* x[b] = tok_emb[tokens[b]] + pos_emb[positions[b] + pos_offset]  (pos_emb/positions nullable;
+ * OPT uses pos_offset 2). tokens/positions: device int32 [B]. */
+dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,
+                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, int32_t pdl, dak_stream_t stream);
+
+/* One split weight of a layer: DAK-KC packed tiers (rows [0,h) host, [h,M) HBM), KC, bias. */
+typedef struct {
+  const void* w_host;
+  const void* w_hbm;
+  int64_t h;
+  int32_t kc;
+  int32_t n_cta_host;   /* 0: the layer cfg's value */
+  const void* bias;     /* nullable */
+} dak_weight;
+
+#define DAK_MODEL_OPT 0   /* pre-LayerNorm, biases, ReLU MLP (OPT family)            */
+
+typedef struct {
+  int32_t model;                      /* DAK_MODEL_OPT                                        */
+  int32_t B, hidden, n_heads, n_kv_heads, head_dim, ffn;
+  float ln_eps;
+  dak_weight qkv;                     /* fused [q;k;v] rows: (n_heads + 2 n_kv_heads) * head_dim */
+  dak_weight o, up, down;             /* OPT: up = fc1 (ReLU), down = fc2                     */
+  const void *ln1_w, *ln1_b, *ln2_w, *ln2_b;
+  void* x;                            /* [B, hidden] bf16 residual stream, updated in place   */
+  void* scratch;                      /* device, >= dak_layer_scratch_size                    */
+  size_t scratch_bytes;
+  void *k_hbm, *v_hbm, *k_host, *v_host;  /* this layer's KV pools (DAK-PG)                   */
+  const int32_t* block_table;         /* [B, max_pages], bit 31 = host                         */
+  const int32_t* positions;           /* [B] position of the new token                         */
+  const int32_t* seq_lens;            /* [B] = positions + 1                                   */
+  int32_t page_size, max_pages, chunk_pages;
+  int32_t tp_rank, tp_size;           /* tp_size must be 1 in this build                       */
+  int32_t reserved;
+  dak_launch_cfg cfg;                 /* linear ops (pdl applies to every kernel)              */
+  dak_launch_cfg attn_cfg;            /* attention                                             */
+} dak_layer_args;
+
+dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);
+/* Enqueue one decode step of one layer: 9 kernels (LN, QKV, KV append, attention + combine,
+ * O + residual, LN, FC1 + ReLU, FC2 + residual). */
+dak_status dak_layer(const dak_layer_args* args, dak_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

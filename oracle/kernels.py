@@ -32,6 +32,18 @@ def bf16_to_f64(bits) -> np.ndarray:
     return b.view(np.float32).astype(np.float64)
 
 
+def round_to_bf16(v) -> np.ndarray:
+    """Round float64 values to the nearest bf16 (ties to even), returned as float64.
+
+    The GPU stores fp32 results as bf16 with round-to-nearest-even; for an exact (integer)
+    accumulation this is the exact expected stored value. Direct f64 -> bf16 (no f32 detour):
+    v = m * 2^e with m in [0.5, 1); bf16 keeps 8 significant bits -> rint(m * 2^8) / 2^8 * 2^e
+    (np.rint rounds half to even). Subnormal bf16 results are out of scope (|v| >= 2^-126)."""
+    v = np.asarray(v, dtype=np.float64)
+    m, e = np.frexp(v)
+    return np.ldexp(np.rint(m * 256.0) / 256.0, e)
+
+
 def _act(t: np.ndarray, act: str) -> np.ndarray:
     if act == "none":
         return t

@@ -22,6 +22,8 @@ SOURCES = [
     ("abi.cpp", []),
     ("planner.cpp", ["-Xcompiler", "-ffp-contract=off", "-fmad=false"]),
     ("linear.cu", []),
+    ("attention.cu", []),
+    ("layer.cu", []),
 ]
 
 

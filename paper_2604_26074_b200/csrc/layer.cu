@@ -1,0 +1,222 @@
+// dak_layer — one decoder-layer decode step composed from the split-source operators
+// (SplitK_GEMM / SplitK_FlashAttn as drop-in nn.Linear / SDPA replacements,
+// the whole decode step captured in a CUDA graph). Glue kernels: LayerNorm, token+position
+// embedding. OPT layer (pre-LN, biases, ReLU MLP, learned positions; P:L690 model family):
+//
+//   h = LN1(x); qkv = h Wqkv^T + b; append k, v at pos; a = attn(q, KV); x += a Wo^T + bo
+//   h = LN2(x); f = relu(h W1^T + b1); x += f W2^T + b2
+//
+// Every weight is split host/HBM at its planned ratio. Each kernel is launched with
+// programmatic dependent launch when cfg.pdl is set, so the next op's weight stream starts while
+// the previous op drains (griddepcontrol.wait guards every dependent read).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "common.h"
+
+namespace dak {
+namespace layer {
+
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+constexpr int kLnThreads = 256;
+
+__device__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < kLnThreads / 32; ++i) t += red[i];  // fixed order: deterministic
+  __syncthreads();
+  return t;
+}
+
+// y[r] = (x[r] - mean) / sqrt(var + eps) * w + b   (fp32 statistics, two-pass)
+__global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                               const __nv_bfloat16* __restrict__ w,
+                                                               const __nv_bfloat16* __restrict__ b,
+                                                               __nv_bfloat16* __restrict__ y, int cols, float eps) {
+  __shared__ float red[kLnThreads / 32];
+  grid_dep_launch();
+  grid_dep_wait();
+  const __nv_bfloat16* xr = x + (long long)blockIdx.x * cols;
+  float s = 0.f;
+  for (int c = threadIdx.x; c < cols; c += kLnThreads) s += __bfloat162float(xr[c]);
+  const float mean = block_sum(s, red) / (float)cols;
+  float v = 0.f;
+  for (int c = threadIdx.x; c < cols; c += kLnThreads) {
+    const float d = __bfloat162float(xr[c]) - mean;
+    v += d * d;
+  }
+  const float rstd = rsqrtf(block_sum(v, red) / (float)cols + eps);
+  __nv_bfloat16* yr = y + (long long)blockIdx.x * cols;
+  for (int c = threadIdx.x; c < cols; c += kLnThreads) {
+    float t = (__bfloat162float(xr[c]) - mean) * rstd;
+    t = t * __bfloat162float(w[c]) + (b ? __bfloat162float(b[c]) : 0.f);
+    yr[c] = __float2bfloat16_rn(t);
+  }
+}
+
+// x[b] = tok[tokens[b]] + pos[positions[b] + pos_offset]
+__global__ void embed_kernel(const int* __restrict__ tokens, const int* __restrict__ positions,
+                             const __nv_bfloat16* __restrict__ tok, const __nv_bfloat16* __restrict__ pos, int hidden,
+                             int pos_offset, __nv_bfloat16* __restrict__ x) {
+  grid_dep_launch();
+  grid_dep_wait();
+  const int b = blockIdx.x;
+  const long long t = tokens[b];
+  const long long p = positions ? (long long)positions[b] + pos_offset : -1;
+  for (int c = threadIdx.x; c < hidden; c += blockDim.x) {
+    float v = __bfloat162float(tok[t * hidden + c]);
+    if (pos && p >= 0) v += __bfloat162float(pos[p * hidden + c]);
+    x[(long long)b * hidden + c] = __float2bfloat16_rn(v);
+  }
+}
+
+static dak_status launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, cudaStream_t s, int pdl) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelExC(&cfg, fn, args));
+  return DAK_OK;
+}
+
+static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+struct Scratch {
+  size_t h, qkv, attn, f, ws, total, ws_bytes;
+};
+
+static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
+  if (a->model != DAK_MODEL_OPT) return fail(DAK_EUNSUPPORTED, "dak_layer: model %d not in this build", a->model);
+  if (a->B <= 0 || a->hidden <= 0 || a->n_heads <= 0 || a->n_kv_heads <= 0 || a->head_dim != 128 || a->ffn <= 0)
+    return fail(DAK_EINVAL, "dak_layer: bad model sizes");
+  if (a->n_heads * a->head_dim != a->hidden) return fail(DAK_EINVAL, "dak_layer: n_heads * head_dim != hidden");
+  const size_t B = a->B;
+  const size_t qkv_cols = (size_t)(a->n_heads + 2 * a->n_kv_heads) * a->head_dim;
+  dak_attention_args at{};
+  at.B = a->B; at.Hq = a->n_heads; at.Hkv = a->n_kv_heads; at.d = a->head_dim;
+  at.page_size = a->page_size; at.max_pages = a->max_pages; at.chunk_pages = a->chunk_pages;
+  at.cfg.n_cta_hbm = 1;
+  size_t ws = 0;
+  dak_status st = dak_attention_workspace_size(&at, &ws);
+  if (st != DAK_OK) return st;
+  s->h = 0;
+  s->qkv = align256(s->h + B * a->hidden * 2);
+  s->attn = align256(s->qkv + B * qkv_cols * 2);
+  s->f = align256(s->attn + B * a->hidden * 2);
+  s->ws = align256(s->f + B * a->ffn * 2);
+  s->ws_bytes = ws;
+  s->total = s->ws + ws;
+  return DAK_OK;
+}
+
+static dak_linear_args lin_args(const dak_weight& w, long long M, long long K, int N, const void* x, void* y,
+                                const void* residual, int act, const dak_launch_cfg& cfg) {
+  dak_linear_args l{};
+  l.w_host = w.w_host;
+  l.w_hbm = w.w_hbm;
+  l.M = M; l.K = K; l.h = w.h; l.kc = w.kc; l.N = N;
+  l.x = x; l.y = y; l.bias = w.bias; l.residual = residual; l.act = act;
+  l.cfg = cfg;
+  l.cfg.n_cta_host = w.n_cta_host > 0 ? w.n_cta_host : cfg.n_cta_host;
+  return l;
+}
+
+}  // namespace layer
+}  // namespace dak
+
+using namespace dak;
+
+extern "C" {
+
+dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, int32_t rows, int32_t cols, float eps,
+                         int32_t pdl, dak_stream_t stream) {
+  if (!x || !w || !y || rows <= 0 || cols <= 0) return fail(DAK_EINVAL, "dak_layernorm: bad arguments");
+  const __nv_bfloat16* xp = (const __nv_bfloat16*)x;
+  const __nv_bfloat16* wp = (const __nv_bfloat16*)w;
+  const __nv_bfloat16* bp = (const __nv_bfloat16*)b;
+  __nv_bfloat16* yp = (__nv_bfloat16*)y;
+  int c = cols;
+  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps};
+  return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
+                           (cudaStream_t)stream, pdl);
+}
+
+dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,
+                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, int32_t pdl, dak_stream_t stream) {
+  if (!tokens || !tok_emb || !x || B <= 0 || hidden <= 0) return fail(DAK_EINVAL, "dak_embed: bad arguments");
+  const int* tp = tokens;
+  const int* pp = positions;
+  const __nv_bfloat16* te = (const __nv_bfloat16*)tok_emb;
+  const __nv_bfloat16* pe = (const __nv_bfloat16*)pos_emb;
+  int h = hidden, off = pos_offset;
+  __nv_bfloat16* xp = (__nv_bfloat16*)x;
+  void* args[] = {&tp, &pp, &te, &pe, &h, &off, &xp};
+  return layer::launch_pdl((const void*)layer::embed_kernel, dim3(B), dim3(256), args, (cudaStream_t)stream, pdl);
+}
+
+dak_status dak_layer_scratch_size(const dak_layer_args* a, size_t* bytes) {
+  if (!a || !bytes) return fail(DAK_EINVAL, "dak_layer_scratch_size: NULL");
+  layer::Scratch s;
+  dak_status st = layer::scratch_layout(a, &s);
+  if (st != DAK_OK) return st;
+  *bytes = s.total;
+  return DAK_OK;
+}
+
+dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
+  if (!a) return fail(DAK_EINVAL, "dak_layer: NULL");
+  layer::Scratch s;
+  dak_status st = layer::scratch_layout(a, &s);
+  if (st != DAK_OK) return st;
+  if (!a->x || !a->scratch || a->scratch_bytes < s.total) return fail(DAK_EINVAL, "dak_layer: x / scratch missing or too small");
+  if (a->tp_size > 1) return fail(DAK_EUNSUPPORTED, "dak_layer: tensor parallel layer not in this build");
+  char* sc = (char*)a->scratch;
+  void* h = sc + s.h;
+  char* qkv = sc + s.qkv;
+  void* attn = sc + s.attn;
+  void* f = sc + s.f;
+  const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads;
+  const long long qkv_cols = (long long)(Hq + 2 * Hkv) * d;
+  const int pdl = a->cfg.pdl;
+  cudaStream_t strm = (cudaStream_t)stream;
+
+  if ((st = dak_layernorm(a->x, a->ln1_w, a->ln1_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
+  dak_linear_args l = layer::lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
+  if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  if ((st = dak_kv_append(qkv + (size_t)Hq * d * 2, qkv + (size_t)(Hq + Hkv) * d * 2, qkv_cols, a->block_table,
+                          a->positions, B, Hkv, d, a->page_size, a->max_pages, a->k_hbm, a->v_hbm, a->k_host,
+                          a->v_host, pdl, strm)) != DAK_OK)
+    return st;
+  dak_attention_args at{};
+  at.q = qkv; at.out = attn;
+  at.k_hbm = a->k_hbm; at.v_hbm = a->v_hbm; at.k_host = a->k_host; at.v_host = a->v_host;
+  at.block_table = a->block_table; at.seq_lens = a->seq_lens;
+  at.B = B; at.Hq = Hq; at.Hkv = Hkv; at.d = d;
+  at.page_size = a->page_size; at.max_pages = a->max_pages; at.chunk_pages = a->chunk_pages;
+  at.scale = 0.f;
+  at.workspace = sc + s.ws; at.workspace_bytes = s.ws_bytes;
+  at.cfg = a->attn_cfg;
+  at.cfg.pdl = pdl;
+  at.q_row_stride = qkv_cols;
+  if ((st = dak_attention(&at, strm)) != DAK_OK) return st;
+  l = layer::lin_args(a->o, H, (long long)Hq * d, B, attn, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  if ((st = dak_layernorm(a->x, a->ln2_w, a->ln2_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
+  l = layer::lin_args(a->up, a->ffn, H, B, h, f, nullptr, DAK_ACT_RELU, a->cfg);
+  if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  l = layer::lin_args(a->down, H, a->ffn, B, f, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  return dak_linear(&l, strm);
+}
+
+}  // extern "C"

@@ -108,8 +108,12 @@ __device__ __forceinline__ uint32_t swz(long long r_tier, int sl) {
 }
 
 // ------------------------------------------------------------------------------------ kernel
-// PATH 1: CUDA-core FMA, NN = N (1..4). PATH 2: mma.sync, NT = ceil(N/8) n8-tiles (1..2).
-template <int PATH, int NN>
+// PATH 1: CUDA-core FMA, NN = N (1..4), MTW = rows per thread bucket.
+// PATH 2: mma.sync,      NN = n8 tiles (1..2), MTW = m16 tiles per warp bucket.
+// Every loop whose body holds a .sync.aligned instruction has a compile-time trip count, so the
+// hot loop is branch-free (the first build spent ~30 SASS instructions per HMMA on predicates,
+// WARPSYNC and ring-index divisions — profiles/r01/linear_v0_ncu.txt).
+template <int PATH, int NN, int MTW>
 __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params p) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -150,36 +154,36 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
 
   const uint32_t w_bytes = (uint32_t)R * kc * 2;
   const uint32_t x_bytes = (uint32_t)kc * 2;
+  const long long chunk_stride = R_tier * kc * 2;  // bytes between consecutive k-chunks of a row
 
   if (warp == 0) {
-    // ============================ producer: one lane issues the W stream, lanes issue x rows
+    // ============================ producer: lane 0 streams W, lanes 0..N-1 stream x rows
     const int pro = min(slots, nchunks);
-    for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
-      if (lane == 0) {
+    const char* src = wsrc + rb * kc * 2;
+    if (lane == 0) {
+      for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
         mbar_expect_tx(&full[i], w_bytes + (uint32_t)N * x_bytes);
-        const char* src = wsrc + ((long long)i * R_tier + rb) * kc * 2;
-        bulk_g2s(wring + (size_t)i * p.w_stage_bytes, src, w_bytes, &full[i]);
+        bulk_g2s(wring + (size_t)i * p.w_stage_bytes, src + (long long)i * chunk_stride, w_bytes, &full[i]);
       }
     }
     grid_dep_wait();  // x is produced by the previous kernel
     __syncwarp();
-    for (int i = 0; i < pro; ++i)
-      for (int n = lane; n < N; n += 32)
-        bulk_g2s(xring + (size_t)i * p.x_stage_bytes + n * p.x_pitch, p.x + (long long)n * p.K + (long long)i * kc,
-                 x_bytes, &full[i]);
+    const __nv_bfloat16* xrow = p.x + (long long)lane * p.K;
+    if (lane < N)
+      for (int i = 0; i < pro; ++i)
+        bulk_g2s(xring + (size_t)i * p.x_stage_bytes + lane * p.x_pitch, xrow + (long long)i * kc, x_bytes, &full[i]);
+    int s = pro == slots ? 0 : pro;
+    uint32_t ph = pro == slots ? 1u : 0u;
     for (int i = pro; i < nchunks; ++i) {
-      const int s = i % slots;
-      const uint32_t ph = (uint32_t)(i / slots) & 1u;
       if (lane == 0) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], w_bytes + (uint32_t)N * x_bytes);
-        const char* src = wsrc + ((long long)i * R_tier + rb) * kc * 2;
-        bulk_g2s(wring + (size_t)s * p.w_stage_bytes, src, w_bytes, &full[s]);
+        bulk_g2s(wring + (size_t)s * p.w_stage_bytes, src + (long long)i * chunk_stride, w_bytes, &full[s]);
       }
       __syncwarp();
-      for (int n = lane; n < N; n += 32)
-        bulk_g2s(xring + (size_t)s * p.x_stage_bytes + n * p.x_pitch, p.x + (long long)n * p.K + (long long)i * kc,
-                 x_bytes, &full[s]);
+      if (lane < N)
+        bulk_g2s(xring + (size_t)s * p.x_stage_bytes + lane * p.x_pitch, xrow + (long long)i * kc, x_bytes, &full[s]);
+      if (++s == slots) { s = 0; ph ^= 1u; }
     }
     return;
   }
@@ -187,18 +191,29 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
   // ================================ consumers
   const int t = threadIdx.x - 32;
   const int cw = warp - 1;
+  const uint32_t wring_u = su32(wring), xring_u = su32(xring);
   if constexpr (PATH == 1) {
+    constexpr int RPT = MTW;
     const int S = kc >> 3;   // 16-byte slices per row chunk
     const int G = kConsumers / S;
     const int sl = t % S, rg = t / S;
-    float acc[kRptMax][NN];
+    const uint32_t row_bytes = (uint32_t)kc * 2;
+    // per-row byte offsets inside a stage (swizzle key = tier-local row & 7), hoisted out of the loop
+    uint32_t roff[RPT];
 #pragma unroll
-    for (int j = 0; j < kRptMax; ++j)
+    for (int j = 0; j < RPT; ++j) {
+      const int r = rg + G * j;
+      roff[j] = (uint32_t)r * row_bytes + swz(rb + r, sl);
+    }
+    float acc[RPT][NN];
+#pragma unroll
+    for (int j = 0; j < RPT; ++j)
 #pragma unroll
       for (int n = 0; n < NN; ++n) acc[j][n] = 0.f;
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
-      const int s = i % slots;
-      mbar_wait(&full[s], (uint32_t)(i / slots) & 1u);
+      mbar_wait(&full[s], ph);
       const unsigned char* ws = wring + (size_t)s * p.w_stage_bytes;
       const unsigned char* xs = xring + (size_t)s * p.x_stage_bytes;
       float xf[NN][8];
@@ -209,10 +224,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
         xf[n][4] = bf_lo(v.z); xf[n][5] = bf_hi(v.z); xf[n][6] = bf_lo(v.w); xf[n][7] = bf_hi(v.w);
       }
 #pragma unroll
-      for (int j = 0; j < kRptMax; ++j) {
-        const int r = rg + G * j;
-        if (r < R) {
-          const uint4 v = *reinterpret_cast<const uint4*>(ws + (size_t)r * kc * 2 + swz(rb + r, sl));
+      for (int j = 0; j < RPT; ++j) {
+        if (rg + G * j < R) {
+          const uint4 v = *reinterpret_cast<const uint4*>(ws + roff[j]);
           const float w[8] = {bf_lo(v.x), bf_hi(v.x), bf_lo(v.y), bf_hi(v.y), bf_lo(v.z), bf_hi(v.z), bf_lo(v.w), bf_hi(v.w)};
 #pragma unroll
           for (int n = 0; n < NN; ++n) {
@@ -225,11 +239,12 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == slots) { s = 0; ph ^= 1u; }
     }
     // reduce the S slice-partials of each row: shuffle inside groups of min(S,32) lanes ...
     const int L = S < 32 ? S : 32;
 #pragma unroll
-    for (int j = 0; j < kRptMax; ++j)
+    for (int j = 0; j < RPT; ++j)
 #pragma unroll
       for (int n = 0; n < NN; ++n)
         for (int off = L >> 1; off >= 1; off >>= 1) acc[j][n] += __shfl_xor_sync(0xffffffffu, acc[j][n], off);
@@ -238,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
     const int wg = (t % S) >> 5;
     if ((t % L) == 0) {
 #pragma unroll
-      for (int j = 0; j < kRptMax; ++j) {
+      for (int j = 0; j < RPT; ++j) {
         const int r = rg + G * j;
         if (r < R)
 #pragma unroll
@@ -260,50 +275,57 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
     const int WK = KS < kConsumerWarps ? KS : kConsumerWarps;
     const int WM = kConsumerWarps / WK;
     const int wk = cw % WK, wm = cw / WK;
+    const int nks = KS / WK;  // k-steps per warp per stage
     const int MT = (R + 15) >> 4;
-    float acc[kMtwMax][NT][4];
+    float acc[MTW][NT][4];
 #pragma unroll
-    for (int a = 0; a < kMtwMax; ++a)
+    for (int a = 0; a < MTW; ++a)
 #pragma unroll
       for (int b = 0; b < NT; ++b)
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.f;
-    const int arow = lane & 15, ahalf = lane >> 4;
-    const int bn = (lane & 7) + ((lane >> 4) << 3), bhalf = (lane >> 3) & 1;
+    const uint32_t row_bytes = (uint32_t)kc * 2;
+    // A rows: tile mt = wm + WM*mi covers rows 16*mt .. +15; lane supplies row (lane & 15).
+    // All tiles of a warp are 16*WM rows apart, so the swizzle key (row & 7) is per-thread constant.
+    const uint32_t a_base = (uint32_t)(wm * 16 + (lane & 15)) * row_bytes;
+    const uint32_t a_step = (uint32_t)(WM * 16) * row_bytes;
+    const int key = (int)((rb + wm * 16 + (lane & 15)) & 7);
+    const int ahalf = lane >> 4;
+    const uint32_t b_base = (uint32_t)((lane & 7) + ((lane >> 4) << 3)) * p.x_pitch + ((lane >> 3) & 1) * 16;
+    int s = 0;
+    uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
-      const int s = i % slots;
-      mbar_wait(&full[s], (uint32_t)(i / slots) & 1u);
-      const uint32_t ws = su32(wring + (size_t)s * p.w_stage_bytes);
-      const uint32_t xs = su32(xring + (size_t)s * p.x_stage_bytes);
-      for (int ks = wk; ks < KS; ks += WK) {
+      mbar_wait(&full[s], ph);
+      const uint32_t ws = wring_u + (uint32_t)s * p.w_stage_bytes + a_base;
+      const uint32_t xs = xring_u + (uint32_t)s * p.x_stage_bytes + b_base;
+      for (int j = 0; j < nks; ++j) {
+        const int ks = wk + j * WK;
         uint32_t b[NT][2];
         if constexpr (NT == 1) {
-          ldsm_x2(xs + bn * p.x_pitch + (ks * 16 + bhalf * 8) * 2, b[0][0], b[0][1]);
+          ldsm_x2(xs + ks * 32, b[0][0], b[0][1]);
         } else {
-          ldsm_x4(xs + bn * p.x_pitch + (ks * 16 + bhalf * 8) * 2, b[0][0], b[0][1], b[1][0], b[1][1]);
+          ldsm_x4(xs + ks * 32, b[0][0], b[0][1], b[1][0], b[1][1]);
         }
         const int sl = 2 * ks + ahalf;
+        const uint32_t coff = (uint32_t)(((sl >> 3) << 7) | (((sl & 7) ^ key) << 4));
 #pragma unroll
-        for (int mi = 0; mi < kMtwMax; ++mi) {
-          const int mt = wm + WM * mi;
-          if (mt < MT) {
-            const int r = mt * 16 + arow;
-            uint32_t a0, a1, a2, a3;
-            ldsm_x4(ws + (uint32_t)r * kc * 2 + swz(rb + r, sl), a0, a1, a2, a3);
+        for (int mi = 0; mi < MTW; ++mi) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4(ws + mi * a_step + coff, a0, a1, a2, a3);
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) mma_bf16(acc[mi][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
-          }
+          for (int nt = 0; nt < NT; ++nt) mma_bf16(acc[mi][nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == slots) { s = 0; ph ^= 1u; }
     }
     // deterministic cross-warp reduction over the WK warps sharing m-tiles (fixed wk order)
     const int g = lane >> 2, c2 = (lane & 3) * 2;
     for (int round = 0; round < WK; ++round) {
       if (wk == round) {
 #pragma unroll
-        for (int mi = 0; mi < kMtwMax; ++mi) {
+        for (int mi = 0; mi < MTW; ++mi) {
           const int mt = wm + WM * mi;
           if (mt < MT) {
 #pragma unroll
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
   grid_dep_wait();  // residual / y may belong to the previous kernel
   const int RN = PATH == 1 ? NN : N;
   for (int q = t; q < R * N; q += kConsumers) {
-    const int n = q / R, r = q % R;
+    const int n = q / R, r = q - n * R;
     float v = res[(size_t)r * RN + n];
     const long long m = row0 + r;
     if (p.bias) v += __bfloat162float(p.bias[m]);
@@ -359,7 +381,7 @@ __global__ void pack_kernel(const uint4* __restrict__ src, long long rows, long 
 // ------------------------------------------------------------------------------------ host side
 struct Plan {
   Params p;
-  int path, nn, grid, smem;
+  int path, nn, bucket, grid, smem;
   long long rmax_host, rmax_hbm;
 };
 
@@ -375,6 +397,16 @@ static dak_status device_sms(int* out) {
 }
 
 static inline long long ceil_div(long long a, long long b) { return (a + b - 1) / b; }
+
+// compiled unroll buckets: FMA rows-per-thread and MMA m16-tiles-per-warp
+static const int kRptBuckets[] = {1, 2, 4, 8, 16};
+static const int kMtwBuckets[] = {1, 2, 3, 4, 6, 8, 12};
+
+static int bucket_of(const int* b, int n, long long need) {
+  for (int i = 0; i < n; ++i)
+    if (b[i] >= need) return b[i];
+  return -1;
+}
 
 // Rows a CTA may own for a given KC (accumulator capacity of each path).
 static long long path_row_cap(int path, int kc) {
@@ -409,10 +441,17 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     dak_status st = device_sms(&sms);
     if (st != DAK_OK) return st;
   }
-  int path = c.force_path ? c.force_path : (N <= 4 ? 1 : 2);
+  // default: tensor-core path for every N (the CUDA-core FMA loop cannot issue fast enough to
+  // keep up with HBM); force_path 1 selects it for N <= 4.
+  int path = c.force_path ? c.force_path : 2;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   if (path != 1 && path != 2) return fail(DAK_EINVAL, "dak_linear: bad force_path");
-  const long long cap = path_row_cap(path, kc);
+  // rows per CTA are bounded by the accumulator capacity of the path and by SMEM: at least three
+  // ring stages of (rows x KC) weights plus the x rows must fit (deep enough to cover HBM latency)
+  const long long x_stage = ceil_div((long long)ceil_div(N, 8) * 8 * (kc * 2 + 16), 128) * 128;
+  const long long smem_rows = ((kSmemBudget - 1024 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
+  const long long cap = std::min(path_row_cap(path, kc), smem_rows);
+  if (cap < 16) return fail(DAK_EUNSUPPORTED, "dak_linear: kc=%d leaves no room for a 16-row stage", kc);
 
   int n_host = 0;
   if (h > 0) {
@@ -431,6 +470,22 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   const long long rmax = std::max(rmax_host, rmax_hbm);
   if (rmax > cap) return fail(DAK_EUNSUPPORTED, "dak_linear: %lld rows per CTA exceed the path capacity %lld (use a smaller kc)", rmax, cap);
 
+  // unroll bucket and the rows one stage must hold (MMA tiles read whole 16-row groups)
+  long long rows_alloc;
+  int bucket;
+  if (path == 1) {
+    const int G = kConsumers / (kc / 8);
+    bucket = bucket_of(kRptBuckets, 5, ceil_div(rmax, G));
+    rows_alloc = ceil_div(rmax, 16) * 16;
+  } else {
+    const int KS = kc / 16;
+    const int WK = KS < kConsumerWarps ? KS : kConsumerWarps;
+    const int WM = kConsumerWarps / WK;
+    bucket = bucket_of(kMtwBuckets, 7, ceil_div(ceil_div(rmax, 16), WM));
+    rows_alloc = (long long)WM * bucket * 16;
+  }
+  if (bucket < 0) return fail(DAK_EUNSUPPORTED, "dak_linear: no unroll bucket for %lld rows per CTA", rmax);
+
   Params p{};
   p.w_host = (const char*)a->w_host;
   p.w_hbm = (const char*)a->w_hbm;
@@ -441,7 +496,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.residual = (const __nv_bfloat16*)a->residual;
   p.act = a->act;
   p.n_host = n_host; p.n_hbm = n_hbm;
-  p.w_stage_bytes = (int)(ceil_div(rmax, 16) * 16 * kc * 2);
+  p.w_stage_bytes = (int)(rows_alloc * kc * 2);
   p.x_pitch = kc * 2 + 16;
   const int x_rows = path == 1 ? N : (int)ceil_div(N, 8) * 8;
   p.x_stage_bytes = (int)(ceil_div((long long)x_rows * p.x_pitch, 128) * 128);
@@ -471,6 +526,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   out->p = p;
   out->path = path;
   out->nn = path == 1 ? N : (int)ceil_div(N, 8);
+  out->bucket = bucket;
   out->grid = n_host + n_hbm;
   out->smem = p.res_offset + res_bytes;
   out->rmax_host = rmax_host;
@@ -478,13 +534,13 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   return DAK_OK;
 }
 
-template <int PATH, int NN>
+template <int PATH, int NN, int B>
 static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
-  auto kern = split_linear_kernel<PATH, NN>;
+  auto kern = split_linear_kernel<PATH, NN, B>;
   static int smem_set = 0;  // raise the opt-in limit once per instance (not a stream op; capture-safe)
-  if (pl.smem > smem_set) {
+  if (!smem_set) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
-    smem_set = kSmemBudget;
+    smem_set = 1;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(pl.grid);
@@ -500,19 +556,43 @@ static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
   return DAK_OK;
 }
 
+template <int PATH, int NN>
+static dak_status launch_b(const Plan& pl, cudaStream_t s, int pdl) {
+  if constexpr (PATH == 1) {
+    switch (pl.bucket) {
+      case 1: return launch_t<1, NN, 1>(pl, s, pdl);
+      case 2: return launch_t<1, NN, 2>(pl, s, pdl);
+      case 4: return launch_t<1, NN, 4>(pl, s, pdl);
+      case 8: return launch_t<1, NN, 8>(pl, s, pdl);
+      case 16: return launch_t<1, NN, 16>(pl, s, pdl);
+    }
+  } else {
+    switch (pl.bucket) {
+      case 1: return launch_t<2, NN, 1>(pl, s, pdl);
+      case 2: return launch_t<2, NN, 2>(pl, s, pdl);
+      case 3: return launch_t<2, NN, 3>(pl, s, pdl);
+      case 4: return launch_t<2, NN, 4>(pl, s, pdl);
+      case 6: return launch_t<2, NN, 6>(pl, s, pdl);
+      case 8: return launch_t<2, NN, 8>(pl, s, pdl);
+      case 12: return launch_t<2, NN, 12>(pl, s, pdl);
+    }
+  }
+  return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for bucket %d", pl.bucket);
+}
+
 static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
   if (pl.path == 1) {
     switch (pl.nn) {
-      case 1: return launch_t<1, 1>(pl, s, pdl);
-      case 2: return launch_t<1, 2>(pl, s, pdl);
-      case 3: return launch_t<1, 3>(pl, s, pdl);
-      case 4: return launch_t<1, 4>(pl, s, pdl);
+      case 1: return launch_b<1, 1>(pl, s, pdl);
+      case 2: return launch_b<1, 2>(pl, s, pdl);
+      case 3: return launch_b<1, 3>(pl, s, pdl);
+      case 4: return launch_b<1, 4>(pl, s, pdl);
     }
   } else {
     switch (pl.nn) {
-      case 1: return launch_t<2, 1>(pl, s, pdl);
-      case 2: return launch_t<2, 2>(pl, s, pdl);
+      case 1: return launch_b<2, 1>(pl, s, pdl);
+      case 2: return launch_b<2, 2>(pl, s, pdl);
     }
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for path %d / %d", pl.path, pl.nn);

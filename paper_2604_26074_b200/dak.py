@@ -90,7 +90,23 @@ _sig("dak_linear_cta_rows", C.c_int32, [C.POINTER(dak_linear_args), C.c_int32, C
                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 _sig("dak_linear", C.c_int32, [C.POINTER(dak_linear_args), C.c_void_p])
 
-EXPORTED = ["dak_last_error", "dak_version", "dak_device_sms", "dak_plan_ratios", "dak_host_alloc", "dak_host_free",
+class dak_attention_args(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("out", C.c_void_p), ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p),
+                ("k_host", C.c_void_p), ("v_host", C.c_void_p), ("block_table", C.c_void_p), ("seq_lens", C.c_void_p),
+                ("B", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("d", C.c_int32), ("page_size", C.c_int32),
+                ("max_pages", C.c_int32), ("chunk_pages", C.c_int32), ("scale", C.c_float), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t), ("cfg", dak_launch_cfg), ("q_row_stride", C.c_int64)]
+
+
+_sig("dak_pack_kv_pages", C.c_int32, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p])
+_sig("dak_attention_workspace_size", C.c_int32, [C.POINTER(dak_attention_args), C.POINTER(C.c_size_t)])
+_sig("dak_attention", C.c_int32, [C.POINTER(dak_attention_args), C.c_void_p])
+_sig("dak_kv_append", C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                                  C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.c_void_p])
+
+EXPORTED = ["dak_pack_kv_pages", "dak_attention_workspace_size", "dak_attention", "dak_kv_append",
+            "dak_last_error", "dak_version", "dak_device_sms", "dak_plan_ratios", "dak_host_alloc", "dak_host_free",
             "dak_linear_packed_bytes", "dak_pack_linear", "dak_linear_default_kc", "dak_linear_query",
             "dak_linear_cta_rows", "dak_linear"]
 
@@ -210,3 +226,95 @@ def linear_cta_rows(args: dak_linear_args, cta: int):
     tier, b, e = C.c_int32(), C.c_int64(), C.c_int64()
     _check(lib.dak_linear_cta_rows(C.byref(args), int(cta), C.byref(tier), C.byref(b), C.byref(e)))
     return ("host" if tier.value else "hbm", b.value, e.value)
+
+
+# ------------------------------------------------------------------------------------- attention
+def pack_kv_pages(src, n_blocks: int, page_size: int, d: int, dst, stream=None):
+    _check(lib.dak_pack_kv_pages(_ptr(src), int(n_blocks), int(page_size), int(d), _ptr(dst), _stream(stream)))
+
+
+def attention_args(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, B, Hq, Hkv, d, page_size, max_pages,
+                   chunk_pages, scale=0.0, workspace=None, workspace_bytes=0, cfg=None, q_row_stride=0):
+    a = dak_attention_args()
+    a.q, a.out = _ptr(q), _ptr(out)
+    a.k_hbm, a.v_hbm, a.k_host, a.v_host = _ptr(k_hbm), _ptr(v_hbm), _ptr(k_host), _ptr(v_host)
+    a.block_table, a.seq_lens = _ptr(block_table), _ptr(seq_lens)
+    a.B, a.Hq, a.Hkv, a.d = int(B), int(Hq), int(Hkv), int(d)
+    a.page_size, a.max_pages, a.chunk_pages = int(page_size), int(max_pages), int(chunk_pages)
+    a.scale = float(scale)
+    a.workspace, a.workspace_bytes = _ptr(workspace), int(workspace_bytes)
+    a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
+    a.q_row_stride = int(q_row_stride)
+    return a
+
+
+def attention_workspace_size(args: dak_attention_args) -> int:
+    v = C.c_size_t()
+    _check(lib.dak_attention_workspace_size(C.byref(args), C.byref(v)))
+    return v.value
+
+
+def attention(args: dak_attention_args, stream=None):
+    _check(lib.dak_attention(C.byref(args), _stream(stream)))
+
+
+def kv_append(k_new, v_new, block_table, positions, B, Hkv, d, page_size, max_pages, k_hbm, v_hbm, k_host, v_host,
+              pdl=0, stream=None, row_stride=0):
+    _check(lib.dak_kv_append(_ptr(k_new), _ptr(v_new), int(row_stride), _ptr(block_table), _ptr(positions), int(B), int(Hkv), int(d),
+                             int(page_size), int(max_pages), _ptr(k_hbm), _ptr(v_hbm), _ptr(k_host), _ptr(v_host),
+                             int(pdl), _stream(stream)))
+
+
+# ------------------------------------------------------------------------------------- layer
+MODEL_OPT = 0
+
+
+class dak_weight(C.Structure):
+    _fields_ = [("w_host", C.c_void_p), ("w_hbm", C.c_void_p), ("h", C.c_int64), ("kc", C.c_int32),
+                ("n_cta_host", C.c_int32), ("bias", C.c_void_p)]
+
+
+class dak_layer_args(C.Structure):
+    _fields_ = [("model", C.c_int32), ("B", C.c_int32), ("hidden", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32), ("ln_eps", C.c_float),
+                ("qkv", dak_weight), ("o", dak_weight), ("up", dak_weight), ("down", dak_weight),
+                ("ln1_w", C.c_void_p), ("ln1_b", C.c_void_p), ("ln2_w", C.c_void_p), ("ln2_b", C.c_void_p),
+                ("x", C.c_void_p), ("scratch", C.c_void_p), ("scratch_bytes", C.c_size_t),
+                ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p), ("k_host", C.c_void_p), ("v_host", C.c_void_p),
+                ("block_table", C.c_void_p), ("positions", C.c_void_p), ("seq_lens", C.c_void_p),
+                ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("reserved", C.c_int32),
+                ("cfg", dak_launch_cfg), ("attn_cfg", dak_launch_cfg)]
+
+
+_sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
+                                  C.c_int32, C.c_void_p])
+_sig("dak_embed", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
+                              C.c_void_p, C.c_int32, C.c_void_p])
+_sig("dak_layer_scratch_size", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_size_t)])
+_sig("dak_layer", C.c_int32, [C.POINTER(dak_layer_args), C.c_void_p])
+EXPORTED += ["dak_layernorm", "dak_embed", "dak_layer_scratch_size", "dak_layer"]
+
+
+def weight(w_host, w_hbm, h, kc, bias=None, n_cta_host=0) -> dak_weight:
+    return dak_weight(_ptr(w_host), _ptr(w_hbm), int(h), int(kc), int(n_cta_host), _ptr(bias))
+
+
+def layernorm(x, w, b, y, rows, cols, eps=1e-5, pdl=0, stream=None):
+    _check(lib.dak_layernorm(_ptr(x), _ptr(w), _ptr(b), _ptr(y), int(rows), int(cols), float(eps), int(pdl),
+                             _stream(stream)))
+
+
+def embed(tokens, positions, tok_emb, pos_emb, B, hidden, pos_offset, x, pdl=0, stream=None):
+    _check(lib.dak_embed(_ptr(tokens), _ptr(positions), _ptr(tok_emb), _ptr(pos_emb), int(B), int(hidden),
+                         int(pos_offset), _ptr(x), int(pdl), _stream(stream)))
+
+
+def layer_scratch_size(args: dak_layer_args) -> int:
+    v = C.c_size_t()
+    _check(lib.dak_layer_scratch_size(C.byref(args), C.byref(v)))
+    return v.value
+
+
+def layer(args: dak_layer_args, stream=None):
+    _check(lib.dak_layer(C.byref(args), _stream(stream)))

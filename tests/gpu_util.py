@@ -79,3 +79,63 @@ def assert_close(got: np.ndarray, ref: np.ndarray, rtol: float = 1e-2):
         raise AssertionError(f"{bad.sum()} / {bad.size} elements out of tolerance; worst at {i}: got {got[i]} ref {ref[i]}")
     fro = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300)
     assert fro <= rtol, fro
+
+
+def make_paged_kv(Ls, Hkv, d, page, host_chunks_frac, chunk_pages, seed, Hq, kind="normal", paper_mode=False):
+    """Logical KV (synth) -> logical page pools + block table. Host = the oldest
+    round_half_up(frac * n_chunks) chunks of each request (DESIGN reading), or whole requests
+    (paper mode). Returns q, K list, V list, (kg, vg, kh, vh, bt) with logical pools."""
+    from oracle.partition import host_pages_prefix, batch_split_host_requests
+    q, K, V = __import__("synth").kv_inputs(Ls, Hkv, d, Hq, seed, kind=kind)
+    g = np.random.default_rng(seed + 1)
+    B = len(Ls)
+    pages = [-(-L // page) for L in Ls]
+    max_pages = max(pages)
+    if paper_mode:
+        nreq = batch_split_host_requests(B, host_chunks_frac)
+        n_host = [pages[b] if b < nreq else 0 for b in range(B)]
+    else:
+        n_host = [host_pages_prefix(pages[b], host_chunks_frac, chunk_pages) for b in range(B)]
+    Ph, Pg = sum(n_host), sum(p - h for p, h in zip(pages, n_host))
+    kh = np.zeros((max(Ph, 1), Hkv, page, d), np.uint16)
+    vh = np.zeros_like(kh)
+    kg = np.zeros((max(Pg, 1), Hkv, page, d), np.uint16)
+    vg = np.zeros_like(kg)
+    bt = np.zeros((B, max_pages), np.int64)
+    ih = list(g.permutation(max(Ph, 1)))
+    ig = list(g.permutation(max(Pg, 1)))
+    for b, L in enumerate(Ls):
+        for pi in range(pages[b]):
+            lo, hi = pi * page, min(L, (pi + 1) * page)
+            if pi < n_host[b]:
+                j = int(ih.pop())
+                kh[j, :, :hi - lo] = K[b][lo:hi].transpose(1, 0, 2)
+                vh[j, :, :hi - lo] = V[b][lo:hi].transpose(1, 0, 2)
+                bt[b, pi] = j | 0x80000000
+            else:
+                j = int(ig.pop())
+                kg[j, :, :hi - lo] = K[b][lo:hi].transpose(1, 0, 2)
+                vg[j, :, :hi - lo] = V[b][lo:hi].transpose(1, 0, 2)
+                bt[b, pi] = j
+    bt = (bt & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    return q, K, V, (kg, vg, kh, vh, bt), n_host
+
+
+class PagedKV:
+    """Device-side tier pools in the DAK-PG layout (packed by dak_pack_kv_pages)."""
+
+    def __init__(self, D, kg, vg, kh, vh, bt, page, has_host=True):
+        import torch
+        self.D = D
+        P, Hkv, pg, d = kg.shape
+        self.kg = torch.empty(kg.size, dtype=torch.int16, device="cuda")
+        self.vg = torch.empty(vg.size, dtype=torch.int16, device="cuda")
+        D.pack_kv_pages(to_dev(kg), kg.shape[0] * Hkv, page, d, self.kg)
+        D.pack_kv_pages(to_dev(vg), vg.shape[0] * Hkv, page, d, self.vg)
+        self.kh = HostBuf(D, kh.size * 2)
+        self.vh = HostBuf(D, vh.size * 2)
+        D.pack_kv_pages(to_dev(kh), kh.shape[0] * Hkv, page, d, self.kh.dp)
+        D.pack_kv_pages(to_dev(vh), vh.shape[0] * Hkv, page, d, self.vh.dp)
+        self.bt = torch.from_numpy(bt.copy()).cuda()
+        self.page = page
+        torch.cuda.synchronize()

@@ -1,0 +1,62 @@
+"""GPU parity of the composed decode step (dak_layer x L + embed + LN + LM head via the engine)
+against the OPT decode-step oracle (itself pinned to transformers OPT in float64).
+
+Tolerance: the GPU keeps activations in bf16 between kernels (h, qkv, attention output, fc1
+output, residual stream), i.e. ~6 sequential roundings of 2^-9 relative per layer; the step is
+compared within 3e-2 of max(|ref|, rms(ref))."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import kernels as Kx
+from oracle import layer as Ly
+from tests.test_oracle_layer import make_params
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine_weights(p, L, torch):
+    def dev(bits):
+        return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16)).cuda().view(torch.bfloat16)
+    w = {}
+    for l in range(L):
+        for ours, theirs in (("qkv", "qkv"), ("o", "o"), ("up", "fc1"), ("down", "fc2")):
+            w[f"L{l}.{ours}"] = dev(p[f"L{l}.{theirs}"])
+            w[f"L{l}.{ours}.b"] = dev(p[f"L{l}.{theirs}_b"])
+        for n in ("ln1_w", "ln1_b", "ln2_w", "ln2_b"):
+            w[f"L{l}.{n}"] = dev(p[f"L{l}.{n}"])
+    for n in ("embed", "pos", "lnf_w", "lnf_b"):
+        w[n] = dev(p[n])
+    return w
+
+
+@pytest.mark.parametrize("frac,B,ctx", [(0.0, 3, 70), (0.2, 3, 70), (0.5, 2, 200)])
+def test_engine_step_matches_oracle(frac, B, ctx):
+    import torch
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
+    L, H, F, V, heads, maxpos = 2, 256, 512, 1000, 2, 256
+    g = np.random.default_rng(2024)
+    p = make_params(g, L, H, F, V, maxpos)
+    cfg = OPTConfig(n_layers=L, hidden=H, n_heads=heads, ffn=F, vocab=V, max_pos=maxpos, name="opt-tiny")
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    total = sum(o for o in [3 * H * H, H * H, F * H, H * F]) * 2 * L + V * H * 2
+    eng = DakOPT(cfg, B, ctx, hw, mode=dak.PLAN_EXACT, y_req=int(frac * total), page_size=64, chunk_pages=1,
+                 weights=_engine_weights(p, L, torch))
+    if frac > 0:
+        assert sum(op.h for op in eng.linear_ops()) > 0
+    Kc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    Vc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    eng.load_kv(Kc, Vc)
+    tokens = np.arange(B) * 37 + 5
+    eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
+    s = torch.cuda.Stream()
+    eng.capture(s)  # also runs one eager step (warm-up) before capture
+    # the eager step appended the new token already; replaying rewrites the same slot
+    eng.graph.replay()
+    torch.cuda.synchronize()
+    ref, _ = Ly.opt_decode_step(tokens, np.full(B, ctx - 1), p, Kc, Vc, heads)
+    got = Kx.bf16_to_f64(eng.logits.view(torch.int16).cpu().numpy().view(np.uint16))
+    from tests.gpu_util import assert_close
+    assert_close(got, ref, rtol=3e-2)
+    eng.close()

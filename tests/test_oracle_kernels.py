@@ -175,3 +175,15 @@ def test_layernorm_closed_form():
     x = np.array([[1.0, 2.0, 3.0, 4.0]])
     y = Kx.layernorm(x, np.ones(4), np.zeros(4), eps=0.0)
     assert np.allclose(y, (x - 2.5) / np.sqrt(1.25))
+
+
+def test_round_to_bf16_matches_bit_definition():
+    """round_to_bf16 == the RNE bit rounding of the input generator on float32-exact values, and
+    is exact on representable values (integers up to 256, powers of two)."""
+    g = np.random.default_rng(4)
+    v = g.standard_normal(20000).astype(np.float32)
+    assert np.array_equal(Kx.round_to_bf16(v.astype(np.float64)), Kx.bf16_to_f64(synth.bf16_bits(v)))
+    ints = np.arange(-256, 257, dtype=np.float64)
+    assert np.array_equal(Kx.round_to_bf16(ints), ints)
+    assert Kx.round_to_bf16(np.array([257.0]))[0] == 256.0  # tie -> even
+    assert Kx.round_to_bf16(np.array([259.0]))[0] == 260.0
