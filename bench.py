@@ -192,6 +192,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--context", type=int, default=64)
     ap.add_argument("--no-pdl", action="store_true")
+    ap.add_argument("--per-op", action="store_true", help="per-op kernels (dak_layer) instead of the persistent step")
     ap.add_argument("--no-cc", action="store_true")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,6 +217,8 @@ def main():
         eng.close()
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, seed=1234 + rank)
+    if not a.per_op:
+        eng.enable_persistent_step()
     nb = eng.bytes_per_step()
     stream = torch.cuda.Stream()
     g = eng.capture(stream)
@@ -302,6 +305,7 @@ def main():
                             host_ratio=round(nb["host"] / nb["total"], 5),
                             l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
+                            execution="per-op kernels (dak_layer)" if a.per_op else "persistent step (dak_step, 1 launch)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
                 gpu_launches=eng.kernels_per_step() * a.steps)

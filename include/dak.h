@@ -154,6 +154,8 @@ typedef struct {
   int32_t act;          /* DAK_ACT_*                                                           */
   int32_t reserved;
   dak_launch_cfg cfg;
+  int64_t ldy;          /* elements between rows n of y and residual (0: M); lets q/k/v write   */
+                        /* into one fused [N, (Hq+2Hkv)d] buffer                                */
 } dak_linear_args;
 
 /* Launch description (pure query; used by tests and the bench to attribute bytes). */
@@ -268,12 +270,93 @@ typedef struct {
   int32_t reserved;
   dak_launch_cfg cfg;                 /* linear ops (pdl applies to every kernel)              */
   dak_launch_cfg attn_cfg;            /* attention                                             */
+  int32_t split_qkv;                  /* 1: use q, k, v below instead of the fused qkv weight  */
+  int32_t reserved2;
+  dak_weight q, k, v;                 /* separate projections (rows Hq*d, Hkv*d, Hkv*d)         */
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);
 /* Enqueue one decode step of one layer: 9 kernels (LN, QKV, KV append, attention + combine,
  * O + residual, LN, FC1 + ReLU, FC2 + residual). */
 dak_status dak_layer(const dak_layer_args* args, dak_stream_t stream);
+
+/* =============================================================================================
+ * 6. Persistent decode step: the whole op sequence of a decode step in ONE co-resident launch.
+ *    Per CTA a producer warp streams every op's weight rows / KV pages back to back (the HBM and
+ *    host streams never drain between ops); activations wait on gpu-scope completion counters.
+ *    Same operators and numerics as sections 3-5.
+ * ============================================================================================= */
+
+#define DAK_STEP_EMBED 0      /* y[b] = tok[tokens[b]] + pos[positions[b]+pos_offset]; cols = hidden */
+#define DAK_STEP_LAYERNORM 1  /* y = LN(x) with mean/var from stats_in (written by the op producing x) */
+#define DAK_STEP_LINEAR 2     /* split linear (section 3) + optional LN stats / fused KV append     */
+#define DAK_STEP_ATTENTION 3  /* split paged attention (section 4), units listed per tier           */
+#define DAK_STEP_COMBINE 4    /* merge split-KV partials of multi-chunk requests; cols = B          */
+
+typedef struct {
+  int32_t type;
+  int32_t dep;                 /* op index whose output this op reads (-1: none); must be < own index */
+  int32_t n_cta_host;          /* host-tier CTAs for this op (0: launch cfg / 1)                      */
+  int32_t act;                 /* LINEAR: DAK_ACT_*                                                   */
+  /* LINEAR (DAK-KC packed tiers; kc in {64,128,256}) */
+  const void* w_host;
+  const void* w_hbm;
+  int64_t M, K, h;
+  int32_t kc;
+  int32_t kv_kind;             /* fused KV append: 1 rows >= kv_row0 are K rows, 2 V rows,            */
+                               /* 3 [K rows; V rows] (fused QKV); 0 / kv_row0 < 0: off                */
+  const void* x;               /* [N, K] (LINEAR) / [N, cols] (LAYERNORM)                             */
+  void* y;                     /* [N, ldy] (LINEAR) / [N, cols] (LAYERNORM, EMBED)                    */
+  int64_t ldy;                 /* LINEAR: row stride of y and residual (0: M)                         */
+  const void* bias;
+  const void* residual;
+  float* stats_out;            /* [grid][N][2] per-CTA sum / sum of squares of y (for the next LN)    */
+  int64_t kv_row0;             /* LINEAR: first K row of a fused [q;k;v] output -> append k,v rows    */
+                               /* at positions into the pools below (-1: off)                         */
+  /* LAYERNORM / EMBED */
+  const float* stats_in;
+  const void* ln_w;
+  const void* ln_b;
+  float eps;
+  int32_t cols;
+  const int32_t* tokens;
+  const int32_t* positions;    /* also used by the fused KV append                                    */
+  const void* tok_emb;
+  const void* pos_emb;
+  int32_t pos_offset, reserved1;
+  /* ATTENTION / COMBINE / fused append */
+  const void* q;
+  int64_t q_stride;            /* elements between requests of q (0: Hq*d)                            */
+  void* out;                   /* [B, Hq*d] bf16                                                      */
+  void *k_hbm, *v_hbm, *k_host, *v_host;
+  const int32_t* block_table;
+  const int32_t* seq_lens;
+  int32_t Hq, Hkv, d, page_size, max_pages, chunk_pages;
+  float scale;
+  int32_t reserved2;
+  const int32_t* units_host;   /* (request*ceil(max_pages/chunk_pages) + chunk) pairs whose chunk      */
+  const int32_t* units_hbm;    /*   starts on a host / HBM page (device arrays)                       */
+  int32_t n_units_host, n_units_hbm;
+  float* part_o;               /* split-KV partial workspace, as dak_attention's                      */
+  float* part_lse;
+} dak_step_op;
+
+typedef struct {
+  void* dev;
+  int32_t n_ops, N, grid, ring_bytes, off_scratch, smem, pdl;
+  void* trace;  /* optional device u64 [n_ops][grid][4] globaltimer stamps: 0 stream-producer start
+                   (attention), 1 dependency satisfied, 2 first stage ready, 3 op done (NULL: off) */
+} dak_step_plan;
+
+/* Device bytes for the compiled op table + completion counters. */
+size_t dak_step_buffer_bytes(int32_t n_ops);
+/* KC to pack a linear with (in {64,128,256}) so that `rows_per_cta` rows fit one ring slot. */
+int32_t dak_step_choose_kc(int64_t rows_per_cta, int64_t K);
+/* Validate and compile an op table into dev_buf (synchronous setup call; not for capture). */
+dak_status dak_step_compile(const dak_step_op* ops, int32_t n_ops, int32_t N, const dak_launch_cfg* cfg,
+                            void* dev_buf, size_t dev_bytes, dak_step_plan* out);
+/* Enqueue the persistent decode step (one cooperative launch; graph-capturable, replayable). */
+dak_status dak_step_launch(const dak_step_plan* plan, dak_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,7 @@ SOURCES = [
     ("linear.cu", []),
     ("attention.cu", []),
     ("layer.cu", []),
+    ("step.cu", []),
 ]
 
 

@@ -192,8 +192,21 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   cudaStream_t strm = (cudaStream_t)stream;
 
   if ((st = dak_layernorm(a->x, a->ln1_w, a->ln1_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
-  dak_linear_args l = layer::lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
-  if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  dak_linear_args l;
+  if (a->split_qkv) {  // q, k, v written side by side into the fused [B, qkv_cols] buffer
+    const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
+    const dak_weight* w[3] = {&a->q, &a->k, &a->v};
+    long long off = 0;
+    for (int i = 0; i < 3; ++i) {
+      l = layer::lin_args(*w[i], rows[i], H, B, h, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
+      l.ldy = qkv_cols;
+      if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+      off += rows[i];
+    }
+  } else {
+    l = layer::lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
+    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  }
   if ((st = dak_kv_append(qkv + (size_t)Hq * d * 2, qkv + (size_t)(Hq + Hkv) * d * 2, qkv_cols, a->block_table,
                           a->positions, B, Hkv, d, a->page_size, a->max_pages, a->k_hbm, a->v_hbm, a->k_host,
                           a->v_host, pdl, strm)) != DAK_OK)

@@ -50,6 +50,7 @@ struct Params {
   int stages, window;
   int w_stage_bytes, x_stage_bytes, x_pitch;
   int res_offset;  // byte offset of the fp32 result buffer in smem
+  long long ldy;   // elements between consecutive rows n of y and residual
 };
 
 // ------------------------------------------------------------------------------------ PTX glue
@@ -355,8 +356,8 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
     const long long m = row0 + r;
     if (p.bias) v += __bfloat162float(p.bias[m]);
     if (p.act == DAK_ACT_RELU) v = fmaxf(v, 0.f);
-    if (p.residual) v += __bfloat162float(p.residual[(long long)n * p.M + m]);
-    p.y[(long long)n * p.M + m] = __float2bfloat16_rn(v);
+    if (p.residual) v += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
+    p.y[(long long)n * p.ldy + m] = __float2bfloat16_rn(v);
   }
 }
 
@@ -495,6 +496,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.bias = (const __nv_bfloat16*)a->bias;
   p.residual = (const __nv_bfloat16*)a->residual;
   p.act = a->act;
+  p.ldy = a->ldy > 0 ? a->ldy : M;
+  if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
   p.n_host = n_host; p.n_hbm = n_hbm;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
   p.x_pitch = kc * 2 + 16;

@@ -58,7 +58,8 @@ class dak_launch_cfg(C.Structure):
 class dak_linear_args(C.Structure):
     _fields_ = [("w_host", C.c_void_p), ("w_hbm", C.c_void_p), ("M", C.c_int64), ("K", C.c_int64), ("h", C.c_int64),
                 ("kc", C.c_int32), ("N", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p), ("bias", C.c_void_p),
-                ("residual", C.c_void_p), ("act", C.c_int32), ("reserved", C.c_int32), ("cfg", dak_launch_cfg)]
+                ("residual", C.c_void_p), ("act", C.c_int32), ("reserved", C.c_int32), ("cfg", dak_launch_cfg),
+                ("ldy", C.c_int64)]
 
 
 class dak_linear_launch_info(C.Structure):
@@ -200,7 +201,7 @@ def launch_cfg(**kw) -> dak_launch_cfg:
     return c
 
 
-def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, act=ACT_NONE, cfg=None):
+def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, act=ACT_NONE, cfg=None, ldy=0):
     a = dak_linear_args()
     a.w_host = _ptr(w_host)
     a.w_hbm = _ptr(w_hbm)
@@ -209,6 +210,7 @@ def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, a
     a.bias, a.residual = _ptr(bias), _ptr(residual)
     a.act = int(act)
     a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
+    a.ldy = int(ldy)
     return a
 
 
@@ -284,7 +286,8 @@ class dak_layer_args(C.Structure):
                 ("block_table", C.c_void_p), ("positions", C.c_void_p), ("seq_lens", C.c_void_p),
                 ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
                 ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("reserved", C.c_int32),
-                ("cfg", dak_launch_cfg), ("attn_cfg", dak_launch_cfg)]
+                ("cfg", dak_launch_cfg), ("attn_cfg", dak_launch_cfg), ("split_qkv", C.c_int32),
+                ("reserved2", C.c_int32), ("q", dak_weight), ("k", dak_weight), ("v", dak_weight)]
 
 
 _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
@@ -318,3 +321,71 @@ def layer_scratch_size(args: dak_layer_args) -> int:
 
 def layer(args: dak_layer_args, stream=None):
     _check(lib.dak_layer(C.byref(args), _stream(stream)))
+
+
+# ------------------------------------------------------------------------------------- persistent step
+STEP_EMBED, STEP_LAYERNORM, STEP_LINEAR, STEP_ATTENTION, STEP_COMBINE = 0, 1, 2, 3, 4
+
+
+class dak_step_op(C.Structure):
+    _fields_ = [("type", C.c_int32), ("dep", C.c_int32), ("n_cta_host", C.c_int32), ("act", C.c_int32),
+                ("w_host", C.c_void_p), ("w_hbm", C.c_void_p), ("M", C.c_int64), ("K", C.c_int64), ("h", C.c_int64),
+                ("kc", C.c_int32), ("kv_kind", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p), ("ldy", C.c_int64),
+                ("bias", C.c_void_p), ("residual", C.c_void_p), ("stats_out", C.c_void_p), ("kv_row0", C.c_int64),
+                ("stats_in", C.c_void_p), ("ln_w", C.c_void_p), ("ln_b", C.c_void_p), ("eps", C.c_float),
+                ("cols", C.c_int32), ("tokens", C.c_void_p), ("positions", C.c_void_p), ("tok_emb", C.c_void_p),
+                ("pos_emb", C.c_void_p), ("pos_offset", C.c_int32), ("reserved1", C.c_int32),
+                ("q", C.c_void_p), ("q_stride", C.c_int64), ("out", C.c_void_p),
+                ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p), ("k_host", C.c_void_p), ("v_host", C.c_void_p),
+                ("block_table", C.c_void_p), ("seq_lens", C.c_void_p), ("Hq", C.c_int32), ("Hkv", C.c_int32),
+                ("d", C.c_int32), ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
+                ("scale", C.c_float), ("reserved2", C.c_int32), ("units_host", C.c_void_p),
+                ("units_hbm", C.c_void_p), ("n_units_host", C.c_int32), ("n_units_hbm", C.c_int32),
+                ("part_o", C.c_void_p), ("part_lse", C.c_void_p)]
+
+
+class dak_step_plan(C.Structure):
+    _fields_ = [("dev", C.c_void_p), ("n_ops", C.c_int32), ("N", C.c_int32), ("grid", C.c_int32),
+                ("ring_bytes", C.c_int32), ("off_scratch", C.c_int32), ("smem", C.c_int32), ("pdl", C.c_int32),
+                ("trace", C.c_void_p)]
+
+
+_sig("dak_step_buffer_bytes", C.c_size_t, [C.c_int32])
+_sig("dak_step_choose_kc", C.c_int32, [C.c_int64, C.c_int64])
+_sig("dak_step_compile", C.c_int32, [C.POINTER(dak_step_op), C.c_int32, C.c_int32, C.POINTER(dak_launch_cfg),
+                                     C.c_void_p, C.c_size_t, C.POINTER(dak_step_plan)])
+_sig("dak_step_launch", C.c_int32, [C.POINTER(dak_step_plan), C.c_void_p])
+EXPORTED += ["dak_step_buffer_bytes", "dak_step_choose_kc", "dak_step_compile", "dak_step_launch"]
+
+
+def step_op(**kw) -> dak_step_op:
+    o = dak_step_op()
+    o.dep = -1
+    o.kv_row0 = -1
+    for k, v in kw.items():
+        f = dict(dak_step_op._fields_)[k]
+        if f is C.c_void_p:
+            setattr(o, k, _ptr(v))
+        else:
+            setattr(o, k, v)
+    return o
+
+
+def step_choose_kc(rows_per_cta: int, K: int) -> int:
+    return int(lib.dak_step_choose_kc(int(rows_per_cta), int(K)))
+
+
+def step_compile(ops: list, N: int, cfg: dict | None = None):
+    """Compile an op table; returns (plan, device buffer tensor)."""
+    import torch
+    arr = (dak_step_op * len(ops))(*ops)
+    nbytes = lib.dak_step_buffer_bytes(len(ops))
+    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    plan = dak_step_plan()
+    c = launch_cfg(**(cfg or {}))
+    _check(lib.dak_step_compile(arr, len(ops), int(N), C.byref(c), buf.data_ptr(), nbytes, C.byref(plan)))
+    return plan, buf
+
+
+def step_launch(plan: dak_step_plan, stream=None):
+    _check(lib.dak_step_launch(C.byref(plan), _stream(stream)))

@@ -79,20 +79,22 @@ class DakOPT:
     def __init__(self, cfg: OPTConfig, batch: int, context: int, hw: HW, mode: int = dak.PLAN_BALANCED,
                  y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 16, seed: int = 0,
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
-                 host_override: dict | None = None):
+                 host_override: dict | None = None, n_cta_host: int = 2):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
         self.pdl = int(pdl)
-        self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control))
+        self.n_cta_host = n_cta_host
+        self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host)
         self.sms = dak.device_sms()
         self.gen = torch.Generator(device="cuda")
         self.gen.manual_seed(seed)
         self._host_blocks = []
         c = cfg
-        qkv_rows = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim
         self.layers = []
-        for i in range(c.n_layers):
-            self.layers.append(dict(qkv=LinearOp(f"L{i}.qkv", qkv_rows, c.hidden),
+        for i in range(c.n_layers):  # q/k/v/o separate, as the paper's op list (P:L981 footnote)
+            self.layers.append(dict(q=LinearOp(f"L{i}.q", c.n_heads * c.head_dim, c.hidden),
+                                    k=LinearOp(f"L{i}.k", c.n_kv_heads * c.head_dim, c.hidden),
+                                    v=LinearOp(f"L{i}.v", c.n_kv_heads * c.head_dim, c.hidden),
                                     o=LinearOp(f"L{i}.o", c.hidden, c.n_heads * c.head_dim),
                                     up=LinearOp(f"L{i}.fc1", c.ffn, c.hidden),
                                     down=LinearOp(f"L{i}.fc2", c.hidden, c.ffn)))
@@ -107,7 +109,7 @@ class DakOPT:
     # ------------------------------------------------------------------ planning
     def linear_ops(self):
         for L in self.layers:
-            yield from (L["qkv"], L["o"], L["up"], L["down"])
+            yield from (L["q"], L["k"], L["v"], L["o"], L["up"], L["down"])
         yield self.head
 
     def kv_bytes_per_layer(self) -> int:
@@ -140,7 +142,10 @@ class DakOPT:
             op.h = min(op.M, plan[i]["host_units"] * self.unit_rows)
             if host_override and op.name.split(".")[-1] in host_override:
                 op.h = host_override[op.name.split(".")[-1]]
-            op.kc = dak.default_kc(op.M - op.h, op.K, self.sms - 1)
+            # one KC for both execution paths: the persistent step's slot constraint (<= 256)
+            n_host = min(self.n_cta_host, op.h) if op.h > 0 else 0
+            rows = max(-(-op.h // max(n_host, 1)) if op.h else 0, -(-(op.M - op.h) // (self.sms - n_host)))
+            op.kc = dak.step_choose_kc(rows, op.K)
             i += 1
         self.attn_host_chunks = [plan[i + l]["host_units"] for l in range(c.n_layers)]
         return plan
@@ -168,11 +173,21 @@ class DakOPT:
     def _allocate(self, weights):
         c = self.cfg
         dev = "cuda"
+        if weights:  # a fused [q;k;v] weight may be given: split it into the three projections
+            weights = dict(weights)
+            for i in range(c.n_layers):
+                if f"L{i}.qkv" in weights:
+                    Wf, bf = weights.pop(f"L{i}.qkv"), weights.pop(f"L{i}.qkv.b")
+                    r0 = 0
+                    for key in ("q", "k", "v"):
+                        M = self.layers[i][key].M
+                        weights[f"L{i}.{key}"], weights[f"L{i}.{key}.b"] = Wf[r0:r0 + M], bf[r0:r0 + M]
+                        r0 += M
         for i, L in enumerate(self.layers):
-            for key, op in L.items():
+            for key, op in list(L.items()):
                 W = weights[f"L{i}.{key}"] if weights else None
                 self._fill_linear(op, W)
-                op.bias = weights[f"L{i}.{key}.b"] if weights else _bf16_rand((op.M,), 0.02, self.gen)
+                op.bias = weights[f"L{i}.{key}.b"].contiguous() if weights else _bf16_rand((op.M,), 0.02, self.gen)
             L["ln1_w"] = weights[f"L{i}.ln1_w"] if weights else torch.ones(c.hidden, dtype=torch.bfloat16, device=dev)
             L["ln1_b"] = weights[f"L{i}.ln1_b"] if weights else torch.zeros(c.hidden, dtype=torch.bfloat16, device=dev)
             L["ln2_w"] = weights[f"L{i}.ln2_w"] if weights else torch.ones(c.hidden, dtype=torch.bfloat16, device=dev)
@@ -267,7 +282,9 @@ class DakOPT:
         a = dak.dak_layer_args()
         a.model, a.B, a.hidden, a.n_heads, a.n_kv_heads = dak.MODEL_OPT, self.B, c.hidden, c.n_heads, c.n_kv_heads
         a.head_dim, a.ffn, a.ln_eps = c.head_dim, c.ffn, 1e-5
-        a.qkv, a.o, a.up, a.down = L["qkv"].weight(), L["o"].weight(), L["up"].weight(), L["down"].weight()
+        a.o, a.up, a.down = L["o"].weight(), L["up"].weight(), L["down"].weight()
+        a.split_qkv = 1
+        a.q, a.k, a.v = L["q"].weight(), L["k"].weight(), L["v"].weight()
         a.ln1_w, a.ln1_b = L["ln1_w"].data_ptr(), L["ln1_b"].data_ptr()
         a.ln2_w, a.ln2_b = L["ln2_w"].data_ptr(), L["ln2_b"].data_ptr()
         a.x = self.x.data_ptr()
@@ -281,8 +298,89 @@ class DakOPT:
         a.attn_cfg = dak.launch_cfg(**self.launch)
         return a
 
+    # ------------------------------------------------------------------ persistent step program
+    def build_step_program(self):
+        """Op table of one decode step for dak_step (embed, then per layer LN1, QKV(+KV append),
+        attention[, combine], O(+residual, LN stats), LN2, FC1, FC2(+residual, LN stats), then
+        LN_f and the LM head)."""
+        c, B, dev = self.cfg, self.B, "cuda"
+        H, F = c.hidden, c.ffn
+        G = self.sms
+        qkv_cols = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim
+        self.sp_h = torch.empty((B, H), dtype=torch.bfloat16, device=dev)
+        self.sp_qkv = torch.empty((B, qkv_cols), dtype=torch.bfloat16, device=dev)
+        self.sp_attn = torch.empty((B, c.n_heads * c.head_dim), dtype=torch.bfloat16, device=dev)
+        self.sp_f = torch.empty((B, F), dtype=torch.bfloat16, device=dev)
+        self.sp_stats = [torch.zeros((G, B, 2), dtype=torch.float32, device=dev) for _ in range(2)]
+        max_chunks = self.chunks_per_req
+        multi = max_chunks > 1
+        n_units = B * c.n_kv_heads * max_chunks
+        self.sp_part_o = torch.empty(max(1, n_units * (c.n_heads // c.n_kv_heads) * c.head_dim), dtype=torch.float32,
+                                     device=dev)
+        self.sp_part_lse = torch.empty(max(1, n_units * (c.n_heads // c.n_kv_heads)), dtype=torch.float32, device=dev)
+        self.sp_units = []
+        ops = []
+
+        def add(**kw):
+            ops.append(dak.step_op(**kw))
+            return len(ops) - 1
+
+        def lin(op: LinearOp, x, y, dep, **kw):
+            return add(type=dak.STEP_LINEAR, dep=dep, w_host=op.host[1] if op.host else None, w_hbm=op.hbm, M=op.M,
+                       K=op.K, h=op.h, kc=op.kc, x=x, y=y, bias=op.bias, **kw)
+
+        prev = add(type=dak.STEP_EMBED, y=self.x, cols=H, tokens=self.tokens, positions=self.positions,
+                   tok_emb=self.tok_emb, pos_emb=self.pos_emb, pos_offset=2, stats_out=self.sp_stats[0])
+        for l, L in enumerate(self.layers):
+            kg, vg, kh, vh, Ph, Pg = self.kv[l]
+            bt = self.block_tables[l].cpu().numpy().view(np.uint32)
+            uh, ug = [], []
+            for b in range(B):
+                for ch in range(max_chunks):
+                    p0 = ch * self.chunk_pages
+                    if p0 >= self.pages_per_req:
+                        continue
+                    (uh if bt[b, p0] & 0x80000000 else ug).append(b * max_chunks + ch)
+            th = torch.tensor(uh or [0], dtype=torch.int32, device=dev)
+            tg = torch.tensor(ug or [0], dtype=torch.int32, device=dev)
+            self.sp_units += [th, tg]
+            ln1 = add(type=dak.STEP_LAYERNORM, dep=prev, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[0],
+                      ln_w=L["ln1_w"], ln_b=L["ln1_b"], eps=1e-5)
+            kv = dict(k_hbm=kg, v_hbm=vg, k_host=kh[1], v_host=vh[1], block_table=self.block_tables[l],
+                      seq_lens=self.seq_lens, positions=self.positions, Hq=c.n_heads, Hkv=c.n_kv_heads, d=c.head_dim,
+                      page_size=self.page, max_pages=self.pages_per_req, chunk_pages=self.chunk_pages)
+            # q, k, v read the same LN1 output: no barrier between them; k / v epilogues append
+            # the new token to the KV pools; attention depends on v (in-order completion per CTA
+            # makes "every CTA finished v" imply q and k finished too)
+            base = self.sp_qkv.data_ptr()
+            hq = c.n_heads * c.head_dim
+            hkv = c.n_kv_heads * c.head_dim
+            lin(L["q"], self.sp_h, base, ln1, ldy=qkv_cols)
+            lin(L["k"], self.sp_h, base + hq * 2, ln1, ldy=qkv_cols, kv_row0=0, kv_kind=1, **kv)
+            qkv = lin(L["v"], self.sp_h, base + (hq + hkv) * 2, ln1, ldy=qkv_cols, kv_row0=0, kv_kind=2, **kv)
+            att = add(type=dak.STEP_ATTENTION, dep=qkv, q=self.sp_qkv, q_stride=qkv_cols, out=self.sp_attn,
+                      units_host=th, units_hbm=tg, n_units_host=len(uh), n_units_hbm=len(ug),
+                      part_o=self.sp_part_o, part_lse=self.sp_part_lse, **kv)
+            if multi:
+                att = add(type=dak.STEP_COMBINE, dep=att, out=self.sp_attn, cols=B, part_o=self.sp_part_o,
+                          part_lse=self.sp_part_lse, **kv)
+            o = lin(L["o"], self.sp_attn, self.x, att, residual=self.x, stats_out=self.sp_stats[1])
+            ln2 = add(type=dak.STEP_LAYERNORM, dep=o, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[1],
+                      ln_w=L["ln2_w"], ln_b=L["ln2_b"], eps=1e-5)
+            f1 = lin(L["up"], self.sp_h, self.sp_f, ln2, act=dak.ACT_RELU)
+            prev = lin(L["down"], self.sp_f, self.x, f1, residual=self.x, stats_out=self.sp_stats[0])
+        lnf = add(type=dak.STEP_LAYERNORM, dep=prev, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[0],
+                  ln_w=self.lnf_w, ln_b=self.lnf_b, eps=1e-5)
+        lin(self.head, self.sp_h, self.logits, lnf)
+        self.step_ops = ops
+        self.step_plan, self.step_buf = dak.step_compile(ops, B, cfg=self.launch)
+        return self.step_plan
+
     # ------------------------------------------------------------------ the decode step (hot path)
     def enqueue_step(self, stream=None):
+        if getattr(self, "use_step", False):
+            dak.step_launch(self.step_plan, stream)
+            return
         c = self.cfg
         dak.embed(self.tokens, self.positions, self.tok_emb, self.pos_emb, self.B, c.hidden, 2, self.x,
                   pdl=self.pdl, stream=stream)
@@ -294,7 +392,13 @@ class DakOPT:
         dak.linear(ha, stream)
 
     def kernels_per_step(self) -> int:
-        return 1 + 9 * self.cfg.n_layers + 2
+        if getattr(self, "use_step", False):
+            return 1
+        return 1 + 11 * self.cfg.n_layers + 2
+
+    def enable_persistent_step(self):
+        self.build_step_program()
+        self.use_step = True
 
     def capture(self, stream: torch.cuda.Stream):
         with torch.cuda.stream(stream):

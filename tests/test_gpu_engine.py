@@ -30,8 +30,9 @@ def _engine_weights(p, L, torch):
     return w
 
 
+@pytest.mark.parametrize("persistent", [False, True])
 @pytest.mark.parametrize("frac,B,ctx", [(0.0, 3, 70), (0.2, 3, 70), (0.5, 2, 200)])
-def test_engine_step_matches_oracle(frac, B, ctx):
+def test_engine_step_matches_oracle(frac, B, ctx, persistent):
     import torch
     from paper_2604_26074_b200 import dak
     from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
@@ -48,6 +49,8 @@ def test_engine_step_matches_oracle(frac, B, ctx):
     Kc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
     Vc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
     eng.load_kv(Kc, Vc)
+    if persistent:
+        eng.enable_persistent_step()
     tokens = np.arange(B) * 37 + 5
     eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
     s = torch.cuda.Stream()
