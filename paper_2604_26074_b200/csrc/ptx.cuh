@@ -45,13 +45,24 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
   asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll with relaxed loads (LDG.STRONG.GPU, served by L2) and acquire ONCE when the target is seen:
+// an acquire load compiles to LDG + CCTL.IVALL, i.e. it invalidates the whole L1 of the SM, so
+// acquiring on every poll evicts every other warp's spills and local data (measured: ~1.5x slower
+// persistent step, profiles/r01/step_v1_ncu.txt).
 __device__ __forceinline__ void spin_until_geq(const int* p, int target) {
-  if (ld_acquire(p) >= target) return;
-  unsigned ns = 32;
-  while (ld_acquire(p) < target) {
-    __nanosleep(ns);
-    if (ns < 256) ns <<= 1;
+  if (ld_relaxed(p) < target) {
+    unsigned ns = 32;
+    while (ld_relaxed(p) < target) {
+      __nanosleep(ns);
+      if (ns < 128) ns <<= 1;
+    }
   }
+  (void)ld_acquire(p);
 }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {

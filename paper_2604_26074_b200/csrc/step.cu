@@ -230,7 +230,9 @@ __global__ void __launch_bounds__(kThreads, 1) step_kernel(const Params P) {
     if (lane == 0) {
       Cur cur{-1, 0, 0};
       long long oldest = 0;    // oldest stage not yet known to be consumed
-      int reg_lo[kNB], reg_hi[kNB];  // byte regions of the in-flight stages (index i % kNB)
+      // byte regions of the in-flight stages (index i % kNB), in SMEM (not local memory)
+      int* reg_lo = reinterpret_cast<int*>(smem + 416);
+      int* reg_hi = reg_lo + kNB;
       // place stage i: wait until its ring region and its barrier pair are free (stages are
       // consumed in order, so waiting on stage j implies every earlier stage is consumed)
       auto acquire = [&](int sz, int win) {
