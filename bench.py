@@ -196,6 +196,9 @@ def main():
     ap.add_argument("--no-cc", action="store_true")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--l2-prefetch-mb", type=float, default=0.0, help="L2 warm-up of the next linear (0: off)")
+    ap.add_argument("--no-evict-first", action="store_true")
+    ap.add_argument("--no-fuse-norm", action="store_true", help="LayerNorm kernels instead of the fused pre-norm")
     ap.add_argument("--layers", type=int, default=48, help="(debug) fewer layers; invalid as a bench number")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -211,12 +214,14 @@ def main():
     hw = HW(hbm_bps=hbm_gbs * 1e9, link_bps=link_gbs * 1e9)
     cfg = OPT_30B if a.layers == 48 else OPTConfig(n_layers=a.layers)
     eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
-                 congestion_control=not a.no_cc, seed=1234 + rank)
+                 congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
+                 evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
     if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
         tot = sum(o["total_bytes"] for o in eng.plan_ops)
         eng.close()
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
-                     congestion_control=not a.no_cc, seed=1234 + rank)
+                     congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
+                 evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
     if not a.per_op:
         eng.enable_persistent_step()
     nb = eng.bytes_per_step()

@@ -47,6 +47,17 @@ const char* dak_version(void);
 /* Number of SMs of the current device (launch sizing; DAK_ECUDA without a device). */
 dak_status dak_device_sms(int32_t* sms);
 
+/* Launch-timeline tracing (debug/measurement; not thread-safe). While enabled, each of the next
+ * max_launches per-op launches (linear, attention, combine, KV append, LayerNorm, embed) records
+ * globaltimer stamps (ns) into dev_buf[launch][cta < 1024][4]: 0 CTA start, 1 dependency wait
+ * returned, 2 first pipeline stage consumed, 3 CTA done (0 where a kernel has no such point).
+ * dev_buf: device, >= max_launches * 32 KB, zeroed by the caller. NULL disables. Launches
+ * recorded under CUDA-graph capture stamp on every replay. */
+dak_status dak_trace_enable(void* dev_buf, int32_t max_launches);
+int32_t dak_trace_count(void);
+/* kind: 1 linear (a = M, b = K), 2 attention, 3 combine, 4 KV append, 5 LayerNorm, 6 embed. */
+dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, int32_t* grid);
+
 /* =============================================================================================
  * 1. Planner — greedy per-op offload ratios (§3.2; App. A)
  * ============================================================================================= */
@@ -138,7 +149,8 @@ typedef struct {
   int32_t pdl;                /* 1: programmatic dependent launch (weights stream before the   */
                               /*    previous kernel finishes; x/residual read after it)        */
   int32_t force_path;         /* 0 auto, 1 CUDA-core FMA path, 2 tensor-core (mma.sync) path   */
-  int32_t reserved;
+  int32_t l2_policy;          /* 0: stream weights/KV with the L2 evict_first hint (they are   */
+                              /*    read once per step), 1: no hint                              */
 } dak_launch_cfg;
 
 typedef struct {
@@ -156,6 +168,26 @@ typedef struct {
   dak_launch_cfg cfg;
   int64_t ldy;          /* elements between rows n of y and residual (0: M); lets q/k/v write   */
                         /* into one fused [N, (Hq+2Hkv)d] buffer                                */
+  const void* l2_prefetch;   /* optional hint (NULL: none): device bytes the NEXT op reads first  */
+  int64_t l2_prefetch_bytes; /* (multiple of 16). Once a CTA has issued its last weight copy, it  */
+                             /* prefetches slice cta/grid of this span into L2, so the next op's  */
+                             /* first stages hit L2 while this op drains. Never changes results.  */
+  /* Fused pre-norm of x (OPT pre-LayerNorm; Llama RMSNorm). When ln_w != NULL the GEMV   */
+  /* operand is bf16(((x - mu_n) * rstd_n) * ln_w + ln_b) -- exactly the dak_layernorm output --  */
+  /* with mu_n, rstd_n = 1/sqrt(var_n + ln_eps) merged (Chan et al., fixed order) from ln_parts    */
+  /* partial statistics ln_stats[part][N] = float4 (count, mean, M2, 0) written by the producer of  */
+  /* x (stats_out of a dak_linear, or dak_embed / dak_row_stats). ln_rms = 1: RMSNorm (mu = 0,     */
+  /* var = mean of squares, ln_b must be NULL). Tensor-core path only.                             */
+  const void* ln_w;
+  const void* ln_b;
+  const float* ln_stats;
+  int32_t ln_parts;
+  int32_t ln_rms;
+  float ln_eps;
+  int32_t reserved2;
+  /* Epilogue row statistics (nullable): CTA c writes float4 (count, mean, M2, 0) of its stored    */
+  /* (bf16-rounded) outputs of row n to stats_out[c * N + n]; `grid` (dak_linear_query) parts.     */
+  float* stats_out;
 } dak_linear_args;
 
 /* Launch description (pure query; used by tests and the bench to attribute bytes). */
@@ -237,7 +269,14 @@ dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, i
 /* x[b] = tok_emb[tokens[b]] + pos_emb[positions[b] + pos_offset]  (pos_emb/positions nullable;
  * OPT uses pos_offset 2). tokens/positions: device int32 [B]. */
 dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,
-                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, int32_t pdl, dak_stream_t stream);
+                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, float* stats_out, int32_t pdl,
+                     dak_stream_t stream);
+
+/* Row statistics for a fused pre-norm (dak_linear_args.ln_stats with ln_parts = 1):
+ * stats_out[r] = float4 (cols, mean, M2 = sum (x - mean)^2, 0) over row r of x (bf16, row stride
+ * ld elements, 0: cols), fp32, two-pass, fixed order. stats_out may be NULL in dak_embed. */
+dak_status dak_row_stats(const void* x, int32_t rows, int32_t cols, int64_t ld, float* stats_out, int32_t pdl,
+                         dak_stream_t stream);
 
 /* One split weight of a layer: DAK-KC packed tiers (rows [0,h) host, [h,M) HBM), KC, bias. */
 typedef struct {
@@ -273,12 +312,23 @@ typedef struct {
   int32_t split_qkv;                  /* 1: use q, k, v below instead of the fused qkv weight  */
   int32_t reserved2;
   dak_weight q, k, v;                 /* separate projections (rows Hq*d, Hkv*d, Hkv*d)         */
+  int64_t l2_prefetch_bytes;          /* 0: off; else each linear warms this many leading bytes  */
+                                      /* of the next linear's HBM tier (dak_linear_args hint)     */
+  const void* next_w_hbm;             /* HBM tier of the op after this layer's last linear (the  */
+  int64_t next_w_hbm_bytes;           /* next layer's q / qkv, or the LM head); nullable          */
+  int32_t fuse_norm;                  /* 1: LN1 / LN2 fused into the consuming linears (no LN    */
+                                      /*    kernels; x read raw, see dak_linear_args.ln_w)        */
+  int32_t stats_in_parts;             /* partials in stats_in (dak_layer_stats_parts of the      */
+  const float* stats_in;              /* previous layer, or 1 for dak_embed's statistics)        */
+  float* stats_out;                   /* row statistics of this layer's output x (FC2 epilogue)  */
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);
 /* Enqueue one decode step of one layer: 9 kernels (LN, QKV, KV append, attention + combine,
  * O + residual, LN, FC1 + ReLU, FC2 + residual). */
 dak_status dak_layer(const dak_layer_args* args, dak_stream_t stream);
+/* Number of statistics partials dak_layer writes to stats_out (the FC2 grid). Needs the device. */
+dak_status dak_layer_stats_parts(const dak_layer_args* args, int32_t* parts);
 
 /* =============================================================================================
  * 6. Persistent decode step: the whole op sequence of a decode step in ONE co-resident launch.

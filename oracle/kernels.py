@@ -165,6 +165,14 @@ def lse_merge(partials_o, partials_lse) -> np.ndarray:
     return np.tensordot(w, np.asarray(partials_o, dtype=np.float64), axes=(0, 0))
 
 
+def rmsnorm(x, w, eps: float = 1e-5) -> np.ndarray:
+    """RMSNorm over the last dim in float64 (Llama decoder layer glue, BASELINE C3 model):
+    x / sqrt(mean(x^2) + eps) * w."""
+    x = np.asarray(x, dtype=np.float64)
+    ms = (x * x).mean(axis=-1, keepdims=True)
+    return x / np.sqrt(ms + eps) * w
+
+
 def layernorm(x, w, b, eps: float = 1e-5) -> np.ndarray:
     """LayerNorm over the last dim in float64 (OPT decoder layer glue)."""
     x = np.asarray(x, dtype=np.float64)

@@ -15,6 +15,20 @@ void set_error(const char* fmt, ...) {
   va_end(ap);
 }
 const char* get_error() { return g_err; }
+
+struct TraceMeta {
+  int kind, grid;
+  long long a, b;
+};
+static unsigned long long* g_trace = nullptr;
+static int g_trace_cap = 0, g_trace_n = 0;
+static TraceMeta* g_trace_meta = nullptr;
+
+unsigned long long* trace_slot(int kind, long long a, long long b, int grid) {
+  if (!g_trace || g_trace_n >= g_trace_cap) return nullptr;
+  g_trace_meta[g_trace_n] = TraceMeta{kind, grid, a, b};
+  return g_trace + (size_t)(g_trace_n++) * kTraceCtas * 4;
+}
 }  // namespace dak
 
 extern "C" {
@@ -22,6 +36,27 @@ extern "C" {
 const char* dak_last_error(void) { return dak::get_error(); }
 
 const char* dak_version(void) { return "dak-b200 0.1 (sm_100a)"; }
+
+dak_status dak_trace_enable(void* dev_buf, int32_t max_launches) {
+  delete[] dak::g_trace_meta;
+  dak::g_trace_meta = nullptr;
+  dak::g_trace = (unsigned long long*)dev_buf;
+  dak::g_trace_cap = dev_buf ? max_launches : 0;
+  dak::g_trace_n = 0;
+  if (dev_buf) dak::g_trace_meta = new dak::TraceMeta[max_launches > 0 ? max_launches : 1];
+  return DAK_OK;
+}
+
+dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, int32_t* grid) {
+  if (i < 0 || i >= dak::g_trace_n || !kind || !a || !b || !grid) return dak::fail(DAK_EINVAL, "dak_trace_launch: bad index");
+  *kind = dak::g_trace_meta[i].kind;
+  *a = dak::g_trace_meta[i].a;
+  *b = dak::g_trace_meta[i].b;
+  *grid = dak::g_trace_meta[i].grid;
+  return DAK_OK;
+}
+
+int32_t dak_trace_count(void) { return dak::g_trace_n; }
 
 dak_status dak_device_sms(int32_t* sms) {
   if (!sms) return dak::fail(DAK_EINVAL, "sms is NULL");

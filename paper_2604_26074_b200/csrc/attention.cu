@@ -57,7 +57,17 @@ struct Params {
   int n_host, n_hbm, stages, window;
   int stage_bytes;   // K page + V page
   int off_q, off_scratch, off_pairs;
+  unsigned long long* trace;   // dak_trace_enable slots (nullable): split kernel, combine kernel
+  unsigned long long* trace2;
 };
+
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
+  if (tr && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 4 + k] = t;
+  }
+}
 
 // ------------------------------------------------------------------------------------ PTX glue
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -158,9 +168,11 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       mbar_init(&empty[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tstamp(p.trace, 0);
   }
   grid_dep_launch();
   grid_dep_wait();  // block table, seq_lens and q come from earlier kernels
+  if (threadIdx.x == 0) tstamp(p.trace, 1);
   // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
   const int n_pairs = p.B * p.max_chunks;
   // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
@@ -359,12 +371,15 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     }
     consumer_sync();
   }
+  if (t == 0) tstamp(p.trace, 3);
 }
 
 // merge chunk partials: out[b, h, :] = sum_c w_c o_c, w_c = 2^(lse_c - LSE)   (fixed chunk order)
 __global__ void combine_kernel(const Params p) {
+  if (threadIdx.x == 0) tstamp(p.trace2, 0);
   grid_dep_launch();
   grid_dep_wait();
+  if (threadIdx.x == 0) tstamp(p.trace2, 1);
   const int bh = blockIdx.x;
   const int b = bh / p.Hq, h = bh % p.Hq;
   const int g = h / p.G, hh = h % p.G;
@@ -383,6 +398,7 @@ __global__ void combine_kernel(const Params p) {
     }
     p.out[((long long)b * p.Hq + h) * kD + d] = __float2bfloat16_rn(num / den);
   }
+  if (threadIdx.x == 0) tstamp(p.trace2, 3);
 }
 
 // logical pages [n_blocks][page][d] -> DAK-PG swizzled pages (one thread per 16 bytes)
@@ -400,9 +416,11 @@ __global__ void pack_pages_kernel(const uint4* __restrict__ src, long long n_blo
 // append one token's K and V rows per (request, kv head) at position pos[b] (decode KV write)
 __global__ void append_kernel(const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, long long stride16,
                               const int* block_table, const int* pos, int B, int Hkv, int page, int max_pages,
-                              uint4* k_hbm, uint4* v_hbm, uint4* k_host, uint4* v_host) {
+                              uint4* k_hbm, uint4* v_hbm, uint4* k_host, uint4* v_host, unsigned long long* tr) {
+  if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
+  if (threadIdx.x == 0) tstamp(tr, 3);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (b, g, j)
   const int per = Hkv * (kD / 8);
   if (i >= B * per) return;
@@ -545,6 +563,8 @@ dak_status dak_attention(const dak_attention_args* args, dak_stream_t stream) {
   cfg.stream = (cudaStream_t)stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  pl.p.trace = trace_slot(DAK_KIND_ATTENTION, args->B, args->Hkv, pl.grid);
+  pl.p.trace2 = trace_slot(DAK_KIND_COMBINE, args->B, args->Hq, args->B * args->Hq);
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::split_attention_kernel, pl.p));
   cudaLaunchConfig_t c2{};
   c2.gridDim = dim3(args->B * args->Hq);
@@ -591,7 +611,7 @@ dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_strid
   cfg.numAttrs = 1;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::append_kernel, (const uint4*)k_new, (const uint4*)v_new, stride / 8,
                                   block_table, positions, B, Hkv, page_size, max_pages, (uint4*)k_hbm, (uint4*)v_hbm,
-                                  (uint4*)k_host, (uint4*)v_host));
+                                  (uint4*)k_host, (uint4*)v_host, trace_slot(DAK_KIND_APPEND, B, Hkv, (n + 255) / 256)));
   return DAK_OK;
 }
 

@@ -24,6 +24,17 @@ inline dak_status fail(dak_status st, const char* fmt, ...) {
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Launch-timeline tracing (dak_trace_enable): a launch that takes a slot gets a device pointer to
+// [kTraceCtas][4] globaltimer stamps; nullptr when tracing is off (the kernels then skip it).
+constexpr int kTraceCtas = 1024;
+unsigned long long* trace_slot(int kind, long long a, long long b, int grid);
+#define DAK_KIND_LINEAR 1
+#define DAK_KIND_ATTENTION 2
+#define DAK_KIND_COMBINE 3
+#define DAK_KIND_APPEND 4
+#define DAK_KIND_LAYERNORM 5
+#define DAK_KIND_EMBED 6
+
 }  // namespace dak
 
 #define DAK_CUDA_TRY(expr)                                                                       \

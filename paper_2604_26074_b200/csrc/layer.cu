@@ -12,6 +12,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.h"
 
 namespace dak {
@@ -19,6 +21,13 @@ namespace layer {
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
+  if (tr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 4 + k] = t;
+  }
+}
 
 constexpr int kLnThreads = 256;
 
@@ -38,10 +47,13 @@ __device__ float block_sum(float v, float* red) {
 __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat16* __restrict__ x,
                                                                const __nv_bfloat16* __restrict__ w,
                                                                const __nv_bfloat16* __restrict__ b,
-                                                               __nv_bfloat16* __restrict__ y, int cols, float eps) {
+                                                               __nv_bfloat16* __restrict__ y, int cols, float eps,
+                                                               unsigned long long* tr) {
   __shared__ float red[kLnThreads / 32];
+  tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
+  tstamp(tr, 1);
   const __nv_bfloat16* xr = x + (long long)blockIdx.x * cols;
   float s = 0.f;
   for (int c = threadIdx.x; c < cols; c += kLnThreads) s += __bfloat162float(xr[c]);
@@ -58,22 +70,60 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat
     t = t * __bfloat162float(w[c]) + (b ? __bfloat162float(b[c]) : 0.f);
     yr[c] = __float2bfloat16_rn(t);
   }
+  tstamp(tr, 3);
 }
 
-// x[b] = tok[tokens[b]] + pos[positions[b] + pos_offset]
-__global__ void embed_kernel(const int* __restrict__ tokens, const int* __restrict__ positions,
+// (count, mean, M2) of one row held as one value per thread-slot, two-pass, fixed order
+__device__ void row_stats_store(const float* v, int nv, int cols, float* red, float4* out) {
+  float s = 0.f;
+  for (int i = 0; i < nv; ++i) s += v[i];
+  const float mean = block_sum(s, red) / (float)cols;
+  float m2 = 0.f;
+  for (int i = 0; i < nv; ++i) {
+    const float d = v[i] - mean;
+    m2 += d * d;
+  }
+  m2 = block_sum(m2, red);
+  if (threadIdx.x == 0) *out = make_float4((float)cols, mean, m2, 0.f);
+}
+
+constexpr int kRowMax = 64;  // values per thread held in registers (cols <= 256 * 64)
+
+// x[b] = tok[tokens[b]] + pos[positions[b] + pos_offset]; optional row statistics of the stored x
+__global__ void __launch_bounds__(kLnThreads) embed_kernel(const int* __restrict__ tokens, const int* __restrict__ positions,
                              const __nv_bfloat16* __restrict__ tok, const __nv_bfloat16* __restrict__ pos, int hidden,
-                             int pos_offset, __nv_bfloat16* __restrict__ x) {
+                             int pos_offset, __nv_bfloat16* __restrict__ x, float4* __restrict__ stats,
+                             unsigned long long* tr) {
+  __shared__ float red[kLnThreads / 32];
+  tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
   const int b = blockIdx.x;
   const long long t = tokens[b];
   const long long p = positions ? (long long)positions[b] + pos_offset : -1;
-  for (int c = threadIdx.x; c < hidden; c += blockDim.x) {
-    float v = __bfloat162float(tok[t * hidden + c]);
-    if (pos && p >= 0) v += __bfloat162float(pos[p * hidden + c]);
-    x[(long long)b * hidden + c] = __float2bfloat16_rn(v);
+  float v[kRowMax];
+  int nv = 0;
+  for (int c = threadIdx.x; c < hidden; c += kLnThreads) {
+    float e = __bfloat162float(tok[t * hidden + c]);
+    if (pos && p >= 0) e += __bfloat162float(pos[p * hidden + c]);
+    const __nv_bfloat16 o = __float2bfloat16_rn(e);
+    x[(long long)b * hidden + c] = o;
+    if (nv < kRowMax) v[nv++] = __bfloat162float(o);
   }
+  if (stats) row_stats_store(v, nv, hidden, red, stats + b);
+  tstamp(tr, 3);
+}
+
+// stats[r] = (cols, mean, M2) of row r of x (bf16, row stride ld): the producer side of a fused pre-norm
+__global__ void __launch_bounds__(kLnThreads) row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long ld, int cols,
+                                                              float4* __restrict__ stats) {
+  __shared__ float red[kLnThreads / 32];
+  grid_dep_launch();
+  grid_dep_wait();
+  float v[kRowMax];
+  int nv = 0;
+  for (int c = threadIdx.x; c < cols && nv < kRowMax; c += kLnThreads) v[nv++] = __bfloat162float(x[blockIdx.x * ld + c]);
+  row_stats_store(v, nv, cols, red, stats + blockIdx.x);
 }
 
 static dak_status launch_pdl(const void* fn, dim3 grid, dim3 block, void** args, cudaStream_t s, int pdl) {
@@ -93,8 +143,9 @@ static dak_status launch_pdl(const void* fn, dim3 grid, dim3 block, void** args,
 static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Scratch {
-  size_t h, qkv, attn, f, ws, total, ws_bytes;
+  size_t h, qkv, attn, f, ws, stats, total, ws_bytes;
 };
+constexpr int kMaxParts = 1024;  // statistics partials (producer CTAs) a fused pre-norm merges
 
 static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
   if (a->model != DAK_MODEL_OPT) return fail(DAK_EUNSUPPORTED, "dak_layer: model %d not in this build", a->model);
@@ -116,7 +167,8 @@ static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
   s->f = align256(s->attn + B * a->hidden * 2);
   s->ws = align256(s->f + B * a->ffn * 2);
   s->ws_bytes = ws;
-  s->total = s->ws + ws;
+  s->stats = align256(s->ws + ws);
+  s->total = s->stats + (size_t)kMaxParts * B * 16;
   return DAK_OK;
 }
 
@@ -147,22 +199,42 @@ dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, i
   const __nv_bfloat16* bp = (const __nv_bfloat16*)b;
   __nv_bfloat16* yp = (__nv_bfloat16*)y;
   int c = cols;
-  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps};
+  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, cols, rows);
+  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr};
   return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
                            (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,
-                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, int32_t pdl, dak_stream_t stream) {
+                     int32_t B, int32_t hidden, int32_t pos_offset, void* x, float* stats_out, int32_t pdl,
+                     dak_stream_t stream) {
   if (!tokens || !tok_emb || !x || B <= 0 || hidden <= 0) return fail(DAK_EINVAL, "dak_embed: bad arguments");
+  if (hidden > layer::kLnThreads * layer::kRowMax) return fail(DAK_EUNSUPPORTED, "dak_embed: hidden > %d", layer::kLnThreads * layer::kRowMax);
+  if (stats_out && !aligned16(stats_out)) return fail(DAK_EINVAL, "dak_embed: stats_out must be 16-byte aligned");
   const int* tp = tokens;
   const int* pp = positions;
   const __nv_bfloat16* te = (const __nv_bfloat16*)tok_emb;
   const __nv_bfloat16* pe = (const __nv_bfloat16*)pos_emb;
   int h = hidden, off = pos_offset;
   __nv_bfloat16* xp = (__nv_bfloat16*)x;
-  void* args[] = {&tp, &pp, &te, &pe, &h, &off, &xp};
-  return layer::launch_pdl((const void*)layer::embed_kernel, dim3(B), dim3(256), args, (cudaStream_t)stream, pdl);
+  float4* sp = (float4*)stats_out;
+  unsigned long long* tr = trace_slot(DAK_KIND_EMBED, B, hidden, B);
+  void* args[] = {&tp, &pp, &te, &pe, &h, &off, &xp, &sp, &tr};
+  return layer::launch_pdl((const void*)layer::embed_kernel, dim3(B), dim3(layer::kLnThreads), args, (cudaStream_t)stream, pdl);
+}
+
+dak_status dak_row_stats(const void* x, int32_t rows, int32_t cols, int64_t ld, float* stats_out, int32_t pdl,
+                         dak_stream_t stream) {
+  if (!x || !stats_out || rows <= 0 || cols <= 0) return fail(DAK_EINVAL, "dak_row_stats: bad arguments");
+  if (cols > layer::kLnThreads * layer::kRowMax) return fail(DAK_EUNSUPPORTED, "dak_row_stats: cols > %d", layer::kLnThreads * layer::kRowMax);
+  if (!aligned16(stats_out)) return fail(DAK_EINVAL, "dak_row_stats: stats_out must be 16-byte aligned");
+  const __nv_bfloat16* xp = (const __nv_bfloat16*)x;
+  long long l = ld > 0 ? ld : cols;
+  int c = cols;
+  float4* sp = (float4*)stats_out;
+  void* args[] = {&xp, &l, &c, &sp};
+  return layer::launch_pdl((const void*)layer::row_stats_kernel, dim3(rows), dim3(layer::kLnThreads), args,
+                           (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_layer_scratch_size(const dak_layer_args* a, size_t* bytes) {
@@ -181,17 +253,34 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   if (st != DAK_OK) return st;
   if (!a->x || !a->scratch || a->scratch_bytes < s.total) return fail(DAK_EINVAL, "dak_layer: x / scratch missing or too small");
   if (a->tp_size > 1) return fail(DAK_EUNSUPPORTED, "dak_layer: tensor parallel layer not in this build");
+  const bool fuse = a->fuse_norm != 0;
+  if (fuse && (!a->stats_in || a->stats_in_parts <= 0))
+    return fail(DAK_EINVAL, "dak_layer: fuse_norm needs stats_in / stats_in_parts (row statistics of x)");
   char* sc = (char*)a->scratch;
   void* h = sc + s.h;
   char* qkv = sc + s.qkv;
   void* attn = sc + s.attn;
   void* f = sc + s.f;
+  float* o_stats = (float*)(sc + s.stats);
   const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads;
   const long long qkv_cols = (long long)(Hq + 2 * Hkv) * d;
   const int pdl = a->cfg.pdl;
   cudaStream_t strm = (cudaStream_t)stream;
+  // L2 warm-up chain: every linear prefetches the leading bytes of the next linear's HBM tier
+  const long long pfb = a->l2_prefetch_bytes;
+  auto pf = [&](dak_linear_args& l, const dak_weight& w, long long rows, long long K) {
+    const long long avail = (rows - w.h) * K * 2;
+    if (pfb <= 0 || !w.w_hbm || avail <= 0) return;
+    l.l2_prefetch = w.w_hbm;
+    l.l2_prefetch_bytes = std::min(pfb, avail) & ~15LL;
+  };
+  // pre-norm: either a LayerNorm kernel into h, or fused into the consuming linears (x read raw)
+  auto norm = [&](dak_linear_args& l, const void* w, const void* b, const float* stats, int parts) {
+    l.x = a->x;
+    l.ln_w = w; l.ln_b = b; l.ln_stats = stats; l.ln_parts = parts; l.ln_eps = a->ln_eps;
+  };
 
-  if ((st = dak_layernorm(a->x, a->ln1_w, a->ln1_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
+  if (!fuse && (st = dak_layernorm(a->x, a->ln1_w, a->ln1_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
   dak_linear_args l;
   if (a->split_qkv) {  // q, k, v written side by side into the fused [B, qkv_cols] buffer
     const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
@@ -200,11 +289,16 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
     for (int i = 0; i < 3; ++i) {
       l = layer::lin_args(*w[i], rows[i], H, B, h, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
       l.ldy = qkv_cols;
+      if (fuse) norm(l, a->ln1_w, a->ln1_b, a->stats_in, a->stats_in_parts);
+      if (i < 2) pf(l, *w[i + 1], rows[i + 1], H);
+      else pf(l, a->o, H, (long long)Hq * d);
       if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
       off += rows[i];
     }
   } else {
     l = layer::lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
+    if (fuse) norm(l, a->ln1_w, a->ln1_b, a->stats_in, a->stats_in_parts);
+    pf(l, a->o, H, (long long)Hq * d);
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
   if ((st = dak_kv_append(qkv + (size_t)Hq * d * 2, qkv + (size_t)(Hq + Hkv) * d * 2, qkv_cols, a->block_table,
@@ -224,12 +318,38 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   at.q_row_stride = qkv_cols;
   if ((st = dak_attention(&at, strm)) != DAK_OK) return st;
   l = layer::lin_args(a->o, H, (long long)Hq * d, B, attn, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  pf(l, a->up, a->ffn, H);
+  int o_parts = 0;
+  if (fuse) {
+    dak_linear_launch_info info;
+    if ((st = dak_linear_query(&l, &info)) != DAK_OK) return st;
+    if (info.grid > layer::kMaxParts) return fail(DAK_EUNSUPPORTED, "dak_layer: o-projection grid %d > %d", info.grid, layer::kMaxParts);
+    o_parts = info.grid;
+    l.stats_out = o_stats;
+  }
   if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-  if ((st = dak_layernorm(a->x, a->ln2_w, a->ln2_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
+  if (!fuse && (st = dak_layernorm(a->x, a->ln2_w, a->ln2_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
   l = layer::lin_args(a->up, a->ffn, H, B, h, f, nullptr, DAK_ACT_RELU, a->cfg);
+  if (fuse) norm(l, a->ln2_w, a->ln2_b, o_stats, o_parts);
+  pf(l, a->down, H, a->ffn);
   if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   l = layer::lin_args(a->down, H, a->ffn, B, f, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  if (pfb > 0 && a->next_w_hbm && a->next_w_hbm_bytes > 0) {
+    l.l2_prefetch = a->next_w_hbm;
+    l.l2_prefetch_bytes = std::min(pfb, (long long)a->next_w_hbm_bytes) & ~15LL;
+  }
+  l.stats_out = a->stats_out;
   return dak_linear(&l, strm);
+}
+
+dak_status dak_layer_stats_parts(const dak_layer_args* a, int32_t* parts) {
+  if (!a || !parts) return fail(DAK_EINVAL, "dak_layer_stats_parts: NULL");
+  dak_linear_args l = layer::lin_args(a->down, a->hidden, a->ffn, a->B, a->x, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  dak_linear_launch_info info;
+  dak_status st = dak_linear_query(&l, &info);
+  if (st != DAK_OK) return st;
+  *parts = info.grid;
+  return DAK_OK;
 }
 
 }  // extern "C"

@@ -17,6 +17,7 @@
 // Weights use the DAK-KC layout (see include/dak.h): chunk-major [K/KC][rows][KC], 16-byte
 // chunks of each 128-byte atom XOR-swizzled by (row & 7). One k-chunk of a contiguous row range
 // is one contiguous span, so a pipeline stage is ONE bulk copy of W plus N small copies of x.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -36,7 +37,8 @@ constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 227 * 1024;
 
-struct Params {
+struct __align__(64) Params {
+  CUtensorMap xmap;  // x [N, K] viewed as (64 elements, N rows, K/64 atoms), 128-byte swizzle
   const char* w_host;
   const char* w_hbm;
   long long M, K, h;
@@ -48,10 +50,31 @@ struct Params {
   int act;
   int n_host, n_hbm;
   int stages, window;
-  int w_stage_bytes, x_stage_bytes, x_pitch;
-  int res_offset;  // byte offset of the fp32 result buffer in smem
+  int w_stage_bytes, x_stage_bytes, n8;
+  int off_x, off_ln, res_offset;  // byte offsets (from the 1024-aligned SMEM base)
   long long ldy;   // elements between consecutive rows n of y and residual
+  const char* pf;  // L2 prefetch hint for the next op (nullable)
+  long long pf_bytes;
+  int evict_first;  // stream weights with the L2 evict_first policy
+  int wm, wk;       // MMA path: consumer warps along M x along K (wm * wk == kConsumerWarps)
+  // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
+  const __nv_bfloat16* ln_w;
+  const __nv_bfloat16* ln_b;
+  const float* ln_stats;
+  int ln_parts;
+  float ln_eps;
+  int ln_rms;       // 1: RMSNorm (no mean subtraction, no bias)
+  float* stats_out;  // epilogue row statistics (count, mean, M2) of this CTA's outputs (nullable)
+  unsigned long long* trace;  // dak_trace_enable slot (nullable)
 };
+
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
+  if (tr && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 4 + k] = t;
+  }
+}
 
 // ------------------------------------------------------------------------------------ PTX glue
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -79,6 +102,29 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
       "l"(src), "r"(bytes), "r"(su32(bar))
       : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "l"(pol)
+      : "memory");
+}
+// 3-D tensor TMA global -> shared (box described by the tensor map), completes on an mbarrier
+__device__ __forceinline__ void tma_3d(void* dst, uint64_t tmap, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -114,13 +160,41 @@ __device__ __forceinline__ uint32_t swz(long long r_tier, int sl) {
 // Every loop whose body holds a .sync.aligned instruction has a compile-time trip count, so the
 // hot loop is branch-free (the first build spent ~30 SASS instructions per HMMA on predicates,
 // WARPSYNC and ring-index divisions — profiles/r01/linear_v0_ncu.txt).
-template <int PATH, int NN, int MTW>
-__global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params p) {
-  extern __shared__ __align__(1024) unsigned char smem[];
+//
+// One pipeline stage = TWO copies: the CTA's (rows x KC) weight span (1-D bulk) and the x chunk
+// [N8 rows x KC] (one 3-D tensor TMA, rows >= N zero-filled). Per-copy issue cost in the TMA unit
+// is ~40 ns regardless of size (measured: profiles/r01/linear_copycount.txt), so the earlier
+// one-bulk-copy-per-x-row scheme spent most of the TMA time on 128-512 B copies.
+// x stage layout (128B swizzle): 16-byte chunk c of atom a (64 elements) of row n lives at
+// ((a * N8 + n) * 128) + ((c ^ (n & 7)) << 4) -> conflict-free ldmatrix / LDS.128.
+__device__ __forceinline__ uint32_t x_off(int n8, int n, int sl) {
+  return (uint32_t)((((sl >> 3) * n8 + n) << 7) + (((sl & 7) ^ (n & 7)) << 4));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // identical on all lanes
+  return v;
+}
+// LN(x) pair: ((x - mu) * rs) * w + b, rounded to bf16 (same expression as layernorm_kernel)
+__device__ __forceinline__ uint32_t ln_pair(uint32_t xv, uint32_t wv, uint32_t bv, float mu, float rs) {
+  float t0 = (bf_lo(xv) - mu) * rs, t1 = (bf_hi(xv) - mu) * rs;
+  t0 = t0 * bf_lo(wv) + bf_lo(bv);
+  t1 = t1 * bf_hi(wv) + bf_hi(bv);
+  __nv_bfloat162 h = __floats2bfloat162_rn(t0, t1);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int PATH, int NN, int MTW, bool LN>
+__global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 128B-swizzled TMA destinations need 1024-byte alignment: align the base by hand
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
+  uint64_t* lnbar = empty + kMaxStages;
   unsigned char* wring = smem + 1024;
-  unsigned char* xring = wring + (size_t)p.stages * p.w_stage_bytes;
+  unsigned char* xring = smem + p.off_x;
   float* res = reinterpret_cast<float*>(smem + p.res_offset);
 
   const int cta = blockIdx.x;
@@ -147,44 +221,73 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
+    mbar_init(lnbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (threadIdx.x == 0) tstamp(p.trace, 0);
   grid_dep_launch();  // the next op may start its weight stream as our CTAs retire
-  if (R <= 0) return;
+  if (R <= 0) {
+    if (p.stats_out && threadIdx.x < N) {
+      float4* so = reinterpret_cast<float4*>(p.stats_out) + (size_t)cta * N + threadIdx.x;
+      *so = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    return;
+  }
 
   const uint32_t w_bytes = (uint32_t)R * kc * 2;
-  const uint32_t x_bytes = (uint32_t)kc * 2;
+  const uint32_t x_tx = (uint32_t)p.x_stage_bytes;  // the full box (zero-filled rows count)
   const long long chunk_stride = R_tier * kc * 2;  // bytes between consecutive k-chunks of a row
 
   if (warp == 0) {
-    // ============================ producer: lane 0 streams W, lanes 0..N-1 stream x rows
+    // ============================ producer (one lane): W span + x box per stage
+    if (lane != 0) return;
     const int pro = min(slots, nchunks);
     const char* src = wsrc + rb * kc * 2;
-    if (lane == 0) {
-      for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
-        mbar_expect_tx(&full[i], w_bytes + (uint32_t)N * x_bytes);
-        bulk_g2s(wring + (size_t)i * p.w_stage_bytes, src + (long long)i * chunk_stride, w_bytes, &full[i]);
-      }
+    // weights are read exactly once per step: evict_first keeps L2 for activations and for the
+    // next op's prefetched prefix
+    const bool ef = p.evict_first != 0;
+    const uint64_t pol = policy_evict_first();
+    const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
+    asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+    auto load_w = [&](int slot, int i) {
+      unsigned char* dst = wring + (size_t)slot * p.w_stage_bytes;
+      const char* s_ = src + (long long)i * chunk_stride;
+      if (ef) bulk_g2s_hint(dst, s_, w_bytes, &full[slot], pol);
+      else bulk_g2s(dst, s_, w_bytes, &full[slot]);
+    };
+    auto load_x = [&](int slot, int i) {
+      tma_3d(xring + (size_t)slot * p.x_stage_bytes, xmap, 0, 0, i * (kc >> 6), &full[slot]);
+    };
+    for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
+      mbar_expect_tx(&full[i], w_bytes + x_tx);
+      load_w(i, i);
+    }
+    if (LN) {  // LN weight / bias are parameters too: resident for the whole kernel
+      const uint32_t kb = (uint32_t)p.K * 2;
+      mbar_expect_tx(lnbar, p.ln_b ? 2 * kb : kb);
+      bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
+      if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
     }
     grid_dep_wait();  // x is produced by the previous kernel
-    __syncwarp();
-    const __nv_bfloat16* xrow = p.x + (long long)lane * p.K;
-    if (lane < N)
-      for (int i = 0; i < pro; ++i)
-        bulk_g2s(xring + (size_t)i * p.x_stage_bytes + lane * p.x_pitch, xrow + (long long)i * kc, x_bytes, &full[i]);
+    tstamp(p.trace, 1);
+    for (int i = 0; i < pro; ++i) load_x(i, i);
     int s = pro == slots ? 0 : pro;
     uint32_t ph = pro == slots ? 1u : 0u;
     for (int i = pro; i < nchunks; ++i) {
-      if (lane == 0) {
-        mbar_wait(&empty[s], ph ^ 1u);
-        mbar_expect_tx(&full[s], w_bytes + (uint32_t)N * x_bytes);
-        bulk_g2s(wring + (size_t)s * p.w_stage_bytes, src + (long long)i * chunk_stride, w_bytes, &full[s]);
-      }
-      __syncwarp();
-      if (lane < N)
-        bulk_g2s(xring + (size_t)s * p.x_stage_bytes + lane * p.x_pitch, xrow + (long long)i * kc, x_bytes, &full[s]);
+      mbar_wait(&empty[s], ph ^ 1u);
+      mbar_expect_tx(&full[s], w_bytes + x_tx);
+      load_w(s, i);
+      load_x(s, i);
       if (++s == slots) { s = 0; ph ^= 1u; }
+    }
+    // this CTA's last weight copies are in flight: warm L2 with its slice of the next op's first
+    // bytes so the next kernel's ramp reads L2 while this one drains (hint only)
+    if (p.pf_bytes > 0) {
+      const long long G = gridDim.x;
+      const long long b = (p.pf_bytes * cta / G) & ~15LL;
+      const long long e = (p.pf_bytes * (cta + 1) / G) & ~15LL;
+      for (long long o = b; o < e; o += 32768) prefetch_l2(p.pf + o, (uint32_t)min(32768LL, e - o));
     }
     return;
   }
@@ -192,7 +295,12 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
   // ================================ consumers
   const int t = threadIdx.x - 32;
   const int cw = warp - 1;
+  if (p.trace && t == 0) {  // first stage landed (a second wait on a completed phase returns at once)
+    mbar_wait(&full[0], 0);
+    tstamp(p.trace, 2);
+  }
   const uint32_t wring_u = su32(wring), xring_u = su32(xring);
+  const int n8 = p.n8;
   if constexpr (PATH == 1) {
     constexpr int RPT = MTW;
     const int S = kc >> 3;   // 16-byte slices per row chunk
@@ -206,6 +314,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
       const int r = rg + G * j;
       roff[j] = (uint32_t)r * row_bytes + swz(rb + r, sl);
     }
+    uint32_t xoff[NN];
+#pragma unroll
+    for (int n = 0; n < NN; ++n) xoff[n] = x_off(n8, n, sl);
     float acc[RPT][NN];
 #pragma unroll
     for (int j = 0; j < RPT; ++j)
@@ -220,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
       float xf[NN][8];
 #pragma unroll
       for (int n = 0; n < NN; ++n) {
-        const uint4 v = *reinterpret_cast<const uint4*>(xs + n * p.x_pitch + sl * 16);
+        const uint4 v = *reinterpret_cast<const uint4*>(xs + xoff[n]);
         xf[n][0] = bf_lo(v.x); xf[n][1] = bf_hi(v.x); xf[n][2] = bf_lo(v.y); xf[n][3] = bf_hi(v.y);
         xf[n][4] = bf_lo(v.z); xf[n][5] = bf_hi(v.z); xf[n][6] = bf_lo(v.w); xf[n][7] = bf_hi(v.w);
       }
@@ -273,8 +384,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
   } else {
     constexpr int NT = NN;  // n8 tiles
     const int KS = kc >> 4;
-    const int WK = KS < kConsumerWarps ? KS : kConsumerWarps;
-    const int WM = kConsumerWarps / WK;
+    const int WK = p.wk, WM = p.wm;
     const int wk = cw % WK, wm = cw / WK;
     const int nks = KS / WK;  // k-steps per warp per stage
     const int MT = (R + 15) >> 4;
@@ -292,20 +402,78 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
     const uint32_t a_step = (uint32_t)(WM * 16) * row_bytes;
     const int key = (int)((rb + wm * 16 + (lane & 15)) & 7);
     const int ahalf = lane >> 4;
-    const uint32_t b_base = (uint32_t)((lane & 7) + ((lane >> 4) << 3)) * p.x_pitch + ((lane >> 3) & 1) * 16;
+    // B rows: lane supplies x row n = (lane & 7) + 8 (lane >> 4), 16-byte chunk 2 ks + ((lane >> 3) & 1)
+    const int bn = (lane & 7) + ((lane >> 4) << 3);
+    const int bjh = (lane >> 3) & 1;
+    const uint32_t b_row = (uint32_t)bn << 7;
+    const uint32_t atom_bytes = (uint32_t)n8 << 7;
+    // fused pre-norm: per-row mean / rstd merged from the producer's partials (count, mean, M2):
+    // mean = sum c_j m_j / sum c_j, M2 = sum M2_j + c_j (m_j - mean)^2 (exact decomposition),
+    // lane-strided then butterfly sums: fixed order, one warp per row n
+    float mu[NT], rs[NT];
+    const unsigned char* lnres = smem + p.off_ln;
+    if constexpr (LN) {
+      grid_dep_wait();
+      float* s_ln = reinterpret_cast<float*>(smem + 256);
+      for (int n = cw; n < N; n += kConsumerWarps) {
+        float c = 0.f, cm = 0.f;
+        for (int j = lane; j < p.ln_parts; j += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
+          c += v.x;
+          cm += v.x * v.y;
+        }
+        c = warp_sum(c);
+        const float mean = warp_sum(cm) / c;
+        float m2 = 0.f;
+        for (int j = lane; j < p.ln_parts; j += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
+          const float d = v.y - mean;
+          m2 += v.z + v.x * d * d;
+        }
+        m2 = warp_sum(m2);
+        if (lane == 0) {
+          const float var = p.ln_rms ? m2 / c + mean * mean : m2 / c;  // RMS: mean of squares
+          s_ln[n] = p.ln_rms ? 0.f : mean;
+          s_ln[16 + n] = rsqrtf(var + p.ln_eps);
+        }
+      }
+      consumer_sync();
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const int n = nt * 8 + (lane >> 2);
+        mu[nt] = n < N ? s_ln[n] : 0.f;
+        rs[nt] = n < N ? s_ln[16 + n] : 0.f;
+      }
+      mbar_wait(lnbar, 0);
+    }
+    const bool has_lnb = p.ln_b != nullptr;
     int s = 0;
     uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
       mbar_wait(&full[s], ph);
       const uint32_t ws = wring_u + (uint32_t)s * p.w_stage_bytes + a_base;
-      const uint32_t xs = xring_u + (uint32_t)s * p.x_stage_bytes + b_base;
+      const uint32_t xs = xring_u + (uint32_t)s * p.x_stage_bytes + b_row;
       for (int j = 0; j < nks; ++j) {
         const int ks = wk + j * WK;
         uint32_t b[NT][2];
+        const int c8 = ((ks & 3) << 1) + bjh;
+        const uint32_t baddr = xs + (uint32_t)(ks >> 2) * atom_bytes + (uint32_t)((c8 ^ (bn & 7)) << 4);
         if constexpr (NT == 1) {
-          ldsm_x2(xs + ks * 32, b[0][0], b[0][1]);
+          ldsm_x2(baddr, b[0][0], b[0][1]);
         } else {
-          ldsm_x4(xs + ks * 32, b[0][0], b[0][1], b[1][0], b[1][1]);
+          ldsm_x4(baddr, b[0][0], b[0][1], b[1][0], b[1][1]);
+        }
+        if constexpr (LN) {  // B fragment (n = lane/4 [+8], k = 16ks + 2(lane%4) [+8]) -> LN(x)
+          const int kk = i * kc + ks * 16 + 2 * (lane & 3);
+          const uint32_t w0 = *reinterpret_cast<const uint32_t*>(lnres + kk * 2);
+          const uint32_t w1 = *reinterpret_cast<const uint32_t*>(lnres + (kk + 8) * 2);
+          const uint32_t c0 = has_lnb ? *reinterpret_cast<const uint32_t*>(lnres + (p.K + kk) * 2) : 0u;
+          const uint32_t c1 = has_lnb ? *reinterpret_cast<const uint32_t*>(lnres + (p.K + kk + 8) * 2) : 0u;
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            b[nt][0] = ln_pair(b[nt][0], w0, c0, mu[nt], rs[nt]);
+            b[nt][1] = ln_pair(b[nt][1], w1, c1, mu[nt], rs[nt]);
+          }
         }
         const int sl = 2 * ks + ahalf;
         const uint32_t coff = (uint32_t)(((sl >> 3) << 7) | (((sl & 7) ^ key) << 4));
@@ -357,7 +525,30 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const Params 
     if (p.bias) v += __bfloat162float(p.bias[m]);
     if (p.act == DAK_ACT_RELU) v = fmaxf(v, 0.f);
     if (p.residual) v += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
-    p.y[(long long)n * p.ldy + m] = __float2bfloat16_rn(v);
+    const __nv_bfloat16 o = __float2bfloat16_rn(v);
+    p.y[(long long)n * p.ldy + m] = o;
+    res[(size_t)r * RN + n] = __bfloat162float(o);  // same thread read this slot: no hazard
+  }
+  // row statistics of the stored outputs for a fused pre-norm in the next op (two-pass, fixed order)
+  if (p.stats_out) {
+    consumer_sync();
+    for (int n = cw; n < N; n += kConsumerWarps) {
+      float sm = 0.f;
+      for (int r = lane; r < R; r += 32) sm += res[(size_t)r * RN + n];
+      const float mean = warp_sum(sm) / (float)R;
+      float m2 = 0.f;
+      for (int r = lane; r < R; r += 32) {
+        const float d = res[(size_t)r * RN + n] - mean;
+        m2 += d * d;
+      }
+      m2 = warp_sum(m2);
+      if (lane == 0)
+        reinterpret_cast<float4*>(p.stats_out)[(size_t)cta * N + n] = make_float4((float)R, mean, m2, 0.f);
+    }
+  }
+  if (p.trace) {
+    consumer_sync();
+    if (t == 0) tstamp(p.trace, 3);
   }
 }
 
@@ -449,8 +640,10 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (path != 1 && path != 2) return fail(DAK_EINVAL, "dak_linear: bad force_path");
   // rows per CTA are bounded by the accumulator capacity of the path and by SMEM: at least three
   // ring stages of (rows x KC) weights plus the x rows must fit (deep enough to cover HBM latency)
-  const long long x_stage = ceil_div((long long)ceil_div(N, 8) * 8 * (kc * 2 + 16), 128) * 128;
-  const long long smem_rows = ((kSmemBudget - 1024 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
+  const int n8 = path == 1 ? 8 : (int)ceil_div(N, 8) * 8;
+  const long long x_stage = (long long)n8 * kc * 2;
+  const long long smem_rows = ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
+  if (path == 1 && kc > 8 * kConsumers) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path needs kc <= %d", 8 * kConsumers);
   const long long cap = std::min(path_row_cap(path, kc), smem_rows);
   if (cap < 16) return fail(DAK_EUNSUPPORTED, "dak_linear: kc=%d leaves no room for a 16-row stage", kc);
 
@@ -473,17 +666,19 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
 
   // unroll bucket and the rows one stage must hold (MMA tiles read whole 16-row groups)
   long long rows_alloc;
-  int bucket;
+  int bucket, wm = 1, wk = 1;
   if (path == 1) {
     const int G = kConsumers / (kc / 8);
     bucket = bucket_of(kRptBuckets, 5, ceil_div(rmax, G));
     rows_alloc = ceil_div(rmax, 16) * 16;
   } else {
+    // warps split K first (the split depends on KC only, so the summation order of a row does
+    // not depend on how many rows its CTA owns: bitwise r-invariance); leftover warps split M
     const int KS = kc / 16;
-    const int WK = KS < kConsumerWarps ? KS : kConsumerWarps;
-    const int WM = kConsumerWarps / WK;
-    bucket = bucket_of(kMtwBuckets, 7, ceil_div(ceil_div(rmax, 16), WM));
-    rows_alloc = (long long)WM * bucket * 16;
+    wk = KS < kConsumerWarps ? KS : kConsumerWarps;
+    wm = kConsumerWarps / wk;
+    bucket = bucket_of(kMtwBuckets, 7, ceil_div(ceil_div(rmax, 16), wm));
+    rows_alloc = (long long)wm * bucket * 16;
   }
   if (bucket < 0) return fail(DAK_EUNSUPPORTED, "dak_linear: no unroll bucket for %lld rows per CTA", rmax);
 
@@ -497,16 +692,43 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.residual = (const __nv_bfloat16*)a->residual;
   p.act = a->act;
   p.ldy = a->ldy > 0 ? a->ldy : M;
+  if (a->l2_prefetch_bytes > 0) {
+    if (!a->l2_prefetch || !aligned16(a->l2_prefetch) || a->l2_prefetch_bytes % 16)
+      return fail(DAK_EINVAL, "dak_linear: l2_prefetch must be 16-byte aligned with a multiple-of-16 size");
+    p.pf = (const char*)a->l2_prefetch;
+    p.pf_bytes = a->l2_prefetch_bytes;
+  }
+  p.evict_first = c.l2_policy == 0;
   if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
   p.n_host = n_host; p.n_hbm = n_hbm;
+  p.wm = wm; p.wk = wk;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
-  p.x_pitch = kc * 2 + 16;
-  const int x_rows = path == 1 ? N : (int)ceil_div(N, 8) * 8;
-  p.x_stage_bytes = (int)(ceil_div((long long)x_rows * p.x_pitch, 128) * 128);
+  p.n8 = n8;
+  p.x_stage_bytes = (int)x_stage;  // [kc/64 atoms][n8 rows][64], 128B-swizzled (a multiple of 1 KB)
+  int ln_bytes = 0;
+  if (a->ln_w) {
+    if (path != 2) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm needs the tensor-core path");
+    if (K > 8192) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm keeps LN weights resident: K <= 8192");
+    ln_bytes = (int)ceil_div((a->ln_b ? 4 : 2) * K, 128) * 128;
+    if (!a->ln_stats || a->ln_parts <= 0) return fail(DAK_EINVAL, "dak_linear: ln_w set but ln_stats / ln_parts missing");
+    if (!aligned16(a->ln_w) || !aligned16(a->ln_b) || !aligned16(a->ln_stats))
+      return fail(DAK_EINVAL, "dak_linear: ln_w / ln_b / ln_stats must be 16-byte aligned");
+    if (a->ln_rms && a->ln_b) return fail(DAK_EINVAL, "dak_linear: RMSNorm takes no bias");
+    p.ln_w = (const __nv_bfloat16*)a->ln_w;
+    p.ln_b = (const __nv_bfloat16*)a->ln_b;
+    p.ln_stats = a->ln_stats;
+    p.ln_parts = a->ln_parts;
+    p.ln_eps = a->ln_eps;
+    p.ln_rms = a->ln_rms ? 1 : 0;
+  }
+  if (a->stats_out && !aligned16(a->stats_out)) return fail(DAK_EINVAL, "dak_linear: stats_out must be 16-byte aligned");
+  p.stats_out = a->stats_out;
   const int W2 = (path == 1 && kc / 8 > 32) ? kc / 8 / 32 : 1;
   const int res_bytes = (int)(ceil_div((long long)W2 * rmax * N * 4, 128) * 128);
   const int per_stage = p.w_stage_bytes + p.x_stage_bytes;
-  int max_stages = (kSmemBudget - 1024 - res_bytes) / per_stage;
+  // SMEM (from a 1024-aligned base; +1 KB for the alignment pad): [1 KB barriers + LN stats]
+  // [stages x W span][stages x x box][LN weight, bias][fp32 results]
+  int max_stages = (kSmemBudget - 2048 - ln_bytes - res_bytes) / per_stage;
   if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_linear: stage of %d B does not fit twice in SMEM (use a smaller kc)", per_stage);
   max_stages = std::min(max_stages, kMaxStages);
   int stages = c.stages > 0 ? std::min(c.stages, max_stages) : max_stages;
@@ -524,22 +746,49 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     }
   }
   p.window = std::max(1, window);
-  p.res_offset = 1024 + stages * per_stage;
+  p.off_x = 1024 + stages * p.w_stage_bytes;
+  p.off_ln = p.off_x + stages * p.x_stage_bytes;
+  p.res_offset = p.off_ln + ln_bytes;
 
   out->p = p;
   out->path = path;
   out->nn = path == 1 ? N : (int)ceil_div(N, 8);
   out->bucket = bucket;
   out->grid = n_host + n_hbm;
-  out->smem = p.res_offset + res_bytes;
+  out->smem = p.res_offset + res_bytes + 1024;
   out->rmax_host = rmax_host;
   out->rmax_hbm = rmax_hbm;
   return DAK_OK;
 }
 
-template <int PATH, int NN, int B>
+// x [N, K] bf16 as a 3-D tensor (64 elements, N rows, K/64 atoms): one box [64, n8, kc/64] per
+// stage, 128-byte swizzle, rows >= N zero-filled by the TMA unit.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static dak_status encode_xmap(Params* p) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    DAK_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) return fail(DAK_ECUDA, "dak_linear: cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)f;
+  }
+  const cuuint64_t dims[3] = {64, (cuuint64_t)p->N, (cuuint64_t)(p->K / 64)};
+  const cuuint64_t strides[2] = {(cuuint64_t)p->K * 2, 128};
+  const cuuint32_t box[3] = {64, (cuuint32_t)p->n8, (cuuint32_t)(p->kc / 64)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(&p->xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)p->x, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DAK_ECUDA, "dak_linear: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DAK_OK;
+}
+
+template <int PATH, int NN, int B, bool LN>
 static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
-  auto kern = split_linear_kernel<PATH, NN, B>;
+  auto kern = split_linear_kernel<PATH, NN, B, LN>;
   static int smem_set = 0;  // raise the opt-in limit once per instance (not a stream op; capture-safe)
   if (!smem_set) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
@@ -559,25 +808,25 @@ static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
   return DAK_OK;
 }
 
-template <int PATH, int NN>
+template <int PATH, int NN, bool LN>
 static dak_status launch_b(const Plan& pl, cudaStream_t s, int pdl) {
   if constexpr (PATH == 1) {
     switch (pl.bucket) {
-      case 1: return launch_t<1, NN, 1>(pl, s, pdl);
-      case 2: return launch_t<1, NN, 2>(pl, s, pdl);
-      case 4: return launch_t<1, NN, 4>(pl, s, pdl);
-      case 8: return launch_t<1, NN, 8>(pl, s, pdl);
-      case 16: return launch_t<1, NN, 16>(pl, s, pdl);
+      case 1: return launch_t<1, NN, 1, false>(pl, s, pdl);
+      case 2: return launch_t<1, NN, 2, false>(pl, s, pdl);
+      case 4: return launch_t<1, NN, 4, false>(pl, s, pdl);
+      case 8: return launch_t<1, NN, 8, false>(pl, s, pdl);
+      case 16: return launch_t<1, NN, 16, false>(pl, s, pdl);
     }
   } else {
     switch (pl.bucket) {
-      case 1: return launch_t<2, NN, 1>(pl, s, pdl);
-      case 2: return launch_t<2, NN, 2>(pl, s, pdl);
-      case 3: return launch_t<2, NN, 3>(pl, s, pdl);
-      case 4: return launch_t<2, NN, 4>(pl, s, pdl);
-      case 6: return launch_t<2, NN, 6>(pl, s, pdl);
-      case 8: return launch_t<2, NN, 8>(pl, s, pdl);
-      case 12: return launch_t<2, NN, 12>(pl, s, pdl);
+      case 1: return launch_t<2, NN, 1, LN>(pl, s, pdl);
+      case 2: return launch_t<2, NN, 2, LN>(pl, s, pdl);
+      case 3: return launch_t<2, NN, 3, LN>(pl, s, pdl);
+      case 4: return launch_t<2, NN, 4, LN>(pl, s, pdl);
+      case 6: return launch_t<2, NN, 6, LN>(pl, s, pdl);
+      case 8: return launch_t<2, NN, 8, LN>(pl, s, pdl);
+      case 12: return launch_t<2, NN, 12, LN>(pl, s, pdl);
     }
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for bucket %d", pl.bucket);
@@ -587,15 +836,15 @@ static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
   if (pl.path == 1) {
     switch (pl.nn) {
-      case 1: return launch_b<1, 1>(pl, s, pdl);
-      case 2: return launch_b<1, 2>(pl, s, pdl);
-      case 3: return launch_b<1, 3>(pl, s, pdl);
-      case 4: return launch_b<1, 4>(pl, s, pdl);
+      case 1: return launch_b<1, 1, false>(pl, s, pdl);
+      case 2: return launch_b<1, 2, false>(pl, s, pdl);
+      case 3: return launch_b<1, 3, false>(pl, s, pdl);
+      case 4: return launch_b<1, 4, false>(pl, s, pdl);
     }
   } else {
     switch (pl.nn) {
-      case 1: return launch_b<2, 1>(pl, s, pdl);
-      case 2: return launch_b<2, 2>(pl, s, pdl);
+      case 1: return pl.p.ln_w ? launch_b<2, 1, true>(pl, s, pdl) : launch_b<2, 1, false>(pl, s, pdl);
+      case 2: return pl.p.ln_w ? launch_b<2, 2, true>(pl, s, pdl) : launch_b<2, 2, false>(pl, s, pdl);
     }
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for path %d / %d", pl.path, pl.nn);
@@ -681,6 +930,8 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
   dak_status st = lin::make_plan(args, &pl);
   if (st != DAK_OK) return st;
   if (pl.grid && !(pl.p.y)) return fail(DAK_EINVAL, "dak_linear: y NULL");
+  if (pl.grid && (st = lin::encode_xmap(&pl.p)) != DAK_OK) return st;
+  pl.p.trace = trace_slot(DAK_KIND_LINEAR, args->M, args->K, pl.grid);
   return lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl);
 }
 

@@ -52,14 +52,16 @@ class dak_op_plan(C.Structure):
 class dak_launch_cfg(C.Structure):
     _fields_ = [("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("window", C.c_int32), ("stages", C.c_int32),
                 ("congestion_control", C.c_int32), ("pdl", C.c_int32), ("force_path", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("l2_policy", C.c_int32)]
 
 
 class dak_linear_args(C.Structure):
     _fields_ = [("w_host", C.c_void_p), ("w_hbm", C.c_void_p), ("M", C.c_int64), ("K", C.c_int64), ("h", C.c_int64),
                 ("kc", C.c_int32), ("N", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p), ("bias", C.c_void_p),
                 ("residual", C.c_void_p), ("act", C.c_int32), ("reserved", C.c_int32), ("cfg", dak_launch_cfg),
-                ("ldy", C.c_int64)]
+                ("ldy", C.c_int64), ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_int64),
+                ("ln_w", C.c_void_p), ("ln_b", C.c_void_p), ("ln_stats", C.c_void_p), ("ln_parts", C.c_int32),
+                ("ln_rms", C.c_int32), ("ln_eps", C.c_float), ("reserved2", C.c_int32), ("stats_out", C.c_void_p)]
 
 
 class dak_linear_launch_info(C.Structure):
@@ -79,6 +81,10 @@ def _sig(name, res, args):
 _sig("dak_last_error", C.c_char_p, [])
 _sig("dak_version", C.c_char_p, [])
 _sig("dak_device_sms", C.c_int32, [C.POINTER(C.c_int32)])
+_sig("dak_trace_enable", C.c_int32, [C.c_void_p, C.c_int32])
+_sig("dak_trace_count", C.c_int32, [])
+_sig("dak_trace_launch", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                     C.POINTER(C.c_int32)])
 _sig("dak_plan_ratios", C.c_int32, [C.POINTER(dak_hw), C.POINTER(dak_op), C.c_int32, C.c_int64, C.c_int32,
                                     C.POINTER(dak_op_plan), C.POINTER(C.c_double)])
 _sig("dak_host_alloc", C.c_int32, [C.c_size_t, C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)])
@@ -109,7 +115,7 @@ _sig("dak_kv_append", C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
 EXPORTED = ["dak_pack_kv_pages", "dak_attention_workspace_size", "dak_attention", "dak_kv_append",
             "dak_last_error", "dak_version", "dak_device_sms", "dak_plan_ratios", "dak_host_alloc", "dak_host_free",
             "dak_linear_packed_bytes", "dak_pack_linear", "dak_linear_default_kc", "dak_linear_query",
-            "dak_linear_cta_rows", "dak_linear"]
+            "dak_linear_cta_rows", "dak_linear", "dak_trace_enable", "dak_trace_count", "dak_trace_launch"]
 
 
 def _check(st: int):
@@ -142,6 +148,24 @@ def _stream(s) -> int | None:
 
 def version() -> str:
     return lib.dak_version().decode()
+
+
+TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed"}
+
+
+def trace_enable(dev_buf, max_launches: int):
+    """Record per-CTA globaltimer stamps of the next max_launches per-op launches (dak.h)."""
+    _check(lib.dak_trace_enable(_ptr(dev_buf), int(max_launches)))
+
+
+def trace_launches() -> list:
+    out = []
+    for i in range(lib.dak_trace_count()):
+        k, g = C.c_int32(), C.c_int32()
+        a, b = C.c_int64(), C.c_int64()
+        _check(lib.dak_trace_launch(i, C.byref(k), C.byref(a), C.byref(b), C.byref(g)))
+        out.append(dict(kind=TRACE_KINDS.get(k.value, k.value), a=a.value, b=b.value, grid=g.value))
+    return out
 
 
 def device_sms() -> int:
@@ -201,7 +225,9 @@ def launch_cfg(**kw) -> dak_launch_cfg:
     return c
 
 
-def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, act=ACT_NONE, cfg=None, ldy=0):
+def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, act=ACT_NONE, cfg=None, ldy=0,
+                l2_prefetch=None, l2_prefetch_bytes=0, ln_w=None, ln_b=None, ln_stats=None, ln_parts=0, ln_rms=0,
+                ln_eps=1e-5, stats_out=None):
     a = dak_linear_args()
     a.w_host = _ptr(w_host)
     a.w_hbm = _ptr(w_hbm)
@@ -211,6 +237,10 @@ def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, a
     a.act = int(act)
     a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
     a.ldy = int(ldy)
+    a.l2_prefetch, a.l2_prefetch_bytes = _ptr(l2_prefetch), int(l2_prefetch_bytes)
+    a.ln_w, a.ln_b, a.ln_stats = _ptr(ln_w), _ptr(ln_b), _ptr(ln_stats)
+    a.ln_parts, a.ln_rms, a.ln_eps = int(ln_parts), int(ln_rms), float(ln_eps)
+    a.stats_out = _ptr(stats_out)
     return a
 
 
@@ -287,16 +317,22 @@ class dak_layer_args(C.Structure):
                 ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
                 ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("reserved", C.c_int32),
                 ("cfg", dak_launch_cfg), ("attn_cfg", dak_launch_cfg), ("split_qkv", C.c_int32),
-                ("reserved2", C.c_int32), ("q", dak_weight), ("k", dak_weight), ("v", dak_weight)]
+                ("reserved2", C.c_int32), ("q", dak_weight), ("k", dak_weight), ("v", dak_weight),
+                ("l2_prefetch_bytes", C.c_int64), ("next_w_hbm", C.c_void_p), ("next_w_hbm_bytes", C.c_int64),
+                ("fuse_norm", C.c_int32), ("stats_in_parts", C.c_int32), ("stats_in", C.c_void_p),
+                ("stats_out", C.c_void_p)]
 
 
 _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
                                   C.c_int32, C.c_void_p])
 _sig("dak_embed", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
-                              C.c_void_p, C.c_int32, C.c_void_p])
+                              C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p])
+_sig("dak_row_stats", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p])
 _sig("dak_layer_scratch_size", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_size_t)])
 _sig("dak_layer", C.c_int32, [C.POINTER(dak_layer_args), C.c_void_p])
-EXPORTED += ["dak_layernorm", "dak_embed", "dak_layer_scratch_size", "dak_layer"]
+_sig("dak_layer_stats_parts", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_int32)])
+EXPORTED += ["dak_layernorm", "dak_embed", "dak_row_stats", "dak_layer_scratch_size", "dak_layer",
+             "dak_layer_stats_parts"]
 
 
 def weight(w_host, w_hbm, h, kc, bias=None, n_cta_host=0) -> dak_weight:
@@ -308,9 +344,19 @@ def layernorm(x, w, b, y, rows, cols, eps=1e-5, pdl=0, stream=None):
                              _stream(stream)))
 
 
-def embed(tokens, positions, tok_emb, pos_emb, B, hidden, pos_offset, x, pdl=0, stream=None):
+def embed(tokens, positions, tok_emb, pos_emb, B, hidden, pos_offset, x, pdl=0, stream=None, stats_out=None):
     _check(lib.dak_embed(_ptr(tokens), _ptr(positions), _ptr(tok_emb), _ptr(pos_emb), int(B), int(hidden),
-                         int(pos_offset), _ptr(x), int(pdl), _stream(stream)))
+                         int(pos_offset), _ptr(x), _ptr(stats_out), int(pdl), _stream(stream)))
+
+
+def row_stats(x, rows, cols, stats_out, ld=0, pdl=0, stream=None):
+    _check(lib.dak_row_stats(_ptr(x), int(rows), int(cols), int(ld), _ptr(stats_out), int(pdl), _stream(stream)))
+
+
+def layer_stats_parts(args: dak_layer_args) -> int:
+    v = C.c_int32()
+    _check(lib.dak_layer_stats_parts(C.byref(args), C.byref(v)))
+    return v.value
 
 
 def layer_scratch_size(args: dak_layer_args) -> int:

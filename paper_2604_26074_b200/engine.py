@@ -79,12 +79,16 @@ class DakOPT:
     def __init__(self, cfg: OPTConfig, batch: int, context: int, hw: HW, mode: int = dak.PLAN_BALANCED,
                  y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 16, seed: int = 0,
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
-                 host_override: dict | None = None, n_cta_host: int = 2):
+                 host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
+                 evict_first: bool = True, fuse_norm: bool = True):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
         self.pdl = int(pdl)
         self.n_cta_host = n_cta_host
-        self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host)
+        self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host,
+                           l2_policy=0 if evict_first else 1)
+        self.l2_prefetch = int(l2_prefetch)
+        self.fuse_norm = bool(fuse_norm)
         self.sms = dak.device_sms()
         self.gen = torch.Generator(device="cuda")
         self.gen.manual_seed(seed)
@@ -249,6 +253,15 @@ class DakOPT:
         self.scratch = torch.empty(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
         for a in self.layer_args:
             a.scratch, a.scratch_bytes = self.scratch.data_ptr(), self.scratch.numel()
+        # fused pre-norm: the residual stream's row statistics travel embed -> FC2 -> FC2 ... -> head
+        # (one buffer: every reader of layer l's statistics finishes before FC2 of layer l rewrites it)
+        self.stats = torch.zeros((1024, B, 4), dtype=torch.float32, device="cuda")
+        parts = 1
+        for a in self.layer_args:
+            a.fuse_norm = int(self.fuse_norm)
+            a.stats_in, a.stats_in_parts, a.stats_out = self.stats.data_ptr(), parts, self.stats.data_ptr()
+            parts = dak.layer_stats_parts(a)
+        self.head_stats_parts = parts
 
     def load_kv(self, K_cache, V_cache):
         """Place a given cache: K_cache[l][b] = [L_b, Hkv, d] bf16 bits (numpy) of the tokens before
@@ -296,6 +309,11 @@ class DakOPT:
         a.tp_rank, a.tp_size = 0, 1
         a.cfg = dak.launch_cfg(**self.launch)
         a.attn_cfg = dak.launch_cfg(**self.launch)
+        # L2 warm-up chain (dak.h): the last linear of layer l warms the next layer's q (or the head)
+        nxt = self.layers[l + 1]["q"] if l + 1 < c.n_layers else self.head
+        a.l2_prefetch_bytes = self.l2_prefetch
+        if nxt.hbm is not None:
+            a.next_w_hbm, a.next_w_hbm_bytes = nxt.hbm.data_ptr(), (nxt.M - nxt.h) * nxt.K * 2
         return a
 
     # ------------------------------------------------------------------ persistent step program
@@ -383,17 +401,25 @@ class DakOPT:
             return
         c = self.cfg
         dak.embed(self.tokens, self.positions, self.tok_emb, self.pos_emb, self.B, c.hidden, 2, self.x,
-                  pdl=self.pdl, stream=stream)
+                  pdl=self.pdl, stream=stream, stats_out=self.stats if self.fuse_norm else None)
         for a in self.layer_args:
             dak.layer(a, stream)
-        dak.layernorm(self.x, self.lnf_w, self.lnf_b, self.h, self.B, c.hidden, 1e-5, pdl=self.pdl, stream=stream)
-        ha = dak.linear_args(self.head.host[1] if self.head.host else None, self.head.hbm, self.head.M, self.head.K,
-                             self.head.h, self.head.kc, self.B, self.h, self.logits, cfg=self.launch)
+        hw = self.head.host[1] if self.head.host else None
+        if self.fuse_norm:  # LN_f fused into the LM head
+            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
+                                 self.x, self.logits, cfg=self.launch, ln_w=self.lnf_w, ln_b=self.lnf_b,
+                                 ln_stats=self.stats, ln_parts=self.head_stats_parts, ln_eps=1e-5)
+        else:
+            dak.layernorm(self.x, self.lnf_w, self.lnf_b, self.h, self.B, c.hidden, 1e-5, pdl=self.pdl, stream=stream)
+            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
+                                 self.h, self.logits, cfg=self.launch)
         dak.linear(ha, stream)
 
     def kernels_per_step(self) -> int:
         if getattr(self, "use_step", False):
             return 1
+        if self.fuse_norm:
+            return 1 + 9 * self.cfg.n_layers + 1
         return 1 + 11 * self.cfg.n_layers + 2
 
     def enable_persistent_step(self):

@@ -177,6 +177,25 @@ def test_layernorm_closed_form():
     assert np.allclose(y, (x - 2.5) / np.sqrt(1.25))
 
 
+def test_rmsnorm_pins():
+    """RMSNorm: a constant row c maps to sign(c) * w (eps = 0); invariant to positive scaling;
+    equals the Llama reference module (transformers LlamaRMSNorm)."""
+    w = np.array([0.5, -1.0, 2.0, 3.0])
+    assert np.allclose(Kx.rmsnorm(np.full((1, 4), -3.0), w, eps=0.0), -w)
+    g = np.random.default_rng(11)
+    x = g.standard_normal((3, 64))
+    w = g.standard_normal(64)
+    assert np.allclose(Kx.rmsnorm(7.5 * x, w, eps=0.0), Kx.rmsnorm(x, w, eps=0.0), rtol=1e-13)
+    import torch
+    from transformers.models.llama.modeling_llama import LlamaRMSNorm
+    m = LlamaRMSNorm(64, eps=1e-5).double()
+    with torch.no_grad():
+        m.weight.copy_(torch.from_numpy(w))
+        ref = m(torch.from_numpy(x)).numpy()
+    # (the module computes its statistics in float32 even for float64 input)
+    assert np.allclose(Kx.rmsnorm(x, w, eps=1e-5), ref, rtol=1e-6, atol=1e-7)
+
+
 def test_round_to_bf16_matches_bit_definition():
     """round_to_bf16 == the RNE bit rounding of the input generator on float32-exact values, and
     is exact on representable values (integers up to 256, powers of two)."""

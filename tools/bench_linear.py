@@ -34,13 +34,21 @@ def setup(M, K, N, h, kc, copies):
     return hbm, hosts, x, y
 
 
-def time_cfg(M, K, N, h, kc, launches=64, reps=10, **cfg):
+def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, **cfg):
     size = M * K * 2
     copies = max(2, min(64, int(np.ceil(4 * L2 / max(size, 1)))))
     hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
+    lnw = torch.ones(K, device="cuda", dtype=torch.bfloat16)
+    lnb = torch.zeros(K, device="cuda", dtype=torch.bfloat16)
+    st_in = torch.zeros((148, N, 4), device="cuda", dtype=torch.float32)
+    st_in[:, :, 0] = K / 148.0
+    st_in[:, :, 2] = K / 148.0
+    st_out = torch.zeros((1024, N, 4), device="cuda", dtype=torch.float32)
+    ln_kw = dict(ln_w=lnw, ln_b=lnb, ln_stats=st_in, ln_parts=148) if ln else {}
     args = []
     for i in range(launches):
-        a = dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg)
+        a = dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg,
+                            stats_out=st_out if stats else None, **ln_kw)
         args.append(a)
     info = dak.linear_query(args[0])
     s = torch.cuda.Stream()
@@ -69,7 +77,7 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, **cfg):
         dak.host_free(hp)
     del hbm
     torch.cuda.empty_cache()
-    return dict(M=M, K=K, N=N, h=h, kc=kc, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
+    return dict(M=M, K=K, N=N, h=h, kc=kc, ln=ln, stats=stats, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
                 host_gbs=h * K * 2 / t / 1e9, info={k: info[k] for k in ("grid", "n_cta_host", "stages_hbm", "window_host",
                                                                         "smem_bytes", "path")}, cfg=cfg)
 
@@ -77,7 +85,15 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, **cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "ln":  # fused pre-norm / stats epilogue cost at the OPT-30B shapes (N = 8)
+        for (M, K, h, kc) in ((7168, 7168, 48, 256), (28672, 7168, 192, 64)):
+            for pdl in (0, 1):
+                for ln, st in ((False, False), (True, False), (False, True)):
+                    print(json.dumps(time_cfg(M, K, 8, h, kc, ln=ln, stats=st, pdl=pdl, n_cta_host=2,
+                                              congestion_control=1)), flush=True)
+        return
     shapes = [(4096, 4096), (7168, 7168), (28672, 7168), (7168, 28672)]
     Ns = [1, 8] if a.quick else [1, 2, 4, 8, 16]
     for (M, K) in shapes:

@@ -1,0 +1,92 @@
+"""Per-op launch timeline of the per-op decode step (dak_layer path) from dak_trace stamps.
+
+Usage: python tools/trace_perop.py [layers] [batch] [--no-fuse-norm] [--no-pdl]
+Captures one decode step in a CUDA graph with tracing on, replays it, and prints per launch the
+CTA start spread, the dependency-release time, the first-stage time and the completion time
+(all relative to the step's first stamp), then per-kind aggregates of the incremental time
+(this op's last CTA done minus the previous op's last CTA done).
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+
+from paper_2604_26074_b200 import dak
+from paper_2604_26074_b200.engine import DakOPT, HW, OPTConfig, OPT_30B
+
+
+def main():
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    layers = int(args[0]) if args else 8
+    batch = int(args[1]) if len(args) > 1 else 8
+    cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    eng = DakOPT(cfg, batch, 64, hw, mode=dak.PLAN_BALANCED, fuse_norm="--no-fuse-norm" not in sys.argv,
+                 pdl="--no-pdl" not in sys.argv)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        eng.enqueue_step(s)
+    s.synchronize()
+    n_launch = eng.kernels_per_step() + 8
+    buf = torch.zeros(n_launch * 1024 * 4, dtype=torch.int64, device="cuda")
+    dak.trace_enable(buf, n_launch)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+        eng.enqueue_step(s)
+    meta = dak.trace_launches()
+    dak.trace_enable(None, 0)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(s)
+    g.replay()
+    ev1.record(s)
+    torch.cuda.synchronize()
+    step_ms = ev0.elapsed_time(ev1)
+    T = buf.view(-1, 1024, 4).cpu().numpy().astype(np.float64)
+    rows = []
+    t0 = None
+    for i, m in enumerate(meta):
+        st = T[i, :m["grid"]]
+        valid = st[:, 0] > 0
+        s0 = st[valid, 0]
+        if t0 is None:
+            t0 = s0.min()
+        end = st[valid, 3].max()
+        dep = st[valid, 1][st[valid, 1] > 0]
+        fs = st[valid, 2][st[valid, 2] > 0]
+        rows.append(dict(i=i, kind=m["kind"], a=m["a"], b=m["b"], grid=m["grid"],
+                         start_min=(s0.min() - t0) / 1e3, start_max=(s0.max() - t0) / 1e3,
+                         dep_max=((dep.max() - t0) / 1e3) if dep.size else None,
+                         first_stage_med=((np.median(fs) - t0) / 1e3) if fs.size else None,
+                         end_max=(end - t0) / 1e3))
+    prev_end = 0.0
+    agg = {}
+    for r in rows:
+        inc = r["end_max"] - prev_end
+        r["inc"] = inc
+        prev_end = r["end_max"]
+        key = r["kind"] + (f"[M={r['a']}]" if r["kind"] == "linear" else "")
+        a = agg.setdefault(key, [0, 0.0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += inc
+        a[2] += r["end_max"] - r["start_min"]
+        a[3] += (r["end_max"] - r["dep_max"]) if r["dep_max"] is not None else 0.0
+    print(json.dumps(dict(layers=layers, batch=batch, step_ms_graph=step_ms, traced_span_us=prev_end,
+                          launches=len(rows))))
+    for k, (c, inc, dur, after_dep) in agg.items():
+        print(json.dumps(dict(kind=k, count=c, total_inc_us=round(inc, 1), mean_inc_us=round(inc / c, 2),
+                              mean_span_us=round(dur / c, 2), mean_after_dep_us=round(after_dep / c, 2))))
+    mid = len(rows) // 2
+    for r in rows[mid - 6: mid + 8]:
+        print(" ".join(f"{k}={v:.2f}" if isinstance(v, float) else f"{k}={v}" for k, v in r.items()))
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
