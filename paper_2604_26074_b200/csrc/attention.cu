@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   uint64_t* empty = full + kMaxStages;
   int* s_count = reinterpret_cast<int*>(empty + kMaxStages);
   unsigned char* ring = smem + 1024;
-  unsigned char* qs = smem + p.off_q;
+  unsigned char* qring = smem + p.off_q;  // [stages][kGmax][kD] bf16: q of the unit starting in that stage
   float* scratch = reinterpret_cast<float*>(smem + p.off_scratch);
   int* pref = reinterpret_cast<int*>(smem + p.off_pairs);
 
@@ -170,6 +170,10 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
   }
+  // q rows >= G of every slot stay zero (the bulk copies write rows < G only)
+  for (int i = threadIdx.x; i < p.stages * kGmax * kD / 8; i += kThreads)
+    reinterpret_cast<uint4*>(qring)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   grid_dep_launch();
   grid_dep_wait();  // block table, seq_lens and q come from earlier kernels
   if (threadIdx.x == 0) tstamp(p.trace, 1);
@@ -231,10 +235,14 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
           const long long idx = (long long)(e & ~kHostBit);
           const bool eh = (e & kHostBit) != 0;
           const long long off = (idx * p.Hkv + g) * (long long)page_bytes;
-          mbar_expect_tx(&full[s], 2u * page_bytes);
+          const uint32_t q_bytes = pg == pg0 ? (uint32_t)p.G * kD * 2 : 0u;  // q rides with the first page
+          mbar_expect_tx(&full[s], 2u * page_bytes + q_bytes);
           unsigned char* dst = ring + (size_t)s * p.stage_bytes;
           bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, page_bytes, &full[s]);
           bulk_g2s(dst + page_bytes, (eh ? p.v_host : p.v_hbm) + off, page_bytes, &full[s]);
+          if (q_bytes)
+            bulk_g2s(qring + (size_t)s * kGmax * kD * 2, p.q + (long long)b * p.q_stride + (long long)g * p.G * kD, q_bytes,
+                     &full[s]);
         }
       }
     }
@@ -255,18 +263,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     const int npg = (L + p.page - 1) / p.page;
     const int pg0 = c * p.chunk_pages, pg1 = min(npg, pg0 + p.chunk_pages);
     const int tok_base = pg0 * p.page;  // first token of the chunk
-    // q of the GQA group -> smem (rows >= G zero), then B fragments in registers
-    for (int i = t; i < kGmax * (kD / 8); i += kConsumers) {
-      const int hh = i / (kD / 8), j = i % (kD / 8);
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (hh < p.G) v = *reinterpret_cast<const uint4*>(p.q + (long long)b * p.q_stride + (long long)(g * p.G + hh) * kD + j * 8);
-      *reinterpret_cast<uint4*>(qs + hh * kQPitch + j * 16) = v;
-    }
-    consumer_sync();
     uint32_t qb[kD / 16][2];
-#pragma unroll
-    for (int ks = 0; ks < kD / 16; ++ks)
-      ldsm_x2(su32(qs) + (lane & 7) * kQPitch + (2 * ks + ((lane >> 3) & 1)) * 16, qb[ks][0], qb[ks][1]);
 
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     float o[kD / 16][4];
@@ -276,6 +273,12 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     for (int pg = pg0; pg < pg1; ++pg, ++it) {
       const int s = it % slots;
       mbar_wait(&full[s], (uint32_t)(it / slots) & 1u);
+      if (pg == pg0) {  // q of the GQA group (prefetched with the unit's first page) -> B fragments
+        const uint32_t qsu = su32(qring + (size_t)s * kGmax * kD * 2);
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks)
+          ldsm_x2(qsu + (lane & 7) * (kD * 2) + (2 * ks + ((lane >> 3) & 1)) * 16, qb[ks][0], qb[ks][1]);
+      }
       const uint32_t kbase = su32(ring + (size_t)s * p.stage_bytes);
       const uint32_t vbase = kbase + page_bytes;
       for (int tl = 0; tl < tiles_per_page; ++tl) {
@@ -353,6 +356,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     }
     consumer_sync();
     const long long ubase = (((long long)b * p.Hkv + g) * p.max_chunks + c) * p.G;
+    const bool direct = npg <= p.chunk_pages;  // the request is one chunk: no combine needed
     for (int i = t; i < p.G * kD; i += kConsumers) {
       const int hh = i / kD, d = i % kD;
       float M = -INFINITY;
@@ -366,10 +370,15 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
         Ls += ww[kGmax * kD + kGmax + hh] * sc;
         Os += ww[hh * kD + d] * sc;
       }
-      p.part_o[(ubase + hh) * kD + d] = Os / Ls;
-      if (d == 0) p.part_lse[ubase + hh] = M + log2f(Ls);
+      if (direct) {
+        p.out[((long long)b * p.Hq + g * p.G + hh) * kD + d] = __float2bfloat16_rn(Os / Ls);
+      } else {
+        p.part_o[(ubase + hh) * kD + d] = Os / Ls;
+        if (d == 0) p.part_lse[ubase + hh] = M + log2f(Ls);
+      }
     }
     consumer_sync();
+    if (t == 0 && k == my_j) tstamp(p.trace, 2);  // first unit done
   }
   if (t == 0) tstamp(p.trace, 3);
 }
@@ -386,6 +395,10 @@ __global__ void combine_kernel(const Params p) {
   const int L = p.seq_lens[b];
   const int npg = (L + p.page - 1) / p.page;
   const int nch = (npg + p.chunk_pages - 1) / p.chunk_pages;
+  if (nch <= 1) {  // written directly by the split kernel
+    if (threadIdx.x == 0) tstamp(p.trace2, 3);
+    return;
+  }
   const long long base = (((long long)b * p.Hkv + g) * p.max_chunks) * p.G + hh;  // + c*G
   float M = -INFINITY;
   for (int c = 0; c < nch; ++c) M = fmaxf(M, p.part_lse[base + (long long)c * p.G]);
@@ -482,8 +495,8 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   p.stage_bytes = 2 * a->page_size * kD * 2;
   // SMEM: [1024 B barriers][ring: stages x (K page + V page)][q rows][merge scratch][pair prefix]
   const int scratch = kConsumerWarps * (kGmax * kD + 2 * kGmax) * 4;
-  const int fixed = 1024 + kGmax * kQPitch + scratch + a->B * max_chunks * 4;
-  int max_stages = std::min((kSmemBudget - fixed) / p.stage_bytes, kMaxStages);
+  const int fixed = 1024 + scratch + a->B * max_chunks * 4;
+  int max_stages = std::min((kSmemBudget - fixed) / (p.stage_bytes + kGmax * kD * 2), kMaxStages);
   if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_attention: page of %d B does not fit twice", p.stage_bytes / 2);
   int stages = c.stages > 0 ? std::min(c.stages, max_stages) : std::min(max_stages, 4);
   p.stages = std::max(2, stages);
@@ -508,7 +521,7 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   p.n_hbm = n_hbm;
   out->grid = n_host + n_hbm;
   p.off_q = 1024 + p.stages * p.stage_bytes;
-  p.off_scratch = p.off_q + kGmax * kQPitch;
+  p.off_scratch = p.off_q + p.stages * kGmax * kD * 2;
   p.off_pairs = p.off_scratch + scratch;
   out->smem = p.off_pairs + a->B * max_chunks * 4;
   if (out->smem > kSmemBudget) return fail(DAK_EUNSUPPORTED, "dak_attention: shared memory plan %d B too large", out->smem);
@@ -564,8 +577,10 @@ dak_status dak_attention(const dak_attention_args* args, dak_stream_t stream) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   pl.p.trace = trace_slot(DAK_KIND_ATTENTION, args->B, args->Hkv, pl.grid);
-  pl.p.trace2 = trace_slot(DAK_KIND_COMBINE, args->B, args->Hq, args->B * args->Hq);
+  const bool need_combine = pl.p.max_chunks > 1;
+  pl.p.trace2 = need_combine ? trace_slot(DAK_KIND_COMBINE, args->B, args->Hq, args->B * args->Hq) : nullptr;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::split_attention_kernel, pl.p));
+  if (!need_combine) return DAK_OK;
   cudaLaunchConfig_t c2{};
   c2.gridDim = dim3(args->B * args->Hq);
   c2.blockDim = dim3(attn::kD);

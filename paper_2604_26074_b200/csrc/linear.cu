@@ -57,6 +57,7 @@ struct __align__(64) Params {
   long long pf_bytes;
   int evict_first;  // stream weights with the L2 evict_first policy
   int wm, wk;       // MMA path: consumer warps along M x along K (wm * wk == kConsumerWarps)
+  int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
   const __nv_bfloat16* ln_w;
   const __nv_bfloat16* ln_b;
@@ -489,9 +490,28 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == slots) { s = 0; ph ^= 1u; }
     }
-    // deterministic cross-warp reduction over the WK warps sharing m-tiles (fixed wk order)
+    // deterministic cross-warp reduction over the WK warps sharing m-tiles (fixed wk order): either
+    // every k-warp stores its partial into its own slot and the epilogue sums slots 0..WK-1 (one
+    // barrier), or (large tiles) serial accumulation rounds in the same order
     const int g = lane >> 2, c2 = (lane & 3) * 2;
-    for (int round = 0; round < WK; ++round) {
+    if (p.red_slots > 1) {
+      float* slot = res + (size_t)wk * R * N;
+#pragma unroll
+      for (int mi = 0; mi < MTW; ++mi) {
+        const int mt = wm + WM * mi;
+        if (mt < MT) {
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const int r = mt * 16 + g + (c >> 1) * 8;
+              const int n = nt * 8 + c2 + (c & 1);
+              if (r < R && n < N) slot[(size_t)r * N + n] = acc[mi][nt][c];
+            }
+        }
+      }
+    }
+    for (int round = 0; round < (p.red_slots > 1 ? 0 : WK); ++round) {
       if (wk == round) {
 #pragma unroll
         for (int mi = 0; mi < MTW; ++mi) {
@@ -518,13 +538,29 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   // ================================ epilogue: bias, activation, residual, bf16 RNE store
   grid_dep_wait();  // residual / y may belong to the previous kernel
   const int RN = PATH == 1 ? NN : N;
+  // bias / residual of this thread's first two items are fetched before the reduction barrier
+  float pre_b[2] = {0.f, 0.f}, pre_r[2] = {0.f, 0.f};
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int q = t + e * kConsumers;
+    if (q < R * N) {
+      const int n = q / R, r = q - n * R;
+      const long long m = row0 + r;
+      if (p.bias) pre_b[e] = __bfloat162float(p.bias[m]);
+      if (p.residual) pre_r[e] = __bfloat162float(p.residual[(long long)n * p.ldy + m]);
+    }
+  }
+  const int nslots = PATH == 2 ? p.red_slots : 1;
+  if (nslots > 1) consumer_sync();
   for (int q = t; q < R * N; q += kConsumers) {
     const int n = q / R, r = q - n * R;
     float v = res[(size_t)r * RN + n];
+    for (int w = 1; w < nslots; ++w) v += res[(size_t)w * R * N + (size_t)r * N + n];
     const long long m = row0 + r;
-    if (p.bias) v += __bfloat162float(p.bias[m]);
+    const int e = (q - t) / kConsumers;
+    if (p.bias) v += e == 0 ? pre_b[0] : (e == 1 ? pre_b[1] : __bfloat162float(p.bias[m]));
     if (p.act == DAK_ACT_RELU) v = fmaxf(v, 0.f);
-    if (p.residual) v += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
+    if (p.residual) v += e == 0 ? pre_r[0] : (e == 1 ? pre_r[1] : __bfloat162float(p.residual[(long long)n * p.ldy + m]));
     const __nv_bfloat16 o = __float2bfloat16_rn(v);
     p.y[(long long)n * p.ldy + m] = o;
     res[(size_t)r * RN + n] = __bfloat162float(o);  // same thread read this slot: no hazard
@@ -724,7 +760,9 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (a->stats_out && !aligned16(a->stats_out)) return fail(DAK_EINVAL, "dak_linear: stats_out must be 16-byte aligned");
   p.stats_out = a->stats_out;
   const int W2 = (path == 1 && kc / 8 > 32) ? kc / 8 / 32 : 1;
-  const int res_bytes = (int)(ceil_div((long long)W2 * rmax * N * 4, 128) * 128);
+  // MMA path: one partial slot per k-warp when they fit in 48 KB (one barrier), else serial rounds
+  p.red_slots = (path == 2 && wk > 1 && (long long)wk * rmax * N * 4 <= 48 * 1024) ? wk : 1;
+  const int res_bytes = (int)(ceil_div((long long)std::max(W2, p.red_slots) * rmax * N * 4, 128) * 128);
   const int per_stage = p.w_stage_bytes + p.x_stage_bytes;
   // SMEM (from a 1024-aligned base; +1 KB for the alignment pad): [1 KB barriers + LN stats]
   // [stages x W span][stages x x box][LN weight, bias][fp32 results]
