@@ -5,14 +5,15 @@
 // Work is split flash-decoding style into units (request b, kv head g, chunk c of chunk_pages
 // pages). Each CTA reads exactly one tier: CTAs [0, n_host) take the units whose chunk
 // starts on a host page, the rest take HBM units, round-robin by the unit's rank within its tier.
-// A producer lane streams the unit's K and V pages into an SMEM ring with 1-D bulk copies
-// (cp.async.bulk, the TMA engine) completing on mbarriers, host stages capped by the congestion
-// window. Eight consumer warps compute on tensor cores (mma.sync m16n8k16 bf16->fp32):
+// Each unit is owned by ONE consumer warp, which walks its 16-token tiles in order; producer lane w
+// streams warp w's tiles (K and V rows of a page, 1-D bulk copies = TMA engine, completing on
+// mbarriers) into a private SMEM ring, host rings capped by the congestion window. The
+// warp computes on tensor cores (mma.sync m16n8k16 bf16->fp32):
 //   S^T[16 tokens x 8 heads] = K_tile . Q^T       (all q heads of the GQA group in one n8 tile)
 //   online softmax per head (exp2 domain), P^T fed back as the B operand via movmatrix.trans
-//   O^T[d x 8 heads]       += V_tile^T . P^T      (ldmatrix.trans on the swizzled V page)
-// Warps own 16-token tiles (tile t -> warp t mod 8); at the end of a unit their (m, l, O) are
-// merged in fixed warp order and the normalised partial (o, log2-sum-exp) goes to workspace.
+//   O^T[d x 8 heads]       += V_tile^T . P^T      (ldmatrix.trans on the swizzled V rows)
+// and writes the normalised output directly (single-chunk request) or the chunk partial
+// (o, log2-sum-exp) to workspace.
 // A combine kernel merges the chunk partials of each (b, q-head) in chunk order -> bf16 output.
 // Every reduction order is fixed by (seq_len, chunk_pages, page_size): outputs are independent
 // of which pages live on the host (bitwise r-invariance).
@@ -35,7 +36,6 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;
 constexpr int kMaxStages = 8;
-constexpr int kQPitch = kD * 2 + 16;  // bytes per q row in smem
 constexpr int kMaxPairs = 8192;       // (request, chunk) pairs scheduled per launch
 constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the kernel's static scan scratch
 constexpr uint32_t kHostBit = 0x80000000u;
@@ -56,7 +56,7 @@ struct Params {
   float* part_lse;   // [B][Hkv][max_chunks][G]   (log2 domain)
   int n_host, n_hbm, stages, window;
   int stage_bytes;   // K page + V page
-  int off_q, off_scratch, off_pairs;
+  int off_pairs;
   unsigned long long* trace;   // dak_trace_enable slots (nullable): split kernel, combine kernel
   unsigned long long* trace2;
 };
@@ -144,14 +144,18 @@ __device__ __forceinline__ int find_pair(const int* pref, int n_pairs, int rank)
   return lo;
 }
 
+// Work split: one consumer WARP owns a whole unit (request b, kv head g, chunk c) and walks its
+// 16-token tiles in order with the online softmax in registers -- no cross-warp merge, no CTA
+// barrier per unit. Unit k of a tier goes to CTA (k mod n) and warp ((k div n) mod 8), so short
+// contexts (few tiles per unit) put up to 8 units in flight per SM. Producer lane w feeds consumer
+// warp w through a private ring of p.stages slots; a slot is one tile of K and V (2 x 16 x 256 B,
+// contiguous rows of a DAK-PG page) plus, on a unit's first tile, the unit's q rows (G x 256 B).
 __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Params p) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kMaxStages;
-  int* s_count = reinterpret_cast<int*>(empty + kMaxStages);
-  unsigned char* ring = smem + 1024;
-  unsigned char* qring = smem + p.off_q;  // [stages][kGmax][kD] bf16: q of the unit starting in that stage
-  float* scratch = reinterpret_cast<float*>(smem + p.off_scratch);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);            // [8 warps][kMaxStages]
+  uint64_t* empty = full + kConsumerWarps * kMaxStages;           // [8 warps][kMaxStages]
+  int* s_count = reinterpret_cast<int*>(empty + kConsumerWarps * kMaxStages);
+  unsigned char* ring = smem + 2048;                              // [8 warps][stages][stage_bytes]
   int* pref = reinterpret_cast<int*>(smem + p.off_pairs);
 
   const int cta = blockIdx.x;
@@ -161,26 +165,22 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   const int slots = host ? p.window : p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
+  constexpr int kTileBytes = 16 * kD * 2;  // 16 token rows of K (or V)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
+    for (int s = 0; s < kConsumerWarps * kMaxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      mbar_init(&empty[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
   }
-  // q rows >= G of every slot stay zero (the bulk copies write rows < G only)
-  for (int i = threadIdx.x; i < p.stages * kGmax * kD / 8; i += kThreads)
-    reinterpret_cast<uint4*>(qring)[i] = make_uint4(0, 0, 0, 0);
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   grid_dep_launch();
   grid_dep_wait();  // block table, seq_lens and q come from earlier kernels
   if (threadIdx.x == 0) tstamp(p.trace, 1);
   // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
   const int n_pairs = p.B * p.max_chunks;
-  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
-  {
+  {  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
     __shared__ int warp_tot[kThreads / 32];
     int carry = 0;
     for (int base = 0; base < n_pairs; base += kThreads) {
@@ -195,7 +195,6 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
           f = ((e & kHostBit) != 0) == host;
         }
       }
-      // inclusive warp scan
       int v = f;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -216,171 +215,158 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     __syncthreads();
   }
   const int n_units = *s_count * p.Hkv;
+  const int stride = my_n * kConsumerWarps;  // units between consecutive units of one warp
 
   if (warp == 0) {
-    // ================================ producer
-    if (lane == 0) {
-      int it = 0;
-      for (int k = my_j; k < n_units; k += my_n) {
-        const int pr = find_pair(pref, n_pairs, k / p.Hkv);
-        const int g = k % p.Hkv;
-        const int b = pr / p.max_chunks, c = pr % p.max_chunks;
-        const int L = p.seq_lens[b];
-        const int npg = (L + p.page - 1) / p.page;
-        const int pg0 = c * p.chunk_pages, pg1 = min(npg, pg0 + p.chunk_pages);
-        for (int pg = pg0; pg < pg1; ++pg, ++it) {
-          const int s = it % slots;
-          if (it >= slots) mbar_wait(&empty[s], ((uint32_t)(it / slots) & 1u) ^ 1u);
-          const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + pg];
-          const long long idx = (long long)(e & ~kHostBit);
-          const bool eh = (e & kHostBit) != 0;
-          const long long off = (idx * p.Hkv + g) * (long long)page_bytes;
-          const uint32_t q_bytes = pg == pg0 ? (uint32_t)p.G * kD * 2 : 0u;  // q rides with the first page
-          mbar_expect_tx(&full[s], 2u * page_bytes + q_bytes);
-          unsigned char* dst = ring + (size_t)s * p.stage_bytes;
-          bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, page_bytes, &full[s]);
-          bulk_g2s(dst + page_bytes, (eh ? p.v_host : p.v_hbm) + off, page_bytes, &full[s]);
-          if (q_bytes)
-            bulk_g2s(qring + (size_t)s * kGmax * kD * 2, p.q + (long long)b * p.q_stride + (long long)g * p.G * kD, q_bytes,
-                     &full[s]);
-        }
+    // ================================ producer: lane w feeds consumer warp w
+    if (lane >= kConsumerWarps) return;
+    const int w = lane;
+    uint64_t* wf = full + w * kMaxStages;
+    uint64_t* we = empty + w * kMaxStages;
+    unsigned char* wr = ring + (size_t)w * p.stages * p.stage_bytes;
+    int it = 0;
+    for (int k = my_j + w * my_n; k < n_units; k += stride) {
+      const int pr = find_pair(pref, n_pairs, k / p.Hkv);
+      const int g = k % p.Hkv;
+      const int b = pr / p.max_chunks, c = pr % p.max_chunks;
+      const int L = p.seq_lens[b];
+      const int t0 = c * p.chunk_pages * p.page;
+      const int t1 = min(L, t0 + p.chunk_pages * p.page);
+      for (int tok = t0; tok < t1; tok += 16, ++it) {
+        const int s = it % slots;
+        if (it >= slots) mbar_wait(&we[s], ((uint32_t)(it / slots) & 1u) ^ 1u);
+        const int pg = tok / p.page, r0 = tok % p.page;
+        const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + pg];
+        const long long idx = (long long)(e & ~kHostBit);
+        const bool eh = (e & kHostBit) != 0;
+        const long long off = (idx * p.Hkv + g) * (long long)page_bytes + (long long)r0 * kD * 2;
+        const uint32_t q_bytes = tok == t0 ? (uint32_t)p.G * kD * 2 : 0u;
+        mbar_expect_tx(&wf[s], 2u * kTileBytes + q_bytes);
+        unsigned char* dst = wr + (size_t)s * p.stage_bytes;
+        bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, kTileBytes, &wf[s]);
+        bulk_g2s(dst + kTileBytes, (eh ? p.v_host : p.v_hbm) + off, kTileBytes, &wf[s]);
+        if (q_bytes)
+          bulk_g2s(dst + 2 * kTileBytes, p.q + (long long)b * p.q_stride + (long long)g * p.G * kD, q_bytes, &wf[s]);
       }
     }
     return;
   }
 
-  // ================================ consumers
+  // ================================ consumers: warp cw owns its units end to end
   const int cw = warp - 1;
-  const int t = threadIdx.x - 32;
   const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column pair
-  const int tiles_per_page = p.page / 16;
+  uint64_t* wf = full + cw * kMaxStages;
+  uint64_t* we = empty + cw * kMaxStages;
+  unsigned char* wr = ring + (size_t)cw * p.stages * p.stage_bytes;
   int it = 0;
-  for (int k = my_j; k < n_units; k += my_n) {
+  bool first_unit = true;
+  for (int k = my_j + cw * my_n; k < n_units; k += stride) {
     const int pr = find_pair(pref, n_pairs, k / p.Hkv);
     const int g = k % p.Hkv;
     const int b = pr / p.max_chunks, c = pr % p.max_chunks;
     const int L = p.seq_lens[b];
     const int npg = (L + p.page - 1) / p.page;
-    const int pg0 = c * p.chunk_pages, pg1 = min(npg, pg0 + p.chunk_pages);
-    const int tok_base = pg0 * p.page;  // first token of the chunk
+    const int t0 = c * p.chunk_pages * p.page;
+    const int t1 = min(L, t0 + p.chunk_pages * p.page);
     uint32_t qb[kD / 16][2];
-
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     float o[kD / 16][4];
 #pragma unroll
     for (int i = 0; i < kD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
-    for (int pg = pg0; pg < pg1; ++pg, ++it) {
+    for (int tok0 = t0; tok0 < t1; tok0 += 16, ++it) {
       const int s = it % slots;
-      mbar_wait(&full[s], (uint32_t)(it / slots) & 1u);
-      if (pg == pg0) {  // q of the GQA group (prefetched with the unit's first page) -> B fragments
-        const uint32_t qsu = su32(qring + (size_t)s * kGmax * kD * 2);
+      mbar_wait(&wf[s], (uint32_t)(it / slots) & 1u);
+      const uint32_t kbase = su32(wr + (size_t)s * p.stage_bytes);
+      const uint32_t vbase = kbase + kTileBytes;
+      if (tok0 == t0) {  // q of the GQA group rides with the unit's first tile (rows >= G unused)
 #pragma unroll
         for (int ks = 0; ks < kD / 16; ++ks)
-          ldsm_x2(qsu + (lane & 7) * (kD * 2) + (2 * ks + ((lane >> 3) & 1)) * 16, qb[ks][0], qb[ks][1]);
+          ldsm_x2(kbase + 2 * kTileBytes + (lane & 7) * (kD * 2) + (2 * ks + ((lane >> 3) & 1)) * 16, qb[ks][0], qb[ks][1]);
       }
-      const uint32_t kbase = su32(ring + (size_t)s * p.stage_bytes);
-      const uint32_t vbase = kbase + page_bytes;
-      for (int tl = 0; tl < tiles_per_page; ++tl) {
-        const int tile = (pg - pg0) * tiles_per_page + tl;
-        if ((tile & (kConsumerWarps - 1)) != cw) continue;
-        const int tok0 = tok_base + tile * 16;  // chunk-relative -> absolute token index
-        if (tok0 >= L) continue;
-        const int r0 = tl * 16;                 // row inside the page
-        // ---- S^T = K . Q^T   [16 tokens x 8 heads]
-        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      // ---- S^T = K . Q^T   [16 tokens x 8 heads]
+      float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks) {
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4(kbase + pg_off(r0 + (lane & 15), 2 * ks + (lane >> 4)), a0, a1, a2, a3);
-          mma_bf16(sc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-        }
-        // ---- scale, mask, online softmax (exp2 domain), per head column
-        const bool v0 = tok0 + gq < L, v1 = tok0 + gq + 8 < L;
-        float s0 = v0 ? sc[0] * p.scale_log2 : -INFINITY;
-        float s1 = v0 ? sc[1] * p.scale_log2 : -INFINITY;
-        float s2 = v1 ? sc[2] * p.scale_log2 : -INFINITY;
-        float s3 = v1 ? sc[3] * p.scale_log2 : -INFINITY;
-        float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+      for (int ks = 0; ks < kD / 16; ++ks) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4(kbase + pg_off(lane & 15, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+        mma_bf16(sc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+      }
+      // ---- scale, mask, online softmax (exp2 domain), per head column
+      const bool v0 = tok0 + gq < t1, v1 = tok0 + gq + 8 < t1;
+      const float s0 = v0 ? sc[0] * p.scale_log2 : -INFINITY;
+      const float s1 = v0 ? sc[1] * p.scale_log2 : -INFINITY;
+      const float s2 = v1 ? sc[2] * p.scale_log2 : -INFINITY;
+      const float s3 = v1 ? sc[3] * p.scale_log2 : -INFINITY;
+      float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-        }
-        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: tile has a valid token
-        const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
-        m[0] = mn0;
-        m[1] = mn1;
-        const float p0 = exp2f(s0 - mn0), p1 = exp2f(s1 - mn1), p2 = exp2f(s2 - mn0), p3 = exp2f(s3 - mn1);
-        l[0] = l[0] * al0 + (p0 + p2);
-        l[1] = l[1] * al1 + (p1 + p3);
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: tile has a valid token
+      const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
+      m[0] = mn0;
+      m[1] = mn1;
+      const float p0 = exp2f(s0 - mn0), p1 = exp2f(s1 - mn1), p2 = exp2f(s2 - mn0), p3 = exp2f(s3 - mn1);
+      l[0] = l[0] * al0 + (p0 + p2);
+      l[1] = l[1] * al1 + (p1 + p3);
 #pragma unroll
-        for (int i = 0; i < kD / 16; ++i) {
-          o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
-        }
-        // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
-        const uint32_t b0 = movm_t(pack_bf16(p0, p1));
-        const uint32_t b1 = movm_t(pack_bf16(p2, p3));
-        // ---- O^T[d x heads] += V^T . P^T
+      for (int i = 0; i < kD / 16; ++i) {
+        o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
+      }
+      // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
+      const uint32_t b0 = movm_t(pack_bf16(p0, p1));
+      const uint32_t b1 = movm_t(pack_bf16(p2, p3));
+      // ---- O^T[d x heads] += V^T . P^T
 #pragma unroll
-        for (int i = 0; i < kD / 16; ++i) {
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4_t(vbase + pg_off(r0 + (lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
-          mma_bf16(o[i], a0, a1, a2, a3, b0, b1);
-        }
+      for (int i = 0; i < kD / 16; ++i) {
+        uint32_t a0, a1, a2, a3;
+        ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
+        mma_bf16(o[i], a0, a1, a2, a3, b0, b1);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&we[s]);
     }
-    // ---- warp partials -> scratch [warp][head][d] (+ m, l), then fixed-order merge
+    // ---- l per head column: sum over the 8 lane groups holding the column
 #pragma unroll
     for (int off = 4; off < 32; off <<= 1) {
       l[0] += __shfl_xor_sync(0xffffffffu, l[0], off);
       l[1] += __shfl_xor_sync(0xffffffffu, l[1], off);
     }
-    float* so = scratch + cw * (kGmax * kD + 2 * kGmax);
-    float* sm = so + kGmax * kD;
-#pragma unroll
-    for (int i = 0; i < kD / 16; ++i) {
-      const int d0 = 16 * i + gq;
-      so[(2 * cq) * kD + d0] = o[i][0];
-      so[(2 * cq + 1) * kD + d0] = o[i][1];
-      so[(2 * cq) * kD + d0 + 8] = o[i][2];
-      so[(2 * cq + 1) * kD + d0 + 8] = o[i][3];
-    }
-    if (gq == 0) {
-      sm[2 * cq] = m[0];
-      sm[2 * cq + 1] = m[1];
-      sm[kGmax + 2 * cq] = l[0];
-      sm[kGmax + 2 * cq + 1] = l[1];
-    }
-    consumer_sync();
-    const long long ubase = (((long long)b * p.Hkv + g) * p.max_chunks + c) * p.G;
+    // lane holds O^T[d][head] for d = 16 i + gq (+8), head = 2 cq (+1)
     const bool direct = npg <= p.chunk_pages;  // the request is one chunk: no combine needed
-    for (int i = t; i < p.G * kD; i += kConsumers) {
-      const int hh = i / kD, d = i % kD;
-      float M = -INFINITY;
-      for (int w = 0; w < kConsumerWarps; ++w) M = fmaxf(M, scratch[w * (kGmax * kD + 2 * kGmax) + kGmax * kD + hh]);
-      float Ls = 0.f, Os = 0.f;
-      for (int w = 0; w < kConsumerWarps; ++w) {
-        const float* ww = scratch + w * (kGmax * kD + 2 * kGmax);
-        const float mw = ww[kGmax * kD + hh];
-        if (mw == -INFINITY) continue;  // warp saw no valid token
-        const float sc = exp2f(mw - M);
-        Ls += ww[kGmax * kD + kGmax + hh] * sc;
-        Os += ww[hh * kD + d] * sc;
-      }
-      if (direct) {
-        p.out[((long long)b * p.Hq + g * p.G + hh) * kD + d] = __float2bfloat16_rn(Os / Ls);
-      } else {
-        p.part_o[(ubase + hh) * kD + d] = Os / Ls;
-        if (d == 0) p.part_lse[ubase + hh] = M + log2f(Ls);
+    const long long ubase = (((long long)b * p.Hkv + g) * p.max_chunks + c) * p.G;
+#pragma unroll
+    for (int hc = 0; hc < 2; ++hc) {
+      const int hh = 2 * cq + hc;
+      if (hh < p.G) {
+        const float inv = 1.f / l[hc];
+        if (direct) {
+          __nv_bfloat16* dst = p.out + ((long long)b * p.Hq + g * p.G + hh) * kD;
+#pragma unroll
+          for (int i = 0; i < kD / 16; ++i) {
+            dst[16 * i + gq] = __float2bfloat16_rn(o[i][hc] * inv);
+            dst[16 * i + gq + 8] = __float2bfloat16_rn(o[i][2 + hc] * inv);
+          }
+        } else {
+          float* dst = p.part_o + (ubase + hh) * kD;
+#pragma unroll
+          for (int i = 0; i < kD / 16; ++i) {
+            dst[16 * i + gq] = o[i][hc] * inv;
+            dst[16 * i + gq + 8] = o[i][2 + hc] * inv;
+          }
+          if (gq == 0) p.part_lse[ubase + hh] = m[hc] + log2f(l[hc]);
+        }
       }
     }
-    consumer_sync();
-    if (t == 0 && k == my_j) tstamp(p.trace, 2);  // first unit done
+    if (first_unit && lane == 0 && cw == 0) tstamp(p.trace, 2);  // first unit of warp 0 done
+    first_unit = false;
   }
-  if (t == 0) tstamp(p.trace, 3);
+  if (p.trace) {
+    consumer_sync();
+    if (lane == 0 && cw == 0) tstamp(p.trace, 3);
+  }
 }
 
 // merge chunk partials: out[b, h, :] = sum_c w_c o_c, w_c = 2^(lse_c - LSE)   (fixed chunk order)
@@ -492,13 +478,12 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   out->ws_o = n_units * G * kD * sizeof(float);
   out->ws_lse = n_units * G * sizeof(float);
   const dak_launch_cfg& c = a->cfg;
-  p.stage_bytes = 2 * a->page_size * kD * 2;
-  // SMEM: [1024 B barriers][ring: stages x (K page + V page)][q rows][merge scratch][pair prefix]
-  const int scratch = kConsumerWarps * (kGmax * kD + 2 * kGmax) * 4;
-  const int fixed = 1024 + scratch + a->B * max_chunks * 4;
-  int max_stages = std::min((kSmemBudget - fixed) / (p.stage_bytes + kGmax * kD * 2), kMaxStages);
-  if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_attention: page of %d B does not fit twice", p.stage_bytes / 2);
-  int stages = c.stages > 0 ? std::min(c.stages, max_stages) : std::min(max_stages, 4);
+  // per consumer warp: a ring of tile stages [K 16 rows][V 16 rows][q G rows (first tile of a unit)]
+  p.stage_bytes = 2 * 16 * kD * 2 + G * kD * 2;
+  const int fixed = 2048 + a->B * max_chunks * 4 + 8 * kD * 2;  // + slack: q ldmatrix reads 8 rows
+  int max_stages = std::min((kSmemBudget - fixed) / (kConsumerWarps * p.stage_bytes), kMaxStages);
+  if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_attention: tile ring does not fit");
+  int stages = c.stages > 0 ? std::min(c.stages, max_stages) : max_stages;
   p.stages = std::max(2, stages);
   // host CTAs: one CTA keeps ~the link's saturating in-flight volume (calibration); window caps it
   int n_host = c.n_cta_host > 0 ? c.n_cta_host : 1;
@@ -506,7 +491,7 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   int window = p.stages;
   if (c.window > 0) window = std::min(c.window, p.stages);
   else if (c.congestion_control)
-    window = std::max(1, std::min(p.stages, (int)cdiv(192 * 1024, (long long)p.stage_bytes * std::max(1, n_host))));
+    window = std::max(1, std::min(p.stages, (int)cdiv(192 * 1024, (long long)p.stage_bytes * kConsumerWarps * std::max(1, n_host))));
   p.window = window;
   int n_hbm = c.n_cta_hbm;
   if (n_hbm <= 0) {
@@ -520,9 +505,7 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   p.n_host = n_host;
   p.n_hbm = n_hbm;
   out->grid = n_host + n_hbm;
-  p.off_q = 1024 + p.stages * p.stage_bytes;
-  p.off_scratch = p.off_q + p.stages * kGmax * kD * 2;
-  p.off_pairs = p.off_scratch + scratch;
+  p.off_pairs = 2048 + kConsumerWarps * p.stages * p.stage_bytes + 8 * kD * 2;
   out->smem = p.off_pairs + a->B * max_chunks * 4;
   if (out->smem > kSmemBudget) return fail(DAK_EUNSUPPORTED, "dak_attention: shared memory plan %d B too large", out->smem);
   if (need_ptrs) {

@@ -417,19 +417,40 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       grid_dep_wait();
       float* s_ln = reinterpret_cast<float*>(smem + 256);
       for (int n = cw; n < N; n += kConsumerWarps) {
+        // batches of 8 independent loads per lane (one L2 round trip per 256 parts); the values
+        // stay in registers for the second pass when parts <= 256 (the usual case: one per CTA)
         float c = 0.f, cm = 0.f;
-        for (int j = lane; j < p.ln_parts; j += 32) {
-          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
-          c += v.x;
-          cm += v.x * v.y;
+        float4 v[8];
+        for (int j0 = 0; j0 < p.ln_parts; j0 += 256) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int j = j0 + u * 32 + lane;
+            v[u] = j < p.ln_parts ? *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            c += v[u].x;
+            cm += v[u].x * v[u].y;
+          }
         }
         c = warp_sum(c);
         const float mean = warp_sum(cm) / c;
         float m2 = 0.f;
-        for (int j = lane; j < p.ln_parts; j += 32) {
-          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
-          const float d = v.y - mean;
-          m2 += v.z + v.x * d * d;
+        for (int j0 = 0; j0 < p.ln_parts; j0 += 256) {
+          if (p.ln_parts > 256) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              const int j = j0 + u * 32 + lane;
+              v[u] = j < p.ln_parts ? *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4)
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const float d = v[u].y - mean;
+            m2 += v[u].z + v[u].x * d * d;
+          }
         }
         m2 = warp_sum(m2);
         if (lane == 0) {

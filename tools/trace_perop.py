@@ -82,6 +82,33 @@ def main():
     for k, (c, inc, dur, after_dep) in agg.items():
         print(json.dumps(dict(kind=k, count=c, total_inc_us=round(inc, 1), mean_inc_us=round(inc / c, 2),
                               mean_span_us=round(dur / c, 2), mean_after_dep_us=round(after_dep / c, 2))))
+    # attention per-CTA phases: dep -> first unit done, then time per further unit
+    for i, m in enumerate(meta):
+        if m["kind"] != "attention":
+            continue
+        st = T[i, :m["grid"]]
+        ok = (st[:, 0] > 0) & (st[:, 2] > 0)
+        first = (st[ok, 2] - st[ok, 1]) / 1e3
+        rest = (st[ok, 3] - st[ok, 2]) / 1e3
+        print(json.dumps(dict(attention_launch=i, ctas_with_units=int(ok.sum()),
+                              dep_to_first_unit_us=[round(float(np.percentile(first, q)), 2) for q in (0, 50, 100)],
+                              after_first_unit_us=[round(float(np.percentile(rest, q)), 2) for q in (0, 50, 100)],
+                              start_to_dep_us=[round(float(np.percentile((st[ok, 1] - st[ok, 0]) / 1e3, q)), 2)
+                                               for q in (0, 50, 100)])))
+        break
+    # linear: host vs HBM CTA completion
+    for i, m in enumerate(meta):
+        if m["kind"] != "linear":
+            continue
+        st = T[i, :m["grid"]]
+        e = st[:, 3]
+        print(json.dumps(dict(linear_launch=i, M=m["a"], end_spread_us=round(float((e.max() - np.median(e)) / 1e3), 2),
+                              first2_end_minus_median_us=round(float((e[:2].max() - np.median(e)) / 1e3), 2),
+                              start_spread_us=round(float((st[:, 0].max() - st[:, 0].min()) / 1e3), 2),
+                              dep_to_first_stage_med_us=round(float(np.median(st[:, 2] - st[:, 1]) / 1e3), 2),
+                              first_stage_to_end_med_us=round(float(np.median(st[:, 3] - st[:, 2]) / 1e3), 2))))
+        if i > 20:
+            break
     mid = len(rows) // 2
     for r in rows[mid - 6: mid + 8]:
         print(" ".join(f"{k}={v:.2f}" if isinstance(v, float) else f"{k}={v}" for k, v in r.items()))
