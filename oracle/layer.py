@@ -18,7 +18,7 @@ import math
 
 import numpy as np
 
-from .kernels import bf16_to_f64, layernorm
+from .kernels import bf16_to_f64, layernorm, rmsnorm
 
 
 def opt_decode_layer(x, p: dict, K_prev: list, V_prev: list, n_heads: int, eps: float = 1e-5):
@@ -57,3 +57,92 @@ def opt_decode_step(tokens, positions, params: dict, K_cache: list, V_cache: lis
         x, _, _ = opt_decode_layer(x, lp, K_cache[l], V_cache[l], n_heads, eps)
     h = layernorm(x, bf16_to_f64(params["lnf_w"]), bf16_to_f64(params["lnf_b"]), eps)
     return h @ E.T, x
+
+
+# ------------------------------------------------------------------------------------------------
+# Llama family (BASELINE.json configs[2]: Llama-3-70B, TP8 over 8 B200). Pre-RMSNorm, no biases,
+# rotary positions (rotate-half convention, theta 500000 for Llama 3), GQA attention, SwiGLU MLP,
+# untied LM head. The split operators replace nn.Linear / SDPA as in the paper.
+
+def rope(x, pos: int, theta: float):
+    """Rotary embedding of x [..., d] at position pos: (x1, x2) -> (x1 c - x2 s, x2 c + x1 s) with
+    angle pos / theta^(2i/d), i < d/2 (Llama's rotate_half layout)."""
+    x = np.asarray(x, dtype=np.float64)
+    d = x.shape[-1]
+    half = d // 2
+    ang = pos * theta ** (-2.0 * np.arange(half) / d)
+    c, s = np.cos(ang), np.sin(ang)
+    x1, x2 = x[..., :half], x[..., half:]
+    return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
+
+
+def silu(x):
+    return x / (1.0 + np.exp(-x))
+
+
+def llama_decode_layer(x, p: dict, K_prev: list, V_prev: list, positions, n_heads: int, n_kv: int,
+                       theta: float = 500000.0, eps: float = 1e-5, shard=None):
+    """One Llama layer for the new token of every request. x: float64 [B, H]; p: bf16-bit params
+    (q [Hq d, H], k, v [Hkv d, H], o [H, Hq d], gate, up [F, H], down [H, F], ln1_w, ln2_w);
+    K_prev/V_prev: per-request [L_b, Hkv, d] bits of the cached (already rotated) keys / values.
+    shard=(rank, world): compute only tensor-parallel rank `rank`'s heads / FFN rows (Megatron
+    column split of q/k/v/gate/up, row split of o/down) and return its PARTIAL o / down outputs
+    (without the residual), which the caller sums over ranks (the all-reduce). Returns
+    (x_out or (attn_partial, mlp_fn), k_new_roped, v_new)."""
+    f = {k: bf16_to_f64(v) for k, v in p.items()}
+    B, H = x.shape
+    d = f["q"].shape[0] // n_heads
+    G = n_heads // n_kv
+    h = rmsnorm(x, f["ln1_w"], eps)
+    q = (h @ f["q"].T).reshape(B, n_heads, d)
+    k = (h @ f["k"].T).reshape(B, n_kv, d)
+    v = (h @ f["v"].T).reshape(B, n_kv, d)
+    for b in range(B):
+        q[b] = rope(q[b], int(positions[b]), theta)
+        k[b] = rope(k[b], int(positions[b]), theta)
+    heads = range(n_heads) if shard is None else range(shard[0] * n_heads // shard[1], (shard[0] + 1) * n_heads // shard[1])
+    a = np.zeros((B, n_heads * d))
+    for b in range(B):
+        K = np.concatenate([bf16_to_f64(K_prev[b]), k[b:b + 1]], axis=0)  # [L+1, Hkv, d]
+        V = np.concatenate([bf16_to_f64(V_prev[b]), v[b:b + 1]], axis=0)
+        for hh in heads:
+            g = hh // G
+            s = K[:, g] @ q[b, hh] / math.sqrt(d)
+            w = np.exp(s - s.max())
+            a[b, hh * d:(hh + 1) * d] = (w / w.sum()) @ V[:, g]
+
+    def mlp(xx, part=None):
+        hm = rmsnorm(xx, f["ln2_w"], eps)
+        F = f["gate"].shape[0]
+        rows = slice(None) if part is None else slice(part[0] * F // part[1], (part[0] + 1) * F // part[1])
+        act = silu(hm @ f["gate"][rows].T) * (hm @ f["up"][rows].T)
+        return act @ f["down"][:, rows].T
+
+    if shard is not None:
+        cols = slice(heads.start * d, heads.stop * d)
+        return (a[:, cols] @ f["o"][:, cols].T, lambda xx: mlp(xx, shard)), k, v
+    x = x + a @ f["o"].T
+    x = x + mlp(x)
+    return x, k, v
+
+
+def llama_decode_layer_tp(x, p: dict, K_prev: list, V_prev: list, positions, n_heads: int, n_kv: int, world: int,
+                          theta: float = 500000.0, eps: float = 1e-5):
+    """The same layer computed as `world` tensor-parallel shards whose o / down partials are summed
+    in rank order (the all-reduce) before each residual add."""
+    parts = [llama_decode_layer(x, p, K_prev, V_prev, positions, n_heads, n_kv, theta, eps, shard=(r, world))
+             for r in range(world)]
+    x = x + sum(pt[0][0] for pt in parts)
+    x = x + sum(pt[0][1](x) for pt in parts)
+    return x, parts[0][1], parts[0][2]
+
+
+def llama_decode_step(tokens, positions, params: dict, K_cache: list, V_cache: list, n_heads: int, n_kv: int,
+                      theta: float = 500000.0, eps: float = 1e-5):
+    """Embedding -> layers -> final RMSNorm -> LM head (untied). Returns (logits, x) float64."""
+    x = bf16_to_f64(params["embed"])[np.asarray(tokens)]
+    for l in range(len(K_cache)):
+        lp = {k.split(".", 1)[1]: v for k, v in params.items() if k.startswith(f"L{l}.")}
+        x, _, _ = llama_decode_layer(x, lp, K_cache[l], V_cache[l], positions, n_heads, n_kv, theta, eps)
+    h = rmsnorm(x, bf16_to_f64(params["lnf_w"]), eps)
+    return h @ bf16_to_f64(params["lm_head"]).T, x
