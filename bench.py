@@ -16,6 +16,7 @@ Under torchrun every rank runs an independent replica (weak scaling, no data-pat
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
 import statistics
@@ -192,7 +193,8 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--context", type=int, default=64)
     ap.add_argument("--no-pdl", action="store_true")
-    ap.add_argument("--per-op", action="store_true", help="per-op kernels (dak_layer) instead of the persistent step")
+    ap.add_argument("--persistent", action="store_true",
+                    help="one persistent launch per step (dak_step) instead of the per-op kernels (dak_layer)")
     ap.add_argument("--no-cc", action="store_true")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -222,7 +224,7 @@ def main():
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
                  evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
-    if not a.per_op:
+    if a.persistent:
         eng.enable_persistent_step()
     nb = eng.bytes_per_step()
     stream = torch.cuda.Stream()
@@ -293,8 +295,16 @@ def main():
     lin_achieved = lin_bytes / lin_time / 1e9
     lin_share = lin_time / step_s
     peak = hbm_gbs + link_gbs
+    # traffic: DRAM read+write bytes per dak_linear launch of one step from the committed ncu
+    # capture (tools/profile_round.sh -> tools/summarize_profiles.py); algorithmic bytes alongside
+    traffic = None
+    tr_files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "linear_traffic.json")))
+    if tr_files:
+        traffic = json.load(open(tr_files[-1]))["dram_bytes_per_launch"]
     roofline = dict(bound="hbm", achieved=round(lin_achieved, 1), peak=round(peak, 1), unit="GB/s",
-                    frac=round(lin_achieved / peak, 4), traffic=None,
+                    frac=round(lin_achieved / peak, 4), traffic=traffic,
+                    algorithmic_bytes_per_launch=round(lin_bytes / len(ops)),
+                    traffic_source=os.path.relpath(tr_files[-1], ROOT) if tr_files else None,
                     kernel="dak_linear (split GEMV/skinny GEMM, all %d launches of a step, per-launch events, no PDL)" % len(ops),
                     peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json) + measured host link %.1f GB/s" % (peak_src, hbm_gbs, link_gbs),
                     step_frac=round(value / world / peak, 4),
@@ -310,7 +320,7 @@ def main():
                             host_ratio=round(nb["host"] / nb["total"], 5),
                             l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
-                            execution="per-op kernels (dak_layer)" if a.per_op else "persistent step (dak_step, 1 launch)",
+                            execution="persistent step (dak_step, 1 launch)" if a.persistent else "per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
                 gpu_launches=eng.kernels_per_step() * a.steps)

@@ -21,7 +21,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = [
     ("abi.cpp", []),
     ("planner.cpp", ["-Xcompiler", "-ffp-contract=off", "-fmad=false"]),
-    ("linear.cu", []),
+    ("linear.cu", ["-DDAK_LINEAR_PART=0"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=1"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=2"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=3"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=4"]),
     ("attention.cu", []),
     ("layer.cu", []),
     ("step.cu", []),
@@ -37,21 +41,23 @@ def _run(cmd):
 
 
 def build(verbose: bool = False) -> str:
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(OBJ, exist_ok=True)
-    objs = []
+    objs, jobs = [], []
     for src, extra in SOURCES:
         path = os.path.join(CSRC, src)
-        obj = os.path.join(OBJ, src + ".o")
-        deps = [path, os.path.join(CSRC, "common.h"), os.path.join(ROOT, "include", "dak.h")]
-        if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps):
+        tag = "".join(e.split("=")[-1] for e in extra if e.startswith("-DDAK_LINEAR_PART"))
+        obj = os.path.join(OBJ, src + tag + ".o")
+        deps = [path, os.path.join(CSRC, "common.h"), os.path.join(CSRC, "ptx.cuh"), os.path.join(ROOT, "include", "dak.h")]
+        if not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(d) for d in deps if os.path.exists(d)):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
                    "-Xptxas", "-v" if verbose else "-O3", *extra, "-c", path, "-o", obj]
-            if src.endswith(".cpp"):
-                cmd = [NVCC, "-x", "cu", *cmd[1:]] if False else cmd
-            out = _run(cmd)
+            jobs.append(cmd)
+        objs.append(obj)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
+        for out in ex.map(_run, jobs):
             if verbose:
                 sys.stderr.write(out)
-        objs.append(obj)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
         _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"])
     return OUT

@@ -25,15 +25,19 @@
 
 #include "common.h"
 
+#ifndef DAK_LINEAR_PART
+#define DAK_LINEAR_PART 0
+#endif
+
 namespace dak {
 namespace lin {
 
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
-constexpr int kMaxN = 16;
+constexpr int kMaxN = 64;
 constexpr int kRptMax = 16;   // FMA path: rows per thread
-constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp
+constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
 constexpr int kMaxStages = 8;
 constexpr int kSmemBudget = 227 * 1024;
 
@@ -58,6 +62,7 @@ struct __align__(64) Params {
   int evict_first;  // stream weights with the L2 evict_first policy
   int wm, wk;       // MMA path: consumer warps along M x along K (wm * wk == kConsumerWarps)
   int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
+  int swiglu;       // x = [gate | up] ([N, 2K]); the operand is silu(gate) * up
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
   const __nv_bfloat16* ln_w;
   const __nv_bfloat16* ln_b;
@@ -186,7 +191,15 @@ __device__ __forceinline__ uint32_t ln_pair(uint32_t xv, uint32_t wv, uint32_t b
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int PATH, int NN, int MTW, bool LN>
+__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+// SwiGLU pair: silu(gate) * up, rounded to bf16
+__device__ __forceinline__ uint32_t swiglu_pair(uint32_t gv, uint32_t uv) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(silu_f(bf_lo(gv)) * bf_lo(uv), silu_f(bf_hi(gv)) * bf_hi(uv));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// XF (operand transform): 0 none, 1 fused pre-norm (LN / RMSNorm), 2 SwiGLU of [gate | up]
+template <int PATH, int NN, int MTW, int XF>
 __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 128B-swizzled TMA destinations need 1024-byte alignment: align the base by hand
@@ -258,13 +271,15 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       else bulk_g2s(dst, s_, w_bytes, &full[slot]);
     };
     auto load_x = [&](int slot, int i) {
-      tma_3d(xring + (size_t)slot * p.x_stage_bytes, xmap, 0, 0, i * (kc >> 6), &full[slot]);
+      unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
+      tma_3d(dst, xmap, 0, 0, i * (kc >> 6), &full[slot]);
+      if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K + (long long)i * kc) >> 6), &full[slot]);
     };
     for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
       mbar_expect_tx(&full[i], w_bytes + x_tx);
       load_w(i, i);
     }
-    if (LN) {  // LN weight / bias are parameters too: resident for the whole kernel
+    if (XF == 1) {  // LN weight / bias are parameters too: resident for the whole kernel
       const uint32_t kb = (uint32_t)p.K * 2;
       mbar_expect_tx(lnbar, p.ln_b ? 2 * kb : kb);
       bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
@@ -413,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
     // lane-strided then butterfly sums: fixed order, one warp per row n
     float mu[NT], rs[NT];
     const unsigned char* lnres = smem + p.off_ln;
-    if constexpr (LN) {
+    if constexpr (XF == 1) {
       grid_dep_wait();
       float* s_ln = reinterpret_cast<float*>(smem + 256);
       for (int n = cw; n < N; n += kConsumerWarps) {
@@ -483,9 +498,27 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         if constexpr (NT == 1) {
           ldsm_x2(baddr, b[0][0], b[0][1]);
         } else {
-          ldsm_x4(baddr, b[0][0], b[0][1], b[1][0], b[1][1]);
+#pragma unroll
+          for (int j2 = 0; j2 < NT / 2; ++j2)  // 16 x rows per ldmatrix.x4 (+2 KB per 16 rows)
+            ldsm_x4(baddr + j2 * 2048, b[2 * j2][0], b[2 * j2][1], b[2 * j2 + 1][0], b[2 * j2 + 1][1]);
         }
-        if constexpr (LN) {  // B fragment (n = lane/4 [+8], k = 16ks + 2(lane%4) [+8]) -> LN(x)
+        if constexpr (XF == 2) {  // gate box first, up box at + x_stage_bytes / 2: silu(g) * u
+          const uint32_t uaddr = baddr + (uint32_t)(p.x_stage_bytes >> 1);
+          uint32_t u[NT][2];
+          if constexpr (NT == 1) {
+            ldsm_x2(uaddr, u[0][0], u[0][1]);
+          } else {
+#pragma unroll
+            for (int j2 = 0; j2 < NT / 2; ++j2)
+              ldsm_x4(uaddr + j2 * 2048, u[2 * j2][0], u[2 * j2][1], u[2 * j2 + 1][0], u[2 * j2 + 1][1]);
+          }
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            b[nt][0] = swiglu_pair(b[nt][0], u[nt][0]);
+            b[nt][1] = swiglu_pair(b[nt][1], u[nt][1]);
+          }
+        }
+        if constexpr (XF == 1) {  // B fragment (n = lane/4 [+8], k = 16ks + 2(lane%4) [+8]) -> LN(x)
           const int kk = i * kc + ks * 16 + 2 * (lane & 3);
           const uint32_t w0 = *reinterpret_cast<const uint32_t*>(lnres + kk * 2);
           const uint32_t w1 = *reinterpret_cast<const uint32_t*>(lnres + (kk + 8) * 2);
@@ -609,6 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   }
 }
 
+#if DAK_LINEAR_PART == 0
 // ------------------------------------------------------------------------------------ packing
 // dst[c][r][kc] with 16-byte chunk sl of row r stored at swz(r, sl); one thread per 16 B.
 __global__ void pack_kernel(const uint4* __restrict__ src, long long rows, long long K, int kc, uint4* __restrict__ dst) {
@@ -626,6 +660,8 @@ __global__ void pack_kernel(const uint4* __restrict__ src, long long rows, long 
     dst[(base + off) / 16] = src[idx];
   }
 }
+
+#endif
 
 // ------------------------------------------------------------------------------------ host side
 struct Plan {
@@ -657,15 +693,18 @@ static int bucket_of(const int* b, int n, long long need) {
   return -1;
 }
 
+// compiled m16-tile buckets per warp for each n8-tile count (accumulators: MTW x NT x 4 registers)
+static int mtw_max_for(int nt) { return nt <= 2 ? 12 : (nt == 4 ? 8 : 4); }
+
 // Rows a CTA may own for a given KC (accumulator capacity of each path).
-static long long path_row_cap(int path, int kc) {
+static long long path_row_cap(int path, int kc, int nt) {
   if (path == 1) {
     const int S = kc / 8;
     return (long long)(kConsumers / S) * kRptMax;
   }
   const int KS = kc / 16;
   const int WK = KS < kConsumerWarps ? KS : kConsumerWarps;
-  return 16LL * (kConsumerWarps / WK) * kMtwMax;
+  return 16LL * (kConsumerWarps / WK) * mtw_max_for(nt);
 }
 
 static dak_status make_plan(const dak_linear_args* a, Plan* out) {
@@ -675,6 +714,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (M <= 0 || K <= 0 || N <= 0) return fail(DAK_EINVAL, "dak_linear: M, K, N must be positive");
   if (h < 0 || h > M) return fail(DAK_EINVAL, "dak_linear: h must be in [0, M]");
   if (N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d (tcgen05 large-N path not in this build)", N, kMaxN);
+  const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : 8));  // n8 tiles (compiled: 1, 2, 4, 8)
   if (K % 64) return fail(DAK_EUNSUPPORTED, "dak_linear: K %% 64 != 0");
   if (kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
     return fail(DAK_EINVAL, "dak_linear: kc must be a power of two in [64, 2048] dividing K");
@@ -697,11 +737,12 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (path != 1 && path != 2) return fail(DAK_EINVAL, "dak_linear: bad force_path");
   // rows per CTA are bounded by the accumulator capacity of the path and by SMEM: at least three
   // ring stages of (rows x KC) weights plus the x rows must fit (deep enough to cover HBM latency)
-  const int n8 = path == 1 ? 8 : (int)ceil_div(N, 8) * 8;
-  const long long x_stage = (long long)n8 * kc * 2;
+  if (a->x_swiglu && (path != 2 || a->ln_w)) return fail(DAK_EINVAL, "dak_linear: x_swiglu needs the tensor-core path and no pre-norm");
+  const int n8 = path == 1 ? 8 : nt * 8;
+  const long long x_stage = (long long)n8 * kc * 2 * (a->x_swiglu ? 2 : 1);
   const long long smem_rows = ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
   if (path == 1 && kc > 8 * kConsumers) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path needs kc <= %d", 8 * kConsumers);
-  const long long cap = std::min(path_row_cap(path, kc), smem_rows);
+  const long long cap = std::min(path_row_cap(path, kc, nt), smem_rows);
   if (cap < 16) return fail(DAK_EUNSUPPORTED, "dak_linear: kc=%d leaves no room for a 16-row stage", kc);
 
   int n_host = 0;
@@ -735,6 +776,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     wk = KS < kConsumerWarps ? KS : kConsumerWarps;
     wm = kConsumerWarps / wk;
     bucket = bucket_of(kMtwBuckets, 7, ceil_div(ceil_div(rmax, 16), wm));
+    if (bucket > mtw_max_for(nt)) bucket = -1;
     rows_alloc = (long long)wm * bucket * 16;
   }
   if (bucket < 0) return fail(DAK_EUNSUPPORTED, "dak_linear: no unroll bucket for %lld rows per CTA", rmax);
@@ -761,7 +803,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.wm = wm; p.wk = wk;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
   p.n8 = n8;
-  p.x_stage_bytes = (int)x_stage;  // [kc/64 atoms][n8 rows][64], 128B-swizzled (a multiple of 1 KB)
+  p.x_stage_bytes = (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
+  p.swiglu = a->x_swiglu ? 1 : 0;
   int ln_bytes = 0;
   if (a->ln_w) {
     if (path != 2) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm needs the tensor-core path");
@@ -811,7 +854,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
 
   out->p = p;
   out->path = path;
-  out->nn = path == 1 ? N : (int)ceil_div(N, 8);
+  out->nn = path == 1 ? N : nt;
   out->bucket = bucket;
   out->grid = n_host + n_hbm;
   out->smem = p.res_offset + res_bytes + 1024;
@@ -834,8 +877,9 @@ static dak_status encode_xmap(Params* p) {
     if (q != cudaDriverEntryPointSuccess || !f) return fail(DAK_ECUDA, "dak_linear: cuTensorMapEncodeTiled unavailable");
     fn = (EncodeTiledFn)f;
   }
-  const cuuint64_t dims[3] = {64, (cuuint64_t)p->N, (cuuint64_t)(p->K / 64)};
-  const cuuint64_t strides[2] = {(cuuint64_t)p->K * 2, 128};
+  const long long ldx = p->swiglu ? 2 * p->K : p->K;  // [gate | up] rows are 2K wide
+  const cuuint64_t dims[3] = {64, (cuuint64_t)p->N, (cuuint64_t)(ldx / 64)};
+  const cuuint64_t strides[2] = {(cuuint64_t)ldx * 2, 128};
   const cuuint32_t box[3] = {64, (cuuint32_t)p->n8, (cuuint32_t)(p->kc / 64)};
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(&p->xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)p->x, dims, strides, box, estr,
@@ -845,9 +889,9 @@ static dak_status encode_xmap(Params* p) {
   return DAK_OK;
 }
 
-template <int PATH, int NN, int B, bool LN>
+template <int PATH, int NN, int B, int XF>
 static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
-  auto kern = split_linear_kernel<PATH, NN, B, LN>;
+  auto kern = split_linear_kernel<PATH, NN, B, XF>;
   static int smem_set = 0;  // raise the opt-in limit once per instance (not a stream op; capture-safe)
   if (!smem_set) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
@@ -867,51 +911,90 @@ static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
   return DAK_OK;
 }
 
-template <int PATH, int NN, bool LN>
-static dak_status launch_b(const Plan& pl, cudaStream_t s, int pdl) {
-  if constexpr (PATH == 1) {
-    switch (pl.bucket) {
-      case 1: return launch_t<1, NN, 1, false>(pl, s, pdl);
-      case 2: return launch_t<1, NN, 2, false>(pl, s, pdl);
-      case 4: return launch_t<1, NN, 4, false>(pl, s, pdl);
-      case 8: return launch_t<1, NN, 8, false>(pl, s, pdl);
-      case 16: return launch_t<1, NN, 16, false>(pl, s, pdl);
-    }
-  } else {
-    switch (pl.bucket) {
-      case 1: return launch_t<2, NN, 1, LN>(pl, s, pdl);
-      case 2: return launch_t<2, NN, 2, LN>(pl, s, pdl);
-      case 3: return launch_t<2, NN, 3, LN>(pl, s, pdl);
-      case 4: return launch_t<2, NN, 4, LN>(pl, s, pdl);
-      case 6: return launch_t<2, NN, 6, LN>(pl, s, pdl);
-      case 8: return launch_t<2, NN, 8, LN>(pl, s, pdl);
-      case 12: return launch_t<2, NN, 12, LN>(pl, s, pdl);
-    }
+template <int NN>
+static dak_status launch_fma(const Plan& pl, cudaStream_t s, int pdl) {
+  switch (pl.bucket) {
+    case 1: return launch_t<1, NN, 1, 0>(pl, s, pdl);
+    case 2: return launch_t<1, NN, 2, 0>(pl, s, pdl);
+    case 4: return launch_t<1, NN, 4, 0>(pl, s, pdl);
+    case 8: return launch_t<1, NN, 8, 0>(pl, s, pdl);
+    case 16: return launch_t<1, NN, 16, 0>(pl, s, pdl);
   }
-  return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for bucket %d", pl.bucket);
+  return fail(DAK_EUNSUPPORTED, "dak_linear: no FMA kernel instance for bucket %d", pl.bucket);
 }
 
+template <int NT, int XF>
+static dak_status launch_mma(const Plan& pl, cudaStream_t s, int pdl) {
+  switch (pl.bucket) {
+    case 1: return launch_t<2, NT, 1, XF>(pl, s, pdl);
+    case 2: return launch_t<2, NT, 2, XF>(pl, s, pdl);
+    case 3: return launch_t<2, NT, 3, XF>(pl, s, pdl);
+    case 4: return launch_t<2, NT, 4, XF>(pl, s, pdl);
+  }
+  if constexpr (NT <= 4) {
+    switch (pl.bucket) {
+      case 6: return launch_t<2, NT, 6, XF>(pl, s, pdl);
+      case 8: return launch_t<2, NT, 8, XF>(pl, s, pdl);
+    }
+  }
+  if constexpr (NT <= 2) {
+    if (pl.bucket == 12) return launch_t<2, NT, 12, XF>(pl, s, pdl);
+  }
+  return fail(DAK_EUNSUPPORTED, "dak_linear: no MMA kernel instance for bucket %d / %d n8 tiles", pl.bucket, NT);
+}
+
+template <int NT>
+static dak_status launch_mma_xf(const Plan& pl, cudaStream_t s, int pdl) {
+  if (pl.p.ln_w) return launch_mma<NT, 1>(pl, s, pdl);
+  if (pl.p.swiglu) return launch_mma<NT, 2>(pl, s, pdl);
+  return launch_mma<NT, 0>(pl, s, pdl);
+}
+
+// The kernel instances are spread over several translation units (this file compiled with
+// DAK_LINEAR_PART = 0..4, see build.py) so they compile in parallel; part 0 holds the host code.
+dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_nt1(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_nt2(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl);
+#if DAK_LINEAR_PART == 0
+dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl) {
+  switch (pl.nn) {
+    case 1: return launch_fma<1>(pl, s, pdl);
+    case 2: return launch_fma<2>(pl, s, pdl);
+    case 3: return launch_fma<3>(pl, s, pdl);
+    case 4: return launch_fma<4>(pl, s, pdl);
+  }
+  return fail(DAK_EUNSUPPORTED, "dak_linear: no FMA kernel instance for N = %d", pl.nn);
+}
+#elif DAK_LINEAR_PART == 1
+dak_status launch_part_nt1(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<1>(pl, s, pdl); }
+#elif DAK_LINEAR_PART == 2
+dak_status launch_part_nt2(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<2>(pl, s, pdl); }
+#elif DAK_LINEAR_PART == 3
+dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<4>(pl, s, pdl); }
+#elif DAK_LINEAR_PART == 4
+dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<8>(pl, s, pdl); }
+#endif
+
+#if DAK_LINEAR_PART == 0
 static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
-  if (pl.path == 1) {
-    switch (pl.nn) {
-      case 1: return launch_b<1, 1, false>(pl, s, pdl);
-      case 2: return launch_b<1, 2, false>(pl, s, pdl);
-      case 3: return launch_b<1, 3, false>(pl, s, pdl);
-      case 4: return launch_b<1, 4, false>(pl, s, pdl);
-    }
-  } else {
-    switch (pl.nn) {
-      case 1: return pl.p.ln_w ? launch_b<2, 1, true>(pl, s, pdl) : launch_b<2, 1, false>(pl, s, pdl);
-      case 2: return pl.p.ln_w ? launch_b<2, 2, true>(pl, s, pdl) : launch_b<2, 2, false>(pl, s, pdl);
-    }
+  if (pl.path == 1) return launch_part_fma(pl, s, pdl);
+  switch (pl.nn) {
+    case 1: return launch_part_nt1(pl, s, pdl);
+    case 2: return launch_part_nt2(pl, s, pdl);
+    case 4: return launch_part_nt4(pl, s, pdl);
+    case 8: return launch_part_nt8(pl, s, pdl);
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no kernel instance for path %d / %d", pl.path, pl.nn);
 }
+#endif
 
 }  // namespace lin
 }  // namespace dak
 
+#if DAK_LINEAR_PART == 0
 using namespace dak;
 
 extern "C" {
@@ -995,3 +1078,5 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
 }
 
 }  // extern "C"
+
+#endif  // DAK_LINEAR_PART == 0

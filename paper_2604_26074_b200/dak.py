@@ -61,7 +61,8 @@ class dak_linear_args(C.Structure):
                 ("residual", C.c_void_p), ("act", C.c_int32), ("reserved", C.c_int32), ("cfg", dak_launch_cfg),
                 ("ldy", C.c_int64), ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_int64),
                 ("ln_w", C.c_void_p), ("ln_b", C.c_void_p), ("ln_stats", C.c_void_p), ("ln_parts", C.c_int32),
-                ("ln_rms", C.c_int32), ("ln_eps", C.c_float), ("reserved2", C.c_int32), ("stats_out", C.c_void_p)]
+                ("ln_rms", C.c_int32), ("ln_eps", C.c_float), ("reserved2", C.c_int32), ("stats_out", C.c_void_p),
+                ("x_swiglu", C.c_int32), ("reserved3", C.c_int32)]
 
 
 class dak_linear_launch_info(C.Structure):
@@ -227,7 +228,7 @@ def launch_cfg(**kw) -> dak_launch_cfg:
 
 def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, act=ACT_NONE, cfg=None, ldy=0,
                 l2_prefetch=None, l2_prefetch_bytes=0, ln_w=None, ln_b=None, ln_stats=None, ln_parts=0, ln_rms=0,
-                ln_eps=1e-5, stats_out=None):
+                ln_eps=1e-5, stats_out=None, x_swiglu=0):
     a = dak_linear_args()
     a.w_host = _ptr(w_host)
     a.w_hbm = _ptr(w_hbm)
@@ -241,6 +242,7 @@ def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, a
     a.ln_w, a.ln_b, a.ln_stats = _ptr(ln_w), _ptr(ln_b), _ptr(ln_stats)
     a.ln_parts, a.ln_rms, a.ln_eps = int(ln_parts), int(ln_rms), float(ln_eps)
     a.stats_out = _ptr(stats_out)
+    a.x_swiglu = int(x_swiglu)
     return a
 
 

@@ -418,9 +418,10 @@ class DakOPT:
     def kernels_per_step(self) -> int:
         if getattr(self, "use_step", False):
             return 1
+        per_layer = 8 + (1 if self.chunks_per_req > 1 else 0)  # q k v append attn [combine] o fc1 fc2
         if self.fuse_norm:
-            return 1 + 9 * self.cfg.n_layers + 1
-        return 1 + 11 * self.cfg.n_layers + 2
+            return 1 + per_layer * self.cfg.n_layers + 1
+        return 1 + (per_layer + 2) * self.cfg.n_layers + 2
 
     def enable_persistent_step(self):
         self.build_step_program()

@@ -51,6 +51,9 @@ CASES = [  # (M, K, N, h, kc) — several tiles, ragged row counts, both tiers, 
     (2000, 1536, 5, 16, 512),
     (129, 8192, 12, 1, 1024),
     (5000, 128, 2, 2500, 64),
+    (1024, 8192, 24, 32, 256),   # 4 n8 tiles
+    (3584, 8192, 64, 48, 256),   # 8 n8 tiles (Llama-3-70B TP8 gate/up shard, b64)
+    (700, 1024, 33, 0, 128),
 ]
 
 
@@ -166,3 +169,23 @@ def test_opt30b_shapes_sampled(D, torch, M, K, N):
     ref = Kx.linear_rowloop(W[rows], x)
     from tests.gpu_util import assert_close
     assert_close(Kx.bf16_to_f64(y[:, rows]), ref)
+
+
+@pytest.mark.parametrize("M,K,N,h,kc", [(1000, 1024, 8, 24, 128), (3584, 2048, 64, 32, 256), (640, 512, 3, 640, 64)])
+def test_linear_swiglu_operand(D, torch, M, K, N, h, kc):
+    """x = [gate | up] of width 2K; the GEMV operand is bf16(silu(gate) * up) (Llama MLP down proj)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    W, _, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(8, M + N))
+    g = synth.rng(M * 3 + N)
+    gu = synth.normal_bf16(g, (N, 2 * K), 1.5)
+    sl = SplitLinear(D, W, h, kc)
+    xd = to_dev(gu)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    a = sl.args(xd, y, N)
+    a.x_swiglu = 1
+    D.linear(a)
+    torch.cuda.synchronize()
+    gf, uf = Kx.bf16_to_f64(gu[:, :K]), Kx.bf16_to_f64(gu[:, K:])
+    act = Kx.round_to_bf16(gf / (1.0 + np.exp(-gf)) * uf)
+    ref = Kx.split_linear(W[:h], W[h:], synth.bf16_bits(act.astype(np.float32)))
+    assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
