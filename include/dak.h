@@ -158,7 +158,7 @@ typedef struct {
   const void* w_hbm;    /* DAK-KC packed rows [h,M)   (device; may be NULL when h == M)       */
   int64_t M, K, h;      /* 0 <= h <= M                                                         */
   int32_t kc;           /* KC used to pack both tiers                                          */
-  int32_t N;            /* batch columns, 1..16                                                */
+  int32_t N;            /* batch columns, 1..64                                                */
   const void* x;        /* [N, K] bf16 row-major, device                                       */
   void* y;              /* [N, M] bf16 row-major, device                                       */
   const void* bias;     /* [M] bf16 or NULL                                                    */
@@ -188,6 +188,10 @@ typedef struct {
   /* Epilogue row statistics (nullable): CTA c writes float4 (count, mean, M2, 0) of its stored    */
   /* (bf16-rounded) outputs of row n to stats_out[c * N + n]; `grid` (dak_linear_query) parts.     */
   float* stats_out;
+  /* SwiGLU operand (Llama MLP down projection): x is [N, 2K] = [gate | up] (row stride 2K) and the  */
+  /* GEMV operand is bf16(silu(gate) * up), computed in fp32. Tensor-core path, no pre-norm.        */
+  int32_t x_swiglu;
+  int32_t reserved3;
 } dak_linear_args;
 
 /* Launch description (pure query; used by tests and the bench to attribute bytes). */
@@ -257,6 +261,32 @@ dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_strid
                          int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
                          dak_stream_t stream);
 
+/* Llama decode KV write with rotary positions (BASELINE configs[2] model): for every request b,
+ * rotate q (in place, all Hq heads) and k of the new token at positions[b] (rotate-half pairs
+ * (i, i + d/2), angle pos / theta^(2i/d)), then write the rotated k and v rows into the pools at
+ * positions[b] like dak_kv_append. qkv: [B, row_stride] bf16 rows holding q | k | v. */
+dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t Hq, int32_t Hkv, int32_t d,
+                             const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
+                             int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
+                             dak_stream_t stream);
+
+/* =============================================================================================
+ * 4b. Tensor-parallel combine (BASELINE north_star: TP over 8 x B200, NCCL over NVLink/NVSwitch)
+ *     Row-parallel projections (o, down) leave a PARTIAL [rows, cols] output on every rank.
+ * ============================================================================================= */
+
+/* NCCL communicator (libnccl.so.2 bound at run time). dak_comm_unique_id writes 128 bytes on one
+ * rank; the caller broadcasts them (e.g. torch.distributed) and every rank calls dak_comm_init. */
+dak_status dak_comm_unique_id(void* id_out);
+dak_status dak_comm_init(const void* id, int32_t rank, int32_t world, void** comm);
+dak_status dak_comm_destroy(void* comm);
+
+/* partial (bf16 [rows, cols], device) is summed over the communicator in place (comm NULL: one
+ * rank, no exchange), then x += partial (bf16 RNE) and, if stats_out != NULL, stats_out[r] =
+ * float4 (cols, mean, M2, 0) of the new row r of x (a fused pre-norm's ln_stats, 1 part). */
+dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t rows, int32_t cols, float* stats_out,
+                                  int32_t pdl, dak_stream_t stream);
+
 /* =============================================================================================
  * 5. Decoder-layer decode step (the split operators as drop-in replacements inside
  *    the model; whole decode step CUDA-graph captured) and its glue kernels
@@ -289,9 +319,10 @@ typedef struct {
 } dak_weight;
 
 #define DAK_MODEL_OPT 0   /* pre-LayerNorm, biases, ReLU MLP (OPT family)            */
+#define DAK_MODEL_LLAMA 1 /* pre-RMSNorm, no biases, rotary, GQA, SwiGLU MLP (BASELINE C3)   */
 
 typedef struct {
-  int32_t model;                      /* DAK_MODEL_OPT                                        */
+  int32_t model;                      /* DAK_MODEL_OPT | DAK_MODEL_LLAMA                      */
   int32_t B, hidden, n_heads, n_kv_heads, head_dim, ffn;
   float ln_eps;
   dak_weight qkv;                     /* fused [q;k;v] rows: (n_heads + 2 n_kv_heads) * head_dim */
@@ -305,7 +336,7 @@ typedef struct {
   const int32_t* positions;           /* [B] position of the new token                         */
   const int32_t* seq_lens;            /* [B] = positions + 1                                   */
   int32_t page_size, max_pages, chunk_pages;
-  int32_t tp_rank, tp_size;           /* tp_size must be 1 in this build                       */
+  int32_t tp_rank, tp_size;           /* tensor-parallel rank / world (Llama)                    */
   int32_t reserved;
   dak_launch_cfg cfg;                 /* linear ops (pdl applies to every kernel)              */
   dak_launch_cfg attn_cfg;            /* attention                                             */
@@ -321,6 +352,13 @@ typedef struct {
   int32_t stats_in_parts;             /* partials in stats_in (dak_layer_stats_parts of the      */
   const float* stats_in;              /* previous layer, or 1 for dak_embed's statistics)        */
   float* stats_out;                   /* row statistics of this layer's output x (FC2 epilogue)  */
+  /* Llama: n_heads / n_kv_heads / ffn are THIS rank's shard (heads n_heads*tp_rank ..); `up` is  */
+  /* the fused [gate; up] weight (2 ffn rows), `down` takes the SwiGLU operand; ln*_w are RMSNorm */
+  /* weights (ln*_b NULL); fuse_norm must be 1. With comm (required when tp_size > 1) o / down     */
+  /* write partials that dak_allreduce_residual sums over `comm` before the residual add.         */
+  float rope_theta;
+  int32_t reserved4;
+  void* comm;                         /* dak_comm_init communicator (required for tp_size > 1)  */
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);

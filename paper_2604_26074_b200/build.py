@@ -29,6 +29,7 @@ SOURCES = [
     ("attention.cu", []),
     ("layer.cu", []),
     ("step.cu", []),
+    ("tp.cu", []),
 ]
 
 
@@ -59,7 +60,7 @@ def build(verbose: bool = False) -> str:
             if verbose:
                 sys.stderr.write(out)
     if not os.path.exists(OUT) or os.path.getmtime(OUT) < max(os.path.getmtime(o) for o in objs):
-        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-o", OUT, *objs, "-lcudart", "-ldl"])
     return OUT
 
 

@@ -435,6 +435,53 @@ __global__ void append_kernel(const uint4* __restrict__ k_new, const uint4* __re
   (eh ? v_host : v_hbm)[off] = v_new[src];
 }
 
+// Llama decode KV write with rotary positions: rotate q (in place) and k of the new token of every
+// request at positions[b] (rotate-half pairs (i, i + d/2), angle pos / theta^(2i/d), computed in
+// double then fp32 sincos of the reduced angle), then append k (rotated) and v to the page pools.
+__global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, long long stride, int Hq, int Hkv,
+                                                          const int* pos, double log2_theta, const int* block_table,
+                                                          int page, int max_pages, uint4* k_hbm, uint4* v_hbm,
+                                                          uint4* k_host, uint4* v_host, unsigned long long* tr) {
+  __shared__ float s_c[kD / 2], s_s[kD / 2];
+  if (threadIdx.x == 0) tstamp(tr, 0);
+  grid_dep_launch();
+  grid_dep_wait();
+  const int b = blockIdx.x;
+  const int ps = pos[b];
+  if (threadIdx.x < kD / 2) {
+    const int i = threadIdx.x;
+    const double inv = exp2(-(2.0 * i / kD) * log2_theta);
+    const double ang = fmod((double)ps * inv, 6.283185307179586476925286766559);
+    float sn, cs;
+    sincosf((float)ang, &sn, &cs);
+    s_c[i] = cs;
+    s_s[i] = sn;
+  }
+  __syncthreads();
+  __nv_bfloat16* row = qkv + (long long)b * stride;
+  for (int j = threadIdx.x; j < (Hq + Hkv) * (kD / 2); j += blockDim.x) {
+    const int hh = j / (kD / 2), i = j % (kD / 2);
+    __nv_bfloat16* v = row + (long long)hh * kD;  // q heads then k heads are contiguous
+    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + kD / 2]);
+    v[i] = __float2bfloat16_rn(x1 * s_c[i] - x2 * s_s[i]);
+    v[i + kD / 2] = __float2bfloat16_rn(x2 * s_c[i] + x1 * s_s[i]);
+  }
+  __syncthreads();
+  const uint32_t e = (uint32_t)block_table[(long long)b * max_pages + ps / page];
+  const long long idx = (long long)(e & ~kHostBit);
+  const bool eh = (e & kHostBit) != 0;
+  const int t = ps % page;
+  const uint4* krow = reinterpret_cast<const uint4*>(row + (long long)Hq * kD);
+  const uint4* vrow = reinterpret_cast<const uint4*>(row + (long long)(Hq + Hkv) * kD);
+  for (int j = threadIdx.x; j < Hkv * (kD / 8); j += blockDim.x) {
+    const int g = j / (kD / 8), c = j % (kD / 8);
+    const long long off = ((idx * Hkv + g) * (long long)page * kD * 2 + pg_off(t, c)) / 16;
+    (eh ? k_host : k_hbm)[off] = krow[j];
+    (eh ? v_host : v_hbm)[off] = vrow[j];
+  }
+  if (threadIdx.x == 0) tstamp(tr, 3);
+}
+
 // ------------------------------------------------------------------------------------ host side
 static inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
@@ -610,6 +657,33 @@ dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_strid
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::append_kernel, (const uint4*)k_new, (const uint4*)v_new, stride / 8,
                                   block_table, positions, B, Hkv, page_size, max_pages, (uint4*)k_hbm, (uint4*)v_hbm,
                                   (uint4*)k_host, (uint4*)v_host, trace_slot(DAK_KIND_APPEND, B, Hkv, (n + 255) / 256)));
+  return DAK_OK;
+}
+
+dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t Hq, int32_t Hkv, int32_t d,
+                             const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
+                             int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
+                             dak_stream_t stream) {
+  if (!qkv || !positions || !block_table || B <= 0 || Hq <= 0 || Hkv <= 0 || page_size <= 0 || max_pages <= 0 ||
+      !(rope_theta > 1.f))
+    return fail(DAK_EINVAL, "dak_rope_kv_append: bad arguments");
+  if (d != attn::kD) return fail(DAK_EUNSUPPORTED, "dak_rope_kv_append: d must be 128");
+  const long long stride = row_stride > 0 ? row_stride : (long long)(Hq + 2 * Hkv) * d;
+  if (stride < (long long)(Hq + 2 * Hkv) * d || stride % 8 || !aligned16(qkv))
+    return fail(DAK_EINVAL, "dak_rope_kv_append: qkv rows must be 16-byte aligned and hold q, k, v");
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(B);
+  cfg.blockDim = dim3(256);
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::rope_append_kernel, (__nv_bfloat16*)qkv, stride, Hq, Hkv, positions,
+                                  (double)log2((double)rope_theta), block_table, page_size, max_pages, (uint4*)k_hbm,
+                                  (uint4*)v_hbm, (uint4*)k_host, (uint4*)v_host,
+                                  trace_slot(DAK_KIND_APPEND, B, Hkv, B)));
   return DAK_OK;
 }
 

@@ -148,10 +148,14 @@ struct Scratch {
 constexpr int kMaxParts = 1024;  // statistics partials (producer CTAs) a fused pre-norm merges
 
 static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
-  if (a->model != DAK_MODEL_OPT) return fail(DAK_EUNSUPPORTED, "dak_layer: model %d not in this build", a->model);
+  if (a->model != DAK_MODEL_OPT && a->model != DAK_MODEL_LLAMA)
+    return fail(DAK_EUNSUPPORTED, "dak_layer: model %d not in this build", a->model);
   if (a->B <= 0 || a->hidden <= 0 || a->n_heads <= 0 || a->n_kv_heads <= 0 || a->head_dim != 128 || a->ffn <= 0)
     return fail(DAK_EINVAL, "dak_layer: bad model sizes");
-  if (a->n_heads * a->head_dim != a->hidden) return fail(DAK_EINVAL, "dak_layer: n_heads * head_dim != hidden");
+  const bool llama = a->model == DAK_MODEL_LLAMA;
+  if (!llama && a->n_heads * a->head_dim != a->hidden) return fail(DAK_EINVAL, "dak_layer: n_heads * head_dim != hidden");
+  if (a->tp_size < 1 || a->tp_rank < 0 || a->tp_rank >= a->tp_size) return fail(DAK_EINVAL, "dak_layer: bad tp rank / size");
+  if (!llama && a->tp_size > 1) return fail(DAK_EUNSUPPORTED, "dak_layer: tensor parallelism is implemented for Llama");
   const size_t B = a->B;
   const size_t qkv_cols = (size_t)(a->n_heads + 2 * a->n_kv_heads) * a->head_dim;
   dak_attention_args at{};
@@ -161,11 +165,13 @@ static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
   size_t ws = 0;
   dak_status st = dak_attention_workspace_size(&at, &ws);
   if (st != DAK_OK) return st;
+  const size_t attn_cols = (size_t)a->n_heads * a->head_dim;
+  const size_t f_cols = (size_t)a->ffn * (llama ? 2 : 1);  // Llama: [gate | up]
   s->h = 0;
-  s->qkv = align256(s->h + B * a->hidden * 2);
+  s->qkv = align256(s->h + B * a->hidden * 2);  // h doubles as the TP partial buffer [B, hidden]
   s->attn = align256(s->qkv + B * qkv_cols * 2);
-  s->f = align256(s->attn + B * a->hidden * 2);
-  s->ws = align256(s->f + B * a->ffn * 2);
+  s->f = align256(s->attn + B * attn_cols * 2);
+  s->ws = align256(s->f + B * f_cols * 2);
   s->ws_bytes = ws;
   s->stats = align256(s->ws + ws);
   s->total = s->stats + (size_t)kMaxParts * B * 16;
@@ -182,6 +188,85 @@ static dak_linear_args lin_args(const dak_weight& w, long long M, long long K, i
   l.cfg = cfg;
   l.cfg.n_cta_host = w.n_cta_host > 0 ? w.n_cta_host : cfg.n_cta_host;
   return l;
+}
+
+// Llama decode layer (one tensor-parallel rank): RMSNorm fused into q/k/v and [gate; up], rotary +
+// KV append, split attention, o (+ all-reduce) + residual, SwiGLU fused into down (+ all-reduce)
+// + residual. 8 kernels per layer on one GPU (+2 NCCL all-reduces and 2 residual kernels at TP>1).
+static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_stream_t stream) {
+  if (!a->fuse_norm || !a->stats_in || a->stats_in_parts <= 0 || a->ln1_b || a->ln2_b)
+    return fail(DAK_EINVAL, "dak_layer (Llama): needs fuse_norm with stats_in and RMSNorm weights without bias");
+  if (!a->split_qkv) return fail(DAK_EINVAL, "dak_layer (Llama): q, k, v must be given separately (split_qkv)");
+  if (a->tp_size > 1 && !a->comm) return fail(DAK_EINVAL, "dak_layer (Llama): tp_size > 1 needs comm");
+  char* sc = (char*)a->scratch;
+  char* qkv = sc + s.qkv;
+  void* attn = sc + s.attn;
+  void* gu = sc + s.f;
+  void* partial = sc + s.h;
+  float* o_stats = (float*)(sc + s.stats);
+  const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads, F = a->ffn;
+  const long long qkv_cols = (long long)(Hq + 2 * Hkv) * d;
+  const int pdl = a->cfg.pdl;
+  const bool tp = a->comm != nullptr;  // row-parallel partials + all-reduce (also usable at tp_size 1)
+  cudaStream_t strm = (cudaStream_t)stream;
+  dak_status st;
+  auto rms = [&](dak_linear_args& l, const void* w, const float* stats, int parts) {
+    l.x = a->x;
+    l.ln_w = w; l.ln_b = nullptr; l.ln_rms = 1; l.ln_stats = stats; l.ln_parts = parts; l.ln_eps = a->ln_eps;
+  };
+  const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
+  const dak_weight* w[3] = {&a->q, &a->k, &a->v};
+  long long off = 0;
+  for (int i = 0; i < 3; ++i) {
+    dak_linear_args l = lin_args(*w[i], rows[i], H, B, a->x, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
+    l.ldy = qkv_cols;
+    rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
+    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+    off += rows[i];
+  }
+  if ((st = dak_rope_kv_append(qkv, qkv_cols, B, Hq, Hkv, d, a->positions, a->rope_theta, a->block_table, a->page_size,
+                               a->max_pages, a->k_hbm, a->v_hbm, a->k_host, a->v_host, pdl, strm)) != DAK_OK)
+    return st;
+  dak_attention_args at{};
+  at.q = qkv; at.out = attn;
+  at.k_hbm = a->k_hbm; at.v_hbm = a->v_hbm; at.k_host = a->k_host; at.v_host = a->v_host;
+  at.block_table = a->block_table; at.seq_lens = a->seq_lens;
+  at.B = B; at.Hq = Hq; at.Hkv = Hkv; at.d = d;
+  at.page_size = a->page_size; at.max_pages = a->max_pages; at.chunk_pages = a->chunk_pages;
+  at.scale = 0.f;
+  at.workspace = sc + s.ws; at.workspace_bytes = s.ws_bytes;
+  at.cfg = a->attn_cfg;
+  at.cfg.pdl = pdl;
+  at.q_row_stride = qkv_cols;
+  if ((st = dak_attention(&at, strm)) != DAK_OK) return st;
+  // o projection: residual + statistics in the epilogue (1 rank), or partial -> all-reduce -> residual
+  int o_parts = 1;
+  {
+    dak_linear_args l = lin_args(a->o, H, (long long)Hq * d, B, attn, tp ? partial : a->x, tp ? nullptr : a->x,
+                                 DAK_ACT_NONE, a->cfg);
+    if (!tp) {
+      dak_linear_launch_info info;
+      if ((st = dak_linear_query(&l, &info)) != DAK_OK) return st;
+      if (info.grid > kMaxParts) return fail(DAK_EUNSUPPORTED, "dak_layer: o grid %d > %d", info.grid, kMaxParts);
+      o_parts = info.grid;
+      l.stats_out = o_stats;
+    }
+    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, o_stats, pdl, strm)) != DAK_OK) return st;
+  }
+  {  // [gate; up] with RMSNorm 2 fused -> gu [B, 2F]
+    dak_linear_args l = lin_args(a->up, 2LL * F, H, B, a->x, gu, nullptr, DAK_ACT_NONE, a->cfg);
+    rms(l, a->ln2_w, o_stats, o_parts);
+    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+  }
+  {  // down with the SwiGLU operand
+    dak_linear_args l = lin_args(a->down, H, F, B, gu, tp ? partial : a->x, tp ? nullptr : a->x, DAK_ACT_NONE, a->cfg);
+    l.x_swiglu = 1;
+    if (!tp) l.stats_out = a->stats_out;
+    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, a->stats_out, pdl, strm)) != DAK_OK) return st;
+  }
+  return DAK_OK;
 }
 
 }  // namespace layer
@@ -252,10 +337,10 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   dak_status st = layer::scratch_layout(a, &s);
   if (st != DAK_OK) return st;
   if (!a->x || !a->scratch || a->scratch_bytes < s.total) return fail(DAK_EINVAL, "dak_layer: x / scratch missing or too small");
-  if (a->tp_size > 1) return fail(DAK_EUNSUPPORTED, "dak_layer: tensor parallel layer not in this build");
   const bool fuse = a->fuse_norm != 0;
   if (fuse && (!a->stats_in || a->stats_in_parts <= 0))
     return fail(DAK_EINVAL, "dak_layer: fuse_norm needs stats_in / stats_in_parts (row statistics of x)");
+  if (a->model == DAK_MODEL_LLAMA) return layer::llama_layer(a, s, stream);
   char* sc = (char*)a->scratch;
   void* h = sc + s.h;
   char* qkv = sc + s.qkv;
@@ -344,6 +429,10 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
 
 dak_status dak_layer_stats_parts(const dak_layer_args* a, int32_t* parts) {
   if (!a || !parts) return fail(DAK_EINVAL, "dak_layer_stats_parts: NULL");
+  if (a->model == DAK_MODEL_LLAMA && a->comm) {  // written by dak_allreduce_residual: 1 per row
+    *parts = 1;
+    return DAK_OK;
+  }
   dak_linear_args l = layer::lin_args(a->down, a->hidden, a->ffn, a->B, a->x, a->x, a->x, DAK_ACT_NONE, a->cfg);
   dak_linear_launch_info info;
   dak_status st = dak_linear_query(&l, &info);

@@ -1,0 +1,164 @@
+// Tensor-parallel combine for row-parallel projections (BASELINE north_star: TP over 8 x B200).
+//
+// Megatron layout: q/k/v/gate/up are split by output rows (heads / FFN rows, no exchange), o and
+// down by input columns, so each rank holds a PARTIAL [B, H] output that is summed over ranks
+// (NCCL all-reduce over NVLink / NVSwitch) before the residual add. dak_allreduce_residual does the
+// all-reduce in place and then x += sum (bf16 RNE) and the row statistics a fused pre-norm of the
+// next op consumes (one part per row). NCCL is bound at run time (dlopen of libnccl.so.2, the one
+// torch already loaded), so the library loads and the single-GPU path runs without NCCL.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <string.h>
+
+#include "common.h"
+
+namespace dak {
+namespace tp {
+
+struct Nccl {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+static dak_status nccl(Nccl** out) {
+  static Nccl n;
+  if (!n.h) {
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return fail(DAK_ENCCL, "libnccl.so.2 not loadable: %s", dlerror());
+    n.get_unique_id = (decltype(n.get_unique_id))dlsym(h, "ncclGetUniqueId");
+    n.comm_init_rank = (decltype(n.comm_init_rank))dlsym(h, "ncclCommInitRank");
+    n.comm_destroy = (decltype(n.comm_destroy))dlsym(h, "ncclCommDestroy");
+    n.all_reduce = (decltype(n.all_reduce))dlsym(h, "ncclAllReduce");
+    n.error_string = (decltype(n.error_string))dlsym(h, "ncclGetErrorString");
+    if (!n.get_unique_id || !n.comm_init_rank || !n.comm_destroy || !n.all_reduce || !n.error_string)
+      return fail(DAK_ENCCL, "libnccl.so.2 lacks a required symbol");
+    n.h = h;
+  }
+  *out = &n;
+  return DAK_OK;
+}
+
+#define DAK_NCCL_TRY(n, expr)                                                                     \
+  do {                                                                                           \
+    ncclResult_t r__ = (expr);                                                                   \
+    if (r__ != ncclSuccess) return fail(DAK_ENCCL, "%s failed: %s", #expr, (n)->error_string(r__)); \
+  } while (0)
+
+__device__ float block_sum(float v, float* red) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];  // fixed order
+  __syncthreads();
+  return t;
+}
+
+constexpr int kThreads = 256;
+constexpr int kPer = 64;  // values per thread (cols <= 16384)
+
+// x[r] += partial[r] (bf16 RNE); stats[r] = (cols, mean, M2) of the new x row (two-pass)
+__global__ void __launch_bounds__(kThreads) residual_stats_kernel(const __nv_bfloat16* __restrict__ partial,
+                                                                  __nv_bfloat16* __restrict__ x, int cols,
+                                                                  float4* __restrict__ stats) {
+  __shared__ float red[kThreads / 32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long base = (long long)blockIdx.x * cols;
+  float v[kPer];
+  int nv = 0;
+  float s = 0.f;
+#pragma unroll 4
+  for (int c = threadIdx.x; c < cols; c += kThreads) {
+    const __nv_bfloat16 o = __float2bfloat16_rn(__bfloat162float(x[base + c]) + __bfloat162float(partial[base + c]));
+    x[base + c] = o;
+    const float f = __bfloat162float(o);
+    if (nv < kPer) v[nv++] = f;
+    s += f;
+  }
+  if (!stats) return;
+  const float mean = block_sum(s, red) / (float)cols;
+  float m2 = 0.f;
+  for (int i = 0; i < nv; ++i) {
+    const float d = v[i] - mean;
+    m2 += d * d;
+  }
+  m2 = block_sum(m2, red);
+  if (threadIdx.x == 0) stats[blockIdx.x] = make_float4((float)cols, mean, m2, 0.f);
+}
+
+}  // namespace tp
+}  // namespace dak
+
+using namespace dak;
+
+extern "C" {
+
+dak_status dak_comm_unique_id(void* id_out) {
+  if (!id_out) return fail(DAK_EINVAL, "dak_comm_unique_id: NULL");
+  tp::Nccl* n;
+  dak_status st = tp::nccl(&n);
+  if (st != DAK_OK) return st;
+  ncclUniqueId id;
+  DAK_NCCL_TRY(n, n->get_unique_id(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return DAK_OK;
+}
+
+dak_status dak_comm_init(const void* id, int32_t rank, int32_t world, void** comm) {
+  if (!id || !comm || world < 1 || rank < 0 || rank >= world) return fail(DAK_EINVAL, "dak_comm_init: bad arguments");
+  tp::Nccl* n;
+  dak_status st = tp::nccl(&n);
+  if (st != DAK_OK) return st;
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c;
+  DAK_NCCL_TRY(n, n->comm_init_rank(&c, world, uid, rank));
+  *comm = (void*)c;
+  return DAK_OK;
+}
+
+dak_status dak_comm_destroy(void* comm) {
+  if (!comm) return DAK_OK;
+  tp::Nccl* n;
+  dak_status st = tp::nccl(&n);
+  if (st != DAK_OK) return st;
+  DAK_NCCL_TRY(n, n->comm_destroy((ncclComm_t)comm));
+  return DAK_OK;
+}
+
+dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t rows, int32_t cols, float* stats_out,
+                                  int32_t pdl, dak_stream_t stream) {
+  if (!partial || !x || rows <= 0 || cols <= 0) return fail(DAK_EINVAL, "dak_allreduce_residual: bad arguments");
+  if (cols > tp::kThreads * tp::kPer) return fail(DAK_EUNSUPPORTED, "dak_allreduce_residual: cols > %d", tp::kThreads * tp::kPer);
+  if (stats_out && !aligned16(stats_out)) return fail(DAK_EINVAL, "dak_allreduce_residual: stats_out must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (comm) {
+    tp::Nccl* n;
+    dak_status st = tp::nccl(&n);
+    if (st != DAK_OK) return st;
+    DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && !comm) ? 1 : 0;  // NCCL kernels are not PDL-aware
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(rows);
+  cfg.blockDim = dim3(tp::kThreads);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_stats_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
+                                  (int)cols, (float4*)stats_out));
+  return DAK_OK;
+}
+
+}  // extern "C"

@@ -322,7 +322,7 @@ class dak_layer_args(C.Structure):
                 ("reserved2", C.c_int32), ("q", dak_weight), ("k", dak_weight), ("v", dak_weight),
                 ("l2_prefetch_bytes", C.c_int64), ("next_w_hbm", C.c_void_p), ("next_w_hbm_bytes", C.c_int64),
                 ("fuse_norm", C.c_int32), ("stats_in_parts", C.c_int32), ("stats_in", C.c_void_p),
-                ("stats_out", C.c_void_p)]
+                ("stats_out", C.c_void_p), ("rope_theta", C.c_float), ("reserved4", C.c_int32), ("comm", C.c_void_p)]
 
 
 _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
@@ -333,8 +333,46 @@ _sig("dak_row_stats", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C
 _sig("dak_layer_scratch_size", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_size_t)])
 _sig("dak_layer", C.c_int32, [C.POINTER(dak_layer_args), C.c_void_p])
 _sig("dak_layer_stats_parts", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_int32)])
+_sig("dak_rope_kv_append", C.c_int32, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p,
+                                       C.c_float, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_int32, C.c_void_p])
+_sig("dak_comm_unique_id", C.c_int32, [C.c_void_p])
+_sig("dak_comm_init", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)])
+_sig("dak_comm_destroy", C.c_int32, [C.c_void_p])
+_sig("dak_allreduce_residual", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                           C.c_int32, C.c_void_p])
 EXPORTED += ["dak_layernorm", "dak_embed", "dak_row_stats", "dak_layer_scratch_size", "dak_layer",
-             "dak_layer_stats_parts"]
+             "dak_layer_stats_parts", "dak_rope_kv_append", "dak_comm_unique_id", "dak_comm_init", "dak_comm_destroy",
+             "dak_allreduce_residual"]
+MODEL_LLAMA = 1
+
+
+def rope_kv_append(qkv, row_stride, B, Hq, Hkv, d, positions, rope_theta, block_table, page_size, max_pages, k_hbm,
+                   v_hbm, k_host, v_host, pdl=0, stream=None):
+    _check(lib.dak_rope_kv_append(_ptr(qkv), int(row_stride), int(B), int(Hq), int(Hkv), int(d), _ptr(positions),
+                                  float(rope_theta), _ptr(block_table), int(page_size), int(max_pages), _ptr(k_hbm),
+                                  _ptr(v_hbm), _ptr(k_host), _ptr(v_host), int(pdl), _stream(stream)))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib.dak_comm_unique_id(buf))
+    return buf.raw
+
+
+def comm_init(uid: bytes, rank: int, world: int) -> int:
+    c = C.c_void_p()
+    _check(lib.dak_comm_init(C.create_string_buffer(uid, 128), int(rank), int(world), C.byref(c)))
+    return c.value
+
+
+def comm_destroy(comm):
+    _check(lib.dak_comm_destroy(comm))
+
+
+def allreduce_residual(comm, partial, x, rows, cols, stats_out=None, pdl=0, stream=None):
+    _check(lib.dak_allreduce_residual(comm, _ptr(partial), _ptr(x), int(rows), int(cols), _ptr(stats_out), int(pdl),
+                                      _stream(stream)))
 
 
 def weight(w_host, w_hbm, h, kc, bias=None, n_cta_host=0) -> dak_weight:

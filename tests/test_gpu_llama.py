@@ -1,0 +1,100 @@
+"""GPU parity of the Llama decode step (DakLlama: dak_layer DAK_MODEL_LLAMA through the C ABI)
+against the CPU oracle (oracle/layer.py llama_decode_step, pinned to transformers Llama), with
+weights and KV split between HBM and pinned host memory, and with the row-parallel combine going
+through an NCCL communicator (1 rank on one GPU: the all-reduce path runs, the sum is identity)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import kernels as Kx
+from oracle import layer as Ly
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(p, torch):
+    return {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16)).cuda().view(torch.bfloat16) for k, v in p.items()}
+
+
+@pytest.mark.parametrize("frac,B,ctx,use_comm", [(0.0, 3, 70, False), (0.3, 2, 150, False), (0.2, 4, 40, True)])
+def test_llama_step_matches_oracle(frac, B, ctx, use_comm):
+    import torch
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import HW
+    from paper_2604_26074_b200.llama import DakLlama, LlamaConfig
+    from tests.test_oracle_llama import make_llama_params
+    L, H, F, V, nh, nkv, d = 2, 512, 768, 96, 4, 2, 128
+    g = synth.rng(4242)
+    p = make_llama_params(g, L, H, F, V, nh, nkv, d)
+    cfg = LlamaConfig(n_layers=L, hidden=H, n_heads=nh, n_kv_heads=nkv, ffn=F, vocab=V, name="llama-tiny")
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    comm = dak.comm_init(dak.comm_unique_id(), 0, 1) if use_comm else None
+    total = L * (H * (nh + 2 * nkv) * d + nh * d * H + 3 * F * H) * 2 + V * H * 2
+    eng = DakLlama(cfg, B, ctx, hw, comm=comm, mode=dak.PLAN_EXACT, y_req=int(frac * total), page_size=64,
+                   chunk_pages=1, weights=_dev(p, torch))
+    if frac > 0:
+        assert sum(op.h for op in eng.linear_ops()) > 0
+    Kc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
+    Vc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
+    eng.load_kv(Kc, Vc)
+    tokens = np.arange(B) * 13 + 3
+    eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
+    s = torch.cuda.Stream()
+    eng.capture(s)
+    eng.graph.replay()
+    torch.cuda.synchronize()
+    ref, _ = Ly.llama_decode_step(tokens, np.full(B, ctx - 1), p, Kc, Vc, nh, nkv)
+    got = Kx.bf16_to_f64(eng.logits.view(torch.int16).cpu().numpy().view(np.uint16))
+    from tests.gpu_util import assert_close
+    assert_close(got, ref, rtol=3e-2)
+    eng.close()
+    if comm:
+        dak.comm_destroy(comm)
+
+
+def test_rope_kv_append_matches_oracle():
+    """Rotated q (in place) and the rotated k / v rows written into the paged pools."""
+    import torch
+    from paper_2604_26074_b200 import dak
+    from tests.gpu_util import to_dev, from_dev
+    B, Hq, Hkv, d, page, max_pages = 3, 8, 2, 128, 64, 4
+    g = synth.rng(99)
+    qkv = synth.normal_bf16(g, (B, (Hq + 2 * Hkv) * d), 1.0)
+    pos = np.array([0, 77, 250], dtype=np.int32)
+    bt = np.array([[0, 1, 2, 3], [4, 5, 6, 7], [8, 9, 10, 0x80000000 | 0]], dtype=np.int64)
+    bt32 = torch.from_numpy((bt & 0xFFFFFFFF).astype(np.uint32).view(np.int32)).cuda()
+    qd = to_dev(qkv)
+    kg = torch.zeros(12 * Hkv * page * d, dtype=torch.int16, device="cuda")
+    vg = torch.zeros_like(kg)
+    from tests.gpu_util import HostBuf
+    kh, vh = HostBuf(dak, Hkv * page * d * 2), HostBuf(dak, Hkv * page * d * 2)
+    dak.rope_kv_append(qd, 0, B, Hq, Hkv, d, torch.from_numpy(pos).cuda(), 500000.0, bt32, page, max_pages, kg, vg,
+                       kh.dp, vh.dp)
+    torch.cuda.synchronize()
+    out = Kx.bf16_to_f64(from_dev(qd)).reshape(B, Hq + 2 * Hkv, d)
+    x = Kx.bf16_to_f64(qkv).reshape(B, Hq + 2 * Hkv, d)
+    for b in range(B):
+        ref_q = Kx.round_to_bf16(Ly.rope(x[b, :Hq], int(pos[b]), 500000.0))
+        ref_k = Kx.round_to_bf16(Ly.rope(x[b, Hq:Hq + Hkv], int(pos[b]), 500000.0))
+        assert np.abs(out[b, :Hq] - ref_q).max() <= 2 ** -7 * np.abs(ref_q).max()
+        assert np.abs(out[b, Hq:Hq + Hkv] - ref_k).max() <= 2 ** -7 * np.abs(ref_k).max()
+        # pool rows (DAK-PG swizzle): un-swizzle the written row and compare with the rotated k / v
+        e = int(bt[b, pos[b] // page])
+        t = int(pos[b]) % page
+        for pool_k, pool_v in ((kg.cpu().numpy().view(np.uint16), vg.cpu().numpy().view(np.uint16)),):
+            pass
+        if e & 0x80000000:
+            kp, vp = kh.numpy(), vh.numpy()
+        else:
+            kp, vp = kg.cpu().numpy().view(np.uint16), vg.cpu().numpy().view(np.uint16)
+        idx = e & 0x7FFFFFFF
+        for gkv in range(Hkv):
+            base = (idx * Hkv + gkv) * page * d
+            row = np.zeros(d, np.uint16)
+            rowv = np.zeros(d, np.uint16)
+            for j in range(d // 8):
+                c = ((j >> 3) << 3) | ((j & 7) ^ (t & 7))
+                row[j * 8:(j + 1) * 8] = kp[base + t * d + c * 8: base + t * d + c * 8 + 8]
+                rowv[j * 8:(j + 1) * 8] = vp[base + t * d + c * 8: base + t * d + c * 8 + 8]
+            assert np.array_equal(row, from_dev(qd).reshape(B, Hq + 2 * Hkv, d)[b, Hq + gkv])
+            assert np.array_equal(rowv, qkv.reshape(B, Hq + 2 * Hkv, d)[b, Hq + Hkv + gkv])
