@@ -184,6 +184,45 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------------------------------------
+def make_llama(a, hw, world, rank, dak):
+    """BASELINE configs[2]: Llama-3-70B decode, batch 64, 64k context, TP8. Weights + KV of one rank
+    (17.6 GB + 171.8 GB) exceed HBM, so the global ratio is forced by capacity (EXACT mode)
+    against an HBM budget of 168 GB (12 GB kept for workspace); the default run is an 8-layer subset
+    with the budget scaled by 8/80 (labelled; per-step time extrapolates x10). On one GPU the rank
+    is rank 0 of 8 and its row-parallel all-reduce runs on a 1-rank NCCL communicator."""
+    from paper_2604_26074_b200.llama import DakLlama, LLAMA3_70B
+    from dataclasses import replace
+    layers = a.layers or 8
+    cfg = replace(LLAMA3_70B, n_layers=layers)
+    tp_size = 8 if world == 1 else world
+    batch = a.batch if a.batch != 8 else 64
+    context = a.context if a.context != 64 else 65536
+    if world == 1:
+        comm = dak.comm_init(dak.comm_unique_id(), 0, 1)
+    else:
+        import torch.distributed as dist
+        uid = [dak.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = dak.comm_init(uid[0], rank, world)
+    from paper_2604_26074_b200 import tp
+    dm = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
+    d, H = cfg.head_dim, cfg.hidden
+    per_layer = (dm["n_heads"] + 2 * dm["n_kv"]) * d * H + H * dm["n_heads"] * d + 3 * dm["ffn"] * H
+    w_bytes = 2 * (layers * per_layer + dm["vocab"] * H)
+    kv_bytes = layers * 2 * (cfg.n_kv_heads // tp_size) * cfg.head_dim * 2 * batch * context
+    budget = int(168e9 * layers / cfg.__class__().n_layers)
+    y_req = max(0, w_bytes + kv_bytes - budget)
+    eng = DakLlama(cfg, batch, context, hw, tp_rank=rank, tp_size=tp_size, comm=comm, mode=dak.PLAN_EXACT,
+                   y_req=y_req, pdl=not a.no_pdl, congestion_control=not a.no_cc, seed=1234 + rank)
+    wl = dict(workload="llama3-70b-tp8-b%d-ctx%d" % (batch, context), model_shape="Llama-3-70B (TP%d shard)" % tp_size,
+              batch=batch, context=context, layers=layers, layers_model=80,
+              extrapolation="x%d per token step" % (80 // layers) if layers != 80 else None,
+              hbm_budget_bytes=budget, y_req_bytes=y_req, plan="EXACT (capacity-forced R=%.4f)" % (y_req / (w_bytes + kv_bytes)),
+              tp="rank 0 of %d on one GPU (1-rank NCCL all-reduce)" % tp_size if world == 1 else "TP%d over NCCL" % world)
+    eng.comm_handle = comm
+    return eng, cfg, wl
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -201,7 +240,11 @@ def main():
     ap.add_argument("--l2-prefetch-mb", type=float, default=0.0, help="L2 warm-up of the next linear (0: off)")
     ap.add_argument("--no-evict-first", action="store_true")
     ap.add_argument("--no-fuse-norm", action="store_true", help="LayerNorm kernels instead of the fused pre-norm")
-    ap.add_argument("--layers", type=int, default=48, help="(debug) fewer layers; invalid as a bench number")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="layers (default: all 48 for OPT-30B; 8 of 80 for the Llama subset, labelled)")
+    ap.add_argument("--workload", default="opt30b", choices=["opt30b", "llama3-70b-tp8"],
+                    help="opt30b: BASELINE configs[1] (the bench line); llama3-70b-tp8: configs[2], this GPU's TP "
+                         "shard (rank 0 of 8 on one GPU, or the real ranks under torchrun), capacity-forced ratios")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.impl == "reference":
@@ -214,16 +257,21 @@ def main():
     world, rank, local = dist_setup()
     hbm_gbs, link_gbs, peak_src = measured_peaks()
     hw = HW(hbm_bps=hbm_gbs * 1e9, link_bps=link_gbs * 1e9)
-    cfg = OPT_30B if a.layers == 48 else OPTConfig(n_layers=a.layers)
-    eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
-                 congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                 evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
-    if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
-        tot = sum(o["total_bytes"] for o in eng.plan_ops)
-        eng.close()
-        eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
+    llama = a.workload == "llama3-70b-tp8"
+    if llama:
+        eng, cfg, wl = make_llama(a, hw, world, rank, dak)
+    else:
+        layers = a.layers or 48
+        cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
+        eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                 evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
+                     evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
+        if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
+            tot = sum(o["total_bytes"] for o in eng.plan_ops)
+            eng.close()
+            eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
+                         congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
+                         evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
     if a.persistent:
         eng.enable_persistent_step()
     nb = eng.bytes_per_step()
@@ -252,11 +300,12 @@ def main():
     t_max = reduce_max(t, world)
     step_s = t_max / a.steps
     value = nb["total"] * world * a.steps / t_max / 1e9
-    tok_s = a.batch * world * a.steps / t_max
+    reqs = eng.B if llama else eng.B * world  # TP: one batch over all ranks; replicas: one per rank
+    tok_s = reqs * a.steps / t_max
 
     # ---------------- end to end through the public API with host buffers
-    tok_host = torch.zeros(a.batch, dtype=torch.int32).pin_memory()
-    logits_host = torch.empty(a.batch, cfg.vocab, dtype=torch.bfloat16).pin_memory()
+    tok_host = torch.zeros(eng.B, dtype=torch.int32).pin_memory()
+    logits_host = torch.empty(eng.B, eng.logits.shape[1], dtype=torch.bfloat16).pin_memory()
     barrier(world)
     torch.cuda.synchronize()
     with torch.cuda.stream(stream):
@@ -270,24 +319,24 @@ def main():
     torch.cuda.synchronize()
     te = reduce_max(e0.elapsed_time(e1) / 1e3, world)
     e2e = dict(value=round(nb["total"] * world * a.steps / te / 1e9, 2), unit="GB/s",
-               tokens_per_s=round(a.batch * world * a.steps / te, 2),
+               tokens_per_s=round(reqs * a.steps / te, 2),
                h2d_bytes_per_step=tok_host.numel() * 4, d2h_bytes_per_step=logits_host.numel() * 2)
 
     # ---------------- roofline of the dominant kernel (dak_linear), CUDA events on its stream
     lin_bytes, lin_time = 0, 0.0
     evs = []
     ops = list(eng.linear_ops())
-    xs = torch.zeros(a.batch, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
-    ys = torch.empty(a.batch, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
+    xs = torch.zeros(eng.B, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
+    ys = torch.empty(eng.B, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
     with torch.cuda.stream(stream):
         for op in ops:
-            la = dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, a.batch, xs, ys,
+            la = dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
                                  cfg=dict(congestion_control=int(not a.no_cc)))
             s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             s0.record(stream)
             dak.linear(la, stream)
             s1.record(stream)
-            evs.append((s0, s1, op.M * op.K * 2 + a.batch * (op.K + op.M) * 2))
+            evs.append((s0, s1, op.M * op.K * 2 + eng.B * (op.K + op.M) * 2))
     torch.cuda.synchronize()
     for s0, s1, b in evs:
         lin_time += s0.elapsed_time(s1) / 1e3
@@ -312,26 +361,33 @@ def main():
 
     line = dict(metric=METRIC, value=round(value, 2), unit="GB/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
                 ms_per_step=round(step_s * 1e3, 4), higher_is_better=True, scaling="weak", vs_baseline=None,
-                dtype="bf16", data="synthetic (random-init OPT-30B weights and KV)",
-                config=dict(workload="opt-30b-decode-b%d-ctx%d" % (a.batch, a.context), model_shape="OPT-30B",
-                            batch=a.batch, context=a.context, layers=cfg.n_layers,
+                dtype="bf16", data="synthetic (random-init %s weights and KV)" % cfg.name,
+                config=(dict(wl, host_bytes_per_step=nb["host"], hbm_bytes_per_step=nb["hbm"],
+                             host_ratio=round(nb["host"] / nb["total"], 5), pdl=not a.no_pdl,
+                             congestion_control=not a.no_cc, execution="per-op kernels (dak_layer, PDL, CUDA graph)")
+                        if llama else dict(workload="opt-30b-decode-b%d-ctx%d" % (eng.B, a.context), model_shape="OPT-30B",
+                            batch=eng.B, context=a.context, layers=cfg.n_layers,
                             plan="BALANCED" if a.ratio is None else "EXACT R=%.4f" % a.ratio,
                             host_bytes_per_step=nb["host"], hbm_bytes_per_step=nb["hbm"],
                             host_ratio=round(nb["host"] / nb["total"], 5),
                             l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
                             execution="persistent step (dak_step, 1 launch)" if a.persistent else "per-op kernels (dak_layer, PDL, CUDA graph)",
-                            parallelism="dp%d replicas (weak scaling, no collective)" % world),
+                            parallelism="dp%d replicas (weak scaling, no collective)" % world)),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
+                **({"tokens_per_s_full_model_extrapolated": round(tok_s * cfg.n_layers / 80, 2)}
+                   if llama and cfg.n_layers != 80 else {}),
                 gpu_launches=eng.kernels_per_step() * a.steps)
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        v, dt, nbytes, threads, reps = oracle_sample(a.batch)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline and not llama:
+        v, dt, nbytes, threads, reps = oracle_sample(eng.B)
         line["cpu_baseline"] = dict(value=round(v, 3), unit="GB/s", cores=threads, kind="oracle",
                                     sample="OPT-30B layer-0 q/k/v/o/fc1/fc2 float64 oracle linears (N=%d) + 56-head "
-                                           "decode attention over 64 tokens, x%d (%.1f s)" % (a.batch, reps, dt))
+                                           "decode attention over 64 tokens, x%d (%.1f s)" % (eng.B, reps, dt))
     if rank == 0:
         print(json.dumps(line), flush=True)
     eng.close()
+    if getattr(eng, "comm_handle", None):
+        dak.comm_destroy(eng.comm_handle)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         if (lane == 0) {
           const float var = p.ln_rms ? m2 / c + mean * mean : m2 / c;  // RMS: mean of squares
           s_ln[n] = p.ln_rms ? 0.f : mean;
-          s_ln[16 + n] = rsqrtf(var + p.ln_eps);
+          s_ln[kMaxN + n] = rsqrtf(var + p.ln_eps);
         }
       }
       consumer_sync();
@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       for (int nt = 0; nt < NT; ++nt) {
         const int n = nt * 8 + (lane >> 2);
         mu[nt] = n < N ? s_ln[n] : 0.f;
-        rs[nt] = n < N ? s_ln[16 + n] : 0.f;
+        rs[nt] = n < N ? s_ln[kMaxN + n] : 0.f;
       }
       mbar_wait(lnbar, 0);
     }

@@ -46,7 +46,7 @@ def _oracle_norm(x, w, b, rms, eps=1e-5):
 
 @pytest.mark.parametrize("rms", [False, True])
 @pytest.mark.parametrize("M,K,N,h,kc", [(700, 1024, 1, 33, 128), (1500, 2048, 8, 64, 256), (512, 4096, 16, 0, 64),
-                                        (333, 512, 5, 333, 64)])
+                                        (333, 512, 5, 333, 64), (1024, 8192, 64, 32, 256), (900, 2048, 40, 0, 128)])
 def test_fused_norm_linear(D, torch, rms, M, K, N, h, kc):
     from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
     W, _, bias = synth.linear_inputs(M, K, N, seed=synth.seed_for(5, M + N), bias=True)
