@@ -151,6 +151,10 @@ typedef struct {
   int32_t force_path;         /* 0 auto, 1 CUDA-core FMA path, 2 tensor-core (mma.sync) path   */
   int32_t l2_policy;          /* 0: stream weights/KV with the L2 evict_first hint (they are   */
                               /*    read once per step), 1: no hint                              */
+  int32_t cluster;            /* dak_linear: CTAs per thread-block cluster sharing ONE fetch of */
+                              /* each x chunk by TMA multicast (P:L555-571 applied to the        */
+                              /* operand every CTA reads); 0/1 off, 2 or 4. Same outputs bitwise */
+  int32_t reserved;
 } dak_launch_cfg;
 
 typedef struct {
@@ -200,6 +204,7 @@ typedef struct {
   int32_t stages_hbm, window_host, smem_bytes, path; /* path: 1 FMA, 2 mma.sync               */
   int64_t rows_per_cta_host_max, rows_per_cta_hbm_max;
   int64_t hbm_bytes, host_bytes;                      /* algorithmic weight bytes per tier     */
+  int32_t cluster, reserved;                          /* CTAs sharing one x fetch (multicast)  */
 } dak_linear_launch_info;
 
 dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);

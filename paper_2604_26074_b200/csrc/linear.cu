@@ -63,6 +63,7 @@ struct __align__(64) Params {
   int wm, wk;       // MMA path: consumer warps along M x along K (wm * wk == kConsumerWarps)
   int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
   int swiglu;       // x = [gate | up] ([N, 2K]); the operand is silu(gate) * up
+  int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
   const __nv_bfloat16* ln_w;
   const __nv_bfloat16* ln_b;
@@ -128,6 +129,29 @@ __device__ __forceinline__ void tma_3d(void* dst, uint64_t tmap, int c0, int c1,
           "r"(su32(dst)),
       "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
       : "memory");
+}
+// the same, delivered to every CTA of the cluster in ctamask (same SMEM offset, each CTA's own
+// mbarrier at the same offset receives the complete_tx)
+__device__ __forceinline__ void tma_3d_mc(void* dst, uint64_t tmap, int c0, int c1, int c2, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;" ::
+          "r"(su32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar)), "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// arrive on the mbarrier at the same SMEM offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t rank) {
+  uint32_t ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(su32(b)), "r"(rank));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
 }
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -207,6 +231,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint64_t* lnbar = empty + kMaxStages;
+  uint64_t* xempty = lnbar + 1;  // [kMaxStages] in the cluster leader: x slot free in EVERY cluster CTA
   unsigned char* wring = smem + 1024;
   unsigned char* xring = smem + p.off_x;
   float* res = reinterpret_cast<float*>(smem + p.res_offset);
@@ -236,9 +261,13 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       mbar_init(&empty[s], kConsumerWarps);
     }
     mbar_init(lnbar, 1);
+    if (p.mc > 1)
+      for (int s = 0; s < p.stages; ++s) mbar_init(&xempty[s], kConsumerWarps * p.mc);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const uint32_t crank = p.mc > 1 ? cluster_rank() : 0u;
+  if (p.mc > 1) cluster_sync();  // peers' barriers are initialised before any multicast / remote arrive
   if (threadIdx.x == 0) tstamp(p.trace, 0);
   grid_dep_launch();  // the next op may start its weight stream as our CTAs retire
   if (R <= 0) {
@@ -255,56 +284,68 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
 
   if (warp == 0) {
     // ============================ producer (one lane): W span + x box per stage
-    if (lane != 0) return;
-    const int pro = min(slots, nchunks);
-    const char* src = wsrc + rb * kc * 2;
-    // weights are read exactly once per step: evict_first keeps L2 for activations and for the
-    // next op's prefetched prefix
-    const bool ef = p.evict_first != 0;
-    const uint64_t pol = policy_evict_first();
-    const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
-    asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
-    auto load_w = [&](int slot, int i) {
-      unsigned char* dst = wring + (size_t)slot * p.w_stage_bytes;
-      const char* s_ = src + (long long)i * chunk_stride;
-      if (ef) bulk_g2s_hint(dst, s_, w_bytes, &full[slot], pol);
-      else bulk_g2s(dst, s_, w_bytes, &full[slot]);
-    };
-    auto load_x = [&](int slot, int i) {
-      unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
-      tma_3d(dst, xmap, 0, 0, i * (kc >> 6), &full[slot]);
-      if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K + (long long)i * kc) >> 6), &full[slot]);
-    };
-    for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
-      mbar_expect_tx(&full[i], w_bytes + x_tx);
-      load_w(i, i);
+    if (lane == 0) {
+      const int pro = min(slots, nchunks);
+      const char* src = wsrc + rb * kc * 2;
+      // weights are read exactly once per step: evict_first keeps L2 for activations and for the
+      // next op's prefetched prefix
+      const bool ef = p.evict_first != 0;
+      const uint64_t pol = policy_evict_first();
+      const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      auto load_w = [&](int slot, int i) {
+        unsigned char* dst = wring + (size_t)slot * p.w_stage_bytes;
+        const char* s_ = src + (long long)i * chunk_stride;
+        if (ef) bulk_g2s_hint(dst, s_, w_bytes, &full[slot], pol);
+        else bulk_g2s(dst, s_, w_bytes, &full[slot]);
+      };
+      const uint16_t mask = (uint16_t)((1u << p.mc) - 1u);
+      auto load_x = [&](int slot, int i) {
+        unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
+        if (p.mc > 1) {  // the leader fetches the chunk once for the whole cluster
+          if (crank != 0) return;
+          tma_3d_mc(dst, xmap, 0, 0, i * (kc >> 6), &full[slot], mask);
+          if (XF == 2)
+            tma_3d_mc(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K + (long long)i * kc) >> 6), &full[slot], mask);
+          return;
+        }
+        tma_3d(dst, xmap, 0, 0, i * (kc >> 6), &full[slot]);
+        if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K + (long long)i * kc) >> 6), &full[slot]);
+      };
+      for (int i = 0; i < pro; ++i) {  // weights do not depend on the previous kernel: start now
+        mbar_expect_tx(&full[i], w_bytes + x_tx);
+        load_w(i, i);
+      }
+      if (XF == 1) {  // LN weight / bias are parameters too: resident for the whole kernel
+        const uint32_t kb = (uint32_t)p.K * 2;
+        mbar_expect_tx(lnbar, p.ln_b ? 2 * kb : kb);
+        bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
+        if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
+      }
+      grid_dep_wait();  // x is produced by the previous kernel
+      tstamp(p.trace, 1);
+      for (int i = 0; i < pro; ++i) load_x(i, i);
+      int s = pro == slots ? 0 : pro;
+      uint32_t ph = pro == slots ? 1u : 0u;
+      for (int i = pro; i < nchunks; ++i) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], w_bytes + x_tx);
+        load_w(s, i);
+        if (p.mc > 1 && crank == 0) mbar_wait(&xempty[s], ph ^ 1u);  // slot s free in every cluster CTA
+        load_x(s, i);
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+      // this CTA's last weight copies are in flight: warm L2 with its slice of the next op's first
+      // bytes so the next kernel's ramp reads L2 while this one drains (hint only)
+      if (p.pf_bytes > 0) {
+        const long long G = gridDim.x;
+        const long long b = (p.pf_bytes * cta / G) & ~15LL;
+        const long long e = (p.pf_bytes * (cta + 1) / G) & ~15LL;
+        for (long long o = b; o < e; o += 32768) prefetch_l2(p.pf + o, (uint32_t)min(32768LL, e - o));
+      }
     }
-    if (XF == 1) {  // LN weight / bias are parameters too: resident for the whole kernel
-      const uint32_t kb = (uint32_t)p.K * 2;
-      mbar_expect_tx(lnbar, p.ln_b ? 2 * kb : kb);
-      bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
-      if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
-    }
-    grid_dep_wait();  // x is produced by the previous kernel
-    tstamp(p.trace, 1);
-    for (int i = 0; i < pro; ++i) load_x(i, i);
-    int s = pro == slots ? 0 : pro;
-    uint32_t ph = pro == slots ? 1u : 0u;
-    for (int i = pro; i < nchunks; ++i) {
-      mbar_wait(&empty[s], ph ^ 1u);
-      mbar_expect_tx(&full[s], w_bytes + x_tx);
-      load_w(s, i);
-      load_x(s, i);
-      if (++s == slots) { s = 0; ph ^= 1u; }
-    }
-    // this CTA's last weight copies are in flight: warm L2 with its slice of the next op's first
-    // bytes so the next kernel's ramp reads L2 while this one drains (hint only)
-    if (p.pf_bytes > 0) {
-      const long long G = gridDim.x;
-      const long long b = (p.pf_bytes * cta / G) & ~15LL;
-      const long long e = (p.pf_bytes * (cta + 1) / G) & ~15LL;
-      for (long long o = b; o < e; o += 32768) prefetch_l2(p.pf + o, (uint32_t)min(32768LL, e - o));
-    }
+    __syncwarp();
+    if (p.mc > 1) cluster_sync();  // peers' remote arrivals on our barriers have landed
     return;
   }
 
@@ -366,7 +407,10 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        if (p.mc > 1) mbar_arrive_remote(&xempty[s], 0);  // the leader refills x for the whole cluster
+      }
       if (++s == slots) { s = 0; ph ^= 1u; }
     }
     // reduce the S slice-partials of each row: shuffle inside groups of min(S,32) lanes ...
@@ -541,7 +585,10 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) {
+        mbar_arrive(&empty[s]);
+        if (p.mc > 1) mbar_arrive_remote(&xempty[s], 0);  // the leader refills x for the whole cluster
+      }
       if (++s == slots) { s = 0; ph ^= 1u; }
     }
     // deterministic cross-warp reduction over the WK warps sharing m-tiles (fixed wk order): either
@@ -640,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
     consumer_sync();
     if (t == 0) tstamp(p.trace, 3);
   }
+  if (p.mc > 1) cluster_sync();
 }
 
 #if DAK_LINEAR_PART == 0
@@ -669,6 +717,35 @@ struct Plan {
   int path, nn, bucket, grid, smem;
   long long rmax_host, rmax_hbm;
 };
+
+// Clusters of `mc` one-CTA-per-SM blocks the device co-schedules at once (GPCs with an odd number
+// of usable SMs leave SMs idle): the multicast grid is sized to this, never to a second wave.
+template <int PATH, int NN, int MTW, int XF>
+__global__ void split_linear_kernel(const __grid_constant__ Params p);
+static dak_status max_active_clusters(int mc, int* out) {
+  static int cache[5] = {0, 0, 0, 0, 0};
+  if (mc < 1 || mc > 4) return fail(DAK_EINVAL, "dak_linear: bad cluster size");
+  if (cache[mc] <= 0) {
+    auto kern = split_linear_kernel<1, 1, 1, 0>;
+    DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(mc * 64);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 200 * 1024;  // any size forcing one CTA per SM
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = mc;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    DAK_CUDA_TRY(cudaOccupancyMaxActiveClusters(&n, (void*)kern, &cfg));
+    cache[mc] = n;
+  }
+  *out = cache[mc];
+  return DAK_OK;
+}
 
 static int g_sms = 0;
 static dak_status device_sms(int* out) {
@@ -757,6 +834,26 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     n_hbm = (int)std::max<long long>(n_hbm, ceil_div(M - h, cap));
     n_hbm = (int)std::min<long long>(n_hbm, M - h);
   }
+  // x multicast: clusters of mc CTAs never mix tiers and every CTA owns >= 1 row (else off)
+  int mc = c.cluster > 1 ? c.cluster : 1;
+  if (mc != 1 && mc != 2 && mc != 4) return fail(DAK_EINVAL, "dak_linear: cluster must be 0, 1, 2 or 4");
+  if (mc > 1 && path != 2) mc = 1;
+  if (mc > 1) {
+    const int nh2 = n_host ? (int)ceil_div(n_host, mc) * mc : 0;
+    int ng2 = n_hbm ? std::max(mc, n_hbm / mc * mc) : 0;
+    if (n_hbm && c.n_cta_hbm <= 0) {  // auto grid: only as many clusters as run concurrently
+      int clusters = 0;
+      dak_status st = max_active_clusters(mc, &clusters);
+      if (st != DAK_OK) return st;
+      ng2 = std::max(mc, std::min(ng2, (clusters - nh2 / mc) * mc));
+    }
+    if (nh2 <= h && ng2 <= M - h && (!n_host || ceil_div(h, nh2) <= cap) && (!n_hbm || ceil_div(M - h, ng2) <= cap)) {
+      n_host = nh2;
+      n_hbm = ng2;
+    } else {
+      mc = 1;
+    }
+  }
   const long long rmax_host = n_host ? ceil_div(h, n_host) : 0;
   const long long rmax_hbm = n_hbm ? ceil_div(M - h, n_hbm) : 0;
   const long long rmax = std::max(rmax_host, rmax_hbm);
@@ -801,6 +898,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
   p.n_host = n_host; p.n_hbm = n_hbm;
   p.wm = wm; p.wk = wk;
+  p.mc = mc;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
   p.n8 = n8;
   p.x_stage_bytes = (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
@@ -902,11 +1000,15 @@ static dak_status launch_t(const Plan& pl, cudaStream_t stream, int pdl) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = pl.p.mc;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pl.p.mc > 1 ? 2 : 1;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pl.p));
   return DAK_OK;
 }
@@ -1047,6 +1149,8 @@ dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info*
   info->rows_per_cta_hbm_max = pl.rmax_hbm;
   info->hbm_bytes = (args->M - args->h) * args->K * 2;
   info->host_bytes = args->h * args->K * 2;
+  info->cluster = pl.p.mc;
+  info->reserved = 0;
   return DAK_OK;
 }
 

@@ -52,7 +52,7 @@ class dak_op_plan(C.Structure):
 class dak_launch_cfg(C.Structure):
     _fields_ = [("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("window", C.c_int32), ("stages", C.c_int32),
                 ("congestion_control", C.c_int32), ("pdl", C.c_int32), ("force_path", C.c_int32),
-                ("l2_policy", C.c_int32)]
+                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("reserved", C.c_int32)]
 
 
 class dak_linear_args(C.Structure):
@@ -69,7 +69,7 @@ class dak_linear_launch_info(C.Structure):
     _fields_ = [("grid", C.c_int32), ("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("threads", C.c_int32),
                 ("stages_hbm", C.c_int32), ("window_host", C.c_int32), ("smem_bytes", C.c_int32), ("path", C.c_int32),
                 ("rows_per_cta_host_max", C.c_int64), ("rows_per_cta_hbm_max", C.c_int64),
-                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64)]
+                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _sig(name, res, args):

@@ -189,3 +189,42 @@ def test_linear_swiglu_operand(D, torch, M, K, N, h, kc):
     act = Kx.round_to_bf16(gf / (1.0 + np.exp(-gf)) * uf)
     ref = Kx.split_linear(W[:h], W[h:], synth.bf16_bits(act.astype(np.float32)))
     assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
+
+
+@pytest.mark.parametrize("M,K,N,h,kc,xf", [(7168, 7168, 8, 48, 256, 0), (3584, 8192, 64, 32, 256, 0),
+                                           (1500, 2048, 8, 64, 256, 1), (1000, 1024, 16, 0, 128, 2)])
+@pytest.mark.parametrize("cluster", [2, 4])
+def test_linear_x_multicast_bitwise(D, torch, M, K, N, h, kc, xf, cluster):
+    """TMA multicast of the x chunk within clusters (one fetch per cluster) gives the
+    same outputs bitwise as one fetch per CTA (and both match the oracle)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(9, M + N), bias=True)
+    g = synth.rng(M + 17 * N)
+    if xf == 2:
+        x = synth.normal_bf16(g, (N, 2 * K), 1.0)
+    sl = SplitLinear(D, W, h, kc)
+    xd, bd = to_dev(x), to_dev(b)
+    extra = {}
+    if xf == 1:
+        w_ln = synth.bf16_bits((1.0 + 0.2 * g.standard_normal(K)).astype(np.float32))
+        b_ln = synth.normal_bf16(g, (K,), 0.1)
+        wd, bld = to_dev(w_ln), to_dev(b_ln)
+        stats = torch.zeros((N, 4), dtype=torch.float32, device="cuda")
+        D.row_stats(xd, N, K, stats)
+    outs = []
+    for cl in (1, cluster):
+        y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+        a = sl.args(xd, y, N, bias=bd, cluster=cl)
+        if xf == 1:
+            a.ln_w, a.ln_b, a.ln_stats, a.ln_parts, a.ln_eps = wd.data_ptr(), bld.data_ptr(), stats.data_ptr(), 1, 1e-5
+        if xf == 2:
+            a.x_swiglu = 1
+        info = D.linear_query(a)
+        assert info["cluster"] == cl
+        D.linear(a)
+        torch.cuda.synchronize()
+        outs.append(from_dev(y))
+    assert np.array_equal(outs[0], outs[1])
+    if xf == 0:
+        ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
+        assert_close(Kx.bf16_to_f64(outs[1]), ref)

@@ -87,6 +87,13 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "mc":  # x multicast within clusters (one fetch per cluster)
+        for (M, K, h, kc, N) in ((7168, 7168, 48, 256, 8), (28672, 7168, 192, 64, 8), (7168, 8192, 48, 256, 64),
+                                 (1024, 8192, 16, 256, 64)):
+            for cl in (1, 2, 4):
+                print(json.dumps(time_cfg(M, K, N, h, kc, pdl=1, n_cta_host=2, congestion_control=1, cluster=cl)),
+                      flush=True)
+        return
     if a.exp == "ln":  # fused pre-norm / stats epilogue cost at the OPT-30B shapes (N = 8)
         for (M, K, h, kc) in ((7168, 7168, 48, 256), (28672, 7168, 192, 64)):
             for pdl in (0, 1):
