@@ -532,8 +532,9 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_attention: tile ring does not fit");
   int stages = c.stages > 0 ? std::min(c.stages, max_stages) : max_stages;
   p.stages = std::max(2, stages);
-  // host CTAs: one CTA keeps ~the link's saturating in-flight volume (calibration); window caps it
-  int n_host = c.n_cta_host > 0 ? c.n_cta_host : 1;
+  // host CTAs (caller-sized: ~one per 8 host units, i.e. one unit per warp; default 2); the
+  // congestion window caps the in-flight host tiles per warp
+  int n_host = c.n_cta_host > 0 ? c.n_cta_host : 2;
   if (!a->k_host) n_host = 0;
   int window = p.stages;
   if (c.window > 0) window = std::min(c.window, p.stages);

@@ -824,7 +824,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
 
   int n_host = 0;
   if (h > 0) {
-    n_host = c.n_cta_host > 0 ? c.n_cta_host : 1;
+    n_host = c.n_cta_host > 0 ? c.n_cta_host : 2;  // 2 CTAs saturate the link (calibration)
     n_host = (int)std::max<long long>(n_host, ceil_div(h, cap));
     n_host = (int)std::min<long long>(n_host, h);
   }

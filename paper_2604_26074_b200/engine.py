@@ -308,7 +308,10 @@ class DakOPT:
         a.page_size, a.max_pages, a.chunk_pages = self.page, self.pages_per_req, self.chunk_pages
         a.tp_rank, a.tp_size = 0, 1
         a.cfg = dak.launch_cfg(**self.launch)
-        a.attn_cfg = dak.launch_cfg(**self.launch)
+        # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
+        n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
+        host_units = self.attn_host_chunks[l] * n_kvh
+        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=max(1, min(16, -(-host_units // 8)))))
         # L2 warm-up chain (dak.h): the last linear of layer l warms the next layer's q (or the head)
         nxt = self.layers[l + 1]["q"] if l + 1 < c.n_layers else self.head
         a.l2_prefetch_bytes = self.l2_prefetch

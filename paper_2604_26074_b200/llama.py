@@ -234,7 +234,10 @@ class DakLlama:
         a.tp_rank, a.tp_size, a.comm = self.rank, self.world, self.comm
         a.fuse_norm = 1
         a.cfg = dak.launch_cfg(**self.launch)
-        a.attn_cfg = dak.launch_cfg(**self.launch)
+        # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
+        n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
+        host_units = self.attn_host_chunks[l] * n_kvh
+        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=max(1, min(16, -(-host_units // 8)))))
         return a
 
     # ------------------------------------------------------------------ the decode step (hot path)
