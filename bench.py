@@ -240,6 +240,9 @@ def main():
     ap.add_argument("--l2-prefetch-mb", type=float, default=0.0, help="L2 warm-up of the next linear (0: off)")
     ap.add_argument("--no-evict-first", action="store_true")
     ap.add_argument("--no-fuse-norm", action="store_true", help="LayerNorm kernels instead of the fused pre-norm")
+    ap.add_argument("--plan-link-gbs", type=float, default=None,
+                    help="host-link rate the planner assumes (default: the calibrated peak)")
+    ap.add_argument("--plan-hbm-gbs", type=float, default=None, help="HBM rate the planner assumes")
     ap.add_argument("--layers", type=int, default=None,
                     help="layers (default: all 48 for OPT-30B; 8 of 80 for the Llama subset, labelled)")
     ap.add_argument("--workload", default="opt30b", choices=["opt30b", "llama3-70b-tp8"],
@@ -256,7 +259,7 @@ def main():
 
     world, rank, local = dist_setup()
     hbm_gbs, link_gbs, peak_src = measured_peaks()
-    hw = HW(hbm_bps=hbm_gbs * 1e9, link_bps=link_gbs * 1e9)
+    hw = HW(hbm_bps=(a.plan_hbm_gbs or hbm_gbs) * 1e9, link_bps=(a.plan_link_gbs or link_gbs) * 1e9)
     llama = a.workload == "llama3-70b-tp8"
     if llama:
         eng, cfg, wl = make_llama(a, hw, world, rank, dak)
@@ -265,13 +268,15 @@ def main():
         cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                     evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
+                     evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, fused_qkv=not a.persistent,
+                     seed=1234 + rank)
         if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
             tot = sum(o["total_bytes"] for o in eng.plan_ops)
             eng.close()
             eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                          congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                         evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, seed=1234 + rank)
+                         evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, fused_qkv=not a.persistent,
+                     seed=1234 + rank)
     if a.persistent:
         eng.enable_persistent_step()
     nb = eng.bytes_per_step()
@@ -324,23 +329,26 @@ def main():
 
     # ---------------- roofline of the dominant kernel (dak_linear), CUDA events on its stream
     lin_bytes, lin_time = 0, 0.0
-    evs = []
     ops = list(eng.linear_ops())
     xs = torch.zeros(eng.B, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
     ys = torch.empty(eng.B, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
-    with torch.cuda.stream(stream):
-        for op in ops:
-            la = dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
-                                 cfg=dict(congestion_control=int(not a.no_cc)))
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record(stream)
-            dak.linear(la, stream)
-            s1.record(stream)
-            evs.append((s0, s1, op.M * op.K * 2 + eng.B * (op.K + op.M) * 2))
-    torch.cuda.synchronize()
-    for s0, s1, b in evs:
-        lin_time += s0.elapsed_time(s1) / 1e3
-        lin_bytes += b
+    largs = [dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
+                             cfg=dict(congestion_control=int(not a.no_cc))) for op in ops]
+    passes = []
+    for _ in range(3):  # every linear launch of a step, each bracketed by events; median of 3 passes
+        evs = []
+        with torch.cuda.stream(stream):
+            for la in largs:
+                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                s0.record(stream)
+                dak.linear(la, stream)
+                s1.record(stream)
+                evs.append((s0, s1))
+        torch.cuda.synchronize()
+        passes.append([s0.elapsed_time(s1) / 1e3 for s0, s1 in evs])
+    for i, op in enumerate(ops):
+        lin_time += statistics.median(p_[i] for p_ in passes)
+        lin_bytes += op.M * op.K * 2 + eng.B * (op.K + op.M) * 2
     lin_achieved = lin_bytes / lin_time / 1e9
     lin_share = lin_time / step_s
     peak = hbm_gbs + link_gbs

@@ -251,6 +251,10 @@ typedef struct {
   int64_t q_row_stride;         /* elements between requests in q (0: Hq*d; fused QKV: (Hq+2Hkv)*d) */
 } dak_attention_args;
 
+/* With cfg.pdl, the block table, seq_lens and the KV rows of tokens < seq_len - 1 are read BEFORE
+ * griddepcontrol.wait (they are step inputs / written by earlier steps), q and the row of the
+ * newest token after it: the kernel immediately preceding may only produce q and that row. */
+
 /* Pure query: workspace bytes (split-KV partials: B*Hkv*ceil(max_pages/chunk_pages)*(Hq/Hkv)*(d+1)*4). */
 dak_status dak_attention_workspace_size(const dak_attention_args* args, size_t* bytes);
 

@@ -176,8 +176,10 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     tstamp(p.trace, 0);
   }
   grid_dep_launch();
-  grid_dep_wait();  // block table, seq_lens and q come from earlier kernels
-  if (threadIdx.x == 0) tstamp(p.trace, 1);
+  // Block table and seq_lens are step inputs, and every KV row except the newest token's was
+  // written by earlier steps: the schedule and those tiles do not wait for the previous kernel
+  // (griddepcontrol.wait). q and the tile holding the new token (position seq_len - 1, written by
+  // the KV-append kernel just before) are read only after it (ABI contract in dak.h).
   // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
   const int n_pairs = p.B * p.max_chunks;
   {  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
@@ -225,6 +227,18 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     uint64_t* we = empty + w * kMaxStages;
     unsigned char* wr = ring + (size_t)w * p.stages * p.stage_bytes;
     int it = 0;
+    bool waited = false;
+    int dq_s[kMaxStages];  // q copies of units whose first tile went out before the wait
+    const __nv_bfloat16* dq_src[kMaxStages];
+    int ndq = 0;
+    const uint32_t q_bytes_unit = (uint32_t)p.G * kD * 2;
+    auto release = [&]() {
+      grid_dep_wait();
+      if (threadIdx.x == 0) tstamp(p.trace, 1);
+      waited = true;
+      for (int i = 0; i < ndq; ++i)
+        bulk_g2s(wr + (size_t)dq_s[i] * p.stage_bytes + 2 * kTileBytes, dq_src[i], q_bytes_unit, &wf[dq_s[i]]);
+    };
     for (int k = my_j + w * my_n; k < n_units; k += stride) {
       const int pr = find_pair(pref, n_pairs, k / p.Hkv);
       const int g = k % p.Hkv;
@@ -232,7 +246,10 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       const int L = p.seq_lens[b];
       const int t0 = c * p.chunk_pages * p.page;
       const int t1 = min(L, t0 + p.chunk_pages * p.page);
+      const __nv_bfloat16* qsrc = p.q + (long long)b * p.q_stride + (long long)g * p.G * kD;
       for (int tok = t0; tok < t1; tok += 16, ++it) {
+        // before the dependency wait: only ring slots never used yet, only tiles of old tokens
+        if (!waited && (it >= slots || tok + 16 > L - 1)) release();
         const int s = it % slots;
         if (it >= slots) mbar_wait(&we[s], ((uint32_t)(it / slots) & 1u) ^ 1u);
         const int pg = tok / p.page, r0 = tok % p.page;
@@ -240,15 +257,23 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
         const long long idx = (long long)(e & ~kHostBit);
         const bool eh = (e & kHostBit) != 0;
         const long long off = (idx * p.Hkv + g) * (long long)page_bytes + (long long)r0 * kD * 2;
-        const uint32_t q_bytes = tok == t0 ? (uint32_t)p.G * kD * 2 : 0u;
+        const uint32_t q_bytes = tok == t0 ? q_bytes_unit : 0u;
         mbar_expect_tx(&wf[s], 2u * kTileBytes + q_bytes);
         unsigned char* dst = wr + (size_t)s * p.stage_bytes;
         bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, kTileBytes, &wf[s]);
         bulk_g2s(dst + kTileBytes, (eh ? p.v_host : p.v_hbm) + off, kTileBytes, &wf[s]);
-        if (q_bytes)
-          bulk_g2s(dst + 2 * kTileBytes, p.q + (long long)b * p.q_stride + (long long)g * p.G * kD, q_bytes, &wf[s]);
+        if (q_bytes) {
+          if (waited) {
+            bulk_g2s(dst + 2 * kTileBytes, qsrc, q_bytes, &wf[s]);
+          } else {  // q is produced by an earlier kernel of this step: after the wait
+            dq_s[ndq] = s;
+            dq_src[ndq] = qsrc;
+            ++ndq;
+          }
+        }
       }
     }
+    if (!waited) release();
     return;
   }
 

@@ -196,7 +196,6 @@ static dak_linear_args lin_args(const dak_weight& w, long long M, long long K, i
 static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_stream_t stream) {
   if (!a->fuse_norm || !a->stats_in || a->stats_in_parts <= 0 || a->ln1_b || a->ln2_b)
     return fail(DAK_EINVAL, "dak_layer (Llama): needs fuse_norm with stats_in and RMSNorm weights without bias");
-  if (!a->split_qkv) return fail(DAK_EINVAL, "dak_layer (Llama): q, k, v must be given separately (split_qkv)");
   if (a->tp_size > 1 && !a->comm) return fail(DAK_EINVAL, "dak_layer (Llama): tp_size > 1 needs comm");
   char* sc = (char*)a->scratch;
   char* qkv = sc + s.qkv;
@@ -214,15 +213,21 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
     l.x = a->x;
     l.ln_w = w; l.ln_b = nullptr; l.ln_rms = 1; l.ln_stats = stats; l.ln_parts = parts; l.ln_eps = a->ln_eps;
   };
-  const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
-  const dak_weight* w[3] = {&a->q, &a->k, &a->v};
-  long long off = 0;
-  for (int i = 0; i < 3; ++i) {
-    dak_linear_args l = lin_args(*w[i], rows[i], H, B, a->x, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
-    l.ldy = qkv_cols;
+  if (a->split_qkv) {  // q, k, v side by side into the [B, qkv_cols] buffer
+    const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
+    const dak_weight* w[3] = {&a->q, &a->k, &a->v};
+    long long off = 0;
+    for (int i = 0; i < 3; ++i) {
+      dak_linear_args l = lin_args(*w[i], rows[i], H, B, a->x, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
+      l.ldy = qkv_cols;
+      rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
+      if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+      off += rows[i];
+    }
+  } else {  // one fused [q; k; v] projection
+    dak_linear_args l = lin_args(a->qkv, qkv_cols, H, B, a->x, qkv, nullptr, DAK_ACT_NONE, a->cfg);
     rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    off += rows[i];
   }
   if ((st = dak_rope_kv_append(qkv, qkv_cols, B, Hq, Hkv, d, a->positions, a->rope_theta, a->block_table, a->page_size,
                                a->max_pages, a->k_hbm, a->v_hbm, a->k_host, a->v_host, pdl, strm)) != DAK_OK)

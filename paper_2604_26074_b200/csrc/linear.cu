@@ -38,7 +38,7 @@ constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
 constexpr int kMaxN = 64;
 constexpr int kRptMax = 16;   // FMA path: rows per thread
 constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
-constexpr int kMaxStages = 8;
+constexpr int kMaxStages = 16;
 constexpr int kSmemBudget = 227 * 1024;
 
 struct __align__(64) Params {
@@ -54,6 +54,7 @@ struct __align__(64) Params {
   int act;
   int n_host, n_hbm;
   int stages, window;
+  int w_stage_host, stages_host;  // host CTAs: dense slots of their (fewer) rows -> a deeper ring
   int w_stage_bytes, x_stage_bytes, n8;
   int off_x, off_ln, res_offset;  // byte offsets (from the 1024-aligned SMEM base)
   long long ldy;   // elements between consecutive rows n of y and residual
@@ -250,19 +251,20 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   const long long row0 = host ? rb : p.h + rb;  // global row of local row 0
   const char* wsrc = host ? p.w_host : p.w_hbm;
   const int slots = host ? p.window : p.stages;
+  const int wstage = host ? p.w_stage_host : p.w_stage_bytes;  // W slot stride of this CTA's ring
   const int kc = p.kc;
   const int nchunks = (int)(p.K / kc);
   const int N = p.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < p.stages; ++s) {
+    for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
     mbar_init(lnbar, 1);
     if (p.mc > 1)
-      for (int s = 0; s < p.stages; ++s) mbar_init(&xempty[s], kConsumerWarps * p.mc);
+      for (int s = 0; s < kMaxStages; ++s) mbar_init(&xempty[s], kConsumerWarps * p.mc);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -294,7 +296,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
       auto load_w = [&](int slot, int i) {
-        unsigned char* dst = wring + (size_t)slot * p.w_stage_bytes;
+        unsigned char* dst = wring + (size_t)slot * wstage;
         const char* s_ = src + (long long)i * chunk_stride;
         if (ef) bulk_g2s_hint(dst, s_, w_bytes, &full[slot], pol);
         else bulk_g2s(dst, s_, w_bytes, &full[slot]);
@@ -383,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
     uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
       mbar_wait(&full[s], ph);
-      const unsigned char* ws = wring + (size_t)s * p.w_stage_bytes;
+      const unsigned char* ws = wring + (size_t)s * wstage;
       const unsigned char* xs = xring + (size_t)s * p.x_stage_bytes;
       float xf[NN][8];
 #pragma unroll
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
     const unsigned char* lnres = smem + p.off_ln;
     if constexpr (XF == 1) {
       grid_dep_wait();
-      float* s_ln = reinterpret_cast<float*>(smem + 256);
+      float* s_ln = reinterpret_cast<float*>(smem + 512);
       for (int n = cw; n < N; n += kConsumerWarps) {
         // batches of 8 independent loads per lane (one L2 round trip per 256 parts); the values
         // stay in registers for the second pass when parts <= 256 (the usual case: one per CTA)
@@ -532,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
     uint32_t ph = 0;
     for (int i = 0; i < nchunks; ++i) {
       mbar_wait(&full[s], ph);
-      const uint32_t ws = wring_u + (uint32_t)s * p.w_stage_bytes + a_base;
+      const uint32_t ws = wring_u + (uint32_t)s * wstage + a_base;
       const uint32_t xs = xring_u + (uint32_t)s * p.x_stage_bytes + b_row;
       for (int j = 0; j < nks; ++j) {
         const int ks = wk + j * WK;
@@ -934,20 +936,40 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   int stages = c.stages > 0 ? std::min(c.stages, max_stages) : max_stages;
   if (stages < 2) stages = 2;
   p.stages = stages;
-  // congestion window (P:L533): in-flight host stages per host CTA. With congestion control the
-  // window is the smallest that keeps ~192 KB in flight on the link (calibrated saturation point,
-  // profiles/r01/calib_loadpath.jsonl); without it every ring slot may be in flight.
-  int window = stages;
+  // host CTAs own fewer rows than HBM CTAs: their slots are packed densely inside the same W ring
+  // region, so the host ring is deeper (more bytes in flight over the link, which needs >= ~256 KB
+  // to saturate; profiles/r01/calib_loadpath.jsonl). MMA tiles read whole rows_alloc groups past a
+  // slot's end: that over-read stays inside the region.
+  p.w_stage_host = p.w_stage_bytes;
+  p.stages_host = stages;
   if (n_host > 0) {
-    if (c.window > 0) window = std::min(c.window, stages);
+    const long long rh = std::min<long long>(rows_alloc, ceil_div(rmax_host, 16) * 16);
+    const long long ws_h = rh * kc * 2;
+    const long long over = (rows_alloc - rh) * kc * 2;
+    const long long region = (long long)stages * p.w_stage_bytes;
+    int sh = (int)std::min<long long>(kMaxStages, (region - over) / ws_h);
+    // the x ring needs as many slots: shrink until the whole layout still fits
+    while (sh > stages && 1024 + region + (long long)sh * p.x_stage_bytes + ln_bytes + res_bytes + 1024 > kSmemBudget) --sh;
+    if (sh > stages) {
+      p.w_stage_host = (int)ws_h;
+      p.stages_host = sh;
+    }
+  }
+  // congestion window (P:L533): in-flight host stages per host CTA. With congestion control the
+  // window is the smallest that keeps ~256 KB in flight on the link (calibrated saturation point);
+  // without it every host ring slot may be in flight.
+  int window = p.stages_host;
+  if (n_host > 0) {
+    if (c.window > 0) window = std::min(c.window, p.stages_host);
     else if (c.congestion_control) {
       const long long hstage = std::max<long long>(1, rmax_host * kc * 2);
-      window = (int)std::min<long long>(stages, std::max<long long>(1, ceil_div(192 * 1024, hstage * n_host)));
+      window = (int)std::min<long long>(p.stages_host, std::max<long long>(1, ceil_div(256 * 1024, hstage * n_host)));
     }
   }
   p.window = std::max(1, window);
+  const int x_slots = std::max(stages, p.stages_host);
   p.off_x = 1024 + stages * p.w_stage_bytes;
-  p.off_ln = p.off_x + stages * p.x_stage_bytes;
+  p.off_ln = p.off_x + x_slots * p.x_stage_bytes;
   p.res_offset = p.off_ln + ln_bytes;
 
   out->p = p;

@@ -80,7 +80,7 @@ class DakOPT:
                  y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 16, seed: int = 0,
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
                  host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
-                 evict_first: bool = True, fuse_norm: bool = True):
+                 evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
         self.pdl = int(pdl)
@@ -89,19 +89,26 @@ class DakOPT:
                            l2_policy=0 if evict_first else 1)
         self.l2_prefetch = int(l2_prefetch)
         self.fuse_norm = bool(fuse_norm)
+        # one [q; k; v] projection per layer (one launch reading x once); the persistent step and
+        # the paper's op list use the three projections separately
+        self.fused_qkv = bool(fused_qkv)
         self.sms = dak.device_sms()
         self.gen = torch.Generator(device="cuda")
         self.gen.manual_seed(seed)
         self._host_blocks = []
         c = cfg
         self.layers = []
-        for i in range(c.n_layers):  # q/k/v/o separate, as the paper's op list (P:L981 footnote)
-            self.layers.append(dict(q=LinearOp(f"L{i}.q", c.n_heads * c.head_dim, c.hidden),
-                                    k=LinearOp(f"L{i}.k", c.n_kv_heads * c.head_dim, c.hidden),
-                                    v=LinearOp(f"L{i}.v", c.n_kv_heads * c.head_dim, c.hidden),
-                                    o=LinearOp(f"L{i}.o", c.hidden, c.n_heads * c.head_dim),
-                                    up=LinearOp(f"L{i}.fc1", c.ffn, c.hidden),
-                                    down=LinearOp(f"L{i}.fc2", c.hidden, c.ffn)))
+        for i in range(c.n_layers):
+            if self.fused_qkv:
+                L = dict(qkv=LinearOp(f"L{i}.qkv", (c.n_heads + 2 * c.n_kv_heads) * c.head_dim, c.hidden))
+            else:  # q/k/v separate, as the paper's op list (P:L981 footnote)
+                L = dict(q=LinearOp(f"L{i}.q", c.n_heads * c.head_dim, c.hidden),
+                         k=LinearOp(f"L{i}.k", c.n_kv_heads * c.head_dim, c.hidden),
+                         v=LinearOp(f"L{i}.v", c.n_kv_heads * c.head_dim, c.hidden))
+            L.update(o=LinearOp(f"L{i}.o", c.hidden, c.n_heads * c.head_dim),
+                     up=LinearOp(f"L{i}.fc1", c.ffn, c.hidden),
+                     down=LinearOp(f"L{i}.fc2", c.hidden, c.ffn))
+            self.layers.append(L)
         self.head = LinearOp("head", c.vocab, c.hidden)
         self.pages_per_req = -(-context // page_size)
         self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
@@ -113,7 +120,10 @@ class DakOPT:
     # ------------------------------------------------------------------ planning
     def linear_ops(self):
         for L in self.layers:
-            yield from (L["q"], L["k"], L["v"], L["o"], L["up"], L["down"])
+            if self.fused_qkv:
+                yield from (L["qkv"], L["o"], L["up"], L["down"])
+            else:
+                yield from (L["q"], L["k"], L["v"], L["o"], L["up"], L["down"])
         yield self.head
 
     def kv_bytes_per_layer(self) -> int:
@@ -180,7 +190,10 @@ class DakOPT:
         if weights:  # a fused [q;k;v] weight may be given: split it into the three projections
             weights = dict(weights)
             for i in range(c.n_layers):
-                if f"L{i}.qkv" in weights:
+                if self.fused_qkv and f"L{i}.qkv" not in weights:
+                    weights[f"L{i}.qkv"] = torch.cat([weights.pop(f"L{i}.{k}") for k in ("q", "k", "v")])
+                    weights[f"L{i}.qkv.b"] = torch.cat([weights.pop(f"L{i}.{k}.b") for k in ("q", "k", "v")])
+                if not self.fused_qkv and f"L{i}.qkv" in weights:
                     Wf, bf = weights.pop(f"L{i}.qkv"), weights.pop(f"L{i}.qkv.b")
                     r0 = 0
                     for key in ("q", "k", "v"):
@@ -296,8 +309,12 @@ class DakOPT:
         a.model, a.B, a.hidden, a.n_heads, a.n_kv_heads = dak.MODEL_OPT, self.B, c.hidden, c.n_heads, c.n_kv_heads
         a.head_dim, a.ffn, a.ln_eps = c.head_dim, c.ffn, 1e-5
         a.o, a.up, a.down = L["o"].weight(), L["up"].weight(), L["down"].weight()
-        a.split_qkv = 1
-        a.q, a.k, a.v = L["q"].weight(), L["k"].weight(), L["v"].weight()
+        if self.fused_qkv:
+            a.split_qkv = 0
+            a.qkv = L["qkv"].weight()
+        else:
+            a.split_qkv = 1
+            a.q, a.k, a.v = L["q"].weight(), L["k"].weight(), L["v"].weight()
         a.ln1_w, a.ln1_b = L["ln1_w"].data_ptr(), L["ln1_b"].data_ptr()
         a.ln2_w, a.ln2_b = L["ln2_w"].data_ptr(), L["ln2_b"].data_ptr()
         a.x = self.x.data_ptr()
@@ -313,7 +330,7 @@ class DakOPT:
         host_units = self.attn_host_chunks[l] * n_kvh
         a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=max(1, min(16, -(-host_units // 8)))))
         # L2 warm-up chain (dak.h): the last linear of layer l warms the next layer's q (or the head)
-        nxt = self.layers[l + 1]["q"] if l + 1 < c.n_layers else self.head
+        nxt = self.layers[l + 1]["qkv" if self.fused_qkv else "q"] if l + 1 < c.n_layers else self.head
         a.l2_prefetch_bytes = self.l2_prefetch
         if nxt.hbm is not None:
             a.next_w_hbm, a.next_w_hbm_bytes = nxt.hbm.data_ptr(), (nxt.M - nxt.h) * nxt.K * 2
@@ -421,12 +438,15 @@ class DakOPT:
     def kernels_per_step(self) -> int:
         if getattr(self, "use_step", False):
             return 1
-        per_layer = 8 + (1 if self.chunks_per_req > 1 else 0)  # q k v append attn [combine] o fc1 fc2
+        # [q k v | qkv] append attn [combine] o fc1 fc2
+        per_layer = (6 if self.fused_qkv else 8) + (1 if self.chunks_per_req > 1 else 0)
         if self.fuse_norm:
             return 1 + per_layer * self.cfg.n_layers + 1
         return 1 + (per_layer + 2) * self.cfg.n_layers + 2
 
     def enable_persistent_step(self):
+        if self.fused_qkv:
+            raise ValueError("the persistent step program uses separate q/k/v projections: fused_qkv=False")
         self.build_step_program()
         self.use_step = True
 

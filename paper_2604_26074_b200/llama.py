@@ -60,8 +60,8 @@ class DakLlama:
         nh, nkv, F = self.dims["n_heads"], self.dims["n_kv"], self.dims["ffn"]
         self.layers = []
         for i in range(c.n_layers):
-            self.layers.append(dict(q=LinearOp(f"L{i}.q", nh * d, c.hidden), k=LinearOp(f"L{i}.k", nkv * d, c.hidden),
-                                    v=LinearOp(f"L{i}.v", nkv * d, c.hidden), o=LinearOp(f"L{i}.o", c.hidden, nh * d),
+            self.layers.append(dict(qkv=LinearOp(f"L{i}.qkv", (nh + 2 * nkv) * d, c.hidden),
+                                    o=LinearOp(f"L{i}.o", c.hidden, nh * d),
                                     up=LinearOp(f"L{i}.gate_up", 2 * F, c.hidden),
                                     down=LinearOp(f"L{i}.down", c.hidden, F)))
         self.head = LinearOp("lm_head", self.dims["vocab"], c.hidden)
@@ -75,7 +75,7 @@ class DakLlama:
     # ------------------------------------------------------------------ planning
     def linear_ops(self):
         for L in self.layers:
-            yield from (L["q"], L["k"], L["v"], L["o"], L["up"], L["down"])
+            yield from (L["qkv"], L["o"], L["up"], L["down"])
         yield self.head
 
     def _plan(self, mode, y_req):
@@ -97,7 +97,7 @@ class DakLlama:
             n_host = min(self.n_cta_host, op.h) if op.h > 0 else 0
             rows = max(-(-op.h // max(n_host, 1)) if op.h else 0, -(-(op.M - op.h) // (self.sms - n_host)))
             op.kc = dak.step_choose_kc(rows, op.K)
-        n_lin = 6 * c.n_layers + 1
+        n_lin = 4 * c.n_layers + 1
         self.attn_host_chunks = [plan[n_lin + l]["host_units"] for l in range(c.n_layers)]
         return plan
 
@@ -133,6 +133,8 @@ class DakLlama:
                     W = None
                 elif key == "up":
                     W = torch.cat([loc[f"L{i}.gate"], loc[f"L{i}.up"]], dim=0)
+                elif key == "qkv":
+                    W = torch.cat([loc[f"L{i}.q"], loc[f"L{i}.k"], loc[f"L{i}.v"]], dim=0)
                 else:
                     W = loc[f"L{i}.{key}"]
                 self._fill_linear(op, W)
@@ -221,8 +223,8 @@ class DakLlama:
         a.model, a.B, a.hidden = dak.MODEL_LLAMA, self.B, c.hidden
         a.n_heads, a.n_kv_heads, a.head_dim, a.ffn = self.dims["n_heads"], self.dims["n_kv"], c.head_dim, self.dims["ffn"]
         a.ln_eps, a.rope_theta = c.rms_eps, c.rope_theta
-        a.split_qkv = 1
-        a.q, a.k, a.v = L["q"].weight(), L["k"].weight(), L["v"].weight()
+        a.split_qkv = 0
+        a.qkv = L["qkv"].weight()
         a.o, a.up, a.down = L["o"].weight(), L["up"].weight(), L["down"].weight()
         a.ln1_w, a.ln2_w = L["ln1_w"].data_ptr(), L["ln2_w"].data_ptr()
         a.x = self.x.data_ptr()
@@ -253,7 +255,7 @@ class DakLlama:
         dak.linear(ha, stream)
 
     def kernels_per_step(self) -> int:
-        per_layer = 8 + (1 if self.chunks_per_req > 1 else 0) + (2 if self.comm else 0)  # + residual kernels
+        per_layer = 6 + (1 if self.chunks_per_req > 1 else 0) + (2 if self.comm else 0)  # + residual kernels
         return 1 + per_layer * self.cfg.n_layers + 1
 
     def capture(self, stream: torch.cuda.Stream):

@@ -30,9 +30,10 @@ def _engine_weights(p, L, torch):
     return w
 
 
-@pytest.mark.parametrize("persistent,fuse", [(False, True), (False, False), (True, True)])
+@pytest.mark.parametrize("persistent,fuse,fused_qkv", [(False, True, True), (False, True, False), (False, False, True),
+                                                      (True, True, False)])
 @pytest.mark.parametrize("frac,B,ctx", [(0.0, 3, 70), (0.2, 3, 70), (0.5, 2, 200)])
-def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse):
+def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse, fused_qkv):
     import torch
     from paper_2604_26074_b200 import dak
     from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
@@ -43,7 +44,7 @@ def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse):
     hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
     total = sum(o for o in [3 * H * H, H * H, F * H, H * F]) * 2 * L + V * H * 2
     eng = DakOPT(cfg, B, ctx, hw, mode=dak.PLAN_EXACT, y_req=int(frac * total), page_size=64, chunk_pages=1,
-                 weights=_engine_weights(p, L, torch), fuse_norm=fuse)
+                 weights=_engine_weights(p, L, torch), fuse_norm=fuse, fused_qkv=fused_qkv)
     if frac > 0:
         assert sum(op.h for op in eng.linear_ops()) > 0
     Kc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]

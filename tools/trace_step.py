@@ -15,7 +15,7 @@ from paper_2604_26074_b200.engine import DakOPT, HW, OPTConfig  # noqa: E402
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 8
 batch = int(sys.argv[2]) if len(sys.argv) > 2 else 8
 cfg = OPTConfig(n_layers=layers)
-eng = DakOPT(cfg, batch, 64, HW(hbm_bps=6555.5e9, link_bps=51.5e9), mode=dak.PLAN_BALANCED)
+eng = DakOPT(cfg, batch, 64, HW(hbm_bps=6555.5e9, link_bps=51.5e9), mode=dak.PLAN_BALANCED, fused_qkv=False)
 eng.enable_persistent_step()
 plan = eng.step_plan
 G, n_ops = plan.grid, plan.n_ops
