@@ -26,6 +26,7 @@ SOURCES = [
     ("linear.cu", ["-DDAK_LINEAR_PART=2"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=3"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=4"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=5"]),
     ("attention.cu", []),
     ("layer.cu", []),
     ("step.cu", []),

@@ -65,6 +65,8 @@ struct __align__(64) Params {
   int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
   int swiglu;       // x = [gate | up] ([N, 2K]); the operand is silu(gate) * up
   int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
+  int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
+  uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
   const __nv_bfloat16* ln_w;
   const __nv_bfloat16* ln_b;
@@ -75,6 +77,15 @@ struct __align__(64) Params {
   float* stats_out;  // epilogue row statistics (count, mean, M2) of this CTA's outputs (nullable)
   unsigned long long* trace;  // dak_trace_enable slot (nullable)
 };
+
+// Row range of CTA j of n in a tier of R rows, in units of g rows (sizes differ by <= one unit).
+__host__ __device__ __forceinline__ void tier_rows(long long R, long long j, long long n, int g, long long* rb,
+                                                   long long* re) {
+  const long long U = (R + g - 1) / g;
+  const long long b = (j * U / n) * g, e = ((j + 1) * U / n) * g;
+  *rb = b < R ? b : R;
+  *re = e < R ? e : R;
+}
 
 __device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
   if (tr && blockIdx.x < kTraceCtas) {
@@ -244,8 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   {
     const long long j = host ? cta : cta - p.n_host;
     const long long n = host ? p.n_host : p.n_hbm;
-    rb = j * R_tier / n;
-    re = (j + 1) * R_tier / n;
+    tier_rows(R_tier, j, n, p.rgran, &rb, &re);
   }
   const int R = (int)(re - rb);
   const long long row0 = host ? rb : p.h + rb;  // global row of local row 0
@@ -692,6 +702,210 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   if (p.mc > 1) cluster_sync();
 }
 
+// ------------------------------------------------------------------------------------ tcgen05 path
+// PATH 3 (large N, BASELINE C3's b64 decode and beyond): the same producer and ring, but the
+// dot products run on the 5th-gen tensor cores. One elected thread issues
+// tcgen05.mma.cta_group::1.kind::f16 (M = 128 weight rows x N = n8 batch columns x K = 16) with
+// both operands read from SMEM through descriptors, accumulating in TMEM; tcgen05.commit releases
+// each ring slot; four epilogue warps move the accumulators TMEM -> registers (tcgen05.ld) for the
+// bias / residual / bf16 epilogue. Operand layouts are the canonical K-major SWIZZLE_128B ones:
+// KC = 64 makes a W stage rows x 128 B with 16-byte chunks XOR-swizzled by (row & 7) -- exactly
+// DAK-KC when CTA row ranges start on multiples of 8 (rgran = 8) -- and the x box is the TMA's
+// 128B-swizzled [n8][64]. Rows beyond R in an M = 128 tile read neighbouring SMEM; their TMEM lanes
+// are never stored.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);  // start address (16-byte units)
+  d |= (uint64_t)1 << 16;                            // leading byte offset (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;                  // stride byte offset: 8-row groups 1 KB apart
+  d |= (uint64_t)1 << 46;                            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                            // SWIZZLE_128B
+  return d;
+}
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+
+template <int NT>  // x rows padded to n8 = 8 NT (NT in 2, 4, 8): MMA N = n8
+__global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* done = empty + kMaxStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
+  unsigned char* wring = smem + 1024;
+  unsigned char* xring = smem + p.off_x;
+  constexpr int N8 = 8 * NT;
+
+  const int cta = blockIdx.x;
+  const bool host = cta < p.n_host;
+  long long rb, re;
+  const long long R_tier = host ? p.h : p.M - p.h;
+  tier_rows(R_tier, host ? cta : cta - p.n_host, host ? p.n_host : p.n_hbm, p.rgran, &rb, &re);
+  const int R = (int)(re - rb);
+  const long long row0 = host ? rb : p.h + rb;
+  const char* wsrc = host ? p.w_host : p.w_hbm;
+  const int slots = host ? p.window : p.stages;
+  const int wstage = host ? p.w_stage_host : p.w_stage_bytes;
+  const int nchunks = (int)(p.K / 64);
+  const int N = p.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mtiles = (R + 127) >> 7;
+  const uint32_t tcols = p.tmem_cols;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1 && R > 0) {  // TMEM accumulator: mtiles x N8 columns (power of two >= 32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) tstamp(p.trace, 0);
+  grid_dep_launch();
+  if (R <= 0) return;
+  const uint32_t tmem = *tslot;
+  const uint32_t w_bytes = (uint32_t)R * 128;
+  const uint32_t x_tx = (uint32_t)p.x_stage_bytes;
+  const long long chunk_stride = R_tier * 128;
+
+  if (warp == 0) {
+    if (lane == 0) {  // producer: W span + x box per 64-column stage
+      const int pro = min(slots, nchunks);
+      const char* src = wsrc + rb * 128;
+      const uint64_t pol = policy_evict_first();
+      const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      for (int i = 0; i < pro; ++i) {
+        mbar_expect_tx(&full[i], w_bytes + x_tx);
+        bulk_g2s_hint(wring + (size_t)i * wstage, src + (long long)i * chunk_stride, w_bytes, &full[i], pol);
+      }
+      grid_dep_wait();
+      tstamp(p.trace, 1);
+      for (int i = 0; i < pro; ++i) tma_3d(xring + (size_t)i * p.x_stage_bytes, xmap, 0, 0, i, &full[i]);
+      int s = pro == slots ? 0 : pro;
+      uint32_t ph = pro == slots ? 1u : 0u;
+      for (int i = pro; i < nchunks; ++i) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], w_bytes + x_tx);
+        bulk_g2s_hint(wring + (size_t)s * wstage, src + (long long)i * chunk_stride, w_bytes, &full[s], pol);
+        tma_3d(xring + (size_t)s * p.x_stage_bytes, xmap, 0, 0, i, &full[s]);
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer: the whole warp walks the ring (converged), one elected lane issues
+    {
+      // kind::f16 instruction descriptor: D f32, A / B bf16, both K-major, N = N8, M = 128
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N8 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      const uint32_t wr = su32(wring), xr = su32(xring);
+      uint32_t leader;
+      asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nchunks; ++i) {
+        mbar_wait(&full[s], ph);
+        tc_fence_after();
+        if (leader) {
+          const uint32_t ws = wr + (uint32_t)s * wstage, xs = xr + (uint32_t)s * p.x_stage_bytes;
+          // 4 x K=16 per 128-byte row, each k-step into its OWN accumulator: consecutive MMAs into
+          // one accumulator form a dependent chain (~140 cycles each, measured) that small-N tiles
+          // cannot hide; four independent chains are summed in fixed order by the epilogue
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t bd = umma_desc_sw128(xs + k * 32);
+            for (int mt = 0; mt < mtiles; ++mt)
+              umma_bf16(tmem + (uint32_t)((k * mtiles + mt) * N8), umma_desc_sw128(ws + mt * 128 * 128 + k * 32), bd,
+                        idesc, i != 0);
+          }
+          umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
+        }
+        __syncwarp();
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+      if (leader) umma_commit(done);
+      __syncwarp();
+    }
+  } else if (warp >= 4 && warp < 8) {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = rows of the M tile. One thread polls
+    // `done` with back-off, the others sleep on a named barrier: 128 threads spinning on an
+    // mbarrier for the whole kernel slowed the producer / MMA barrier traffic 3x (measured).
+    if (threadIdx.x == 128) {
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(su32(done)), "r"(0u)
+            : "memory");
+        if (!ok) __nanosleep(256);
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    tc_fence_after();
+    grid_dep_wait();  // residual / y may belong to the previous kernel
+    const int q = warp & 3;
+    for (int mt = 0; mt < mtiles; ++mt) {
+      const int r = mt * 128 + 32 * q + lane;
+      const long long m = row0 + r;
+      const float bias = (r < R && p.bias) ? __bfloat162float(p.bias[m]) : 0.f;
+#pragma unroll
+      for (int c0 = 0; c0 < N8; c0 += 8) {
+        float acc[8];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // fixed-order sum of the four k-chains
+          uint32_t v[8];
+          tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)((k * mtiles + mt) * N8 + c0), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = k == 0 ? __uint_as_float(v[e]) : acc[e] + __uint_as_float(v[e]);
+        }
+        if (r < R) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int n = c0 + e;
+            if (n < N) {
+              float o = acc[e] + bias;
+              if (p.act == DAK_ACT_RELU) o = fmaxf(o, 0.f);
+              if (p.residual) o += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
+              p.y[(long long)n * p.ldy + m] = __float2bfloat16_rn(o);
+            }
+          }
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (threadIdx.x == 32 && p.trace) tstamp(p.trace, 3);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+
 #if DAK_LINEAR_PART == 0
 // ------------------------------------------------------------------------------------ packing
 // dst[c][r][kc] with 16-byte chunk sl of row r stored at swz(r, sl); one thread per 16 B.
@@ -811,17 +1025,27 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   // default: tensor-core path for every N (the CUDA-core FMA loop cannot issue fast enough to
   // keep up with HBM); force_path 1 selects it for N <= 4.
+  // default: tensor cores for every N -- mma.sync (path 2) up to N = 16; tcgen05 (path 3) beyond,
+  // where mma.sync becomes issue-bound, when its operand constraints hold
   int path = c.force_path ? c.force_path : 2;
+  if (!c.force_path && N > 16 && kc == 64 && !a->ln_w && !a->x_swiglu && !a->stats_out && c.cluster <= 1 && h % 8 == 0)
+    path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
-  if (path != 1 && path != 2) return fail(DAK_EINVAL, "dak_linear: bad force_path");
+  if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
+  if (path == 3) {  // tcgen05: canonical SWIZZLE_128B K-major operands need KC = 64; plain GEMV only
+    if (kc != 64) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path needs kc = 64");
+    if (a->ln_w || a->x_swiglu || a->stats_out) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path has no operand transforms / statistics");
+  }
+  const int nt_eff = path == 3 ? std::max(2, nt) : nt;  // tcgen05 M = 128 needs N >= 16
+  const int rg = path == 3 ? 8 : 1;                     // 8-row swizzle atoms per CTA range
   // rows per CTA are bounded by the accumulator capacity of the path and by SMEM: at least three
   // ring stages of (rows x KC) weights plus the x rows must fit (deep enough to cover HBM latency)
   if (a->x_swiglu && (path != 2 || a->ln_w)) return fail(DAK_EINVAL, "dak_linear: x_swiglu needs the tensor-core path and no pre-norm");
-  const int n8 = path == 1 ? 8 : nt * 8;
+  const int n8 = path == 1 ? 8 : nt_eff * 8;
   const long long x_stage = (long long)n8 * kc * 2 * (a->x_swiglu ? 2 : 1);
   const long long smem_rows = ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
   if (path == 1 && kc > 8 * kConsumers) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path needs kc <= %d", 8 * kConsumers);
-  const long long cap = std::min(path_row_cap(path, kc, nt), smem_rows);
+  const long long cap = std::min(path == 3 ? 256LL : path_row_cap(path, kc, nt), smem_rows);
   if (cap < 16) return fail(DAK_EUNSUPPORTED, "dak_linear: kc=%d leaves no room for a 16-row stage", kc);
 
   int n_host = 0;
@@ -840,6 +1064,11 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   int mc = c.cluster > 1 ? c.cluster : 1;
   if (mc != 1 && mc != 2 && mc != 4) return fail(DAK_EINVAL, "dak_linear: cluster must be 0, 1, 2 or 4");
   if (mc > 1 && path != 2) mc = 1;
+  if (rg > 1) {  // every CTA owns whole 8-row units
+    n_host = (int)std::min<long long>(n_host, ceil_div(h, rg));
+    n_hbm = (int)std::min<long long>(n_hbm, ceil_div(M - h, rg));
+    if (h > 0 && h % rg) return fail(DAK_EINVAL, "dak_linear: the tcgen05 path needs h %% 8 == 0");
+  }
   if (mc > 1) {
     const int nh2 = n_host ? (int)ceil_div(n_host, mc) * mc : 0;
     int ng2 = n_hbm ? std::max(mc, n_hbm / mc * mc) : 0;
@@ -856,8 +1085,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       mc = 1;
     }
   }
-  const long long rmax_host = n_host ? ceil_div(h, n_host) : 0;
-  const long long rmax_hbm = n_hbm ? ceil_div(M - h, n_hbm) : 0;
+  const long long rmax_host = n_host ? ceil_div(ceil_div(h, rg), n_host) * rg : 0;
+  const long long rmax_hbm = n_hbm ? ceil_div(ceil_div(M - h, rg), n_hbm) * rg : 0;
   const long long rmax = std::max(rmax_host, rmax_hbm);
   if (rmax > cap) return fail(DAK_EUNSUPPORTED, "dak_linear: %lld rows per CTA exceed the path capacity %lld (use a smaller kc)", rmax, cap);
 
@@ -868,6 +1097,9 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     const int G = kConsumers / (kc / 8);
     bucket = bucket_of(kRptBuckets, 5, ceil_div(rmax, G));
     rows_alloc = ceil_div(rmax, 16) * 16;
+  } else if (path == 3) {
+    bucket = 1;
+    rows_alloc = ceil_div(rmax, 8) * 8;
   } else {
     // warps split K first (the split depends on KC only, so the summation order of a row does
     // not depend on how many rows its CTA owns: bitwise r-invariance); leftover warps split M
@@ -900,6 +1132,11 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
   p.n_host = n_host; p.n_hbm = n_hbm;
   p.wm = wm; p.wk = wk;
+  p.rgran = rg;
+  if (path == 3) {
+    const int cols = 4 * (int)ceil_div(rmax, 128) * n8;  // four k-chain accumulators
+    p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+  }
   p.mc = mc;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
   p.n8 = n8;
@@ -926,7 +1163,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   const int W2 = (path == 1 && kc / 8 > 32) ? kc / 8 / 32 : 1;
   // MMA path: one partial slot per k-warp when they fit in 48 KB (one barrier), else serial rounds
   p.red_slots = (path == 2 && wk > 1 && (long long)wk * rmax * N * 4 <= 48 * 1024) ? wk : 1;
-  const int res_bytes = (int)(ceil_div((long long)std::max(W2, p.red_slots) * rmax * N * 4, 128) * 128);
+  // tcgen05 path: no SMEM results; 16 KB of slack for the M = 128 tile reads past a slot
+  const int res_bytes = path == 3 ? 16 * 1024 : (int)(ceil_div((long long)std::max(W2, p.red_slots) * rmax * N * 4, 128) * 128);
   const int per_stage = p.w_stage_bytes + p.x_stage_bytes;
   // SMEM (from a 1024-aligned base; +1 KB for the alignment pad): [1 KB barriers + LN stats]
   // [stages x W span][stages x x box][LN weight, bias][fp32 results]
@@ -974,7 +1212,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
 
   out->p = p;
   out->path = path;
-  out->nn = path == 1 ? N : nt;
+  out->nn = path == 1 ? N : nt_eff;
   out->bucket = bucket;
   out->grid = n_host + n_hbm;
   out->smem = p.res_offset + res_bytes + 1024;
@@ -1081,6 +1319,7 @@ dak_status launch_part_nt1(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt2(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl);
 #if DAK_LINEAR_PART == 0
 dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl) {
   switch (pl.nn) {
@@ -1099,12 +1338,43 @@ dak_status launch_part_nt2(const Plan& pl, cudaStream_t s, int pdl) { return lau
 dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<4>(pl, s, pdl); }
 #elif DAK_LINEAR_PART == 4
 dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<8>(pl, s, pdl); }
+#elif DAK_LINEAR_PART == 5
+template <int NT>
+static dak_status launch_umma_t(const Plan& pl, cudaStream_t stream, int pdl) {
+  auto kern = umma_linear_kernel<NT>;
+  static int smem_set = 0;
+  if (!smem_set) {
+    DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    smem_set = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pl.p));
+  return DAK_OK;
+}
+dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
+  switch (pl.nn) {
+    case 2: return launch_umma_t<2>(pl, s, pdl);
+    case 4: return launch_umma_t<4>(pl, s, pdl);
+    case 8: return launch_umma_t<8>(pl, s, pdl);
+  }
+  return fail(DAK_EUNSUPPORTED, "dak_linear: no tcgen05 kernel instance for %d n8 tiles", pl.nn);
+}
 #endif
 
 #if DAK_LINEAR_PART == 0
 static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
   if (pl.path == 1) return launch_part_fma(pl, s, pdl);
+  if (pl.path == 3) return launch_part_umma(pl, s, pdl);
   switch (pl.nn) {
     case 1: return launch_part_nt1(pl, s, pdl);
     case 2: return launch_part_nt2(pl, s, pdl);
@@ -1187,9 +1457,11 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
   const long long j = host ? cta : cta - pl.p.n_host;
   const long long n = host ? pl.p.n_host : pl.p.n_hbm;
   const long long off = host ? 0 : args->h;
+  long long rb, re;
+  lin::tier_rows(R, j, n, pl.p.rgran, &rb, &re);
   *tier = host ? 1 : 0;
-  *row_begin = off + j * R / n;
-  *row_end = off + (j + 1) * R / n;
+  *row_begin = off + rb;
+  *row_end = off + re;
   return DAK_OK;
 }
 

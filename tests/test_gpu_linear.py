@@ -228,3 +228,31 @@ def test_linear_x_multicast_bitwise(D, torch, M, K, N, h, kc, xf, cluster):
     if xf == 0:
         ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
         assert_close(Kx.bf16_to_f64(outs[1]), ref)
+
+
+@pytest.mark.parametrize("M,K,N,h", [(1024, 8192, 64, 32), (3584, 4096, 32, 0), (7168, 7168, 16, 56),
+                                     (1000, 2048, 40, 16), (300, 1024, 64, 296), (28672, 1024, 64, 224)])
+def test_linear_tcgen05_path(D, torch, M, K, N, h):
+    """force_path = 3: tcgen05.mma (M=128 x N x K=16, TMEM accumulators) on SWIZZLE_128B SMEM operands
+    (KC = 64), against the oracle."""
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(10, M + N), bias=True)
+    y, sl, a = run_linear(D, torch, W, x, h, 64, bias=b, force_path=3)
+    assert D.linear_query(a)["path"] == 3
+    ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y), ref)
+
+
+def test_linear_tcgen05_r_invariance_and_integer_exact(D, torch):
+    """Integer inputs: exact sums -> bitwise equal to the oracle's RNE rounding; the output is the
+    same bitwise for every split point (tier / CTA partition)."""
+    M, K, N = 2000, 2048, 48
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(10, 5), kind="int")
+    outs = []
+    for h in (0, 64, 1000, 2000):
+        y, _, _ = run_linear(D, torch, W, x, h, 64, force_path=3)
+        outs.append(y)
+    ref = Kx.split_linear(W[:0], W, x)
+    assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(ref))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])

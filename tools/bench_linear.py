@@ -87,6 +87,17 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "tc":  # tcgen05 (path 3, kc 64) vs mma.sync (path 2) at growing N
+        for (M, K) in ((7168, 8192), (28672, 7168), (1024, 8192)):
+            for N in (8, 16, 32, 64):
+                for path in (2, 3):
+                    kc = 64 if path == 3 else dak.default_kc(M, K, 147)
+                    try:
+                        r = time_cfg(M, K, N, 0, kc, pdl=1, force_path=path)
+                        print(json.dumps(r), flush=True)
+                    except Exception as e:  # noqa: BLE001
+                        print(json.dumps(dict(M=M, K=K, N=N, path=path, error=str(e))), flush=True)
+        return
     if a.exp == "mc":  # x multicast within clusters (one fetch per cluster)
         for (M, K, h, kc, N) in ((7168, 7168, 48, 256, 8), (28672, 7168, 192, 64, 8), (7168, 8192, 48, 256, 64),
                                  (1024, 8192, 16, 256, 64)):
