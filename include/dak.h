@@ -148,7 +148,7 @@ typedef struct {
   int32_t congestion_control; /* 1: cap host CTAs / window as calibrated          */
   int32_t pdl;                /* 1: programmatic dependent launch (weights stream before the   */
                               /*    previous kernel finishes; x/residual read after it)        */
-  int32_t force_path;         /* 0 auto, 1 CUDA-core FMA path, 2 tensor-core (mma.sync) path   */
+  int32_t force_path;         /* 0 auto, 1 CUDA-core FMA, 2 mma.sync, 3 tcgen05 (kc == 64)     */
   int32_t l2_policy;          /* 0: stream weights/KV with the L2 evict_first hint (they are   */
                               /*    read once per step), 1: no hint                              */
   int32_t cluster;            /* dak_linear: CTAs per thread-block cluster sharing ONE fetch of */
@@ -162,7 +162,7 @@ typedef struct {
   const void* w_hbm;    /* DAK-KC packed rows [h,M)   (device; may be NULL when h == M)       */
   int64_t M, K, h;      /* 0 <= h <= M                                                         */
   int32_t kc;           /* KC used to pack both tiers                                          */
-  int32_t N;            /* batch columns, 1..64                                                */
+  int32_t N;            /* batch columns, 1..64 (1..256 on the tcgen05 path: kc == 64)         */
   const void* x;        /* [N, K] bf16 row-major, device                                       */
   void* y;              /* [N, M] bf16 row-major, device                                       */
   const void* bias;     /* [M] bf16 or NULL                                                    */

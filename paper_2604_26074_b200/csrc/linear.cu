@@ -35,7 +35,8 @@ namespace lin {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
-constexpr int kMaxN = 64;
+constexpr int kMaxN = 64;     // mma.sync paths
+constexpr int kMaxNTc = 256;  // tcgen05 path (one MMA covers N <= 256)
 constexpr int kRptMax = 16;   // FMA path: rows per thread
 constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
 constexpr int kMaxStages = 16;
@@ -750,6 +751,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   unsigned char* wring = smem + 1024;
   unsigned char* xring = smem + p.off_x;
   constexpr int N8 = 8 * NT;
+  constexpr int KCH = N8 >= 128 ? 1 : 4;  // independent k-chains (large N keeps one chain busy)
 
   const int cta = blockIdx.x;
   const bool host = cta < p.n_host;
@@ -837,8 +839,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
           for (int k = 0; k < 4; ++k) {
             const uint64_t bd = umma_desc_sw128(xs + k * 32);
             for (int mt = 0; mt < mtiles; ++mt)
-              umma_bf16(tmem + (uint32_t)((k * mtiles + mt) * N8), umma_desc_sw128(ws + mt * 128 * 128 + k * 32), bd,
-                        idesc, i != 0);
+              umma_bf16(tmem + (uint32_t)(((k % KCH) * mtiles + mt) * N8), umma_desc_sw128(ws + mt * 128 * 128 + k * 32),
+                        bd, idesc, (KCH == 4 ? i : (i | k)) != 0);
           }
           umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
         }
@@ -875,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       for (int c0 = 0; c0 < N8; c0 += 8) {
         float acc[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {  // fixed-order sum of the four k-chains
+        for (int k = 0; k < KCH; ++k) {  // fixed-order sum of the k-chains
           uint32_t v[8];
           tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)((k * mtiles + mt) * N8 + c0), v);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -1006,8 +1008,9 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   const int N = a->N, kc = a->kc;
   if (M <= 0 || K <= 0 || N <= 0) return fail(DAK_EINVAL, "dak_linear: M, K, N must be positive");
   if (h < 0 || h > M) return fail(DAK_EINVAL, "dak_linear: h must be in [0, M]");
-  if (N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d (tcgen05 large-N path not in this build)", N, kMaxN);
-  const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : 8));  // n8 tiles (compiled: 1, 2, 4, 8)
+  if (N > kMaxNTc) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d", N, kMaxNTc);
+  // n8 tiles (compiled: 1, 2, 4, 8 on every path; 16, 32 on the tcgen05 path)
+  const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : (N <= 64 ? 8 : (N <= 128 ? 16 : 32))));
   if (K % 64) return fail(DAK_EUNSUPPORTED, "dak_linear: K %% 64 != 0");
   if (kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
     return fail(DAK_EINVAL, "dak_linear: kc must be a power of two in [64, 2048] dividing K");
@@ -1032,6 +1035,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
+  if (path != 3 && N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d needs the tcgen05 path (kc = 64)", N, kMaxN);
   if (path == 3) {  // tcgen05: canonical SWIZZLE_128B K-major operands need KC = 64; plain GEMV only
     if (kc != 64) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path needs kc = 64");
     if (a->ln_w || a->x_swiglu || a->stats_out) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path has no operand transforms / statistics");
@@ -1134,7 +1138,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.wm = wm; p.wk = wk;
   p.rgran = rg;
   if (path == 3) {
-    const int cols = 4 * (int)ceil_div(rmax, 128) * n8;  // four k-chain accumulators
+    const int cols = (n8 >= 128 ? 1 : 4) * (int)ceil_div(rmax, 128) * n8;  // k-chain accumulators
     p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   }
   p.mc = mc;
@@ -1365,6 +1369,8 @@ dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
     case 2: return launch_umma_t<2>(pl, s, pdl);
     case 4: return launch_umma_t<4>(pl, s, pdl);
     case 8: return launch_umma_t<8>(pl, s, pdl);
+    case 16: return launch_umma_t<16>(pl, s, pdl);
+    case 32: return launch_umma_t<32>(pl, s, pdl);
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no tcgen05 kernel instance for %d n8 tiles", pl.nn);
 }

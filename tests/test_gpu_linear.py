@@ -231,7 +231,8 @@ def test_linear_x_multicast_bitwise(D, torch, M, K, N, h, kc, xf, cluster):
 
 
 @pytest.mark.parametrize("M,K,N,h", [(1024, 8192, 64, 32), (3584, 4096, 32, 0), (7168, 7168, 16, 56),
-                                     (1000, 2048, 40, 16), (300, 1024, 64, 296), (28672, 1024, 64, 224)])
+                                     (1000, 2048, 40, 16), (300, 1024, 64, 296), (28672, 1024, 64, 224),
+                                     (7168, 1024, 128, 48), (2000, 2048, 256, 0), (500, 512, 200, 40)])
 def test_linear_tcgen05_path(D, torch, M, K, N, h):
     """force_path = 3: tcgen05.mma (M=128 x N x K=16, TMEM accumulators) on SWIZZLE_128B SMEM operands
     (KC = 64), against the oracle."""

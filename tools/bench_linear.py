@@ -89,8 +89,8 @@ def main():
     a = ap.parse_args()
     if a.exp == "tc":  # tcgen05 (path 3, kc 64) vs mma.sync (path 2) at growing N
         for (M, K) in ((7168, 8192), (28672, 7168), (1024, 8192)):
-            for N in (8, 16, 32, 64):
-                for path in (2, 3):
+            for N in (8, 16, 32, 64, 128, 256):
+                for path in ((2, 3) if N <= 64 else (3,)):
                     kc = 64 if path == 3 else dak.default_kc(M, K, 147)
                     try:
                         r = time_cfg(M, K, N, 0, kc, pdl=1, force_path=path)
