@@ -31,6 +31,23 @@ METRIC = "aggregate GB/s (HBM+host link) vs roofline; decode tokens/s at 1/2/4/8
 LINK_GBS_DEFAULT = 51.5  # profiles/r01/calib_loadpath.jsonl: SM bulk-copy read of pinned host memory
 
 
+def planner_rates(hbm_gbs, link_gbs):
+    """Rates the planner balances (reading R10): what the split kernel itself sustains on this box
+    -- HBM read stream with no host share and the host link at the balanced ratio -- from the
+    committed C5 sweep (tools/sweep.py c5 -> profiles/r*/sweep_c5_ratio.jsonl); else the peaks."""
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "sweep_c5_ratio.jsonl")))
+    if not files:
+        return hbm_gbs, link_gbs, "peaks"
+    pts = [json.loads(l) for l in open(files[-1]) if l.strip()]
+    fc1 = [d for d in pts if d.get("M") == 28672 and d.get("cc") == 1]
+    h0 = [d["gbs"] for d in fc1 if d["r"] == 0.0]
+    rs = link_gbs / (hbm_gbs + link_gbs)
+    near = sorted((d for d in fc1 if d["r"] > 0), key=lambda d: abs(d["r"] - rs))
+    if not h0 or not near:
+        return hbm_gbs, link_gbs, "peaks"
+    return h0[0], near[0]["host_gbs"], os.path.relpath(files[-1], ROOT)
+
+
 def measured_peaks():
     hbm, link = None, None
     try:
@@ -259,7 +276,8 @@ def main():
 
     world, rank, local = dist_setup()
     hbm_gbs, link_gbs, peak_src = measured_peaks()
-    hw = HW(hbm_bps=(a.plan_hbm_gbs or hbm_gbs) * 1e9, link_bps=(a.plan_link_gbs or link_gbs) * 1e9)
+    ph, pl, plan_src = planner_rates(hbm_gbs, link_gbs)
+    hw = HW(hbm_bps=(a.plan_hbm_gbs or ph) * 1e9, link_bps=(a.plan_link_gbs or pl) * 1e9)
     llama = a.workload == "llama3-70b-tp8"
     if llama:
         eng, cfg, wl = make_llama(a, hw, world, rank, dak)
@@ -380,6 +398,8 @@ def main():
                             host_ratio=round(nb["host"] / nb["total"], 5),
                             l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
+                            planner_rates_gbs=dict(hbm=round(hw.hbm_bps / 1e9, 1), link=round(hw.link_bps / 1e9, 2),
+                                                   source=plan_src),
                             execution="persistent step (dak_step, 1 launch)" if a.persistent else "per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world)),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
