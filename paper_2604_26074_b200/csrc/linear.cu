@@ -740,14 +740,20 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
                : "r"(taddr));
 }
 
-template <int NT>  // x rows padded to n8 = 8 NT (NT in 2, 4, 8): MMA N = n8
+// XF: operand transform as on the mma.sync path (0 none, 1 pre-norm, 2 SwiGLU), applied by three
+// transform warps to each landed x box in SMEM (in place; SwiGLU writes into the gate box), made
+// visible to the tensor core's async proxy, then released to the MMA issuer through xready[s].
+template <int NT, int XF>  // x rows padded to n8 = 8 NT: MMA N = n8
 __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
   uint64_t* done = empty + kMaxStages;
+  uint64_t* xready = done + 1;  // [kMaxStages] transformed x box ready (XF != 0)
+  uint64_t* lnbar = xready + kMaxStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
+  float* s_ln = reinterpret_cast<float*>(smem + p.res_offset);  // mean[256], rstd[256] (in the slack region)
   unsigned char* wring = smem + 1024;
   unsigned char* xring = smem + p.off_x;
   constexpr int N8 = 8 * NT;
@@ -775,6 +781,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    for (int s = 0; s < kMaxStages; ++s) mbar_init(&xready[s], 3);  // three transform warps
+    mbar_init(lnbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1 && R > 0) {  // TMEM accumulator: mtiles x N8 columns (power of two >= 32)
@@ -787,7 +795,11 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   tc_fence_after();
   if (threadIdx.x == 0) tstamp(p.trace, 0);
   grid_dep_launch();
-  if (R <= 0) return;
+  if (R <= 0) {
+    if (p.stats_out && threadIdx.x < N)
+      reinterpret_cast<float4*>(p.stats_out)[(size_t)cta * N + threadIdx.x] = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
   const uint32_t tmem = *tslot;
   const uint32_t w_bytes = (uint32_t)R * 128;
   const uint32_t x_tx = (uint32_t)p.x_stage_bytes;
@@ -806,14 +818,25 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       }
       grid_dep_wait();
       tstamp(p.trace, 1);
-      for (int i = 0; i < pro; ++i) tma_3d(xring + (size_t)i * p.x_stage_bytes, xmap, 0, 0, i, &full[i]);
+      if (XF == 1) {  // LN weight (+ bias) resident for the whole kernel
+        const uint32_t kb = (uint32_t)p.K * 2;
+        mbar_expect_tx(lnbar, p.ln_b ? 2 * kb : kb);
+        bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
+        if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
+      }
+      auto load_x = [&](int slot, int i) {
+        unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
+        tma_3d(dst, xmap, 0, 0, i, &full[slot]);
+        if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K >> 6) + i), &full[slot]);
+      };
+      for (int i = 0; i < pro; ++i) load_x(i, i);
       int s = pro == slots ? 0 : pro;
       uint32_t ph = pro == slots ? 1u : 0u;
       for (int i = pro; i < nchunks; ++i) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], w_bytes + x_tx);
         bulk_g2s_hint(wring + (size_t)s * wstage, src + (long long)i * chunk_stride, w_bytes, &full[s], pol);
-        tma_3d(xring + (size_t)s * p.x_stage_bytes, xmap, 0, 0, i, &full[s]);
+        load_x(s, i);
         if (++s == slots) { s = 0; ph ^= 1u; }
       }
     }
@@ -828,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       int s = 0;
       uint32_t ph = 0;
       for (int i = 0; i < nchunks; ++i) {
-        mbar_wait(&full[s], ph);
+        mbar_wait(XF ? &xready[s] : &full[s], ph);
         tc_fence_after();
         if (leader) {
           const uint32_t ws = wr + (uint32_t)s * wstage, xs = xr + (uint32_t)s * p.x_stage_bytes;
@@ -850,6 +873,67 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       if (leader) umma_commit(done);
       __syncwarp();
     }
+  } else if (XF != 0 && (warp == 2 || warp == 3 || warp == 8)) {
+    const int tw = warp == 8 ? 2 : warp - 2;  // transform warp 0..2
+    const int tt = tw * 32 + lane;             // 0..95
+    if constexpr (XF == 1) {  // per-row mean / rstd from the producer's partials (as on path 2)
+      grid_dep_wait();
+      for (int n = tw; n < N; n += 3) {
+        float c = 0.f, cm = 0.f;
+        for (int j = lane; j < p.ln_parts; j += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
+          c += v.x;
+          cm += v.x * v.y;
+        }
+        c = warp_sum(c);
+        const float mean = warp_sum(cm) / c;
+        float m2 = 0.f;
+        for (int j = lane; j < p.ln_parts; j += 32) {
+          const float4 v = *reinterpret_cast<const float4*>(p.ln_stats + ((size_t)j * N + n) * 4);
+          const float d = v.y - mean;
+          m2 += v.z + v.x * d * d;
+        }
+        m2 = warp_sum(m2);
+        if (lane == 0) {
+          const float var = p.ln_rms ? m2 / c + mean * mean : m2 / c;
+          s_ln[n] = p.ln_rms ? 0.f : mean;
+          s_ln[256 + n] = rsqrtf(var + p.ln_eps);
+        }
+      }
+      asm volatile("bar.sync 3, 96;" ::: "memory");
+      mbar_wait(lnbar, 0);
+    }
+    const unsigned char* lnres = smem + p.off_ln;
+    const bool has_lnb = p.ln_b != nullptr;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nchunks; ++i) {
+      mbar_wait(&full[s], ph);
+      unsigned char* xs = xring + (size_t)s * p.x_stage_bytes;
+      // 16-byte chunk c of row n sits at n * 128 + ((c ^ (n & 7)) << 4): elements k = 64 i + 8 c ..
+      for (int q = tt; q < N8 * 8; q += 96) {
+        const int n = q >> 3, c = q & 7;
+        uint4* g = reinterpret_cast<uint4*>(xs + n * 128 + ((c ^ (n & 7)) << 4));
+        uint4 v = *g;
+        if constexpr (XF == 2) {
+          const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(g) + (p.x_stage_bytes >> 1));
+          v.x = swiglu_pair(v.x, u.x); v.y = swiglu_pair(v.y, u.y);
+          v.z = swiglu_pair(v.z, u.z); v.w = swiglu_pair(v.w, u.w);
+        } else {
+          const float mu = n < N ? s_ln[n] : 0.f, rs = n < N ? s_ln[256 + n] : 0.f;
+          const int k0 = i * 64 + c * 8;
+          const uint4 wv = *reinterpret_cast<const uint4*>(lnres + k0 * 2);
+          const uint4 bv = has_lnb ? *reinterpret_cast<const uint4*>(lnres + (p.K + k0) * 2) : make_uint4(0, 0, 0, 0);
+          v.x = ln_pair(v.x, wv.x, bv.x, mu, rs); v.y = ln_pair(v.y, wv.y, bv.y, mu, rs);
+          v.z = ln_pair(v.z, wv.z, bv.z, mu, rs); v.w = ln_pair(v.w, wv.w, bv.w, mu, rs);
+        }
+        *g = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&xready[s]);
+      if (++s == slots) { s = 0; ph ^= 1u; }
+    }
   } else if (warp >= 4 && warp < 8) {
     // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +31 = rows of the M tile. One thread polls
     // `done` with back-off, the others sleep on a named barrier: 128 threads spinning on an
@@ -869,12 +953,18 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
     tc_fence_after();
     grid_dep_wait();  // residual / y may belong to the previous kernel
     const int q = warp & 3;
-    for (int mt = 0; mt < mtiles; ++mt) {
-      const int r = mt * 128 + 32 * q + lane;
-      const long long m = row0 + r;
-      const float bias = (r < R && p.bias) ? __bfloat162float(p.bias[m]) : 0.f;
+    // row statistics (stats_out): per column, this warp's rows summed (sum, sum of squares, fixed
+    // butterfly order), the four warps combined in order; M2 = sumsq - R mean^2 (R <= 256 rows)
+    float* st_part = s_ln + 512;  // [4 warps][N8][2] in the slack region
+#pragma unroll 1
+    for (int c0 = 0; c0 < N8; c0 += 8) {
+      float ssum[8], ssq[8];
 #pragma unroll
-      for (int c0 = 0; c0 < N8; c0 += 8) {
+      for (int e = 0; e < 8; ++e) ssum[e] = ssq[e] = 0.f;
+      for (int mt = 0; mt < mtiles; ++mt) {
+        const int r = mt * 128 + 32 * q + lane;
+        const long long m = row0 + r;
+        const float bias = (r < R && p.bias) ? __bfloat162float(p.bias[m]) : 0.f;
         float acc[8];
 #pragma unroll
         for (int k = 0; k < KCH; ++k) {  // fixed-order sum of the k-chains
@@ -892,10 +982,37 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
               float o = acc[e] + bias;
               if (p.act == DAK_ACT_RELU) o = fmaxf(o, 0.f);
               if (p.residual) o += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
-              p.y[(long long)n * p.ldy + m] = __float2bfloat16_rn(o);
+              const __nv_bfloat16 ob = __float2bfloat16_rn(o);
+              p.y[(long long)n * p.ldy + m] = ob;
+              const float f = __bfloat162float(ob);
+              ssum[e] += f;
+              ssq[e] += f * f;
             }
           }
         }
+      }
+      if (p.stats_out) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float a = warp_sum(ssum[e]), b2 = warp_sum(ssq[e]);
+          if (lane == 0) {
+            st_part[(q * N8 + c0 + e) * 2 + 0] = a;
+            st_part[(q * N8 + c0 + e) * 2 + 1] = b2;
+          }
+        }
+      }
+    }
+    if (p.stats_out) {
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      for (int n = threadIdx.x - 128; n < N; n += 128) {
+        float a = 0.f, b2 = 0.f;
+        for (int w = 0; w < 4; ++w) {
+          a += st_part[(w * N8 + n) * 2 + 0];
+          b2 += st_part[(w * N8 + n) * 2 + 1];
+        }
+        const float mean = a / (float)R;
+        const float m2 = fmaxf(b2 - (float)R * mean * mean, 0.f);
+        reinterpret_cast<float4*>(p.stats_out)[(size_t)cta * N + n] = make_float4((float)R, mean, m2, 0.f);
       }
     }
     tc_fence_before();
@@ -1031,20 +1148,19 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // default: tensor cores for every N -- mma.sync (path 2) up to N = 16; tcgen05 (path 3) beyond,
   // where mma.sync becomes issue-bound, when its operand constraints hold
   int path = c.force_path ? c.force_path : 2;
-  if (!c.force_path && N > 16 && kc == 64 && !a->ln_w && !a->x_swiglu && !a->stats_out && c.cluster <= 1 && h % 8 == 0)
+  if (!c.force_path && N > 16 && kc == 64 && c.cluster <= 1 && h % 8 == 0)
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
   if (path != 3 && N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d needs the tcgen05 path (kc = 64)", N, kMaxN);
   if (path == 3) {  // tcgen05: canonical SWIZZLE_128B K-major operands need KC = 64; plain GEMV only
     if (kc != 64) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path needs kc = 64");
-    if (a->ln_w || a->x_swiglu || a->stats_out) return fail(DAK_EUNSUPPORTED, "dak_linear: the tcgen05 path has no operand transforms / statistics");
   }
   const int nt_eff = path == 3 ? std::max(2, nt) : nt;  // tcgen05 M = 128 needs N >= 16
   const int rg = path == 3 ? 8 : 1;                     // 8-row swizzle atoms per CTA range
   // rows per CTA are bounded by the accumulator capacity of the path and by SMEM: at least three
   // ring stages of (rows x KC) weights plus the x rows must fit (deep enough to cover HBM latency)
-  if (a->x_swiglu && (path != 2 || a->ln_w)) return fail(DAK_EINVAL, "dak_linear: x_swiglu needs the tensor-core path and no pre-norm");
+  if (a->x_swiglu && (path == 1 || a->ln_w)) return fail(DAK_EINVAL, "dak_linear: x_swiglu needs a tensor-core path and no pre-norm");
   const int n8 = path == 1 ? 8 : nt_eff * 8;
   const long long x_stage = (long long)n8 * kc * 2 * (a->x_swiglu ? 2 : 1);
   const long long smem_rows = ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
@@ -1148,7 +1264,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.swiglu = a->x_swiglu ? 1 : 0;
   int ln_bytes = 0;
   if (a->ln_w) {
-    if (path != 2) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm needs the tensor-core path");
+    if (path == 1) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm needs a tensor-core path");
     if (K > 8192) return fail(DAK_EUNSUPPORTED, "dak_linear: fused pre-norm keeps LN weights resident: K <= 8192");
     ln_bytes = (int)ceil_div((a->ln_b ? 4 : 2) * K, 128) * 128;
     if (!a->ln_stats || a->ln_parts <= 0) return fail(DAK_EINVAL, "dak_linear: ln_w set but ln_stats / ln_parts missing");
@@ -1343,9 +1459,9 @@ dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl) { return lau
 #elif DAK_LINEAR_PART == 4
 dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl) { return launch_mma_xf<8>(pl, s, pdl); }
 #elif DAK_LINEAR_PART == 5
-template <int NT>
+template <int NT, int XF>
 static dak_status launch_umma_t(const Plan& pl, cudaStream_t stream, int pdl) {
-  auto kern = umma_linear_kernel<NT>;
+  auto kern = umma_linear_kernel<NT, XF>;
   static int smem_set = 0;
   if (!smem_set) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
@@ -1364,13 +1480,19 @@ static dak_status launch_umma_t(const Plan& pl, cudaStream_t stream, int pdl) {
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pl.p));
   return DAK_OK;
 }
+template <int NT>
+static dak_status launch_umma_xf(const Plan& pl, cudaStream_t s, int pdl) {
+  if (pl.p.ln_w) return launch_umma_t<NT, 1>(pl, s, pdl);
+  if (pl.p.swiglu) return launch_umma_t<NT, 2>(pl, s, pdl);
+  return launch_umma_t<NT, 0>(pl, s, pdl);
+}
 dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
   switch (pl.nn) {
-    case 2: return launch_umma_t<2>(pl, s, pdl);
-    case 4: return launch_umma_t<4>(pl, s, pdl);
-    case 8: return launch_umma_t<8>(pl, s, pdl);
-    case 16: return launch_umma_t<16>(pl, s, pdl);
-    case 32: return launch_umma_t<32>(pl, s, pdl);
+    case 2: return launch_umma_xf<2>(pl, s, pdl);
+    case 4: return launch_umma_xf<4>(pl, s, pdl);
+    case 8: return launch_umma_xf<8>(pl, s, pdl);
+    case 16: return launch_umma_xf<16>(pl, s, pdl);
+    case 32: return launch_umma_xf<32>(pl, s, pdl);
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no tcgen05 kernel instance for %d n8 tiles", pl.nn);
 }

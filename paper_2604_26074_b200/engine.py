@@ -159,7 +159,8 @@ class DakOPT:
             # one KC for both execution paths: the persistent step's slot constraint (<= 256)
             n_host = min(self.n_cta_host, op.h) if op.h > 0 else 0
             rows = max(-(-op.h // max(n_host, 1)) if op.h else 0, -(-(op.M - op.h) // (self.sms - n_host)))
-            op.kc = dak.step_choose_kc(rows, op.K)
+            # KC = 64 above 16 batch columns: the tcgen05 path (canonical SWIZZLE_128B operands)
+            op.kc = 64 if self.B > 16 else dak.step_choose_kc(rows, op.K)
             i += 1
         self.attn_host_chunks = [plan[i + l]["host_units"] for l in range(c.n_layers)]
         return plan

@@ -68,19 +68,20 @@ def test_fused_norm_linear(D, torch, rms, M, K, N, h, kc):
     assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
 
 
-@pytest.mark.parametrize("M,N,h", [(7168, 8, 56), (1024, 3, 0), (320, 16, 320)])
-def test_stats_epilogue_then_fused_norm(D, torch, M, N, h):
+@pytest.mark.parametrize("M,N,h,path", [(7168, 8, 56, 0), (1024, 3, 0, 0), (320, 16, 320, 0), (7168, 64, 64, 3),
+                                         (2048, 40, 0, 3)])
+def test_stats_epilogue_then_fused_norm(D, torch, M, N, h, path):
     """Producer linear writes per-CTA (count, mean, M2) of its bf16 outputs; (1) the merged
     statistics equal mean / variance of those outputs, (2) a consumer linear fused with LN over
     them equals LN(y) -> GEMV in the oracle."""
     from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
     K = 1024
     W, x, bias = synth.linear_inputs(M, K, N, seed=synth.seed_for(6, M), bias=True)
-    sl = SplitLinear(D, W, h, 128)
+    sl = SplitLinear(D, W, h, 64 if path == 3 else 128)
     xd = to_dev(x)
     y = torch.empty((N, M), dtype=torch.int16, device="cuda")
     biasd = to_dev(bias)  # keep every device buffer referenced until the kernels ran
-    a = sl.args(xd, y, N, bias=biasd)
+    a = sl.args(xd, y, N, bias=biasd, force_path=path)
     grid = D.linear_query(a)["grid"]
     stats = torch.full((grid, N, 4), float("nan"), dtype=torch.float32, device="cuda")
     a.stats_out = stats.data_ptr()

@@ -257,3 +257,38 @@ def test_linear_tcgen05_r_invariance_and_integer_exact(D, torch):
     assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(ref))
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+@pytest.mark.parametrize("xf,N", [(1, 64), (1, 24), (2, 64), (2, 128)])
+def test_linear_tcgen05_operand_transforms(D, torch, xf, N):
+    """tcgen05 path with the fused pre-norm (RMSNorm) or SwiGLU operand applied in SMEM by the
+    transform warps, against the oracle."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    M, K, h = 3584, 2048, 32
+    W, _, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(11, M + N + xf))
+    g = synth.rng(N * 7 + xf)
+    sl = SplitLinear(D, W, h, 64)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    if xf == 1:
+        x = synth.bf16_bits((g.standard_normal((N, K)) * 1.5 + 0.3).astype(np.float32))
+        w_ln = synth.bf16_bits((1.0 + 0.2 * g.standard_normal(K)).astype(np.float32))
+        xd, wd = to_dev(x), to_dev(w_ln)
+        stats = torch.zeros((N, 4), dtype=torch.float32, device="cuda")
+        D.row_stats(xd, N, K, stats)
+        a = sl.args(xd, y, N, force_path=3)
+        a.ln_w, a.ln_stats, a.ln_parts, a.ln_rms, a.ln_eps = wd.data_ptr(), stats.data_ptr(), 1, 1, 1e-5
+        xf64 = Kx.bf16_to_f64(x)
+        from oracle import layer as Ly  # noqa: F401
+        hx = Kx.round_to_bf16(Kx.rmsnorm(xf64, Kx.bf16_to_f64(w_ln), 1e-5))
+    else:
+        x = synth.normal_bf16(g, (N, 2 * K), 1.5)
+        xd = to_dev(x)
+        a = sl.args(xd, y, N, force_path=3)
+        a.x_swiglu = 1
+        gf, uf = Kx.bf16_to_f64(x[:, :K]), Kx.bf16_to_f64(x[:, K:])
+        hx = Kx.round_to_bf16(gf / (1.0 + np.exp(-gf)) * uf)
+    assert D.linear_query(a)["path"] == 3
+    D.linear(a)
+    torch.cuda.synchronize()
+    ref = Kx.split_linear(W[:h], W[h:], synth.bf16_bits(hx.astype(np.float32)))
+    assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
