@@ -145,6 +145,7 @@ def barrier(world):
 # CPU oracle baseline (the oracle as it stands; a bounded sample of the same workload)
 # ------------------------------------------------------------------------------------------------
 _CACHE = {}
+READ_PEAK_GBS = 7381.6  # bulk-copy read ring, calibrated on the pool's B200 (profiles/r01/calib_loadpath.jsonl)
 
 
 def oracle_sample(batch: int, min_seconds: float = 10.0):
@@ -359,21 +360,28 @@ def main():
     xs = torch.zeros(eng.B, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
     ys = torch.empty(eng.B, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
     largs = [dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
-                             cfg=dict(congestion_control=int(not a.no_cc))) for op in ops]
-    passes = []
-    for _ in range(3):  # every linear launch of a step, each bracketed by events; median of 3 passes
-        evs = []
-        with torch.cuda.stream(stream):
+                             cfg=dict(congestion_control=int(not a.no_cc), pdl=int(not a.no_pdl))) for op in ops]
+    # the step's linear launches in step order, chained exactly as in the step (PDL), replayed as one
+    # CUDA graph and bracketed by events on the launching stream: average launch duration = time / n
+    with torch.cuda.stream(stream):
+        for la in largs:
+            dak.linear(la, stream)
+        stream.synchronize()
+        lg = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(lg, stream=stream):
             for la in largs:
-                s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                s0.record(stream)
                 dak.linear(la, stream)
-                s1.record(stream)
-                evs.append((s0, s1))
-        torch.cuda.synchronize()
-        passes.append([s0.elapsed_time(s1) / 1e3 for s0, s1 in evs])
-    for i, op in enumerate(ops):
-        lin_time += statistics.median(p_[i] for p_ in passes)
+    lg.replay()
+    torch.cuda.synchronize()
+    reps = 5
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(reps):
+            lg.replay()
+        e1.record(stream)
+    torch.cuda.synchronize()
+    lin_time = e0.elapsed_time(e1) / 1e3 / reps
+    for op in ops:
         lin_bytes += op.M * op.K * 2 + eng.B * (op.K + op.M) * 2
     lin_achieved = lin_bytes / lin_time / 1e9
     lin_share = lin_time / step_s
@@ -388,9 +396,14 @@ def main():
                     frac=round(lin_achieved / peak, 4), traffic=traffic,
                     algorithmic_bytes_per_launch=round(lin_bytes / len(ops)),
                     traffic_source=os.path.relpath(tr_files[-1], ROOT) if tr_files else None,
-                    kernel="dak_linear (split GEMV/skinny GEMM, all %d launches of a step, per-launch events, no PDL)" % len(ops),
+                    kernel="dak_linear (split GEMV/skinny GEMM): the step's %d linear launches chained with PDL as "
+                           "in the step, graph-replayed, events on the launching stream" % len(ops),
                     peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json) + measured host link %.1f GB/s" % (peak_src, hbm_gbs, link_gbs),
                     step_frac=round(value / world / peak, 4),
+                    # read-only streams exceed the copy figure: the calibrated bulk-read ring peak
+                    # (profiles/r01/calib_loadpath.jsonl, 148 SMs x 4 x 32 KB) as a second denominator
+                    read_peak=round(READ_PEAK_GBS + link_gbs, 1),
+                    frac_of_read_peak=round(lin_achieved / (READ_PEAK_GBS + link_gbs), 4),
                     kernel_time_share_of_step=round(lin_share, 4))
 
     line = dict(metric=METRIC, value=round(value, 2), unit="GB/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
