@@ -44,6 +44,13 @@ def round_to_bf16(v) -> np.ndarray:
     return np.ldexp(np.rint(m * 256.0) / 256.0, e)
 
 
+def bf16_bits_rne(v) -> np.ndarray:
+    """bf16 bit patterns (uint16) of float64 values rounded to nearest even (round_to_bf16): the
+    rounded values are exactly representable, so their float32 images carry them in the top half."""
+    r = round_to_bf16(v).astype(np.float32)
+    return (r.view(np.uint32) >> 16).astype(np.uint16)
+
+
 def _act(t: np.ndarray, act: str) -> np.ndarray:
     if act == "none":
         return t

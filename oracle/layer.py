@@ -146,3 +146,32 @@ def llama_decode_step(tokens, positions, params: dict, K_cache: list, V_cache: l
         x, _, _ = llama_decode_layer(x, lp, K_cache[l], V_cache[l], positions, n_heads, n_kv, theta, eps)
     h = rmsnorm(x, bf16_to_f64(params["lnf_w"]), eps)
     return h @ bf16_to_f64(params["lm_head"]).T, x
+
+
+def opt_decode_steps(tokens_seq, start_pos: int, params: dict, K_cache: list, V_cache: list, n_heads: int,
+                     eps: float = 1e-5):
+    """Several decode steps with teacher forcing: step s feeds tokens_seq[s] at position
+    start_pos + s and appends each layer's new k / v to the cache (stored as bf16, the KV cache's
+    storage type). Returns the list of per-step logits (float64)."""
+    from .kernels import bf16_bits_rne
+    L = len(K_cache)
+    K = [[np.asarray(k) for k in layer] for layer in K_cache]
+    V = [[np.asarray(v) for v in layer] for layer in V_cache]
+    E = bf16_to_f64(params["embed"])
+    P = bf16_to_f64(params["pos"])
+    out = []
+    for s, toks in enumerate(tokens_seq):
+        toks = np.asarray(toks)
+        B = toks.shape[0]
+        x = E[toks] + P[np.full(B, start_pos + s) + 2]
+        for l in range(L):
+            lp = {k.split(".", 1)[1]: v for k, v in params.items() if k.startswith(f"L{l}.")}
+            x, k_new, v_new = opt_decode_layer(x, lp, K[l], V[l], n_heads, eps)
+            for b in range(B):
+                kb = bf16_bits_rne(k_new[b])[None]
+                vb = bf16_bits_rne(v_new[b])[None]
+                K[l][b] = np.concatenate([K[l][b], kb], axis=0)
+                V[l][b] = np.concatenate([V[l][b], vb], axis=0)
+        h = layernorm(x, bf16_to_f64(params["lnf_w"]), bf16_to_f64(params["lnf_b"]), eps)
+        out.append(h @ E.T)
+    return out

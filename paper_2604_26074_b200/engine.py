@@ -80,7 +80,8 @@ class DakOPT:
                  y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 16, seed: int = 0,
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
                  host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
-                 evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True):
+                 evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
+                 max_context: int | None = None):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
         self.pdl = int(pdl)
@@ -110,7 +111,9 @@ class DakOPT:
                      down=LinearOp(f"L{i}.fc2", c.hidden, c.ffn))
             self.layers.append(L)
         self.head = LinearOp("head", c.vocab, c.hidden)
-        self.pages_per_req = -(-context // page_size)
+        # KV pages per request cover max_context tokens: decode steps append beyond the prompt
+        self.max_context = max(context, max_context or context)
+        self.pages_per_req = -(-self.max_context // page_size)
         self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
         self.plan = self._plan(mode, y_req, host_override)
         self._allocate(weights)
@@ -435,6 +438,14 @@ class DakOPT:
             ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
                                  self.h, self.logits, cfg=self.launch)
         dak.linear(ha, stream)
+
+    def advance(self, stream=None):
+        """Move every request to the next position (after a step appended its token's KV)."""
+        if int(self.positions.max()) + 1 >= self.max_context:
+            raise ValueError("decode past max_context")
+        with torch.cuda.stream(stream or torch.cuda.current_stream()):
+            self.positions.add_(1)
+            self.seq_lens.add_(1)
 
     def kernels_per_step(self) -> int:
         if getattr(self, "use_step", False):

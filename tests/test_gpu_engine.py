@@ -64,3 +64,42 @@ def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse, fused_qkv):
     from tests.gpu_util import assert_close
     assert_close(got, ref, rtol=3e-2)
     eng.close()
+
+
+@pytest.mark.parametrize("frac", [0.0, 0.3])
+def test_engine_multistep_decode_matches_oracle(frac):
+    """Four decode steps (teacher-forced tokens) through one captured CUDA graph: each step appends
+    its KV row at the next position (crossing a page and a split-KV chunk boundary) and the logits
+    of every step match the oracle, which carries its own bf16 KV cache forward."""
+    import torch
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
+    L, H, F, V, heads, maxpos, B, prompt, steps = 2, 256, 512, 1000, 2, 256, 2, 62, 4
+    g = np.random.default_rng(77)
+    p = make_params(g, L, H, F, V, maxpos)
+    cfg = OPTConfig(n_layers=L, hidden=H, n_heads=heads, ffn=F, vocab=V, max_pos=maxpos, name="opt-tiny")
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    total = (4 * H * H + 2 * F * H) * 2 * L + V * H * 2
+    eng = DakOPT(cfg, B, prompt + 1, hw, mode=dak.PLAN_EXACT, y_req=int(frac * total), page_size=64, chunk_pages=1,
+                 weights=_engine_weights(p, L, torch), max_context=prompt + steps + 1)
+    Kc = [[synth.normal_bf16(g, (prompt, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    Vc = [[synth.normal_bf16(g, (prompt, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    eng.load_kv(Kc, Vc)
+    toks = [np.array([3 + 11 * s, 500 + 7 * s]) for s in range(steps)]
+    s_ = torch.cuda.Stream()
+    eng.tokens.copy_(torch.from_numpy(toks[0].astype(np.int32)))
+    eng.capture(s_)  # eager warm step writes position `prompt` with toks[0]; replay rewrites it
+    got = []
+    for s in range(steps):
+        eng.tokens.copy_(torch.from_numpy(toks[s].astype(np.int32)))
+        eng.graph.replay()
+        torch.cuda.synchronize()
+        got.append(Kx.bf16_to_f64(eng.logits.view(torch.int16).cpu().numpy().view(np.uint16)))
+        if s + 1 < steps:
+            eng.advance()
+            torch.cuda.synchronize()
+    ref = Ly.opt_decode_steps(toks, prompt, p, Kc, Vc, heads)
+    from tests.gpu_util import assert_close
+    for s in range(steps):
+        assert_close(got[s], ref[s], rtol=3e-2)
+    eng.close()

@@ -196,6 +196,14 @@ def test_rmsnorm_pins():
     assert np.allclose(Kx.rmsnorm(x, w, eps=1e-5), ref, rtol=1e-6, atol=1e-7)
 
 
+def test_bf16_bits_rne_roundtrip():
+    """bits -> value -> bits is the identity on finite bf16 patterns; values round to nearest even."""
+    g = np.random.default_rng(21)
+    bits = synth.bf16_bits(g.standard_normal(5000).astype(np.float32))
+    assert np.array_equal(Kx.bf16_bits_rne(Kx.bf16_to_f64(bits)), bits)
+    assert Kx.bf16_to_f64(Kx.bf16_bits_rne(np.array([257.0])))[0] == 256.0
+
+
 def test_round_to_bf16_matches_bit_definition():
     """round_to_bf16 == the RNE bit rounding of the input generator on float32-exact values, and
     is exact on representable values (integers up to 256, powers of two)."""
