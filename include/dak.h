@@ -311,6 +311,13 @@ dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void
                      int32_t B, int32_t hidden, int32_t pos_offset, void* x, float* stats_out, int32_t pdl,
                      dak_stream_t stream);
 
+/* y[r] = x[r] / sqrt(mean(x[r]^2) + eps) * w  (RMSNorm, fp32 statistics). */
+dak_status dak_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t cols, float eps, int32_t pdl,
+                       dak_stream_t stream);
+
+/* out[r, j] = bf16(silu(gu[r, j]) * gu[r, F + j]) for gu = [gate | up] rows of width 2F. */
+dak_status dak_silu_mul(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, dak_stream_t stream);
+
 /* Row statistics for a fused pre-norm (dak_linear_args.ln_stats with ln_parts = 1):
  * stats_out[r] = float4 (cols, mean, M2 = sum (x - mean)^2, 0) over row r of x (bf16, row stride
  * ld elements, 0: cols), fp32, two-pass, fixed order. stats_out may be NULL in dak_embed. */

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat
                                                                const __nv_bfloat16* __restrict__ w,
                                                                const __nv_bfloat16* __restrict__ b,
                                                                __nv_bfloat16* __restrict__ y, int cols, float eps,
-                                                               unsigned long long* tr) {
+                                                               unsigned long long* tr, int rms) {
   __shared__ float red[kLnThreads / 32];
   tstamp(tr, 0);
   grid_dep_launch();
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat
   const __nv_bfloat16* xr = x + (long long)blockIdx.x * cols;
   float s = 0.f;
   for (int c = threadIdx.x; c < cols; c += kLnThreads) s += __bfloat162float(xr[c]);
-  const float mean = block_sum(s, red) / (float)cols;
+  const float mean = rms ? 0.f : block_sum(s, red) / (float)cols;  // RMSNorm: no centring
   float v = 0.f;
   for (int c = threadIdx.x; c < cols; c += kLnThreads) {
     const float d = __bfloat162float(xr[c]) - mean;
@@ -88,6 +88,20 @@ __device__ void row_stats_store(const float* v, int nv, int cols, float* red, fl
 }
 
 constexpr int kRowMax = 64;  // values per thread held in registers (cols <= 256 * 64)
+
+// out[r, j] = bf16(silu(gu[r, j]) * gu[r, F + j])  (Llama MLP gate / up combine)
+__global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int F,
+                                unsigned long long* tr) {
+  if (threadIdx.x == 0) tstamp(tr, 0);
+  grid_dep_launch();
+  grid_dep_wait();
+  const __nv_bfloat16* g = gu + (long long)blockIdx.y * 2 * F;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+    const float a = __bfloat162float(g[j]), u = __bfloat162float(g[F + j]);
+    out[(long long)blockIdx.y * F + j] = __float2bfloat16_rn(a / (1.f + __expf(-a)) * u);
+  }
+  if (threadIdx.x == 0) tstamp(tr, 3);
+}
 
 // x[b] = tok[tokens[b]] + pos[positions[b] + pos_offset]; optional row statistics of the stored x
 __global__ void __launch_bounds__(kLnThreads) embed_kernel(const int* __restrict__ tokens, const int* __restrict__ positions,
@@ -143,7 +157,7 @@ static dak_status launch_pdl(const void* fn, dim3 grid, dim3 block, void** args,
 static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Scratch {
-  size_t h, qkv, attn, f, ws, stats, total, ws_bytes;
+  size_t h, qkv, attn, f, f2, ws, stats, total, ws_bytes;
 };
 constexpr int kMaxParts = 1024;  // statistics partials (producer CTAs) a fused pre-norm merges
 
@@ -171,7 +185,8 @@ static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
   s->qkv = align256(s->h + B * a->hidden * 2);  // h doubles as the TP partial buffer [B, hidden]
   s->attn = align256(s->qkv + B * qkv_cols * 2);
   s->f = align256(s->attn + B * attn_cols * 2);
-  s->ws = align256(s->f + B * f_cols * 2);
+  s->f2 = align256(s->f + B * f_cols * 2);  // Llama unfused: silu(gate) * up [B, ffn]
+  s->ws = align256(s->f2 + (llama ? B * a->ffn * 2 : 0));
   s->ws_bytes = ws;
   s->stats = align256(s->ws + ws);
   s->total = s->stats + (size_t)kMaxParts * B * 16;
@@ -194,13 +209,16 @@ static dak_linear_args lin_args(const dak_weight& w, long long M, long long K, i
 // KV append, split attention, o (+ all-reduce) + residual, SwiGLU fused into down (+ all-reduce)
 // + residual. 8 kernels per layer on one GPU (+2 NCCL all-reduces and 2 residual kernels at TP>1).
 static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_stream_t stream) {
-  if (!a->fuse_norm || !a->stats_in || a->stats_in_parts <= 0 || a->ln1_b || a->ln2_b)
-    return fail(DAK_EINVAL, "dak_layer (Llama): needs fuse_norm with stats_in and RMSNorm weights without bias");
+  const bool fuse = a->fuse_norm != 0;
+  if ((fuse && (!a->stats_in || a->stats_in_parts <= 0)) || a->ln1_b || a->ln2_b)
+    return fail(DAK_EINVAL, "dak_layer (Llama): RMSNorm weights have no bias; fuse_norm needs stats_in");
   if (a->tp_size > 1 && !a->comm) return fail(DAK_EINVAL, "dak_layer (Llama): tp_size > 1 needs comm");
   char* sc = (char*)a->scratch;
   char* qkv = sc + s.qkv;
   void* attn = sc + s.attn;
   void* gu = sc + s.f;
+  void* f2 = sc + s.f2;
+  void* hbuf = sc + s.h;  // normalised x (unfused) -- the TP partial also lives here, never both at once
   void* partial = sc + s.h;
   float* o_stats = (float*)(sc + s.stats);
   const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads, F = a->ffn;
@@ -209,9 +227,19 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   const bool tp = a->comm != nullptr;  // row-parallel partials + all-reduce (also usable at tp_size 1)
   cudaStream_t strm = (cudaStream_t)stream;
   dak_status st;
+  // pre-norm: fused into the consuming linear (small batch: the per-CTA operand transform is
+  // cheap), or one RMSNorm kernel into hbuf (large batch: every CTA would re-normalise all of x)
   auto rms = [&](dak_linear_args& l, const void* w, const float* stats, int parts) {
     l.x = a->x;
     l.ln_w = w; l.ln_b = nullptr; l.ln_rms = 1; l.ln_stats = stats; l.ln_parts = parts; l.ln_eps = a->ln_eps;
+  };
+  auto prenorm = [&](dak_linear_args& l, const void* w, const float* stats, int parts) -> dak_status {
+    if (fuse) {
+      rms(l, w, stats, parts);
+      return DAK_OK;
+    }
+    l.x = hbuf;
+    return dak_rmsnorm(a->x, w, hbuf, B, H, a->ln_eps, pdl, strm);
   };
   if (a->split_qkv) {  // q, k, v side by side into the [B, qkv_cols] buffer
     const long long rows[3] = {(long long)Hq * d, (long long)Hkv * d, (long long)Hkv * d};
@@ -220,13 +248,15 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
     for (int i = 0; i < 3; ++i) {
       dak_linear_args l = lin_args(*w[i], rows[i], H, B, a->x, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
       l.ldy = qkv_cols;
-      rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
+      if (fuse) rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
+      else if (i == 0 && (st = dak_rmsnorm(a->x, a->ln1_w, hbuf, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
+      if (!fuse) l.x = hbuf;
       if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
       off += rows[i];
     }
   } else {  // one fused [q; k; v] projection
     dak_linear_args l = lin_args(a->qkv, qkv_cols, H, B, a->x, qkv, nullptr, DAK_ACT_NONE, a->cfg);
-    rms(l, a->ln1_w, a->stats_in, a->stats_in_parts);
+    if ((st = prenorm(l, a->ln1_w, a->stats_in, a->stats_in_parts)) != DAK_OK) return st;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
   if ((st = dak_rope_kv_append(qkv, qkv_cols, B, Hq, Hkv, d, a->positions, a->rope_theta, a->block_table, a->page_size,
@@ -249,7 +279,7 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   {
     dak_linear_args l = lin_args(a->o, H, (long long)Hq * d, B, attn, tp ? partial : a->x, tp ? nullptr : a->x,
                                  DAK_ACT_NONE, a->cfg);
-    if (!tp) {
+    if (!tp && fuse) {
       dak_linear_launch_info info;
       if ((st = dak_linear_query(&l, &info)) != DAK_OK) return st;
       if (info.grid > kMaxParts) return fail(DAK_EUNSUPPORTED, "dak_layer: o grid %d > %d", info.grid, kMaxParts);
@@ -257,19 +287,23 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
       l.stats_out = o_stats;
     }
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, o_stats, pdl, strm)) != DAK_OK) return st;
+    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? o_stats : nullptr, pdl, strm)) != DAK_OK)
+      return st;
   }
-  {  // [gate; up] with RMSNorm 2 fused -> gu [B, 2F]
+  {  // [gate; up] after RMSNorm 2 -> gu [B, 2F]
     dak_linear_args l = lin_args(a->up, 2LL * F, H, B, a->x, gu, nullptr, DAK_ACT_NONE, a->cfg);
-    rms(l, a->ln2_w, o_stats, o_parts);
+    if ((st = prenorm(l, a->ln2_w, o_stats, o_parts)) != DAK_OK) return st;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
-  {  // down with the SwiGLU operand
-    dak_linear_args l = lin_args(a->down, H, F, B, gu, tp ? partial : a->x, tp ? nullptr : a->x, DAK_ACT_NONE, a->cfg);
-    l.x_swiglu = 1;
-    if (!tp) l.stats_out = a->stats_out;
+  {  // down: the SwiGLU operand fused (small batch) or one silu * up kernel (large batch)
+    dak_linear_args l = lin_args(a->down, H, F, B, fuse ? gu : f2, tp ? partial : a->x, tp ? nullptr : a->x,
+                                 DAK_ACT_NONE, a->cfg);
+    if (fuse) l.x_swiglu = 1;
+    else if ((st = dak_silu_mul(gu, f2, B, F, pdl, strm)) != DAK_OK) return st;
+    if (!tp && fuse) l.stats_out = a->stats_out;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, a->stats_out, pdl, strm)) != DAK_OK) return st;
+    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? a->stats_out : nullptr, pdl, strm)) != DAK_OK)
+      return st;
   }
   return DAK_OK;
 }
@@ -290,9 +324,36 @@ dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, i
   __nv_bfloat16* yp = (__nv_bfloat16*)y;
   int c = cols;
   unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, cols, rows);
-  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr};
+  int rms = 0;
+  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr, &rms};
   return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
                            (cudaStream_t)stream, pdl);
+}
+
+dak_status dak_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t cols, float eps, int32_t pdl,
+                       dak_stream_t stream) {
+  if (!x || !w || !y || rows <= 0 || cols <= 0) return fail(DAK_EINVAL, "dak_rmsnorm: bad arguments");
+  const __nv_bfloat16* xp = (const __nv_bfloat16*)x;
+  const __nv_bfloat16* wp = (const __nv_bfloat16*)w;
+  const __nv_bfloat16* bp = nullptr;
+  __nv_bfloat16* yp = (__nv_bfloat16*)y;
+  int c = cols;
+  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, cols, rows);
+  int rms = 1;
+  void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr, &rms};
+  return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
+                           (cudaStream_t)stream, pdl);
+}
+
+dak_status dak_silu_mul(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, dak_stream_t stream) {
+  if (!gu || !out || rows <= 0 || F <= 0) return fail(DAK_EINVAL, "dak_silu_mul: bad arguments");
+  const __nv_bfloat16* gp = (const __nv_bfloat16*)gu;
+  __nv_bfloat16* op = (__nv_bfloat16*)out;
+  int f = F;
+  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, F, rows);
+  void* args[] = {&gp, &op, &f, &tr};
+  const int bx = (F + 255) / 256 < 8 ? (F + 255) / 256 : 8;
+  return layer::launch_pdl((const void*)layer::silu_mul_kernel, dim3(bx, rows), dim3(256), args, (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,

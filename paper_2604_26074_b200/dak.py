@@ -329,6 +329,9 @@ _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p
                                   C.c_int32, C.c_void_p])
 _sig("dak_embed", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
                               C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p])
+_sig("dak_rmsnorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.c_int32,
+                                C.c_void_p])
+_sig("dak_silu_mul", C.c_int32, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p])
 _sig("dak_row_stats", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p, C.c_int32, C.c_void_p])
 _sig("dak_layer_scratch_size", C.c_int32, [C.POINTER(dak_layer_args), C.POINTER(C.c_size_t)])
 _sig("dak_layer", C.c_int32, [C.POINTER(dak_layer_args), C.c_void_p])
@@ -341,7 +344,7 @@ _sig("dak_comm_init", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.
 _sig("dak_comm_destroy", C.c_int32, [C.c_void_p])
 _sig("dak_allreduce_residual", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                            C.c_int32, C.c_void_p])
-EXPORTED += ["dak_layernorm", "dak_embed", "dak_row_stats", "dak_layer_scratch_size", "dak_layer",
+EXPORTED += ["dak_layernorm", "dak_rmsnorm", "dak_silu_mul", "dak_embed", "dak_row_stats", "dak_layer_scratch_size", "dak_layer",
              "dak_layer_stats_parts", "dak_rope_kv_append", "dak_comm_unique_id", "dak_comm_init", "dak_comm_destroy",
              "dak_allreduce_residual"]
 MODEL_LLAMA = 1
@@ -387,6 +390,14 @@ def layernorm(x, w, b, y, rows, cols, eps=1e-5, pdl=0, stream=None):
 def embed(tokens, positions, tok_emb, pos_emb, B, hidden, pos_offset, x, pdl=0, stream=None, stats_out=None):
     _check(lib.dak_embed(_ptr(tokens), _ptr(positions), _ptr(tok_emb), _ptr(pos_emb), int(B), int(hidden),
                          int(pos_offset), _ptr(x), _ptr(stats_out), int(pdl), _stream(stream)))
+
+
+def rmsnorm(x, w, y, rows, cols, eps=1e-5, pdl=0, stream=None):
+    _check(lib.dak_rmsnorm(_ptr(x), _ptr(w), _ptr(y), int(rows), int(cols), float(eps), int(pdl), _stream(stream)))
+
+
+def silu_mul(gu, out, rows, F, pdl=0, stream=None):
+    _check(lib.dak_silu_mul(_ptr(gu), _ptr(out), int(rows), int(F), int(pdl), _stream(stream)))
 
 
 def row_stats(x, rows, cols, stats_out, ld=0, pdl=0, stream=None):

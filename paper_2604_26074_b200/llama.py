@@ -44,9 +44,12 @@ class DakLlama:
     def __init__(self, cfg: LlamaConfig, batch: int, context: int, hw: HW, tp_rank: int = 0, tp_size: int = 1,
                  comm=None, mode: int = dak.PLAN_BALANCED, y_req: int = 0, unit_rows: int = 16, page_size: int = 64,
                  chunk_pages: int = 16, seed: int = 0, pdl: bool = True, congestion_control: bool = True,
-                 weights: dict | None = None, n_cta_host: int = 2):
+                 weights: dict | None = None, n_cta_host: int = 2, fuse_norm: bool | None = None):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.rank, self.world, self.comm = tp_rank, tp_size, comm
+        # operand transforms fused into the linears only at small batch: above 16 columns every CTA
+        # would re-normalise / re-activate the whole operand (measured 3-8x slower than one kernel)
+        self.fuse_norm = (batch <= 16) if fuse_norm is None else bool(fuse_norm)
         self.dims = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
         self.pdl = int(pdl)
@@ -183,6 +186,7 @@ class DakLlama:
         self.seq_lens = self.positions + 1
         self.tokens = torch.zeros((B,), dtype=torch.int32, device="cuda")
         self.x = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
+        self.hnorm = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
         self.logits = torch.empty((B, self.dims["vocab"]), dtype=torch.bfloat16, device="cuda")
         self.layer_args = [self._layer_args(l) for l in range(c.n_layers)]
         self.scratch = torch.empty(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
@@ -235,7 +239,7 @@ class DakLlama:
                                                   self.seq_lens.data_ptr())
         a.page_size, a.max_pages, a.chunk_pages = self.page, self.pages_per_req, self.chunk_pages
         a.tp_rank, a.tp_size, a.comm = self.rank, self.world, self.comm
-        a.fuse_norm = 1
+        a.fuse_norm = int(self.fuse_norm)
         a.cfg = dak.launch_cfg(**self.launch)
         # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
         n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
@@ -247,16 +251,25 @@ class DakLlama:
     def enqueue_step(self, stream=None):
         c = self.cfg
         dak.embed(self.tokens, None, self.tok_emb, None, self.B, c.hidden, 0, self.x, pdl=self.pdl, stream=stream,
-                  stats_out=self.stats)
+                  stats_out=self.stats if self.fuse_norm else None)
         for a in self.layer_args:
             dak.layer(a, stream)
-        ha = dak.linear_args(self.head.host[1] if self.head.host else None, self.head.hbm, self.head.M, self.head.K,
-                             self.head.h, self.head.kc, self.B, self.x, self.logits, cfg=self.launch, ln_w=self.lnf_w,
-                             ln_stats=self.stats, ln_parts=self.head_stats_parts, ln_rms=1, ln_eps=c.rms_eps)
+        hw = self.head.host[1] if self.head.host else None
+        if self.fuse_norm:  # final RMSNorm fused into the LM head
+            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B, self.x,
+                                 self.logits, cfg=self.launch, ln_w=self.lnf_w, ln_stats=self.stats,
+                                 ln_parts=self.head_stats_parts, ln_rms=1, ln_eps=c.rms_eps)
+        else:
+            dak.rmsnorm(self.x, self.lnf_w, self.hnorm, self.B, c.hidden, c.rms_eps, pdl=self.pdl, stream=stream)
+            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
+                                 self.hnorm, self.logits, cfg=self.launch)
         dak.linear(ha, stream)
 
     def kernels_per_step(self) -> int:
-        per_layer = 6 + (1 if self.chunks_per_req > 1 else 0) + (2 if self.comm else 0)  # + residual kernels
+        per_layer = (6 + (1 if self.chunks_per_req > 1 else 0) + (2 if self.comm else 0)  # + residual kernels
+                     + (0 if self.fuse_norm else 3))  # + 2 RMSNorm + silu*up kernels
+        if not self.fuse_norm:
+            return 1 + per_layer * self.cfg.n_layers + 2
         return 1 + per_layer * self.cfg.n_layers + 1
 
     def capture(self, stream: torch.cuda.Stream):

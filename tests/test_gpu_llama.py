@@ -16,8 +16,10 @@ def _dev(p, torch):
     return {k: torch.from_numpy(np.ascontiguousarray(v).view(np.int16)).cuda().view(torch.bfloat16) for k, v in p.items()}
 
 
-@pytest.mark.parametrize("frac,B,ctx,use_comm", [(0.0, 3, 70, False), (0.3, 2, 150, False), (0.2, 4, 40, True)])
-def test_llama_step_matches_oracle(frac, B, ctx, use_comm):
+@pytest.mark.parametrize("frac,B,ctx,use_comm,fuse", [(0.0, 3, 70, False, True), (0.3, 2, 150, False, True),
+                                                     (0.2, 4, 40, True, True), (0.2, 4, 40, True, False),
+                                                     (0.3, 24, 90, False, None)])
+def test_llama_step_matches_oracle(frac, B, ctx, use_comm, fuse):
     import torch
     from paper_2604_26074_b200 import dak
     from paper_2604_26074_b200.engine import HW
@@ -31,13 +33,13 @@ def test_llama_step_matches_oracle(frac, B, ctx, use_comm):
     comm = dak.comm_init(dak.comm_unique_id(), 0, 1) if use_comm else None
     total = L * (H * (nh + 2 * nkv) * d + nh * d * H + 3 * F * H) * 2 + V * H * 2
     eng = DakLlama(cfg, B, ctx, hw, comm=comm, mode=dak.PLAN_EXACT, y_req=int(frac * total), page_size=64,
-                   chunk_pages=1, weights=_dev(p, torch))
+                   chunk_pages=1, weights=_dev(p, torch), fuse_norm=fuse)
     if frac > 0:
         assert sum(op.h for op in eng.linear_ops()) > 0
     Kc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
     Vc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
     eng.load_kv(Kc, Vc)
-    tokens = np.arange(B) * 13 + 3
+    tokens = (np.arange(B) * 13 + 3) % V
     eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
     s = torch.cuda.Stream()
     eng.capture(s)
@@ -131,3 +133,27 @@ def test_llama_tp8_shard_shapes_b64():
     from tests.gpu_util import assert_close
     assert_close(got, ref, rtol=3e-2)
     eng.close()
+
+
+def test_rmsnorm_and_silu_mul_kernels():
+    import torch
+    from paper_2604_26074_b200 import dak
+    from tests.gpu_util import to_dev, from_dev
+    g = synth.rng(31)
+    x = synth.normal_bf16(g, (5, 8192), 1.3)
+    w = synth.bf16_bits((1.0 + 0.2 * g.standard_normal(8192)).astype(np.float32))
+    y = torch.empty((5, 8192), dtype=torch.int16, device="cuda")
+    xd, wd = to_dev(x), to_dev(w)
+    dak.rmsnorm(xd, wd, y, 5, 8192, 1e-5)
+    gu = synth.normal_bf16(g, (3, 2 * 3584), 2.0)
+    gd = to_dev(gu)
+    o = torch.empty((3, 3584), dtype=torch.int16, device="cuda")
+    dak.silu_mul(gd, o, 3, 3584)
+    torch.cuda.synchronize()
+    ref = Kx.round_to_bf16(Kx.rmsnorm(Kx.bf16_to_f64(x), Kx.bf16_to_f64(w), 1e-5))
+    got = Kx.bf16_to_f64(from_dev(y))
+    assert np.abs(got - ref).max() <= 2 ** -7 * np.abs(ref).max()
+    gf, uf = Kx.bf16_to_f64(gu[:, :3584]), Kx.bf16_to_f64(gu[:, 3584:])
+    ref2 = Kx.round_to_bf16(Ly.silu(gf) * uf)
+    got2 = Kx.bf16_to_f64(from_dev(o))
+    assert np.abs(got2 - ref2).max() <= 2 ** -7 * max(1.0, np.abs(ref2).max())

@@ -28,13 +28,13 @@ def setup(M, K, N, h, kc, copies):
         hosts.append((hp, dp))
         src = (torch.randn(h * K, device="cuda") * 0.01).to(torch.bfloat16)
         dak.pack_linear(src, h, K, kc, dp)
-    x = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    x = torch.randn(N, 2 * K, device="cuda").to(torch.bfloat16)  # [gate | up] when swiglu
     y = torch.empty(N, M, device="cuda", dtype=torch.bfloat16)
     torch.cuda.synchronize()
     return hbm, hosts, x, y
 
 
-def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, **cfg):
+def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu=False, **cfg):
     size = M * K * 2
     copies = max(2, min(64, int(np.ceil(4 * L2 / max(size, 1)))))
     hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
@@ -48,7 +48,7 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, **cfg)
     args = []
     for i in range(launches):
         a = dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg,
-                            stats_out=st_out if stats else None, **ln_kw)
+                            stats_out=st_out if stats else None, x_swiglu=int(swiglu), **ln_kw)
         args.append(a)
     info = dak.linear_query(args[0])
     s = torch.cuda.Stream()
@@ -77,7 +77,7 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, **cfg)
         dak.host_free(hp)
     del hbm
     torch.cuda.empty_cache()
-    return dict(M=M, K=K, N=N, h=h, kc=kc, ln=ln, stats=stats, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
+    return dict(M=M, K=K, N=N, h=h, kc=kc, ln=ln, stats=stats, swiglu=swiglu, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
                 host_gbs=h * K * 2 / t / 1e9, info={k: info[k] for k in ("grid", "n_cta_host", "stages_hbm", "window_host",
                                                                         "smem_bytes", "path")}, cfg=cfg)
 
@@ -87,6 +87,17 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "tcx":  # tcgen05 operand transforms at the Llama TP8 shard shapes, b64
+        for (M, K, kw) in ((8192, 3584, dict(swiglu=True)), (7168, 8192, dict(ln=True)), (8192, 3584, {}),
+                           (7168, 8192, {})):
+            for path in (2, 3):
+                kc = 64 if path == 3 else 256
+                try:
+                    r = time_cfg(M, K, 64, 0, kc, pdl=1, force_path=path, **kw)
+                    print(json.dumps(r), flush=True)
+                except Exception as e:  # noqa: BLE001
+                    print(json.dumps(dict(M=M, K=K, path=path, error=str(e))), flush=True)
+        return
     if a.exp == "tc":  # tcgen05 (path 3, kc 64) vs mma.sync (path 2) at growing N
         for (M, K) in ((7168, 8192), (28672, 7168), (1024, 8192)):
             for N in (8, 16, 32, 64, 128, 256):
