@@ -196,6 +196,10 @@ typedef struct {
   /* GEMV operand is bf16(silu(gate) * up), computed in fp32. Tensor-core path, no pre-norm.        */
   int32_t x_swiglu;
   int32_t reserved3;
+  /* Workspace (device, nullable): lets the tcgen05 path split K when its 128-row tiles would be   */
+  /* mostly empty (fp32 partials [splits][N][M], combined in fixed order by a second kernel).      */
+  void* workspace;
+  int64_t workspace_bytes;
 } dak_linear_args;
 
 /* Launch description (pure query; used by tests and the bench to attribute bytes). */
@@ -208,6 +212,9 @@ typedef struct {
 } dak_linear_launch_info;
 
 dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);
+
+/* Workspace bytes the launch would use for split-K (0: none). Needs the device. */
+size_t dak_linear_workspace_size(const dak_linear_args* args);
 
 /* Row ownership of CTA `cta` (0 <= cta < grid): tier (0 HBM, 1 host) and [row_begin,row_end)
  * in global row numbering. Host CTAs split [0,h), HBM CTAs split [h,M), each into contiguous

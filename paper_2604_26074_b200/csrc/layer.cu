@@ -157,7 +157,7 @@ static dak_status launch_pdl(const void* fn, dim3 grid, dim3 block, void** args,
 static inline size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 struct Scratch {
-  size_t h, qkv, attn, f, f2, ws, stats, total, ws_bytes;
+  size_t h, qkv, attn, f, f2, ws, stats, splitk, splitk_bytes, total, ws_bytes;
 };
 constexpr int kMaxParts = 1024;  // statistics partials (producer CTAs) a fused pre-norm merges
 
@@ -189,7 +189,11 @@ static dak_status scratch_layout(const dak_layer_args* a, Scratch* s) {
   s->ws = align256(s->f2 + (llama ? B * a->ffn * 2 : 0));
   s->ws_bytes = ws;
   s->stats = align256(s->ws + ws);
-  s->total = s->stats + (size_t)kMaxParts * B * 16;
+  // split-K partials of the tcgen05 path (batch > 16): <= 16 splits x B x the widest projection
+  const size_t widest = std::max<size_t>(std::max<size_t>(qkv_cols, a->hidden), (size_t)a->ffn * (llama ? 2 : 1));
+  s->splitk = align256(s->stats + (size_t)kMaxParts * B * 16);
+  s->splitk_bytes = B > 16 ? 16 * B * widest * 4 : 0;
+  s->total = s->splitk + s->splitk_bytes;
   return DAK_OK;
 }
 
@@ -209,6 +213,16 @@ static dak_linear_args lin_args(const dak_weight& w, long long M, long long K, i
 // KV append, split attention, o (+ all-reduce) + residual, SwiGLU fused into down (+ all-reduce)
 // + residual. 8 kernels per layer on one GPU (+2 NCCL all-reduces and 2 residual kernels at TP>1).
 static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_stream_t stream) {
+  // every linear of the layer may split K on the tcgen05 path: partials go to the scratch region
+  void* const ws = s.splitk_bytes ? (char*)a->scratch + s.splitk : nullptr;
+  const int64_t wsb = (int64_t)s.splitk_bytes;
+  auto lin_args = [&](const dak_weight& w, long long M, long long K, int N, const void* x, void* y, const void* residual,
+                      int act, const dak_launch_cfg& cfg) {
+    dak_linear_args l = layer::lin_args(w, M, K, N, x, y, residual, act, cfg);
+    l.workspace = ws;
+    l.workspace_bytes = wsb;
+    return l;
+  };
   const bool fuse = a->fuse_norm != 0;
   if ((fuse && (!a->stats_in || a->stats_in_parts <= 0)) || a->ln1_b || a->ln2_b)
     return fail(DAK_EINVAL, "dak_layer (Llama): RMSNorm weights have no bias; fuse_norm needs stats_in");
@@ -413,6 +427,15 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   void* attn = sc + s.attn;
   void* f = sc + s.f;
   float* o_stats = (float*)(sc + s.stats);
+  void* const ws = s.splitk_bytes ? sc + s.splitk : nullptr;
+  const int64_t wsb = (int64_t)s.splitk_bytes;
+  auto lin_args = [&](const dak_weight& w, long long M, long long K, int N, const void* x, void* y, const void* residual,
+                      int act, const dak_launch_cfg& cfg) {
+    dak_linear_args l = layer::lin_args(w, M, K, N, x, y, residual, act, cfg);
+    l.workspace = ws;
+    l.workspace_bytes = wsb;
+    return l;
+  };
   const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads;
   const long long qkv_cols = (long long)(Hq + 2 * Hkv) * d;
   const int pdl = a->cfg.pdl;
@@ -438,7 +461,7 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
     const dak_weight* w[3] = {&a->q, &a->k, &a->v};
     long long off = 0;
     for (int i = 0; i < 3; ++i) {
-      l = layer::lin_args(*w[i], rows[i], H, B, h, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
+      l = lin_args(*w[i], rows[i], H, B, h, qkv + off * 2, nullptr, DAK_ACT_NONE, a->cfg);
       l.ldy = qkv_cols;
       if (fuse) norm(l, a->ln1_w, a->ln1_b, a->stats_in, a->stats_in_parts);
       if (i < 2) pf(l, *w[i + 1], rows[i + 1], H);
@@ -447,7 +470,7 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
       off += rows[i];
     }
   } else {
-    l = layer::lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
+    l = lin_args(a->qkv, qkv_cols, H, B, h, qkv, nullptr, DAK_ACT_NONE, a->cfg);
     if (fuse) norm(l, a->ln1_w, a->ln1_b, a->stats_in, a->stats_in_parts);
     pf(l, a->o, H, (long long)Hq * d);
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
@@ -468,7 +491,7 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   at.cfg.pdl = pdl;
   at.q_row_stride = qkv_cols;
   if ((st = dak_attention(&at, strm)) != DAK_OK) return st;
-  l = layer::lin_args(a->o, H, (long long)Hq * d, B, attn, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  l = lin_args(a->o, H, (long long)Hq * d, B, attn, a->x, a->x, DAK_ACT_NONE, a->cfg);
   pf(l, a->up, a->ffn, H);
   int o_parts = 0;
   if (fuse) {
@@ -480,11 +503,11 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
   }
   if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   if (!fuse && (st = dak_layernorm(a->x, a->ln2_w, a->ln2_b, h, B, H, a->ln_eps, pdl, strm)) != DAK_OK) return st;
-  l = layer::lin_args(a->up, a->ffn, H, B, h, f, nullptr, DAK_ACT_RELU, a->cfg);
+  l = lin_args(a->up, a->ffn, H, B, h, f, nullptr, DAK_ACT_RELU, a->cfg);
   if (fuse) norm(l, a->ln2_w, a->ln2_b, o_stats, o_parts);
   pf(l, a->down, H, a->ffn);
   if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-  l = layer::lin_args(a->down, H, a->ffn, B, f, a->x, a->x, DAK_ACT_NONE, a->cfg);
+  l = lin_args(a->down, H, a->ffn, B, f, a->x, a->x, DAK_ACT_NONE, a->cfg);
   if (pfb > 0 && a->next_w_hbm && a->next_w_hbm_bytes > 0) {
     l.l2_prefetch = a->next_w_hbm;
     l.l2_prefetch_bytes = std::min(pfb, (long long)a->next_w_hbm_bytes) & ~15LL;

@@ -68,6 +68,9 @@ struct __align__(64) Params {
   int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
+  int ksplit;       // tcgen05 split-K: K splits (1: off); CTA = (tier row block of 128, split)
+  int k64_split;    // 64-column chunks per split
+  float* part;      // split-K fp32 partials [ksplit][N][M] (workspace)
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
   const __nv_bfloat16* ln_w;
   const __nv_bfloat16* ln_b;
@@ -763,13 +766,23 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   const bool host = cta < p.n_host;
   long long rb, re;
   const long long R_tier = host ? p.h : p.M - p.h;
-  tier_rows(R_tier, host ? cta : cta - p.n_host, host ? p.n_host : p.n_hbm, p.rgran, &rb, &re);
+  int kbeg = 0, kend = (int)(p.K / 64), ks = 0;  // this CTA's 64-column chunks [kbeg, kend)
+  if (p.ksplit > 1) {  // split-K: (128-row block, K split) per CTA; splits fixed by K alone
+    const int j = host ? cta : cta - p.n_host;
+    ks = j % p.ksplit;
+    rb = (long long)(j / p.ksplit) * 128;
+    re = rb + 128 < R_tier ? rb + 128 : R_tier;
+    kbeg = ks * p.k64_split;
+    kend = kbeg + p.k64_split < kend ? kbeg + p.k64_split : kend;
+  } else {
+    tier_rows(R_tier, host ? cta : cta - p.n_host, host ? p.n_host : p.n_hbm, p.rgran, &rb, &re);
+  }
   const int R = (int)(re - rb);
   const long long row0 = host ? rb : p.h + rb;
   const char* wsrc = host ? p.w_host : p.w_hbm;
   const int slots = host ? p.window : p.stages;
   const int wstage = host ? p.w_stage_host : p.w_stage_bytes;
-  const int nchunks = (int)(p.K / 64);
+  const int nchunks = kend - kbeg;
   const int N = p.N;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mtiles = (R + 127) >> 7;
@@ -808,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   if (warp == 0) {
     if (lane == 0) {  // producer: W span + x box per 64-column stage
       const int pro = min(slots, nchunks);
-      const char* src = wsrc + rb * 128;
+      const char* src = wsrc + rb * 128 + (long long)kbeg * chunk_stride;
       const uint64_t pol = policy_evict_first();
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
@@ -826,8 +839,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       }
       auto load_x = [&](int slot, int i) {
         unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
-        tma_3d(dst, xmap, 0, 0, i, &full[slot]);
-        if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K >> 6) + i), &full[slot]);
+        tma_3d(dst, xmap, 0, 0, kbeg + i, &full[slot]);
+        if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K >> 6) + kbeg + i), &full[slot]);
       };
       for (int i = 0; i < pro; ++i) load_x(i, i);
       int s = pro == slots ? 0 : pro;
@@ -921,7 +934,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
           v.z = swiglu_pair(v.z, u.z); v.w = swiglu_pair(v.w, u.w);
         } else {
           const float mu = n < N ? s_ln[n] : 0.f, rs = n < N ? s_ln[256 + n] : 0.f;
-          const int k0 = i * 64 + c * 8;
+          const int k0 = (kbeg + i) * 64 + c * 8;
           const uint4 wv = *reinterpret_cast<const uint4*>(lnres + k0 * 2);
           const uint4 bv = has_lnb ? *reinterpret_cast<const uint4*>(lnres + (p.K + k0) * 2) : make_uint4(0, 0, 0, 0);
           v.x = ln_pair(v.x, wv.x, bv.x, mu, rs); v.y = ln_pair(v.y, wv.y, bv.y, mu, rs);
@@ -973,6 +986,16 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = k == 0 ? __uint_as_float(v[e]) : acc[e] + __uint_as_float(v[e]);
+        }
+        if (p.ksplit > 1) {  // raw fp32 partial; bias / act / residual in splitk_reduce_kernel
+          if (r < R) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int n = c0 + e;
+              if (n < N) p.part[((size_t)ks * N + n) * p.M + m] = acc[e];
+            }
+          }
+          continue;
         }
         if (r < R) {
 #pragma unroll
@@ -1026,6 +1049,24 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
 }
 
 #if DAK_LINEAR_PART == 0
+// y[n, m] = act(sum_s part[s][n][m] + bias[m]) + residual[n, m]: the fixed-order split-K combine
+__global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int N, long long M,
+                                     const __nv_bfloat16* __restrict__ bias, int act,
+                                     const __nv_bfloat16* residual, __nv_bfloat16* y, long long ldy) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const long long total = (long long)N * M;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long n = i / M, m = i - n * M;
+    float v = part[i];
+    for (int s = 1; s < S; ++s) v += part[(long long)s * total + i];
+    if (bias) v += __bfloat162float(bias[m]);
+    if (act == DAK_ACT_RELU) v = fmaxf(v, 0.f);
+    if (residual) v += __bfloat162float(residual[n * ldy + m]);
+    y[n * ldy + m] = __float2bfloat16_rn(v);
+  }
+}
+
 // ------------------------------------------------------------------------------------ packing
 // dst[c][r][kc] with 16-byte chunk sl of row r stored at swz(r, sl); one thread per 16 B.
 __global__ void pack_kernel(const uint4* __restrict__ src, long long rows, long long K, int kc, uint4* __restrict__ dst) {
@@ -1205,8 +1246,25 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       mc = 1;
     }
   }
-  const long long rmax_host = n_host ? ceil_div(ceil_div(h, rg), n_host) * rg : 0;
-  const long long rmax_hbm = n_hbm ? ceil_div(ceil_div(M - h, rg), n_hbm) * rg : 0;
+  // tcgen05 split-K: an M = 128 tile costs the same time however few of its rows are real, so when
+  // the auto partition leaves < 128 rows per CTA, CTAs take (128-row block, K split) items instead;
+  // splits are fixed by K alone (1024 columns each), keeping every row's summation order
+  // independent of the tier split (bitwise r-invariance). Needs caller workspace for the partials.
+  int ksplit = 1, k64_split = (int)(K / 64);
+  if (path == 3 && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
+    const int S = (int)std::min<long long>(16, std::max<long long>(1, (K / 64) / 16));
+    const long long tiles = ceil_div(h, 128) + ceil_div(M - h, 128);
+    if (S > 1 && tiles * 128 < (long long)std::max(1, sms) * 128 && (n_hbm == 0 || ceil_div(M - h, n_hbm) < 128)) {
+      ksplit = S;
+      k64_split = (int)ceil_div(K / 64, S);
+      n_host = (int)ceil_div(h, 128) * S;
+      n_hbm = (int)ceil_div(M - h, 128) * S;
+    }
+  }
+  const long long rmax_host = ksplit > 1 ? std::min<long long>(h, 128)
+                                         : (n_host ? ceil_div(ceil_div(h, rg), n_host) * rg : 0);
+  const long long rmax_hbm = ksplit > 1 ? std::min<long long>(M - h, 128)
+                                        : (n_hbm ? ceil_div(ceil_div(M - h, rg), n_hbm) * rg : 0);
   const long long rmax = std::max(rmax_host, rmax_hbm);
   if (rmax > cap) return fail(DAK_EUNSUPPORTED, "dak_linear: %lld rows per CTA exceed the path capacity %lld (use a smaller kc)", rmax, cap);
 
@@ -1255,6 +1313,14 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.rgran = rg;
   if (path == 3) {
     const int cols = (n8 >= 128 ? 1 : 4) * (int)ceil_div(rmax, 128) * n8;  // k-chain accumulators
+    p.ksplit = ksplit;
+    p.k64_split = k64_split;
+    if (ksplit > 1) {
+      const size_t need = (size_t)ksplit * N * M * 4;
+      if (a->workspace_bytes < (int64_t)need) return fail(DAK_EINVAL, "dak_linear: split-K workspace %lld < %zu", (long long)a->workspace_bytes, need);
+      if (!aligned16(a->workspace)) return fail(DAK_EINVAL, "dak_linear: workspace must be 16-byte aligned");
+      p.part = (float*)a->workspace;
+    }
     p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
   }
   p.mc = mc;
@@ -1519,6 +1585,8 @@ static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
 #if DAK_LINEAR_PART == 0
 using namespace dak;
 
+static inline long long ceil_div_ll(long long a, long long b) { return (a + b - 1) / b; }
+
 extern "C" {
 
 size_t dak_linear_packed_bytes(int64_t rows, int64_t K, int32_t kc) {
@@ -1600,7 +1668,32 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
   if (pl.grid && !(pl.p.y)) return fail(DAK_EINVAL, "dak_linear: y NULL");
   if (pl.grid && (st = lin::encode_xmap(&pl.p)) != DAK_OK) return st;
   pl.p.trace = trace_slot(DAK_KIND_LINEAR, args->M, args->K, pl.grid);
-  return lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl);
+  if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
+  if (pl.p.ksplit > 1) {
+    const long long total = (long long)args->N * args->M;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = args->cfg.pdl ? 1 : 0;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)std::min<long long>(ceil_div_ll(total, 256), 148LL * 8));
+    cfg.blockDim = dim3(256);
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, lin::splitk_reduce_kernel, (const float*)pl.p.part, pl.p.ksplit, (int)args->N,
+                                    (long long)args->M, pl.p.bias, pl.p.act, pl.p.residual, pl.p.y, pl.p.ldy));
+  }
+  return DAK_OK;
+}
+
+size_t dak_linear_workspace_size(const dak_linear_args* args) {
+  if (!args) return 0;
+  dak_linear_args a = *args;
+  a.workspace = (void*)16;  // probe: would the plan split K?
+  a.workspace_bytes = INT64_MAX;
+  lin::Plan pl;
+  if (lin::make_plan(&a, &pl) != DAK_OK || pl.p.ksplit <= 1) return 0;
+  return (size_t)pl.p.ksplit * a.N * a.M * 4;
 }
 
 }  // extern "C"

@@ -62,7 +62,8 @@ class dak_linear_args(C.Structure):
                 ("ldy", C.c_int64), ("l2_prefetch", C.c_void_p), ("l2_prefetch_bytes", C.c_int64),
                 ("ln_w", C.c_void_p), ("ln_b", C.c_void_p), ("ln_stats", C.c_void_p), ("ln_parts", C.c_int32),
                 ("ln_rms", C.c_int32), ("ln_eps", C.c_float), ("reserved2", C.c_int32), ("stats_out", C.c_void_p),
-                ("x_swiglu", C.c_int32), ("reserved3", C.c_int32)]
+                ("x_swiglu", C.c_int32), ("reserved3", C.c_int32), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_int64)]
 
 
 class dak_linear_launch_info(C.Structure):
@@ -97,6 +98,7 @@ _sig("dak_linear_query", C.c_int32, [C.POINTER(dak_linear_args), C.POINTER(dak_l
 _sig("dak_linear_cta_rows", C.c_int32, [C.POINTER(dak_linear_args), C.c_int32, C.POINTER(C.c_int32),
                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 _sig("dak_linear", C.c_int32, [C.POINTER(dak_linear_args), C.c_void_p])
+_sig("dak_linear_workspace_size", C.c_size_t, [C.POINTER(dak_linear_args)])
 
 class dak_attention_args(C.Structure):
     _fields_ = [("q", C.c_void_p), ("out", C.c_void_p), ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p),
@@ -116,7 +118,7 @@ _sig("dak_kv_append", C.c_int32, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
 EXPORTED = ["dak_pack_kv_pages", "dak_attention_workspace_size", "dak_attention", "dak_kv_append",
             "dak_last_error", "dak_version", "dak_device_sms", "dak_plan_ratios", "dak_host_alloc", "dak_host_free",
             "dak_linear_packed_bytes", "dak_pack_linear", "dak_linear_default_kc", "dak_linear_query",
-            "dak_linear_cta_rows", "dak_linear", "dak_trace_enable", "dak_trace_count", "dak_trace_launch"]
+            "dak_linear_cta_rows", "dak_linear", "dak_linear_workspace_size", "dak_trace_enable", "dak_trace_count", "dak_trace_launch"]
 
 
 def _check(st: int):
@@ -248,6 +250,10 @@ def linear_args(w_host, w_hbm, M, K, h, kc, N, x, y, bias=None, residual=None, a
 
 def linear(args: dak_linear_args, stream=None):
     _check(lib.dak_linear(C.byref(args), _stream(stream)))
+
+
+def linear_workspace_size(args: dak_linear_args) -> int:
+    return int(lib.dak_linear_workspace_size(C.byref(args)))
 
 
 def linear_query(args: dak_linear_args) -> dict:

@@ -437,6 +437,12 @@ class DakOPT:
             dak.layernorm(self.x, self.lnf_w, self.lnf_b, self.h, self.B, c.hidden, 1e-5, pdl=self.pdl, stream=stream)
             ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
                                  self.h, self.logits, cfg=self.launch)
+        if self.B > 16:  # tcgen05 split-K partials for the head
+            need = dak.linear_workspace_size(ha)
+            if need:
+                if getattr(self, "head_ws", None) is None or self.head_ws.numel() < need:
+                    self.head_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+                ha.workspace, ha.workspace_bytes = self.head_ws.data_ptr(), self.head_ws.numel()
         dak.linear(ha, stream)
 
     def advance(self, stream=None):

@@ -292,3 +292,47 @@ def test_linear_tcgen05_operand_transforms(D, torch, xf, N):
     torch.cuda.synchronize()
     ref = Kx.split_linear(W[:h], W[h:], synth.bf16_bits(hx.astype(np.float32)))
     assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
+
+
+@pytest.mark.parametrize("M,K,N,h", [(1280, 8192, 64, 0), (1024, 8192, 48, 32), (7168, 8192, 64, 48), (300, 2048, 16, 0)])
+def test_linear_tcgen05_split_k(D, torch, M, K, N, h):
+    """tcgen05 with few rows per CTA: (128-row block, K split) items, fp32 partials in the caller's
+    workspace, fixed-order combine kernel (bias / residual applied there), against the oracle."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, M + N), bias=True)
+    g = synth.rng(M + N)
+    res = synth.normal_bf16(g, (N, M), 1.0)
+    sl = SplitLinear(D, W, h, 64)
+    xd, bd, rd = to_dev(x), to_dev(b), to_dev(res)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    a = sl.args(xd, y, N, bias=bd, residual=rd, force_path=3)
+    ws = D.linear_workspace_size(a)
+    assert ws > 0
+    wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
+    a.workspace, a.workspace_bytes = wsb.data_ptr(), ws
+    D.linear(a)
+    torch.cuda.synchronize()
+    ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b, residual_bits=res)
+    assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
+
+
+def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch):
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    M, K, N = 1280, 4096, 32
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, 3), kind="int")
+    outs = []
+    for h in (0, 128, 640):
+        sl = SplitLinear(D, W, h, 64)
+        xd = to_dev(x)
+        y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+        a = sl.args(xd, y, N, force_path=3)
+        ws = D.linear_workspace_size(a)
+        assert ws > 0
+        wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
+        a.workspace, a.workspace_bytes = wsb.data_ptr(), ws
+        D.linear(a)
+        torch.cuda.synchronize()
+        outs.append(from_dev(y))
+    ref = Kx.split_linear(W[:0], W, x)
+    assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(ref))
+    assert np.array_equal(outs[1], outs[0]) and np.array_equal(outs[2], outs[0])
