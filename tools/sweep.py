@@ -5,6 +5,8 @@
        EB(r) = 1 / max((1 - r) / B_g, r / B_l)  (equals B_g + B_l at r* = B_l / (B_g + B_l))
   c4   GQA decode attention, 64 q / 8 kv heads, 131072 tokens, B in {1, 4}, host share r of the
        oldest KV chunks in {0, r*, 0.5}
+  pf   direct split access vs the prefetch-to-HBM baseline (copy the host rows into HBM
+       with the copy engine, then run the GEMV from HBM) on fc1 28672x7168 at N=8 over r
 Prints one JSON line per point. B_g: MEASURED_PEAKS.json HBM copy; B_l: measured link 51.5 GB/s.
 """
 from __future__ import annotations
@@ -125,6 +127,65 @@ def c4():
             dak.host_free(vh[0])
             del kg, vg
             torch.cuda.empty_cache()
+
+
+def _cudart():
+    import ctypes
+    import glob
+    for cand in glob.glob("/usr/local/cuda/lib64/libcudart.so*") + ["libcudart.so.12", "libcudart.so"]:
+        try:
+            lib = ctypes.CDLL(cand)
+            lib.cudaMemcpyAsync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int,
+                                            ctypes.c_void_p]
+            return lib
+        except OSError:
+            continue
+    raise RuntimeError("libcudart not found")
+
+
+def pf():
+    """Per r: (a) direct: one dak_linear reading the h host rows over the link while the rest
+    streams from HBM (DAK); (b) prefetch: cudaMemcpyAsync (copy engine) of the h host rows into
+    HBM, then one all-HBM dak_linear. Both timed per call with events, median of 5."""
+    bg, bl = peaks()
+    M, K, N, kc = 28672, 7168, 8, 64
+    rs = bl / (bg + bl)
+    rt = _cudart()
+    x = torch.randn(N, K, device="cuda").to(torch.bfloat16)
+    y = torch.empty(N, M, device="cuda", dtype=torch.bfloat16)
+    w_all = torch.randn(M * K, device="cuda").to(torch.bfloat16)  # HBM image of the whole matrix
+    for r in sorted({0.0, rs, 2 * rs, 0.02, 0.05, 0.1, 0.2, 0.5}):
+        h = min(M, int(round(r * M / 16)) * 16)
+        hp, dp = dak.host_alloc(max(h * K * 2, 16))
+        if h:
+            dak.pack_linear(torch.randn(h * K, device="cuda").to(torch.bfloat16), h, K, kc, dp)
+        direct = dak.linear_args(dp if h else None, w_all[h * K:], M, K, h, kc, N, x, y, cfg=dict(pdl=0))
+        pref = dak.linear_args(None, w_all, M, K, 0, kc, N, x, y, cfg=dict(pdl=0))
+        s_ = torch.cuda.Stream()
+        times = {}
+        for name in ("direct", "prefetch"):
+            def run():
+                if name == "direct":
+                    dak.linear(direct, s_)
+                else:
+                    if h:
+                        assert rt.cudaMemcpyAsync(w_all.data_ptr(), hp, h * K * 2, 1, s_.cuda_stream) == 0
+                    dak.linear(pref, s_)
+            run()
+            s_.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ts = []
+            for _ in range(5):
+                e0.record(s_)
+                run()
+                e1.record(s_)
+                s_.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e3)
+            times[name] = float(np.median(ts))
+        print(json.dumps(dict(exp="pf", M=M, K=K, N=N, r=round(h / M, 5), h=h, direct_us=round(times["direct"], 1),
+                              prefetch_us=round(times["prefetch"], 1),
+                              speedup_direct_over_prefetch=round(times["prefetch"] / times["direct"], 3))), flush=True)
+        dak.host_free(hp)
 
 
 if __name__ == "__main__":
