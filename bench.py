@@ -269,6 +269,8 @@ def main():
     ap.add_argument("--plan-link-gbs", type=float, default=None,
                     help="host-link rate the planner assumes (default: the calibrated peak)")
     ap.add_argument("--plan-hbm-gbs", type=float, default=None, help="HBM rate the planner assumes")
+    ap.add_argument("--plan-host-latency-us", type=float, default=0.0,
+                    help="host-path latency the planner charges an op reading host bytes (latency-aware mode)")
     ap.add_argument("--layers", type=int, default=None,
                     help="layers (default: all 48 for OPT-30B; 8 of 80 for the Llama subset, labelled)")
     ap.add_argument("--workload", default="opt30b", choices=["opt30b", "llama3-70b-tp8"],
@@ -286,7 +288,8 @@ def main():
     world, rank, local = dist_setup()
     hbm_gbs, link_gbs, peak_src = measured_peaks()
     ph, pl, plan_src = planner_rates(hbm_gbs, link_gbs)
-    hw = HW(hbm_bps=(a.plan_hbm_gbs or ph) * 1e9, link_bps=(a.plan_link_gbs or pl) * 1e9)
+    hw = HW(hbm_bps=(a.plan_hbm_gbs or ph) * 1e9, link_bps=(a.plan_link_gbs or pl) * 1e9,
+            host_latency_s=a.plan_host_latency_us * 1e-6)
     llama = a.workload == "llama3-70b-tp8"
     if llama:
         eng, cfg, wl = make_llama(a, hw, world, rank, dak)
@@ -420,7 +423,7 @@ def main():
                             l2="inputs (60 GB of weights) >> 126 MB L2; no flush",
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
                             planner_rates_gbs=dict(hbm=round(hw.hbm_bps / 1e9, 1), link=round(hw.link_bps / 1e9, 2),
-                                                   source=plan_src),
+                                                   host_latency_us=a.plan_host_latency_us, source=plan_src),
                             execution="persistent step (dak_step, 1 launch)" if a.persistent else "per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world)),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,

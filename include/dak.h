@@ -63,12 +63,16 @@ dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, in
  * ============================================================================================= */
 
 /* Machine model. B_g = hbm_bps; B_h = min(link_bps, host_dram_bps) (P:L216 footnote).
- * Bandwidths in bytes/s (> 0). host_capacity_bytes < 0 means unlimited. */
+ * Bandwidths in bytes/s (> 0). host_capacity_bytes < 0 means unlimited. host_latency_s >= 0
+ * (latency-aware extension): an op reading any host byte pays it once,
+ * T_h = y/B_h + tau, which moves each op's balance point to T* = max(T, (C + B_h tau)/(B_g + B_h));
+ * 0 reproduces the paper's model exactly. */
 typedef struct {
   double hbm_bps;
   double link_bps;
   double host_dram_bps;
   int64_t host_capacity_bytes;
+  double host_latency_s;
 } dak_hw;
 
 #define DAK_OP_LINEAR 0     /* C_i = weight bytes                              (P:L422 fn) */

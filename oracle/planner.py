@@ -52,14 +52,15 @@ def machine_balance(peak_flops, hbm_bw):
 # ----------------------------------------------------------------------------------------------
 
 
-def op_latency(C, T, y, Bg, Bh):
+def op_latency(C, T, y, Bg, Bh, tau=0):
     """Latency of an op with C offloadable bytes, compute time T, y bytes on host.
 
     max(T_comp, T_mem), T_mem = max(T_h, T_g), T_g = (C-y)/B_g, T_h = y/B_h  (P:L422, P:L426).
-    Works with float or Fraction arguments.
+    tau (latency-aware extension): a fixed host-path latency paid once the
+    op reads any host byte, T_h = y/B_h + tau for y > 0. Works with float or Fraction arguments.
     """
     tg = (C - y) / Bg
-    th = y / Bh
+    th = y / Bh + (tau if y > 0 else 0)
     return max(T, max(tg, th))
 
 
@@ -77,32 +78,37 @@ def turning_point_paper(C, T, Bg, Bh, memory_bound: bool):
     return min(1, Bh / Bi)
 
 
-def thresholds_exact(C, T, Bg, Bh):
+def thresholds_exact(C, T, Bg, Bh, tau=0):
     """Reading R1 (exact arithmetic): T* = max(T, C/(Bg+Bh)), a = max(0, C - Bg T*), b = min(C, Bh T*).
 
     L(y) decreases with slope -1/Bg on [0,a], is flat (= T*) on [a,b], increases with slope 1/Bh
     on [b, C]. For a memory-bound op (T <= C/(Bg+Bh)) a = b = C*Bh/(Bg+Bh)  (P:L426);
     for a compute-bound op (T >= C/Bg) a = 0 and b = C*min(1, Bh/B_i).
+    With a host latency tau the balance moves to T* = max(T, (C + Bh tau)/(Bg + Bh)) and the
+    host side of the flat segment ends at b = min(C, Bh (T* - tau)) (b >= a); tau = 0 is R1.
     """
-    C, T, Bg, Bh = (Fraction(v) for v in (C, T, Bg, Bh))
-    Ts = max(T, C / (Bg + Bh))
+    C, T, Bg, Bh, tau = (Fraction(v) for v in (C, T, Bg, Bh, tau))
+    Ts = max(T, (C + Bh * tau) / (Bg + Bh))
     a = max(Fraction(0), C - Bg * Ts)
-    b = min(C, Bh * Ts)
+    b = max(a, min(C, Bh * (Ts - tau)))
     return Ts, a, b
 
 
-def thresholds_double(C: float, T: float, Bg: float, Bh: float):
+def thresholds_double(C: float, T: float, Bg: float, Bh: float, tau: float = 0.0):
     """Reading R6: the same thresholds in IEEE double in this exact operation order
-    (the C++ planner mirrors it bit-for-bit; compiled with -ffp-contract=off)."""
-    Ts = C / (Bg + Bh)
+    (the C++ planner mirrors it bit-for-bit; compiled with -ffp-contract=off). tau = 0 gives
+    exactly the R1 values (C + 0.0 == C, x - 0.0 == x)."""
+    Ts = (C + Bh * tau) / (Bg + Bh)
     if T > Ts:
         Ts = T
     a = C - Bg * Ts
     if a < 0.0:
         a = 0.0
-    b = Bh * Ts
+    b = Bh * (Ts - tau)
     if b > C:
         b = C
+    if b < a:
+        b = a
     return Ts, a, b
 
 
@@ -225,7 +231,7 @@ def _unit_bytes_of(k: int, n: int, u: int, C: int) -> int:
 
 
 def plan_units(ops: Sequence[dict], Bg: float, Bh: float, y_req: int, mode: int,
-               host_capacity: int | None = None):
+               host_capacity: int | None = None, tau: float = 0.0):
     """Greedy per-op offload plan at unit granularity (P:L475-482 with readings R4-R6).
 
     ops: dicts with n_units, unit_bytes, total_bytes (ints) and T (seconds, float).
@@ -263,7 +269,7 @@ def plan_units(ops: Sequence[dict], Bg: float, Bh: float, y_req: int, mode: int,
 
     a_u, b_u = [], []
     for i in range(n_ops):
-        _, a, b = thresholds_double(float(C[i]), T[i], Bg, Bh)
+        _, a, b = thresholds_double(float(C[i]), T[i], Bg, Bh, tau)
         au = math.floor(a / float(u[i]) + 0.5)
         au = min(max(au, 0), n[i])
         bu = math.floor(b / float(u[i]))
@@ -340,7 +346,7 @@ def plan_units(ops: Sequence[dict], Bg: float, Bh: float, y_req: int, mode: int,
     for i in range(n_ops):
         hbf = float(host_bytes[i])
         tg = (float(C[i]) - hbf) / Bg
-        th = hbf / Bh
+        th = hbf / Bh + (tau if host_bytes[i] > 0 else 0.0)
         lat = tg if tg > th else th
         if T[i] > lat:
             lat = T[i]

@@ -31,6 +31,8 @@ extern "C" dak_status dak_plan_ratios(const dak_hw* hw, const dak_op* ops, int32
   const double Bh = hw->link_bps < hw->host_dram_bps ? hw->link_bps : hw->host_dram_bps;
   if (!(Bg > 0.0) || !(Bh > 0.0)) return dak::fail(DAK_EINVAL, "dak_plan_ratios: bandwidths must be positive");
   if (y_req < 0) return dak::fail(DAK_EINVAL, "dak_plan_ratios: y_req < 0");
+  const double tau = hw->host_latency_s;
+  if (!(tau >= 0.0)) return dak::fail(DAK_EINVAL, "dak_plan_ratios: host_latency_s must be >= 0");
 
   std::vector<OpU> op(n_ops);
   __int128 total = 0;
@@ -47,16 +49,18 @@ extern "C" dak_status dak_plan_ratios(const dak_hw* hw, const dak_op* ops, int32
     return dak::fail(DAK_ECAPACITY, "dak_plan_ratios: required host bytes %lld exceed offloadable bytes / host capacity",
                      (long long)y_req);
 
-  // thresholds (reading R1, order R6): T* = max(T, C/(Bg+Bh)); a = max(0, C - Bg T*); b = min(C, Bh T*)
+  // thresholds (reading R1, order R6; host latency tau): T* = max(T, (C + Bh tau)/(Bg+Bh));
+  // a = max(0, C - Bg T*); b = max(a, min(C, Bh (T* - tau))). tau = 0 is exactly R1.
   std::vector<int64_t> a_u(n_ops), b_u(n_ops);
   for (int i = 0; i < n_ops; ++i) {
     const double C = (double)op[i].C;
-    double Ts = C / (Bg + Bh);
+    double Ts = (C + Bh * tau) / (Bg + Bh);
     if (op[i].T > Ts) Ts = op[i].T;
     double a = C - Bg * Ts;
     if (a < 0.0) a = 0.0;
-    double b = Bh * Ts;
+    double b = Bh * (Ts - tau);
     if (b > C) b = C;
+    if (b < a) b = a;
     int64_t au = (int64_t)std::floor(a / (double)op[i].u + 0.5);  // round half up
     au = std::min(std::max(au, (int64_t)0), op[i].n);
     int64_t bu = (int64_t)std::floor(b / (double)op[i].u);
@@ -138,7 +142,7 @@ extern "C" dak_status dak_plan_ratios(const dak_hw* hw, const dak_op* ops, int32
     const int64_t hbytes = unit_bytes_of(units[i], op[i]);
     const double hbf = (double)hbytes;
     const double tg = ((double)op[i].C - hbf) / Bg;  // T_g
-    const double th = hbf / Bh;                       // T_h
+    const double th = hbf / Bh + (hbytes > 0 ? tau : 0.0);  // T_h (+ host latency)
     double lat = tg > th ? tg : th;
     if (op[i].T > lat) lat = op[i].T;                 // max(T_comp, T_mem)
     out[i].host_units = units[i];

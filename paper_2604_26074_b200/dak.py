@@ -36,7 +36,7 @@ lib = C.CDLL(_LIB_PATH)
 # ------------------------------------------------------------------------------------- structs
 class dak_hw(C.Structure):
     _fields_ = [("hbm_bps", C.c_double), ("link_bps", C.c_double), ("host_dram_bps", C.c_double),
-                ("host_capacity_bytes", C.c_int64)]
+                ("host_capacity_bytes", C.c_int64), ("host_latency_s", C.c_double)]
 
 
 class dak_op(C.Structure):
@@ -182,7 +182,7 @@ def plan_ratios(hw: dict, ops: list, y_req_bytes: int, mode: int = PLAN_EXACT):
     """dak_plan_ratios: hw = {hbm_bps, link_bps, host_dram_bps, host_capacity_bytes};
     ops = [{kind, n_units, unit_bytes, total_bytes, T}]. Returns (list of plan dicts, objective)."""
     h = dak_hw(float(hw["hbm_bps"]), float(hw["link_bps"]), float(hw.get("host_dram_bps", hw["link_bps"])),
-               int(hw.get("host_capacity_bytes", -1)))
+               int(hw.get("host_capacity_bytes", -1)), float(hw.get("host_latency_s", 0.0)))
     n = len(ops)
     arr = (dak_op * max(n, 1))()
     for i, o in enumerate(ops):

@@ -44,10 +44,12 @@ class HW:
     link_bps: float
     host_dram_bps: float = 0.0
     peak_flops: float = 1.3554e15
+    host_latency_s: float = 0.0  # latency-aware planner extension (dak_hw.host_latency_s)
 
     def as_dict(self):
         return dict(hbm_bps=self.hbm_bps, link_bps=self.link_bps,
-                    host_dram_bps=self.host_dram_bps or self.link_bps, host_capacity_bytes=-1)
+                    host_dram_bps=self.host_dram_bps or self.link_bps, host_capacity_bytes=-1,
+                    host_latency_s=self.host_latency_s)
 
 
 @dataclass

@@ -73,8 +73,10 @@ def test_planner_bit_exact_vs_oracle(D):
         Bg = float(g.choice([7.38e12, 6.5555e12, 4.0e12]))
         Bh = float(g.choice([51.5e9, 450e9, 64e9]))
         dram = Bh * float(g.choice([1.0, 2.0]))
-        ref = P.plan_units(ops, Bg, min(Bh, dram), y_req, mode)
-        got, obj = D.plan_ratios(dict(hbm_bps=Bg, link_bps=Bh, host_dram_bps=dram), ops, y_req, mode)
+        tau = float(g.choice([0.0, 0.0, 2.4e-6, 1e-5]))  # host latency (latency-aware extension)
+        ref = P.plan_units(ops, Bg, min(Bh, dram), y_req, mode, tau=tau)
+        got, obj = D.plan_ratios(dict(hbm_bps=Bg, link_bps=Bh, host_dram_bps=dram, host_latency_s=tau), ops, y_req,
+                                 mode)
         for i in range(len(ops)):
             assert got[i]["host_units"] == ref["host_units"][i]
             assert got[i]["host_bytes"] == ref["host_bytes"][i]

@@ -330,3 +330,27 @@ def test_global_ratio_capacity_error():
     with pytest.raises(P.PlanError):
         P.global_offload_ratio(100, 100, 50, host_capacity=10)
     assert P.global_offload_ratio(10, 10, 50) == 0
+
+
+def test_latency_aware_thresholds_pins():
+    """Host latency tau: tau = 0 is the paper's model; for a memory-bound op
+    the threshold a = b is the argmin of L(y) = max((C-y)/Bg, y/Bh + tau) (brute force on a
+    fine grid, exact Fractions); ops too small to amortise tau (C <= tau Bg) get no host share;
+    the double thresholds equal the exact ones to rounding."""
+    from fractions import Fraction as Fr
+    Bg, Bh = 6700e9, 47e9
+    for C, tau in ((102760448, 2.4e-6), (411041792, 2.4e-6), (10_000_000, 2.4e-6), (411041792, 0.0)):
+        Ts, a, b = P.thresholds_exact(C, 0, Bg, Bh, tau)
+        if C <= tau * Bg:
+            assert a == 0
+            continue
+        assert a == b
+        grid = [Fr(C) * k / 20000 for k in range(0, 400)]  # y in [0, 2% of C]
+        best = min(grid, key=lambda y: P.op_latency(Fr(C), Fr(0), y, Fr(Bg), Fr(Bh), Fr(tau)))
+        assert abs(best - a) <= Fr(C, 20000)
+        assert P.op_latency(Fr(C), Fr(0), a, Fr(Bg), Fr(Bh), Fr(tau)) == Ts
+        Tsd, ad, bd = P.thresholds_double(float(C), 0.0, Bg, Bh, tau)
+        assert abs(ad - float(a)) <= 1e-6 * C and abs(Tsd - float(Ts)) <= 1e-12
+    # tau = 0 reproduces R1 bit for bit
+    for C, T in ((102760448, 0.0), (411041792, 1e-4), (12345, 3e-9)):
+        assert P.thresholds_double(float(C), T, Bg, Bh, 0.0) == P.thresholds_double(float(C), T, Bg, Bh)
