@@ -79,13 +79,17 @@ class DakOPT:
     """OPT decode step over HBM + pinned host memory at per-op planned ratios."""
 
     def __init__(self, cfg: OPTConfig, batch: int, context: int, hw: HW, mode: int = dak.PLAN_BALANCED,
-                 y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 16, seed: int = 0,
+                 y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 0, seed: int = 0,
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
                  host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
                  evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
                  max_context: int | None = None):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
+        if not chunk_pages:  # split-KV chunk: about one (request, kv head, chunk) unit per two warp slots (measured best)
+            pages = -(-max(context, max_context or 0) // page_size)
+            units_1 = batch * cfg.n_kv_heads * pages
+            self.chunk_pages = max(1, min(16, units_1 // (148 * 4)))
         self.pdl = int(pdl)
         self.n_cta_host = n_cta_host
         self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host,
@@ -116,7 +120,7 @@ class DakOPT:
         # KV pages per request cover max_context tokens: decode steps append beyond the prompt
         self.max_context = max(context, max_context or context)
         self.pages_per_req = -(-self.max_context // page_size)
-        self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
+        self.chunks_per_req = -(-self.pages_per_req // self.chunk_pages)
         self.plan = self._plan(mode, y_req, host_override)
         self._allocate(weights)
         self._kv()

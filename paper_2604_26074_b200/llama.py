@@ -43,7 +43,7 @@ class DakLlama:
 
     def __init__(self, cfg: LlamaConfig, batch: int, context: int, hw: HW, tp_rank: int = 0, tp_size: int = 1,
                  comm=None, mode: int = dak.PLAN_BALANCED, y_req: int = 0, unit_rows: int = 16, page_size: int = 64,
-                 chunk_pages: int = 16, seed: int = 0, pdl: bool = True, congestion_control: bool = True,
+                 chunk_pages: int = 0, seed: int = 0, pdl: bool = True, congestion_control: bool = True,
                  weights: dict | None = None, n_cta_host: int = 2, fuse_norm: bool | None = None):
         self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
         self.rank, self.world, self.comm = tp_rank, tp_size, comm
@@ -52,6 +52,10 @@ class DakLlama:
         self.fuse_norm = (batch <= 16) if fuse_norm is None else bool(fuse_norm)
         self.dims = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
         self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
+        if not chunk_pages:  # split-KV chunk: about one (request, kv head, chunk) unit per two warp slots (measured best)
+            pages = -(-context // page_size)
+            units_1 = batch * (cfg.n_kv_heads // tp_size) * pages
+            self.chunk_pages = max(1, min(16, units_1 // (148 * 4)))
         self.pdl = int(pdl)
         self.n_cta_host = n_cta_host
         self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host)
@@ -69,7 +73,7 @@ class DakLlama:
                                     down=LinearOp(f"L{i}.down", c.hidden, F)))
         self.head = LinearOp("lm_head", self.dims["vocab"], c.hidden)
         self.pages_per_req = -(-context // page_size)
-        self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
+        self.chunks_per_req = -(-self.pages_per_req // self.chunk_pages)
         self.plan = self._plan(mode, y_req)
         self._allocate(weights)
         self._kv()
