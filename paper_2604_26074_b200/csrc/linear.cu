@@ -767,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   long long rb, re;
   const long long R_tier = host ? p.h : p.M - p.h;
   int kbeg = 0, kend = (int)(p.K / 64), ks = 0;  // this CTA's 64-column chunks [kbeg, kend)
-  if (p.ksplit > 1) {  // split-K: (128-row block, K split) per CTA; splits fixed by K alone
+  if (p.ksplit > 1) {  // split-K: (128-row block, K split) per CTA; splits fixed by (M, K)
     const int j = host ? cta : cta - p.n_host;
     ks = j % p.ksplit;
     rb = (long long)(j / p.ksplit) * 128;
@@ -1248,17 +1248,25 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   // tcgen05 split-K: an M = 128 tile costs the same time however few of its rows are real, so when
   // the auto partition leaves < 128 rows per CTA, CTAs take (128-row block, K split) items instead;
-  // splits are fixed by K alone (1024 columns each), keeping every row's summation order
+  // splits are fixed by (M, K, SM count), never by the tier split h, keeping every row's summation order
   // independent of the tier split (bitwise r-invariance). Needs caller workspace for the partials.
   int ksplit = 1, k64_split = (int)(K / 64);
   if (path == 3 && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
-    const int S = (int)std::min<long long>(16, std::max<long long>(1, (K / 64) / 16));
-    const long long tiles = ceil_div(h, 128) + ceil_div(M - h, 128);
-    if (S > 1 && tiles * 128 < (long long)std::max(1, sms) * 128 && (n_hbm == 0 || ceil_div(M - h, n_hbm) < 128)) {
-      ksplit = S;
-      k64_split = (int)ceil_div(K / 64, S);
-      n_host = (int)ceil_div(h, 128) * S;
-      n_hbm = (int)ceil_div(M - h, 128) * S;
+    // S from (M, K, SM count) only: as many splits as keep all items in ONE wave (even if h adds a
+    // tile). Measured at the Llama TP8 b64 shapes (profiles/r01/splitk_sweep.txt): a second wave or
+    // shorter splits cost more than the idle SMs of a partial wave.
+    const long long C = K / 64, nsm = std::max(1, sms);
+    long long S = std::min<long long>(std::min<long long>(16, C), nsm / (ceil_div(M, 128) + 1));
+    long long bks = C;
+    if (S > 1) {
+      bks = ceil_div(C, S);
+      S = ceil_div(C, bks);
+    }
+    if (S > 1 && (n_hbm == 0 || ceil_div(M - h, n_hbm) < 128)) {
+      ksplit = (int)S;
+      k64_split = (int)bks;
+      n_host = (int)(ceil_div(h, 128) * S);
+      n_hbm = (int)(ceil_div(M - h, 128) * S);
     }
   }
   const long long rmax_host = ksplit > 1 ? std::min<long long>(h, 128)

@@ -34,7 +34,7 @@ def setup(M, K, N, h, kc, copies):
     return hbm, hosts, x, y
 
 
-def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu=False, **cfg):
+def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu=False, ws=False, **cfg):
     size = M * K * 2
     copies = max(2, min(64, int(np.ceil(4 * L2 / max(size, 1)))))
     hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
@@ -50,7 +50,15 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu
         a = dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg,
                             stats_out=st_out if stats else None, x_swiglu=int(swiglu), **ln_kw)
         args.append(a)
+    wsb = None
+    if ws:
+        need = dak.linear_workspace_size(args[0])
+        if need:
+            wsb = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            for a in args:
+                a.workspace, a.workspace_bytes = wsb.data_ptr(), need
     info = dak.linear_query(args[0])
+    info["ws"] = dak.linear_workspace_size(args[0]) if ws else 0
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         for a in args[:4]:
@@ -79,7 +87,7 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu
     torch.cuda.empty_cache()
     return dict(M=M, K=K, N=N, h=h, kc=kc, ln=ln, stats=stats, swiglu=swiglu, us=t * 1e6, gbs=alg / t / 1e9, hbm_gbs=(M - h) * K * 2 / t / 1e9,
                 host_gbs=h * K * 2 / t / 1e9, info={k: info[k] for k in ("grid", "n_cta_host", "stages_hbm", "window_host",
-                                                                        "smem_bytes", "path")}, cfg=cfg)
+                                                                        "smem_bytes", "path", "ws")}, cfg=cfg)
 
 
 def main():
@@ -87,6 +95,16 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "sk":  # split-K count at the Llama TP8 shard shapes, b64 (S from DAK_SPLITK_S)
+        for (M, K) in ((1280, 8192), (8192, 1024), (7168, 8192), (8192, 3584)):
+            for kc in [int(v) for v in os.environ.get("KCS", "64").split(",")]:
+                try:
+                    r = time_cfg(M, K, 64, 0, kc, pdl=1, force_path=3, ws=True)
+                except Exception as e:  # noqa: BLE001
+                    r = dict(M=M, K=K, kc=kc, error=str(e))
+                r["S"] = os.environ.get("DAK_SPLITK_S", "auto")
+                print(json.dumps(r), flush=True)
+        return
     if a.exp == "tcx":  # tcgen05 operand transforms at the Llama TP8 shard shapes, b64
         for (M, K, kw) in ((8192, 3584, dict(swiglu=True)), (7168, 8192, dict(ln=True)), (8192, 3584, {}),
                            (7168, 8192, {})):

@@ -13,6 +13,10 @@ hp, dp = dak.host_alloc(max(h * K * 2, 16)) if h else (None, None)
 x = torch.randn(N, K, device="cuda").to(torch.bfloat16)
 y = torch.empty(N, M, device="cuda", dtype=torch.bfloat16)
 a = dak.linear_args(dp, w, M, K, h, kc, N, x, y, cfg=dict(force_path=path, pdl=0))
+need = dak.linear_workspace_size(a) if path == 3 else 0
+if need:  # split-K workspace (tcgen05 path)
+    ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    a.workspace, a.workspace_bytes = ws.data_ptr(), need
 print(dak.linear_query(a))
 for _ in range(3):
     dak.linear(a)
