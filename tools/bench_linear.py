@@ -95,14 +95,13 @@ def main():
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
-    if a.exp == "sk":  # split-K count at the Llama TP8 shard shapes, b64 (S from DAK_SPLITK_S)
+    if a.exp == "sk":  # tcgen05 split-K at the Llama TP8 shard shapes, b64 (kc from env KCS, default 64)
         for (M, K) in ((1280, 8192), (8192, 1024), (7168, 8192), (8192, 3584)):
             for kc in [int(v) for v in os.environ.get("KCS", "64").split(",")]:
                 try:
                     r = time_cfg(M, K, 64, 0, kc, pdl=1, force_path=3, ws=True)
                 except Exception as e:  # noqa: BLE001
                     r = dict(M=M, K=K, kc=kc, error=str(e))
-                r["S"] = os.environ.get("DAK_SPLITK_S", "auto")
                 print(json.dumps(r), flush=True)
         return
     if a.exp == "tcx":  # tcgen05 operand transforms at the Llama TP8 shard shapes, b64
