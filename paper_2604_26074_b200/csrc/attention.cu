@@ -5,9 +5,10 @@
 // Work is split flash-decoding style into units (request b, kv head g, chunk c of chunk_pages
 // pages). Each CTA reads exactly one tier: CTAs [0, n_host) take the units whose chunk
 // starts on a host page, the rest take HBM units, round-robin by the unit's rank within its tier.
-// Each unit is owned by ONE consumer warp, which walks its 16-token tiles in order; producer lane w
-// streams warp w's tiles (K and V rows of a page, 1-D bulk copies = TMA engine, completing on
-// mbarriers) into a private SMEM ring, host rings capped by the congestion window. The
+// Each unit is owned by ONE warp, which walks its tiles in order and is its own producer: lane 0
+// streams the warp's next tiles (K and V rows of a page, 1-D bulk copies = TMA engine, completing on
+// mbarriers) into a private SMEM ring whose depth the CTA sizes from the warps that own units; host
+// CTAs cap their in-flight bytes (congestion control). The
 // warp computes on tensor cores (mma.sync m16n8k16 bf16->fp32):
 //   S^T[16 tokens x 8 heads] = K_tile . Q^T       (all q heads of the GQA group in one n8 tile)
 //   online softmax per head (exp2 domain), P^T fed back as the B operand via movmatrix.trans
@@ -32,12 +33,12 @@ namespace attn {
 
 constexpr int kD = 128;
 constexpr int kGmax = 8;              // q heads per kv head handled in one n8 tile
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = 32 * kConsumerWarps;
-constexpr int kThreads = 32 + kConsumers;
-constexpr int kMaxStages = 8;
+constexpr int kWarps = 8;              // each warp produces and consumes its own units
+constexpr int kThreads = 32 * kWarps;
+constexpr int kMaxSlots = 16;          // ring slots per warp
+constexpr int kRingOff = 2048;         // barriers + unit count live below the ring
 constexpr int kMaxPairs = 8192;       // (request, chunk) pairs scheduled per launch
-constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the kernel's static scan scratch
+constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the 1 KB the extern alignment adds statically
 constexpr uint32_t kHostBit = 0x80000000u;
 
 struct Params {
@@ -54,8 +55,11 @@ struct Params {
   float scale_log2;  // softmax scale * log2(e)
   float* part_o;     // [B][Hkv][max_chunks][G][d]
   float* part_lse;   // [B][Hkv][max_chunks][G]   (log2 domain)
-  int n_host, n_hbm, stages, window;
-  int stage_bytes;   // K page + V page
+  int n_host, n_hbm;
+  int ring_bytes;     // SMEM ring bytes per CTA, shared by the CTA's active warps
+  int max_slots;      // ring slots per warp cap (<= kMaxSlots)
+  int host_window;    // host CTAs: max in-flight tiles per warp (0: none)
+  int host_inflight;  // host CTAs: max in-flight bytes per CTA (congestion control; 0: none)
   int off_pairs;
   unsigned long long* trace;   // dak_trace_enable slots (nullable): split kernel, combine kernel
   unsigned long long* trace2;
@@ -98,7 +102,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
-__device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
@@ -144,34 +147,34 @@ __device__ __forceinline__ int find_pair(const int* pref, int n_pairs, int rank)
   return lo;
 }
 
-// Work split: one consumer WARP owns a whole unit (request b, kv head g, chunk c) and walks its
-// 16-token tiles in order with the online softmax in registers -- no cross-warp merge, no CTA
-// barrier per unit. Unit k of a tier goes to CTA (k mod n) and warp ((k div n) mod 8), so short
-// contexts (few tiles per unit) put up to 8 units in flight per SM. Producer lane w feeds consumer
-// warp w through a private ring of p.stages slots; a slot is one tile of K and V (2 x 16 x 256 B,
-// contiguous rows of a DAK-PG page) plus, on a unit's first tile, the unit's q rows (G x 256 B).
+// Work split: one WARP owns a whole unit (request b, kv head g, chunk c) and walks its tokens in
+// order with the online softmax in registers -- no cross-warp merge, no CTA barrier per unit. Unit k
+// of a tier goes to CTA (k mod n) and warp ((k div n) mod 8), so short contexts put up to 8 units in
+// flight per SM. Each warp is its own producer: lane 0 keeps the warp's private ring of `slots`
+// slots filled with the warp's next tiles (a slot = `tt` token rows of K and of V, 16 or 32,
+// contiguous rows of a DAK-PG page: two bulk copies completing on the slot's mbarrier) and refills
+// a slot as soon as the warp has consumed it. The ring depth is sized per CTA from the units it
+// actually owns, so a CTA with few units keeps as many bytes in flight as one with eight (Little's
+// law, not the unit count, sets the per-SM bandwidth). q of the unit's GQA group is read straight
+// into the B-fragment registers.
 __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Params p) {
   extern __shared__ __align__(1024) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);            // [8 warps][kMaxStages]
-  uint64_t* empty = full + kConsumerWarps * kMaxStages;           // [8 warps][kMaxStages]
-  int* s_count = reinterpret_cast<int*>(empty + kConsumerWarps * kMaxStages);
-  unsigned char* ring = smem + 2048;                              // [8 warps][stages][stage_bytes]
-  int* pref = reinterpret_cast<int*>(smem + p.off_pairs);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);            // [8 warps][kMaxSlots]
+  int* s_count = reinterpret_cast<int*>(full + kWarps * kMaxSlots);
+  int* warp_tot = s_count + 4;                                     // [kWarps] scan scratch
+  unsigned char* ring = smem + kRingOff;                          // [8 warps][slots][slot bytes]
+  int* pref = reinterpret_cast<int*>(smem + p.off_pairs);       // [B * max_chunks] tier-rank prefix
+  int* s_len = pref + p.B * p.max_chunks;                          // [B] seq_lens
 
   const int cta = blockIdx.x;
   const bool host = cta < p.n_host;
   const int my_j = host ? cta : cta - p.n_host;
   const int my_n = host ? p.n_host : p.n_hbm;
-  const int slots = host ? p.window : p.stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
-  constexpr int kTileBytes = 16 * kD * 2;  // 16 token rows of K (or V)
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kConsumerWarps * kMaxStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
-    }
+    for (int s = 0; s < kWarps * kMaxSlots; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
   }
@@ -183,7 +186,6 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
   const int n_pairs = p.B * p.max_chunks;
   {  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
-    __shared__ int warp_tot[kThreads / 32];
     int carry = 0;
     for (int base = 0; base < n_pairs; base += kThreads) {
       const int i = base + threadIdx.x;
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       if (i < n_pairs) {
         const int b = i / p.max_chunks, c = i % p.max_chunks;
         const int L = p.seq_lens[b];
+        if (c == 0) s_len[b] = L;
         const int npg = (L + p.page - 1) / p.page;
         if (c * p.chunk_pages < npg) {
           const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages];
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       for (int w = 0; w < warp; ++w) before += warp_tot[w];
       if (i < n_pairs) pref[i] = before + v - f;  // exclusive
       int tot = 0;
-      for (int w = 0; w < kThreads / 32; ++w) tot += warp_tot[w];
+      for (int w = 0; w < kWarps; ++w) tot += warp_tot[w];
       carry += tot;
       __syncthreads();
     }
@@ -217,141 +220,153 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     __syncthreads();
   }
   const int n_units = *s_count * p.Hkv;
-  const int stride = my_n * kConsumerWarps;  // units between consecutive units of one warp
+  const int stride = my_n * kWarps;  // units between consecutive units of one warp
+  // ---- ring geometry of this CTA: warps that own a unit share the ring bytes
+  const int my_units = my_j < n_units ? (n_units - my_j + my_n - 1) / my_n : 0;
+  const int active = min(kWarps, my_units);
+  if (warp >= active) return;
+  const int per_warp = (p.ring_bytes / active) & ~127;
+  int tt = 16;
+  if (p.page % 32 == 0 && per_warp >= 2 * (4 * 32 * kD)) tt = 32;  // 2 slots of 32-token tiles fit
+  const int slot_bytes = 2 * tt * kD * 2;
+  int slots = max(1, min(p.max_slots, per_warp / slot_bytes));
+  if (host && p.host_window > 0) slots = min(slots, p.host_window);
+  if (host && p.host_inflight > 0) slots = min(slots, max(1, p.host_inflight / (active * slot_bytes)));  // congestion cap
+  const int tile_bytes = tt * kD * 2;
 
-  if (warp == 0) {
-    // ================================ producer: lane w feeds consumer warp w
-    if (lane >= kConsumerWarps) return;
-    const int w = lane;
-    uint64_t* wf = full + w * kMaxStages;
-    uint64_t* we = empty + w * kMaxStages;
-    unsigned char* wr = ring + (size_t)w * p.stages * p.stage_bytes;
-    int it = 0;
-    bool waited = false;
-    int dq_s[kMaxStages];  // q copies of units whose first tile went out before the wait
-    const __nv_bfloat16* dq_src[kMaxStages];
-    int ndq = 0;
-    const uint32_t q_bytes_unit = (uint32_t)p.G * kD * 2;
-    auto release = [&]() {
-      grid_dep_wait();
-      if (threadIdx.x == 0) tstamp(p.trace, 1);
-      waited = true;
-      for (int i = 0; i < ndq; ++i)
-        bulk_g2s(wr + (size_t)dq_s[i] * p.stage_bytes + 2 * kTileBytes, dq_src[i], q_bytes_unit, &wf[dq_s[i]]);
-    };
-    for (int k = my_j + w * my_n; k < n_units; k += stride) {
-      const int pr = find_pair(pref, n_pairs, k / p.Hkv);
-      const int g = k % p.Hkv;
-      const int b = pr / p.max_chunks, c = pr % p.max_chunks;
-      const int L = p.seq_lens[b];
-      const int t0 = c * p.chunk_pages * p.page;
-      const int t1 = min(L, t0 + p.chunk_pages * p.page);
-      const __nv_bfloat16* qsrc = p.q + (long long)b * p.q_stride + (long long)g * p.G * kD;
-      for (int tok = t0; tok < t1; tok += 16, ++it) {
-        // before the dependency wait: only ring slots never used yet, only tiles of old tokens
-        if (!waited && (it >= slots || tok + 16 > L - 1)) release();
-        const int s = it % slots;
-        if (it >= slots) mbar_wait(&we[s], ((uint32_t)(it / slots) & 1u) ^ 1u);
-        const int pg = tok / p.page, r0 = tok % p.page;
-        const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + pg];
-        const long long idx = (long long)(e & ~kHostBit);
-        const bool eh = (e & kHostBit) != 0;
-        const long long off = (idx * p.Hkv + g) * (long long)page_bytes + (long long)r0 * kD * 2;
-        const uint32_t q_bytes = tok == t0 ? q_bytes_unit : 0u;
-        mbar_expect_tx(&wf[s], 2u * kTileBytes + q_bytes);
-        unsigned char* dst = wr + (size_t)s * p.stage_bytes;
-        bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, kTileBytes, &wf[s]);
-        bulk_g2s(dst + kTileBytes, (eh ? p.v_host : p.v_hbm) + off, kTileBytes, &wf[s]);
-        if (q_bytes) {
-          if (waited) {
-            bulk_g2s(dst + 2 * kTileBytes, qsrc, q_bytes, &wf[s]);
-          } else {  // q is produced by an earlier kernel of this step: after the wait
-            dq_s[ndq] = s;
-            dq_src[ndq] = qsrc;
-            ++ndq;
-          }
-        }
-      }
-    }
-    if (!waited) release();
-    return;
+  uint64_t* wf = full + warp * kMaxSlots;
+  unsigned char* wr = ring + (size_t)warp * per_warp;
+
+  // ---- producer cursor (lane 0 issues; every lane tracks it so the control flow stays uniform)
+  int pk = my_j + warp * my_n, ptok = 0, pt1 = 0, pb = 0, pg = 0, pL = 0;
+  auto unit_open = [&](int k, int& b, int& g, int& L, int& t0, int& t1) {
+    const int pr = find_pair(pref, n_pairs, k / p.Hkv);
+    g = k % p.Hkv;
+    b = pr / p.max_chunks;
+    const int c = pr % p.max_chunks;
+    L = s_len[b];
+    t0 = c * p.chunk_pages * p.page;
+    t1 = min(L, t0 + p.chunk_pages * p.page);
+  };
+  // block-table entries of pages [ent_base, ent_base + 32) of the cursor's request, one per lane,
+  // loaded one tile ahead of their first use so the load latency hides behind a tile of compute
+  int ent = 0, ent_base = 0;
+  auto load_ents = [&]() {
+    ent_base = ptok / p.page;
+    const int pgi = ent_base + lane;
+    ent = pgi < p.max_pages ? p.block_table[(long long)pb * p.max_pages + pgi] : 0;
+  };
+  if (pk < n_units) {
+    unit_open(pk, pb, pg, pL, ptok, pt1);
+    load_ents();
   }
+  int pit = 0;  // tiles issued
+  auto issue = [&]() {  // next tile of the stream into slot pit % slots
+    const int s = pit % slots;
+    const int page_i = ptok / p.page, r0 = ptok % p.page;
+    const uint32_t e = (uint32_t)__shfl_sync(0xffffffffu, ent, page_i - ent_base);
+    if (lane == 0) {
+      const long long idx = (long long)(e & ~kHostBit);
+      const bool eh = (e & kHostBit) != 0;
+      const long long off = (idx * p.Hkv + pg) * (long long)page_bytes + (long long)r0 * kD * 2;
+      unsigned char* dst = wr + (size_t)s * slot_bytes;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+      mbar_expect_tx(&wf[s], 2u * tile_bytes);
+      bulk_g2s(dst, (eh ? p.k_host : p.k_hbm) + off, tile_bytes, &wf[s]);
+      bulk_g2s(dst + tile_bytes, (eh ? p.v_host : p.v_hbm) + off, tile_bytes, &wf[s]);
+    }
+    ++pit;
+    ptok += tt;
+    if (ptok >= pt1) {
+      pk += stride;
+      if (pk < n_units) {
+        unit_open(pk, pb, pg, pL, ptok, pt1);
+        load_ents();
+      }
+    } else if (ptok / p.page - ent_base >= 32) {
+      load_ents();
+    }
+  };
+  // prologue: only tiles of old tokens (not holding position L - 1) before the dependency wait
+  while (pit < slots && pk < n_units && ptok + tt <= pL - 1) issue();
+  grid_dep_wait();
+  if (threadIdx.x == 0) tstamp(p.trace, 1);
+  while (pit < slots && pk < n_units) issue();
 
-  // ================================ consumers: warp cw owns its units end to end
-  const int cw = warp - 1;
   const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column pair
-  uint64_t* wf = full + cw * kMaxStages;
-  uint64_t* we = empty + cw * kMaxStages;
-  unsigned char* wr = ring + (size_t)cw * p.stages * p.stage_bytes;
   int it = 0;
   bool first_unit = true;
-  for (int k = my_j + cw * my_n; k < n_units; k += stride) {
-    const int pr = find_pair(pref, n_pairs, k / p.Hkv);
-    const int g = k % p.Hkv;
-    const int b = pr / p.max_chunks, c = pr % p.max_chunks;
-    const int L = p.seq_lens[b];
+  for (int k = my_j + warp * my_n; k < n_units; k += stride) {
+    int b, g, L, t0, t1;
+    unit_open(k, b, g, L, t0, t1);
     const int npg = (L + p.page - 1) / p.page;
-    const int t0 = c * p.chunk_pages * p.page;
-    const int t1 = min(L, t0 + p.chunk_pages * p.page);
+    // q of the GQA group as the B operand: b0 = q[head gq][16 ks + 2 cq, +1], b1 = ... + 8 (heads >= G: 0)
     uint32_t qb[kD / 16][2];
+    {
+      const uint32_t* qrow = reinterpret_cast<const uint32_t*>(p.q + (long long)b * p.q_stride + ((long long)g * p.G + gq) * kD);
+#pragma unroll
+      for (int ks = 0; ks < kD / 16; ++ks) {
+        qb[ks][0] = gq < p.G ? qrow[8 * ks + cq] : 0u;
+        qb[ks][1] = gq < p.G ? qrow[8 * ks + 4 + cq] : 0u;
+      }
+    }
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     float o[kD / 16][4];
 #pragma unroll
     for (int i = 0; i < kD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
-    for (int tok0 = t0; tok0 < t1; tok0 += 16, ++it) {
+    for (int tile0 = t0; tile0 < t1; tile0 += tt, ++it) {
       const int s = it % slots;
       mbar_wait(&wf[s], (uint32_t)(it / slots) & 1u);
-      const uint32_t kbase = su32(wr + (size_t)s * p.stage_bytes);
-      const uint32_t vbase = kbase + kTileBytes;
-      if (tok0 == t0) {  // q of the GQA group rides with the unit's first tile (rows >= G unused)
+      const uint32_t kslot = su32(wr + (size_t)s * slot_bytes);
+      for (int sub = 0; sub < tt && tile0 + sub < t1; sub += 16) {
+        const int tok0 = tile0 + sub;
+        const uint32_t kbase = kslot + sub * (kD * 2);
+        const uint32_t vbase = kslot + tile_bytes + sub * (kD * 2);
+        // ---- S^T = K . Q^T   [16 tokens x 8 heads]   (row t of the tile: swizzle phase t & 7)
+        float sc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks)
-          ldsm_x2(kbase + 2 * kTileBytes + (lane & 7) * (kD * 2) + (2 * ks + ((lane >> 3) & 1)) * 16, qb[ks][0], qb[ks][1]);
-      }
-      // ---- S^T = K . Q^T   [16 tokens x 8 heads]
-      float sc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int ks = 0; ks < kD / 16; ++ks) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4(kbase + pg_off(lane & 15, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+          mma_bf16(sc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+        }
+        // ---- scale, mask, online softmax (exp2 domain), per head column
+        const bool v0 = tok0 + gq < t1, v1 = tok0 + gq + 8 < t1;
+        const float s0 = v0 ? sc[0] * p.scale_log2 : -INFINITY;
+        const float s1 = v0 ? sc[1] * p.scale_log2 : -INFINITY;
+        const float s2 = v1 ? sc[2] * p.scale_log2 : -INFINITY;
+        const float s3 = v1 ? sc[3] * p.scale_log2 : -INFINITY;
+        float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
 #pragma unroll
-      for (int ks = 0; ks < kD / 16; ++ks) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4(kbase + pg_off(lane & 15, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
-        mma_bf16(sc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
-      }
-      // ---- scale, mask, online softmax (exp2 domain), per head column
-      const bool v0 = tok0 + gq < t1, v1 = tok0 + gq + 8 < t1;
-      const float s0 = v0 ? sc[0] * p.scale_log2 : -INFINITY;
-      const float s1 = v0 ? sc[1] * p.scale_log2 : -INFINITY;
-      const float s2 = v1 ? sc[2] * p.scale_log2 : -INFINITY;
-      const float s3 = v1 ? sc[3] * p.scale_log2 : -INFINITY;
-      float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+        for (int off = 4; off < 32; off <<= 1) {
+          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+        }
+        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: tile has a valid token
+        const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
+        m[0] = mn0;
+        m[1] = mn1;
+        const float p0 = exp2f(s0 - mn0), p1 = exp2f(s1 - mn1), p2 = exp2f(s2 - mn0), p3 = exp2f(s3 - mn1);
+        l[0] = l[0] * al0 + (p0 + p2);
+        l[1] = l[1] * al1 + (p1 + p3);
 #pragma unroll
-      for (int off = 4; off < 32; off <<= 1) {
-        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
-      }
-      const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: tile has a valid token
-      const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
-      m[0] = mn0;
-      m[1] = mn1;
-      const float p0 = exp2f(s0 - mn0), p1 = exp2f(s1 - mn1), p2 = exp2f(s2 - mn0), p3 = exp2f(s3 - mn1);
-      l[0] = l[0] * al0 + (p0 + p2);
-      l[1] = l[1] * al1 + (p1 + p3);
+        for (int i = 0; i < kD / 16; ++i) {
+          o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
+        }
+        // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
+        const uint32_t b0 = movm_t(pack_bf16(p0, p1));
+        const uint32_t b1 = movm_t(pack_bf16(p2, p3));
+        // ---- O^T[d x heads] += V^T . P^T
 #pragma unroll
-      for (int i = 0; i < kD / 16; ++i) {
-        o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
-      }
-      // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
-      const uint32_t b0 = movm_t(pack_bf16(p0, p1));
-      const uint32_t b1 = movm_t(pack_bf16(p2, p3));
-      // ---- O^T[d x heads] += V^T . P^T
-#pragma unroll
-      for (int i = 0; i < kD / 16; ++i) {
-        uint32_t a0, a1, a2, a3;
-        ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
-        mma_bf16(o[i], a0, a1, a2, a3, b0, b1);
+        for (int i = 0; i < kD / 16; ++i) {
+          uint32_t a0, a1, a2, a3;
+          ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
+          mma_bf16(o[i], a0, a1, a2, a3, b0, b1);
+        }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&we[s]);
+      if (pk < n_units) issue();  // refill the slot just consumed with the stream's next tile
     }
     // ---- l per head column: sum over the 8 lane groups holding the column
 #pragma unroll
@@ -361,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     }
     // lane holds O^T[d][head] for d = 16 i + gq (+8), head = 2 cq (+1)
     const bool direct = npg <= p.chunk_pages;  // the request is one chunk: no combine needed
+    const int c = t0 / (p.chunk_pages * p.page);
     const long long ubase = (((long long)b * p.Hkv + g) * p.max_chunks + c) * p.G;
 #pragma unroll
     for (int hc = 0; hc < 2; ++hc) {
@@ -385,17 +401,24 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
         }
       }
     }
-    if (first_unit && lane == 0 && cw == 0) tstamp(p.trace, 2);  // first unit of warp 0 done
+    if (first_unit && lane == 0 && warp == 0) tstamp(p.trace, 2);  // first unit of warp 0 done
     first_unit = false;
   }
   if (p.trace) {
-    consumer_sync();
-    if (lane == 0 && cw == 0) tstamp(p.trace, 3);
+    asm volatile("bar.sync 1, %0;" ::"r"(active * 32) : "memory");
+    if (lane == 0 && warp == 0) tstamp(p.trace, 3);
   }
 }
 
-// merge chunk partials: out[b, h, :] = sum_c w_c o_c, w_c = 2^(lse_c - LSE)   (fixed chunk order)
-__global__ void combine_kernel(const Params p) {
+// merge chunk partials: out[b, h, :] = sum_c w_c o_c / sum_c w_c, w_c = 2^(lse_c - max lse).
+// One 256-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 8, ... (lane = 4 dims,
+// float4 loads, several chunks in flight), then the 8 warp partials are summed in warp order.
+// The order depends only on the chunk count (bitwise r-invariant).
+constexpr int kCombineThreads = 256;
+__global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p) {
+  __shared__ float s_red[kCombineThreads / 32];
+  __shared__ float4 s_acc[kCombineThreads / 32][kD / 4];
+  __shared__ float s_den[kCombineThreads / 32];
   if (threadIdx.x == 0) tstamp(p.trace2, 0);
   grid_dep_launch();
   grid_dep_wait();
@@ -410,17 +433,43 @@ __global__ void combine_kernel(const Params p) {
     if (threadIdx.x == 0) tstamp(p.trace2, 3);
     return;
   }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long base = (((long long)b * p.Hkv + g) * p.max_chunks) * p.G + hh;  // + c*G
   float M = -INFINITY;
-  for (int c = 0; c < nch; ++c) M = fmaxf(M, p.part_lse[base + (long long)c * p.G]);
-  for (int d = threadIdx.x; d < kD; d += blockDim.x) {
-    float num = 0.f, den = 0.f;
-    for (int c = 0; c < nch; ++c) {
-      const float w = exp2f(p.part_lse[base + (long long)c * p.G] - M);
-      den += w;
-      num += w * p.part_o[(base + (long long)c * p.G) * kD + d];
+  for (int c = threadIdx.x; c < nch; c += kCombineThreads) M = fmaxf(M, p.part_lse[base + (long long)c * p.G]);
+#pragma unroll
+  for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
+  if (lane == 0) s_red[warp] = M;
+  __syncthreads();
+  M = s_red[0];
+#pragma unroll
+  for (int w = 1; w < kCombineThreads / 32; ++w) M = fmaxf(M, s_red[w]);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float den = 0.f;
+#pragma unroll 4
+  for (int c = warp; c < nch; c += kCombineThreads / 32) {
+    const long long u = base + (long long)c * p.G;
+    const float w = exp2f(p.part_lse[u] - M);
+    const float4 v = reinterpret_cast<const float4*>(p.part_o + u * kD)[lane];
+    den += w;
+    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+  }
+  s_acc[warp][lane] = acc;
+  if (lane == 0) s_den[warp] = den;
+  __syncthreads();
+  if (threadIdx.x < kD / 4) {
+    float4 t = s_acc[0][threadIdx.x];
+    float dn = s_den[0];
+#pragma unroll
+    for (int w = 1; w < kCombineThreads / 32; ++w) {
+      const float4 v = s_acc[w][threadIdx.x];
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      dn += s_den[w];
     }
-    p.out[((long long)b * p.Hq + h) * kD + d] = __float2bfloat16_rn(num / den);
+    const float inv = 1.f / dn;
+    __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.out + ((long long)b * p.Hq + h) * kD) + 2 * threadIdx.x;
+    dst[0] = __floats2bfloat162_rn(t.x * inv, t.y * inv);
+    dst[1] = __floats2bfloat162_rn(t.z * inv, t.w * inv);
   }
   if (threadIdx.x == 0) tstamp(p.trace2, 3);
 }
@@ -550,22 +599,21 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   out->ws_o = n_units * G * kD * sizeof(float);
   out->ws_lse = n_units * G * sizeof(float);
   const dak_launch_cfg& c = a->cfg;
-  // per consumer warp: a ring of tile stages [K 16 rows][V 16 rows][q G rows (first tile of a unit)]
-  p.stage_bytes = 2 * 16 * kD * 2 + G * kD * 2;
-  const int fixed = 2048 + a->B * max_chunks * 4 + 8 * kD * 2;  // + slack: q ldmatrix reads 8 rows
-  int max_stages = std::min((kSmemBudget - fixed) / (kConsumerWarps * p.stage_bytes), kMaxStages);
-  if (max_stages < 2) return fail(DAK_EUNSUPPORTED, "dak_attention: tile ring does not fit");
-  int stages = c.stages > 0 ? std::min(c.stages, max_stages) : max_stages;
-  p.stages = std::max(2, stages);
-  // host CTAs (caller-sized: ~one per 8 host units, i.e. one unit per warp; default 2); the
-  // congestion window caps the in-flight host tiles per warp
+  // per warp: a ring of tile slots [K tt rows][V tt rows]; the kernel sizes tt and the slot count
+  // per CTA from the warps that own units (the ring bytes are shared by them)
+  p.off_pairs = kSmemBudget - (a->B * max_chunks + a->B) * 4;
+  p.off_pairs &= ~127;
+  p.ring_bytes = p.off_pairs - kRingOff;
+  if (p.ring_bytes < kWarps * 2 * 16 * kD * 2)
+    return fail(DAK_EUNSUPPORTED, "dak_attention: tile ring does not fit (B * chunks too large)");
+  p.max_slots = c.stages > 0 ? std::min(c.stages, kMaxSlots) : kMaxSlots;
+  // host CTAs (caller-sized: ~one per 8 host units, i.e. one unit per warp; default 2). Congestion
+  // control caps the host bytes in flight: 256 KB over all host CTAs keeps the PCIe link
+  // saturated (calibration: ~192 KB in flight reach 51.5 GB/s) without queueing more
   int n_host = c.n_cta_host > 0 ? c.n_cta_host : 2;
   if (!a->k_host) n_host = 0;
-  int window = p.stages;
-  if (c.window > 0) window = std::min(c.window, p.stages);
-  else if (c.congestion_control)
-    window = std::max(1, std::min(p.stages, (int)cdiv(192 * 1024, (long long)p.stage_bytes * kConsumerWarps * std::max(1, n_host))));
-  p.window = window;
+  p.host_window = c.window > 0 ? c.window : 0;
+  p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, (256 * 1024) / std::max(1, n_host)) : 0;
   int n_hbm = c.n_cta_hbm;
   if (n_hbm <= 0) {
     if (g_sms <= 0) {
@@ -578,9 +626,7 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   p.n_host = n_host;
   p.n_hbm = n_hbm;
   out->grid = n_host + n_hbm;
-  p.off_pairs = 2048 + kConsumerWarps * p.stages * p.stage_bytes + 8 * kD * 2;
-  out->smem = p.off_pairs + a->B * max_chunks * 4;
-  if (out->smem > kSmemBudget) return fail(DAK_EUNSUPPORTED, "dak_attention: shared memory plan %d B too large", out->smem);
+  out->smem = p.off_pairs + (a->B * max_chunks + a->B) * 4;
   if (need_ptrs) {
     if (!a->q || !a->out || !a->block_table || !a->seq_lens) return fail(DAK_EINVAL, "dak_attention: NULL tensor");
     if (!a->k_hbm && !a->k_host) return fail(DAK_EINVAL, "dak_attention: no KV pool");
@@ -639,7 +685,7 @@ dak_status dak_attention(const dak_attention_args* args, dak_stream_t stream) {
   if (!need_combine) return DAK_OK;
   cudaLaunchConfig_t c2{};
   c2.gridDim = dim3(args->B * args->Hq);
-  c2.blockDim = dim3(attn::kD);
+  c2.blockDim = dim3(attn::kCombineThreads);
   c2.dynamicSmemBytes = 0;
   c2.stream = (cudaStream_t)stream;
   c2.attrs = attr;

@@ -65,7 +65,8 @@ def c5():
 def c4():
     bg, bl = peaks()
     rs = bl / (bg + bl)
-    d, Hq, Hkv, L, page, cp = 128, 64, 8, 131072, 64, 16
+    d, Hq, Hkv, L, page = 128, 64, 8, 131072, 64
+    cp = int(os.environ.get("DAK_C4_CHUNK_PAGES", "16"))
     for B in (1, 4):
         pages = L // page
         for r in (0.0, rs, 0.5):
