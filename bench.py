@@ -223,13 +223,20 @@ def make_llama(a, hw, world, rank, dak):
     tp_size = 8 if world == 1 else world
     batch = a.batch if a.batch != 8 else 64
     context = a.context if a.context != 64 else 65536
-    if world == 1:
-        comm = dak.comm_init(dak.comm_unique_id(), 0, 1)
-    else:
-        import torch.distributed as dist
-        uid = [dak.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        comm = dak.comm_init(uid[0], rank, world)
+    saved = os.dup(1)  # NCCL may print its version banner on stdout: keep stdout one JSON line
+    os.dup2(2, 1)
+    try:
+        if world == 1:
+            comm = dak.comm_init(dak.comm_unique_id(), 0, 1)
+        else:
+            import torch.distributed as dist
+            uid = [dak.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            comm = dak.comm_init(uid[0], rank, world)
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
     from paper_2604_26074_b200 import tp
     dm = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
     d, H = cfg.head_dim, cfg.hidden
@@ -408,6 +415,12 @@ def main():
                     read_peak=round(READ_PEAK_GBS + link_gbs, 1),
                     frac_of_read_peak=round(lin_achieved / (READ_PEAK_GBS + link_gbs), 4),
                     kernel_time_share_of_step=round(lin_share, 4))
+    # the split roofline at the step's host ratio r: EB(r) = 1 / max((1 - r)/B_g, r/B_l),
+    # = B_g + B_l at r* and B_l / r above it (a capacity-forced step is link-bound)
+    r_step = nb["host"] / nb["total"]
+    eb_r = 1.0 / max((1.0 - r_step) / hbm_gbs, r_step / link_gbs)
+    roofline.update(split_roofline_gbs=round(eb_r, 1), split_roofline_r=round(r_step, 5),
+                    step_frac_of_split_roofline=round(value / world / eb_r, 4))
 
     line = dict(metric=METRIC, value=round(value, 2), unit="GB/s", n_gpus=world, steps=a.steps, warmup=a.warmup,
                 ms_per_step=round(step_s * 1e3, 4), higher_is_better=True, scaling="weak", vs_baseline=None,

@@ -36,7 +36,7 @@ constexpr int kGmax = 8;              // q heads per kv head handled in one n8 t
 constexpr int kWarps = 8;              // each warp produces and consumes its own units
 constexpr int kThreads = 32 * kWarps;
 constexpr int kMaxSlots = 16;          // ring slots per warp
-constexpr int kRingOff = 2048;         // barriers + unit count live below the ring
+constexpr int kRingOff = 1152;         // barriers (1 KB) + unit count + scan scratch below the ring
 constexpr int kMaxPairs = 8192;       // (request, chunk) pairs scheduled per launch
 constexpr int kSmemBudget = 226 * 1024;  // 227 KB opt-in minus the 1 KB the extern alignment adds statically
 constexpr uint32_t kHostBit = 0x80000000u;
@@ -226,8 +226,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   const int active = min(kWarps, my_units);
   if (warp >= active) return;
   const int per_warp = (p.ring_bytes / active) & ~127;
-  int tt = 16;
-  if (p.page % 32 == 0 && per_warp >= 2 * (4 * 32 * kD)) tt = 32;  // 2 slots of 32-token tiles fit
+  // 32-token tiles (two 8 KB copies) whenever the page allows: measured faster than 16-token tiles
+  // even at one slot per warp (eight warps interleave; the per-copy cost favours larger copies)
+  const int tt = p.page % 32 == 0 ? 32 : 16;
   const int slot_bytes = 2 * tt * kD * 2;
   int slots = max(1, min(p.max_slots, per_warp / slot_bytes));
   if (host && p.host_window > 0) slots = min(slots, p.host_window);
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
 
   // ---- producer cursor (lane 0 issues; every lane tracks it so the control flow stays uniform)
   int pk = my_j + warp * my_n, ptok = 0, pt1 = 0, pb = 0, pg = 0, pL = 0;
+  int ppg = 0, pr0 = 0;  // cursor's page index within the request and row within the page
   auto unit_open = [&](int k, int& b, int& g, int& L, int& t0, int& t1) {
     const int pr = find_pair(pref, n_pairs, k / p.Hkv);
     g = k % p.Hkv;
@@ -252,19 +254,22 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   // loaded one tile ahead of their first use so the load latency hides behind a tile of compute
   int ent = 0, ent_base = 0;
   auto load_ents = [&]() {
-    ent_base = ptok / p.page;
+    ent_base = ppg;
     const int pgi = ent_base + lane;
     ent = pgi < p.max_pages ? p.block_table[(long long)pb * p.max_pages + pgi] : 0;
   };
-  if (pk < n_units) {
+  auto open_next = [&]() {
     unit_open(pk, pb, pg, pL, ptok, pt1);
+    ppg = ptok / p.page;  // = chunk * chunk_pages
+    pr0 = 0;
     load_ents();
-  }
-  int pit = 0;  // tiles issued
-  auto issue = [&]() {  // next tile of the stream into slot pit % slots
-    const int s = pit % slots;
-    const int page_i = ptok / p.page, r0 = ptok % p.page;
-    const uint32_t e = (uint32_t)__shfl_sync(0xffffffffu, ent, page_i - ent_base);
+  };
+  if (pk < n_units) open_next();
+  int pit = 0, ps = 0;  // tiles issued, slot of the next one (incremental: no divisions per tile)
+  auto issue = [&]() {
+    const int s = ps;
+    const int r0 = pr0;
+    const uint32_t e = (uint32_t)__shfl_sync(0xffffffffu, ent, ppg - ent_base);
     if (lane == 0) {
       const long long idx = (long long)(e & ~kHostBit);
       const bool eh = (e & kHostBit) != 0;
@@ -276,14 +281,17 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       bulk_g2s(dst + tile_bytes, (eh ? p.v_host : p.v_hbm) + off, tile_bytes, &wf[s]);
     }
     ++pit;
+    if (++ps == slots) ps = 0;
     ptok += tt;
+    pr0 += tt;
+    if (pr0 == p.page) {  // tt divides page
+      pr0 = 0;
+      ++ppg;
+    }
     if (ptok >= pt1) {
       pk += stride;
-      if (pk < n_units) {
-        unit_open(pk, pb, pg, pL, ptok, pt1);
-        load_ents();
-      }
-    } else if (ptok / p.page - ent_base >= 32) {
+      if (pk < n_units) open_next();
+    } else if (ppg - ent_base >= 32) {
       load_ents();
     }
   };
@@ -294,7 +302,8 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   while (pit < slots && pk < n_units) issue();
 
   const int gq = lane >> 2, cq = lane & 3;  // fragment row group / column pair
-  int it = 0;
+  int cs = 0;
+  uint32_t cph = 0;  // consumer slot and its barrier phase
   bool first_unit = true;
   for (int k = my_j + warp * my_n; k < n_units; k += stride) {
     int b, g, L, t0, t1;
@@ -315,9 +324,13 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
 #pragma unroll
     for (int i = 0; i < kD / 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
 
-    for (int tile0 = t0; tile0 < t1; tile0 += tt, ++it) {
-      const int s = it % slots;
-      mbar_wait(&wf[s], (uint32_t)(it / slots) & 1u);
+    for (int tile0 = t0; tile0 < t1; tile0 += tt) {
+      const int s = cs;
+      mbar_wait(&wf[s], cph);
+      if (++cs == slots) {
+        cs = 0;
+        cph ^= 1u;
+      }
       const uint32_t kslot = su32(wr + (size_t)s * slot_bytes);
       for (int sub = 0; sub < tt && tile0 + sub < t1; sub += 16) {
         const int tok0 = tile0 + sub;
@@ -411,8 +424,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
 }
 
 // merge chunk partials: out[b, h, :] = sum_c w_c o_c / sum_c w_c, w_c = 2^(lse_c - max lse).
-// One 256-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 8, ... (lane = 4 dims,
-// float4 loads, several chunks in flight), then the 8 warp partials are summed in warp order.
+// One 256-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 8, ... with a running
+// max (lane = 4 dims, float4 loads, several chunks in flight), then the 8 warp partials are
+// rescaled to the common max and summed in warp order.
 // The order depends only on the chunk count (bitwise r-invariant).
 constexpr int kCombineThreads = 256;
 __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p) {
@@ -435,36 +449,39 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p
   }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const long long base = (((long long)b * p.Hkv + g) * p.max_chunks) * p.G + hh;  // + c*G
-  float M = -INFINITY;
-  for (int c = threadIdx.x; c < nch; c += kCombineThreads) M = fmaxf(M, p.part_lse[base + (long long)c * p.G]);
-#pragma unroll
-  for (int off = 16; off; off >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, off));
-  if (lane == 0) s_red[warp] = M;
-  __syncthreads();
-  M = s_red[0];
-#pragma unroll
-  for (int w = 1; w < kCombineThreads / 32; ++w) M = fmaxf(M, s_red[w]);
+  // warp j: running max m, den = sum 2^(lse_c - m), acc = sum 2^(lse_c - m) o_c over its chunks
+  // (no separate max pass: the loads of every chunk are independent of the arithmetic)
+  float m = -INFINITY, den = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float den = 0.f;
 #pragma unroll 4
   for (int c = warp; c < nch; c += kCombineThreads / 32) {
     const long long u = base + (long long)c * p.G;
-    const float w = exp2f(p.part_lse[u] - M);
+    const float ls = p.part_lse[u];
     const float4 v = reinterpret_cast<const float4*>(p.part_o + u * kD)[lane];
-    den += w;
-    acc.x += w * v.x; acc.y += w * v.y; acc.z += w * v.z; acc.w += w * v.w;
+    const float mn = fmaxf(m, ls);
+    const float sc = exp2f(m - mn), w = exp2f(ls - mn);
+    m = mn;
+    den = den * sc + w;
+    acc.x = acc.x * sc + w * v.x; acc.y = acc.y * sc + w * v.y;
+    acc.z = acc.z * sc + w * v.z; acc.w = acc.w * sc + w * v.w;
   }
   s_acc[warp][lane] = acc;
-  if (lane == 0) s_den[warp] = den;
+  if (lane == 0) {
+    s_den[warp] = den;
+    s_red[warp] = m;
+  }
   __syncthreads();
   if (threadIdx.x < kD / 4) {
-    float4 t = s_acc[0][threadIdx.x];
-    float dn = s_den[0];
-#pragma unroll
-    for (int w = 1; w < kCombineThreads / 32; ++w) {
+    const int nw = min(nch, kCombineThreads / 32);  // warps that own a chunk
+    float M = s_red[0];
+    for (int w = 1; w < nw; ++w) M = fmaxf(M, s_red[w]);
+    float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+    float dn = 0.f;
+    for (int w = 0; w < nw; ++w) {  // fixed warp order
+      const float sc = exp2f(s_red[w] - M);
       const float4 v = s_acc[w][threadIdx.x];
-      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
-      dn += s_den[w];
+      t.x += sc * v.x; t.y += sc * v.y; t.z += sc * v.z; t.w += sc * v.w;
+      dn += sc * s_den[w];
     }
     const float inv = 1.f / dn;
     __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(p.out + ((long long)b * p.Hq + h) * kD) + 2 * threadIdx.x;
@@ -608,12 +625,12 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
     return fail(DAK_EUNSUPPORTED, "dak_attention: tile ring does not fit (B * chunks too large)");
   p.max_slots = c.stages > 0 ? std::min(c.stages, kMaxSlots) : kMaxSlots;
   // host CTAs (caller-sized: ~one per 8 host units, i.e. one unit per warp; default 2). Congestion
-  // control caps the host bytes in flight: 256 KB over all host CTAs keeps the PCIe link
-  // saturated (calibration: ~192 KB in flight reach 51.5 GB/s) without queueing more
+  // control caps the host bytes in flight: 512 KB over all host CTAs keeps the PCIe link
+  // saturated with 8 KB copies (256 KB reached only ~42 GB/s at C4 B = 4, r*) without queueing more
   int n_host = c.n_cta_host > 0 ? c.n_cta_host : 2;
   if (!a->k_host) n_host = 0;
   p.host_window = c.window > 0 ? c.window : 0;
-  p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, (256 * 1024) / std::max(1, n_host)) : 0;
+  p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, (512 * 1024) / std::max(1, n_host)) : 0;
   int n_hbm = c.n_cta_hbm;
   if (n_hbm <= 0) {
     if (g_sms <= 0) {

@@ -288,6 +288,13 @@ def attention_args(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, 
     return a
 
 
+def attention_host_ctas(host_units: int) -> int:
+    """Host-tier CTAs for dak_attention: one per 4 host units (request, kv head, chunk), 1..16.
+    Host CTAs are bound by the link latency, not by SM throughput: a few more CTAs keep more
+    bytes in flight (each warp owns a unit) at the cost of HBM CTAs."""
+    return max(1, min(16, -(-int(host_units) // 4)))
+
+
 def attention_workspace_size(args: dak_attention_args) -> int:
     v = C.c_size_t()
     _check(lib.dak_attention_workspace_size(C.byref(args), C.byref(v)))

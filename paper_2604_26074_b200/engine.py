@@ -338,7 +338,7 @@ class DakOPT:
         # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
         n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
         host_units = self.attn_host_chunks[l] * n_kvh
-        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=max(1, min(16, -(-host_units // 8)))))
+        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=dak.attention_host_ctas(host_units)))
         # L2 warm-up chain (dak.h): the last linear of layer l warms the next layer's q (or the head)
         nxt = self.layers[l + 1]["qkv" if self.fused_qkv else "q"] if l + 1 < c.n_layers else self.head
         a.l2_prefetch_bytes = self.l2_prefetch

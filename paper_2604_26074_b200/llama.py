@@ -248,7 +248,7 @@ class DakLlama:
         # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
         n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
         host_units = self.attn_host_chunks[l] * n_kvh
-        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=max(1, min(16, -(-host_units // 8)))))
+        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=dak.attention_host_ctas(host_units)))
         return a
 
     # ------------------------------------------------------------------ the decode step (hot path)
