@@ -48,4 +48,14 @@ a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
 for _ in range(3):
     dak.attention(a)
 torch.cuda.synchronize()
-print(dict(B=B, L=L, Hq=Hq, Hkv=Hkv, chunk_pages=cp, host_pages=hp, n_cta_host=nh))
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+reps = 5
+e0.record()
+for _ in range(reps):
+    dak.attention(a)
+e1.record()
+torch.cuda.synchronize()
+us = e0.elapsed_time(e1) * 1e3 / reps
+kv = 2 * B * L * Hkv * d * 2
+print(dict(B=B, L=L, Hq=Hq, Hkv=Hkv, chunk_pages=cp, host_pages=hp, n_cta_host=nh, us=round(us, 1),
+           gbs=round(kv / us / 1e3, 1), host_gbs=round(2 * B * hp * page * Hkv * d * 2 / us / 1e3, 2)))
