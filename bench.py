@@ -371,6 +371,11 @@ def main():
     ys = torch.empty(eng.B, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
     largs = [dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
                              cfg=dict(congestion_control=int(not a.no_cc), pdl=int(not a.no_pdl))) for op in ops]
+    ws_need = max(dak.linear_workspace_size(la) for la in largs)  # tcgen05 split-K partials, as in the step
+    lws = torch.empty(max(ws_need, 16), dtype=torch.uint8, device="cuda")
+    if ws_need:
+        for la in largs:
+            la.workspace, la.workspace_bytes = lws.data_ptr(), lws.numel()
     # the step's linear launches in step order, chained exactly as in the step (PDL), replayed as one
     # CUDA graph and bracketed by events on the launching stream: average launch duration = time / n
     with torch.cuda.stream(stream):

@@ -212,7 +212,9 @@ typedef struct {
   int32_t stages_hbm, window_host, smem_bytes, path; /* path: 1 FMA, 2 mma.sync               */
   int64_t rows_per_cta_host_max, rows_per_cta_hbm_max;
   int64_t hbm_bytes, host_bytes;                      /* algorithmic weight bytes per tier     */
-  int32_t cluster, reserved;                          /* CTAs sharing one x fetch (multicast)  */
+  int32_t cluster;                                    /* CTAs sharing one x fetch (multicast)  */
+  int32_t ksplit;                                     /* K splits (tcgen05 path, caller workspace); */
+                                                      /* > 1 adds one split-K reduce launch     */
 } dak_linear_launch_info;
 
 dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);
@@ -304,6 +306,12 @@ dak_status dak_comm_destroy(void* comm);
 /* partial (bf16 [rows, cols], device) is summed over the communicator in place (comm NULL: one
  * rank, no exchange), then x += partial (bf16 RNE) and, if stats_out != NULL, stats_out[r] =
  * float4 (cols, mean, M2, 0) of the new row r of x (a fused pre-norm's ln_stats, 1 part). */
+/* As dak_allreduce_residual, then y_norm = RMSNorm(x) * norm_w (bf16 [rows, cols], the same
+ * arithmetic as dak_rmsnorm) in the same kernel: the row-parallel o projection's combine and the
+ * MLP pre-norm of a Llama layer in one launch. cols % 8 == 0, cols <= 16384, 16-byte aligned
+ * pointers; y_norm may alias partial. Errors: EINVAL (NULL / misaligned), EUNSUPPORTED (cols). */
+dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, int32_t rows, int32_t cols,
+                                          const void* norm_w, float eps, void* y_norm, int32_t pdl, dak_stream_t stream);
 dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t rows, int32_t cols, float* stats_out,
                                   int32_t pdl, dak_stream_t stream);
 

@@ -73,6 +73,94 @@ __global__ void __launch_bounds__(kLnThreads) layernorm_kernel(const __nv_bfloat
   tstamp(tr, 3);
 }
 
+// Vectorised form of layernorm_kernel for rows of cols % 8 == 0, cols <= 256 * 8 * kLnVec: each
+// thread loads its 16-byte chunks once into registers (one HBM/L2 round trip per row instead of
+// three scalar passes); RMSNorm skips the mean. Same per-element arithmetic as layernorm_kernel.
+constexpr int kLnVec = 8;  // 16-byte chunks per thread
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 t = __bfloat1622float2(h[i]);
+    f[2 * i] = t.x;
+    f[2 * i + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 f32_to_bf16x8(const float* f) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(f[2 * i], f[2 * i + 1]);
+  return u;
+}
+__global__ void __launch_bounds__(kLnThreads) layernorm_vec_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const __nv_bfloat16* __restrict__ w,
+                                                                   const __nv_bfloat16* __restrict__ b,
+                                                                   __nv_bfloat16* __restrict__ y, int cols, float eps,
+                                                                   unsigned long long* tr, int rms) {
+  __shared__ float red[kLnThreads / 32];
+  tstamp(tr, 0);
+  grid_dep_launch();
+  grid_dep_wait();
+  tstamp(tr, 1);
+  const int nc = cols / 8;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + (long long)blockIdx.x * cols);
+  uint4 raw[kLnVec];
+#pragma unroll
+  for (int i = 0; i < kLnVec; ++i) {
+    const int c = threadIdx.x + i * kLnThreads;
+    raw[i] = c < nc ? xr[c] : make_uint4(0u, 0u, 0u, 0u);
+  }
+  float mean = 0.f;
+  if (!rms) {
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kLnVec; ++i) {
+      float f[8];
+      bf16x8_to_f32(raw[i], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += f[j];
+    }
+    mean = block_sum(s, red) / (float)cols;
+  }
+  float v = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnVec; ++i) {
+    if (threadIdx.x + i * kLnThreads < nc) {
+      float f[8];
+      bf16x8_to_f32(raw[i], f);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = f[j] - mean;
+        v += d * d;
+      }
+    }
+  }
+  const float rstd = rsqrtf(block_sum(v, red) / (float)cols + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + (long long)blockIdx.x * cols);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  const uint4* bv = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+  for (int i = 0; i < kLnVec; ++i) {
+    const int c = threadIdx.x + i * kLnThreads;
+    if (c < nc) {
+      float f[8], wf[8], bf[8];
+      bf16x8_to_f32(raw[i], f);
+      bf16x8_to_f32(wv[c], wf);
+      if (b) bf16x8_to_f32(bv[c], bf);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) f[j] = (f[j] - mean) * rstd * wf[j] + (b ? bf[j] : 0.f);
+      yr[c] = f32_to_bf16x8(f);
+    }
+  }
+  tstamp(tr, 3);
+}
+
+static bool ln_vec_ok(const void* x, const void* w, const void* b, const void* y, int cols) {
+  return cols % 8 == 0 && cols <= kLnThreads * 8 * kLnVec && aligned16(x) && aligned16(w) && (!b || aligned16(b)) &&
+         aligned16(y);
+}
+
 // (count, mean, M2) of one row held as one value per thread-slot, two-pass, fixed order
 __device__ void row_stats_store(const float* v, int nv, int cols, float* red, float4* out) {
   float s = 0.f;
@@ -89,16 +177,29 @@ __device__ void row_stats_store(const float* v, int nv, int cols, float* red, fl
 
 constexpr int kRowMax = 64;  // values per thread held in registers (cols <= 256 * 64)
 
-// out[r, j] = bf16(silu(gu[r, j]) * gu[r, F + j])  (Llama MLP gate / up combine)
+// out[r, j] = bf16(silu(gu[r, j]) * gu[r, F + j])  (Llama MLP gate / up combine); 8 columns per
+// thread (F % 8 == 0, 16-byte aligned rows), else one
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int F,
-                                unsigned long long* tr) {
+                                unsigned long long* tr, int vec) {
   if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
   const __nv_bfloat16* g = gu + (long long)blockIdx.y * 2 * F;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
-    const float a = __bfloat162float(g[j]), u = __bfloat162float(g[F + j]);
-    out[(long long)blockIdx.y * F + j] = __float2bfloat16_rn(a / (1.f + __expf(-a)) * u);
+  __nv_bfloat16* o = out + (long long)blockIdx.y * F;
+  if (vec) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F / 8; j += gridDim.x * blockDim.x) {
+      float a[8], u[8];
+      bf16x8_to_f32(reinterpret_cast<const uint4*>(g)[j], a);
+      bf16x8_to_f32(reinterpret_cast<const uint4*>(g + F)[j], u);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = a[i] / (1.f + __expf(-a[i])) * u[i];
+      reinterpret_cast<uint4*>(o)[j] = f32_to_bf16x8(a);
+    }
+  } else {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F; j += gridDim.x * blockDim.x) {
+      const float a = __bfloat162float(g[j]), u = __bfloat162float(g[F + j]);
+      o[j] = __float2bfloat16_rn(a / (1.f + __expf(-a)) * u);
+    }
   }
   if (threadIdx.x == 0) tstamp(tr, 3);
 }
@@ -301,12 +402,19 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
       l.stats_out = o_stats;
     }
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? o_stats : nullptr, pdl, strm)) != DAK_OK)
+  }
+  // unfused TP: the combine kernel also writes RMSNorm 2 of the new x into hbuf (aliases partial)
+  const bool norm2_done = tp && !fuse;
+  if (norm2_done) {
+    if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
       return st;
+  } else if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? o_stats : nullptr, pdl, strm)) != DAK_OK) {
+    return st;
   }
   {  // [gate; up] after RMSNorm 2 -> gu [B, 2F]
     dak_linear_args l = lin_args(a->up, 2LL * F, H, B, a->x, gu, nullptr, DAK_ACT_NONE, a->cfg);
-    if ((st = prenorm(l, a->ln2_w, o_stats, o_parts)) != DAK_OK) return st;
+    if (norm2_done) l.x = hbuf;
+    else if ((st = prenorm(l, a->ln2_w, o_stats, o_parts)) != DAK_OK) return st;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
   {  // down: the SwiGLU operand fused (small batch) or one silu * up kernel (large batch)
@@ -340,8 +448,9 @@ dak_status dak_layernorm(const void* x, const void* w, const void* b, void* y, i
   unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, cols, rows);
   int rms = 0;
   void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr, &rms};
-  return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
-                           (cudaStream_t)stream, pdl);
+  const bool vec = layer::ln_vec_ok(xp, wp, bp, yp, cols);
+  return layer::launch_pdl(vec ? (const void*)layer::layernorm_vec_kernel : (const void*)layer::layernorm_kernel,
+                           dim3(rows), dim3(layer::kLnThreads), args, (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int32_t cols, float eps, int32_t pdl,
@@ -355,8 +464,9 @@ dak_status dak_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int3
   unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, cols, rows);
   int rms = 1;
   void* args[] = {&xp, &wp, &bp, &yp, &c, &eps, &tr, &rms};
-  return layer::launch_pdl((const void*)layer::layernorm_kernel, dim3(rows), dim3(layer::kLnThreads), args,
-                           (cudaStream_t)stream, pdl);
+  const bool vec = layer::ln_vec_ok(xp, wp, bp, yp, cols);
+  return layer::launch_pdl(vec ? (const void*)layer::layernorm_vec_kernel : (const void*)layer::layernorm_kernel,
+                           dim3(rows), dim3(layer::kLnThreads), args, (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_silu_mul(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, dak_stream_t stream) {
@@ -365,8 +475,10 @@ dak_status dak_silu_mul(const void* gu, void* out, int32_t rows, int32_t F, int3
   __nv_bfloat16* op = (__nv_bfloat16*)out;
   int f = F;
   unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, F, rows);
-  void* args[] = {&gp, &op, &f, &tr};
-  const int bx = (F + 255) / 256 < 8 ? (F + 255) / 256 : 8;
+  int vec = F % 8 == 0 && aligned16(gu) && aligned16(out);
+  void* args[] = {&gp, &op, &f, &tr, &vec};
+  const int per = vec ? F / 8 : F;
+  const int bx = (per + 255) / 256 < 8 ? (per + 255) / 256 : 8;
   return layer::launch_pdl((const void*)layer::silu_mul_kernel, dim3(bx, rows), dim3(256), args, (cudaStream_t)stream, pdl);
 }
 

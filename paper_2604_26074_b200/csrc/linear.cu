@@ -1049,21 +1049,56 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
 }
 
 #if DAK_LINEAR_PART == 0
-// y[n, m] = act(sum_s part[s][n][m] + bias[m]) + residual[n, m]: the fixed-order split-K combine
+// y[n, m] = act(sum_s part[s][n][m] + bias[m]) + residual[n, m]: the fixed-order split-K combine.
+// Grid (x: column groups, y: row n); vec = 4 columns per thread (float4 partial loads, 8-byte
+// bf16 stores; M % 4 == 0 and 8-byte aligned y / residual rows), else one.
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int N, long long M,
                                      const __nv_bfloat16* __restrict__ bias, int act,
-                                     const __nv_bfloat16* residual, __nv_bfloat16* y, long long ldy) {
+                                     const __nv_bfloat16* residual, __nv_bfloat16* y, long long ldy, int vec) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const long long total = (long long)N * M;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-    const long long n = i / M, m = i - n * M;
-    float v = part[i];
-    for (int s = 1; s < S; ++s) v += part[(long long)s * total + i];
+  const int n = blockIdx.y;
+  const float* pr = part + (long long)n * M;
+  __nv_bfloat16* yr = y + (long long)n * ldy;
+  const __nv_bfloat16* rr = residual ? residual + (long long)n * ldy : nullptr;
+  if (vec) {
+    for (long long m4 = (long long)blockIdx.x * blockDim.x + threadIdx.x; m4 < M / 4; m4 += (long long)gridDim.x * blockDim.x) {
+      float4 v = reinterpret_cast<const float4*>(pr)[m4];
+      for (int s = 1; s < S; ++s) {
+        const float4 t = reinterpret_cast<const float4*>(pr + (long long)s * total)[m4];
+        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+      }
+      float f[4] = {v.x, v.y, v.z, v.w};
+      if (bias) {
+        const uint2 bb = reinterpret_cast<const uint2*>(bias)[m4];
+        const float2 b0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb.x));
+        const float2 b1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&bb.y));
+        f[0] += b0.x; f[1] += b0.y; f[2] += b1.x; f[3] += b1.y;
+      }
+      if (act == DAK_ACT_RELU)
+        for (int i = 0; i < 4; ++i) f[i] = fmaxf(f[i], 0.f);
+      if (rr) {
+        const uint2 rb = reinterpret_cast<const uint2*>(rr)[m4];
+        const float2 r0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rb.x));
+        const float2 r1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&rb.y));
+        f[0] += r0.x; f[1] += r0.y; f[2] += r1.x; f[3] += r1.y;
+      }
+      __nv_bfloat162 o0 = __floats2bfloat162_rn(f[0], f[1]), o1 = __floats2bfloat162_rn(f[2], f[3]);
+      uint2 ob;
+      ob.x = *reinterpret_cast<uint32_t*>(&o0);
+      ob.y = *reinterpret_cast<uint32_t*>(&o1);
+      reinterpret_cast<uint2*>(yr)[m4] = ob;
+    }
+    return;
+  }
+  for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (long long)gridDim.x * blockDim.x) {
+    float v = pr[m];
+    for (int s = 1; s < S; ++s) v += pr[(long long)s * total + m];
     if (bias) v += __bfloat162float(bias[m]);
     if (act == DAK_ACT_RELU) v = fmaxf(v, 0.f);
-    if (residual) v += __bfloat162float(residual[n * ldy + m]);
-    y[n * ldy + m] = __float2bfloat16_rn(v);
+    if (rr) v += __bfloat162float(rr[m]);
+    yr[m] = __float2bfloat16_rn(v);
   }
 }
 
@@ -1646,7 +1681,7 @@ dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info*
   info->hbm_bytes = (args->M - args->h) * args->K * 2;
   info->host_bytes = args->h * args->K * 2;
   info->cluster = pl.p.mc;
-  info->reserved = 0;
+  info->ksplit = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;
   return DAK_OK;
 }
 
@@ -1678,18 +1713,20 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
   pl.p.trace = trace_slot(DAK_KIND_LINEAR, args->M, args->K, pl.grid);
   if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
   if (pl.p.ksplit > 1) {
-    const long long total = (long long)args->N * args->M;
+    const int vec = args->M % 4 == 0 && pl.p.ldy % 4 == 0 && ((uintptr_t)pl.p.y & 7) == 0 &&
+                    ((uintptr_t)pl.p.residual & 7) == 0 && ((uintptr_t)pl.p.bias & 7) == 0;
+    const long long per_row = vec ? args->M / 4 : args->M;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = args->cfg.pdl ? 1 : 0;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)std::min<long long>(ceil_div_ll(total, 256), 148LL * 8));
+    cfg.gridDim = dim3((unsigned)std::min<long long>(ceil_div_ll(per_row, 256), 64), (unsigned)args->N);
     cfg.blockDim = dim3(256);
     cfg.stream = (cudaStream_t)stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, lin::splitk_reduce_kernel, (const float*)pl.p.part, pl.p.ksplit, (int)args->N,
-                                    (long long)args->M, pl.p.bias, pl.p.act, pl.p.residual, pl.p.y, pl.p.ldy));
+                                    (long long)args->M, pl.p.bias, pl.p.act, pl.p.residual, pl.p.y, pl.p.ldy, vec));
   }
   return DAK_OK;
 }

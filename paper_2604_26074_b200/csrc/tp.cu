@@ -95,6 +95,66 @@ __global__ void __launch_bounds__(kThreads) residual_stats_kernel(const __nv_bfl
   if (threadIdx.x == 0) stats[blockIdx.x] = make_float4((float)cols, mean, m2, 0.f);
 }
 
+// x[r] += partial[r] (bf16 RNE), then y[r] = bf16(x[r] * rstd * w) with rstd = 1/sqrt(mean(x^2) + eps)
+// (RMSNorm of the new row: the same arithmetic as dak_rmsnorm, fused so the MLP pre-norm needs no
+// launch of its own). 8 columns per 16-byte chunk, chunks held in registers; y may alias partial
+// (each thread reads its own chunks before the first barrier and writes only those).
+constexpr int kVec = 8;  // 16-byte chunks per thread (cols <= 256 * 64)
+__global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_bfloat16* partial,
+                                                                    __nv_bfloat16* __restrict__ x, int cols,
+                                                                    const __nv_bfloat16* __restrict__ w, float eps,
+                                                                    __nv_bfloat16* y) {
+  __shared__ float red[kThreads / 32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int nc = cols / 8;
+  const long long base = (long long)blockIdx.x * nc;
+  uint4* xr = reinterpret_cast<uint4*>(x) + base;
+  const uint4* pr = reinterpret_cast<const uint4*>(partial) + base;
+  float f[kVec][8];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int c = threadIdx.x + i * kThreads;
+    if (c < nc) {
+      const uint4 a = xr[c], b = pr[c];
+      const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&b);
+      uint4 o;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 u = __bfloat1622float2(ah[j]), v = __bfloat1622float2(bh[j]);
+        oh[j] = __floats2bfloat162_rn(u.x + v.x, u.y + v.y);
+        const float2 r = __bfloat1622float2(oh[j]);
+        f[i][2 * j] = r.x;
+        f[i][2 * j + 1] = r.y;
+        ss += r.x * r.x + r.y * r.y;
+      }
+      xr[c] = o;
+    }
+  }
+  const float rstd = rsqrtf(block_sum(ss, red) / (float)cols + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y) + base;
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+#pragma unroll
+  for (int i = 0; i < kVec; ++i) {
+    const int c = threadIdx.x + i * kThreads;
+    if (c < nc) {
+      const uint4 wu = wv[c];
+      const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&wu);
+      uint4 o;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 ww = __bfloat1622float2(wh[j]);
+        oh[j] = __floats2bfloat162_rn(f[i][2 * j] * rstd * ww.x, f[i][2 * j + 1] * rstd * ww.y);
+      }
+      yr[c] = o;
+    }
+  }
+}
+
 }  // namespace tp
 }  // namespace dak
 
@@ -158,6 +218,35 @@ dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t ro
   cfg.numAttrs = 1;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_stats_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
                                   (int)cols, (float4*)stats_out));
+  return DAK_OK;
+}
+
+dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, int32_t rows, int32_t cols,
+                                          const void* norm_w, float eps, void* y_norm, int32_t pdl, dak_stream_t stream) {
+  if (!partial || !x || !norm_w || !y_norm || rows <= 0 || cols <= 0)
+    return fail(DAK_EINVAL, "dak_allreduce_residual_rmsnorm: bad arguments");
+  if (cols % 8 || cols > tp::kThreads * 8 * tp::kVec)
+    return fail(DAK_EUNSUPPORTED, "dak_allreduce_residual_rmsnorm: cols must be a multiple of 8, <= %d", tp::kThreads * 8 * tp::kVec);
+  if (!aligned16(partial) || !aligned16(x) || !aligned16(norm_w) || !aligned16(y_norm))
+    return fail(DAK_EINVAL, "dak_allreduce_residual_rmsnorm: pointers must be 16-byte aligned");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (comm) {
+    tp::Nccl* n;
+    dak_status st = tp::nccl(&n);
+    if (st != DAK_OK) return st;
+    DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = (pdl && !comm) ? 1 : 0;  // NCCL kernels are not PDL-aware
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(rows);
+  cfg.blockDim = dim3(tp::kThreads);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_rmsnorm_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
+                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm));
   return DAK_OK;
 }
 

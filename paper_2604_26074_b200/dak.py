@@ -52,7 +52,7 @@ class dak_op_plan(C.Structure):
 class dak_launch_cfg(C.Structure):
     _fields_ = [("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("window", C.c_int32), ("stages", C.c_int32),
                 ("congestion_control", C.c_int32), ("pdl", C.c_int32), ("force_path", C.c_int32),
-                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("reserved", C.c_int32)]
+                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("ksplit", C.c_int32)]
 
 
 class dak_linear_args(C.Structure):
@@ -70,7 +70,7 @@ class dak_linear_launch_info(C.Structure):
     _fields_ = [("grid", C.c_int32), ("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("threads", C.c_int32),
                 ("stages_hbm", C.c_int32), ("window_host", C.c_int32), ("smem_bytes", C.c_int32), ("path", C.c_int32),
                 ("rows_per_cta_host_max", C.c_int64), ("rows_per_cta_hbm_max", C.c_int64),
-                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("reserved", C.c_int32)]
+                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("ksplit", C.c_int32)]
 
 
 def _sig(name, res, args):
@@ -357,9 +357,11 @@ _sig("dak_comm_init", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.
 _sig("dak_comm_destroy", C.c_int32, [C.c_void_p])
 _sig("dak_allreduce_residual", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                            C.c_int32, C.c_void_p])
+_sig("dak_allreduce_residual_rmsnorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                                   C.c_float, C.c_void_p, C.c_int32, C.c_void_p])
 EXPORTED += ["dak_layernorm", "dak_rmsnorm", "dak_silu_mul", "dak_embed", "dak_row_stats", "dak_layer_scratch_size", "dak_layer",
              "dak_layer_stats_parts", "dak_rope_kv_append", "dak_comm_unique_id", "dak_comm_init", "dak_comm_destroy",
-             "dak_allreduce_residual"]
+             "dak_allreduce_residual", "dak_allreduce_residual_rmsnorm"]
 MODEL_LLAMA = 1
 
 
@@ -389,6 +391,11 @@ def comm_destroy(comm):
 def allreduce_residual(comm, partial, x, rows, cols, stats_out=None, pdl=0, stream=None):
     _check(lib.dak_allreduce_residual(comm, _ptr(partial), _ptr(x), int(rows), int(cols), _ptr(stats_out), int(pdl),
                                       _stream(stream)))
+
+
+def allreduce_residual_rmsnorm(comm, partial, x, rows, cols, norm_w, eps, y_norm, pdl=0, stream=None):
+    _check(lib.dak_allreduce_residual_rmsnorm(comm, _ptr(partial), _ptr(x), int(rows), int(cols), _ptr(norm_w),
+                                              float(eps), _ptr(y_norm), int(pdl), _stream(stream)))
 
 
 def weight(w_host, w_hbm, h, kc, bias=None, n_cta_host=0) -> dak_weight:

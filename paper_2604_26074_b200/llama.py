@@ -275,12 +275,23 @@ class DakLlama:
                 ha.workspace, ha.workspace_bytes = self.head_ws.data_ptr(), self.head_ws.numel()
         dak.linear(ha, stream)
 
+    def _reduce_launches(self, op) -> int:
+        """1 when this linear splits K on the tcgen05 path (one split-K reduce kernel), else 0."""
+        if self.B <= 16:
+            return 0
+        w = op.weight()
+        la = dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, self.B, 16, 16,
+                             cfg=dict(self.launch, n_cta_host=w.n_cta_host or self.launch["n_cta_host"]))
+        la.workspace, la.workspace_bytes = 256, 1 << 40  # query only: the plan splits K when workspace is given
+        return int(dak.linear_query(la)["ksplit"] > 1)
+
     def kernels_per_step(self) -> int:
-        per_layer = (6 + (1 if self.chunks_per_req > 1 else 0) + (2 if self.comm else 0)  # + residual kernels
-                     + (0 if self.fuse_norm else 3))  # + 2 RMSNorm + silu*up kernels
-        if not self.fuse_norm:
-            return 1 + per_layer * self.cfg.n_layers + 2
-        return 1 + per_layer * self.cfg.n_layers + 1
+        """Kernels of this library per decode step (NCCL's own kernels not counted)."""
+        per_layer = (6 + (1 if self.chunks_per_req > 1 else 0)  # qkv, rope+append, attention, o, up, down (+combine)
+                     + (2 if self.comm else 0)  # residual kernels after the all-reduces
+                     + (0 if self.fuse_norm else (2 if self.comm else 3)))  # RMSNorm 1 (+ RMSNorm 2) + silu*up
+        n = 1 + per_layer * self.cfg.n_layers + (1 if self.fuse_norm else 2)  # embed ... (final RMSNorm +) head
+        return n + sum(self._reduce_launches(op) for op in self.linear_ops())
 
     def capture(self, stream: torch.cuda.Stream):
         with torch.cuda.stream(stream):

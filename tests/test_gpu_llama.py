@@ -18,7 +18,7 @@ def _dev(p, torch):
 
 @pytest.mark.parametrize("frac,B,ctx,use_comm,fuse", [(0.0, 3, 70, False, True), (0.3, 2, 150, False, True),
                                                      (0.2, 4, 40, True, True), (0.2, 4, 40, True, False),
-                                                     (0.3, 24, 90, False, None)])
+                                                     (0.3, 24, 90, False, None), (0.3, 24, 90, True, None)])
 def test_llama_step_matches_oracle(frac, B, ctx, use_comm, fuse):
     import torch
     from paper_2604_26074_b200 import dak
@@ -157,3 +157,46 @@ def test_rmsnorm_and_silu_mul_kernels():
     ref2 = Kx.round_to_bf16(Ly.silu(gf) * uf)
     got2 = Kx.bf16_to_f64(from_dev(o))
     assert np.abs(got2 - ref2).max() <= 2 ** -7 * max(1.0, np.abs(ref2).max())
+
+
+@pytest.mark.parametrize("rows,cols", [(4, 8192), (3, 520), (2, 16384)])
+def test_allreduce_residual_rmsnorm_kernel(rows, cols):
+    """x += partial (bf16 RNE) and y = RMSNorm(x) * w in one kernel (1-rank: no exchange), vs the
+    oracle's residual add + rmsnorm; y aliasing partial (as in the Llama layer) gives the same."""
+    import torch
+    from paper_2604_26074_b200 import dak
+    from tests.gpu_util import to_dev, from_dev
+    g = synth.rng(77 + cols)
+    x = synth.normal_bf16(g, (rows, cols), 1.1)
+    pa = synth.normal_bf16(g, (rows, cols), 0.7)
+    w = synth.bf16_bits((1.0 + 0.2 * g.standard_normal(cols)).astype(np.float32))
+    xs = Kx.round_to_bf16(Kx.bf16_to_f64(x) + Kx.bf16_to_f64(pa))
+    ref = Kx.round_to_bf16(Kx.rmsnorm(xs, Kx.bf16_to_f64(w), 1e-5))
+    for alias in (False, True):
+        xd, pd, wd = to_dev(x), to_dev(pa), to_dev(w)
+        y = pd if alias else torch.empty((rows, cols), dtype=torch.int16, device="cuda")
+        dak.allreduce_residual_rmsnorm(None, pd, xd, rows, cols, wd, 1e-5, y)
+        torch.cuda.synchronize()
+        assert np.array_equal(Kx.bf16_to_f64(from_dev(xd)), xs)  # bf16(x + p): exact
+        got = Kx.bf16_to_f64(from_dev(y))
+        assert np.abs(got - ref).max() <= 2 ** -7 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("cols,bias", [(8192, True), (8192, False), (7168, True), (1000, True)])
+def test_layernorm_vectorised_and_scalar(cols, bias):
+    """dak_layernorm on the vectorised path (cols % 8 == 0) and the scalar fallback (cols = 1000 is
+    vectorised too; odd strides are exercised by the OPT engine tests) vs the oracle LayerNorm."""
+    import torch
+    from paper_2604_26074_b200 import dak
+    from tests.gpu_util import to_dev, from_dev
+    g = synth.rng(5 + cols)
+    x = synth.normal_bf16(g, (6, cols), 1.3)
+    w = synth.bf16_bits((1.0 + 0.2 * g.standard_normal(cols)).astype(np.float32))
+    b = synth.normal_bf16(g, (cols,), 0.1) if bias else None
+    y = torch.empty((6, cols), dtype=torch.int16, device="cuda")
+    dak.layernorm(to_dev(x), to_dev(w), to_dev(b) if bias else None, y, 6, cols, 1e-5)
+    torch.cuda.synchronize()
+    ref = Kx.round_to_bf16(Kx.layernorm(Kx.bf16_to_f64(x), Kx.bf16_to_f64(w),
+                                        Kx.bf16_to_f64(b) if bias else np.zeros(cols), 1e-5))
+    got = Kx.bf16_to_f64(from_dev(y))
+    assert np.abs(got - ref).max() <= 2 ** -7 * np.abs(ref).max()
