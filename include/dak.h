@@ -372,7 +372,9 @@ typedef struct {
   const int32_t* seq_lens;            /* [B] = positions + 1                                   */
   int32_t page_size, max_pages, chunk_pages;
   int32_t tp_rank, tp_size;           /* tensor-parallel rank / world (Llama)                    */
-  int32_t reserved;
+  int32_t x_prenormed;                /* Llama, fuse_norm 0: the scratch's normalised-x buffer   */
+                                      /* already holds RMSNorm 1 of x (written by the previous   */
+                                      /* layer's combine, see next_ln_w): skip that kernel       */
   dak_launch_cfg cfg;                 /* linear ops (pdl applies to every kernel)              */
   dak_launch_cfg attn_cfg;            /* attention                                             */
   int32_t split_qkv;                  /* 1: use q, k, v below instead of the fused qkv weight  */
@@ -394,6 +396,10 @@ typedef struct {
   float rope_theta;
   int32_t reserved4;
   void* comm;                         /* dak_comm_init communicator (required for tp_size > 1)  */
+  const void* next_ln_w;              /* Llama, fuse_norm 0, comm set: the down projection's     */
+                                      /* combine also writes RMSNorm(x) * next_ln_w (the next    */
+                                      /* layer's RMSNorm 1) into the scratch for a next call with */
+                                      /* x_prenormed = 1 and the same scratch; NULL: off          */
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);

@@ -529,16 +529,39 @@ __global__ void append_kernel(const uint4* __restrict__ k_new, const uint4* __re
 // Llama decode KV write with rotary positions: rotate q (in place) and k of the new token of every
 // request at positions[b] (rotate-half pairs (i, i + d/2), angle pos / theta^(2i/d), computed in
 // double then fp32 sincos of the reduced angle), then append k (rotated) and v to the page pools.
+// With part != nullptr the row is first materialised from the producing linear's split-K fp32
+// partials: qkv[b][c] = bf16(sum_s part[s][b][c]) in split order (the split-K reduce, fused here;
+// part row stride = (Hq + 2 Hkv) * d, N = gridDim.x rows per split).
 __global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, long long stride, int Hq, int Hkv,
                                                           const int* pos, double log2_theta, const int* block_table,
                                                           int page, int max_pages, uint4* k_hbm, uint4* v_hbm,
-                                                          uint4* k_host, uint4* v_host, unsigned long long* tr) {
+                                                          uint4* k_host, uint4* v_host, unsigned long long* tr,
+                                                          const float* part, int S) {
   __shared__ float s_c[kD / 2], s_s[kD / 2];
   if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
   const int b = blockIdx.x;
   const int ps = pos[b];
+  if (part) {
+    const int cols4 = (Hq + 2 * Hkv) * kD / 4;
+    const long long split = (long long)gridDim.x * cols4;  // float4s per split
+    const float4* pr = reinterpret_cast<const float4*>(part) + (long long)b * cols4;
+    uint2* dst = reinterpret_cast<uint2*>(qkv + (long long)b * stride);
+    for (int j = threadIdx.x; j < cols4; j += blockDim.x) {
+      float4 v = pr[j];
+      for (int sp = 1; sp < S; ++sp) {
+        const float4 t = pr[sp * split + j];
+        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
+      }
+      __nv_bfloat162 o0 = __floats2bfloat162_rn(v.x, v.y), o1 = __floats2bfloat162_rn(v.z, v.w);
+      uint2 ob;
+      ob.x = *reinterpret_cast<uint32_t*>(&o0);
+      ob.y = *reinterpret_cast<uint32_t*>(&o1);
+      dst[j] = ob;
+    }
+    __syncthreads();
+  }
   if (threadIdx.x < kD / 2) {
     const int i = threadIdx.x;
     const double inv = exp2(-(2.0 * i / kD) * log2_theta);
@@ -753,6 +776,16 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
                              const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
                              int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
                              dak_stream_t stream) {
+  return dak::rope_kv_append_part(qkv, row_stride, B, Hq, Hkv, d, positions, rope_theta, block_table, page_size,
+                                  max_pages, k_hbm, v_hbm, k_host, v_host, pdl, stream, nullptr, 1);
+}
+
+}  // extern "C"
+
+dak_status dak::rope_kv_append_part(void* qkv, int64_t row_stride, int32_t B, int32_t Hq, int32_t Hkv, int32_t d,
+                                    const int32_t* positions, float rope_theta, const int32_t* block_table,
+                                    int32_t page_size, int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host,
+                                    void* v_host, int32_t pdl, void* stream, const float* part, int32_t S) {
   if (!qkv || !positions || !block_table || B <= 0 || Hq <= 0 || Hkv <= 0 || page_size <= 0 || max_pages <= 0 ||
       !(rope_theta > 1.f))
     return fail(DAK_EINVAL, "dak_rope_kv_append: bad arguments");
@@ -760,6 +793,7 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
   const long long stride = row_stride > 0 ? row_stride : (long long)(Hq + 2 * Hkv) * d;
   if (stride < (long long)(Hq + 2 * Hkv) * d || stride % 8 || !aligned16(qkv))
     return fail(DAK_EINVAL, "dak_rope_kv_append: qkv rows must be 16-byte aligned and hold q, k, v");
+  if (part && (!aligned16(part) || S < 1)) return fail(DAK_EINVAL, "dak_rope_kv_append: bad split-K partials");
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
@@ -772,8 +806,7 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::rope_append_kernel, (__nv_bfloat16*)qkv, stride, Hq, Hkv, positions,
                                   (double)log2((double)rope_theta), block_table, page_size, max_pages, (uint4*)k_hbm,
                                   (uint4*)v_hbm, (uint4*)k_host, (uint4*)v_host,
-                                  trace_slot(DAK_KIND_APPEND, B, Hkv, B)));
+                                  trace_slot(DAK_KIND_APPEND, B, Hkv, B), part, (int)S));
   return DAK_OK;
 }
 
-}  // extern "C"

@@ -35,6 +35,19 @@ unsigned long long* trace_slot(int kind, long long a, long long b, int grid);
 #define DAK_KIND_LAYERNORM 5
 #define DAK_KIND_EMBED 6
 
+// dak_linear with the split-K reduce optionally left to the consumer (dak_layer fuses it into the
+// next kernel): *ksplit_out = K splits of the launch (1: none, y written); with defer_reduce and
+// ksplit > 1 the fp32 partials part[s][n][m] (row stride M) stay in args->workspace.
+dak_status linear_enqueue(const dak_linear_args* args, void* stream, bool defer_reduce, int* ksplit_out);
+// Llama glue with the split-K reduce of the producing linear fused in (part == nullptr: plain bf16
+// input, as the exported dak_rope_kv_append / dak_silu_mul).
+dak_status rope_kv_append_part(void* qkv, int64_t row_stride, int32_t B, int32_t Hq, int32_t Hkv, int32_t d,
+                               const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
+                               int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
+                               void* stream, const float* part, int32_t S);
+dak_status silu_mul_part(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, void* stream,
+                         const float* part, int32_t S);
+
 }  // namespace dak
 
 #define DAK_CUDA_TRY(expr)                                                                       \

@@ -179,14 +179,41 @@ constexpr int kRowMax = 64;  // values per thread held in registers (cols <= 256
 
 // out[r, j] = bf16(silu(gu[r, j]) * gu[r, F + j])  (Llama MLP gate / up combine); 8 columns per
 // thread (F % 8 == 0, 16-byte aligned rows), else one
+// With part != nullptr, gate and up come from the producing linear's split-K fp32 partials
+// (part[s][r][j], row stride 2F, gridDim.y rows): g = bf16(sum_s part) in split order, exactly the
+// split-K reduce's value, then the same silu * up.
 __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloat16* __restrict__ out, int F,
-                                unsigned long long* tr, int vec) {
+                                unsigned long long* tr, int vec, const float* __restrict__ part, int S) {
   if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
   const __nv_bfloat16* g = gu + (long long)blockIdx.y * 2 * F;
   __nv_bfloat16* o = out + (long long)blockIdx.y * F;
-  if (vec) {
+  if (part) {  // F % 4 == 0: 4 columns per thread
+    const long long split = (long long)gridDim.y * 2 * F;
+    const float* pr = part + (long long)blockIdx.y * 2 * F;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F / 4; j += gridDim.x * blockDim.x) {
+      float4 a = reinterpret_cast<const float4*>(pr)[j], u = reinterpret_cast<const float4*>(pr + F)[j];
+      for (int sp = 1; sp < S; ++sp) {
+        const float4 ta = reinterpret_cast<const float4*>(pr + sp * split)[j];
+        const float4 tu = reinterpret_cast<const float4*>(pr + sp * split + F)[j];
+        a.x += ta.x; a.y += ta.y; a.z += ta.z; a.w += ta.w;
+        u.x += tu.x; u.y += tu.y; u.z += tu.z; u.w += tu.w;
+      }
+      const float av[4] = {a.x, a.y, a.z, a.w}, uv[4] = {u.x, u.y, u.z, u.w};
+      float r[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float ga = __bfloat162float(__float2bfloat16_rn(av[i])), ua = __bfloat162float(__float2bfloat16_rn(uv[i]));
+        r[i] = ga / (1.f + __expf(-ga)) * ua;
+      }
+      __nv_bfloat162 o0 = __floats2bfloat162_rn(r[0], r[1]), o1 = __floats2bfloat162_rn(r[2], r[3]);
+      uint2 ob;
+      ob.x = *reinterpret_cast<uint32_t*>(&o0);
+      ob.y = *reinterpret_cast<uint32_t*>(&o1);
+      reinterpret_cast<uint2*>(o)[j] = ob;
+    }
+  } else if (vec) {
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F / 8; j += gridDim.x * blockDim.x) {
       float a[8], u[8];
       bf16x8_to_f32(reinterpret_cast<const uint4*>(g)[j], a);
@@ -369,13 +396,17 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
       if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
       off += rows[i];
     }
-  } else {  // one fused [q; k; v] projection
-    dak_linear_args l = lin_args(a->qkv, qkv_cols, H, B, a->x, qkv, nullptr, DAK_ACT_NONE, a->cfg);
-    if ((st = prenorm(l, a->ln1_w, a->stats_in, a->stats_in_parts)) != DAK_OK) return st;
-    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
-  if ((st = dak_rope_kv_append(qkv, qkv_cols, B, Hq, Hkv, d, a->positions, a->rope_theta, a->block_table, a->page_size,
-                               a->max_pages, a->k_hbm, a->v_hbm, a->k_host, a->v_host, pdl, strm)) != DAK_OK)
+  int qkv_split = 1;  // split-K partials of the qkv projection, reduced inside the rotary/append kernel
+  if (!a->split_qkv) {  // one fused [q; k; v] projection
+    dak_linear_args l = lin_args(a->qkv, qkv_cols, H, B, a->x, qkv, nullptr, DAK_ACT_NONE, a->cfg);
+    if (a->x_prenormed && !fuse) l.x = hbuf;  // RMSNorm 1 written by the previous layer's combine
+    else if ((st = prenorm(l, a->ln1_w, a->stats_in, a->stats_in_parts)) != DAK_OK) return st;
+    if ((st = linear_enqueue(&l, strm, true, &qkv_split)) != DAK_OK) return st;
+  }
+  if ((st = rope_kv_append_part(qkv, qkv_cols, B, Hq, Hkv, d, a->positions, a->rope_theta, a->block_table, a->page_size,
+                                a->max_pages, a->k_hbm, a->v_hbm, a->k_host, a->v_host, pdl, strm,
+                                qkv_split > 1 ? (const float*)ws : nullptr, qkv_split)) != DAK_OK)
     return st;
   dak_attention_args at{};
   at.q = qkv; at.out = attn;
@@ -411,21 +442,27 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   } else if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? o_stats : nullptr, pdl, strm)) != DAK_OK) {
     return st;
   }
+  int up_split = 1;  // split-K partials of [gate; up], reduced inside the silu * up kernel
   {  // [gate; up] after RMSNorm 2 -> gu [B, 2F]
     dak_linear_args l = lin_args(a->up, 2LL * F, H, B, a->x, gu, nullptr, DAK_ACT_NONE, a->cfg);
     if (norm2_done) l.x = hbuf;
     else if ((st = prenorm(l, a->ln2_w, o_stats, o_parts)) != DAK_OK) return st;
-    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
+    if ((st = linear_enqueue(&l, strm, !fuse, &up_split)) != DAK_OK) return st;
   }
   {  // down: the SwiGLU operand fused (small batch) or one silu * up kernel (large batch)
     dak_linear_args l = lin_args(a->down, H, F, B, fuse ? gu : f2, tp ? partial : a->x, tp ? nullptr : a->x,
                                  DAK_ACT_NONE, a->cfg);
     if (fuse) l.x_swiglu = 1;
-    else if ((st = dak_silu_mul(gu, f2, B, F, pdl, strm)) != DAK_OK) return st;
+    else if ((st = silu_mul_part(gu, f2, B, F, pdl, strm, up_split > 1 ? (const float*)ws : nullptr, up_split)) != DAK_OK)
+      return st;
     if (!tp && fuse) l.stats_out = a->stats_out;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? a->stats_out : nullptr, pdl, strm)) != DAK_OK)
+    if (tp && !fuse && a->next_ln_w) {  // the next layer's RMSNorm 1 in the same combine kernel
+      if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
+        return st;
+    } else if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? a->stats_out : nullptr, pdl, strm)) != DAK_OK) {
       return st;
+    }
   }
   return DAK_OK;
 }
@@ -470,16 +507,7 @@ dak_status dak_rmsnorm(const void* x, const void* w, void* y, int32_t rows, int3
 }
 
 dak_status dak_silu_mul(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, dak_stream_t stream) {
-  if (!gu || !out || rows <= 0 || F <= 0) return fail(DAK_EINVAL, "dak_silu_mul: bad arguments");
-  const __nv_bfloat16* gp = (const __nv_bfloat16*)gu;
-  __nv_bfloat16* op = (__nv_bfloat16*)out;
-  int f = F;
-  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, F, rows);
-  int vec = F % 8 == 0 && aligned16(gu) && aligned16(out);
-  void* args[] = {&gp, &op, &f, &tr, &vec};
-  const int per = vec ? F / 8 : F;
-  const int bx = (per + 255) / 256 < 8 ? (per + 255) / 256 : 8;
-  return layer::launch_pdl((const void*)layer::silu_mul_kernel, dim3(bx, rows), dim3(256), args, (cudaStream_t)stream, pdl);
+  return dak::silu_mul_part(gu, out, rows, F, pdl, stream, nullptr, 1);
 }
 
 dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void* tok_emb, const void* pos_emb,
@@ -643,3 +671,20 @@ dak_status dak_layer_stats_parts(const dak_layer_args* a, int32_t* parts) {
 }
 
 }  // extern "C"
+
+dak_status dak::silu_mul_part(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, void* stream,
+                              const float* part, int32_t S) {
+  if ((!gu && !part) || !out || rows <= 0 || F <= 0) return fail(DAK_EINVAL, "dak_silu_mul: bad arguments");
+  if (part && (F % 4 || !aligned16(part) || ((uintptr_t)out & 7) || S < 1))
+    return fail(DAK_EINVAL, "dak_silu_mul: split-K partials need F %% 4 == 0 and aligned buffers");
+  const __nv_bfloat16* gp = (const __nv_bfloat16*)gu;
+  __nv_bfloat16* op = (__nv_bfloat16*)out;
+  int f = F;
+  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, F, rows);
+  int vec = F % 8 == 0 && aligned16(gu) && aligned16(out);
+  int s = S;
+  void* args[] = {&gp, &op, &f, &tr, &vec, &part, &s};
+  const int per = part ? F / 4 : vec ? F / 8 : F;
+  const int bx = (per + 255) / 256 < 8 ? (per + 255) / 256 : 8;
+  return layer::launch_pdl((const void*)layer::silu_mul_kernel, dim3(bx, rows), dim3(256), args, (cudaStream_t)stream, pdl);
+}

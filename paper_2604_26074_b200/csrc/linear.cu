@@ -1705,6 +1705,12 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
 }
 
 dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
+  return dak::linear_enqueue(args, stream, false, nullptr);
+}
+
+}  // extern "C"
+
+dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool defer_reduce, int* ksplit_out) {
   lin::Plan pl;
   dak_status st = lin::make_plan(args, &pl);
   if (st != DAK_OK) return st;
@@ -1712,7 +1718,9 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
   if (pl.grid && (st = lin::encode_xmap(&pl.p)) != DAK_OK) return st;
   pl.p.trace = trace_slot(DAK_KIND_LINEAR, args->M, args->K, pl.grid);
   if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
-  if (pl.p.ksplit > 1) {
+  const int S = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;
+  if (ksplit_out) *ksplit_out = S;
+  if (S > 1 && !defer_reduce) {
     const int vec = args->M % 4 == 0 && pl.p.ldy % 4 == 0 && ((uintptr_t)pl.p.y & 7) == 0 &&
                     ((uintptr_t)pl.p.residual & 7) == 0 && ((uintptr_t)pl.p.bias & 7) == 0;
     const long long per_row = vec ? args->M / 4 : args->M;
@@ -1730,6 +1738,8 @@ dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream) {
   }
   return DAK_OK;
 }
+
+extern "C" {
 
 size_t dak_linear_workspace_size(const dak_linear_args* args) {
   if (!args) return 0;

@@ -330,12 +330,13 @@ class dak_layer_args(C.Structure):
                 ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p), ("k_host", C.c_void_p), ("v_host", C.c_void_p),
                 ("block_table", C.c_void_p), ("positions", C.c_void_p), ("seq_lens", C.c_void_p),
                 ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
-                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("reserved", C.c_int32),
+                ("tp_rank", C.c_int32), ("tp_size", C.c_int32), ("x_prenormed", C.c_int32),
                 ("cfg", dak_launch_cfg), ("attn_cfg", dak_launch_cfg), ("split_qkv", C.c_int32),
                 ("reserved2", C.c_int32), ("q", dak_weight), ("k", dak_weight), ("v", dak_weight),
                 ("l2_prefetch_bytes", C.c_int64), ("next_w_hbm", C.c_void_p), ("next_w_hbm_bytes", C.c_int64),
                 ("fuse_norm", C.c_int32), ("stats_in_parts", C.c_int32), ("stats_in", C.c_void_p),
-                ("stats_out", C.c_void_p), ("rope_theta", C.c_float), ("reserved4", C.c_int32), ("comm", C.c_void_p)]
+                ("stats_out", C.c_void_p), ("rope_theta", C.c_float), ("reserved4", C.c_int32), ("comm", C.c_void_p),
+                ("next_ln_w", C.c_void_p)]
 
 
 _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,

@@ -244,6 +244,9 @@ class DakLlama:
         a.page_size, a.max_pages, a.chunk_pages = self.page, self.pages_per_req, self.chunk_pages
         a.tp_rank, a.tp_size, a.comm = self.rank, self.world, self.comm
         a.fuse_norm = int(self.fuse_norm)
+        if not self.fuse_norm and self.comm:  # the down combine writes the next layer's RMSNorm 1
+            a.x_prenormed = int(l > 0)
+            a.next_ln_w = self.layers[l + 1]["ln1_w"].data_ptr() if l + 1 < c.n_layers else None
         a.cfg = dak.launch_cfg(**self.launch)
         # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
         n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
@@ -287,11 +290,19 @@ class DakLlama:
 
     def kernels_per_step(self) -> int:
         """Kernels of this library per decode step (NCCL's own kernels not counted)."""
+        L = self.cfg.n_layers
         per_layer = (6 + (1 if self.chunks_per_req > 1 else 0)  # qkv, rope+append, attention, o, up, down (+combine)
-                     + (2 if self.comm else 0)  # residual kernels after the all-reduces
-                     + (0 if self.fuse_norm else (2 if self.comm else 3)))  # RMSNorm 1 (+ RMSNorm 2) + silu*up
-        n = 1 + per_layer * self.cfg.n_layers + (1 if self.fuse_norm else 2)  # embed ... (final RMSNorm +) head
-        return n + sum(self._reduce_launches(op) for op in self.linear_ops())
+                     + (2 if self.comm else 0)  # residual (+ RMSNorm) kernels after the all-reduces
+                     + (0 if self.fuse_norm else (1 if self.comm else 3)))  # silu*up (+ RMSNorm 1, RMSNorm 2)
+        n = 1 + per_layer * L + (1 if self.fuse_norm else 2)  # embed ... (final RMSNorm +) head
+        if not self.fuse_norm and self.comm:
+            n += 1  # RMSNorm 1 of layer 0 (later layers get it from the previous combine)
+        # split-K reduces: qkv's and [gate; up]'s are fused into the rotary / silu kernels when unfused
+        ops = list(self.linear_ops())
+        for i, op in enumerate(ops):
+            fused_reduce = not self.fuse_norm and i < 4 * L and i % 4 in (0, 2)
+            n += 0 if fused_reduce else self._reduce_launches(op)
+        return n
 
     def capture(self, stream: torch.cuda.Stream):
         with torch.cuda.stream(stream):

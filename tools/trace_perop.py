@@ -1,6 +1,8 @@
 """Per-op launch timeline of the per-op decode step (dak_layer path) from dak_trace stamps.
 
 Usage: python tools/trace_perop.py [layers] [batch] [--no-fuse-norm] [--no-pdl]
+       python tools/trace_perop.py [layers] [batch] --llama [--context N]   (Llama-3-70B TP8 rank shard,
+       HBM only, 1-rank NCCL communicator, as bench.py --workload llama3-70b-tp8)
 Captures one decode step in a CUDA graph with tracing on, replays it, and prints per launch the
 CTA start spread, the dependency-release time, the first-stage time and the completion time
 (all relative to the step's first stamp), then per-kind aggregates of the incremental time
@@ -20,13 +22,21 @@ from paper_2604_26074_b200.engine import DakOPT, HW, OPTConfig, OPT_30B
 
 
 def main():
-    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    args = [a for i, a in enumerate(sys.argv[1:], 1) if not a.startswith("--") and sys.argv[i - 1] != "--context"]
     layers = int(args[0]) if args else 8
     batch = int(args[1]) if len(args) > 1 else 8
-    cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
     hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
-    eng = DakOPT(cfg, batch, 64, hw, mode=dak.PLAN_BALANCED, fuse_norm="--no-fuse-norm" not in sys.argv,
-                 pdl="--no-pdl" not in sys.argv)
+    if "--llama" in sys.argv:
+        from dataclasses import replace
+        from paper_2604_26074_b200.llama import DakLlama, LLAMA3_70B
+        ctx = int(sys.argv[sys.argv.index("--context") + 1]) if "--context" in sys.argv else 4096
+        comm = dak.comm_init(dak.comm_unique_id(), 0, 1)
+        eng = DakLlama(replace(LLAMA3_70B, n_layers=layers), batch, ctx, hw, tp_rank=0, tp_size=8, comm=comm,
+                       mode=dak.PLAN_EXACT, y_req=0, pdl="--no-pdl" not in sys.argv)
+    else:
+        cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
+        eng = DakOPT(cfg, batch, 64, hw, mode=dak.PLAN_BALANCED, fuse_norm="--no-fuse-norm" not in sys.argv,
+                     pdl="--no-pdl" not in sys.argv)
     s = torch.cuda.Stream()
     with torch.cuda.stream(s):
         eng.enqueue_step(s)
