@@ -21,3 +21,8 @@ timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byt
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:split_linear \
   --launch-skip $(( LIN * 4 + 4 )) --launch-count 4 -o $OUT/prof_linear_$R \
   python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$R.log 2>&1; echo "ncu full rc $?"
+# full capture: layer 1's split attention inside the timed step
+ATT=$(python -c "from paper_2604_26074_b200.engine import OPT_30B; print(OPT_30B.n_layers)")
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:split_attention \
+  --launch-skip $(( ATT * 4 + 1 )) --launch-count 1 -o $OUT/prof_attn_$R \
+  python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $OUT/ncu_attn_$R.log 2>&1; echo "ncu attn rc $?"
