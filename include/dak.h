@@ -262,6 +262,11 @@ typedef struct {
   dak_launch_cfg cfg;           /* n_cta_host, n_cta_hbm, window, stages, congestion_control,   */
                                 /* pdl are honoured; force_path is ignored                      */
   int64_t q_row_stride;         /* elements between requests in q (0: Hq*d; fused QKV: (Hq+2Hkv)*d) */
+  const void* k_new;            /* optional fused KV append (dak_kv_append in the same kernel): the */
+  const void* v_new;            /* new token's k / v rows [B, Hkv, d] bf16 (row stride below) are  */
+  int64_t kv_new_stride;        /* written at position seq_len - 1 into the pools (which must be   */
+                                /* writable) and used for this step. NULL: the pools already hold */
+                                /* the token (dak_kv_append ran). Stride 0: Hkv*d; 16-byte aligned */
 } dak_attention_args;
 
 /* With cfg.pdl, the block table, seq_lens and the KV rows of tokens < seq_len - 1 are read BEFORE
@@ -403,7 +408,7 @@ typedef struct {
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);
-/* Enqueue one decode step of one layer: 9 kernels (LN, QKV, KV append, attention + combine,
+/* Enqueue one decode step of one layer: 8 kernels (LN, QKV, attention with the fused KV append + combine,
  * O + residual, LN, FC1 + ReLU, FC2 + residual). */
 dak_status dak_layer(const dak_layer_args* args, dak_stream_t stream);
 /* Number of statistics partials dak_layer writes to stats_out (the FC2 grid). Needs the device. */

@@ -61,6 +61,9 @@ struct Params {
   int host_window;    // host CTAs: max in-flight tiles per warp (0: none)
   int host_inflight;  // host CTAs: max in-flight bytes per CTA (congestion control; 0: none)
   int off_pairs;
+  const uint4* k_new;  // fused append: new token rows (16-byte units), nullptr: off
+  const uint4* v_new;
+  long long new_stride16;  // 16-byte units between requests of k_new / v_new
   unsigned long long* trace;   // dak_trace_enable slots (nullable): split kernel, combine kernel
   unsigned long long* trace2;
 };
@@ -295,8 +298,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
       load_ents();
     }
   };
-  // prologue: only tiles of old tokens (not holding position L - 1) before the dependency wait
-  while (pit < slots && pk < n_units && ptok + tt <= pL - 1) issue();
+  // prologue: only tiles of old tokens (not holding position L - 1) before the dependency wait; with
+  // the fused append every tile (the new token's row is patched into the slot after the wait)
+  while (pit < slots && pk < n_units && (p.k_new || ptok + tt <= pL - 1)) issue();
   grid_dep_wait();
   if (threadIdx.x == 0) tstamp(p.trace, 1);
   while (pit < slots && pk < n_units) issue();
@@ -332,6 +336,24 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
         cph ^= 1u;
       }
       const uint32_t kslot = su32(wr + (size_t)s * slot_bytes);
+      if (p.k_new && tile0 <= L - 1 && L - 1 < tile0 + tt) {
+        // fused KV append: the new token's K (lanes 0-15) / V (lanes 16-31) chunks go into this
+        // slot's row (the page row is stale) and into the page for later steps
+        const int t = L - 1 - tile0, j = lane & 15;
+        const uint4 v = (lane < 16 ? p.k_new : p.v_new)[(long long)b * p.new_stride16 + (long long)g * (kD / 8) + j];
+        const uint32_t off = (uint32_t)(t * (kD * 2) + ((((j >> 3) << 3) | ((j & 7) ^ (t & 7))) << 4));
+        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(kslot + (lane < 16 ? 0u : (uint32_t)tile_bytes) + off),
+                     "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the slot's next TMA refill
+        const int pg_i = (L - 1) / p.page;
+        const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + pg_i];
+        const long long idx = (long long)(e & ~kHostBit);
+        const bool eh = (e & kHostBit) != 0;
+        const char* pool = lane < 16 ? (eh ? p.k_host : p.k_hbm) : (eh ? p.v_host : p.v_hbm);
+        *reinterpret_cast<uint4*>(const_cast<char*>(pool) + (idx * p.Hkv + g) * (long long)page_bytes +
+                                  pg_off((L - 1) % p.page, j)) = v;
+        __syncwarp();
+      }
       for (int sub = 0; sub < tt && tile0 + sub < t1; sub += 16) {
         const int tok0 = tile0 + sub;
         const uint32_t kbase = kslot + sub * (kD * 2);
@@ -670,6 +692,15 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   if (need_ptrs) {
     if (!a->q || !a->out || !a->block_table || !a->seq_lens) return fail(DAK_EINVAL, "dak_attention: NULL tensor");
     if (!a->k_hbm && !a->k_host) return fail(DAK_EINVAL, "dak_attention: no KV pool");
+    if ((a->k_new == nullptr) != (a->v_new == nullptr)) return fail(DAK_EINVAL, "dak_attention: k_new and v_new go together");
+    if (a->k_new) {
+      const long long st = a->kv_new_stride > 0 ? a->kv_new_stride : (long long)a->Hkv * kD;
+      if (st % 8 || !aligned16(a->k_new) || !aligned16(a->v_new))
+        return fail(DAK_EINVAL, "dak_attention: k_new / v_new rows must be 16-byte aligned");
+      p.k_new = (const uint4*)a->k_new;
+      p.v_new = (const uint4*)a->v_new;
+      p.new_stride16 = st / 8;
+    }
     if (!aligned16(a->q) || !aligned16(a->k_hbm) || !aligned16(a->v_hbm) || !aligned16(a->k_host) || !aligned16(a->v_host))
       return fail(DAK_EINVAL, "dak_attention: q and pools must be 16-byte aligned");
     if (!a->workspace || a->workspace_bytes < out->ws_o + out->ws_lse)

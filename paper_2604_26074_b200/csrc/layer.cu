@@ -615,11 +615,11 @@ dak_status dak_layer(const dak_layer_args* a, dak_stream_t stream) {
     pf(l, a->o, H, (long long)Hq * d);
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
   }
-  if ((st = dak_kv_append(qkv + (size_t)Hq * d * 2, qkv + (size_t)(Hq + Hkv) * d * 2, qkv_cols, a->block_table,
-                          a->positions, B, Hkv, d, a->page_size, a->max_pages, a->k_hbm, a->v_hbm, a->k_host,
-                          a->v_host, pdl, strm)) != DAK_OK)
-    return st;
+  // the KV append (new token's k, v at position seq_len - 1) is fused into the attention kernel
   dak_attention_args at{};
+  at.k_new = qkv + (size_t)Hq * d * 2;
+  at.v_new = qkv + (size_t)(Hq + Hkv) * d * 2;
+  at.kv_new_stride = qkv_cols;
   at.q = qkv; at.out = attn;
   at.k_hbm = a->k_hbm; at.v_hbm = a->v_hbm; at.k_host = a->k_host; at.v_host = a->v_host;
   at.block_table = a->block_table; at.seq_lens = a->seq_lens;

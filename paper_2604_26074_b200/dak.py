@@ -105,7 +105,8 @@ class dak_attention_args(C.Structure):
                 ("k_host", C.c_void_p), ("v_host", C.c_void_p), ("block_table", C.c_void_p), ("seq_lens", C.c_void_p),
                 ("B", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("d", C.c_int32), ("page_size", C.c_int32),
                 ("max_pages", C.c_int32), ("chunk_pages", C.c_int32), ("scale", C.c_float), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("cfg", dak_launch_cfg), ("q_row_stride", C.c_int64)]
+                ("workspace_bytes", C.c_size_t), ("cfg", dak_launch_cfg), ("q_row_stride", C.c_int64),
+                ("k_new", C.c_void_p), ("v_new", C.c_void_p), ("kv_new_stride", C.c_int64)]
 
 
 _sig("dak_pack_kv_pages", C.c_int32, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p])
@@ -274,7 +275,8 @@ def pack_kv_pages(src, n_blocks: int, page_size: int, d: int, dst, stream=None):
 
 
 def attention_args(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, B, Hq, Hkv, d, page_size, max_pages,
-                   chunk_pages, scale=0.0, workspace=None, workspace_bytes=0, cfg=None, q_row_stride=0):
+                   chunk_pages, scale=0.0, workspace=None, workspace_bytes=0, cfg=None, q_row_stride=0, k_new=None,
+                   v_new=None, kv_new_stride=0):
     a = dak_attention_args()
     a.q, a.out = _ptr(q), _ptr(out)
     a.k_hbm, a.v_hbm, a.k_host, a.v_host = _ptr(k_hbm), _ptr(v_hbm), _ptr(k_host), _ptr(v_host)
@@ -285,6 +287,7 @@ def attention_args(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, 
     a.workspace, a.workspace_bytes = _ptr(workspace), int(workspace_bytes)
     a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
     a.q_row_stride = int(q_row_stride)
+    a.k_new, a.v_new, a.kv_new_stride = _ptr(k_new), _ptr(v_new), int(kv_new_stride)
     return a
 
 

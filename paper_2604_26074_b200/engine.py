@@ -462,8 +462,8 @@ class DakOPT:
     def kernels_per_step(self) -> int:
         if getattr(self, "use_step", False):
             return 1
-        # [q k v | qkv] append attn [combine] o fc1 fc2
-        per_layer = (6 if self.fused_qkv else 8) + (1 if self.chunks_per_req > 1 else 0)
+        # [q k v | qkv] attn(+ fused KV append) [combine] o fc1 fc2
+        per_layer = (5 if self.fused_qkv else 7) + (1 if self.chunks_per_req > 1 else 0)
         if self.fuse_norm:
             return 1 + per_layer * self.cfg.n_layers + 1
         return 1 + (per_layer + 2) * self.cfg.n_layers + 2

@@ -127,6 +127,52 @@ def test_kv_append(D, torch):
     assert_close(Kx.bf16_to_f64(from_dev(out)), ref)
 
 
+@pytest.mark.parametrize("Ls,cp", [([130, 64, 1], 1), ([700, 63, 129], 2), ([2, 1025], 4)])
+def test_attention_fused_kv_append(D, torch, Ls, cp):
+    """dak_attention with k_new / v_new (the KV append fused into the attention kernel): the pools
+    end up exactly as after dak_kv_append (both tiers), and the output equals the oracle over the
+    full context (the new token's row is used although the pool row was blank when the kernel
+    started). Half of each request's chunks on the host."""
+    from tests.gpu_util import make_paged_kv, PagedKV, to_dev, from_dev, assert_close
+    Hkv, Hq, page, d = 2, 8, 64, 128
+    q, K, V, (kg, vg, kh, vh, bt), _ = make_paged_kv([L + 1 for L in Ls], Hkv, d, page, 0.5, cp, 91, Hq)
+    kg2, vg2, kh2, vh2 = kg.copy(), vg.copy(), kh.copy(), vh.copy()
+    for b, L in enumerate(Ls):
+        e = int(np.uint32(bt[b, L // page]))
+        pool_k, pool_v = (kh2, vh2) if e & 0x80000000 else (kg2, vg2)
+        pool_k[e & 0x7FFFFFFF, :, L % page] = 0
+        pool_v[e & 0x7FFFFFFF, :, L % page] = 0
+    kv = PagedKV(D, kg2, vg2, kh2, vh2, bt, page)
+    full = PagedKV(D, kg, vg, kh, vh, bt, page)
+    # new rows inside a strided [B, (Hq + 2 Hkv) d] buffer, as the fused QKV projection leaves them
+    B = len(Ls)
+    qkv = np.zeros((B, (Hq + 2 * Hkv) * d), np.uint16)
+    qkv[:, Hq * d:(Hq + Hkv) * d] = np.stack([K[b][L] for b, L in enumerate(Ls)]).reshape(B, -1)
+    qkv[:, (Hq + Hkv) * d:] = np.stack([V[b][L] for b, L in enumerate(Ls)]).reshape(B, -1)
+    qkvd = to_dev(qkv)
+    out = torch.empty((B, Hq, d), dtype=torch.int16, device="cuda")
+    sl = torch.tensor([L + 1 for L in Ls], dtype=torch.int32, device="cuda")
+    qd = to_dev(q)
+    a = D.attention_args(qd, out, kv.kg, kv.vg, kv.kh.dp, kv.vh.dp, kv.bt, sl, B, Hq, Hkv, d, page, bt.shape[1], cp,
+                         k_new=qkvd.data_ptr() + Hq * d * 2, v_new=qkvd.data_ptr() + (Hq + Hkv) * d * 2,
+                         kv_new_stride=(Hq + 2 * Hkv) * d)
+    ws = torch.empty(max(D.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
+    D.attention(a)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(kv.kg), from_dev(full.kg)) and np.array_equal(from_dev(kv.vg), from_dev(full.vg))
+    assert np.array_equal(kv.kh.numpy(), full.kh.numpy()) and np.array_equal(kv.vh.numpy(), full.vh.numpy())
+    ref = Kx.paged_attention(q, kg, vg, kh, vh, bt, [L + 1 for L in Ls], page)
+    assert_close(Kx.bf16_to_f64(from_dev(out)), ref)
+    # and bitwise equal to the unfused path (append first, then attention over the full pools)
+    out2 = torch.empty_like(out)
+    a2 = D.attention_args(qd, out2, full.kg, full.vg, full.kh.dp, full.vh.dp, full.bt, sl, B, Hq, Hkv, d, page,
+                          bt.shape[1], cp, workspace=ws, workspace_bytes=ws.numel())
+    D.attention(a2)
+    torch.cuda.synchronize()
+    assert np.array_equal(from_dev(out), from_dev(out2))
+
+
 @pytest.mark.slow
 def test_c4_128k_half_host_sampled(D, torch):
     """BASELINE configs[3]: GQA decode attention over a 128k-token context, 64 q / 8 kv heads,
