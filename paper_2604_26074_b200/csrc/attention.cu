@@ -235,7 +235,9 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   const int slot_bytes = 2 * tt * kD * 2;
   int slots = max(1, min(p.max_slots, per_warp / slot_bytes));
   if (host && p.host_window > 0) slots = min(slots, p.host_window);
-  if (host && p.host_inflight > 0) slots = min(slots, max(1, p.host_inflight / (active * slot_bytes)));  // congestion cap
+  // congestion cap on in-flight host bytes, but never below double buffering per warp (one slot per
+  // warp exposes the full link latency per tile: C4 B = 4 at r*, 0.90 -> 0.97 of EB(r*) without it)
+  if (host && p.host_inflight > 0) slots = min(slots, max(2, p.host_inflight / (active * slot_bytes)));
   const int tile_bytes = tt * kD * 2;
 
   uint64_t* wf = full + warp * kMaxSlots;
@@ -446,11 +448,11 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
 }
 
 // merge chunk partials: out[b, h, :] = sum_c w_c o_c / sum_c w_c, w_c = 2^(lse_c - max lse).
-// One 256-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 8, ... with a running
-// max (lane = 4 dims, float4 loads, several chunks in flight), then the 8 warp partials are
-// rescaled to the common max and summed in warp order.
+// One 512-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 16, ... with a running
+// max (lane = 4 dims, float4 loads, several chunks in flight), then the 16 warp partials are
+// rescaled to the common max and summed in warp order (16 warps: one L2 round trip for 128 chunks).
 // The order depends only on the chunk count (bitwise r-invariant).
-constexpr int kCombineThreads = 256;
+constexpr int kCombineThreads = 512;
 __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p) {
   __shared__ float s_red[kCombineThreads / 32];
   __shared__ float4 s_acc[kCombineThreads / 32][kD / 4];
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p
   // (no separate max pass: the loads of every chunk are independent of the arithmetic)
   float m = -INFINITY, den = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
+#pragma unroll 8
   for (int c = warp; c < nch; c += kCombineThreads / 32) {
     const long long u = base + (long long)c * p.G;
     const float ls = p.part_lse[u];
