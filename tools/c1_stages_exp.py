@@ -1,3 +1,6 @@
+"""C1 (4096 x 4096 GEMV, N = 1) per-launch time over the ring depth and KC (development experiment):
+smaller SMEM footprints would let two CTAs share an SM so that chained launches overlap (PDL).
+Result (profiles/r01/sweeps.txt): none beat the default (kc 512, 5 stages, 7.1 us per launch)."""
 import sys, os, json
 sys.path.insert(0, "/root/repo")
 from tools.bench_linear import time_cfg
