@@ -553,69 +553,62 @@ __global__ void append_kernel(const uint4* __restrict__ k_new, const uint4* __re
 // Llama decode KV write with rotary positions: rotate q (in place) and k of the new token of every
 // request at positions[b] (rotate-half pairs (i, i + d/2), angle pos / theta^(2i/d), computed in
 // double then fp32 sincos of the reduced angle), then append k (rotated) and v to the page pools.
-// With part != nullptr the row is first materialised from the producing linear's split-K fp32
-// partials: qkv[b][c] = bf16(sum_s part[s][b][c]) in split order (the split-K reduce, fused here;
-// part row stride = (Hq + 2 Hkv) * d, N = gridDim.x rows per split).
-__global__ void __launch_bounds__(256) rope_append_kernel(__nv_bfloat16* qkv, long long stride, int Hq, int Hkv,
-                                                          const int* pos, double log2_theta, const int* block_table,
-                                                          int page, int max_pages, uint4* k_hbm, uint4* v_hbm,
-                                                          uint4* k_host, uint4* v_host, unsigned long long* tr,
-                                                          const float* part, int S) {
-  __shared__ float s_c[kD / 2], s_s[kD / 2];
+// One 64-thread CTA per (request b, head hh) of the [q heads | k heads | v heads] row; thread i owns
+// the rotate-half pair (i, i + 64). With part != nullptr the two values are first reduced from the
+// producing linear's split-K fp32 partials: bf16(sum_s part[s][b][c]) in split order (the split-K
+// reduce, fused here; part row stride = (Hq + 2 Hkv) * d, B rows per split). q and k heads are
+// rotated (angle pos / theta^(2i/d), double-reduced, fp32 sincos); k and v heads are also written
+// into the page at position pos (DAK-PG swizzle). The row in qkv is rewritten (q is read by attention).
+__global__ void __launch_bounds__(64) rope_append_kernel(__nv_bfloat16* qkv, long long stride, int Hq, int Hkv,
+                                                         const int* pos, double log2_theta, const int* block_table,
+                                                         int page, int max_pages, uint4* k_hbm, uint4* v_hbm,
+                                                         uint4* k_host, uint4* v_host, unsigned long long* tr,
+                                                         const float* part, int S, int B) {
   if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
   grid_dep_wait();
-  const int b = blockIdx.x;
+  const int H3 = Hq + 2 * Hkv;
+  const int b = blockIdx.x / H3, hh = blockIdx.x % H3;
+  const int i = threadIdx.x;  // 0 .. 63
   const int ps = pos[b];
+  __nv_bfloat16* v = qkv + (long long)b * stride + (long long)hh * kD;
+  float x1, x2;
   if (part) {
-    const int cols4 = (Hq + 2 * Hkv) * kD / 4;
-    const long long split = (long long)gridDim.x * cols4;  // float4s per split
-    const float4* pr = reinterpret_cast<const float4*>(part) + (long long)b * cols4;
-    uint2* dst = reinterpret_cast<uint2*>(qkv + (long long)b * stride);
-    for (int j = threadIdx.x; j < cols4; j += blockDim.x) {
-      float4 v = pr[j];
-      for (int sp = 1; sp < S; ++sp) {
-        const float4 t = pr[sp * split + j];
-        v.x += t.x; v.y += t.y; v.z += t.z; v.w += t.w;
-      }
-      __nv_bfloat162 o0 = __floats2bfloat162_rn(v.x, v.y), o1 = __floats2bfloat162_rn(v.z, v.w);
-      uint2 ob;
-      ob.x = *reinterpret_cast<uint32_t*>(&o0);
-      ob.y = *reinterpret_cast<uint32_t*>(&o1);
-      dst[j] = ob;
+    const long long cols = (long long)H3 * kD, split = (long long)B * cols;
+    const float* pr = part + (long long)b * cols + (long long)hh * kD;
+    float a1 = pr[i], a2 = pr[i + kD / 2];
+    for (int sp = 1; sp < S; ++sp) {
+      a1 += pr[sp * split + i];
+      a2 += pr[sp * split + i + kD / 2];
     }
-    __syncthreads();
+    x1 = __bfloat162float(__float2bfloat16_rn(a1));
+    x2 = __bfloat162float(__float2bfloat16_rn(a2));
+  } else {
+    x1 = __bfloat162float(v[i]);
+    x2 = __bfloat162float(v[i + kD / 2]);
   }
-  if (threadIdx.x < kD / 2) {
-    const int i = threadIdx.x;
+  __nv_bfloat16 o1 = __float2bfloat16_rn(x1), o2 = __float2bfloat16_rn(x2);
+  if (hh < Hq + Hkv) {  // rotary on q and k heads
     const double inv = exp2(-(2.0 * i / kD) * log2_theta);
     const double ang = fmod((double)ps * inv, 6.283185307179586476925286766559);
     float sn, cs;
     sincosf((float)ang, &sn, &cs);
-    s_c[i] = cs;
-    s_s[i] = sn;
+    o1 = __float2bfloat16_rn(x1 * cs - x2 * sn);
+    o2 = __float2bfloat16_rn(x2 * cs + x1 * sn);
   }
-  __syncthreads();
-  __nv_bfloat16* row = qkv + (long long)b * stride;
-  for (int j = threadIdx.x; j < (Hq + Hkv) * (kD / 2); j += blockDim.x) {
-    const int hh = j / (kD / 2), i = j % (kD / 2);
-    __nv_bfloat16* v = row + (long long)hh * kD;  // q heads then k heads are contiguous
-    const float x1 = __bfloat162float(v[i]), x2 = __bfloat162float(v[i + kD / 2]);
-    v[i] = __float2bfloat16_rn(x1 * s_c[i] - x2 * s_s[i]);
-    v[i + kD / 2] = __float2bfloat16_rn(x2 * s_c[i] + x1 * s_s[i]);
-  }
-  __syncthreads();
-  const uint32_t e = (uint32_t)block_table[(long long)b * max_pages + ps / page];
-  const long long idx = (long long)(e & ~kHostBit);
-  const bool eh = (e & kHostBit) != 0;
-  const int t = ps % page;
-  const uint4* krow = reinterpret_cast<const uint4*>(row + (long long)Hq * kD);
-  const uint4* vrow = reinterpret_cast<const uint4*>(row + (long long)(Hq + Hkv) * kD);
-  for (int j = threadIdx.x; j < Hkv * (kD / 8); j += blockDim.x) {
-    const int g = j / (kD / 8), c = j % (kD / 8);
-    const long long off = ((idx * Hkv + g) * (long long)page * kD * 2 + pg_off(t, c)) / 16;
-    (eh ? k_host : k_hbm)[off] = krow[j];
-    (eh ? v_host : v_hbm)[off] = vrow[j];
+  v[i] = o1;
+  v[i + kD / 2] = o2;
+  if (hh >= Hq) {  // k or v head: append at position ps
+    const bool is_k = hh < Hq + Hkv;
+    const int g = is_k ? hh - Hq : hh - Hq - Hkv;
+    const uint32_t e = (uint32_t)block_table[(long long)b * max_pages + ps / page];
+    const long long idx = (long long)(e & ~kHostBit);
+    const bool eh = (e & kHostBit) != 0;
+    const int t = ps % page;
+    char* pool = reinterpret_cast<char*>(is_k ? (eh ? k_host : k_hbm) : (eh ? v_host : v_hbm));
+    char* pg = pool + (idx * Hkv + g) * (long long)page * kD * 2;
+    *reinterpret_cast<__nv_bfloat16*>(pg + pg_off(t, i >> 3) + (i & 7) * 2) = o1;
+    *reinterpret_cast<__nv_bfloat16*>(pg + pg_off(t, (i + kD / 2) >> 3) + (i & 7) * 2) = o2;
   }
   if (threadIdx.x == 0) tstamp(tr, 3);
 }
@@ -831,15 +824,15 @@ dak_status dak::rope_kv_append_part(void* qkv, int64_t row_stride, int32_t B, in
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(B);
-  cfg.blockDim = dim3(256);
+  cfg.gridDim = dim3(B * (Hq + 2 * Hkv));
+  cfg.blockDim = dim3(64);
   cfg.stream = (cudaStream_t)stream;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::rope_append_kernel, (__nv_bfloat16*)qkv, stride, Hq, Hkv, positions,
                                   (double)log2((double)rope_theta), block_table, page_size, max_pages, (uint4*)k_hbm,
                                   (uint4*)v_hbm, (uint4*)k_host, (uint4*)v_host,
-                                  trace_slot(DAK_KIND_APPEND, B, Hkv, B), part, (int)S));
+                                  trace_slot(DAK_KIND_APPEND, B, Hkv, B * (Hq + 2 * Hkv)), part, (int)S, (int)B));
   return DAK_OK;
 }
 
