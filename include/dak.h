@@ -166,7 +166,8 @@ typedef struct {
   const void* w_hbm;    /* DAK-KC packed rows [h,M)   (device; may be NULL when h == M)       */
   int64_t M, K, h;      /* 0 <= h <= M                                                         */
   int32_t kc;           /* KC used to pack both tiers                                          */
-  int32_t N;            /* batch columns, 1..64 (1..256 on the tcgen05 path: kc == 64)         */
+  int32_t N;            /* batch columns, 1..64 (1..512 on the tcgen05 path: kc == 64; N > 256 */
+                        /* plain GEMM only: no ln_w / x_swiglu / stats_out)                  */
   const void* x;        /* [N, K] bf16 row-major, device                                       */
   void* y;              /* [N, M] bf16 row-major, device                                       */
   const void* bias;     /* [M] bf16 or NULL                                                    */

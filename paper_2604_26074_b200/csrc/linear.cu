@@ -36,7 +36,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
 constexpr int kMaxN = 64;     // mma.sync paths
-constexpr int kMaxNTc = 256;  // tcgen05 path (one MMA covers N <= 256)
+constexpr int kMaxNTc = 512;  // tcgen05 path (one MMA covers N <= 256; two N halves up to 512)
 constexpr int kRptMax = 16;   // FMA path: rows per thread
 constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
 constexpr int kMaxStages = 16;
@@ -840,6 +840,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       auto load_x = [&](int slot, int i) {
         unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
         tma_3d(dst, xmap, 0, 0, kbeg + i, &full[slot]);
+        if constexpr (N8 > 256) tma_3d(dst + 256 * 128, xmap, 0, 256, kbeg + i, &full[slot]);  // rows 256..: 2nd box
         if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K >> 6) + kbeg + i), &full[slot]);
       };
       for (int i = 0; i < pro; ++i) load_x(i, i);
@@ -857,7 +858,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
     // MMA issuer: the whole warp walks the ring (converged), one elected lane issues
     {
       // kind::f16 instruction descriptor: D f32, A / B bf16, both K-major, N = N8, M = 128
-      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N8 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+      constexpr int NI = N8 > 256 ? 256 : N8;  // N per instruction (N8 = 512: two halves of 256 columns)
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(NI >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
       const uint32_t wr = su32(wring), xr = su32(xring);
       uint32_t leader;
       asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
@@ -877,6 +879,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
             for (int mt = 0; mt < mtiles; ++mt)
               umma_bf16(tmem + (uint32_t)(((k % KCH) * mtiles + mt) * N8), umma_desc_sw128(ws + mt * 128 * 128 + k * 32),
                         bd, idesc, (KCH == 4 ? i : (i | k)) != 0);
+            if constexpr (N8 > 256)  // columns 256..511: x rows 256.. (second box, 32 KB on), TMEM +256
+              umma_bf16(tmem + 256u, umma_desc_sw128(ws + k * 32), umma_desc_sw128(xs + 256 * 128 + k * 32), idesc,
+                        (i | k) != 0);
           }
           umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
         }
@@ -1203,7 +1208,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (h < 0 || h > M) return fail(DAK_EINVAL, "dak_linear: h must be in [0, M]");
   if (N > kMaxNTc) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d", N, kMaxNTc);
   // n8 tiles (compiled: 1, 2, 4, 8 on every path; 16, 32 on the tcgen05 path)
-  const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : (N <= 64 ? 8 : (N <= 128 ? 16 : 32))));
+  const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : (N <= 64 ? 8 : (N <= 128 ? 16 : (N <= 256 ? 32 : 64)))));
   if (K % 64) return fail(DAK_EUNSUPPORTED, "dak_linear: K %% 64 != 0");
   if (kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
     return fail(DAK_EINVAL, "dak_linear: kc must be a power of two in [64, 2048] dividing K");
@@ -1239,9 +1244,14 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (a->x_swiglu && (path == 1 || a->ln_w)) return fail(DAK_EINVAL, "dak_linear: x_swiglu needs a tensor-core path and no pre-norm");
   const int n8 = path == 1 ? 8 : nt_eff * 8;
   const long long x_stage = (long long)n8 * kc * 2 * (a->x_swiglu ? 2 : 1);
-  const long long smem_rows = ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
+  // N > 256 (tcgen05, 512 TMEM columns): one M tile per CTA, a 64 KB x box per stage, two stages
+  const bool wide = path == 3 && n8 > 256;
+  if (wide && (a->ln_w || a->x_swiglu || a->stats_out))
+    return fail(DAK_EUNSUPPORTED, "dak_linear: N > 256 supports the plain GEMM only (no pre-norm / SwiGLU / statistics)");
+  const long long smem_rows = wide ? ((kSmemBudget - 2048 - 16384) / 2 - x_stage) / (kc * 2) / 16 * 16
+                                   : ((kSmemBudget - 2048 - 8192) / 3 - x_stage) / (kc * 2) / 16 * 16;
   if (path == 1 && kc > 8 * kConsumers) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path needs kc <= %d", 8 * kConsumers);
-  const long long cap = std::min(path == 3 ? 256LL : path_row_cap(path, kc, nt), smem_rows);
+  const long long cap = std::min(path == 3 ? (wide ? 128LL : 256LL) : path_row_cap(path, kc, nt), smem_rows);
   if (cap < 16) return fail(DAK_EUNSUPPORTED, "dak_linear: kc=%d leaves no room for a 16-row stage", kc);
 
   int n_host = 0;
@@ -1286,7 +1296,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // splits are fixed by (M, K, SM count), never by the tier split h, keeping every row's summation order
   // independent of the tier split (bitwise r-invariance). Needs caller workspace for the partials.
   int ksplit = 1, k64_split = (int)(K / 64);
-  if (path == 3 && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
+  if (path == 3 && !wide && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
     // S from (M, K, SM count) only: as many splits as keep all items in ONE wave (even if h adds a
     // tile). Measured at the Llama TP8 b64 shapes (profiles/r01/splitk_sweep.txt): a second wave or
     // shorter splits cost more than the idle SMs of a partial wave.
@@ -1467,7 +1477,7 @@ static dak_status encode_xmap(Params* p) {
   const long long ldx = p->swiglu ? 2 * p->K : p->K;  // [gate | up] rows are 2K wide
   const cuuint64_t dims[3] = {64, (cuuint64_t)p->N, (cuuint64_t)(ldx / 64)};
   const cuuint64_t strides[2] = {(cuuint64_t)ldx * 2, 128};
-  const cuuint32_t box[3] = {64, (cuuint32_t)p->n8, (cuuint32_t)(p->kc / 64)};
+  const cuuint32_t box[3] = {64, (cuuint32_t)(p->n8 > 256 ? 256 : p->n8), (cuuint32_t)(p->kc / 64)};  // TMA box <= 256 rows
   const cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(&p->xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)p->x, dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1602,6 +1612,7 @@ dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
     case 8: return launch_umma_xf<8>(pl, s, pdl);
     case 16: return launch_umma_xf<16>(pl, s, pdl);
     case 32: return launch_umma_xf<32>(pl, s, pdl);
+    case 64: return launch_umma_t<64, 0>(pl, s, pdl);  // N 257..512: plain GEMM only
   }
   return fail(DAK_EUNSUPPORTED, "dak_linear: no tcgen05 kernel instance for %d n8 tiles", pl.nn);
 }

@@ -259,6 +259,26 @@ def test_linear_tcgen05_r_invariance_and_integer_exact(D, torch):
         assert np.array_equal(o, outs[0])
 
 
+@pytest.mark.parametrize("M,K,N,h", [(1024, 1024, 512, 64), (700, 2048, 384, 0), (300, 512, 257, 296),
+                                     (7168, 1024, 512, 56)])
+def test_linear_tcgen05_wide_n(D, torch, M, K, N, h):
+    """N in (256, 512] (prefill-like batch): two N = 256 MMAs per K step into 512
+    TMEM columns, x as two 256-row TMA boxes, one M tile per CTA -- vs the oracle; integer inputs
+    bitwise, and bitwise independent of the tier split."""
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, M + N), bias=True)
+    y, sl, a = run_linear(D, torch, W, x, h, 64, bias=b)
+    q = D.linear_query(a)
+    assert q["path"] == 3 and q["rows_per_cta_hbm_max"] <= 128
+    ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
+    from tests.gpu_util import assert_close
+    assert_close(Kx.bf16_to_f64(y), ref)
+    Wi, xi, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, M), kind="int")
+    outs = [run_linear(D, torch, Wi, xi, hh, 64)[0] for hh in (0, h, M - M % 8)]  # auto tcgen05: h % 8 == 0
+    assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(Kx.split_linear(Wi[:0], Wi, xi)))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+
+
 @pytest.mark.parametrize("xf,N", [(1, 64), (1, 24), (2, 64), (2, 128)])
 def test_linear_tcgen05_operand_transforms(D, torch, xf, N):
     """tcgen05 path with the fused pre-norm (RMSNorm) or SwiGLU operand applied in SMEM by the
