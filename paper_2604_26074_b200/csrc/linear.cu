@@ -36,7 +36,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
 constexpr int kMaxN = 64;     // mma.sync paths
-constexpr int kMaxNTc = 512;  // tcgen05 path (one MMA covers N <= 256; two N halves up to 512)
+constexpr int kMaxNTc = 1024;  // tcgen05 path (one MMA covers N <= 256; two N halves up to 512; CTA pairs up to 1024)
 constexpr int kRptMax = 16;   // FMA path: rows per thread
 constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
 constexpr int kMaxStages = 16;
@@ -66,6 +66,8 @@ struct __align__(64) Params {
   int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
   int swiglu;       // x = [gate | up] ([N, 2K]); the operand is silu(gate) * up
   int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
+  int pair;         // tcgen05, N > 512: CTA pairs share rows, rank r computes columns [512 r, 512 r + 512)
+  int wmc;          // pair mode: the pair is a 2-CTA cluster and rank 0 multicasts each W tile to both
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
   int ksplit;       // tcgen05 split-K: K splits (1: off); CTA = (tier row block of 128, split)
@@ -735,6 +737,25 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
                : "memory");
 }
+// the same arrive delivered to the mbarrier at this offset in every CTA of ctamask (cluster)
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   su32(bar)), "h"(mask)
+               : "memory");
+}
+// 1-D bulk copy delivered to the same SMEM offset of every CTA in ctamask (each CTA's own mbarrier
+// at that offset receives the complete_tx): one fetch of a weight tile for both CTAs of a pair
+__device__ __forceinline__ void bulk_g2s_mc_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask,
+                                                 uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar)), "h"(mask), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
@@ -774,9 +795,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
     re = rb + 128 < R_tier ? rb + 128 : R_tier;
     kbeg = ks * p.k64_split;
     kend = kbeg + p.k64_split < kend ? kbeg + p.k64_split : kend;
+  } else if (N8 > 256 && p.pair) {  // CTA pairs: both ranks take the pair's rows
+    tier_rows(R_tier, (host ? cta : cta - p.n_host) >> 1, (host ? p.n_host : p.n_hbm) >> 1, p.rgran, &rb, &re);
   } else {
     tier_rows(R_tier, host ? cta : cta - p.n_host, host ? p.n_host : p.n_hbm, p.rgran, &rb, &re);
   }
+  const int prank = (N8 > 256 && p.pair) ? (cta & 1) : 0;  // pair rank = cluster rank (pairs start even)
+  const bool wmc = N8 > 256 && p.pair && p.wmc;
   const int R = (int)(re - rb);
   const long long row0 = host ? rb : p.h + rb;
   const char* wsrc = host ? p.w_host : p.w_hbm;
@@ -791,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], wmc && prank == 0 ? 2 : 1);  // W multicast: rank 0 refills after BOTH consumed
     }
     mbar_init(done, 1);
     for (int s = 0; s < kMaxStages; ++s) mbar_init(&xready[s], 3);  // three transform warps
@@ -806,6 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (wmc) cluster_sync_all();  // the peer's barrier inits are visible before any multicast / remote arrive
   if (threadIdx.x == 0) tstamp(p.trace, 0);
   grid_dep_launch();
   if (R <= 0) {
@@ -825,9 +851,16 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       const uint64_t pol = policy_evict_first();
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      // W tile of a stage: own copy, or (pair + multicast) rank 0 fetches it once for both CTAs;
+      // every CTA's full barrier expects the W bytes either way
+      auto load_w = [&](int slot, int i) {
+        if (!wmc) bulk_g2s_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot], pol);
+        else if (prank == 0)
+          bulk_g2s_mc_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot], 3, pol);
+      };
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);
-        bulk_g2s_hint(wring + (size_t)i * wstage, src + (long long)i * chunk_stride, w_bytes, &full[i], pol);
+        load_w(i, i);
       }
       grid_dep_wait();
       tstamp(p.trace, 1);
@@ -839,8 +872,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       }
       auto load_x = [&](int slot, int i) {
         unsigned char* dst = xring + (size_t)slot * p.x_stage_bytes;
-        tma_3d(dst, xmap, 0, 0, kbeg + i, &full[slot]);
-        if constexpr (N8 > 256) tma_3d(dst + 256 * 128, xmap, 0, 256, kbeg + i, &full[slot]);  // rows 256..: 2nd box
+        tma_3d(dst, xmap, 0, 512 * prank, kbeg + i, &full[slot]);
+        if constexpr (N8 > 256) tma_3d(dst + 256 * 128, xmap, 0, 512 * prank + 256, kbeg + i, &full[slot]);  // 2nd box
         if (XF == 2) tma_3d(dst + (p.x_stage_bytes >> 1), xmap, 0, 0, (int)((p.K >> 6) + kbeg + i), &full[slot]);
       };
       for (int i = 0; i < pro; ++i) load_x(i, i);
@@ -849,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       for (int i = pro; i < nchunks; ++i) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], w_bytes + x_tx);
-        bulk_g2s_hint(wring + (size_t)s * wstage, src + (long long)i * chunk_stride, w_bytes, &full[s], pol);
+        load_w(s, i);
         load_x(s, i);
         if (++s == slots) { s = 0; ph ^= 1u; }
       }
@@ -883,7 +916,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
               umma_bf16(tmem + 256u, umma_desc_sw128(ws + k * 32), umma_desc_sw128(xs + 256 * 128 + k * 32), idesc,
                         (i | k) != 0);
           }
-          umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
+          if (wmc && prank == 1) umma_commit_mc(&empty[s], 3);  // both CTAs' slot s: rank 0 refills W into both
+          else umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
         }
         __syncwarp();
         if (++s == slots) { s = 0; ph ^= 1u; }
@@ -1005,7 +1039,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
         if (r < R) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int n = c0 + e;
+            const int n = 512 * prank + c0 + e;  // pair rank 1 owns columns 512..
             if (n < N) {
               float o = acc[e] + bias;
               if (p.act == DAK_ACT_RELU) o = fmaxf(o, 0.f);
@@ -1046,6 +1080,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
     tc_fence_before();
   }
   __syncthreads();
+  if (wmc) cluster_sync_all();  // neither CTA exits while its peer may still arrive on its barriers
   if (threadIdx.x == 32 && p.trace) tstamp(p.trace, 3);
   if (warp == 1) {
     tc_fence_after();
@@ -1209,6 +1244,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (N > kMaxNTc) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d", N, kMaxNTc);
   // n8 tiles (compiled: 1, 2, 4, 8 on every path; 16, 32 on the tcgen05 path)
   const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : (N <= 64 ? 8 : (N <= 128 ? 16 : (N <= 256 ? 32 : 64)))));
+  // N > 512: CTA pairs over the same rows (rank r: columns [512 r, 512 r + 512)); counts below are pairs
+  const bool pair = N > 512;
   if (K % 64) return fail(DAK_EUNSUPPORTED, "dak_linear: K %% 64 != 0");
   if (kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
     return fail(DAK_EINVAL, "dak_linear: kc must be a power of two in [64, 2048] dividing K");
@@ -1229,7 +1266,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // default: tensor cores for every N -- mma.sync (path 2) up to N = 16; tcgen05 (path 3) beyond,
   // where mma.sync becomes issue-bound, when its operand constraints hold
   int path = c.force_path ? c.force_path : 2;
-  if (!c.force_path && N > 16 && kc == 64 && c.cluster <= 1 && h % 8 == 0)
+  if (!c.force_path && N > 16 && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster 2 at N > 512: W multicast pairs
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
@@ -1262,7 +1299,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   int n_hbm = 0;
   if (h < M) {
-    n_hbm = c.n_cta_hbm > 0 ? c.n_cta_hbm : std::max(1, sms - n_host);
+    n_hbm = c.n_cta_hbm > 0 ? c.n_cta_hbm : std::max(1, (pair ? sms / 2 : sms) - n_host);
     n_hbm = (int)std::max<long long>(n_hbm, ceil_div(M - h, cap));
     n_hbm = (int)std::min<long long>(n_hbm, M - h);
   }
@@ -1361,6 +1398,13 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   p.evict_first = c.l2_policy == 0;
   if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
+  if (pair) {  // CTA pairs: consecutive (even, odd) CTAs, one 2-CTA cluster each when W is multicast
+    if (path != 3) return fail(DAK_EUNSUPPORTED, "dak_linear: N > 512 needs the tcgen05 path");
+    n_host *= 2;
+    n_hbm *= 2;
+    p.pair = 1;
+    p.wmc = c.cluster == 2 ? 1 : 0;
+  }
   p.n_host = n_host; p.n_hbm = n_hbm;
   p.wm = wm; p.wk = wk;
   p.rgran = rg;
@@ -1591,11 +1635,15 @@ static dak_status launch_umma_t(const Plan& pl, cudaStream_t stream, int pdl) {
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // W multicast pairs: one 2-CTA cluster per pair
+  attr[1].val.clusterDim.x = pl.p.pair && pl.p.wmc ? 2 : 1;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pl.p));
   return DAK_OK;
 }
