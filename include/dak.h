@@ -158,6 +158,9 @@ typedef struct {
   int32_t cluster;            /* dak_linear: CTAs per thread-block cluster sharing ONE fetch of */
                               /* each x chunk by TMA multicast (P:L555-571 applied to the        */
                               /* operand every CTA reads); 0/1 off, 2 or 4. Same outputs bitwise */
+                              /* N > 512 (tcgen05 groups of ceil(N/512) CTAs over the same rows): */
+                              /* >= 2 makes each group one cluster whose rank 0 multicasts every  */
+                              /* weight tile to the group: one HBM / link fetch per tile (Table 1)*/
   int32_t reserved;
 } dak_launch_cfg;
 
@@ -166,7 +169,7 @@ typedef struct {
   const void* w_hbm;    /* DAK-KC packed rows [h,M)   (device; may be NULL when h == M)       */
   int64_t M, K, h;      /* 0 <= h <= M                                                         */
   int32_t kc;           /* KC used to pack both tiers                                          */
-  int32_t N;            /* batch columns, 1..64 (1..512 on the tcgen05 path: kc == 64; N > 256 */
+  int32_t N;            /* batch columns, 1..64 (1..4096 on the tcgen05 path: kc == 64; N > 256 */
                         /* plain GEMM only: no ln_w / x_swiglu / stats_out)                  */
   const void* x;        /* [N, K] bf16 row-major, device                                       */
   void* y;              /* [N, M] bf16 row-major, device                                       */

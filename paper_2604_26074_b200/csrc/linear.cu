@@ -36,7 +36,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kThreads = 32 + kConsumers;  // warp 0 = producer
 constexpr int kMaxN = 64;     // mma.sync paths
-constexpr int kMaxNTc = 1024;  // tcgen05 path (one MMA covers N <= 256; two N halves up to 512; CTA pairs up to 1024)
+constexpr int kMaxNTc = 4096;  // tcgen05 path (one MMA covers N <= 256; two N halves up to 512; CTA groups of <= 8 up to 4096)
 constexpr int kRptMax = 16;   // FMA path: rows per thread
 constexpr int kMtwMax = 12;   // MMA path: m16 tiles per warp (n8 tiles <= 2; 8 for 4 n8 tiles, 4 for 8)
 constexpr int kMaxStages = 16;
@@ -66,8 +66,8 @@ struct __align__(64) Params {
   int red_slots;    // MMA path: WK -> every k-warp writes its own partial slot (one barrier), 1 -> serial
   int swiglu;       // x = [gate | up] ([N, 2K]); the operand is silu(gate) * up
   int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
-  int pair;         // tcgen05, N > 512: CTA pairs share rows, rank r computes columns [512 r, 512 r + 512)
-  int wmc;          // pair mode: the pair is a 2-CTA cluster and rank 0 multicasts each W tile to both
+  int pair;         // tcgen05, N > 512: groups of `pair` CTAs share rows, rank r computes columns [512 r, 512 r + 512)
+  int wmc;          // group mode: the group is one cluster and rank 0 multicasts each W tile to all of it
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
   int ksplit;       // tcgen05 split-K: K splits (1: off); CTA = (tier row block of 128, split)
@@ -744,7 +744,7 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
                : "memory");
 }
 // 1-D bulk copy delivered to the same SMEM offset of every CTA in ctamask (each CTA's own mbarrier
-// at that offset receives the complete_tx): one fetch of a weight tile for both CTAs of a pair
+// at that offset receives the complete_tx): one fetch of a weight tile for every CTA of a group
 __device__ __forceinline__ void bulk_g2s_mc_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask,
                                                  uint64_t pol) {
   asm volatile(
@@ -795,13 +795,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
     re = rb + 128 < R_tier ? rb + 128 : R_tier;
     kbeg = ks * p.k64_split;
     kend = kbeg + p.k64_split < kend ? kbeg + p.k64_split : kend;
-  } else if (N8 > 256 && p.pair) {  // CTA pairs: both ranks take the pair's rows
-    tier_rows(R_tier, (host ? cta : cta - p.n_host) >> 1, (host ? p.n_host : p.n_hbm) >> 1, p.rgran, &rb, &re);
+  } else if (N8 > 256 && p.pair > 1) {  // CTA groups: every rank takes the group's rows
+    tier_rows(R_tier, (host ? cta : cta - p.n_host) / p.pair, (host ? p.n_host : p.n_hbm) / p.pair, p.rgran, &rb, &re);
   } else {
     tier_rows(R_tier, host ? cta : cta - p.n_host, host ? p.n_host : p.n_hbm, p.rgran, &rb, &re);
   }
-  const int prank = (N8 > 256 && p.pair) ? (cta & 1) : 0;  // pair rank = cluster rank (pairs start even)
-  const bool wmc = N8 > 256 && p.pair && p.wmc;
+  const int G = (N8 > 256 && p.pair > 1) ? p.pair : 1;  // CTAs per group
+  const int prank = cta % G;  // group rank = cluster rank (groups start at multiples of G)
+  const bool wmc = G > 1 && p.wmc;
   const int R = (int)(re - rb);
   const long long row0 = host ? rb : p.h + rb;
   const char* wsrc = host ? p.w_host : p.w_hbm;
@@ -816,7 +817,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], wmc && prank == 0 ? 2 : 1);  // W multicast: rank 0 refills after BOTH consumed
+      mbar_init(&empty[s], wmc && prank == 0 ? G : 1);  // W multicast: rank 0 refills after ALL consumed
     }
     mbar_init(done, 1);
     for (int s = 0; s < kMaxStages; ++s) mbar_init(&xready[s], 3);  // three transform warps
@@ -851,12 +852,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       const uint64_t pol = policy_evict_first();
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
-      // W tile of a stage: own copy, or (pair + multicast) rank 0 fetches it once for both CTAs;
+      // W tile of a stage: own copy, or (group + multicast) rank 0 fetches it once for all G CTAs;
       // every CTA's full barrier expects the W bytes either way
       auto load_w = [&](int slot, int i) {
         if (!wmc) bulk_g2s_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot], pol);
         else if (prank == 0)
-          bulk_g2s_mc_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot], 3, pol);
+          bulk_g2s_mc_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot],
+                           (uint16_t)((1u << G) - 1u), pol);
       };
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);
@@ -916,7 +918,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
               umma_bf16(tmem + 256u, umma_desc_sw128(ws + k * 32), umma_desc_sw128(xs + 256 * 128 + k * 32), idesc,
                         (i | k) != 0);
           }
-          if (wmc && prank == 1) umma_commit_mc(&empty[s], 3);  // both CTAs' slot s: rank 0 refills W into both
+          if (wmc && prank > 0) umma_commit_mc(&empty[s], (uint16_t)(1u | (1u << prank)));  // own + rank 0's slot s
           else umma_commit(&empty[s]);  // the slot is free once these MMAs have read it
         }
         __syncwarp();
@@ -1039,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
         if (r < R) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
-            const int n = 512 * prank + c0 + e;  // pair rank 1 owns columns 512..
+            const int n = 512 * prank + c0 + e;  // group rank r owns columns 512 r ..
             if (n < N) {
               float o = acc[e] + bias;
               if (p.act == DAK_ACT_RELU) o = fmaxf(o, 0.f);
@@ -1244,8 +1246,10 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (N > kMaxNTc) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d", N, kMaxNTc);
   // n8 tiles (compiled: 1, 2, 4, 8 on every path; 16, 32 on the tcgen05 path)
   const int nt = N <= 8 ? 1 : (N <= 16 ? 2 : (N <= 32 ? 4 : (N <= 64 ? 8 : (N <= 128 ? 16 : (N <= 256 ? 32 : 64)))));
-  // N > 512: CTA pairs over the same rows (rank r: columns [512 r, 512 r + 512)); counts below are pairs
-  const bool pair = N > 512;
+  // N > 512: groups of G = ceil(N / 512) CTAs over the same rows (rank r: columns [512 r, 512 r + 512));
+  // CTA counts below are groups
+  const int G = N > 512 ? (N + 511) / 512 : 1;
+  const bool pair = G > 1;
   if (K % 64) return fail(DAK_EUNSUPPORTED, "dak_linear: K %% 64 != 0");
   if (kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
     return fail(DAK_EINVAL, "dak_linear: kc must be a power of two in [64, 2048] dividing K");
@@ -1266,7 +1270,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // default: tensor cores for every N -- mma.sync (path 2) up to N = 16; tcgen05 (path 3) beyond,
   // where mma.sync becomes issue-bound, when its operand constraints hold
   int path = c.force_path ? c.force_path : 2;
-  if (!c.force_path && N > 16 && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster 2 at N > 512: W multicast pairs
+  if (!c.force_path && N > 16 && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster at N > 512: W multicast groups
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
@@ -1299,7 +1303,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   int n_hbm = 0;
   if (h < M) {
-    n_hbm = c.n_cta_hbm > 0 ? c.n_cta_hbm : std::max(1, (pair ? sms / 2 : sms) - n_host);
+    n_hbm = c.n_cta_hbm > 0 ? c.n_cta_hbm : std::max(1, sms / G - n_host);
     n_hbm = (int)std::max<long long>(n_hbm, ceil_div(M - h, cap));
     n_hbm = (int)std::min<long long>(n_hbm, M - h);
   }
@@ -1398,12 +1402,12 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   p.evict_first = c.l2_policy == 0;
   if (p.ldy < M) return fail(DAK_EINVAL, "dak_linear: ldy < M");
-  if (pair) {  // CTA pairs: consecutive (even, odd) CTAs, one 2-CTA cluster each when W is multicast
+  if (pair) {  // groups of G consecutive CTAs, one G-CTA cluster each when W is multicast
     if (path != 3) return fail(DAK_EUNSUPPORTED, "dak_linear: N > 512 needs the tcgen05 path");
-    n_host *= 2;
-    n_hbm *= 2;
-    p.pair = 1;
-    p.wmc = c.cluster == 2 ? 1 : 0;
+    n_host *= G;
+    n_hbm *= G;
+    p.pair = G;
+    p.wmc = c.cluster >= 2 ? 1 : 0;  // cluster >= 2 at N > 512: W multicast across the group
   }
   p.n_host = n_host; p.n_hbm = n_hbm;
   p.wm = wm; p.wk = wk;
@@ -1638,8 +1642,8 @@ static dak_status launch_umma_t(const Plan& pl, cudaStream_t stream, int pdl) {
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  attr[1].id = cudaLaunchAttributeClusterDimension;  // W multicast pairs: one 2-CTA cluster per pair
-  attr[1].val.clusterDim.x = pl.p.pair && pl.p.wmc ? 2 : 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // W multicast groups: one G-CTA cluster per group
+  attr[1].val.clusterDim.x = pl.p.pair > 1 && pl.p.wmc ? pl.p.pair : 1;
   attr[1].val.clusterDim.y = 1;
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;

@@ -138,7 +138,7 @@ def test_cta_rows_match_oracle(D, M, h, nh, ng):
 
 
 def test_linear_arg_validation(D):
-    bad = [dict(M=0), dict(h=5000), dict(N=513), dict(K=100), dict(kc=96), dict(kc=8192)]
+    bad = [dict(M=0), dict(h=5000), dict(N=4097), dict(K=100), dict(kc=96), dict(kc=8192)]
     for b in bad:
         kw = dict(M=4096, K=4096, h=0, kc=64, N=1)
         kw.update(b)

@@ -279,19 +279,20 @@ def test_linear_tcgen05_wide_n(D, torch, M, K, N, h):
         assert np.array_equal(o, outs[0])
 
 
-@pytest.mark.parametrize("M,K,N,h", [(1024, 1024, 1024, 64), (700, 2048, 640, 0), (7168, 512, 1000, 256)])
+@pytest.mark.parametrize("M,K,N,h", [(1024, 1024, 1024, 64), (700, 2048, 640, 0), (7168, 512, 1000, 256),
+                                     (512, 512, 2048, 128), (300, 256, 4096, 0), (1000, 256, 3000, 504)])
 def test_linear_tcgen05_pairs_w_multicast(D, torch, M, K, N, h):
-    """N in (512, 1024]: CTA pairs share rows (rank r computes columns [512 r, 512 r + 512)). With
-    cluster = 2 each pair is a 2-CTA cluster and rank 0 fetches every weight tile ONCE for both
-    (bulk-copy multicast; a host tile crosses the link once); without it each CTA fetches
-    its own copy (read amplification x2, Table 1). Outputs vs the oracle, bitwise equal with and
+    """N in (512, 4096]: groups of G = ceil(N / 512) CTAs share rows (rank r computes columns
+    [512 r, 512 r + 512)). With cluster = 2 each group is a G-CTA cluster and rank 0 fetches every
+    weight tile ONCE for all of it (bulk-copy multicast; a host tile crosses the link
+    once); without it each CTA fetches its own copy (read amplification x G, Table 1). Outputs vs the oracle, bitwise equal with and
     without multicast, integer inputs bitwise exact."""
     W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(13, M + N), bias=True)
     ys = []
     for cl in (0, 2):
         y, sl, a = run_linear(D, torch, W, x, h, 64, bias=b, cluster=cl)
         q = D.linear_query(a)
-        assert q["path"] == 3 and q["grid"] % 2 == 0
+        assert q["path"] == 3 and q["grid"] % (-(-N // 512)) == 0
         ys.append(y)
     ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
     from tests.gpu_util import assert_close

@@ -7,9 +7,9 @@
        oldest KV chunks in {0, r*, 0.5}
   pf   direct split access vs the prefetch-to-HBM baseline (copy the host rows into HBM
        with the copy engine, then run the GEMV from HBM) on fc1 28672x7168 at N=8 over r
-  t1   Table 1 on B200: the 7168 x 7168 matrix at N in {256, 512, 1024}, host share r in
-       {0, 0.25, 0.5}; N = 1024 runs as CTA pairs with and without the weight-tile multicast
-       (without it every host tile crosses the link twice: read amplification x2)
+  t1   Table 1 (P:L537-554) on B200: the 7168 x 7168 matrix at N in {256 .. 4096}, host share r;
+       N > 512 runs as groups of N/512 CTAs with and without the weight-tile multicast (without it
+       every host tile crosses the link N/512 times: Table 1's read amplification)
 Prints one JSON line per point. B_g: MEASURED_PEAKS.json HBM copy; B_l: measured link 51.5 GB/s.
 """
 from __future__ import annotations
@@ -195,13 +195,13 @@ def pf():
 def t1():
     bg, bl = peaks()
     M = K = 7168
-    for N in (256, 512, 1024):
-        for r in (0.0, 0.25, 0.5):
+    for N in (256, 512, 1024, 2048, 4096):
+        for r in ((0.0, 0.25, 0.5) if N <= 1024 else (0.25,)):
             h = int(round(r * M / 128)) * 128
             for cl in ((0, 2) if N > 512 else (0,)):
                 res = time_cfg(M, K, N, h, 64, launches=8 if h else 32, reps=3, pdl=1, cluster=cl)
                 t = res["us"] * 1e-6
-                amp = 2 if (N > 512 and cl != 2) else 1  # host tiles fetched per pair
+                amp = -(-N // 512) if (N > 512 and cl != 2) else 1  # host fetches of a tile per CTA group
                 rr = h / M
                 print(json.dumps(dict(exp="t1", M=M, K=K, N=N, r=round(rr, 4), multicast=int(cl == 2) if N > 512 else None,
                                       us=round(res["us"], 1), alg_gbs=round(res["hbm_gbs"] + res["host_gbs"], 1),
