@@ -1337,7 +1337,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // splits are fixed by (M, K, SM count), never by the tier split h, keeping every row's summation order
   // independent of the tier split (bitwise r-invariance). Needs caller workspace for the partials.
   int ksplit = 1, k64_split = (int)(K / 64);
-  if (path == 3 && !wide && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
+  if (path == 3 && !pair && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
     // S from (M, K, SM count) only: as many splits as keep all items in ONE wave (even if h adds a
     // tile). Measured at the Llama TP8 b64 shapes (profiles/r01/splitk_sweep.txt): a second wave or
     // shorter splits cost more than the idle SMs of a partial wave.

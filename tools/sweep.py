@@ -199,7 +199,7 @@ def t1():
         for r in ((0.0, 0.25, 0.5) if N <= 1024 else (0.25,)):
             h = int(round(r * M / 128)) * 128
             for cl in ((0, 2) if N > 512 else (0,)):
-                res = time_cfg(M, K, N, h, 64, launches=8 if h else 32, reps=3, pdl=1, cluster=cl)
+                res = time_cfg(M, K, N, h, 64, launches=8 if h else 32, reps=3, pdl=1, cluster=cl, ws=True)
                 t = res["us"] * 1e-6
                 amp = -(-N // 512) if (N > 512 and cl != 2) else 1  # host fetches of a tile per CTA group
                 rr = h / M
