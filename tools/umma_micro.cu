@@ -28,7 +28,7 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t ph) {
 
 // mode bit0: commit after every stage (4 MMAs); bit1: wait for that commit before the next stage;
 // bit2: A operand from 2 different 16 KB buffers alternating (else the same)
-__global__ void __launch_bounds__(128, 1) k(int N, int chains, int stages, int mode, long long* out) {
+__global__ void __launch_bounds__(128, 1) k(int M, int N, int chains, int stages, int mode, long long* out) {
   extern __shared__ __align__(1024) unsigned char raw[];
   unsigned char* sm = raw + ((1024u - (su32(raw) & 1023u)) & 1023u);
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm);
@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(128, 1) k(int N, int chains, int stages, int m
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tslot;
   if (threadIdx.x == 0) {
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
     uint32_t ph = 0;
     long long t0 = clock64();
     for (int s = 0; s < stages; ++s) {
@@ -79,20 +79,21 @@ int main() {
   const int smem = 1024 + 2 * 16384 + 32768 + 1024;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int stages = 2000;
-  printf("grid N chains mode cycles_per_mma\n");
+  printf("grid M N chains mode cycles_per_mma\n");
   for (int grid : {1, 148})
-    for (int N : {8, 64, 128, 256})
-      for (int chains : {1, 4})
-        for (int mode : {0, 1, 3, 5}) {
-          if (chains * N > 512) continue;
-          k<<<grid, 128, smem>>>(N, chains, stages, mode, d);
-          cudaError_t e = cudaDeviceSynchronize();
-          if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-          long long h[148];
-          cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
-          long long mx = 0;
-          for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
-          printf("%d %d %d %d %.1f\n", grid, N, chains, mode, (double)mx / (stages * 4));
-        }
+    for (int M : {64, 128})
+      for (int N : {8, 64, 128, 256})
+        for (int chains : {1, 4})
+          for (int mode : {0, 1}) {
+            if (chains * N > 512) continue;
+            k<<<grid, 128, smem>>>(M, N, chains, stages, mode, d);
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+            long long h[148];
+            cudaMemcpy(h, d, grid * 8, cudaMemcpyDeviceToHost);
+            long long mx = 0;
+            for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+            printf("%d %d %d %d %d %.1f\n", grid, M, N, chains, mode, (double)mx / (stages * 4));
+          }
   return 0;
 }
