@@ -68,6 +68,8 @@ struct __align__(64) Params {
   int mc;           // cluster size sharing one multicast fetch of each x chunk (1: off)
   int pair;         // tcgen05, N > 512: groups of `pair` CTAs share rows, rank r computes columns [512 r, 512 r + 512)
   int wmc;          // group mode: the group is one cluster and rank 0 multicasts each W tile to all of it
+  int swap;         // tcgen05 swapped operands (umma_swap_kernel): batch = MMA M, weight rows = MMA N
+  int kblock;       // split-K item rows (128, or 256 when swapped)
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
   int ksplit;       // tcgen05 split-K: K splits (1: off); CTA = (tier row block of 128, split)
@@ -1090,6 +1092,156 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   }
 }
 
+#if DAK_LINEAR_PART == 5
+// Swapped-operand tcgen05 split GEMM for decode batches (N <= 128), split K: the batch is the MMA's
+// M side (x box of 128 rows, TMA zero-fills rows >= N) and the weight rows are its N side (up to 256
+// per instruction). A kind::f16 MMA costs ~100 cycles for any N <= 128 and 128 at N = 256
+// (profiles/r01/umma_micro.txt), so 256 weight rows per instruction move twice the weight bytes per
+// MMA of the M = 128 weight-tile form. CTA = (block of kblock <= 256 rows of one tier, K split);
+// D[batch row][weight row] in TMEM, epilogue warp q reads lanes 32q.. (batch rows) and writes the
+// fp32 partial part[s][n][m] (8 consecutive m per load). Summation order of a row: fixed by the
+// split (S from M, K only) -- independent of the tier split (bitwise r-invariant).
+__global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  uint64_t* done = empty + kMaxStages;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
+  unsigned char* wring = smem + 1024;
+  unsigned char* xring = smem + p.off_x;
+  const int cta = blockIdx.x;
+  const bool host = cta < p.n_host;
+  const long long R_tier = host ? p.h : p.M - p.h;
+  const int j = host ? cta : cta - p.n_host;
+  const int ks = j % p.ksplit;
+  const long long rb = (long long)(j / p.ksplit) * p.kblock;
+  const long long re = rb + p.kblock < R_tier ? rb + p.kblock : R_tier;
+  const int kbeg = ks * p.k64_split;
+  const int kend = min(kbeg + p.k64_split, (int)(p.K / 64));
+  const int R = (int)(re - rb);
+  const long long row0 = host ? rb : p.h + rb;
+  const char* wsrc = host ? p.w_host : p.w_hbm;
+  const int slots = host ? p.window : p.stages;
+  const int nchunks = kend - kbeg;
+  const int N = p.N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t tcols = p.tmem_cols;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1 && R > 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(tcols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (threadIdx.x == 0) tstamp(p.trace, 0);
+  grid_dep_launch();
+  if (R <= 0 || nchunks <= 0) return;
+  const uint32_t tmem = *tslot;
+  const uint32_t w_bytes = (uint32_t)R * 128;
+  const uint32_t x_tx = (uint32_t)p.x_stage_bytes;
+  const long long chunk_stride = R_tier * 128;
+  const int wstage = p.w_stage_bytes;
+  if (warp == 0) {
+    if (lane == 0) {  // producer: W span + x box per 64-column stage
+      const int pro = min(slots, nchunks);
+      const char* src = wsrc + rb * 128 + (long long)kbeg * chunk_stride;
+      const uint64_t pol = policy_evict_first();
+      const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      for (int i = 0; i < pro; ++i) {
+        mbar_expect_tx(&full[i], w_bytes + x_tx);
+        bulk_g2s_hint(wring + (size_t)i * wstage, src + (long long)i * chunk_stride, w_bytes, &full[i], pol);
+      }
+      grid_dep_wait();
+      tstamp(p.trace, 1);
+      for (int i = 0; i < pro; ++i) tma_3d(xring + (size_t)i * p.x_stage_bytes, xmap, 0, 0, kbeg + i, &full[i]);
+      int s = pro == slots ? 0 : pro;
+      uint32_t ph = pro == slots ? 1u : 0u;
+      for (int i = pro; i < nchunks; ++i) {
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], w_bytes + x_tx);
+        bulk_g2s_hint(wring + (size_t)s * wstage, src + (long long)i * chunk_stride, w_bytes, &full[s], pol);
+        tma_3d(xring + (size_t)s * p.x_stage_bytes, xmap, 0, 0, kbeg + i, &full[s]);
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {  // MMA issuer: D[128 batch rows][RN weight rows] += x . W^T
+    const int RN = (R + 15) & ~15;  // M = 128 needs N % 16 == 0 (rows past R: ignored columns)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(RN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t wr = su32(wring), xr = su32(xring);
+    uint32_t leader;
+    asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < nchunks; ++i) {
+      mbar_wait(&full[s], ph);
+      tc_fence_after();
+      if (leader) {
+        const uint32_t ws = wr + (uint32_t)s * wstage, xs = xr + (uint32_t)s * p.x_stage_bytes;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16(tmem, umma_desc_sw128(xs + k * 32), umma_desc_sw128(ws + k * 32), idesc, (i | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      __syncwarp();
+      if (++s == slots) { s = 0; ph ^= 1u; }
+    }
+    if (leader) umma_commit(done);
+    __syncwarp();
+  } else if (warp >= 4 && warp < 8) {  // epilogue: warp q <-> TMEM lanes 32q.. = batch rows
+    if (threadIdx.x == 128) {
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(su32(done)), "r"(0u)
+            : "memory");
+        if (!ok) __nanosleep(256);
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    tc_fence_after();
+    grid_dep_wait();  // the partial buffer may still be read by the previous kernel's consumer
+    const int q = warp & 3;
+    const int n = 32 * q + lane;
+    float* dst = p.part + ((size_t)ks * N + n) * p.M + row0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < R; c0 += 8) {
+      uint32_t v[8];
+      tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (n < N) {
+        if (c0 + 8 <= R) {
+          float4* d4 = reinterpret_cast<float4*>(dst + c0);
+          d4[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
+          d4[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]), __uint_as_float(v[7]));
+        } else {
+          for (int e = 0; e < R - c0; ++e) dst[c0 + e] = __uint_as_float(v[e]);
+        }
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (threadIdx.x == 32 && p.trace) tstamp(p.trace, 3);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tcols) : "memory");
+  }
+}
+#endif
+
 #if DAK_LINEAR_PART == 0
 // y[n, m] = act(sum_s part[s][n][m] + bias[m]) + residual[n, m]: the fixed-order split-K combine.
 // Grid (x: column groups, y: row n); vec = 4 columns per thread (float4 partial loads, 8-byte
@@ -1273,6 +1425,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (!c.force_path && N > 16 && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster at N > 512: W multicast groups
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
+  const bool force_swap = path == 4;  // force_path 4: tcgen05 with swapped operands (split-K decode form)
+  if (force_swap) path = 3;
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
   if (path != 3 && N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d needs the tcgen05 path (kc = 64)", N, kMaxN);
   if (path == 3) {  // tcgen05: canonical SWIZZLE_128B K-major operands need KC = 64; plain GEMV only
@@ -1336,7 +1490,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // the auto partition leaves < 128 rows per CTA, CTAs take (128-row block, K split) items instead;
   // splits are fixed by (M, K, SM count), never by the tier split h, keeping every row's summation order
   // independent of the tier split (bitwise r-invariance). Needs caller workspace for the partials.
-  int ksplit = 1, k64_split = (int)(K / 64);
+  int ksplit = 1, k64_split = (int)(K / 64), swap = 0, kblock = 128;
   if (path == 3 && !pair && !a->stats_out && !a->ln_w && !a->x_swiglu && c.n_cta_hbm <= 0 && a->workspace) {
     // S from (M, K, SM count) only: as many splits as keep all items in ONE wave (even if h adds a
     // tile). Measured at the Llama TP8 b64 shapes (profiles/r01/splitk_sweep.txt): a second wave or
@@ -1354,10 +1508,16 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       n_host = (int)(ceil_div(h, 128) * S);
       n_hbm = (int)(ceil_div(M - h, 128) * S);
     }
+    // swapped operands (N <= 128, same items): the batch is the MMA's M = 128 side, the item's 128
+    // weight rows its N side (umma_swap_kernel). Measured 5-12% faster than the weight-rows-as-M
+    // form at the Llama TP8 b64 shapes; 256-row items (one instruction per 256 rows) were slower
+    // (4 deeper stages instead of 6: profiles/r01/splitk_sweep.txt)
+    if (ksplit > 1 && N <= 128 && M % 4 == 0 && (force_swap || !c.force_path)) swap = 1;
   }
-  const long long rmax_host = ksplit > 1 ? std::min<long long>(h, 128)
+  if (force_swap && !swap) return fail(DAK_EUNSUPPORTED, "dak_linear: swapped tcgen05 form needs N <= 128, M %% 4 == 0 and a split-K workspace");
+  const long long rmax_host = ksplit > 1 ? std::min<long long>(h, kblock)
                                          : (n_host ? ceil_div(ceil_div(h, rg), n_host) * rg : 0);
-  const long long rmax_hbm = ksplit > 1 ? std::min<long long>(M - h, 128)
+  const long long rmax_hbm = ksplit > 1 ? std::min<long long>(M - h, kblock)
                                         : (n_hbm ? ceil_div(ceil_div(M - h, rg), n_hbm) * rg : 0);
   const long long rmax = std::max(rmax_host, rmax_hbm);
   if (rmax > cap) return fail(DAK_EUNSUPPORTED, "dak_linear: %lld rows per CTA exceed the path capacity %lld (use a smaller kc)", rmax, cap);
@@ -1371,7 +1531,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     rows_alloc = ceil_div(rmax, 16) * 16;
   } else if (path == 3) {
     bucket = 1;
-    rows_alloc = ceil_div(rmax, 8) * 8;
+    rows_alloc = swap ? ceil_div(rmax, 16) * 16 : ceil_div(rmax, 8) * 8;  // swapped: MMA N % 16 == 0
   } else {
     // warps split K first (the split depends on KC only, so the summation order of a row does
     // not depend on how many rows its CTA owns: bitwise r-invariance); leftover warps split M
@@ -1423,11 +1583,14 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       p.part = (float*)a->workspace;
     }
     p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+    if (swap) p.tmem_cols = kblock;  // D[128 batch rows][kblock weight rows]
+    p.swap = swap;
+    p.kblock = kblock;
   }
   p.mc = mc;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
-  p.n8 = n8;
-  p.x_stage_bytes = (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
+  p.n8 = swap ? 128 : n8;  // swapped: the batch is the MMA's M = 128 side (TMA zero-fills rows >= N)
+  p.x_stage_bytes = swap ? 128 * 128 : (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
   p.swiglu = a->x_swiglu ? 1 : 0;
   int ln_bytes = 0;
   if (a->ln_w) {
@@ -1467,7 +1630,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // slot's end: that over-read stays inside the region.
   p.w_stage_host = p.w_stage_bytes;
   p.stages_host = stages;
-  if (n_host > 0) {
+  if (n_host > 0 && !swap) {  // (the swapped kernel uses one slot size for both tiers)
     const long long rh = std::min<long long>(rows_alloc, ceil_div(rmax_host, 16) * 16);
     const long long ws_h = rh * kc * 2;
     const long long over = (rows_alloc - rh) * kc * 2;
@@ -1607,6 +1770,7 @@ dak_status launch_part_nt2(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_swap(const Plan& pl, cudaStream_t s, int pdl);
 #if DAK_LINEAR_PART == 0
 dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl) {
   switch (pl.nn) {
@@ -1657,6 +1821,25 @@ static dak_status launch_umma_xf(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.p.swiglu) return launch_umma_t<NT, 2>(pl, s, pdl);
   return launch_umma_t<NT, 0>(pl, s, pdl);
 }
+dak_status launch_part_swap(const Plan& pl, cudaStream_t stream, int pdl) {
+  static int smem_set = 0;
+  if (!smem_set) {
+    DAK_CUDA_TRY(cudaFuncSetAttribute(umma_swap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    smem_set = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, umma_swap_kernel, pl.p));
+  return DAK_OK;
+}
 dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
   switch (pl.nn) {
     case 2: return launch_umma_xf<2>(pl, s, pdl);
@@ -1674,7 +1857,7 @@ dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
 static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
   if (pl.path == 1) return launch_part_fma(pl, s, pdl);
-  if (pl.path == 3) return launch_part_umma(pl, s, pdl);
+  if (pl.path == 3) return pl.p.swap ? launch_part_swap(pl, s, pdl) : launch_part_umma(pl, s, pdl);
   switch (pl.nn) {
     case 1: return launch_part_nt1(pl, s, pdl);
     case 2: return launch_part_nt2(pl, s, pdl);

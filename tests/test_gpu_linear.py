@@ -338,10 +338,14 @@ def test_linear_tcgen05_operand_transforms(D, torch, xf, N):
     assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
 
 
-@pytest.mark.parametrize("M,K,N,h", [(1280, 8192, 64, 0), (1024, 8192, 48, 32), (7168, 8192, 64, 48), (300, 2048, 16, 0)])
-def test_linear_tcgen05_split_k(D, torch, M, K, N, h):
-    """tcgen05 with few rows per CTA: (128-row block, K split) items, fp32 partials in the caller's
-    workspace, fixed-order combine kernel (bias / residual applied there), against the oracle."""
+@pytest.mark.parametrize("fp", [3, 4])
+@pytest.mark.parametrize("M,K,N,h", [(1280, 8192, 64, 0), (1024, 8192, 48, 32), (7168, 8192, 64, 48), (300, 2048, 16, 0),
+                                     (8192, 1024, 64, 256), (8192, 3584, 64, 0), (7168, 1024, 128, 8)])
+def test_linear_tcgen05_split_k(D, torch, M, K, N, h, fp):
+    """tcgen05 with few rows per CTA: (row block, K split) items, fp32 partials in the caller's
+    workspace, fixed-order combine kernel (bias / residual applied there), against the oracle.
+    force_path 3: weight rows as the MMA's M (128-row blocks); 4: swapped operands (batch = M,
+    128 or 256 weight rows = N per instruction, umma_swap_kernel)."""
     from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
     W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, M + N), bias=True)
     g = synth.rng(M + N)
@@ -349,7 +353,7 @@ def test_linear_tcgen05_split_k(D, torch, M, K, N, h):
     sl = SplitLinear(D, W, h, 64)
     xd, bd, rd = to_dev(x), to_dev(b), to_dev(res)
     y = torch.empty((N, M), dtype=torch.int16, device="cuda")
-    a = sl.args(xd, y, N, bias=bd, residual=rd, force_path=3)
+    a = sl.args(xd, y, N, bias=bd, residual=rd, force_path=fp)
     ws = D.linear_workspace_size(a)
     assert ws > 0
     wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
@@ -360,7 +364,8 @@ def test_linear_tcgen05_split_k(D, torch, M, K, N, h):
     assert_close(Kx.bf16_to_f64(from_dev(y)), ref)
 
 
-def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch):
+@pytest.mark.parametrize("fp", [3, 4])
+def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch, fp):
     from tests.gpu_util import SplitLinear, to_dev, from_dev
     M, K, N = 1280, 4096, 32
     W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(12, 3), kind="int")
@@ -369,7 +374,7 @@ def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch):
         sl = SplitLinear(D, W, h, 64)
         xd = to_dev(x)
         y = torch.empty((N, M), dtype=torch.int16, device="cuda")
-        a = sl.args(xd, y, N, force_path=3)
+        a = sl.args(xd, y, N, force_path=fp)
         ws = D.linear_workspace_size(a)
         assert ws > 0
         wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
