@@ -2,8 +2,8 @@
 # Round profiling recipe (run on the GPU box from the repo root, one GPU):
 #   bench line (+ cpu_baseline), reference arm, ncu launch list of ONE timed decode step with
 #   per-launch DRAM bytes, and a --set full capture of the dominant kernels (q and fc1 linears).
-# Kernel launches per step (per-op path, fused pre-norm, fused QKV): 1 embed + 48 x (qkv, append,
-# attention, o, fc1, fc2) + head = 290. The bench runs: eager warm step, 3 warm-up replays, K timed replays,
+# Kernel launches per step (per-op path, fused pre-norm, fused QKV, KV append fused into attention): 1 embed + 48 x (qkv,
+# attention, o, fc1, fc2) + head = 242. The bench runs: eager warm step, 3 warm-up replays, K timed replays,
 # K e2e replays, then the per-launch roofline loop -> skip 4 steps to land on the first timed one.
 set -u
 R=${1:-r01}
@@ -11,7 +11,7 @@ OUT=gpurun_out
 mkdir -p $OUT
 python bench.py --steps 20 --warmup 3 > $OUT/bench_$R.json 2> $OUT/bench_$R.err; echo "bench rc $?"
 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref_$R.json 2> $OUT/bench_ref_$R.err; echo "ref rc $?"
-PER=$(python -c "from paper_2604_26074_b200.engine import OPT_30B; print(1 + 6 * OPT_30B.n_layers + 1)")
+PER=$(python -c "from paper_2604_26074_b200.engine import OPT_30B; print(1 + 5 * OPT_30B.n_layers + 1)")
 LIN=$(python -c "from paper_2604_26074_b200.engine import OPT_30B; print(4 * OPT_30B.n_layers + 1)")
 KF='regex:split_linear|split_attention|combine_kernel|embed_kernel|append_kernel|layernorm_kernel'
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
