@@ -256,6 +256,63 @@ __global__ void __launch_bounds__(kLnThreads) embed_kernel(const int* __restrict
   tstamp(tr, 3);
 }
 
+// Vectorised embed_kernel (hidden % 8 == 0, 16-byte aligned tables, hidden <= 256 * 8 * kLnVec):
+// each thread gathers its 16-byte chunks of the token and position rows at once (one memory round
+// trip instead of one per scalar), same per-element arithmetic; statistics two-pass from registers.
+__global__ void __launch_bounds__(kLnThreads) embed_vec_kernel(const int* __restrict__ tokens, const int* __restrict__ positions,
+                                 const __nv_bfloat16* __restrict__ tok, const __nv_bfloat16* __restrict__ pos, int hidden,
+                                 int pos_offset, __nv_bfloat16* __restrict__ x, float4* __restrict__ stats,
+                                 unsigned long long* tr) {
+  __shared__ float red[kLnThreads / 32];
+  tstamp(tr, 0);
+  grid_dep_launch();
+  grid_dep_wait();
+  const int b = blockIdx.x;
+  const long long t = tokens[b];
+  const long long p = positions ? (long long)positions[b] + pos_offset : -1;
+  const int nc = hidden / 8;
+  const uint4* tr4 = reinterpret_cast<const uint4*>(tok + t * hidden);
+  const uint4* pr4 = (pos && p >= 0) ? reinterpret_cast<const uint4*>(pos + p * hidden) : nullptr;
+  uint4* xr = reinterpret_cast<uint4*>(x + (long long)b * hidden);
+  float f[kLnVec][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < kLnVec; ++i) {
+    const int c = threadIdx.x + i * kLnThreads;
+    if (c < nc) {
+      float a[8];
+      bf16x8_to_f32(tr4[c], a);
+      if (pr4) {
+        float q[8];
+        bf16x8_to_f32(pr4[c], q);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) a[j] += q[j];
+      }
+      const uint4 o = f32_to_bf16x8(a);
+      xr[c] = o;
+      bf16x8_to_f32(o, f[i]);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s += f[i][j];
+    }
+  }
+  if (stats) {
+    const float mean = block_sum(s, red) / (float)hidden;
+    float m2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kLnVec; ++i)
+      if (threadIdx.x + i * kLnThreads < nc) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float d = f[i][j] - mean;
+          m2 += d * d;
+        }
+      }
+    m2 = block_sum(m2, red);
+    if (threadIdx.x == 0) stats[b] = make_float4((float)hidden, mean, m2, 0.f);
+  }
+  tstamp(tr, 3);
+}
+
 // stats[r] = (cols, mean, M2) of row r of x (bf16, row stride ld): the producer side of a fused pre-norm
 __global__ void __launch_bounds__(kLnThreads) row_stats_kernel(const __nv_bfloat16* __restrict__ x, long long ld, int cols,
                                                               float4* __restrict__ stats) {
@@ -525,7 +582,10 @@ dak_status dak_embed(const int32_t* tokens, const int32_t* positions, const void
   float4* sp = (float4*)stats_out;
   unsigned long long* tr = trace_slot(DAK_KIND_EMBED, B, hidden, B);
   void* args[] = {&tp, &pp, &te, &pe, &h, &off, &xp, &sp, &tr};
-  return layer::launch_pdl((const void*)layer::embed_kernel, dim3(B), dim3(layer::kLnThreads), args, (cudaStream_t)stream, pdl);
+  const bool vec = hidden % 8 == 0 && hidden <= layer::kLnThreads * 8 * layer::kLnVec && aligned16(tok_emb) &&
+                   (!pos_emb || aligned16(pos_emb)) && aligned16(x);
+  return layer::launch_pdl(vec ? (const void*)layer::embed_vec_kernel : (const void*)layer::embed_kernel, dim3(B),
+                           dim3(layer::kLnThreads), args, (cudaStream_t)stream, pdl);
 }
 
 dak_status dak_row_stats(const void* x, int32_t rows, int32_t cols, int64_t ld, float* stats_out, int32_t pdl,
