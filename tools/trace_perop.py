@@ -25,7 +25,11 @@ def main():
     args = [a for i, a in enumerate(sys.argv[1:], 1) if not a.startswith("--") and sys.argv[i - 1] != "--context"]
     layers = int(args[0]) if args else 8
     batch = int(args[1]) if len(args) > 1 else 8
-    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    # the bench's planner rates (the C5 sweep's sustained HBM / link rates), so the plan matches bench.py
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    ph, pl, _ = bench.planner_rates(6555.5, 51.5)
+    hw = HW(hbm_bps=ph * 1e9, link_bps=pl * 1e9)
     if "--llama" in sys.argv:
         from dataclasses import replace
         from paper_2604_26074_b200.llama import DakLlama, LLAMA3_70B
