@@ -148,7 +148,10 @@ typedef struct {
   int32_t n_cta_host;         /* CTAs that read the host tier (0: auto from calibration)       */
   int32_t n_cta_hbm;          /* CTAs that read HBM (0: SMs - n_cta_host)                      */
   int32_t window;             /* congestion window W: max in-flight host stages per CTA*/
-  int32_t stages;             /* SMEM ring depth for HBM CTAs (0: fill shared memory)          */
+                              /* (dak_attention: per warp; 0 with congestion_control: 512 KB of */
+                              /* host tiles in flight over all host CTAs, >= 2 tiles per warp)  */
+  int32_t stages;             /* SMEM ring depth for HBM CTAs (0: fill shared memory; attention: */
+                              /* cap on ring slots per warp)                                     */
   int32_t congestion_control; /* 1: cap host CTAs / window as calibrated          */
   int32_t pdl;                /* 1: programmatic dependent launch (weights stream before the   */
                               /*    previous kernel finishes; x/residual read after it)        */
