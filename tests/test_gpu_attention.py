@@ -75,11 +75,14 @@ def test_attention_r_invariance_bitwise(D, torch):
     assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
 
 
-@pytest.mark.parametrize("nh,win", [(1, 1), (2, 2), (3, 4)])
-def test_attention_launch_config_invariance(D, torch, nh, win):
-    """Congestion-control knobs (host CTAs, window) never change results (bitwise)."""
+@pytest.mark.parametrize("nh,win,st,cc", [(1, 1, 0, 1), (2, 2, 0, 1), (3, 4, 0, 1), (2, 0, 1, 1), (2, 0, 3, 0),
+                                         (16, 0, 0, 1), (1, 0, 16, 0)])
+def test_attention_launch_config_invariance(D, torch, nh, win, st, cc):
+    """Congestion-control / ring knobs (host CTAs, window, ring-slot cap per warp, congestion cap)
+    never change results (bitwise): every unit's reduction order is fixed by the chunking."""
     base, _, _ = run_attn(D, torch, [900, 40], 2, 8, 64, 2, 0.5, seed=55)
-    got, _, _ = run_attn(D, torch, [900, 40], 2, 8, 64, 2, 0.5, seed=55, n_cta_host=nh, window=win, n_cta_hbm=37)
+    got, _, _ = run_attn(D, torch, [900, 40], 2, 8, 64, 2, 0.5, seed=55, n_cta_host=nh, window=win, n_cta_hbm=37,
+                         stages=st, congestion_control=cc)
     assert np.array_equal(base, got)
 
 
