@@ -1135,7 +1135,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 1 && R > 0) {
+  if (warp == 1 && R > 0 && nchunks > 0) {  // (the same condition as the early return below: no leak)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(tcols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
