@@ -1177,7 +1177,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     }
   } else if (warp == 1) {  // MMA issuer: D[128 batch rows][RN weight rows] += x . W^T
     const int RN = (R + 15) & ~15;  // M = 128 needs N % 16 == 0 (rows past R: ignored columns)
-    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(RN >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t MM = p.swap == 2 ? 64u : 128u;  // batch <= 64: M = 64 (x box of 64 rows)
+    const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(RN >> 3) << 17) | ((MM >> 4) << 24);
     const uint32_t wr = su32(wring), xr = su32(xring);
     uint32_t leader;
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
@@ -1214,7 +1215,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     tc_fence_after();
     grid_dep_wait();  // the partial buffer may still be read by the previous kernel's consumer
     const int q = warp & 3;
-    const int n = 32 * q + lane;
+    // M = 128: TMEM lane 32q + l holds batch row 32q + l. M = 64 (measured, tools/umma_m64_layout.cu):
+    // batch row r sits in lane 32 (r / 16) + r % 16, i.e. lanes 0..15 of each warp quadrant
+    const int n = p.swap == 2 ? (lane < 16 ? 16 * q + lane : 1 << 30) : 32 * q + lane;
     float* dst = p.part + ((size_t)ks * N + n) * p.M + row0;
 #pragma unroll 1
     for (int c0 = 0; c0 < R; c0 += 8) {
@@ -1512,7 +1515,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     // weight rows its N side (umma_swap_kernel). Measured 5-12% faster than the weight-rows-as-M
     // form at the Llama TP8 b64 shapes; 256-row items (one instruction per 256 rows) were slower
     // (4 deeper stages instead of 6: profiles/r01/splitk_sweep.txt)
-    if (ksplit > 1 && N <= 128 && M % 4 == 0 && (force_swap || !c.force_path)) swap = 1;
+    if (ksplit > 1 && N <= 128 && M % 4 == 0 && (force_swap || !c.force_path)) swap = N <= 64 ? 2 : 1;  // 2: M = 64
   }
   if (force_swap && !swap) return fail(DAK_EUNSUPPORTED, "dak_linear: swapped tcgen05 form needs N <= 128, M %% 4 == 0 and a split-K workspace");
   const long long rmax_host = ksplit > 1 ? std::min<long long>(h, kblock)
@@ -1589,8 +1592,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   p.mc = mc;
   p.w_stage_bytes = (int)(rows_alloc * kc * 2);
-  p.n8 = swap ? 128 : n8;  // swapped: the batch is the MMA's M = 128 side (TMA zero-fills rows >= N)
-  p.x_stage_bytes = swap ? 128 * 128 : (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
+  p.n8 = swap ? (swap == 2 ? 64 : 128) : n8;  // swapped: the batch is the MMA's M side (TMA zero-fills rows >= N)
+  p.x_stage_bytes = swap ? p.n8 * 128 : (int)x_stage;  // [kc/64 atoms][n8 rows][64] (x2: gate, up), 128B-swizzled, 1 KB multiple
   p.swiglu = a->x_swiglu ? 1 : 0;
   int ln_bytes = 0;
   if (a->ln_w) {
