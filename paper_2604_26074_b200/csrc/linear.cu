@@ -1586,7 +1586,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       p.part = (float*)a->workspace;
     }
     p.tmem_cols = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
-    if (swap) p.tmem_cols = kblock;  // D[128 batch rows][kblock weight rows]
+    if (swap) p.tmem_cols = kblock <= 32 ? 32 : kblock <= 64 ? 64 : kblock <= 128 ? 128 : 256;  // D[batch][kblock rows], pow2
     p.swap = swap;
     p.kblock = kblock;
   }
