@@ -95,6 +95,57 @@ __global__ void __launch_bounds__(kThreads) residual_stats_kernel(const __nv_bfl
   if (threadIdx.x == 0) stats[blockIdx.x] = make_float4((float)cols, mean, m2, 0.f);
 }
 
+// Vectorised residual_stats_kernel (cols % 8 == 0, 16-byte aligned rows): chunks held in registers,
+// the same per-element arithmetic; statistics two-pass from registers (fixed order).
+__global__ void __launch_bounds__(kThreads) residual_stats_vec_kernel(const __nv_bfloat16* __restrict__ partial,
+                                                                      __nv_bfloat16* __restrict__ x, int cols,
+                                                                      float4* __restrict__ stats) {
+  __shared__ float red[kThreads / 32];
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int nc = cols / 8;
+  const long long base = (long long)blockIdx.x * nc;
+  uint4* xr = reinterpret_cast<uint4*>(x) + base;
+  const uint4* pr = reinterpret_cast<const uint4*>(partial) + base;
+  float f[8][8];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int c = threadIdx.x + i * kThreads;
+    if (c < nc) {
+      const uint4 a = xr[c], b = pr[c];
+      const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
+      const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&b);
+      uint4 o;
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 u = __bfloat1622float2(ah[j]), v = __bfloat1622float2(bh[j]);
+        oh[j] = __floats2bfloat162_rn(u.x + v.x, u.y + v.y);
+        const float2 r = __bfloat1622float2(oh[j]);
+        f[i][2 * j] = r.x;
+        f[i][2 * j + 1] = r.y;
+        s += r.x + r.y;
+      }
+      xr[c] = o;
+    }
+  }
+  if (!stats) return;
+  const float mean = block_sum(s, red) / (float)cols;
+  float m2 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (threadIdx.x + i * kThreads < nc) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float d = f[i][j] - mean;
+        m2 += d * d;
+      }
+    }
+  m2 = block_sum(m2, red);
+  if (threadIdx.x == 0) stats[blockIdx.x] = make_float4((float)cols, mean, m2, 0.f);
+}
+
 // x[r] += partial[r] (bf16 RNE), then y[r] = bf16(x[r] * rstd * w) with rstd = 1/sqrt(mean(x^2) + eps)
 // (RMSNorm of the new row: the same arithmetic as dak_rmsnorm, fused so the MLP pre-norm needs no
 // launch of its own). 8 columns per 16-byte chunk, chunks held in registers; y may alias partial
@@ -216,8 +267,9 @@ dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t ro
   cfg.stream = s;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_stats_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
-                                  (int)cols, (float4*)stats_out));
+  const bool vec = cols % 8 == 0 && cols <= tp::kThreads * 64 && aligned16(partial) && aligned16(x);
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, vec ? tp::residual_stats_vec_kernel : tp::residual_stats_kernel,
+                                  (const __nv_bfloat16*)partial, (__nv_bfloat16*)x, (int)cols, (float4*)stats_out));
   return DAK_OK;
 }
 

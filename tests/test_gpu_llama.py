@@ -200,3 +200,25 @@ def test_layernorm_vectorised_and_scalar(cols, bias):
                                         Kx.bf16_to_f64(b) if bias else np.zeros(cols), 1e-5))
     got = Kx.bf16_to_f64(from_dev(y))
     assert np.abs(got - ref).max() <= 2 ** -7 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("rows,cols", [(3, 8192), (2, 1000), (4, 520)])
+def test_allreduce_residual_stats_kernel(rows, cols):
+    """x += partial (bf16 RNE) and per-row (cols, mean, M2) of the new x (1-rank: no exchange) vs
+    the oracle (float64 statistics of the bf16 row); vectorised and scalar kernels alike."""
+    import torch
+    from paper_2604_26074_b200 import dak
+    from tests.gpu_util import to_dev, from_dev
+    g = synth.rng(303 + cols)
+    x = synth.normal_bf16(g, (rows, cols), 1.1)
+    pa = synth.normal_bf16(g, (rows, cols), 0.7)
+    xs = Kx.round_to_bf16(Kx.bf16_to_f64(x) + Kx.bf16_to_f64(pa))
+    xd, pd = to_dev(x), to_dev(pa)
+    st = torch.zeros((rows, 4), dtype=torch.float32, device="cuda")
+    dak.allreduce_residual(None, pd, xd, rows, cols, st)
+    torch.cuda.synchronize()
+    assert np.array_equal(Kx.bf16_to_f64(from_dev(xd)), xs)
+    s = st.cpu().numpy().astype(np.float64)
+    assert np.array_equal(s[:, 0], np.full(rows, cols))
+    mean, m2 = xs.mean(axis=1), ((xs - xs.mean(axis=1, keepdims=True)) ** 2).sum(axis=1)
+    assert np.allclose(s[:, 1], mean, atol=1e-5, rtol=1e-5) and np.allclose(s[:, 2], m2, rtol=1e-4)
