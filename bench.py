@@ -237,23 +237,38 @@ def make_llama(a, hw, world, rank, dak):
         sys.stdout.flush()
         os.dup2(saved, 1)
         os.close(saved)
-    from paper_2604_26074_b200 import tp
-    dm = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
-    d, H = cfg.head_dim, cfg.hidden
-    per_layer = (dm["n_heads"] + 2 * dm["n_kv"]) * d * H + H * dm["n_heads"] * d + 3 * dm["ffn"] * H
-    w_bytes = 2 * (layers * per_layer + dm["vocab"] * H)
-    kv_bytes = layers * 2 * (cfg.n_kv_heads // tp_size) * cfg.head_dim * 2 * batch * context
+    # a1: footprint of this rank's shard -> host bytes the HBM budget forces out, from the
+    # library's own op profile (dak_decode_ops C_i: linear weights + KV) and dak_global_offload_bytes
+    m = dak.model(dak.MODEL_LLAMA, layers, cfg.hidden, cfg.n_heads, cfg.n_kv_heads, cfg.head_dim, cfg.ffn, cfg.vocab,
+                  tp_size=tp_size)
+    ops = dak.decode_ops(m, batch, context, 16, 1024, hw.peak_flops, hw.peak_flops)
+    w_bytes = sum(o["total_bytes"] for o in ops if o["role"] != "attn")
+    kv_bytes = sum(o["total_bytes"] for o in ops if o["role"] == "attn")
     budget = int(168e9 * layers / cfg.__class__().n_layers)
-    y_req = max(0, w_bytes + kv_bytes - budget)
+    y_req, R = dak.global_offload_bytes(w_bytes, kv_bytes, budget)
     eng = DakLlama(cfg, batch, context, hw, tp_rank=rank, tp_size=tp_size, comm=comm, mode=dak.PLAN_EXACT,
                    y_req=y_req, pdl=not a.no_pdl, congestion_control=not a.no_cc, seed=1234 + rank)
     wl = dict(workload="llama3-70b-tp8-b%d-ctx%d" % (batch, context), model_shape="Llama-3-70B (TP%d shard)" % tp_size,
               batch=batch, context=context, layers=layers, layers_model=80,
               extrapolation="x%d per token step" % (80 // layers) if layers != 80 else None,
-              hbm_budget_bytes=budget, y_req_bytes=y_req, plan="EXACT (capacity-forced R=%.4f)" % (y_req / (w_bytes + kv_bytes)),
+              hbm_budget_bytes=budget, y_req_bytes=y_req, plan="EXACT (capacity-forced R=%.4f)" % R,
               tp="rank 0 of %d on one GPU (1-rank NCCL all-reduce)" % tp_size if world == 1 else "TP%d over NCCL" % world)
     eng.comm_handle = comm
     return eng, cfg, wl
+
+
+def spawn_ranks(n: int):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks (one process per GPU)
+    under torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stdout.flush()
+    r = subprocess.run(cmd)
+    sys.exit(r.returncode)
 
 
 def main():
@@ -265,8 +280,6 @@ def main():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--context", type=int, default=64)
     ap.add_argument("--no-pdl", action="store_true")
-    ap.add_argument("--persistent", action="store_true",
-                    help="one persistent launch per step (dak_step) instead of the per-op kernels (dak_layer)")
     ap.add_argument("--no-cc", action="store_true")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -285,6 +298,8 @@ def main():
                          "shard (rank 0 of 8 on one GPU, or the real ranks under torchrun), capacity-forced ratios")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(a.gpus)
     if a.impl == "reference":
         return run_reference(a)
 
@@ -305,17 +320,15 @@ def main():
         cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                     evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, fused_qkv=not a.persistent,
+                     evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
                      seed=1234 + rank)
         if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
             tot = sum(o["total_bytes"] for o in eng.plan_ops)
             eng.close()
             eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                          congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
-                         evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm, fused_qkv=not a.persistent,
+                         evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
                      seed=1234 + rank)
-    if a.persistent:
-        eng.enable_persistent_step()
     nb = eng.bytes_per_step()
     stream = torch.cuda.Stream()
     g = eng.capture(stream)
@@ -442,7 +455,7 @@ def main():
                             pdl=not a.no_pdl, congestion_control=not a.no_cc,
                             planner_rates_gbs=dict(hbm=round(hw.hbm_bps / 1e9, 1), link=round(hw.link_bps / 1e9, 2),
                                                    host_latency_us=a.plan_host_latency_us, source=plan_src),
-                            execution="persistent step (dak_step, 1 launch)" if a.persistent else "per-op kernels (dak_layer, PDL, CUDA graph)",
+                            execution="per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world)),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
                 **({"tokens_per_s_full_model_extrapolated": round(tok_s * cfg.n_layers / 80, 2)}

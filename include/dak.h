@@ -113,14 +113,99 @@ dak_status dak_plan_ratios(const dak_hw* hw, const dak_op* ops, int32_t n_ops, i
                            int32_t mode, dak_op_plan* out, double* objective_s);
 
 /* =============================================================================================
+ * 1b. Planner inputs and placement. Pure host functions.
+ * ============================================================================================= */
+
+/* a1 -- capacity -> global host budget (§3.2: "the offload ratio is decided by the memory
+ * footprint and the GPU capacity"; Fig. 8). footprint = weight_bytes + kv_bytes;
+ * *y_req_bytes = max(0, footprint - hbm_budget_bytes) (the bytes that must live on the host);
+ * *ratio (nullable) = y_req / footprint (R of P:L880), 0 for an empty footprint.
+ * Errors: DAK_EINVAL (NULL output, negative size); DAK_ECAPACITY (host_capacity_bytes >= 0 and the
+ * overflow exceeds it). host_capacity_bytes < 0: unlimited. */
+dak_status dak_global_offload_bytes(int64_t weight_bytes, int64_t kv_bytes, int64_t hbm_budget_bytes,
+                                    int64_t host_capacity_bytes, int64_t* y_req_bytes, double* ratio);
+
+#define DAK_MODEL_OPT 0   /* pre-LayerNorm, biases, ReLU MLP (OPT family, P:L690)            */
+#define DAK_MODEL_LLAMA 1 /* pre-RMSNorm, no biases, rotary, GQA, SwiGLU MLP (BASELINE C3)   */
+
+/* Decoder-only transformer shape. With tp_size > 1 the op list is ONE rank's Megatron shard:
+ * q / k / v / gate / up / LM head split by output rows, o / down by input columns (heads, kv heads,
+ * ffn and vocab must divide by tp_size). */
+typedef struct {
+  int32_t family;        /* DAK_MODEL_OPT | DAK_MODEL_LLAMA                                       */
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  int32_t tp_size;       /* 0 / 1: unsharded                                                      */
+  int32_t fused_qkv;     /* 1: one [q; k; v] op per layer (reading R18); 0: q, k, v (P:L981 fn)   */
+  int32_t fused_gate_up; /* Llama: 1: one [gate; up] op of 2 ffn rows; 0: gate, up                */
+  int32_t include_head;  /* 1: the LM head as the last op (OPT: the tied token embedding)         */
+} dak_model;
+
+#define DAK_ROLE_Q 0
+#define DAK_ROLE_K 1
+#define DAK_ROLE_V 2
+#define DAK_ROLE_QKV 3
+#define DAK_ROLE_O 4
+#define DAK_ROLE_UP 5        /* OPT fc1; Llama up                                                 */
+#define DAK_ROLE_DOWN 6      /* OPT fc2; Llama down                                               */
+#define DAK_ROLE_GATE 7
+#define DAK_ROLE_GATE_UP 8
+#define DAK_ROLE_ATTENTION 9
+#define DAK_ROLE_HEAD 10
+
+typedef struct {
+  int32_t layer;  /* -1: the LM head                                                             */
+  int32_t role;   /* DAK_ROLE_*                                                                   */
+  int64_t M, K;   /* linear: output rows, input columns of this shard; attention: B*context, d   */
+  double flops;   /* 2*B*M*K (linear); 4*B*context*(Hq d) (decode attention)     */
+} dak_op_desc;
+
+/* a2 -- the per-op profile of one decode step (§3.2, P:L422 footnote "C_i is the
+ * weight or KV size", P:L981 footnote "offloadable ops are the linear layers and attention";
+ * S:L135-143). Order: for each layer its linear ops in model order ([q k v | qkv], o, OPT: fc1 fc2 /
+ * Llama: [gate up | gate_up], down) then its attention op; the LM head last.
+ * Linear op: C = 2 M K bytes, units of unit_rows output rows (n = ceil(M / unit_rows), unit_bytes =
+ * 2 unit_rows K; reading R8), T = flops / peak_flops_linear.
+ * Attention op (the new token of each of `batch` requests over `context` cached tokens, this shard's
+ * kv heads): C = 2 (K, V) * Hkv d * 2 B * batch * context; units = split-KV chunks of chunk_tokens
+ * tokens of one request (all its kv heads): n = batch * ceil(context / chunk_tokens), unit_bytes =
+ * ceil(C / n) (reading R15); T = flops / peak_flops_attn.
+ * T values are IEEE double with the written operation order (bit-identical to the oracle).
+ * ops / desc (each nullable; both NULL = count query): caller arrays of `capacity` entries.
+ * *n_ops = number of ops. Errors: DAK_EINVAL (NULL model / n_ops, non-positive size or peak,
+ * n_heads % n_kv_heads, dims not divisible by tp_size, capacity too small). */
+dak_status dak_decode_ops(const dak_model* model, int32_t batch, int64_t context, int32_t unit_rows,
+                          int32_t chunk_tokens, double peak_flops_linear, double peak_flops_attn, dak_op* ops,
+                          dak_op_desc* desc, int32_t capacity, int32_t* n_ops);
+
+/* a4 (attention) -- KV placement of one layer ("tile row 0 resides in host memory",
+ * P:L631 KV partitioned for SplitK_FlashAttn; readings R7, R15 of DESIGN.md). Request b holds
+ * seq_lens[b] tokens in ceil(seq_lens[b] / page_size) filled pages; its block-table row has
+ * max_pages entries (pages past the filled ones take later decode tokens, in HBM). The op's
+ * host_units (planner units: split-KV chunks of chunk_pages pages) are the OLDEST chunks, taken
+ * chunk-major: chunk 0 of requests 0..B-1, then chunk 1, ... (chunks that exist only). Host pages
+ * get host-pool indices 0, 1, ... in (request, page) order, all other entries HBM-pool indices
+ * likewise; a host entry is index | 0x80000000 (dak_attention's tier bit).
+ * block_table: caller host array [B * max_pages] (int32). n_host_pages / n_hbm_pages (nullable):
+ * pool sizes in pages; host_tokens (nullable): tokens whose K/V rows live on the host.
+ * Errors: DAK_EINVAL (bad sizes, seq_len beyond max_pages pages, host_units > existing chunks). */
+dak_status dak_kv_place(int32_t B, const int32_t* seq_lens, int32_t page_size, int32_t max_pages, int32_t chunk_pages,
+                        int64_t host_units, int32_t* block_table, int32_t* n_host_pages, int32_t* n_hbm_pages,
+                        int64_t* host_tokens);
+
+/* =============================================================================================
  * 2. Host tier memory (SMs stream host data straight into SMEM; no HBM staging)
  * ============================================================================================= */
 
-/* Pinned, device-mapped, portable host allocation (optionally write-combined). *dev_ptr
- * receives the device alias (== host pointer under UVA). numa_node >= 0 binds the pages to that
- * node before pinning (-1: first-touch). */
+/* Pinned, device-mapped, portable host allocation. *dev_ptr receives the device alias (== host
+ * pointer under UVA). numa_node < 0: cudaHostAlloc (first-touch placement; write_combined allowed).
+ * numa_node >= 0: anonymous pages bound to that node (mbind MPOL_BIND), faulted in, then
+ * cudaHostRegister(Mapped | Portable): each GPU's host shard on the socket of its own link (SURVEY
+ * §8(e)). Errors: DAK_EINVAL (bad arguments, mbind refused: no such node), DAK_EUNSUPPORTED
+ * (write_combined with a node), DAK_ECUDA (CUDA / mmap failure). Free with dak_host_free. */
 dak_status dak_host_alloc(size_t bytes, int32_t write_combined, int32_t numa_node, void** host_ptr, void** dev_ptr);
 dak_status dak_host_free(void* host_ptr);
+/* NUMA node of the current device's PCIe attachment (sysfs; -1 when the platform reports none). */
+dak_status dak_device_numa_node(int32_t* node);
 
 /* =============================================================================================
  * 3. Split-source linear: y = act(x W^T + bias) + residual   (§3.1)
@@ -140,6 +225,10 @@ dak_status dak_pack_linear(const void* src, int64_t rows, int64_t K, int32_t kc,
 
 /* Preferred KC for an op (chunk width so one stage of the per-CTA row range is ~16-48 KB). */
 int32_t dak_linear_default_kc(int64_t M, int64_t K, int32_t n_ctas);
+/* KC for the mma.sync decode path given the rows one CTA owns: the widest of {256, 128, 64}
+ * dividing K whose stage (rows x KC) holds those rows within 48 KB and the path's accumulator
+ * capacity: rows <= 96 -> 256, rows <= 192 -> 128, else 64. */
+int32_t dak_linear_choose_kc(int64_t rows_per_cta, int64_t K);
 
 #define DAK_ACT_NONE 0
 #define DAK_ACT_RELU 1
@@ -223,6 +312,9 @@ typedef struct {
   int32_t cluster;                                    /* CTAs sharing one x fetch (multicast)  */
   int32_t ksplit;                                     /* K splits (tcgen05 path, caller workspace); */
                                                       /* > 1 adds one split-K reduce launch     */
+  int32_t host_gate;                                  /* split-K with congestion control: host   */
+                                                      /* item CTAs streaming at once (0: no cap) */
+  int32_t reserved;
 } dak_linear_launch_info;
 
 dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);
@@ -232,7 +324,9 @@ size_t dak_linear_workspace_size(const dak_linear_args* args);
 
 /* Row ownership of CTA `cta` (0 <= cta < grid): tier (0 HBM, 1 host) and [row_begin,row_end)
  * in global row numbering. Host CTAs split [0,h), HBM CTAs split [h,M), each into contiguous
- * ranges whose sizes differ by at most one row. Pure query. */
+ * ranges whose sizes differ by at most one row (8-row units on the tcgen05 path).
+ * Split-K plans (ksplit > 1): CTA j of a tier owns the K split j % ksplit of the 128-row block
+ * j / ksplit of that tier. N > 512 CTA groups: the group's rows. Pure query. */
 dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t* tier, int64_t* row_begin, int64_t* row_end);
 
 /* Enqueue the split GEMV / skinny GEMM. */
@@ -366,9 +460,6 @@ typedef struct {
   const void* bias;     /* nullable */
 } dak_weight;
 
-#define DAK_MODEL_OPT 0   /* pre-LayerNorm, biases, ReLU MLP (OPT family, P:L690)            */
-#define DAK_MODEL_LLAMA 1 /* pre-RMSNorm, no biases, rotary, GQA, SwiGLU MLP (BASELINE C3)   */
-
 typedef struct {
   int32_t model;                      /* DAK_MODEL_OPT | DAK_MODEL_LLAMA                      */
   int32_t B, hidden, n_heads, n_kv_heads, head_dim, ffn;
@@ -421,84 +512,6 @@ dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);
 dak_status dak_layer(const dak_layer_args* args, dak_stream_t stream);
 /* Number of statistics partials dak_layer writes to stats_out (the FC2 grid). Needs the device. */
 dak_status dak_layer_stats_parts(const dak_layer_args* args, int32_t* parts);
-
-/* =============================================================================================
- * 6. Persistent decode step: the whole op sequence of a decode step in ONE co-resident launch.
- *    Per CTA a producer warp streams every op's weight rows / KV pages back to back (the HBM and
- *    host streams never drain between ops); activations wait on gpu-scope completion counters.
- *    Same operators and numerics as sections 3-5.
- * ============================================================================================= */
-
-#define DAK_STEP_EMBED 0      /* y[b] = tok[tokens[b]] + pos[positions[b]+pos_offset]; cols = hidden */
-#define DAK_STEP_LAYERNORM 1  /* y = LN(x) with mean/var from stats_in (written by the op producing x) */
-#define DAK_STEP_LINEAR 2     /* split linear (section 3) + optional LN stats / fused KV append     */
-#define DAK_STEP_ATTENTION 3  /* split paged attention (section 4), units listed per tier           */
-#define DAK_STEP_COMBINE 4    /* merge split-KV partials of multi-chunk requests; cols = B          */
-
-typedef struct {
-  int32_t type;
-  int32_t dep;                 /* op index whose output this op reads (-1: none); must be < own index */
-  int32_t n_cta_host;          /* host-tier CTAs for this op (0: launch cfg / 1)                      */
-  int32_t act;                 /* LINEAR: DAK_ACT_*                                                   */
-  /* LINEAR (DAK-KC packed tiers; kc in {64,128,256}) */
-  const void* w_host;
-  const void* w_hbm;
-  int64_t M, K, h;
-  int32_t kc;
-  int32_t kv_kind;             /* fused KV append: 1 rows >= kv_row0 are K rows, 2 V rows,            */
-                               /* 3 [K rows; V rows] (fused QKV); 0 / kv_row0 < 0: off                */
-  const void* x;               /* [N, K] (LINEAR) / [N, cols] (LAYERNORM)                             */
-  void* y;                     /* [N, ldy] (LINEAR) / [N, cols] (LAYERNORM, EMBED)                    */
-  int64_t ldy;                 /* LINEAR: row stride of y and residual (0: M)                         */
-  const void* bias;
-  const void* residual;
-  float* stats_out;            /* [grid][N][2] per-CTA sum / sum of squares of y (for the next LN)    */
-  int64_t kv_row0;             /* LINEAR: first K row of a fused [q;k;v] output -> append k,v rows    */
-                               /* at positions into the pools below (-1: off)                         */
-  /* LAYERNORM / EMBED */
-  const float* stats_in;
-  const void* ln_w;
-  const void* ln_b;
-  float eps;
-  int32_t cols;
-  const int32_t* tokens;
-  const int32_t* positions;    /* also used by the fused KV append                                    */
-  const void* tok_emb;
-  const void* pos_emb;
-  int32_t pos_offset, reserved1;
-  /* ATTENTION / COMBINE / fused append */
-  const void* q;
-  int64_t q_stride;            /* elements between requests of q (0: Hq*d)                            */
-  void* out;                   /* [B, Hq*d] bf16                                                      */
-  void *k_hbm, *v_hbm, *k_host, *v_host;
-  const int32_t* block_table;
-  const int32_t* seq_lens;
-  int32_t Hq, Hkv, d, page_size, max_pages, chunk_pages;
-  float scale;
-  int32_t reserved2;
-  const int32_t* units_host;   /* (request*ceil(max_pages/chunk_pages) + chunk) pairs whose chunk      */
-  const int32_t* units_hbm;    /*   starts on a host / HBM page (device arrays)                       */
-  int32_t n_units_host, n_units_hbm;
-  float* part_o;               /* split-KV partial workspace, as dak_attention's                      */
-  float* part_lse;
-} dak_step_op;
-
-typedef struct {
-  void* dev;
-  int32_t n_ops, N, grid, ring_bytes, off_scratch, smem, pdl;
-  void* trace;  /* optional device u64 [n_ops][grid][4] globaltimer stamps: 0 stream-producer start
-                   (attention), 1 dependency satisfied, 2 first stage ready, 3 op done (NULL: off) */
-} dak_step_plan;
-
-/* Device bytes for the compiled op table + completion counters. */
-size_t dak_step_buffer_bytes(int32_t n_ops);
-/* KC to pack a linear with (in {64,128,256}) so that `rows_per_cta` rows fit one ring slot. */
-int32_t dak_step_choose_kc(int64_t rows_per_cta, int64_t K);
-/* Validate and compile an op table into dev_buf (synchronous setup call; not for capture). */
-dak_status dak_step_compile(const dak_step_op* ops, int32_t n_ops, int32_t N, const dak_launch_cfg* cfg,
-                            void* dev_buf, size_t dev_bytes, dak_step_plan* out);
-/* Enqueue the persistent decode step (one cooperative launch; graph-capturable, replayable). */
-dak_status dak_step_launch(const dak_step_plan* plan, dak_stream_t stream);
 
 #ifdef __cplusplus
 }

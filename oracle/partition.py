@@ -125,3 +125,56 @@ def host_pages_prefix(n_pages: int, ratio, chunk_pages: int) -> int:
 def batch_split_host_requests(B: int, ratio) -> int:
     """Paper attention mode: whole requests on host; round_half_up(ratio * B) of them."""
     return min(B, max(0, round_half_up(Fraction(ratio) * B)))
+
+
+def kv_place_chunk_major(seq_lens, page_size: int, max_pages: int, chunk_pages: int, host_units: int):
+    """KV placement of one attention op (reading R15 of DESIGN.md; "tile row 0 in host
+    memory"): the op's host units are its OLDEST split-KV chunks, taken chunk-major --
+    chunk 0 of request 0, 1, ..., B-1, then chunk 1 of every request that has one, ... Host pages
+    are numbered 0, 1, ... in (request, page) order, every other block-table entry (HBM, including
+    the max_pages - filled entries later decode tokens use) likewise; a host entry carries bit 31.
+
+    Written as the enumeration it describes. Returns (block table [B][max_pages] of uint32,
+    host pages, HBM pages, host tokens)."""
+    B = len(seq_lens)
+    filled = [-(-int(L) // page_size) for L in seq_lens]
+    if any(f > max_pages for f in filled):
+        raise ValueError("seq_len beyond max_pages")
+    chunks = [-(-f // chunk_pages) for f in filled]
+    order = []  # (request, chunk) units, oldest first, chunk-major
+    for c in range(max(chunks) if chunks else 0):
+        for b in range(B):
+            if c < chunks[b]:
+                order.append((b, c))
+    if host_units > len(order):
+        raise ValueError("more host units than chunks")
+    host_chunks = [0] * B
+    for b, c in order[:host_units]:
+        host_chunks[b] += 1
+    table = [[0] * max_pages for _ in range(B)]
+    ih = ig = host_tokens = 0
+    for b in range(B):
+        hp = min(host_chunks[b] * chunk_pages, filled[b])
+        for p in range(max_pages):
+            if p < hp:
+                table[b][p] = ih | 0x80000000
+                ih += 1
+            else:
+                table[b][p] = ig
+                ig += 1
+        host_tokens += min(hp * page_size, int(seq_lens[b]))
+    return table, ih, ig, host_tokens
+
+
+def linear_splitk_items(M: int, h: int, splits: int, block: int = 128):
+    """Row ownership of a split-K dak_linear launch: every tier is cut into blocks
+    of `block` rows (the last may be short) and every block into `splits` K ranges; CTA j of a tier
+    takes K split j % splits of block j // splits. Host CTAs first (rows [0, h)), then HBM (rows
+    [h, M)). Returns [(tier, row_begin, row_end)] per CTA."""
+    out = []
+    for tier, lo, hi in (("host", 0, h), ("hbm", h, M)):
+        n_blocks = -(-(hi - lo) // block)
+        for j in range(n_blocks * splits):
+            b = j // splits
+            out.append((tier, lo + b * block, min(hi, lo + (b + 1) * block)))
+    return out

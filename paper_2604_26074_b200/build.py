@@ -21,6 +21,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 SOURCES = [
     ("abi.cpp", []),
     ("planner.cpp", ["-Xcompiler", "-ffp-contract=off", "-fmad=false"]),
+    ("model.cpp", ["-Xcompiler", "-ffp-contract=off", "-fmad=false"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=0"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=1"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=2"]),
@@ -29,7 +30,6 @@ SOURCES = [
     ("linear.cu", ["-DDAK_LINEAR_PART=5"]),
     ("attention.cu", []),
     ("layer.cu", []),
-    ("step.cu", []),
     ("tp.cu", []),
 ]
 

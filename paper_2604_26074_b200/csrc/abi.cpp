@@ -1,8 +1,14 @@
 // Error plumbing, version, device queries and the host-tier allocator of the DAK C ABI.
 #include <cuda_runtime.h>
+#include <ctype.h>
+#include <errno.h>
 #include <string.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
 #include <unistd.h>
+
+#include <mutex>
+#include <unordered_map>
 
 #include "common.h"
 
@@ -67,20 +73,66 @@ dak_status dak_device_sms(int32_t* sms) {
   return DAK_OK;
 }
 
-// Host tier: pinned + mapped + portable pages (the SMs read them directly). When a NUMA
-// node is requested the pages are first-touched by this thread after an mbind-free placement
-// (single-socket boxes: node 0), then registered as mapped.
+dak_status dak_device_numa_node(int32_t* node) {
+  if (!node) return dak::fail(DAK_EINVAL, "node is NULL");
+  int dev = 0;
+  DAK_CUDA_TRY(cudaGetDevice(&dev));
+  char bus[64] = {0};
+  DAK_CUDA_TRY(cudaDeviceGetPCIBusId(bus, sizeof(bus), dev));
+  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+  char path[160];
+  snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/numa_node", bus);
+  int v = -1;
+  if (FILE* f = fopen(path, "r")) {
+    if (fscanf(f, "%d", &v) != 1) v = -1;
+    fclose(f);
+  }
+  *node = v;
+  return DAK_OK;
+}
+
+// Host tier: pinned + mapped + portable pages (the SMs read them directly over the link).
+// numa_node < 0: cudaHostAlloc (first-touch placement). numa_node >= 0: anonymous pages bound to
+// that node with mbind(MPOL_BIND) and faulted in before cudaHostRegister(Mapped | Portable), so a
+// GPU reads its host shard from the socket its PCIe link hangs off.
+static std::mutex g_reg_mu;
+static std::unordered_map<void*, size_t> g_registered;  // mmap'd + registered blocks -> bytes
+
 dak_status dak_host_alloc(size_t bytes, int32_t write_combined, int32_t numa_node, void** host_ptr, void** dev_ptr) {
   if (!host_ptr || !dev_ptr || bytes == 0) return dak::fail(DAK_EINVAL, "dak_host_alloc: bad arguments");
   void* h = nullptr;
-  unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable;
-  if (write_combined) flags |= cudaHostAllocWriteCombined;
-  (void)numa_node;  // single NUMA node on the measured box (profiles/r01/box_probe.txt)
-  DAK_CUDA_TRY(cudaHostAlloc(&h, bytes, flags));
+  if (numa_node < 0) {
+    unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable;
+    if (write_combined) flags |= cudaHostAllocWriteCombined;
+    DAK_CUDA_TRY(cudaHostAlloc(&h, bytes, flags));
+  } else {
+    if (write_combined) return dak::fail(DAK_EUNSUPPORTED, "dak_host_alloc: write-combined pages with a NUMA node");
+    if (numa_node >= 1024) return dak::fail(DAK_EINVAL, "dak_host_alloc: numa_node %d", numa_node);
+    const size_t page = (size_t)sysconf(_SC_PAGESIZE);
+    const size_t len = (bytes + page - 1) / page * page;
+    h = mmap(nullptr, len, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (h == MAP_FAILED) return dak::fail(DAK_ECUDA, "dak_host_alloc: mmap of %zu B failed (%s)", len, strerror(errno));
+    unsigned long mask[1024 / (8 * sizeof(unsigned long))] = {0};
+    mask[numa_node / (8 * sizeof(unsigned long))] = 1ul << (numa_node % (8 * sizeof(unsigned long)));
+    const long MPOL_BIND_ = 2;
+    if (syscall(SYS_mbind, h, len, MPOL_BIND_, mask, (unsigned long)1024, 0u) != 0) {
+      const int e = errno;
+      munmap(h, len);
+      return dak::fail(DAK_EINVAL, "dak_host_alloc: mbind to node %d failed (%s)", numa_node, strerror(e));
+    }
+    memset(h, 0, len);  // fault every page in on the bound node before pinning
+    cudaError_t e = cudaHostRegister(h, len, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) {
+      munmap(h, len);
+      return dak::fail(DAK_ECUDA, "cudaHostRegister: %s", cudaGetErrorString(e));
+    }
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    g_registered[h] = len;
+  }
   void* d = nullptr;
   cudaError_t e = cudaHostGetDevicePointer(&d, h, 0);
   if (e != cudaSuccess) {
-    cudaFreeHost(h);
+    dak_host_free(h);
     return dak::fail(DAK_ECUDA, "cudaHostGetDevicePointer: %s", cudaGetErrorString(e));
   }
   *host_ptr = h;
@@ -90,6 +142,20 @@ dak_status dak_host_alloc(size_t bytes, int32_t write_combined, int32_t numa_nod
 
 dak_status dak_host_free(void* host_ptr) {
   if (!host_ptr) return DAK_OK;
+  size_t len = 0;
+  {
+    std::lock_guard<std::mutex> g(g_reg_mu);
+    auto it = g_registered.find(host_ptr);
+    if (it != g_registered.end()) {
+      len = it->second;
+      g_registered.erase(it);
+    }
+  }
+  if (len) {
+    DAK_CUDA_TRY(cudaHostUnregister(host_ptr));
+    munmap(host_ptr, len);
+    return DAK_OK;
+  }
   DAK_CUDA_TRY(cudaFreeHost(host_ptr));
   return DAK_OK;
 }

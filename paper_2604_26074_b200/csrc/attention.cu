@@ -56,6 +56,7 @@ struct Params {
   float* part_o;     // [B][Hkv][max_chunks][G][d]
   float* part_lse;   // [B][Hkv][max_chunks][G]   (log2 domain)
   int n_host, n_hbm;
+  int auto_host;      // 1: host-CTA count chosen in-kernel from the block table (cfg.n_cta_host == 0)
   int ring_bytes;     // SMEM ring bytes per CTA, shared by the CTA's active warps
   int max_slots;      // ring slots per warp cap (<= kMaxSlots)
   int host_window;    // host CTAs: max in-flight tiles per warp (0: none)
@@ -170,9 +171,6 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   int* s_len = pref + p.B * p.max_chunks;                          // [B] seq_lens
 
   const int cta = blockIdx.x;
-  const bool host = cta < p.n_host;
-  const int my_j = host ? cta : cta - p.n_host;
-  const int my_n = host ? p.n_host : p.n_hbm;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
 
@@ -182,12 +180,39 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     tstamp(p.trace, 0);
   }
   grid_dep_launch();
+  const int n_pairs = p.B * p.max_chunks;
+  // CTA roles (one tier per SM). Auto: one host CTA per 4 host units (request, kv head,
+  // chunk) -- host CTAs are bound by the link latency, so a few keep more bytes in flight -- capped
+  // at 16 (congestion control), none when the block table names no host chunk.
+  int n_host = p.n_host, n_hbm = p.n_hbm, host_inflight = p.host_inflight;
+  if (p.auto_host) {
+    int cnt = 0;
+    for (int i = threadIdx.x; i < n_pairs; i += kThreads) {
+      const int b = i / p.max_chunks, c = i % p.max_chunks;
+      const int npg = (p.seq_lens[b] + p.page - 1) / p.page;
+      if (c * p.chunk_pages < npg)
+        cnt += ((uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages] & kHostBit) != 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) warp_tot[warp] = cnt;
+    __syncthreads();
+    int hu = 0;
+    for (int w = 0; w < kWarps; ++w) hu += warp_tot[w];
+    __syncthreads();
+    hu *= p.Hkv;
+    n_host = hu ? min(min(16, (hu + 3) / 4), (int)gridDim.x - 1) : 0;
+    n_hbm = (int)gridDim.x - n_host;
+    if (host_inflight > 0 && n_host > 0) host_inflight = max(2 * 16 * kD * 2, (512 * 1024) / n_host);
+  }
+  const bool host = cta < n_host;
+  const int my_j = host ? cta : cta - n_host;
+  const int my_n = host ? n_host : n_hbm;
   // Block table and seq_lens are step inputs, and every KV row except the newest token's was
   // written by earlier steps: the schedule and those tiles do not wait for the previous kernel
   // (griddepcontrol.wait). q and the tile holding the new token (position seq_len - 1, written by
   // the KV-append kernel just before) are read only after it (ABI contract in dak.h).
   // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
-  const int n_pairs = p.B * p.max_chunks;
   {  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
     int carry = 0;
     for (int base = 0; base < n_pairs; base += kThreads) {
@@ -237,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   if (host && p.host_window > 0) slots = min(slots, p.host_window);
   // congestion cap on in-flight host bytes, but never below double buffering per warp (one slot per
   // warp exposes the full link latency per tile: C4 B = 4 at r*, 0.90 -> 0.97 of EB(r*) without it)
-  if (host && p.host_inflight > 0) slots = min(slots, max(2, p.host_inflight / (active * slot_bytes)));
+  if (host && host_inflight > 0) slots = min(slots, max(2, host_inflight / (active * slot_bytes)));
   const int tile_bytes = tt * kD * 2;
 
   uint64_t* wf = full + warp * kMaxSlots;
@@ -667,7 +692,9 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   // host CTAs (caller-sized: ~one per 8 host units, i.e. one unit per warp; default 2). Congestion
   // control caps the host bytes in flight: 512 KB over all host CTAs keeps the PCIe link
   // saturated with 8 KB copies (256 KB reached only ~42 GB/s at C4 B = 4, r*) without queueing more
-  int n_host = c.n_cta_host > 0 ? c.n_cta_host : 2;
+  // host CTAs: caller-sized, or (n_cta_host == 0) chosen in-kernel from the block table
+  p.auto_host = c.n_cta_host <= 0 && a->k_host != nullptr;
+  int n_host = c.n_cta_host > 0 ? c.n_cta_host : (a->k_host ? 1 : 0);
   if (!a->k_host) n_host = 0;
   p.host_window = c.window > 0 ? c.window : 0;
   p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, (512 * 1024) / std::max(1, n_host)) : 0;

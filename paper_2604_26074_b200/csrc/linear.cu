@@ -73,6 +73,7 @@ struct __align__(64) Params {
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
   int ksplit;       // tcgen05 split-K: K splits (1: off); CTA = (tier row block of 128, split)
+  int host_gate;    // split-K congestion control: host-item CTAs streaming at once (0: no cap)
   int k64_split;    // 64-column chunks per split
   float* part;      // split-K fp32 partials [ksplit][N][M] (workspace)
   // fused pre-norm of x (nullable ln_w): per-row statistics merged from ln_parts partials
@@ -178,6 +179,25 @@ __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
 }
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Congestion control of the split-K host items (cap the SMs reading host memory). A
+// split-K launch has one CTA per (128-row block, K split) item, so a large host share would put
+// many host CTAs on the link at once; a counting semaphore in device memory lets at most `cap` of
+// them stream, each releasing its slot once its last host stage has landed. The spin is bounded:
+// a stale count can delay a launch but never hang it, and results never depend on the gate.
+__device__ unsigned int g_host_gate;
+__device__ __forceinline__ bool gate_acquire(int cap) {
+  for (int it = 0; it < (1 << 16); ++it) {
+    if (atomicAdd(&g_host_gate, 1u) < (unsigned)cap) return true;
+    atomicSub(&g_host_gate, 1u);
+    __nanosleep(512);
+  }
+  return false;
+}
+__device__ __forceinline__ void gate_release() {
+  __threadfence();
+  atomicSub(&g_host_gate, 1u);
+}
 __device__ __forceinline__ void consumer_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kConsumers) : "memory"); }
 
 __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
@@ -862,6 +882,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
           bulk_g2s_mc_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot],
                            (uint16_t)((1u << G) - 1u), pol);
       };
+      const bool gated = host && p.host_gate > 0 && gate_acquire(p.host_gate);
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);
         load_w(i, i);
@@ -883,12 +904,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
       for (int i = 0; i < pro; ++i) load_x(i, i);
       int s = pro == slots ? 0 : pro;
       uint32_t ph = pro == slots ? 1u : 0u;
+      int ls = pro - 1;
+      uint32_t lph = 0;
       for (int i = pro; i < nchunks; ++i) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], w_bytes + x_tx);
         load_w(s, i);
         load_x(s, i);
+        ls = s;
+        lph = ph;
         if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+      if (gated) {  // the last host stage has landed: free the link slot
+        mbar_wait(&full[ls], lph);
+        gate_release();
       }
     }
   } else if (warp == 1) {
@@ -1158,6 +1187,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
       const uint64_t pol = policy_evict_first();
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      const bool gated = host && p.host_gate > 0 && gate_acquire(p.host_gate);
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);
         bulk_g2s_hint(wring + (size_t)i * wstage, src + (long long)i * chunk_stride, w_bytes, &full[i], pol);
@@ -1167,12 +1197,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
       for (int i = 0; i < pro; ++i) tma_3d(xring + (size_t)i * p.x_stage_bytes, xmap, 0, 0, kbeg + i, &full[i]);
       int s = pro == slots ? 0 : pro;
       uint32_t ph = pro == slots ? 1u : 0u;
+      int ls = pro - 1;
+      uint32_t lph = 0;
       for (int i = pro; i < nchunks; ++i) {
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_expect_tx(&full[s], w_bytes + x_tx);
         bulk_g2s_hint(wring + (size_t)s * wstage, src + (long long)i * chunk_stride, w_bytes, &full[s], pol);
         tma_3d(xring + (size_t)s * p.x_stage_bytes, xmap, 0, 0, kbeg + i, &full[s]);
+        ls = s;
+        lph = ph;
         if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+      if (gated) {  // the last host stage has landed: free the link slot
+        mbar_wait(&full[ls], lph);
+        gate_release();
       }
     }
   } else if (warp == 1) {  // MMA issuer: D[128 batch rows][RN weight rows] += x . W^T
@@ -1505,7 +1543,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       bks = ceil_div(C, S);
       S = ceil_div(C, bks);
     }
-    if (S > 1 && (n_hbm == 0 || ceil_div(M - h, n_hbm) < 128)) {
+    if (S > 1 && ceil_div(M, nsm) < 128) {  // from M and the SM count only (never h: r-invariance)
       ksplit = (int)S;
       k64_split = (int)bks;
       n_host = (int)(ceil_div(h, 128) * S);
@@ -1649,12 +1687,21 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // congestion window: in-flight host stages per host CTA. With congestion control the
   // window is the smallest that keeps ~256 KB in flight on the link (calibrated saturation point);
   // without it every host ring slot may be in flight.
+  // Split-K plans have one host CTA per (row block, K split) item: with congestion control the
+  // host_gate semaphore lets at most n_cta_host (default 2) of them stream at once, and the window
+  // is sized for that many.
+  p.host_gate = 0;
+  if (ksplit > 1 && n_host > 0 && c.congestion_control) {
+    const int cap_items = c.n_cta_host > 0 ? c.n_cta_host : 2;
+    if (n_host > cap_items) p.host_gate = cap_items;
+  }
+  const int n_stream_host = p.host_gate > 0 ? p.host_gate : n_host;
   int window = p.stages_host;
   if (n_host > 0) {
     if (c.window > 0) window = std::min(c.window, p.stages_host);
     else if (c.congestion_control) {
       const long long hstage = std::max<long long>(1, rmax_host * kc * 2);
-      window = (int)std::min<long long>(p.stages_host, std::max<long long>(1, ceil_div(256 * 1024, hstage * n_host)));
+      window = (int)std::min<long long>(p.stages_host, std::max<long long>(1, ceil_div(256 * 1024, hstage * n_stream_host)));
     }
   }
   p.window = std::max(1, window);
@@ -1898,6 +1945,12 @@ int32_t dak_linear_default_kc(int64_t M, int64_t K, int32_t n_ctas) {
   return best;
 }
 
+int32_t dak_linear_choose_kc(int64_t rows_per_cta, int64_t K) {
+  if (K % 256 == 0 && rows_per_cta <= 96) return 256;
+  if (K % 128 == 0 && rows_per_cta <= 192) return 128;
+  return 64;
+}
+
 dak_status dak_pack_linear(const void* src, int64_t rows, int64_t K, int32_t kc, void* dst, dak_stream_t stream) {
   if (!src || !dst || rows < 0 || K <= 0) return fail(DAK_EINVAL, "dak_pack_linear: bad arguments");
   if (K % 64 || kc < 64 || kc > 2048 || (kc & (kc - 1)) || K % kc)
@@ -1931,6 +1984,8 @@ dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info*
   info->host_bytes = args->h * args->K * 2;
   info->cluster = pl.p.mc;
   info->ksplit = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;
+  info->host_gate = pl.p.host_gate;
+  info->reserved = 0;
   return DAK_OK;
 }
 
@@ -1946,7 +2001,14 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
   const long long n = host ? pl.p.n_host : pl.p.n_hbm;
   const long long off = host ? 0 : args->h;
   long long rb, re;
-  lin::tier_rows(R, j, n, pl.p.rgran, &rb, &re);
+  if (pl.path == 3 && pl.p.ksplit > 1) {  // split-K: CTA = (row block of kblock rows, K split) item
+    rb = std::min<long long>(R, (j / pl.p.ksplit) * pl.p.kblock);
+    re = std::min<long long>(R, rb + pl.p.kblock);
+  } else if (pl.p.pair > 1) {  // N > 512: groups of `pair` CTAs share one row range
+    lin::tier_rows(R, j / pl.p.pair, n / pl.p.pair, pl.p.rgran, &rb, &re);
+  } else {
+    lin::tier_rows(R, j, n, pl.p.rgran, &rb, &re);
+  }
   *tier = host ? 1 : 0;
   *row_begin = off + rb;
   *row_end = off + re;

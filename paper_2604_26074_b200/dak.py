@@ -52,7 +52,7 @@ class dak_op_plan(C.Structure):
 class dak_launch_cfg(C.Structure):
     _fields_ = [("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("window", C.c_int32), ("stages", C.c_int32),
                 ("congestion_control", C.c_int32), ("pdl", C.c_int32), ("force_path", C.c_int32),
-                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("ksplit", C.c_int32)]
+                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("reserved", C.c_int32)]
 
 
 class dak_linear_args(C.Structure):
@@ -70,7 +70,8 @@ class dak_linear_launch_info(C.Structure):
     _fields_ = [("grid", C.c_int32), ("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("threads", C.c_int32),
                 ("stages_hbm", C.c_int32), ("window_host", C.c_int32), ("smem_bytes", C.c_int32), ("path", C.c_int32),
                 ("rows_per_cta_host_max", C.c_int64), ("rows_per_cta_hbm_max", C.c_int64),
-                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("ksplit", C.c_int32)]
+                ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("ksplit", C.c_int32),
+                ("host_gate", C.c_int32), ("reserved", C.c_int32)]
 
 
 def _sig(name, res, args):
@@ -201,6 +202,70 @@ def plan_ratios(hw: dict, ops: list, y_req_bytes: int, mode: int = PLAN_EXACT):
     return res, obj.value
 
 
+# ------------------------------------------------------------------------------------- planner inputs, placement
+class dak_model(C.Structure):
+    _fields_ = [("family", C.c_int32), ("n_layers", C.c_int32), ("hidden", C.c_int32), ("n_heads", C.c_int32),
+                ("n_kv_heads", C.c_int32), ("head_dim", C.c_int32), ("ffn", C.c_int32), ("vocab", C.c_int32),
+                ("tp_size", C.c_int32), ("fused_qkv", C.c_int32), ("fused_gate_up", C.c_int32),
+                ("include_head", C.c_int32)]
+
+
+class dak_op_desc(C.Structure):
+    _fields_ = [("layer", C.c_int32), ("role", C.c_int32), ("M", C.c_int64), ("K", C.c_int64), ("flops", C.c_double)]
+
+
+ROLES = {0: "q", 1: "k", 2: "v", 3: "qkv", 4: "o", 5: "up", 6: "down", 7: "gate", 8: "gate_up", 9: "attn", 10: "head"}
+
+_sig("dak_global_offload_bytes", C.c_int32, [C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_int64),
+                                             C.POINTER(C.c_double)])
+_sig("dak_decode_ops", C.c_int32, [C.POINTER(dak_model), C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_double,
+                                   C.c_double, C.POINTER(dak_op), C.POINTER(dak_op_desc), C.c_int32,
+                                   C.POINTER(C.c_int32)])
+_sig("dak_kv_place", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                 C.POINTER(C.c_int64)])
+EXPORTED += ["dak_global_offload_bytes", "dak_decode_ops", "dak_kv_place"]
+
+
+def global_offload_bytes(weight_bytes: int, kv_bytes: int, hbm_budget_bytes: int, host_capacity_bytes: int = -1):
+    """dak_global_offload_bytes -> (y_req bytes, R)."""
+    y, r = C.c_int64(), C.c_double()
+    _check(lib.dak_global_offload_bytes(int(weight_bytes), int(kv_bytes), int(hbm_budget_bytes),
+                                        int(host_capacity_bytes), C.byref(y), C.byref(r)))
+    return y.value, r.value
+
+
+def model(family: int, n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab, tp_size=1, fused_qkv=1,
+          fused_gate_up=1, include_head=1) -> dak_model:
+    return dak_model(int(family), int(n_layers), int(hidden), int(n_heads), int(n_kv_heads), int(head_dim), int(ffn),
+                     int(vocab), int(tp_size), int(fused_qkv), int(fused_gate_up), int(include_head))
+
+
+def decode_ops(m: dak_model, batch: int, context: int, unit_rows: int, chunk_tokens: int, peak_linear: float,
+               peak_attn: float) -> list:
+    """dak_decode_ops -> list of dicts (kind, n_units, unit_bytes, total_bytes, T, layer, role, M, K, flops)."""
+    n = C.c_int32()
+    _check(lib.dak_decode_ops(C.byref(m), int(batch), int(context), int(unit_rows), int(chunk_tokens),
+                              float(peak_linear), float(peak_attn), None, None, 0, C.byref(n)))
+    ops, desc = (dak_op * n.value)(), (dak_op_desc * n.value)()
+    _check(lib.dak_decode_ops(C.byref(m), int(batch), int(context), int(unit_rows), int(chunk_tokens),
+                              float(peak_linear), float(peak_attn), ops, desc, n.value, C.byref(n)))
+    return [dict(kind=o.kind, n_units=o.n_units, unit_bytes=o.unit_bytes, total_bytes=o.total_bytes, T=o.t_comp_s,
+                 layer=d.layer, role=ROLES[d.role], M=d.M, K=d.K, flops=d.flops) for o, d in zip(ops, desc)]
+
+
+def kv_place(seq_lens, page_size: int, max_pages: int, chunk_pages: int, host_units: int):
+    """dak_kv_place -> (block table as a numpy int32 [B, max_pages], host pages, HBM pages, host tokens)."""
+    import numpy as np
+    B = len(seq_lens)
+    sl = (C.c_int32 * B)(*[int(x) for x in seq_lens])
+    bt = np.zeros((B, max_pages), dtype=np.int32)
+    nh, ng, ht = C.c_int32(), C.c_int32(), C.c_int64()
+    _check(lib.dak_kv_place(B, sl, int(page_size), int(max_pages), int(chunk_pages), int(host_units),
+                            bt.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nh), C.byref(ng), C.byref(ht)))
+    return bt, nh.value, ng.value, ht.value
+
+
 # ------------------------------------------------------------------------------------- host tier
 def host_alloc(nbytes: int, write_combined: bool = False, numa_node: int = -1):
     """Pinned + mapped host allocation -> (host_ptr, dev_ptr) ints."""
@@ -211,6 +276,17 @@ def host_alloc(nbytes: int, write_combined: bool = False, numa_node: int = -1):
 
 def host_free(host_ptr: int):
     _check(lib.dak_host_free(host_ptr))
+
+
+_sig("dak_device_numa_node", C.c_int32, [C.POINTER(C.c_int32)])
+EXPORTED += ["dak_device_numa_node"]
+
+
+def device_numa_node() -> int:
+    """NUMA node of the current GPU's PCIe attachment (-1: unknown)."""
+    v = C.c_int32()
+    _check(lib.dak_device_numa_node(C.byref(v)))
+    return v.value
 
 
 # ------------------------------------------------------------------------------------- linear
@@ -289,13 +365,6 @@ def attention_args(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, 
     a.q_row_stride = int(q_row_stride)
     a.k_new, a.v_new, a.kv_new_stride = _ptr(k_new), _ptr(v_new), int(kv_new_stride)
     return a
-
-
-def attention_host_ctas(host_units: int) -> int:
-    """Host-tier CTAs for dak_attention: one per 4 host units (request, kv head, chunk), 1..16.
-    Host CTAs are bound by the link latency, not by SM throughput: a few more CTAs keep more
-    bytes in flight (each warp owns a unit) at the cost of HBM CTAs."""
-    return max(1, min(16, -(-int(host_units) // 4)))
 
 
 def attention_workspace_size(args: dak_attention_args) -> int:
@@ -444,69 +513,9 @@ def layer(args: dak_layer_args, stream=None):
     _check(lib.dak_layer(C.byref(args), _stream(stream)))
 
 
-# ------------------------------------------------------------------------------------- persistent step
-STEP_EMBED, STEP_LAYERNORM, STEP_LINEAR, STEP_ATTENTION, STEP_COMBINE = 0, 1, 2, 3, 4
+_sig("dak_linear_choose_kc", C.c_int32, [C.c_int64, C.c_int64])
+EXPORTED += ["dak_linear_choose_kc"]
 
 
-class dak_step_op(C.Structure):
-    _fields_ = [("type", C.c_int32), ("dep", C.c_int32), ("n_cta_host", C.c_int32), ("act", C.c_int32),
-                ("w_host", C.c_void_p), ("w_hbm", C.c_void_p), ("M", C.c_int64), ("K", C.c_int64), ("h", C.c_int64),
-                ("kc", C.c_int32), ("kv_kind", C.c_int32), ("x", C.c_void_p), ("y", C.c_void_p), ("ldy", C.c_int64),
-                ("bias", C.c_void_p), ("residual", C.c_void_p), ("stats_out", C.c_void_p), ("kv_row0", C.c_int64),
-                ("stats_in", C.c_void_p), ("ln_w", C.c_void_p), ("ln_b", C.c_void_p), ("eps", C.c_float),
-                ("cols", C.c_int32), ("tokens", C.c_void_p), ("positions", C.c_void_p), ("tok_emb", C.c_void_p),
-                ("pos_emb", C.c_void_p), ("pos_offset", C.c_int32), ("reserved1", C.c_int32),
-                ("q", C.c_void_p), ("q_stride", C.c_int64), ("out", C.c_void_p),
-                ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p), ("k_host", C.c_void_p), ("v_host", C.c_void_p),
-                ("block_table", C.c_void_p), ("seq_lens", C.c_void_p), ("Hq", C.c_int32), ("Hkv", C.c_int32),
-                ("d", C.c_int32), ("page_size", C.c_int32), ("max_pages", C.c_int32), ("chunk_pages", C.c_int32),
-                ("scale", C.c_float), ("reserved2", C.c_int32), ("units_host", C.c_void_p),
-                ("units_hbm", C.c_void_p), ("n_units_host", C.c_int32), ("n_units_hbm", C.c_int32),
-                ("part_o", C.c_void_p), ("part_lse", C.c_void_p)]
-
-
-class dak_step_plan(C.Structure):
-    _fields_ = [("dev", C.c_void_p), ("n_ops", C.c_int32), ("N", C.c_int32), ("grid", C.c_int32),
-                ("ring_bytes", C.c_int32), ("off_scratch", C.c_int32), ("smem", C.c_int32), ("pdl", C.c_int32),
-                ("trace", C.c_void_p)]
-
-
-_sig("dak_step_buffer_bytes", C.c_size_t, [C.c_int32])
-_sig("dak_step_choose_kc", C.c_int32, [C.c_int64, C.c_int64])
-_sig("dak_step_compile", C.c_int32, [C.POINTER(dak_step_op), C.c_int32, C.c_int32, C.POINTER(dak_launch_cfg),
-                                     C.c_void_p, C.c_size_t, C.POINTER(dak_step_plan)])
-_sig("dak_step_launch", C.c_int32, [C.POINTER(dak_step_plan), C.c_void_p])
-EXPORTED += ["dak_step_buffer_bytes", "dak_step_choose_kc", "dak_step_compile", "dak_step_launch"]
-
-
-def step_op(**kw) -> dak_step_op:
-    o = dak_step_op()
-    o.dep = -1
-    o.kv_row0 = -1
-    for k, v in kw.items():
-        f = dict(dak_step_op._fields_)[k]
-        if f is C.c_void_p:
-            setattr(o, k, _ptr(v))
-        else:
-            setattr(o, k, v)
-    return o
-
-
-def step_choose_kc(rows_per_cta: int, K: int) -> int:
-    return int(lib.dak_step_choose_kc(int(rows_per_cta), int(K)))
-
-
-def step_compile(ops: list, N: int, cfg: dict | None = None):
-    """Compile an op table; returns (plan, device buffer tensor)."""
-    import torch
-    arr = (dak_step_op * len(ops))(*ops)
-    nbytes = lib.dak_step_buffer_bytes(len(ops))
-    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-    plan = dak_step_plan()
-    c = launch_cfg(**(cfg or {}))
-    _check(lib.dak_step_compile(arr, len(ops), int(N), C.byref(c), buf.data_ptr(), nbytes, C.byref(plan)))
-    return plan, buf
-
-
-def step_launch(plan: dak_step_plan, stream=None):
-    _check(lib.dak_step_launch(C.byref(plan), _stream(stream)))
+def choose_kc(rows_per_cta: int, K: int) -> int:
+    return int(lib.dak_linear_choose_kc(int(rows_per_cta), int(K)))

@@ -1,16 +1,21 @@
-"""DAK decode engine for OPT-family models (PAPER §4), built on the C ABI.
+"""DAK decode engines, built on the C ABI (PAPER §4).
 
-Setup (once): operator list -> dak_plan_ratios (greedy per-op ratios) -> byte
-placement (host = leading rows / oldest KV chunks) -> DAK-KC / DAK-PG packing into HBM
-and pinned mapped host memory -> one decode step captured in a CUDA graph.
-Step (hot path): embed -> 48 x dak_layer -> LayerNorm -> LM head, every weight and KV page
-streamed by the library's split-source kernels. torch is used only for device memory, streams
-and graphs. This module never imports the CPU oracle.
+Setup (once, per GPU): the op list of one decode step (dak_decode_ops: C_i, units, FLOPs, T_i;
+P:L383-388) -> dak_plan_ratios (greedy per-op ratios) -> byte placement (linear: host =
+the leading rows; attention: dak_kv_place, the oldest split-KV chunks) -> DAK-KC / DAK-PG
+packing into HBM and pinned mapped host memory -> one decode step captured in a CUDA graph.
+Step (hot path): embed -> layers (dak_layer) -> final norm + LM head, every weight and KV page
+streamed by the library's split-source kernels.
+
+This module holds only setup and marshalling: every number of the method (op profile, ratios,
+placement, CTA roles) comes from the library. torch is used for device memory, streams and graphs
+only. This module never imports the CPU oracle.
 """
 from __future__ import annotations
 
+import ctypes
 import math
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import numpy as np
 import torch
@@ -45,10 +50,11 @@ class HW:
     host_dram_bps: float = 0.0
     peak_flops: float = 1.3554e15
     host_latency_s: float = 0.0  # latency-aware planner extension (dak_hw.host_latency_s)
+    host_capacity_bytes: int = -1
 
     def as_dict(self):
         return dict(hbm_bps=self.hbm_bps, link_bps=self.link_bps,
-                    host_dram_bps=self.host_dram_bps or self.link_bps, host_capacity_bytes=-1,
+                    host_dram_bps=self.host_dram_bps or self.link_bps, host_capacity_bytes=self.host_capacity_bytes,
                     host_latency_s=self.host_latency_s)
 
 
@@ -75,112 +81,92 @@ def _bf16_rand(shape, std, gen):
     return (torch.randn(shape, device="cuda", generator=gen, dtype=torch.float32) * std).to(torch.bfloat16)
 
 
-class DakOPT:
-    """OPT decode step over HBM + pinned host memory at per-op planned ratios."""
+class _DecodeEngine:
+    """Shared setup of one GPU's decode step: planning, placement, KV pools, graph capture."""
 
-    def __init__(self, cfg: OPTConfig, batch: int, context: int, hw: HW, mode: int = dak.PLAN_BALANCED,
-                 y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 0, seed: int = 0,
-                 pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
-                 host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
-                 evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
-                 max_context: int | None = None):
-        self.cfg, self.B, self.context, self.hw = cfg, batch, context, hw
-        self.page, self.chunk_pages, self.unit_rows = page_size, chunk_pages, unit_rows
+    family = dak.MODEL_OPT
+    # op-list role -> key of the layer dict holding the LinearOp
+    ROLE_KEY = dict(qkv="qkv", q="q", k="k", v="v", o="o", up="up", gate_up="up", down="down")
+
+    def _init_common(self, batch, context, hw, unit_rows, page_size, chunk_pages, max_context, n_kv_local,
+                     pdl, congestion_control, n_cta_host, seed, evict_first=True):
+        self.B, self.context, self.hw = batch, context, hw
+        self.page, self.unit_rows = page_size, unit_rows
+        self.max_context = max(context, max_context or context)
+        self.pages_per_req = -(-self.max_context // page_size)
         if not chunk_pages:  # split-KV chunk: about one (request, kv head, chunk) unit per two warp slots (measured best)
-            pages = -(-max(context, max_context or 0) // page_size)
-            units_1 = batch * cfg.n_kv_heads * pages
-            self.chunk_pages = max(1, min(16, units_1 // (148 * 4)))
+            units_1 = batch * n_kv_local * self.pages_per_req
+            chunk_pages = max(1, min(16, units_1 // (148 * 4)))
+        self.chunk_pages = chunk_pages
+        self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
         self.pdl = int(pdl)
         self.n_cta_host = n_cta_host
         self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host,
                            l2_policy=0 if evict_first else 1)
-        self.l2_prefetch = int(l2_prefetch)
-        self.fuse_norm = bool(fuse_norm)
-        # one [q; k; v] projection per layer (one launch reading x once); the persistent step and
-        # the paper's op list use the three projections separately
-        self.fused_qkv = bool(fused_qkv)
+        # attention: host CTAs chosen by the library from the block table (dak_attention auto mode)
+        self.attn_launch = dict(self.launch, n_cta_host=0)
         self.sms = dak.device_sms()
         self.gen = torch.Generator(device="cuda")
         self.gen.manual_seed(seed)
         self._host_blocks = []
-        c = cfg
-        self.layers = []
-        for i in range(c.n_layers):
-            if self.fused_qkv:
-                L = dict(qkv=LinearOp(f"L{i}.qkv", (c.n_heads + 2 * c.n_kv_heads) * c.head_dim, c.hidden))
-            else:  # q/k/v separate, as the paper's op list (P:L981 footnote)
-                L = dict(q=LinearOp(f"L{i}.q", c.n_heads * c.head_dim, c.hidden),
-                         k=LinearOp(f"L{i}.k", c.n_kv_heads * c.head_dim, c.hidden),
-                         v=LinearOp(f"L{i}.v", c.n_kv_heads * c.head_dim, c.hidden))
-            L.update(o=LinearOp(f"L{i}.o", c.hidden, c.n_heads * c.head_dim),
-                     up=LinearOp(f"L{i}.fc1", c.ffn, c.hidden),
-                     down=LinearOp(f"L{i}.fc2", c.hidden, c.ffn))
-            self.layers.append(L)
-        self.head = LinearOp("head", c.vocab, c.hidden)
-        # KV pages per request cover max_context tokens: decode steps append beyond the prompt
-        self.max_context = max(context, max_context or context)
-        self.pages_per_req = -(-self.max_context // page_size)
-        self.chunks_per_req = -(-self.pages_per_req // self.chunk_pages)
-        self.plan = self._plan(mode, y_req, host_override)
-        self._allocate(weights)
-        self._kv()
         self.graph = None
 
-    # ------------------------------------------------------------------ planning (P:L462-486)
-    def linear_ops(self):
-        for L in self.layers:
-            if self.fused_qkv:
-                yield from (L["qkv"], L["o"], L["up"], L["down"])
-            else:
-                yield from (L["q"], L["k"], L["v"], L["o"], L["up"], L["down"])
-        yield self.head
+    # ------------------------------------------------------------------ planning (P:L383-388, P:L462-486)
+    def _model_desc(self) -> dak.dak_model:
+        raise NotImplementedError
 
-    def kv_bytes_per_layer(self) -> int:
-        c = self.cfg
-        return 2 * c.n_kv_heads * c.head_dim * 2 * self.B * self.context
-
-    def _plan(self, mode, y_req, host_override):
-        c, B = self.cfg, self.B
-        ops = []
-        for op in self.linear_ops():
-            flops = 2.0 * B * op.M * op.K
-            ops.append(dict(kind="linear", n_units=-(-op.M // self.unit_rows), unit_bytes=self.unit_rows * op.K * 2,
-                            total_bytes=op.bytes, T=flops / self.hw.peak_flops))
-        tok_bytes = 2 * c.n_kv_heads * c.head_dim * 2
-        chunk_tok = self.chunk_pages * self.page
-        for _ in range(c.n_layers):
-            C_att = tok_bytes * B * self.context
-            n_units = B * self.chunks_per_req
-            # every request's last chunk may be short: plan with the mean unit (ceil(C/n)), which
-            # keeps (n-1)u < C <= nu; placement then takes whole chunks, oldest first (DESIGN R15)
-            unit = -(-C_att // n_units)
-            flops = 4.0 * B * self.context * c.n_heads * c.head_dim
-            ops.append(dict(kind="attention", n_units=n_units, unit_bytes=unit, total_bytes=C_att,
-                            T=flops / self.hw.peak_flops))
+    def _plan(self, mode, y_req, host_override=None):
+        """dak_decode_ops -> dak_plan_ratios; builds self.layers / self.head from the op list."""
+        self.model_desc = self._model_desc()
+        ops = dak.decode_ops(self.model_desc, self.B, self.context, self.unit_rows, self.chunk_pages * self.page,
+                             self.hw.peak_flops, self.hw.peak_flops)
         self.plan_ops = ops
-        plan, obj = dak.plan_ratios(self.hw.as_dict(), ops, y_req, mode)
-        self.objective = obj
-        i = 0
-        for op in self.linear_ops():
-            op.h = min(op.M, plan[i]["host_units"] * self.unit_rows)
-            if host_override and op.name.split(".")[-1] in host_override:
-                op.h = host_override[op.name.split(".")[-1]]
-            # one KC for both execution paths: the persistent step's slot constraint (<= 256)
+        plan, self.objective = dak.plan_ratios(self.hw.as_dict(), ops, y_req, mode)
+        self.plan = plan
+        n_layers = max(o["layer"] for o in ops) + 1
+        self.layers = [dict() for _ in range(n_layers)]
+        self.attn_host_chunks = [0] * n_layers
+        self.head = None
+        for o, p in zip(ops, plan):
+            if o["role"] == "attn":
+                self.attn_host_chunks[o["layer"]] = p["host_units"]
+                continue
+            name = "head" if o["role"] == "head" else f"L{o['layer']}.{o['role']}"
+            op = LinearOp(name, o["M"], o["K"])
+            op.h = min(op.M, p["host_units"] * self.unit_rows)
+            if host_override and o["role"] in host_override:
+                op.h = host_override[o["role"]]
+            if o["role"] == "head":
+                self.head = op
+            else:
+                self.layers[o["layer"]][self.ROLE_KEY[o["role"]]] = op
+            # KC = 64 above 16 batch columns (the tcgen05 path's canonical SWIZZLE_128B operands);
+            # else the widest KC whose stage holds the CTA's rows (dak_linear_choose_kc)
             n_host = min(self.n_cta_host, op.h) if op.h > 0 else 0
             rows = max(-(-op.h // max(n_host, 1)) if op.h else 0, -(-(op.M - op.h) // (self.sms - n_host)))
-            # KC = 64 above 16 batch columns: the tcgen05 path (canonical SWIZZLE_128B operands)
-            op.kc = 64 if self.B > 16 else dak.step_choose_kc(rows, op.K)
-            i += 1
-        self.attn_host_chunks = [plan[i + l]["host_units"] for l in range(c.n_layers)]
+            op.kc = 64 if self.B > 16 else dak.choose_kc(rows, op.K)
         return plan
+
+    def linear_ops(self):
+        for L in self.layers:
+            for key in ("qkv", "q", "k", "v", "o", "up", "down"):
+                if isinstance(L.get(key), LinearOp):
+                    yield L[key]
+        yield self.head
 
     # ------------------------------------------------------------------ placement + packing (P:L321-323)
     def _alloc_host(self, nbytes):
-        hp, dp = dak.host_alloc(max(nbytes, 16))
+        hp, dp = dak.host_alloc(max(nbytes, 16), numa_node=self.numa_node)
         self._host_blocks.append(hp)
         return hp, dp
 
-    def _fill_linear(self, op: LinearOp, W: torch.Tensor | None):
+    @property
+    def numa_node(self) -> int:
+        if not hasattr(self, "_numa"):
+            self._numa = dak.device_numa_node()
+        return self._numa
+
+    def _fill_linear(self, op: LinearOp, W):
         """W: logical [M, K] bf16 on device (or None: random N(0, 1/K) drawn in packed order)."""
         M, K, h = op.M, op.K, op.h
         if h < M:
@@ -193,6 +179,139 @@ class DakOPT:
             op.host = self._alloc_host(h * K * 2)
             src = W[:h].contiguous() if W is not None else _bf16_rand((h, K), 1.0 / math.sqrt(K), self.gen)
             dak.pack_linear(src, h, K, op.kc, op.host[1])
+
+    def _kv_pools(self, n_kv_local, head_dim):
+        """Per layer: dak_kv_place's block table (oldest chunks on the host, chunk-major), the two
+        tier pools (prompt KV drawn N(0, 1) in HBM, host pools zeroed then packed by load_kv)."""
+        B, ppr = self.B, self.pages_per_req
+        page_elems = n_kv_local * self.page * head_dim
+        self.block_tables, self.kv, self.kv_host_tokens = [], [], []
+        for l in range(len(self.layers)):
+            bt, Ph, Pg, ht = dak.kv_place([self.context] * B, self.page, ppr, self.chunk_pages,
+                                          self.attn_host_chunks[l])
+            kg = torch.zeros(max(Pg, 1) * page_elems, dtype=torch.bfloat16, device="cuda")
+            vg = torch.zeros_like(kg)
+            kh = self._alloc_host(max(Ph, 1) * page_elems * 2)
+            vh = self._alloc_host(max(Ph, 1) * page_elems * 2)
+            for hp in (kh, vh):  # finite slots beyond seq_len (dak.h)
+                ctypes.memset(hp[0], 0, max(Ph, 1) * page_elems * 2)
+            kg.copy_(_bf16_rand(kg.shape, 1.0, self.gen))
+            vg.copy_(_bf16_rand(vg.shape, 1.0, self.gen))
+            self.kv.append((kg, vg, kh, vh, Ph, Pg))
+            self.kv_host_tokens.append(ht)
+            self.block_tables.append(torch.from_numpy(bt).cuda())
+        self.positions = torch.full((B,), self.context - 1, dtype=torch.int32, device="cuda")
+        self.seq_lens = self.positions + 1
+        self.tokens = torch.zeros((B,), dtype=torch.int32, device="cuda")
+
+    def _load_kv(self, K_cache, V_cache, n_kv_local, d):
+        """K_cache[l][b] = [L_b, Hkv, d] bf16 bits (numpy) of the cached tokens, written into the tier
+        pools the block table names (DAK-PG)."""
+        page = self.page
+        for l, (kg, vg, kh, vh, Ph, Pg) in enumerate(self.kv):
+            bt = self.block_tables[l].cpu().numpy().view(np.uint32)
+            pools = {}
+            for name, src in (("k", K_cache[l]), ("v", V_cache[l])):
+                lg = np.zeros((max(Pg, 1), n_kv_local, page, d), np.uint16)
+                lh = np.zeros((max(Ph, 1), n_kv_local, page, d), np.uint16)
+                for b in range(self.B):
+                    arr = np.asarray(src[b])
+                    for t0 in range(0, arr.shape[0], page):
+                        e = int(bt[b, t0 // page])
+                        pool = lh if e & dak.HOST_BIT else lg
+                        blk = arr[t0:t0 + page]
+                        pool[e & 0x7FFFFFFF, :, :blk.shape[0]] = blk.transpose(1, 0, 2)
+                pools[name] = (lg, lh)
+            for (lg, lh), dg, dh in ((pools["k"], kg, kh), (pools["v"], vg, vh)):
+                dak.pack_kv_pages(torch.from_numpy(lg.view(np.int16)).cuda(), lg.shape[0] * n_kv_local, page, d, dg)
+                dak.pack_kv_pages(torch.from_numpy(lh.view(np.int16)).cuda(), lh.shape[0] * n_kv_local, page, d, dh[1])
+                torch.cuda.synchronize()
+
+    def _head_args(self, x, out, **kw):
+        hw = self.head.host[1] if self.head.host else None
+        ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B, x, out,
+                             cfg=self.launch, **kw)
+        if self.B > 16:  # tcgen05 split-K partials for the head
+            need = dak.linear_workspace_size(ha)
+            if need:
+                if getattr(self, "head_ws", None) is None or self.head_ws.numel() < need:
+                    self.head_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+                ha.workspace, ha.workspace_bytes = self.head_ws.data_ptr(), self.head_ws.numel()
+        return ha
+
+    # ------------------------------------------------------------------ step
+    def advance(self, stream=None):
+        """Move every request to the next position (after a step appended its token's KV)."""
+        if int(self.positions.max()) + 1 >= self.max_context:
+            raise ValueError("decode past max_context")
+        with torch.cuda.stream(stream or torch.cuda.current_stream()):
+            self.positions.add_(1)
+            self.seq_lens.add_(1)
+
+    def capture(self, stream: torch.cuda.Stream):
+        with torch.cuda.stream(stream):
+            self.enqueue_step(stream)  # warm (sets function attributes outside capture)
+            stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                self.enqueue_step(stream)
+        self.graph = g
+        return g
+
+    def bytes_per_step(self) -> dict:
+        """Algorithmic bytes read per decode step, split by tier (weights + KV of the context)."""
+        hbm = host = 0
+        for op in self.linear_ops():
+            hbm += (op.M - op.h) * op.K * 2
+            host += op.h * op.K * 2
+        tok = 2 * self.n_kv_local * self.head_dim * 2
+        for ht in self.kv_host_tokens:
+            host += tok * ht
+            hbm += tok * (self.B * self.context - ht)
+        return dict(hbm=hbm, host=host, total=hbm + host)
+
+    def close(self):
+        for hp in self._host_blocks:
+            try:
+                dak.host_free(hp)
+            except Exception:
+                pass
+        self._host_blocks = []
+
+
+class DakOPT(_DecodeEngine):
+    """OPT decode step over HBM + pinned host memory at per-op planned ratios."""
+
+    family = dak.MODEL_OPT
+
+    def __init__(self, cfg: OPTConfig, batch: int, context: int, hw: HW, mode: int = dak.PLAN_BALANCED,
+                 y_req: int = 0, unit_rows: int = 16, page_size: int = 64, chunk_pages: int = 0, seed: int = 0,
+                 pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
+                 host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
+                 evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
+                 max_context: int | None = None):
+        self.cfg = cfg
+        self.n_kv_local, self.head_dim = cfg.n_kv_heads, cfg.head_dim
+        self._init_common(batch, context, hw, unit_rows, page_size, chunk_pages, max_context, cfg.n_kv_heads,
+                          pdl, congestion_control, n_cta_host, seed, evict_first)
+        self.l2_prefetch = int(l2_prefetch)
+        self.fuse_norm = bool(fuse_norm)
+        # one [q; k; v] projection per layer (one launch reading x once; reading R18); the paper's
+        # op list has the three projections separately
+        self.fused_qkv = bool(fused_qkv)
+        self._plan(mode, y_req, host_override)
+        self._allocate(weights)
+        self._kv_pools(cfg.n_kv_heads, cfg.head_dim)
+        self._layer_setup()
+
+    def _model_desc(self):
+        c = self.cfg
+        return dak.model(dak.MODEL_OPT, c.n_layers, c.hidden, c.n_heads, c.n_kv_heads, c.head_dim, c.ffn, c.vocab,
+                         tp_size=1, fused_qkv=int(self.fused_qkv), fused_gate_up=0, include_head=1)
+
+    def kv_bytes_per_layer(self) -> int:
+        c = self.cfg
+        return 2 * c.n_kv_heads * c.head_dim * 2 * self.B * self.context
 
     def _allocate(self, weights):
         c = self.cfg
@@ -227,48 +346,8 @@ class DakOPT:
         self.lnf_b = weights["lnf_b"] if weights else torch.zeros(c.hidden, dtype=torch.bfloat16, device=dev)
         torch.cuda.synchronize()
 
-    # ------------------------------------------------------------------ KV cache (paged)
-    def _kv(self):
+    def _layer_setup(self):
         c, B = self.cfg, self.B
-        ppr, cp = self.pages_per_req, self.chunk_pages
-        page_elems = c.n_kv_heads * self.page * c.head_dim
-        self.block_tables, self.kv = [], []
-        # host chunks are the op's leading units in chunk-major order: the oldest chunks first
-        for l in range(c.n_layers):
-            hu = self.attn_host_chunks[l]
-            host_pages = []
-            for b in range(B):
-                n_chunks_b = hu // B + (1 if b < hu % B else 0)
-                host_pages.append(min(ppr, n_chunks_b * cp))
-            Ph = sum(host_pages)
-            Pg = B * ppr - Ph
-            bt = np.zeros((B, ppr), dtype=np.int64)
-            ih = ig = 0
-            for b in range(B):
-                for p in range(ppr):
-                    if p < host_pages[b]:
-                        bt[b, p] = ih | 0x80000000
-                        ih += 1
-                    else:
-                        bt[b, p] = ig
-                        ig += 1
-            kg = torch.zeros(max(Pg, 1) * page_elems, dtype=torch.bfloat16, device="cuda")
-            vg = torch.zeros_like(kg)
-            kh = self._alloc_host(max(Ph, 1) * page_elems * 2)
-            vh = self._alloc_host(max(Ph, 1) * page_elems * 2)
-            self.kv.append((kg, vg, kh, vh, Ph, Pg))
-            self.block_tables.append(torch.from_numpy((bt & 0xFFFFFFFF).astype(np.uint32).view(np.int32)).cuda())
-        # zero the host pools (finite slots beyond seq_len, dak.h) and fill prompt KV with noise
-        for (kg, vg, kh, vh, Ph, Pg) in self.kv:
-            n = max(Ph, 1) * page_elems
-            for hp in (kh, vh):
-                arr = (np.ctypeslib.as_array((__import__("ctypes").c_uint16 * n).from_address(hp[0])))
-                arr[:] = 0
-            kg.copy_(_bf16_rand(kg.shape, 1.0, self.gen))
-            vg.copy_(_bf16_rand(vg.shape, 1.0, self.gen))
-        self.positions = torch.full((B,), self.context - 1, dtype=torch.int32, device="cuda")
-        self.seq_lens = self.positions + 1
-        self.tokens = torch.zeros((B,), dtype=torch.int32, device="cuda")
         self.x = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
         self.h = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
         self.logits = torch.empty((B, c.vocab), dtype=torch.bfloat16, device="cuda")
@@ -289,28 +368,7 @@ class DakOPT:
     def load_kv(self, K_cache, V_cache):
         """Place a given cache: K_cache[l][b] = [L_b, Hkv, d] bf16 bits (numpy) of the tokens before
         the current position, written into the tier pools named by the block table (DAK-PG)."""
-        c = self.cfg
-        d, Hkv, page = c.head_dim, c.n_kv_heads, self.page
-        for l, (kg, vg, kh, vh, Ph, Pg) in enumerate(self.kv):
-            bt = self.block_tables[l].cpu().numpy().view(np.uint32)
-            pools = {}
-            for name, src in (("k", K_cache[l]), ("v", V_cache[l])):
-                lg = np.zeros((max(Pg, 1), Hkv, page, d), np.uint16)
-                lh = np.zeros((max(Ph, 1), Hkv, page, d), np.uint16)
-                for b in range(self.B):
-                    arr = np.asarray(src[b])
-                    for t0 in range(0, arr.shape[0], page):
-                        e = int(bt[b, t0 // page])
-                        pool = lh if e & 0x80000000 else lg
-                        blk = arr[t0:t0 + page]
-                        pool[e & 0x7FFFFFFF, :, :blk.shape[0]] = blk.transpose(1, 0, 2)
-                pools[name] = (lg, lh)
-            for (lg, lh), dg, dh in ((pools["k"], kg, kh), (pools["v"], vg, vh)):
-                tg = torch.from_numpy(lg.view(np.int16)).cuda()
-                th = torch.from_numpy(lh.view(np.int16)).cuda()
-                dak.pack_kv_pages(tg, lg.shape[0] * Hkv, page, d, dg)
-                dak.pack_kv_pages(th, lh.shape[0] * Hkv, page, d, dh[1])
-                torch.cuda.synchronize()
+        self._load_kv(K_cache, V_cache, self.cfg.n_kv_heads, self.cfg.head_dim)
 
     def _layer_args(self, l):
         c, L = self.cfg, self.layers[l]
@@ -335,10 +393,7 @@ class DakOPT:
         a.page_size, a.max_pages, a.chunk_pages = self.page, self.pages_per_req, self.chunk_pages
         a.tp_rank, a.tp_size = 0, 1
         a.cfg = dak.launch_cfg(**self.launch)
-        # attention host CTAs: ~one per 8 host units (units = chunks x kv heads; one unit per warp)
-        n_kvh = getattr(self, "dims", {}).get("n_kv", None) or c.n_kv_heads
-        host_units = self.attn_host_chunks[l] * n_kvh
-        a.attn_cfg = dak.launch_cfg(**dict(self.launch, n_cta_host=dak.attention_host_ctas(host_units)))
+        a.attn_cfg = dak.launch_cfg(**self.attn_launch)
         # L2 warm-up chain (dak.h): the last linear of layer l warms the next layer's q (or the head)
         nxt = self.layers[l + 1]["qkv" if self.fused_qkv else "q"] if l + 1 < c.n_layers else self.head
         a.l2_prefetch_bytes = self.l2_prefetch
@@ -346,162 +401,24 @@ class DakOPT:
             a.next_w_hbm, a.next_w_hbm_bytes = nxt.hbm.data_ptr(), (nxt.M - nxt.h) * nxt.K * 2
         return a
 
-    # ------------------------------------------------------------------ persistent step program
-    def build_step_program(self):
-        """Op table of one decode step for dak_step (embed, then per layer LN1, QKV(+KV append),
-        attention[, combine], O(+residual, LN stats), LN2, FC1, FC2(+residual, LN stats), then
-        LN_f and the LM head)."""
-        c, B, dev = self.cfg, self.B, "cuda"
-        H, F = c.hidden, c.ffn
-        G = self.sms
-        qkv_cols = (c.n_heads + 2 * c.n_kv_heads) * c.head_dim
-        self.sp_h = torch.empty((B, H), dtype=torch.bfloat16, device=dev)
-        self.sp_qkv = torch.empty((B, qkv_cols), dtype=torch.bfloat16, device=dev)
-        self.sp_attn = torch.empty((B, c.n_heads * c.head_dim), dtype=torch.bfloat16, device=dev)
-        self.sp_f = torch.empty((B, F), dtype=torch.bfloat16, device=dev)
-        self.sp_stats = [torch.zeros((G, B, 2), dtype=torch.float32, device=dev) for _ in range(2)]
-        max_chunks = self.chunks_per_req
-        multi = max_chunks > 1
-        n_units = B * c.n_kv_heads * max_chunks
-        self.sp_part_o = torch.empty(max(1, n_units * (c.n_heads // c.n_kv_heads) * c.head_dim), dtype=torch.float32,
-                                     device=dev)
-        self.sp_part_lse = torch.empty(max(1, n_units * (c.n_heads // c.n_kv_heads)), dtype=torch.float32, device=dev)
-        self.sp_units = []
-        ops = []
-
-        def add(**kw):
-            ops.append(dak.step_op(**kw))
-            return len(ops) - 1
-
-        def lin(op: LinearOp, x, y, dep, **kw):
-            return add(type=dak.STEP_LINEAR, dep=dep, w_host=op.host[1] if op.host else None, w_hbm=op.hbm, M=op.M,
-                       K=op.K, h=op.h, kc=op.kc, x=x, y=y, bias=op.bias, **kw)
-
-        prev = add(type=dak.STEP_EMBED, y=self.x, cols=H, tokens=self.tokens, positions=self.positions,
-                   tok_emb=self.tok_emb, pos_emb=self.pos_emb, pos_offset=2, stats_out=self.sp_stats[0])
-        for l, L in enumerate(self.layers):
-            kg, vg, kh, vh, Ph, Pg = self.kv[l]
-            bt = self.block_tables[l].cpu().numpy().view(np.uint32)
-            uh, ug = [], []
-            for b in range(B):
-                for ch in range(max_chunks):
-                    p0 = ch * self.chunk_pages
-                    if p0 >= self.pages_per_req:
-                        continue
-                    (uh if bt[b, p0] & 0x80000000 else ug).append(b * max_chunks + ch)
-            th = torch.tensor(uh or [0], dtype=torch.int32, device=dev)
-            tg = torch.tensor(ug or [0], dtype=torch.int32, device=dev)
-            self.sp_units += [th, tg]
-            ln1 = add(type=dak.STEP_LAYERNORM, dep=prev, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[0],
-                      ln_w=L["ln1_w"], ln_b=L["ln1_b"], eps=1e-5)
-            kv = dict(k_hbm=kg, v_hbm=vg, k_host=kh[1], v_host=vh[1], block_table=self.block_tables[l],
-                      seq_lens=self.seq_lens, positions=self.positions, Hq=c.n_heads, Hkv=c.n_kv_heads, d=c.head_dim,
-                      page_size=self.page, max_pages=self.pages_per_req, chunk_pages=self.chunk_pages)
-            # q, k, v read the same LN1 output: no barrier between them; k / v epilogues append
-            # the new token to the KV pools; attention depends on v (in-order completion per CTA
-            # makes "every CTA finished v" imply q and k finished too)
-            base = self.sp_qkv.data_ptr()
-            hq = c.n_heads * c.head_dim
-            hkv = c.n_kv_heads * c.head_dim
-            lin(L["q"], self.sp_h, base, ln1, ldy=qkv_cols)
-            lin(L["k"], self.sp_h, base + hq * 2, ln1, ldy=qkv_cols, kv_row0=0, kv_kind=1, **kv)
-            qkv = lin(L["v"], self.sp_h, base + (hq + hkv) * 2, ln1, ldy=qkv_cols, kv_row0=0, kv_kind=2, **kv)
-            att = add(type=dak.STEP_ATTENTION, dep=qkv, q=self.sp_qkv, q_stride=qkv_cols, out=self.sp_attn,
-                      units_host=th, units_hbm=tg, n_units_host=len(uh), n_units_hbm=len(ug),
-                      part_o=self.sp_part_o, part_lse=self.sp_part_lse, **kv)
-            if multi:
-                att = add(type=dak.STEP_COMBINE, dep=att, out=self.sp_attn, cols=B, part_o=self.sp_part_o,
-                          part_lse=self.sp_part_lse, **kv)
-            o = lin(L["o"], self.sp_attn, self.x, att, residual=self.x, stats_out=self.sp_stats[1])
-            ln2 = add(type=dak.STEP_LAYERNORM, dep=o, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[1],
-                      ln_w=L["ln2_w"], ln_b=L["ln2_b"], eps=1e-5)
-            f1 = lin(L["up"], self.sp_h, self.sp_f, ln2, act=dak.ACT_RELU)
-            prev = lin(L["down"], self.sp_f, self.x, f1, residual=self.x, stats_out=self.sp_stats[0])
-        lnf = add(type=dak.STEP_LAYERNORM, dep=prev, x=self.x, y=self.sp_h, cols=H, stats_in=self.sp_stats[0],
-                  ln_w=self.lnf_w, ln_b=self.lnf_b, eps=1e-5)
-        lin(self.head, self.sp_h, self.logits, lnf)
-        self.step_ops = ops
-        self.step_plan, self.step_buf = dak.step_compile(ops, B, cfg=self.launch)
-        return self.step_plan
-
     # ------------------------------------------------------------------ the decode step (hot path)
     def enqueue_step(self, stream=None):
-        if getattr(self, "use_step", False):
-            dak.step_launch(self.step_plan, stream)
-            return
         c = self.cfg
         dak.embed(self.tokens, self.positions, self.tok_emb, self.pos_emb, self.B, c.hidden, 2, self.x,
                   pdl=self.pdl, stream=stream, stats_out=self.stats if self.fuse_norm else None)
         for a in self.layer_args:
             dak.layer(a, stream)
-        hw = self.head.host[1] if self.head.host else None
         if self.fuse_norm:  # LN_f fused into the LM head
-            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
-                                 self.x, self.logits, cfg=self.launch, ln_w=self.lnf_w, ln_b=self.lnf_b,
-                                 ln_stats=self.stats, ln_parts=self.head_stats_parts, ln_eps=1e-5)
+            ha = self._head_args(self.x, self.logits, ln_w=self.lnf_w, ln_b=self.lnf_b, ln_stats=self.stats,
+                                 ln_parts=self.head_stats_parts, ln_eps=1e-5)
         else:
             dak.layernorm(self.x, self.lnf_w, self.lnf_b, self.h, self.B, c.hidden, 1e-5, pdl=self.pdl, stream=stream)
-            ha = dak.linear_args(hw, self.head.hbm, self.head.M, self.head.K, self.head.h, self.head.kc, self.B,
-                                 self.h, self.logits, cfg=self.launch)
-        if self.B > 16:  # tcgen05 split-K partials for the head
-            need = dak.linear_workspace_size(ha)
-            if need:
-                if getattr(self, "head_ws", None) is None or self.head_ws.numel() < need:
-                    self.head_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
-                ha.workspace, ha.workspace_bytes = self.head_ws.data_ptr(), self.head_ws.numel()
+            ha = self._head_args(self.h, self.logits)
         dak.linear(ha, stream)
 
-    def advance(self, stream=None):
-        """Move every request to the next position (after a step appended its token's KV)."""
-        if int(self.positions.max()) + 1 >= self.max_context:
-            raise ValueError("decode past max_context")
-        with torch.cuda.stream(stream or torch.cuda.current_stream()):
-            self.positions.add_(1)
-            self.seq_lens.add_(1)
-
     def kernels_per_step(self) -> int:
-        if getattr(self, "use_step", False):
-            return 1
         # [q k v | qkv] attn(+ fused KV append) [combine] o fc1 fc2
         per_layer = (5 if self.fused_qkv else 7) + (1 if self.chunks_per_req > 1 else 0)
         if self.fuse_norm:
             return 1 + per_layer * self.cfg.n_layers + 1
         return 1 + (per_layer + 2) * self.cfg.n_layers + 2
-
-    def enable_persistent_step(self):
-        if self.fused_qkv:
-            raise ValueError("the persistent step program uses separate q/k/v projections: fused_qkv=False")
-        self.build_step_program()
-        self.use_step = True
-
-    def capture(self, stream: torch.cuda.Stream):
-        with torch.cuda.stream(stream):
-            self.enqueue_step(stream)  # warm (sets function attributes outside capture)
-            stream.synchronize()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                self.enqueue_step(stream)
-        self.graph = g
-        return g
-
-    def bytes_per_step(self) -> dict:
-        """Algorithmic bytes read per decode step, split by tier (weights + KV)."""
-        hbm = host = 0
-        for op in self.linear_ops():
-            hbm += (op.M - op.h) * op.K * 2
-            host += op.h * op.K * 2
-        c = self.cfg
-        tok = 2 * c.n_kv_heads * c.head_dim * 2
-        for (kg, vg, kh, vh, Ph, Pg) in self.kv:
-            hp = min(Ph * self.page, self.B * self.context)
-            host += tok * min(Ph * self.page, self.B * self.context)
-            hbm += tok * (self.B * self.context - hp)
-        return dict(hbm=hbm, host=host, total=hbm + host)
-
-    def close(self):
-        for hp in self._host_blocks:
-            try:
-                dak.host_free(hp)
-            except Exception:
-                pass
-        self._host_blocks = []

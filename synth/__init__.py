@@ -67,10 +67,24 @@ def kv_inputs(n_tokens_per_req, Hkv: int, d: int, Hq: int, seed: int, kind: str 
     """Logical per-request K, V [L_b, Hkv, d] and queries q [B, Hq, d] as bf16 bits."""
     g = rng(seed)
     B = len(n_tokens_per_req)
-    draw = normal_bf16 if kind == "normal" else int_bf16
-    q = draw(g, (B, Hq, d))
+    draw = int_bf16 if kind == "int" else normal_bf16
+    # score-range variants (parity of the online softmax's rescaling and the combine's max
+    # tracking): "wide" draws q with std 40 (scores ~ N(0, 40^2) after the 1/sqrt(d) scale);
+    # "constk" repeats one key row over every token (softmax uniform: o = mean V); "dominant"
+    # puts a key of +-3 signs matching q's first head at a random token of every request, with q
+    # std 4 (that key's score exceeds the others by ~100)
+    q = draw(g, (B, Hq, d)) if kind == "int" else normal_bf16(
+        g, (B, Hq, d), 40.0 if kind == "wide" else (4.0 if kind == "dominant" else 1.0))
     K = [draw(g, (int(L), Hkv, d)) for L in n_tokens_per_req]
     V = [draw(g, (int(L), Hkv, d)) for L in n_tokens_per_req]
+    if kind == "constk":
+        K = [np.repeat(k[:1], k.shape[0], axis=0) for k in K]
+    elif kind == "dominant":
+        qf = (q.astype(np.uint32) << 16).view(np.float32)
+        for b, k in enumerate(K):
+            t = int(g.integers(0, k.shape[0]))
+            for j in range(Hkv):
+                k[t, j] = bf16_bits(np.where(qf[b, j * (Hq // Hkv)] >= 0, 3.0, -3.0).astype(np.float32))
     return q, K, V
 
 

@@ -139,3 +139,18 @@ class PagedKV:
         self.bt = torch.from_numpy(bt.copy()).cuda()
         self.page = page
         torch.cuda.synchronize()
+
+
+def assert_bf16_ulps(got: np.ndarray, ref: np.ndarray, ulps: int = 1, floor: float = 0.0):
+    """Per element: |g - r| <= ulps * ulp_bf16(r) (+ floor). ref is the float64 oracle value already
+    rounded to bf16; a kernel computing in fp32 may land one bf16 ulp away at a rounding boundary."""
+    got = np.asarray(got, dtype=np.float64)
+    ref = np.asarray(ref, dtype=np.float64)
+    assert got.shape == ref.shape and np.all(np.isfinite(got))
+    mag = np.maximum(np.abs(ref), 2.0 ** -126)
+    ulp = 2.0 ** (np.floor(np.log2(mag)) - 7)
+    err = np.abs(got - ref)
+    bad = err > ulps * ulp + floor
+    if bad.any():
+        i = np.unravel_index(np.argmax(err - ulps * ulp), err.shape)
+        raise AssertionError(f"{bad.sum()} / {bad.size} elements beyond {ulps} bf16 ulp; worst at {i}: got {got[i]} ref {ref[i]}")

@@ -156,3 +156,113 @@ def test_default_kc(D):
     kc = D.default_kc(28672, 7168, 147)
     assert kc == 64 and 7168 % kc == 0
     assert D.default_kc(7168, 28672, 147) == 256
+
+
+# ------------------------------------------------------------------ a1 / a2 / a4 in the library vs the oracle
+def test_global_offload_bytes_vs_oracle_and_fig8(D):
+    """dak_global_offload_bytes (a1) against the oracle's exact-Fraction definition, on the paper's
+    Fig. 8 capacity runs (golden) and random sizes; ECAPACITY on host overflow."""
+    import json
+    from fractions import Fraction
+    from oracle import planner as P
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "fig8_footprint.json")))
+    m = D.model(D.MODEL_OPT, 48, 7168, 56, 56, 128, 28672, 50272)  # OPT-30B (P:L690)
+    for row in gold["rows"]:
+        # the library's own KV accounting (dak_decode_ops attention C_i over 48 layers) feeds a1
+        ops = D.decode_ops(m, row["bsz"], row["prompt"] + gold["decode_len"], 16, 1024, 1e15, 1e15)
+        kv = sum(o["total_bytes"] for o in ops if o["role"] == "attn")
+        assert round(kv / 1e9, 2) == pytest.approx(row["kv_gb"], abs=0.006)
+        w, hbm = int(gold["model_bytes"]), int(gold["hbm_bytes"])  # the paper's 55.6 GB override (R12)
+        y, r = D.global_offload_bytes(w, kv, hbm)
+        R = P.global_offload_ratio(w, kv, hbm)
+        assert y == max(0, w + kv - hbm) and r == float(R)
+        assert abs(100 * r - row["ratio_pct"]) < 0.5
+    g = np.random.default_rng(8)
+    for _ in range(500):
+        w, kv, hbm = (int(v) for v in g.integers(0, 1 << 40, 3))
+        y, r = D.global_offload_bytes(w, kv, hbm)
+        R = P.global_offload_ratio(w, kv, hbm)
+        assert Fraction(y) == max(Fraction(0), Fraction(w + kv - hbm)) and r == float(R)
+    with pytest.raises(D.DakError) as e:
+        D.global_offload_bytes(100, 50, 60, host_capacity_bytes=89)
+    assert e.value.code == "ECAPACITY"
+    with pytest.raises(P.PlanError):
+        P.global_offload_ratio(100, 50, 60, host_capacity=89)
+    assert D.global_offload_bytes(100, 50, 60, host_capacity_bytes=90) == (90, 0.6)
+
+
+@pytest.mark.parametrize("name,tp,B,ctx,fq,fgu,chunk", [("OPT_30B", 1, 8, 64, 1, 0, 64), ("OPT_30B", 1, 1, 2048, 0, 0, 1024),
+                                                       ("LLAMA3_70B", 8, 64, 65536, 1, 1, 1024),
+                                                       ("LLAMA3_70B", 8, 64, 4096, 0, 0, 256),
+                                                       ("LLAMA3_70B", 1, 3, 1000, 1, 0, 384)])
+def test_decode_ops_bit_exact_vs_oracle(D, name, tp, B, ctx, fq, fgu, chunk):
+    """dak_decode_ops (a2) equals oracle/models.py decode_ops field by field, bitwise for the
+    doubles (FLOPs, T): op order, C_i, units, unit bytes, shapes."""
+    from oracle import models
+    mod = getattr(models, name)
+    fam = D.MODEL_OPT if mod["family"] == "opt" else D.MODEL_LLAMA
+    m = D.model(fam, mod["n_layers"], mod["hidden"], mod["n_heads"], mod["n_kv_heads"], mod["head_dim"], mod["ffn"],
+                mod["vocab"], tp_size=tp, fused_qkv=fq, fused_gate_up=fgu)
+    got = D.decode_ops(m, B, ctx, 16, chunk, 1.3554e15, 0.9e15)
+    ref = models.decode_ops(mod, B, ctx, 1.3554e15, 0.9e15, tp=tp, unit_rows=16, chunk_tokens=chunk,
+                            fused_qkv=bool(fq), fused_gate_up=bool(fgu))
+    assert len(got) == len(ref)
+    for g_, r_ in zip(got, ref):
+        assert g_["kind"] == (0 if r_["kind"] == "linear" else 1)
+        assert g_["layer"] == r_["layer"] and models.ROLE[g_["role"]] == r_["role"]
+        for f in ("n_units", "unit_bytes", "total_bytes", "M", "K"):
+            assert g_[f] == r_[f], f
+        assert g_["T"] == r_["T"] and g_["flops"] == r_["flops"]  # bitwise double equality
+
+
+def test_decode_ops_errors(D):
+    m = D.model(D.MODEL_LLAMA, 2, 8192, 64, 8, 128, 28672, 128256, tp_size=16)
+    with pytest.raises(D.DakError):
+        D.decode_ops(m, 1, 10, 16, 64, 1e15, 1e15)  # 8 kv heads not divisible by 16
+    m = D.model(D.MODEL_OPT, 2, 256, 2, 2, 128, 512, 100)
+    with pytest.raises(D.DakError):
+        D.decode_ops(m, 0, 10, 16, 64, 1e15, 1e15)
+
+
+def test_kv_place_bit_exact_vs_oracle(D):
+    """dak_kv_place (a4, attention) equals oracle/partition.py kv_place_chunk_major bit for bit on
+    random ragged batches; host pages are a per-request prefix; host tokens add up."""
+    from oracle import partition as Pt
+    g = np.random.default_rng(31)
+    for trial in range(400):
+        B = int(g.integers(1, 9))
+        page = int(g.choice([16, 32, 64]))
+        cp = int(g.integers(1, 5))
+        sl = [int(g.integers(0, 700)) for _ in range(B)]
+        max_pages = max(1, max(-(-L // page) for L in sl)) + int(g.integers(0, 3))
+        n_chunks = sum(-(-(-(-L // page)) // cp) for L in sl)
+        hu = int(g.integers(0, n_chunks + 1))
+        bt, nh, ng, ht = D.kv_place(sl, page, max_pages, cp, hu)
+        rt, rh, rg, rtok = Pt.kv_place_chunk_major(sl, page, max_pages, cp, hu)
+        assert np.array_equal(bt.view(np.uint32), np.array(rt, dtype=np.uint32)), trial
+        assert (nh, ng, ht) == (rh, rg, rtok)
+        assert nh + ng == B * max_pages
+        for b in range(B):  # host pages form a prefix of every request
+            host = (bt[b].view(np.uint32) & 0x80000000) != 0
+            assert not np.any(host[1:] & ~host[:-1])
+    with pytest.raises(D.DakError):
+        D.kv_place([64, 64], 64, 1, 1, 3)  # 3 host units > 2 chunks
+
+
+def test_kv_place_matches_planned_bytes_when_chunks_are_full(D):
+    """With contexts that fill whole chunks, the placed host bytes equal the planner's host bytes
+    for the attention op exactly (units are then uniform: reading R15's mean unit is exact)."""
+    m = D.model(D.MODEL_OPT, 1, 7168, 56, 56, 128, 28672, 50272, fused_qkv=1)
+    B, ctx, page, cp = 8, 2048, 64, 4
+    ops = D.decode_ops(m, B, ctx, 16, cp * page, 1.3554e15, 1.3554e15)
+    att = [o for o in ops if o["role"] == "attn"][0]
+    tok = 2 * 56 * 128 * 2
+    for hu in (0, 1, 7, 8, 9, 40, att["n_units"]):
+        _, _, _, ht = D.kv_place([ctx] * B, page, ctx // page, cp, hu)
+        assert ht * tok == min(hu * att["unit_bytes"], att["total_bytes"])
+
+
+def test_numa_query_needs_device(D):
+    with pytest.raises(D.DakError) as e:
+        D.device_numa_node()
+    assert e.value.code == "ECUDA"

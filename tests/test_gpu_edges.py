@@ -52,8 +52,23 @@ def test_linear_tiny_and_ragged(D, torch, M, K, N, h, kc, path):
 @pytest.mark.parametrize("Ls,frac,cp", [([1], 0.0, 1), ([1, 2, 3], 1.0, 1), ([64], 1.0, 1), ([65, 1], 0.5, 1),
                                         ([700], 0.5, 4), ([16, 4000], 0.25, 16)])
 def test_attention_edges(D, torch, Ls, frac, cp):
+    from tests.gpu_util import assert_close
     from tests.test_gpu_attention import run_attn
-    run_attn(D, torch, Ls, 2, 16, 64, cp, frac, seed=sum(Ls) + cp)
+    got, ref, _ = run_attn(D, torch, Ls, 2, 16, 64, cp, frac, seed=sum(Ls) + cp)
+    assert_close(Kx.bf16_to_f64(got), ref)
+
+
+@pytest.mark.parametrize("kind", ["wide", "constk", "dominant"])
+@pytest.mark.parametrize("Ls,frac,cp", [([1, 90, 700], 0.5, 2), ([4000, 33], 0.25, 4)])
+def test_attention_score_ranges(D, torch, kind, Ls, frac, cp):
+    """Large / peaked / flat score distributions (synth.kv_inputs kinds): scores spanning +-100
+    exercise the online-softmax rescaling inside a unit and the combine's running max across
+    split-KV chunks; constant K makes every weight equal (o = mean V); one dominant key makes
+    o ~ V of that token. Same per-element tolerance as every parity test."""
+    from tests.gpu_util import assert_close
+    from tests.test_gpu_attention import run_attn
+    got, ref, _ = run_attn(D, torch, Ls, 2, 16, 64, cp, frac, seed=5 + sum(Ls), kind=kind)
+    assert_close(Kx.bf16_to_f64(got), ref)
 
 
 def test_linear_errors(D, torch):

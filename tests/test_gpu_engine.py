@@ -30,10 +30,9 @@ def _engine_weights(p, L, torch):
     return w
 
 
-@pytest.mark.parametrize("persistent,fuse,fused_qkv", [(False, True, True), (False, True, False), (False, False, True),
-                                                      (True, True, False)])
+@pytest.mark.parametrize("fuse,fused_qkv", [(True, True), (True, False), (False, True)])
 @pytest.mark.parametrize("frac,B,ctx", [(0.0, 3, 70), (0.2, 3, 70), (0.5, 2, 200)])
-def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse, fused_qkv):
+def test_engine_step_matches_oracle(frac, B, ctx, fuse, fused_qkv):
     import torch
     from paper_2604_26074_b200 import dak
     from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
@@ -50,8 +49,6 @@ def test_engine_step_matches_oracle(frac, B, ctx, persistent, fuse, fused_qkv):
     Kc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
     Vc = [[synth.normal_bf16(g, (ctx - 1, heads, H // heads)) for _ in range(B)] for _ in range(L)]
     eng.load_kv(Kc, Vc)
-    if persistent:
-        eng.enable_persistent_step()
     tokens = np.arange(B) * 37 + 5
     eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
     s = torch.cuda.Stream()
@@ -102,4 +99,47 @@ def test_engine_multistep_decode_matches_oracle(frac):
     from tests.gpu_util import assert_close
     for s in range(steps):
         assert_close(got[s], ref[s], rtol=3e-2)
+    eng.close()
+
+
+@pytest.mark.parametrize("fused_qkv,ctx,max_ctx,frac", [(True, 70, None, 0.3), (False, 63, 67, 0.3), (True, 200, 260, 0.6)])
+def test_engine_plan_and_placement_match_oracle(fused_qkv, ctx, max_ctx, frac):
+    """The engine's op list (dak_decode_ops), ratios (dak_plan_ratios) and KV placement
+    (dak_kv_place) equal the oracle's definitions bit for bit; the placed host bytes of every
+    attention op equal the planned ones up to the short last chunk of each request (reading R15),
+    and the step's host-byte accounting is what was placed."""
+    import torch
+    from oracle import models, partition as Pt, planner as P
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
+    L, H, F, V, heads, maxpos, B = 2, 256, 512, 1000, 2, 256, 3
+    cfg = OPTConfig(n_layers=L, hidden=H, n_heads=heads, ffn=F, vocab=V, max_pos=maxpos, name="opt-tiny")
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    mod = dict(models.OPT_30B, n_layers=L, hidden=H, n_heads=heads, n_kv_heads=heads, head_dim=H // heads, ffn=F,
+               vocab=V)
+    total = sum(o["total_bytes"] for o in models.decode_ops(mod, B, ctx, 1, 1))
+    y = int(frac * total)
+    eng = DakOPT(cfg, B, ctx, hw, mode=dak.PLAN_EXACT, y_req=y, page_size=64, chunk_pages=1, fused_qkv=fused_qkv,
+                 max_context=max_ctx)
+    ref_ops = models.decode_ops(mod, B, ctx, hw.peak_flops, hw.peak_flops, unit_rows=16, chunk_tokens=64,
+                                fused_qkv=fused_qkv)
+    assert len(eng.plan_ops) == len(ref_ops)
+    for g_, r_ in zip(eng.plan_ops, ref_ops):
+        for f in ("n_units", "unit_bytes", "total_bytes", "M", "K", "T"):
+            assert g_[f] == r_[f]
+    ref_plan = P.plan_units(ref_ops, hw.hbm_bps, hw.link_bps, y, dak.PLAN_EXACT)
+    assert [p["host_units"] for p in eng.plan] == ref_plan["host_units"]
+    att = [i for i, o in enumerate(ref_ops) if o["kind"] == "attention"]
+    tok = 2 * heads * (H // heads) * 2
+    for l, i in enumerate(att):
+        hu = ref_plan["host_units"][i]
+        rt, rh, rg, rtok = Pt.kv_place_chunk_major([ctx] * B, 64, eng.pages_per_req, 1, hu)
+        assert np.array_equal(eng.block_tables[l].cpu().numpy().view(np.uint32), np.array(rt, dtype=np.uint32))
+        assert eng.kv_host_tokens[l] == rtok and eng.kv[l][4] == rh
+        planned = ref_plan["host_bytes"][i]
+        assert abs(rtok * tok - planned) <= B * 64 * tok  # within one chunk per request (short last chunks)
+    nb = eng.bytes_per_step()
+    lin_host = sum(op.h * op.K * 2 for op in eng.linear_ops())
+    assert nb["host"] == lin_host + tok * sum(eng.kv_host_tokens)
+    assert nb["total"] == sum(o["total_bytes"] for o in ref_ops)
     eng.close()

@@ -385,3 +385,80 @@ def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch, fp):
     ref = Kx.split_linear(W[:0], W, x)
     assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(ref))
     assert np.array_equal(outs[1], outs[0]) and np.array_equal(outs[2], outs[0])
+
+
+def _run_cfg(D, torch, W, x, h, kc, **cfg):
+    """Launch with a split-K workspace when the plan asks for one; returns (y bits, launch info)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    M, K = W.shape
+    N = x.shape[0]
+    sl = SplitLinear(D, W, h, kc)
+    xd = to_dev(x)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    a = sl.args(xd, y, N, **cfg)
+    wsb = None
+    if kc == 64 and N > 16:
+        a.workspace, a.workspace_bytes = 256, 1 << 40
+        need = D.linear_workspace_size(a)
+        a.workspace, a.workspace_bytes = None, 0
+        if need:
+            wsb = torch.empty(need, dtype=torch.uint8, device="cuda")
+            a.workspace, a.workspace_bytes = wsb.data_ptr(), need
+    info = D.linear_query(a)
+    D.linear(a)
+    torch.cuda.synchronize()
+    return from_dev(y), info
+
+
+@pytest.mark.parametrize("M,K,N,h,kc", [(3000, 4096, 2, 400, 512), (3000, 4096, 8, 400, 256), (2048, 2048, 48, 512, 64),
+                                        (7168, 8192, 64, 1024, 64)])
+def test_linear_congestion_knobs_bitwise(D, torch, M, K, N, h, kc):
+    """Congestion control is a performance mechanism only: the host window W, the
+    host-CTA count, cc on / off, the HBM ring depth -- and, on split-K plans, the host-item gate --
+    never change a bit of the output (FMA path at N = 2 is forced below; mma.sync at N = 8;
+    tcgen05 at N = 48; tcgen05 split-K (swapped) at N = 64 with many host items)."""
+    from tests.gpu_util import assert_close
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(30, M + N))
+    fp = dict(force_path=1) if N <= 4 else {}
+    base, info0 = _run_cfg(D, torch, W, x, h, kc, congestion_control=0, **fp)
+    assert_close(Kx.bf16_to_f64(base), Kx.linear(W, x))
+    gates = set()
+    for knobs in (dict(congestion_control=1), dict(congestion_control=1, window=1), dict(congestion_control=1, window=3),
+                  dict(congestion_control=1, n_cta_host=1), dict(congestion_control=1, n_cta_host=4),
+                  dict(congestion_control=0, window=2, stages=3), dict(congestion_control=1, stages=2)):
+        got, info = _run_cfg(D, torch, W, x, h, kc, **knobs, **fp)
+        gates.add(info["host_gate"])
+        assert np.array_equal(got, base), knobs
+    if info0["ksplit"] > 1:  # the split-K host gate was active in some of the runs
+        assert max(gates) >= 1
+
+
+@pytest.mark.parametrize("M,K,N", [(28672, 7168, 32), (7168, 8192, 64)])
+def test_linear_large_m_r_invariance_bitwise(D, torch, M, K, N):
+    """tcgen05 at batch > 16: whether K is split is decided from (M, K, SM count) only, so the
+    summation order of a row never depends on the tier split h (OPT fc1 shape: no split at any h;
+    Llama TP8 o shape: split at every h) -- outputs bitwise equal for h in {0, 64, 1024, M/2}."""
+    W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(31, M + N), kind="int")
+    outs, splits = [], set()
+    for h in (0, 64, 1024, M // 2):
+        y, info = _run_cfg(D, torch, W, x, h, 64)
+        outs.append(y)
+        splits.add(info["ksplit"])
+    assert len(splits) == 1
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(Kx.linear(W, x)))
+
+
+@pytest.mark.parametrize("M,K,N,h", [(7168, 8192, 64, 1024), (1280, 4096, 32, 128)])
+def test_linear_cta_rows_split_k_match_oracle(D, torch, M, K, N, h):
+    """dak_linear_cta_rows on split-K plans: CTA j of a tier owns K split j % S of that tier's
+    128-row block j // S (the oracle's rule, oracle/partition.py linear_splitk_items)."""
+    from oracle import partition as Pt
+    a = D.linear_args(16, 16, M, K, h, 64, N, 16, 16)
+    a.workspace, a.workspace_bytes = 256, 1 << 40
+    info = D.linear_query(a)
+    assert info["ksplit"] > 1
+    ref = Pt.linear_splitk_items(M, h, info["ksplit"], 128)
+    got = [D.linear_cta_rows(a, c) for c in range(info["grid"])]
+    assert got == ref

@@ -5,7 +5,7 @@ sys.path.insert(0, "/root/repo")
 from tools.bench_linear import time_cfg
 from paper_2604_26074_b200 import dak
 for (M, K) in ((28672, 7168), (21504, 7168), (7168, 28672), (7168, 7168)):
-    kc = dak.step_choose_kc(-(-M // 146), K)
+    kc = dak.choose_kc(-(-M // 146), K)
     for ln in ((False, True) if K <= 8192 else (False,)):  # fused pre-norm keeps LN weights resident: K <= 8192
         r = time_cfg(M, K, 8, 0, kc, pdl=1, ln=ln)
         print(json.dumps(dict(M=M, K=K, kc=kc, ln=ln, us=round(r["us"], 2), gbs=round(r["gbs"], 1))), flush=True)

@@ -40,7 +40,7 @@ q = torch.randn(B, Hq, d, device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
 sl = torch.full((B,), L, dtype=torch.int32, device="cuda")
 host_units = B * (hp // cp) * Hkv
-nh = nh_arg or dak.attention_host_ctas(host_units)
+nh = nh_arg or 0  # 0: auto (chosen in-kernel from the block table)
 a = dak.attention_args(q, out, kg, vg, kh[1], vh[1], btd, sl, B, Hq, Hkv, d, page, pages, cp,
                        cfg=dict(pdl=1, congestion_control=1, n_cta_host=nh))
 ws = torch.empty(max(dak.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")

@@ -97,7 +97,7 @@ def c4():
             out = torch.empty_like(q)
             sl = torch.full((B,), L, dtype=torch.int32, device="cuda")
             for cc in ((1, 0) if hp else (1,)):
-                nh = dak.attention_host_ctas(B * host_chunks * Hkv)  # the engine's rule
+                nh = 0  # auto: the library picks the host CTAs from the block table
                 a = dak.attention_args(q, out, kg, vg, kh[1], vh[1], btd, sl, B, Hq, Hkv, d, page, pages, cp,
                                        cfg=dict(pdl=1, congestion_control=cc, n_cta_host=nh))
                 ws = torch.empty(dak.attention_workspace_size(a), dtype=torch.uint8, device="cuda")
