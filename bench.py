@@ -180,6 +180,50 @@ def oracle_sample(batch: int, min_seconds: float = 10.0):
     return nbytes * reps / dt / 1e9, dt, nbytes * reps, threads, reps
 
 
+def in_step_profile(eng, stream, torch, dak, reps: int = 5) -> dict:
+    """Per-kind time inside one decode step (see the roofline block in main)."""
+    import numpy as np
+    n_launch = eng.kernels_per_step() + 16
+    buf = torch.zeros(n_launch * 1024 * 4, dtype=torch.int64, device="cuda")
+    dak.trace_enable(buf, n_launch)
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream), torch.cuda.graph(g, stream=stream):
+            eng.enqueue_step(stream)
+        meta = dak.trace_launches()
+    finally:
+        dak.trace_enable(None, 0)
+    for _ in range(2):
+        g.replay()
+    torch.cuda.synchronize()
+    by_kind, steps = {}, []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(reps):
+        buf.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            g.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        steps.append(e0.elapsed_time(e1) / 1e3)
+        T = buf.view(-1, 1024, 4).cpu().numpy()
+        prev_end = None
+        for i, m in enumerate(meta):
+            st = T[i, :min(m["grid"], 1024)]
+            ok = st[:, 3] > 0
+            if not ok.any():
+                continue
+            end = float(st[ok, 3].max())
+            if prev_end is None:  # the first launch: from its first CTA's start
+                prev_end = float(st[st[:, 0] > 0, 0].min())
+            by_kind[m["kind"]] = by_kind.get(m["kind"], 0.0) + max(0.0, end - prev_end) * 1e-9
+            prev_end = max(prev_end, end)
+    by_kind = {k: v / reps for k, v in by_kind.items()}
+    return dict(linear_s=by_kind.get("linear", 0.0), by_kind_s=by_kind, traced_step_s=float(np.median(steps)),
+                launches=len(meta))
+
+
 def run_reference(a):
     """--impl reference: the CPU oracle on bounded samples of the same workload (rank 0 only)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -353,6 +397,14 @@ def main():
     clocks = sampler.stop()
     t = e0.elapsed_time(e1) / 1e3
     t_max = reduce_max(t, world)
+    # per-rank rates (each GPU reads its own host shard over its own link)
+    mine = dict(rank=rank, ms_per_step=round(t / a.steps * 1e3, 4), host_link_gbs=round(nb["host"] * a.steps / t / 1e9, 2),
+                hbm_gbs=round(nb["hbm"] * a.steps / t / 1e9, 1))
+    per_rank = [mine]
+    if world > 1:
+        import torch.distributed as dist
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
     step_s = t_max / a.steps
     value = nb["total"] * world * a.steps / t_max / 1e9
     reqs = eng.B if llama else eng.B * world  # TP: one batch over all ranks; replicas: one per rank
@@ -377,62 +429,46 @@ def main():
                tokens_per_s=round(reqs * a.steps / te, 2),
                h2d_bytes_per_step=tok_host.numel() * 4, d2h_bytes_per_step=logits_host.numel() * 2)
 
-    # ---------------- roofline of the dominant kernel (dak_linear), CUDA events on its stream
-    lin_bytes, lin_time = 0, 0.0
+    # ---------------- roofline of the dominant kernel (dak_linear), measured INSIDE the step
+    # One step is captured with the library's globaltimer launch trace on (dak_trace_enable) and
+    # replayed; each launch is charged the time it adds to the step's timeline (its last CTA's end
+    # minus the previous launch's last end: with PDL the launches overlap, so this partitions the
+    # step without double counting). dak_linear's share = the sum over its launches, in the exact
+    # variants the step runs (fused pre-norm, SwiGLU operand, residual epilogues, attention between).
+    # The replays are bracketed by CUDA events on the launching stream (traced vs untraced step time).
+    prof = in_step_profile(eng, stream, torch, dak, reps=5)
     ops = list(eng.linear_ops())
-    xs = torch.zeros(eng.B, max(op.K for op in ops), dtype=torch.bfloat16, device="cuda")
-    ys = torch.empty(eng.B, max(op.M for op in ops), dtype=torch.bfloat16, device="cuda")
-    largs = [dak.linear_args(op.host[1] if op.host else None, op.hbm, op.M, op.K, op.h, op.kc, eng.B, xs, ys,
-                             cfg=dict(congestion_control=int(not a.no_cc), pdl=int(not a.no_pdl))) for op in ops]
-    ws_need = max(dak.linear_workspace_size(la) for la in largs)  # tcgen05 split-K partials, as in the step
-    lws = torch.empty(max(ws_need, 16), dtype=torch.uint8, device="cuda")
-    if ws_need:
-        for la in largs:
-            la.workspace, la.workspace_bytes = lws.data_ptr(), lws.numel()
-    # the step's linear launches in step order, chained exactly as in the step (PDL), replayed as one
-    # CUDA graph and bracketed by events on the launching stream: average launch duration = time / n
-    with torch.cuda.stream(stream):
-        for la in largs:
-            dak.linear(la, stream)
-        stream.synchronize()
-        lg = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(lg, stream=stream):
-            for la in largs:
-                dak.linear(la, stream)
-    lg.replay()
-    torch.cuda.synchronize()
-    reps = 5
-    with torch.cuda.stream(stream):
-        e0.record(stream)
-        for _ in range(reps):
-            lg.replay()
-        e1.record(stream)
-    torch.cuda.synchronize()
-    lin_time = e0.elapsed_time(e1) / 1e3 / reps
-    for op in ops:
-        lin_bytes += op.M * op.K * 2 + eng.B * (op.K + op.M) * 2
+    lin_bytes = sum(op.M * op.K * 2 + eng.B * (op.K + op.M) * 2 for op in ops)  # algorithmic, per step
+    lin_time = prof["linear_s"]
     lin_achieved = lin_bytes / lin_time / 1e9
-    lin_share = lin_time / step_s
     peak = hbm_gbs + link_gbs
-    # traffic: DRAM read+write bytes per dak_linear launch of one step from the committed ncu
-    # capture (tools/profile_round.sh -> tools/summarize_profiles.py); algorithmic bytes alongside
-    traffic = None
-    tr_files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "linear_traffic.json")))
+    # traffic: DRAM read+write bytes per dak_linear launch of THIS workload from the committed ncu
+    # capture (profiles/r*/linear_traffic_<workload>.json, tools/summarize_profiles.py)
+    wl_name = wl["workload"] if llama else "opt-30b-decode-b%d-ctx%d" % (eng.B, a.context)
+    traffic, tr_src = None, None
+    tr_files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "linear_traffic_%s.json" % wl_name)))
     if tr_files:
-        traffic = json.load(open(tr_files[-1]))["dram_bytes_per_launch"]
+        tr = json.load(open(tr_files[-1]))
+        traffic, tr_src = tr["dram_bytes_per_launch"], os.path.relpath(tr_files[-1], ROOT)
     roofline = dict(bound="hbm", achieved=round(lin_achieved, 1), peak=round(peak, 1), unit="GB/s",
                     frac=round(lin_achieved / peak, 4), traffic=traffic,
                     algorithmic_bytes_per_launch=round(lin_bytes / len(ops)),
-                    traffic_source=os.path.relpath(tr_files[-1], ROOT) if tr_files else None,
-                    kernel="dak_linear (split GEMV/skinny GEMM): the step's %d linear launches chained with PDL as "
-                           "in the step, graph-replayed, events on the launching stream" % len(ops),
-                    peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json) + measured host link %.1f GB/s" % (peak_src, hbm_gbs, link_gbs),
+                    launches_per_step=len(ops), avg_launch_us=round(lin_time / len(ops) * 1e6, 3),
+                    traffic_source=tr_src,
+                    kernel="dak_linear (split GEMV / skinny GEMM), timed inside the captured decode step: per-launch "
+                           "timeline increments from the library's globaltimer trace, summed over the step's %d "
+                           "linear launches" % len(ops),
+                    peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json hbm_gbs) + measured host link %.1f GB/s"
+                                % (peak_src, hbm_gbs, link_gbs),
                     step_frac=round(value / world / peak, 4),
                     # read-only streams exceed the copy figure: the calibrated bulk-read ring peak
                     # (profiles/r01/calib_loadpath.jsonl, 148 SMs x 4 x 32 KB) as a second denominator
                     read_peak=round(READ_PEAK_GBS + link_gbs, 1),
                     frac_of_read_peak=round(lin_achieved / (READ_PEAK_GBS + link_gbs), 4),
-                    kernel_time_share_of_step=round(lin_share, 4))
+                    kernel_time_share_of_step=round(lin_time / prof["traced_step_s"], 4),
+                    traced_step_ms=round(prof["traced_step_s"] * 1e3, 4),
+                    untraced_step_ms=round(step_s * 1e3, 4),
+                    share_by_kind={k: round(v / prof["traced_step_s"], 4) for k, v in prof["by_kind_s"].items()})
     # the split roofline at the step's host ratio r: EB(r) = 1 / max((1 - r)/B_g, r/B_l),
     # = B_g + B_l at r* and B_l / r above it (a capacity-forced step is link-bound)
     r_step = nb["host"] / nb["total"]
@@ -457,7 +493,7 @@ def main():
                                                    host_latency_us=a.plan_host_latency_us, source=plan_src),
                             execution="per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world)),
-                tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks,
+                tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks, per_rank=per_rank,
                 **({"tokens_per_s_full_model_extrapolated": round(tok_s * cfg.n_layers / 80, 2)}
                    if llama and cfg.n_layers != 80 else {}),
                 gpu_launches=eng.kernels_per_step() * a.steps)

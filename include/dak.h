@@ -55,7 +55,8 @@ dak_status dak_device_sms(int32_t* sms);
  * recorded under CUDA-graph capture stamp on every replay. */
 dak_status dak_trace_enable(void* dev_buf, int32_t max_launches);
 int32_t dak_trace_count(void);
-/* kind: 1 linear (a = M, b = K), 2 attention, 3 combine, 4 KV append, 5 LayerNorm, 6 embed. */
+/* kind: 1 linear (a = M, b = K), 2 attention, 3 combine, 4 KV append, 5 LayerNorm, 6 embed,
+ * 7 split-K reduce (a = M, b = splits). */
 dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, int32_t* grid);
 
 /* =============================================================================================
@@ -409,6 +410,18 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
 dak_status dak_comm_unique_id(void* id_out);
 dak_status dak_comm_init(const void* id, int32_t rank, int32_t world, void** comm);
 dak_status dak_comm_destroy(void* comm);
+
+/* Ranks in the communicator (comm NULL: 1). */
+dak_status dak_comm_size(void* comm, int32_t* world);
+
+/* Column-parallel combine (Megatron column split: rank r computed output features
+ * [r Ml, (r + 1) Ml) of y = x W^T, e.g. a TP-sharded GEMV of BASELINE configs[4]): recv [N, world*Ml]
+ * bf16 row-major = the ranks' send [N, Ml] blocks side by side (ncclAllGather over NVLink, then one
+ * re-layout kernel from NCCL's rank-major [world][N][Ml] in `scratch`; N == 1 or one rank: no
+ * re-layout, scratch may be NULL). comm NULL: one rank (recv = send, copied unless aliased).
+ * Ml % 8 == 0; 16-byte aligned device buffers. Errors: EINVAL, ENCCL, ECUDA. */
+dak_status dak_allgather_cols(void* comm, const void* send, void* recv, void* scratch, int32_t N, int64_t Ml,
+                              dak_stream_t stream);
 
 /* partial (bf16 [rows, cols], device) is summed over the communicator in place (comm NULL: one
  * rank, no exchange), then x += partial (bf16 RNE) and, if stats_out != NULL, stats_out[r] =

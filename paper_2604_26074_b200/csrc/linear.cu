@@ -1287,11 +1287,22 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
 // y[n, m] = act(sum_s part[s][n][m] + bias[m]) + residual[n, m]: the fixed-order split-K combine.
 // Grid (x: column groups, y: row n); vec = 4 columns per thread (float4 partial loads, 8-byte
 // bf16 stores; M % 4 == 0 and 8-byte aligned y / residual rows), else one.
+__device__ __forceinline__ void tstamp2d(unsigned long long* tr, int k) {  // 2-D grid: CTA = y * gridDim.x + x
+  const unsigned c = blockIdx.y * gridDim.x + blockIdx.x;
+  if (tr && threadIdx.x == 0 && c < (unsigned)kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[c * 4 + k] = t;
+  }
+}
 __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int N, long long M,
                                      const __nv_bfloat16* __restrict__ bias, int act,
-                                     const __nv_bfloat16* residual, __nv_bfloat16* y, long long ldy, int vec) {
+                                     const __nv_bfloat16* residual, __nv_bfloat16* y, long long ldy, int vec,
+                                     unsigned long long* tr) {
+  tstamp2d(tr, 0);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  tstamp2d(tr, 1);
   const long long total = (long long)N * M;
   const int n = blockIdx.y;
   const float* pr = part + (long long)n * M;
@@ -1325,6 +1336,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int 
       ob.y = *reinterpret_cast<uint32_t*>(&o1);
       reinterpret_cast<uint2*>(yr)[m4] = ob;
     }
+    tstamp2d(tr, 3);
     return;
   }
   for (long long m = (long long)blockIdx.x * blockDim.x + threadIdx.x; m < M; m += (long long)gridDim.x * blockDim.x) {
@@ -1335,6 +1347,7 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int S, int 
     if (rr) v += __bfloat162float(rr[m]);
     yr[m] = __float2bfloat16_rn(v);
   }
+  tstamp2d(tr, 3);
 }
 
 // ------------------------------------------------------------------------------------ packing
@@ -2045,7 +2058,8 @@ dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool d
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, lin::splitk_reduce_kernel, (const float*)pl.p.part, pl.p.ksplit, (int)args->N,
-                                    (long long)args->M, pl.p.bias, pl.p.act, pl.p.residual, pl.p.y, pl.p.ldy, vec));
+                                    (long long)args->M, pl.p.bias, pl.p.act, pl.p.residual, pl.p.y, pl.p.ldy, vec,
+                                    trace_slot(DAK_KIND_REDUCE, args->M, pl.p.ksplit, (int)(cfg.gridDim.x * cfg.gridDim.y))));
   }
   return DAK_OK;
 }

@@ -6,6 +6,8 @@
 // all-reduce in place and then x += sum (bf16 RNE) and the row statistics a fused pre-norm of the
 // next op consumes (one part per row). NCCL is bound at run time (dlopen of libnccl.so.2, the one
 // torch already loaded), so the library loads and the single-GPU path runs without NCCL.
+#include <algorithm>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
@@ -23,6 +25,8 @@ struct Nccl {
   ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
   ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*comm_count)(const ncclComm_t, int*) = nullptr;
   const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -36,7 +40,10 @@ static dak_status nccl(Nccl** out) {
     n.comm_destroy = (decltype(n.comm_destroy))dlsym(h, "ncclCommDestroy");
     n.all_reduce = (decltype(n.all_reduce))dlsym(h, "ncclAllReduce");
     n.error_string = (decltype(n.error_string))dlsym(h, "ncclGetErrorString");
-    if (!n.get_unique_id || !n.comm_init_rank || !n.comm_destroy || !n.all_reduce || !n.error_string)
+    n.all_gather = (decltype(n.all_gather))dlsym(h, "ncclAllGather");
+    n.comm_count = (decltype(n.comm_count))dlsym(h, "ncclCommCount");
+    if (!n.get_unique_id || !n.comm_init_rank || !n.comm_destroy || !n.all_reduce || !n.error_string || !n.all_gather ||
+        !n.comm_count)
       return fail(DAK_ENCCL, "libnccl.so.2 lacks a required symbol");
     n.h = h;
   }
@@ -206,6 +213,17 @@ __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_b
   }
 }
 
+// rank-major gather [world][N][Ml] -> row-major [N][world * Ml] (16-byte chunks; Ml % 8 == 0)
+__global__ void gather_cols_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int world, int N, long long ml16) {
+  const long long total = (long long)world * N * ml16;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long c = i % ml16;
+    const long long n = (i / ml16) % N;
+    const long long r = i / (ml16 * N);
+    dst[(n * world + r) * ml16 + c] = src[i];
+  }
+}
+
 }  // namespace tp
 }  // namespace dak
 
@@ -270,6 +288,53 @@ dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t ro
   const bool vec = cols % 8 == 0 && cols <= tp::kThreads * 64 && aligned16(partial) && aligned16(x);
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, vec ? tp::residual_stats_vec_kernel : tp::residual_stats_kernel,
                                   (const __nv_bfloat16*)partial, (__nv_bfloat16*)x, (int)cols, (float4*)stats_out));
+  return DAK_OK;
+}
+
+dak_status dak_comm_size(void* comm, int32_t* world) {
+  if (!world) return fail(DAK_EINVAL, "dak_comm_size: NULL");
+  if (!comm) {
+    *world = 1;
+    return DAK_OK;
+  }
+  tp::Nccl* n;
+  dak_status st = tp::nccl(&n);
+  if (st != DAK_OK) return st;
+  int w = 0;
+  DAK_NCCL_TRY(n, n->comm_count((ncclComm_t)comm, &w));
+  *world = w;
+  return DAK_OK;
+}
+
+dak_status dak_allgather_cols(void* comm, const void* send, void* recv, void* scratch, int32_t N, int64_t Ml,
+                              dak_stream_t stream) {
+  if (!send || !recv || N <= 0 || Ml <= 0) return fail(DAK_EINVAL, "dak_allgather_cols: bad arguments");
+  if (Ml % 8 || !aligned16(send) || !aligned16(recv) || !aligned16(scratch))
+    return fail(DAK_EINVAL, "dak_allgather_cols: Ml %% 8 == 0 and 16-byte aligned buffers required");
+  int32_t world = 1;
+  dak_status st = dak_comm_size(comm, &world);
+  if (st != DAK_OK) return st;
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t shard = (size_t)N * Ml;
+  if (world == 1 || N == 1) {  // the rank-major gather already is row-major
+    if (!comm) {
+      if (recv != send) DAK_CUDA_TRY(cudaMemcpyAsync(recv, send, shard * 2, cudaMemcpyDeviceToDevice, s));
+      return DAK_OK;
+    }
+    tp::Nccl* n;
+    if ((st = tp::nccl(&n)) != DAK_OK) return st;
+    DAK_NCCL_TRY(n, n->all_gather(send, recv, shard, ncclBfloat16, (ncclComm_t)comm, s));
+    return DAK_OK;
+  }
+  if (!scratch) return fail(DAK_EINVAL, "dak_allgather_cols: scratch [world][N][Ml] needed for N > 1");
+  tp::Nccl* n;
+  if ((st = tp::nccl(&n)) != DAK_OK) return st;
+  DAK_NCCL_TRY(n, n->all_gather(send, scratch, shard, ncclBfloat16, (ncclComm_t)comm, s));
+  const long long ml16 = Ml / 8;
+  const long long total = (long long)world * N * ml16;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  tp::gather_cols_kernel<<<grid, 256, 0, s>>>((const uint4*)scratch, (uint4*)recv, world, N, ml16);
+  DAK_CUDA_TRY(cudaGetLastError());
   return DAK_OK;
 }
 

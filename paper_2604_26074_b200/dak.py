@@ -155,7 +155,7 @@ def version() -> str:
     return lib.dak_version().decode()
 
 
-TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed"}
+TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed", 7: "splitk_reduce"}
 
 
 def trace_enable(dev_buf, max_launches: int):
@@ -455,6 +455,21 @@ def comm_init(uid: bytes, rank: int, world: int) -> int:
     c = C.c_void_p()
     _check(lib.dak_comm_init(C.create_string_buffer(uid, 128), int(rank), int(world), C.byref(c)))
     return c.value
+
+
+_sig("dak_comm_size", C.c_int32, [C.c_void_p, C.POINTER(C.c_int32)])
+_sig("dak_allgather_cols", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_void_p])
+EXPORTED += ["dak_comm_size", "dak_allgather_cols"]
+
+
+def comm_size(comm) -> int:
+    v = C.c_int32()
+    _check(lib.dak_comm_size(comm, C.byref(v)))
+    return v.value
+
+
+def allgather_cols(comm, send, recv, scratch, N, Ml, stream=None):
+    _check(lib.dak_allgather_cols(comm, _ptr(send), _ptr(recv), _ptr(scratch), int(N), int(Ml), _stream(stream)))
 
 
 def comm_destroy(comm):
