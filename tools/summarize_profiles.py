@@ -33,10 +33,11 @@ def family(name):
     return re.sub(r"\(.*", "", name).replace("void ", "").split("::")[-1]
 
 
-def main(rnd="r01"):
+def main(rnd="r02", csv_name="launches_opt.csv", workload="opt-30b-decode-b8-ctx64"):
     out_dir = os.path.join(ROOT, "profiles", rnd)
     os.makedirs(out_dir, exist_ok=True)
-    per = launch_table(os.path.join(ROOT, "gpurun_out", f"launches_{rnd}.csv"))
+    src = os.path.join(ROOT, "gpurun_out", rnd, csv_name)
+    per = launch_table(src)
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     lin_n, lin_bytes = 0, 0.0
     for (_, name), m in per.items():
@@ -45,21 +46,21 @@ def main(rnd="r01"):
         a[0] += 1
         a[1] += m.get("gpu__time_duration.sum", 0.0)
         a[2] += b
-        if "split_linear" in name:
+        if re.search(r"split_linear|umma_linear|umma_swap", name):
             lin_n += 1
             lin_bytes += b
     tot = sum(a[1] for a in agg.values())
-    lines = [f"# one timed OPT-30B b8 decode step ({len(per)} launches), ncu --metrics gpu__time_duration.sum,"
+    lines = [f"# one timed {workload} decode step ({len(per)} launches), ncu --metrics gpu__time_duration.sum,"
              "dram__bytes_read.sum,dram__bytes_write.sum --clock-control none (serialised, cold L2:",
              "shares are meaningful, absolute times are not the graph's); tools/profile_round.sh",
              f"{'launches':>8} {'total_us':>10} {'share':>6} {'mean_us':>8} {'dram_MB/launch':>15}  kernel"]
     for k, (c, t, b) in sorted(agg.items(), key=lambda x: -x[1][1]):
         lines.append(f"{c:8d} {t / 1e3:10.1f} {100 * t / tot:5.1f}% {t / c / 1e3:8.2f} {b / c / 1e6:15.2f}  {k}")
     lines.append(f"total {tot / 1e3:.1f} us")
-    open(os.path.join(out_dir, "step_launches.txt"), "w").write("\n".join(lines) + "\n")
-    json.dump(dict(source=f"gpurun_out/launches_{rnd}.csv (ncu, one timed step)", linear_launches=lin_n,
+    open(os.path.join(out_dir, f"step_launches_{workload}.txt"), "w").write("\n".join(lines) + "\n")
+    json.dump(dict(source=f"gpurun_out/{rnd}/{csv_name} (ncu, one timed step of {workload})", linear_launches=lin_n,
                    dram_bytes_per_launch=round(lin_bytes / max(lin_n, 1))),
-              open(os.path.join(out_dir, "linear_traffic.json"), "w"), indent=1)
+              open(os.path.join(out_dir, f"linear_traffic_{workload}.json"), "w"), indent=1)
     print("\n".join(lines))
 
 
