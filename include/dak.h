@@ -56,7 +56,7 @@ dak_status dak_device_sms(int32_t* sms);
 dak_status dak_trace_enable(void* dev_buf, int32_t max_launches);
 int32_t dak_trace_count(void);
 /* kind: 1 linear (a = M, b = K), 2 attention, 3 combine, 4 KV append, 5 LayerNorm, 6 embed,
- * 7 split-K reduce (a = M, b = splits). */
+ * 7 split-K reduce (a = M, b = splits), 8 prefill attention (a = B, b = T). */
 dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, int32_t* grid);
 
 /* =============================================================================================
@@ -399,6 +399,33 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
                              const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
                              int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
                              dak_stream_t stream);
+
+/* Causal prefill attention over the same tier-split paged KV cache (P:L388
+ * §3.2 "prefill ... arithmetic intensity O(L)": compute-bound at long L, the planner's Phase 2
+ * regime, P:L429 / P:L453). Request b's T newest tokens sit at positions seq_lens[b] - T ..
+ * seq_lens[b] - 1 and their K / V rows are already in the pools; query i attends keys
+ * 0 .. seq_lens[b] - T + i (causal), kv head g = h / (Hq / Hkv):
+ *   out[b, i, h] = softmax(scale * K_b[0 .. L-T+i] q[b, i, h]) V_b[0 .. L-T+i].
+ * One CTA per (request, kv head, 128 query rows (token, head of the group)); 64-token K / V tiles
+ * stream in key order from the tier each page's block-table entry names (bit 31 = host pool), so
+ * the result is bitwise independent of the tier split. */
+typedef struct {
+  const void* q;                /* [B, T, Hq, d] bf16, device                                   */
+  void* out;                    /* [B, T, Hq, d] bf16, device                                   */
+  const void *k_hbm, *v_hbm;    /* DAK-PG pools in HBM (may be NULL if unused)                  */
+  const void *k_host, *v_host;  /* DAK-PG pools in pinned mapped host memory (may be NULL)      */
+  const int32_t* block_table;   /* [B, max_pages] device; bit 31 = host tier                   */
+  const int32_t* seq_lens;      /* [B] device, T <= seq_len <= max_pages * page_size            */
+  int32_t B, T, Hq, Hkv, d;     /* d == 128; Hq % Hkv == 0                                      */
+  int32_t page_size;            /* multiple of 64 tokens                                        */
+  int32_t max_pages;
+  float scale;                  /* <= 0: 1/sqrt(d)                                              */
+  dak_launch_cfg cfg;           /* stages (ring depth, 0: 6) is honoured                         */
+} dak_prefill_args;
+
+/* Errors: DAK_EINVAL (NULL / misaligned / non-positive sizes, Hq % Hkv), DAK_EUNSUPPORTED (d != 128,
+ * page_size % 64). seq_lens are not checked on the host (device data). */
+dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stream);
 
 /* =============================================================================================
  * 4b. Tensor-parallel combine (BASELINE north_star: TP over 8 x B200, NCCL over NVLink/NVSwitch)

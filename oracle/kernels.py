@@ -186,3 +186,37 @@ def layernorm(x, w, b, eps: float = 1e-5) -> np.ndarray:
     mu = x.mean(axis=-1, keepdims=True)
     var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
     return (x - mu) / np.sqrt(var + eps) * w + b
+
+
+def paged_prefill_attention(q_bits, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, page_size: int,
+                            scale: float = 0.0) -> np.ndarray:
+    """Causal prefill attention over a tier-split paged KV cache, float64 (SURVEY §8(f) rank 3;
+    P:L388 "prefill attention ... arithmetic intensity O(L)", P:L631 SDPA).
+
+    q_bits [B, T, Hq, d]: the T newest tokens of request b, at positions L_b - T .. L_b - 1
+    (L_b = seq_lens[b] >= T; their K / V rows are already in the cache). Query i attends keys
+    0 .. L_b - T + i (causal); kv head g = h // (Hq / Hkv). Returns o [B, T, Hq, d] float64.
+    """
+    q = bf16_to_f64(q_bits)
+    B, T, Hq, d = q.shape
+    Hkv = np.asarray(k_hbm if k_hbm is not None and np.asarray(k_hbm).size else k_host).shape[1]
+    if Hq % Hkv:
+        raise ValueError("Hq % Hkv != 0")
+    grp = Hq // Hkv
+    sc = scale if scale else 1.0 / math.sqrt(d)
+    out = np.zeros((B, T, Hq, d), dtype=np.float64)
+    for b in range(B):
+        L = int(seq_lens[b])
+        if L < T:
+            raise ValueError("seq_len < T")
+        for g in range(Hkv):
+            K = gather_kv(k_hbm, k_host, block_table[b], L, g, page_size)
+            V = gather_kv(v_hbm, v_host, block_table[b], L, g, page_size)
+            for i in range(T):
+                n = L - T + i + 1  # keys visible to query i
+                for hh in range(grp):
+                    h = g * grp + hh
+                    s = sc * (K[:n] @ q[b, i, h])
+                    p = np.exp(s - s.max())
+                    out[b, i, h] = (p / p.sum()) @ V[:n]
+    return out

@@ -29,6 +29,7 @@ SOURCES = [
     ("linear.cu", ["-DDAK_LINEAR_PART=4"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=5"]),
     ("attention.cu", []),
+    ("prefill.cu", []),
     ("layer.cu", []),
     ("tp.cu", []),
 ]

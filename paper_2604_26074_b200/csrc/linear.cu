@@ -882,6 +882,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
           bulk_g2s_mc_hint(wring + (size_t)slot * wstage, src + (long long)i * chunk_stride, w_bytes, &full[slot],
                            (uint16_t)((1u << G) - 1u), pol);
       };
+      // gated host items wait for the previous kernel first: a slot held across griddepcontrol.wait
+      // would block that kernel's own host items (programmatic dependent launch overlaps the two)
+      if (host && p.host_gate > 0) grid_dep_wait();
       const bool gated = host && p.host_gate > 0 && gate_acquire(p.host_gate);
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);
@@ -1187,6 +1190,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
       const uint64_t pol = policy_evict_first();
       const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
       asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      if (host && p.host_gate > 0) grid_dep_wait();  // never hold a slot across the dependency wait
       const bool gated = host && p.host_gate > 0 && gate_acquire(p.host_gate);
       for (int i = 0; i < pro; ++i) {
         mbar_expect_tx(&full[i], w_bytes + x_tx);

@@ -1,0 +1,356 @@
+// dak_prefill_attention -- causal prefill attention over the HBM / host-split paged KV cache
+// (§3.2: prefill attention has arithmetic intensity O(L) and is
+// compute-bound at long L, which is the regime where the planner's Phase 2 can move up to
+// B_h * T_comp bytes of an op to the host at no cost, P:L429 / P:L453).
+//
+// Work split: CTA = (request b, kv head g, block of 128 query rows), a query row being one (new
+// token i, q head of g's GQA group) pair -- the G heads of a group share every K / V tile, so one
+// CTA reads each tile once for all of them. Warps 0-7 each own 16 query rows (FlashAttention-2
+// style, mma.sync m16n8k16 bf16 -> fp32: S = Q K^T with K rows via ldmatrix, online softmax in the
+// exp2 domain in registers, O += P V with P re-used from the S accumulators as the A operand and V
+// via ldmatrix.trans); warp 8 lane 0 streams 64-token K and V tiles of the CTA's causal key range
+// [0, kmax) into a ring of shared-memory stages with 1-D bulk copies (cp.async.bulk), each tile from
+// the tier its page's block-table entry names (bit 31: host pool over the link, else HBM).
+// Tiles are consumed in key order: the reduction order of a row depends on (seq_len, T) only, never
+// on the tier split (bitwise r-invariant). DAK-PG pages (include/dak.h): row t's 16-byte chunks are
+// swizzled by t & 7, so both ldmatrix forms are bank-conflict free.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.h"
+
+namespace dak {
+namespace pf {
+
+constexpr int kD = 128;
+constexpr int kConsumers = 8;
+constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kRows = kConsumers * 16;  // query rows per CTA
+constexpr int kTile = 64;               // keys per stage
+constexpr int kTileBytes = kTile * kD * 2;
+constexpr int kMaxStages = 6;
+constexpr uint32_t kHostBit = 0x80000000u;
+
+struct Params {
+  const __nv_bfloat16* q;
+  __nv_bfloat16* out;
+  const char* k_hbm;
+  const char* v_hbm;
+  const char* k_host;
+  const char* v_host;
+  const int* block_table;
+  const int* seq_lens;
+  int B, T, Hq, Hkv, G, page, max_pages;
+  int blocks_per_bg;  // CTAs per (request, kv head)
+  int stages;
+  float scale_log2;
+  unsigned long long* trace;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(su32(b)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+// byte offset of 16-byte chunk j of token row t in a DAK-PG page (row pitch 256 B)
+__device__ __forceinline__ uint32_t pg_off(int t, int j) {
+  return (uint32_t)(t * (kD * 2) + ((((j >> 3) << 3) | ((j & 7) ^ (t & 7))) << 4));
+}
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
+  if (tr && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 4 + k] = t;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  unsigned char* ring = smem + 1024;  // [stages][K tile | V tile]
+
+  const int bg = blockIdx.x / p.blocks_per_bg, blk = blockIdx.x % p.blocks_per_bg;
+  const int b = bg / p.Hkv, g = bg % p.Hkv;
+  const int L = p.seq_lens[b];
+  const int rows = p.T * p.G;            // query rows of (b, g): row r = (token r / G, head r % G)
+  const int r0 = blk * kRows;
+  const int r_last = min(rows, r0 + kRows) - 1;
+  const int kmax = L - p.T + r_last / p.G + 1;  // keys [0, kmax) cover every row of the block
+  const int ntiles = (kmax + kTile - 1) / kTile;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tstamp(p.trace, 0);
+  }
+  __syncthreads();
+  const int S = p.stages;
+  const int page_bytes = p.page * kD * 2;
+
+  if (warp == kConsumers) {  // ---- producer: K and V tile of every key block, in key order
+    if (lane == 0) {
+      const int* bt = p.block_table + (long long)b * p.max_pages;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
+        const int key0 = t * kTile;
+        const uint32_t e = (uint32_t)bt[key0 / p.page];
+        const bool host = (e & kHostBit) != 0;
+        const long long off = ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + (long long)(key0 % p.page) * kD * 2;
+        unsigned char* dst = ring + (size_t)s * 2 * kTileBytes;
+        mbar_expect_tx(&full[s], 2u * kTileBytes);
+        bulk_g2s(dst, (host ? p.k_host : p.k_hbm) + off, kTileBytes, &full[s]);
+        bulk_g2s(dst + kTileBytes, (host ? p.v_host : p.v_hbm) + off, kTileBytes, &full[s]);
+        if (++s == S) { s = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+
+  // ---- consumers: rows rw0 .. rw0 + 15 of the block
+  const int gq = lane >> 2, cq = lane & 3;
+  const int rw0 = r0 + warp * 16;
+  const int ra = rw0 + gq, rb = rw0 + gq + 8;  // the two rows this thread holds
+  // key limit of each row (causal): key k visible iff k < lim
+  const int lim_a = ra < rows ? L - p.T + ra / p.G + 1 : 0;
+  const int lim_b = rb < rows ? L - p.T + rb / p.G + 1 : 0;
+  // Q as the A operand (rows ra / rb, 16 columns per k-step), straight from global memory
+  uint32_t qa[kD / 16][4];
+  {
+    auto qrow = [&](int r) -> const uint32_t* {
+      const int i = r / p.G, hh = r % p.G;
+      return reinterpret_cast<const uint32_t*>(p.q + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD);
+    };
+    const uint32_t* qa_row = ra < rows ? qrow(ra) : nullptr;
+    const uint32_t* qb_row = rb < rows ? qrow(rb) : nullptr;
+#pragma unroll
+    for (int ks = 0; ks < kD / 16; ++ks) {
+      qa[ks][0] = qa_row ? qa_row[8 * ks + cq] : 0u;
+      qa[ks][1] = qb_row ? qb_row[8 * ks + cq] : 0u;
+      qa[ks][2] = qa_row ? qa_row[8 * ks + 4 + cq] : 0u;
+      qa[ks][3] = qb_row ? qb_row[8 * ks + 4 + cq] : 0u;
+    }
+  }
+  float o[kD / 8][4];
+#pragma unroll
+  for (int i = 0; i < kD / 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+  const int warp_lim = min(rows, rw0 + 16) > rw0 ? L - p.T + (min(rows, rw0 + 16) - 1) / p.G + 1 : 0;
+
+  int s = 0;
+  uint32_t ph = 0;
+  for (int t = 0; t < ntiles; ++t) {
+    mbar_wait(&full[s], ph);
+    const int key0 = t * kTile;
+    if (key0 < warp_lim) {  // tiles past every row of this warp only need the release below
+      const uint32_t kb = su32(ring + (size_t)s * 2 * kTileBytes);
+      const uint32_t vb = kb + kTileBytes;
+      // ---- S = Q K^T : 16 rows x 64 keys (8 n8 tiles)
+      float sc[kTile / 8][4];
+#pragma unroll
+      for (int j = 0; j < kTile / 8; ++j) sc[j][0] = sc[j][1] = sc[j][2] = sc[j][3] = 0.f;
+#pragma unroll
+      for (int ks = 0; ks < kD / 16; ++ks) {
+#pragma unroll
+        for (int jj = 0; jj < kTile / 16; ++jj) {
+          const int mtx = lane >> 3;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4(kb + pg_off(16 * jj + ((mtx >> 1) << 3) + (lane & 7), 2 * ks + (mtx & 1)), b0, b1, b2, b3);
+          mma_bf16(sc[2 * jj], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+          mma_bf16(sc[2 * jj + 1], qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+        }
+      }
+      // ---- causal mask, scale, online softmax (exp2 domain); row a: sc[.][0..1], row b: sc[.][2..3]
+      float mx0 = -INFINITY, mx1 = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kTile / 8; ++j) {
+        const int k = key0 + 8 * j + 2 * cq;
+        sc[j][0] = k < lim_a ? sc[j][0] * p.scale_log2 : -INFINITY;
+        sc[j][1] = k + 1 < lim_a ? sc[j][1] * p.scale_log2 : -INFINITY;
+        sc[j][2] = k < lim_b ? sc[j][2] * p.scale_log2 : -INFINITY;
+        sc[j][3] = k + 1 < lim_b ? sc[j][3] * p.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, fmaxf(sc[j][0], sc[j][1]));
+        mx1 = fmaxf(mx1, fmaxf(sc[j][2], sc[j][3]));
+      }
+#pragma unroll
+      for (int off = 1; off < 4; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);
+      // rows with no visible key yet (or padding rows) keep m = -inf: use 0 as the reference
+      const float ref0 = mn0 == -INFINITY ? 0.f : mn0, ref1 = mn1 == -INFINITY ? 0.f : mn1;
+      const float al0 = exp2f(m[0] - ref0), al1 = exp2f(m[1] - ref1);
+      m[0] = mn0;
+      m[1] = mn1;
+      float ls0 = 0.f, ls1 = 0.f;
+      uint32_t pa[kTile / 16][4];  // P as the A operand of P V: k16 block kk = n8 tiles 2kk, 2kk+1
+#pragma unroll
+      for (int j = 0; j < kTile / 8; ++j) {
+        const float p0 = exp2f(sc[j][0] - ref0), p1 = exp2f(sc[j][1] - ref0);
+        const float p2 = exp2f(sc[j][2] - ref1), p3 = exp2f(sc[j][3] - ref1);
+        ls0 += p0 + p1;
+        ls1 += p2 + p3;
+        pa[j >> 1][(j & 1) * 2 + 0] = pack_bf16(p0, p1);
+        pa[j >> 1][(j & 1) * 2 + 1] = pack_bf16(p2, p3);
+      }
+      l[0] = l[0] * al0 + ls0;
+      l[1] = l[1] * al1 + ls1;
+#pragma unroll
+      for (int i = 0; i < kD / 8; ++i) {
+        o[i][0] *= al0; o[i][1] *= al0; o[i][2] *= al1; o[i][3] *= al1;
+      }
+      // ---- O += P V : V rows [key][d] through ldmatrix.trans (B operand, k = keys)
+#pragma unroll
+      for (int kk = 0; kk < kTile / 16; ++kk) {
+#pragma unroll
+        for (int i = 0; i < kD / 8; i += 2) {
+          const int mtx = lane >> 3;
+          uint32_t b0, b1, b2, b3;
+          ldsm_x4_t(vb + pg_off(16 * kk + ((mtx & 1) << 3) + (lane & 7), i + (mtx >> 1)), b0, b1, b2, b3);
+          mma_bf16(o[i], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+          mma_bf16(o[i + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    if (++s == S) { s = 0; ph ^= 1u; }
+  }
+  // ---- normalise and store: row sums over the 4 lanes of a row group
+#pragma unroll
+  for (int off = 1; off < 4; off <<= 1) {
+    l[0] += __shfl_xor_sync(0xffffffffu, l[0], off);
+    l[1] += __shfl_xor_sync(0xffffffffu, l[1], off);
+  }
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    const int r = half ? rb : ra;
+    if (r >= rows) continue;
+    const float inv = 1.f / l[half];
+    const int i = r / p.G, hh = r % p.G;
+    __nv_bfloat16* dst = p.out + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD;
+#pragma unroll
+    for (int n = 0; n < kD / 8; ++n)
+      *reinterpret_cast<uint32_t*>(dst + 8 * n + 2 * cq) = pack_bf16(o[n][2 * half] * inv, o[n][2 * half + 1] * inv);
+  }
+  if (p.trace) {
+    asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
+    if (threadIdx.x == 0) tstamp(p.trace, 3);
+  }
+}
+
+}  // namespace pf
+}  // namespace dak
+
+using namespace dak;
+
+extern "C" {
+
+static dak_status prefill_plan(const dak_prefill_args* a, pf::Params* p, int* grid, int* smem) {
+  if (!a) return fail(DAK_EINVAL, "dak_prefill_attention: args NULL");
+  if (a->B <= 0 || a->T <= 0 || a->Hq <= 0 || a->Hkv <= 0 || a->page_size <= 0 || a->max_pages <= 0)
+    return fail(DAK_EINVAL, "dak_prefill_attention: sizes must be positive");
+  if (a->Hq % a->Hkv) return fail(DAK_EINVAL, "dak_prefill_attention: Hq %% Hkv != 0");
+  if (a->d != pf::kD) return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: head dim %d (this build: d = 128)", a->d);
+  if (a->page_size % pf::kTile) return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: page_size must be a multiple of 64");
+  if (!a->q || !a->out || !a->block_table || !a->seq_lens || (!a->k_hbm && !a->k_host))
+    return fail(DAK_EINVAL, "dak_prefill_attention: NULL tensor");
+  if (!aligned16(a->q) || !aligned16(a->out) || !aligned16(a->k_hbm) || !aligned16(a->v_hbm) || !aligned16(a->k_host) ||
+      !aligned16(a->v_host))
+    return fail(DAK_EINVAL, "dak_prefill_attention: pointers must be 16-byte aligned");
+  pf::Params q{};
+  q.q = (const __nv_bfloat16*)a->q;
+  q.out = (__nv_bfloat16*)a->out;
+  q.k_hbm = (const char*)a->k_hbm;
+  q.v_hbm = (const char*)a->v_hbm;
+  q.k_host = (const char*)a->k_host;
+  q.v_host = (const char*)a->v_host;
+  q.block_table = a->block_table;
+  q.seq_lens = a->seq_lens;
+  q.B = a->B; q.T = a->T; q.Hq = a->Hq; q.Hkv = a->Hkv; q.G = a->Hq / a->Hkv;
+  q.page = a->page_size; q.max_pages = a->max_pages;
+  q.blocks_per_bg = (a->T * q.G + pf::kRows - 1) / pf::kRows;
+  q.stages = a->cfg.stages > 0 ? std::min(a->cfg.stages, pf::kMaxStages) : pf::kMaxStages;
+  if (q.stages < 2) q.stages = 2;
+  const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf((float)pf::kD);
+  q.scale_log2 = scale * 1.4426950408889634f;
+  const long long g = (long long)a->B * a->Hkv * q.blocks_per_bg;
+  if (g > 0x7fffffffLL) return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: grid too large");
+  *p = q;
+  *grid = (int)g;
+  *smem = 1024 + q.stages * 2 * pf::kTileBytes + 1024;
+  return DAK_OK;
+}
+
+dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stream) {
+  pf::Params p;
+  int grid = 0, smem = 0;
+  dak_status st = prefill_plan(args, &p, &grid, &smem);
+  if (st != DAK_OK) return st;
+  static bool attr = false;
+  if (!attr) {
+    DAK_CUDA_TRY(cudaFuncSetAttribute(pf::prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      1024 + pf::kMaxStages * 2 * pf::kTileBytes + 1024));
+    attr = true;
+  }
+  p.trace = trace_slot(DAK_KIND_PREFILL, args->B, args->T, grid);
+  pf::prefill_attention_kernel<<<grid, pf::kThreads, smem, (cudaStream_t)stream>>>(p);
+  DAK_CUDA_TRY(cudaGetLastError());
+  return DAK_OK;
+}
+
+}  // extern "C"

@@ -155,7 +155,7 @@ def version() -> str:
     return lib.dak_version().decode()
 
 
-TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed", 7: "splitk_reduce"}
+TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed", 7: "splitk_reduce", 8: "prefill"}
 
 
 def trace_enable(dev_buf, max_launches: int):
@@ -375,6 +375,29 @@ def attention_workspace_size(args: dak_attention_args) -> int:
 
 def attention(args: dak_attention_args, stream=None):
     _check(lib.dak_attention(C.byref(args), _stream(stream)))
+
+
+class dak_prefill_args(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("out", C.c_void_p), ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p),
+                ("k_host", C.c_void_p), ("v_host", C.c_void_p), ("block_table", C.c_void_p), ("seq_lens", C.c_void_p),
+                ("B", C.c_int32), ("T", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("d", C.c_int32),
+                ("page_size", C.c_int32), ("max_pages", C.c_int32), ("scale", C.c_float), ("cfg", dak_launch_cfg)]
+
+
+_sig("dak_prefill_attention", C.c_int32, [C.POINTER(dak_prefill_args), C.c_void_p])
+EXPORTED += ["dak_prefill_attention"]
+
+
+def prefill_attention(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, B, T, Hq, Hkv, d, page_size,
+                      max_pages, scale=0.0, cfg=None, stream=None):
+    a = dak_prefill_args()
+    a.q, a.out = _ptr(q), _ptr(out)
+    a.k_hbm, a.v_hbm, a.k_host, a.v_host = _ptr(k_hbm), _ptr(v_hbm), _ptr(k_host), _ptr(v_host)
+    a.block_table, a.seq_lens = _ptr(block_table), _ptr(seq_lens)
+    a.B, a.T, a.Hq, a.Hkv, a.d = int(B), int(T), int(Hq), int(Hkv), int(d)
+    a.page_size, a.max_pages, a.scale = int(page_size), int(max_pages), float(scale)
+    a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
+    _check(lib.dak_prefill_attention(C.byref(a), _stream(stream)))
 
 
 def kv_append(k_new, v_new, block_table, positions, B, Hkv, d, page_size, max_pages, k_hbm, v_hbm, k_host, v_host,

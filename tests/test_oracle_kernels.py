@@ -214,3 +214,64 @@ def test_round_to_bf16_matches_bit_definition():
     assert np.array_equal(Kx.round_to_bf16(ints), ints)
     assert Kx.round_to_bf16(np.array([257.0]))[0] == 256.0  # tie -> even
     assert Kx.round_to_bf16(np.array([259.0]))[0] == 260.0
+
+
+def _paged_from_logical(K, V, page, Hkv, d, frac, seed):
+    """Lay logical per-request K/V out in paged tier pools (host = the oldest pages)."""
+    g = np.random.default_rng(seed)
+    B = len(K)
+    pages = [-(-k.shape[0] // page) for k in K]
+    nh = [int(round(frac * p)) for p in pages]
+    Ph, Pg = max(1, sum(nh)), max(1, sum(p - h for p, h in zip(pages, nh)))
+    kh, vh = np.zeros((Ph, Hkv, page, d), np.uint16), np.zeros((Ph, Hkv, page, d), np.uint16)
+    kg, vg = np.zeros((Pg, Hkv, page, d), np.uint16), np.zeros((Pg, Hkv, page, d), np.uint16)
+    bt = np.zeros((B, max(pages)), np.int64)
+    ih, ig = list(g.permutation(Ph)), list(g.permutation(Pg))
+    for b in range(B):
+        for p in range(pages[b]):
+            lo, hi = p * page, min(K[b].shape[0], (p + 1) * page)
+            host = p < nh[b]
+            j = int((ih if host else ig).pop())
+            (kh if host else kg)[j, :, :hi - lo] = K[b][lo:hi].transpose(1, 0, 2)
+            (vh if host else vg)[j, :, :hi - lo] = V[b][lo:hi].transpose(1, 0, 2)
+            bt[b, p] = j | (0x80000000 if host else 0)
+    return kg, vg, kh, vh, bt.astype(np.uint32).view(np.int32)
+
+
+def test_prefill_attention_vs_torch_sdpa_causal():
+    """Prefill oracle (T new tokens after a prefix) = torch SDPA in float64 with the causal mask
+    offset by the prefix (prefix 0: is_causal=True), any tier split; GQA by repeating kv heads."""
+    torch = pytest.importorskip("torch")
+    import synth
+    d, page, Hq, Hkv = 32, 16, 4, 2
+    for Ls, T in (([20, 37], 20), ([50, 9], 9), ([70], 33)):
+        q, _, _ = synth.kv_inputs([T] * len(Ls), Hkv, d, Hq * T, seed=11 + T)
+        q = q.reshape(len(Ls), T, Hq, d)
+        _, K, V = synth.kv_inputs(Ls, Hkv, d, Hq, seed=12 + T)
+        for frac in (0.0, 0.5, 1.0):
+            kg, vg, kh, vh, bt = _paged_from_logical(K, V, page, Hkv, d, frac, 5)
+            got = Kx.paged_prefill_attention(q, kg, vg, kh, vh, bt, Ls, page)
+            for b, L in enumerate(Ls):
+                qt = torch.from_numpy(Kx.bf16_to_f64(q[b])).permute(1, 0, 2)            # [Hq, T, d]
+                kt = torch.from_numpy(Kx.bf16_to_f64(K[b])).permute(1, 0, 2).repeat_interleave(Hq // Hkv, 0)
+                vt = torch.from_numpy(Kx.bf16_to_f64(V[b])).permute(1, 0, 2).repeat_interleave(Hq // Hkv, 0)
+                if L == T:
+                    ref = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, is_causal=True)
+                else:
+                    mask = torch.arange(L)[None, :] <= (L - T + torch.arange(T))[:, None]
+                    ref = torch.nn.functional.scaled_dot_product_attention(qt, kt, vt, attn_mask=mask)
+                assert np.allclose(got[b], ref.permute(1, 0, 2).numpy(), rtol=1e-12, atol=1e-12)
+
+
+def test_prefill_attention_last_row_is_decode():
+    """The last query of a prefill sees the whole sequence: it equals the decode oracle; T = 1 is
+    decode attention exactly."""
+    import synth
+    d, page, Hq, Hkv, Ls, T = 32, 16, 4, 2, [40, 77], 5
+    q, _, _ = synth.kv_inputs([T] * 2, Hkv, d, Hq * T, seed=3)
+    q = q.reshape(2, T, Hq, d)
+    _, K, V = synth.kv_inputs(Ls, Hkv, d, Hq, seed=4)
+    kg, vg, kh, vh, bt = _paged_from_logical(K, V, page, Hkv, d, 0.5, 6)
+    pre = Kx.paged_prefill_attention(q, kg, vg, kh, vh, bt, Ls, page)
+    dec = Kx.paged_attention(np.ascontiguousarray(q[:, -1]), kg, vg, kh, vh, bt, Ls, page)
+    assert np.allclose(pre[:, -1], dec, rtol=1e-13, atol=1e-13)

@@ -29,7 +29,7 @@ def load_ncu(path):
         except ValueError:
             continue
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1024, "MB": 1 << 20, "GB": 1 << 30,
-                 "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "sector": 1}.get(unit, 1)
+                 "ns": 1e-9, "us": 1e-6, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3, "second": 1, "sector": 1}.get(unit, 1)
         e = out.setdefault(key, dict(kernel=d["Kernel Name"]))
         e[d["Metric Name"]] = v * scale
     return [out[k] for k in sorted(out)]
