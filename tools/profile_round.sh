@@ -13,7 +13,7 @@ mkdir -p $OUT
 python bench.py --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc $?"
 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc $?"
 python bench.py --workload llama3-70b-tp8 --steps 10 --warmup 3 > $OUT/bench_llama.json 2> $OUT/bench_llama.err; echo "llama rc $?"
-KF='regex:linear_kernel|umma_swap|splitk_reduce|split_attention|combine_kernel|embed_kernel|append_kernel|norm_kernel|residual|silu|rope'
+KF='regex:linear_kernel|umma_swap|splitk_reduce|split_attention|combine_kernel|embed|append_kernel|norm|residual|silu|rope|row_stats|prefill'
 per() { python -c "import json,sys; d=json.load(open('$1')); print(d['gpu_launches']//d['steps'])"; }
 PER=$(per $OUT/bench.json)
 timeout 1500 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
