@@ -22,6 +22,7 @@
 // KV page layout ("DAK-PG"): a page of one kv head is [page_size][d] bf16 with the 16-byte chunk
 // j of token row t stored at chunk ((j>>3)<<3) | ((j&7) ^ (t&7)) (bank-conflict-free ldmatrix).
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -131,6 +132,24 @@ __device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uin
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_f16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two fp32 -> f16x2 (round to nearest, saturating at +-65504)
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16x2 -> f16x2: exact for |v| in [2^-14, 65504] (bf16's 8-bit significand fits fp16's 11 bits)
+__device__ __forceinline__ uint32_t bf2_to_h2(uint32_t r) {
+  return pack_f16(__uint_as_float(r << 16), __uint_as_float(r & 0xffff0000u));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -409,22 +428,27 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
         const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
         m[0] = mn0;
         m[1] = mn1;
-        const float p0 = exp2f(s0 - mn0), p1 = exp2f(s1 - mn1), p2 = exp2f(s2 - mn0), p3 = exp2f(s3 - mn1);
-        l[0] = l[0] * al0 + (p0 + p2);
-        l[1] = l[1] * al1 + (p1 + p3);
+        // P in fp16 for the P V product (11-bit significand for p in [0, 1]; bf16's 8 bits move o by up
+        // to ~1% of |V| when a few keys dominate); l sums the same rounded weights
+        const uint32_t h01 = pack_f16(exp2f(s0 - mn0), exp2f(s1 - mn1));
+        const uint32_t h23 = pack_f16(exp2f(s2 - mn0), exp2f(s3 - mn1));
+        const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&h01));
+        const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&h23));
+        l[0] = l[0] * al0 + (f01.x + f23.x);
+        l[1] = l[1] * al1 + (f01.y + f23.y);
 #pragma unroll
         for (int i = 0; i < kD / 16; ++i) {
           o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
         }
         // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
-        const uint32_t b0 = movm_t(pack_bf16(p0, p1));
-        const uint32_t b1 = movm_t(pack_bf16(p2, p3));
+        const uint32_t b0 = movm_t(h01);
+        const uint32_t b1 = movm_t(h23);
         // ---- O^T[d x heads] += V^T . P^T
 #pragma unroll
         for (int i = 0; i < kD / 16; ++i) {
           uint32_t a0, a1, a2, a3;
           ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
-          mma_bf16(o[i], a0, a1, a2, a3, b0, b1);
+          mma_f16(o[i], bf2_to_h2(a0), bf2_to_h2(a1), bf2_to_h2(a2), bf2_to_h2(a3), b0, b1);
         }
       }
       __syncwarp();

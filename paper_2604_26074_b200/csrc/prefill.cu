@@ -6,15 +6,17 @@
 // Work split: CTA = (request b, kv head g, block of 128 query rows), a query row being one (new
 // token i, q head of g's GQA group) pair -- the G heads of a group share every K / V tile, so one
 // CTA reads each tile once for all of them. Warps 0-7 each own 16 query rows (FlashAttention-2
-// style, mma.sync m16n8k16 bf16 -> fp32: S = Q K^T with K rows via ldmatrix, online softmax in the
-// exp2 domain in registers, O += P V with P re-used from the S accumulators as the A operand and V
-// via ldmatrix.trans); warp 8 lane 0 streams 64-token K and V tiles of the CTA's causal key range
+// style, mma.sync m16n8k16 -> fp32: S = Q K^T in bf16 with K rows via ldmatrix, online softmax in
+// the exp2 domain in registers, O += P V in fp16 with P re-used from the S accumulators as the A
+// operand and V via ldmatrix.trans converted bf16 -> fp16 in registers (exact for |v| <= 65504,
+// saturating beyond; reading R20 of DESIGN.md)); warp 8 lane 0 streams 64-token K and V tiles of the CTA's causal key range
 // [0, kmax) into a ring of shared-memory stages with 1-D bulk copies (cp.async.bulk), each tile from
 // the tier its page's block-table entry names (bit 31: host pool over the link, else HBM).
 // Tiles are consumed in key order: the reduction order of a row depends on (seq_len, T) only, never
 // on the tier split (bitwise r-invariant). DAK-PG pages (include/dak.h): row t's 16-byte chunks are
 // swizzled by t & 7, so both ldmatrix forms are bank-conflict free.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <math.h>
 
@@ -93,6 +95,24 @@ __device__ __forceinline__ void mma_bf16(float* d, uint32_t a0, uint32_t a1, uin
       "{%0,%1,%2,%3};"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void mma_f16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// two fp32 -> f16x2 (round to nearest, saturating at +-65504)
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16x2 -> f16x2: exact for |v| in [2^-14, 65504] (bf16's 8-bit significand fits fp16's 11 bits)
+__device__ __forceinline__ uint32_t bf2_to_h2(uint32_t r) {
+  return pack_f16(__uint_as_float(r << 16), __uint_as_float(r & 0xffff0000u));
 }
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -242,12 +262,14 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
       for (int j = 0; j < kTile / 8; ++j) {
         const float p0 = exp2f(sc[j][0] - ref0), p1 = exp2f(sc[j][1] - ref0);
         const float p2 = exp2f(sc[j][2] - ref1), p3 = exp2f(sc[j][3] - ref1);
-        const uint32_t h01 = pack_bf16(p0, p1), h23 = pack_bf16(p2, p3);
-        // the normaliser sums the bf16 weights the P V product actually uses: o is then an exact
-        // weighted average of V rows with weights off by <= 2^-8 relative (errors scale with the
-        // spread of V, not with |V|)
-        ls0 += __uint_as_float(h01 << 16) + __uint_as_float(h01 & 0xffff0000u);
-        ls1 += __uint_as_float(h23 << 16) + __uint_as_float(h23 & 0xffff0000u);
+        // P in fp16 (11-bit significand, p in [0, 1]): bf16's 8 bits put up to 2^-9 relative error
+        // on each weight, which for a row with a few dominant keys moves o by ~1% of |V| (measured
+        // against the float64 oracle); the normaliser sums the same rounded weights
+        const uint32_t h01 = pack_f16(p0, p1), h23 = pack_f16(p2, p3);
+        const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&h01));
+        const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&h23));
+        ls0 += f01.x + f01.y;
+        ls1 += f23.x + f23.y;
         pa[j >> 1][(j & 1) * 2 + 0] = h01;
         pa[j >> 1][(j & 1) * 2 + 1] = h23;
       }
@@ -265,8 +287,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
           const int mtx = lane >> 3;
           uint32_t b0, b1, b2, b3;
           ldsm_x4_t(vb + pg_off(16 * kk + ((mtx & 1) << 3) + (lane & 7), i + (mtx >> 1)), b0, b1, b2, b3);
-          mma_bf16(o[i], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
-          mma_bf16(o[i + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
+          mma_f16(o[i], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], bf2_to_h2(b0), bf2_to_h2(b1));
+          mma_f16(o[i + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], bf2_to_h2(b2), bf2_to_h2(b3));
         }
       }
     }
