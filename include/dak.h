@@ -462,6 +462,23 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
 dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t rows, int32_t cols, float* stats_out,
                                   int32_t pdl, dak_stream_t stream);
 
+/* NVLink-SHARP combine: a symmetric window of `bytes` (ncclMemAlloc +
+ * ncclCommWindowRegister, bound to an NVSwitch multicast object) and an NCCL device communicator
+ * with max_rows LSA barriers. Collective: every rank of `comm` calls it. *local_buf = this rank's
+ * copy (device, 4 KB aligned): a row-parallel linear writes its bf16 partial there (dak_linear y).
+ * Errors: DAK_EUNSUPPORTED (one rank, no multicast team, NCCL < 2.28: keep the ncclAllReduce
+ * path), DAK_ENCCL, DAK_EINVAL. */
+dak_status dak_nvls_create(void* comm, size_t bytes, int32_t max_rows, void** nvls, void** local_buf);
+dak_status dak_nvls_destroy(void* nvls);
+void* dak_nvls_local(void* nvls);
+/* One kernel: LSA barrier; two-shot sum of the ranks' partials [rows, cols] at `offset` in the
+ * window (rank r reduces rows i % world == r in the switch with multimem.ld_reduce, fp32
+ * accumulation, and broadcasts them with multimem.st); barrier; x += sum (bf16 RNE); if norm_w:
+ * y_norm = RMSNorm(x) * norm_w (as dak_allreduce_residual_rmsnorm). rows <= max_rows, cols % 8 == 0,
+ * cols <= 16384. Every rank launches it for the same (offset, rows, cols). */
+dak_status dak_nvls_residual_rmsnorm(void* nvls, size_t offset, void* x, int32_t rows, int32_t cols, const void* norm_w,
+                                     float eps, void* y_norm, dak_stream_t stream);
+
 /* =============================================================================================
  * 5. Decoder-layer decode step (the split operators as drop-in replacements inside
  *    the model; whole decode step CUDA-graph captured) and its glue kernels
@@ -544,6 +561,10 @@ typedef struct {
                                       /* combine also writes RMSNorm(x) * next_ln_w (the next    */
                                       /* layer's RMSNorm 1) into the scratch for a next call with */
                                       /* x_prenormed = 1 and the same scratch; NULL: off          */
+  void* nvls;                         /* Llama, fuse_norm 0, comm set: dak_nvls_create handle of */
+                                      /* >= B * hidden * 2 bytes, B <= max_rows: o / down write    */
+                                      /* their partials into its window and combine with          */
+                                      /* dak_nvls_residual_rmsnorm (no ncclAllReduce); NULL: NCCL */
 } dak_layer_args;
 
 dak_status dak_layer_scratch_size(const dak_layer_args* args, size_t* bytes);

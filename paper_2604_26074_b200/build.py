@@ -17,6 +17,13 @@ OUT = os.path.join(PKG, "libdak.so")
 OBJ = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL >= 2.28 headers (device API) shipped with torch's NCCL wheel (only nvls.cu uses them)
+NCCL_INC = ""
+try:
+    import nvidia.nccl as _nn
+    NCCL_INC = os.path.join(list(_nn.__path__)[0], "include")
+except Exception:
+    pass
 
 SOURCES = [
     ("abi.cpp", []),
@@ -32,6 +39,7 @@ SOURCES = [
     ("prefill.cu", []),
     ("layer.cu", []),
     ("tp.cu", []),
+    ("nvls.cu", ["-I", NCCL_INC]),
 ]
 
 

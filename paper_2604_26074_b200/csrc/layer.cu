@@ -418,7 +418,9 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   void* gu = sc + s.f;
   void* f2 = sc + s.f2;
   void* hbuf = sc + s.h;  // normalised x (unfused) -- the TP partial also lives here, never both at once
-  void* partial = sc + s.h;
+  // NVLS combine (unfused TP): the partials go into the symmetric window, one combine kernel
+  const bool nv = a->nvls != nullptr && a->comm != nullptr && a->fuse_norm == 0;
+  void* partial = nv ? dak_nvls_local(a->nvls) : sc + s.h;
   float* o_stats = (float*)(sc + s.stats);
   const int B = a->B, H = a->hidden, d = a->head_dim, Hq = a->n_heads, Hkv = a->n_kv_heads, F = a->ffn;
   const long long qkv_cols = (long long)(Hq + 2 * Hkv) * d;
@@ -493,7 +495,9 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   }
   // unfused TP: the combine kernel also writes RMSNorm 2 of the new x into hbuf (aliases partial)
   const bool norm2_done = tp && !fuse;
-  if (norm2_done) {
+  if (norm2_done && nv) {
+    if ((st = dak_nvls_residual_rmsnorm(a->nvls, 0, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, strm)) != DAK_OK) return st;
+  } else if (norm2_done) {
     if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
       return st;
   } else if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? o_stats : nullptr, pdl, strm)) != DAK_OK) {
@@ -514,7 +518,9 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
       return st;
     if (!tp && fuse) l.stats_out = a->stats_out;
     if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (tp && !fuse && a->next_ln_w) {  // the next layer's RMSNorm 1 in the same combine kernel
+    if (nv) {  // NVLS: one kernel (the next layer's RMSNorm 1 too when given)
+      if ((st = dak_nvls_residual_rmsnorm(a->nvls, 0, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, strm)) != DAK_OK) return st;
+    } else if (tp && !fuse && a->next_ln_w) {  // the next layer's RMSNorm 1 in the same combine kernel
       if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
         return st;
     } else if (tp && (st = dak_allreduce_residual(a->comm, partial, a->x, B, H, fuse ? a->stats_out : nullptr, pdl, strm)) != DAK_OK) {

@@ -431,7 +431,7 @@ class dak_layer_args(C.Structure):
                 ("l2_prefetch_bytes", C.c_int64), ("next_w_hbm", C.c_void_p), ("next_w_hbm_bytes", C.c_int64),
                 ("fuse_norm", C.c_int32), ("stats_in_parts", C.c_int32), ("stats_in", C.c_void_p),
                 ("stats_out", C.c_void_p), ("rope_theta", C.c_float), ("reserved4", C.c_int32), ("comm", C.c_void_p),
-                ("next_ln_w", C.c_void_p)]
+                ("next_ln_w", C.c_void_p), ("nvls", C.c_void_p)]
 
 
 _sig("dak_layernorm", C.c_int32, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
@@ -493,6 +493,30 @@ def comm_size(comm) -> int:
 
 def allgather_cols(comm, send, recv, scratch, N, Ml, stream=None):
     _check(lib.dak_allgather_cols(comm, _ptr(send), _ptr(recv), _ptr(scratch), int(N), int(Ml), _stream(stream)))
+
+
+_sig("dak_nvls_create", C.c_int32, [C.c_void_p, C.c_size_t, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)])
+_sig("dak_nvls_destroy", C.c_int32, [C.c_void_p])
+_sig("dak_nvls_local", C.c_void_p, [C.c_void_p])
+_sig("dak_nvls_residual_rmsnorm", C.c_int32, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
+                                              C.c_float, C.c_void_p, C.c_void_p])
+EXPORTED += ["dak_nvls_create", "dak_nvls_destroy", "dak_nvls_local", "dak_nvls_residual_rmsnorm"]
+
+
+def nvls_create(comm, nbytes: int, max_rows: int):
+    """-> (handle, local window pointer); raises DakError EUNSUPPORTED without a multicast team."""
+    h, buf = C.c_void_p(), C.c_void_p()
+    _check(lib.dak_nvls_create(comm, int(nbytes), int(max_rows), C.byref(h), C.byref(buf)))
+    return h.value, buf.value
+
+
+def nvls_destroy(h):
+    _check(lib.dak_nvls_destroy(h))
+
+
+def nvls_residual_rmsnorm(h, offset, x, rows, cols, norm_w, eps, y_norm, stream=None):
+    _check(lib.dak_nvls_residual_rmsnorm(h, int(offset), _ptr(x), int(rows), int(cols), _ptr(norm_w), float(eps),
+                                         _ptr(y_norm), _stream(stream)))
 
 
 def comm_destroy(comm):

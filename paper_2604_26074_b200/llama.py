@@ -44,7 +44,8 @@ class DakLlama(_DecodeEngine):
     def __init__(self, cfg: LlamaConfig, batch: int, context: int, hw: HW, tp_rank: int = 0, tp_size: int = 1,
                  comm=None, mode: int = dak.PLAN_BALANCED, y_req: int = 0, unit_rows: int = 16, page_size: int = 64,
                  chunk_pages: int = 0, seed: int = 0, pdl: bool = True, congestion_control: bool = True,
-                 weights: dict | None = None, n_cta_host: int = 2, fuse_norm: bool | None = None):
+                 weights: dict | None = None, n_cta_host: int = 2, fuse_norm: bool | None = None,
+                 nvls: bool = False):
         self.cfg = cfg
         self.rank, self.world, self.comm = tp_rank, tp_size, comm
         # operand transforms fused into the linears only at small batch: above 16 columns every CTA
@@ -57,6 +58,11 @@ class DakLlama(_DecodeEngine):
         self._plan(mode, y_req)
         self._allocate(weights)
         self._kv_pools(self.dims["n_kv"], cfg.head_dim)
+        # NVLS combine (unfused TP path): o / down partials into a symmetric NCCL window, one
+        # combine kernel with the reduction in the NVSwitch (dak_nvls_create; collective call)
+        self.nvls = None
+        if nvls and comm and not self.fuse_norm:
+            self.nvls, _ = dak.nvls_create(comm, batch * cfg.hidden * 2, batch)
         self._layer_setup()
 
     def _model_desc(self):
@@ -131,6 +137,7 @@ class DakLlama(_DecodeEngine):
         if not self.fuse_norm and self.comm:  # the down combine writes the next layer's RMSNorm 1
             a.x_prenormed = int(l > 0)
             a.next_ln_w = self.layers[l + 1]["ln1_w"].data_ptr() if l + 1 < c.n_layers else None
+        a.nvls = self.nvls
         a.cfg = dak.launch_cfg(**self.launch)
         a.attn_cfg = dak.launch_cfg(**self.attn_launch)
         return a
@@ -149,6 +156,12 @@ class DakLlama(_DecodeEngine):
             dak.rmsnorm(self.x, self.lnf_w, self.hnorm, self.B, c.hidden, c.rms_eps, pdl=self.pdl, stream=stream)
             ha = self._head_args(self.hnorm, self.logits)
         dak.linear(ha, stream)
+
+    def close(self):
+        if getattr(self, "nvls", None):
+            dak.nvls_destroy(self.nvls)
+            self.nvls = None
+        super().close()
 
     def _reduce_launches(self, op) -> int:
         """1 when this linear splits K on the tcgen05 path (one split-K reduce kernel), else 0."""

@@ -42,6 +42,19 @@ def test_allgather_cols_one_rank(N, Ml, use_comm):
         dak.comm_destroy(comm)
 
 
+def test_nvls_needs_a_multicast_team():
+    """dak_nvls_create refuses a one-rank communicator cleanly (EUNSUPPORTED: the engine keeps the
+    ncclAllReduce combine), and the combine kernel rejects bad shapes."""
+    from paper_2604_26074_b200 import dak
+    comm = dak.comm_init(dak.comm_unique_id(), 0, 1)
+    with pytest.raises(dak.DakError) as e:
+        dak.nvls_create(comm, 1 << 20, 64)
+    assert e.value.code in ("EUNSUPPORTED",)
+    dak.comm_destroy(comm)
+    with pytest.raises(dak.DakError):
+        dak.nvls_residual_rmsnorm(None, 0, None, 4, 8192, None, 1e-5, None)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -100,11 +113,32 @@ def _tp_worker(rank, world, uid, q):
         dak.allgather_cols(comm, yl, y, scratch, N, Ml)
         torch.cuda.synchronize()
         yg = Kx.bf16_to_f64(from_dev(y))
-        q.put((rank, got, ref_shard, yg, Kx.linear(W, x)))
+        # NVLS combine (unfused TP path, batch 24): the same layer with the switch reduction
+        nv_res = None
+        Bn = 24
+        tok_n = (np.arange(Bn) * 7 + 1) % V
+        Kn = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(Bn)] for _ in range(L)]
+        Vn = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(Bn)] for _ in range(L)]
+        try:
+            eng2 = DakLlama(cfg, Bn, ctx, hw, tp_rank=rank, tp_size=world, comm=comm, mode=dak.PLAN_EXACT, y_req=0,
+                            page_size=64, chunk_pages=1, weights=dev, nvls=True)
+        except dak.DakError as e:
+            nv_res = ("unsupported", str(e))
+        else:
+            eng2.load_kv([[k[:, kvr] for k in layer] for layer in Kn], [[v[:, kvr] for v in layer] for layer in Vn])
+            eng2.tokens.copy_(torch.from_numpy(tok_n.astype(np.int32)))
+            eng2.capture(s)
+            eng2.graph.replay()
+            torch.cuda.synchronize()
+            got2 = Kx.bf16_to_f64(eng2.logits.view(torch.int16).cpu().numpy().view(np.uint16))
+            ref2, _ = Ly.llama_decode_step(tok_n, np.full(Bn, ctx - 1), p, Kn, Vn, nh, nkv)
+            nv_res = (got2, ref2[:, vr])
+            eng2.close()
+        q.put((rank, got, ref_shard, yg, Kx.linear(W, x), nv_res))
         dak.comm_destroy(comm)
     except Exception as e:  # surface the failure in the parent
         import traceback
-        q.put((rank, "error", traceback.format_exc(), None, None))
+        q.put((rank, "error", traceback.format_exc(), None, None, None))
 
 
 @pytest.mark.parametrize("world", [2, 8])
@@ -123,7 +157,9 @@ def test_tp_layer_multi_rank_matches_oracle(world):
     res = [q.get(timeout=600) for _ in procs]
     for pr in procs:
         pr.join(timeout=120)
-    for rank, got, ref, yg, yref in res:
+    for rank, got, ref, yg, yref, nv in res:
         assert not isinstance(got, str), ref
         assert_close(got, ref, rtol=3e-2)
         assert_close(yg, yref)
+        if nv[0] != "unsupported":  # NVSwitch box: the NVLS combine must match the oracle too
+            assert_close(nv[0], nv[1], rtol=3e-2)
