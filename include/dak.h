@@ -407,8 +407,8 @@ dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t 
  * 0 .. seq_lens[b] - T + i (causal), kv head g = h / (Hq / Hkv):
  *   out[b, i, h] = softmax(scale * K_b[0 .. L-T+i] q[b, i, h]) V_b[0 .. L-T+i].
  * One CTA per (request, kv head, 128 query rows (token, head of the group)); 64-token K / V tiles
- * stream in key order from the tier each page's block-table entry names (bit 31 = host pool), so
- * the result is bitwise independent of the tier split. */
+ * stream newest keys first from the tier each page's block-table entry names (bit 31 = host pool),
+ * so the result is bitwise independent of the tier split. */
 typedef struct {
   const void* q;                /* [B, T, Hq, d] bf16, device                                   */
   void* out;                    /* [B, T, Hq, d] bf16, device                                   */
@@ -420,11 +420,21 @@ typedef struct {
   int32_t page_size;            /* multiple of 64 tokens                                        */
   int32_t max_pages;
   float scale;                  /* <= 0: 1/sqrt(d)                                              */
-  dak_launch_cfg cfg;           /* stages (ring depth, 0: 6) is honoured                         */
+  dak_launch_cfg cfg;           /* stages (ring depth, 0: 6); n_cta_host = host streamer CTAs    */
+  void* workspace;              /* device, >= dak_prefill_workspace_size, or NULL (see below)    */
+  size_t workspace_bytes;
 } dak_prefill_args;
 
-/* Errors: DAK_EINVAL (NULL / misaligned / non-positive sizes, Hq % Hkv), DAK_EUNSUPPORTED (d != 128,
- * page_size % 64). seq_lens are not checked on the host (device data). */
+/* Host tier (one tier per SM): with a workspace, cfg.n_cta_host (default 4) streamer CTAs
+ * read every host page of the batch ONCE over the link into a device staging pool (newest pages
+ * first) while the compute CTAs work newest-keys-first from HBM; a compute CTA reads a host-tier
+ * tile from the staging pool once its page flag is up. Without a workspace every CTA reads host
+ * tiles over the link itself: each host byte crosses the link once per query block of its
+ * (request, kv head) -- Table 1's read amplification. Either way the result is the
+ * same bits (keys are consumed newest first whatever their tier).
+ * Errors: DAK_EINVAL (NULL / misaligned / non-positive sizes, Hq % Hkv, workspace too small),
+ * DAK_EUNSUPPORTED (d != 128, page_size % 64). seq_lens are not checked on the host (device data). */
+dak_status dak_prefill_workspace_size(const dak_prefill_args* args, size_t* bytes);
 dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stream);
 
 /* =============================================================================================

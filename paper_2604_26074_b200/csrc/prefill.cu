@@ -48,6 +48,13 @@ struct Params {
   int B, T, Hq, Hkv, G, page, max_pages;
   int blocks_per_bg;  // CTAs per (request, kv head)
   int stages;
+  // host-tier streaming (workspace given): CTAs [0, n_stream) copy every host page of the batch once
+  // over the link into the device staging pool (newest pages first) and raise its flag; compute
+  // CTAs read host-tier tiles from the staging pool after the flag (no read amplification)
+  int n_stream;
+  char* k_stage;
+  char* v_stage;
+  int* flags;  // [B][Hkv][max_pages]
   float scale_log2;
   unsigned long long* trace;
 };
@@ -122,6 +129,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
 __device__ __forceinline__ uint32_t pg_off(int t, int j) {
   return (uint32_t)(t * (kD * 2) + ((((j >> 3) << 3) | ((j & 7) ^ (t & 7))) << 4));
 }
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
   if (tr && blockIdx.x < kTraceCtas) {
     unsigned long long t;
@@ -137,7 +148,72 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   uint64_t* empty = full + kMaxStages;
   unsigned char* ring = smem + 1024;  // [stages][K tile | V tile]
 
-  const int bg = blockIdx.x / p.blocks_per_bg, blk = blockIdx.x % p.blocks_per_bg;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = p.stages;
+  const int page_bytes = p.page * kD * 2;
+  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer (an SM reads one tier)
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < kMaxStages; ++s) mbar_init(&full[s], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    // items: host pages (b, g, page), newest page first (the compute CTAs consume keys newest first);
+    // this CTA takes items n_stream apart. A slot holds one page of K and one of V.
+    const int n_items_max = p.max_pages * p.B * p.Hkv;
+    auto item = [&](int k, int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {  // k-th item of the scan
+      const int pg = p.max_pages - 1 - k / (p.B * p.Hkv);
+      const int b2 = (k / p.Hkv) % p.B, g2 = k % p.Hkv;
+      const int filled = (p.seq_lens[b2] + p.page - 1) / p.page;
+      if (pg >= filled) return false;
+      e_ = (uint32_t)p.block_table[(long long)b2 * p.max_pages + pg];
+      if (!(e_ & kHostBit)) return false;
+      b_ = b2; g_ = g2; pg_ = pg;
+      return true;
+    };
+    // my items, in scan order
+    int k = 0, mine = 0;
+    auto next_mine = [&](int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {
+      for (; k < n_items_max; ++k)
+        if (item(k, b_, g_, pg_, e_) && (mine++ % p.n_stream) == (int)blockIdx.x) { ++k; return true; }
+      return false;
+    };
+    int qb[kMaxStages], qg[kMaxStages], qp[kMaxStages];
+    int issued = 0, done = 0;
+    auto issue = [&](int slot) -> bool {
+      int b_, g_, pg_;
+      uint32_t e_;
+      if (!next_mine(b_, g_, pg_, e_)) return false;
+      const long long off = ((long long)(e_ & ~kHostBit) * p.Hkv + g_) * page_bytes;
+      unsigned char* dst = ring + (size_t)slot * 2 * kTileBytes * (p.page / kTile);
+      mbar_expect_tx(&full[slot], 2u * page_bytes);
+      bulk_g2s(dst, p.k_host + off, page_bytes, &full[slot]);
+      bulk_g2s(dst + page_bytes, p.v_host + off, page_bytes, &full[slot]);
+      qb[slot] = b_; qg[slot] = g_; qp[slot] = pg_;
+      ++issued;
+      return true;
+    };
+    const int SS = S * kTile / p.page > 0 ? S * kTile / p.page : 1;  // page slots in the ring
+    for (int sl = 0; sl < SS && issue(sl); ++sl) {}
+    while (done < issued) {
+      const int sl = done % SS;
+      mbar_wait(&full[sl], (uint32_t)((done / SS) & 1));
+      const long long so = (((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl]) * page_bytes;
+      unsigned char* src = ring + (size_t)sl * 2 * kTileBytes * (p.page / kTile);
+      bulk_s2g(p.k_stage + so, src, page_bytes);
+      bulk_s2g(p.v_stage + so, src + page_bytes, page_bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      int* f = p.flags + ((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl];
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+      ++done;
+      issue(sl);
+    }
+    return;
+  }
+  const int cta = (int)blockIdx.x - p.n_stream;
+  const int bg = cta / p.blocks_per_bg, blk = cta % p.blocks_per_bg;
   const int b = bg / p.Hkv, g = bg % p.Hkv;
   const int L = p.seq_lens[b];
   const int rows = p.T * p.G;            // query rows of (b, g): row r = (token r / G, head r % G)
@@ -145,7 +221,6 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   const int r_last = min(rows, r0 + kRows) - 1;
   const int kmax = L - p.T + r_last / p.G + 1;  // keys [0, kmax) cover every row of the block
   const int ntiles = (kmax + kTile - 1) / kTile;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kMaxStages; ++s) {
@@ -156,24 +231,39 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
     tstamp(p.trace, 0);
   }
   __syncthreads();
-  const int S = p.stages;
-  const int page_bytes = p.page * kD * 2;
 
-  if (warp == kConsumers) {  // ---- producer: K and V tile of every key block, in key order
+  if (warp == kConsumers) {  // ---- producer: K and V tile of every key block, newest keys first
     if (lane == 0) {
       const int* bt = p.block_table + (long long)b * p.max_pages;
       int s = 0;
       uint32_t ph = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
-        const int key0 = t * kTile;
-        const uint32_t e = (uint32_t)bt[key0 / p.page];
+      for (int i = 0; i < ntiles; ++i) {
+        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        const int key0 = (ntiles - 1 - i) * kTile;
+        const int pg = key0 / p.page;
+        const uint32_t e = (uint32_t)bt[pg];
         const bool host = (e & kHostBit) != 0;
-        const long long off = ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + (long long)(key0 % p.page) * kD * 2;
+        const long long in_page = (long long)(key0 % p.page) * kD * 2;
+        const char* ksrc = (host ? p.k_host : p.k_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
+        const char* vsrc = (host ? p.v_host : p.v_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
+        if (host && p.n_stream > 0) {  // staged copy once its flag is up (bounded wait: else read the link)
+          const long long so = (((long long)b * p.Hkv + g) * p.max_pages + pg) * page_bytes + in_page;
+          const int* f = p.flags + ((long long)b * p.Hkv + g) * p.max_pages + pg;
+          int ready = 0;
+          for (int it = 0; it < (1 << 22) && !ready; ++it) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
+            if (!ready) __nanosleep(64);
+          }
+          if (ready) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            ksrc = p.k_stage + so;
+            vsrc = p.v_stage + so;
+          }
+        }
         unsigned char* dst = ring + (size_t)s * 2 * kTileBytes;
         mbar_expect_tx(&full[s], 2u * kTileBytes);
-        bulk_g2s(dst, (host ? p.k_host : p.k_hbm) + off, kTileBytes, &full[s]);
-        bulk_g2s(dst + kTileBytes, (host ? p.v_host : p.v_hbm) + off, kTileBytes, &full[s]);
+        bulk_g2s(dst, ksrc, kTileBytes, &full[s]);
+        bulk_g2s(dst + kTileBytes, vsrc, kTileBytes, &full[s]);
         if (++s == S) { s = 0; ph ^= 1u; }
       }
     }
@@ -214,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   uint32_t ph = 0;
   for (int t = 0; t < ntiles; ++t) {
     mbar_wait(&full[s], ph);
-    const int key0 = t * kTile;
+    const int key0 = (ntiles - 1 - t) * kTile;  // newest keys first (the host prefix streams meanwhile)
     if (key0 < warp_lim) {  // tiles past every row of this warp only need the release below
       const uint32_t kb = su32(ring + (size_t)s * 2 * kTileBytes);
       const uint32_t vb = kb + kTileBytes;
@@ -354,11 +444,31 @@ static dak_status prefill_plan(const dak_prefill_args* a, pf::Params* p, int* gr
   if (q.stages < 2) q.stages = 2;
   const float scale = a->scale > 0.f ? a->scale : 1.0f / sqrtf((float)pf::kD);
   q.scale_log2 = scale * 1.4426950408889634f;
-  const long long g = (long long)a->B * a->Hkv * q.blocks_per_bg;
+  // host-tier streaming through the caller's workspace: [flags][K stage][V stage]
+  const size_t flag_bytes = ((size_t)a->B * a->Hkv * a->max_pages * 4 + 255) / 256 * 256;
+  const size_t stage_bytes = (size_t)a->B * a->Hkv * a->max_pages * a->page_size * pf::kD * 2;
+  q.n_stream = 0;
+  if (a->workspace && a->k_host) {
+    if (a->workspace_bytes < flag_bytes + 2 * stage_bytes || !aligned16(a->workspace))
+      return fail(DAK_EINVAL, "dak_prefill_attention: workspace %zu < %zu", a->workspace_bytes, flag_bytes + 2 * stage_bytes);
+    q.n_stream = a->cfg.n_cta_host > 0 ? a->cfg.n_cta_host : 4;
+    q.flags = (int*)a->workspace;
+    q.k_stage = (char*)a->workspace + flag_bytes;
+    q.v_stage = q.k_stage + stage_bytes;
+  }
+  const long long g = (long long)a->B * a->Hkv * q.blocks_per_bg + q.n_stream;
   if (g > 0x7fffffffLL) return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: grid too large");
   *p = q;
   *grid = (int)g;
   *smem = 1024 + q.stages * 2 * pf::kTileBytes + 1024;
+  return DAK_OK;
+}
+
+dak_status dak_prefill_workspace_size(const dak_prefill_args* a, size_t* bytes) {
+  if (!a || !bytes || a->B <= 0 || a->Hkv <= 0 || a->max_pages <= 0 || a->page_size <= 0)
+    return fail(DAK_EINVAL, "dak_prefill_workspace_size: bad arguments");
+  const size_t flag_bytes = ((size_t)a->B * a->Hkv * a->max_pages * 4 + 255) / 256 * 256;
+  *bytes = flag_bytes + 2 * (size_t)a->B * a->Hkv * a->max_pages * a->page_size * pf::kD * 2;
   return DAK_OK;
 }
 
@@ -373,6 +483,8 @@ dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stre
                                       1024 + pf::kMaxStages * 2 * pf::kTileBytes + 1024));
     attr = true;
   }
+  if (p.n_stream > 0)  // staged-page flags start lowered (a memset node under graph capture)
+    DAK_CUDA_TRY(cudaMemsetAsync(p.flags, 0, (size_t)args->B * args->Hkv * args->max_pages * 4, (cudaStream_t)stream));
   p.trace = trace_slot(DAK_KIND_PREFILL, args->B, args->T, grid);
   pf::prefill_attention_kernel<<<grid, pf::kThreads, smem, (cudaStream_t)stream>>>(p);
   DAK_CUDA_TRY(cudaGetLastError());

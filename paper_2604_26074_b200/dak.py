@@ -381,15 +381,25 @@ class dak_prefill_args(C.Structure):
     _fields_ = [("q", C.c_void_p), ("out", C.c_void_p), ("k_hbm", C.c_void_p), ("v_hbm", C.c_void_p),
                 ("k_host", C.c_void_p), ("v_host", C.c_void_p), ("block_table", C.c_void_p), ("seq_lens", C.c_void_p),
                 ("B", C.c_int32), ("T", C.c_int32), ("Hq", C.c_int32), ("Hkv", C.c_int32), ("d", C.c_int32),
-                ("page_size", C.c_int32), ("max_pages", C.c_int32), ("scale", C.c_float), ("cfg", dak_launch_cfg)]
+                ("page_size", C.c_int32), ("max_pages", C.c_int32), ("scale", C.c_float), ("cfg", dak_launch_cfg),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_size_t)]
 
 
 _sig("dak_prefill_attention", C.c_int32, [C.POINTER(dak_prefill_args), C.c_void_p])
-EXPORTED += ["dak_prefill_attention"]
+_sig("dak_prefill_workspace_size", C.c_int32, [C.POINTER(dak_prefill_args), C.POINTER(C.c_size_t)])
+EXPORTED += ["dak_prefill_attention", "dak_prefill_workspace_size"]
+
+
+def prefill_workspace_size(B, Hkv, page_size, max_pages) -> int:
+    a = dak_prefill_args()
+    a.B, a.Hkv, a.page_size, a.max_pages = int(B), int(Hkv), int(page_size), int(max_pages)
+    v = C.c_size_t()
+    _check(lib.dak_prefill_workspace_size(C.byref(a), C.byref(v)))
+    return v.value
 
 
 def prefill_attention(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_lens, B, T, Hq, Hkv, d, page_size,
-                      max_pages, scale=0.0, cfg=None, stream=None):
+                      max_pages, scale=0.0, cfg=None, stream=None, workspace=None, workspace_bytes=0):
     a = dak_prefill_args()
     a.q, a.out = _ptr(q), _ptr(out)
     a.k_hbm, a.v_hbm, a.k_host, a.v_host = _ptr(k_hbm), _ptr(v_hbm), _ptr(k_host), _ptr(v_host)
@@ -397,6 +407,7 @@ def prefill_attention(q, out, k_hbm, v_hbm, k_host, v_host, block_table, seq_len
     a.B, a.T, a.Hq, a.Hkv, a.d = int(B), int(T), int(Hq), int(Hkv), int(d)
     a.page_size, a.max_pages, a.scale = int(page_size), int(max_pages), float(scale)
     a.cfg = cfg if isinstance(cfg, dak_launch_cfg) else launch_cfg(**(cfg or {}))
+    a.workspace, a.workspace_bytes = _ptr(workspace), int(workspace_bytes)
     _check(lib.dak_prefill_attention(C.byref(a), _stream(stream)))
 
 

@@ -15,7 +15,7 @@ def D():
     return dak
 
 
-def run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed, kind="normal", cp=1, **cfg):
+def run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed, kind="normal", cp=1, stage=True, **cfg):
     import torch
     from tests.gpu_util import make_paged_kv, PagedKV, to_dev, from_dev
     d = 128
@@ -26,8 +26,11 @@ def run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed, kind="normal", cp=1, **cfg)
     qd = to_dev(q)
     out = torch.full((B, T, Hq, d), 0x7FC0, dtype=torch.int16, device="cuda")  # NaN fill: every row must be written
     sl = torch.tensor(Ls, dtype=torch.int32, device="cuda")
+    ws = None
+    if stage:  # host streamer CTAs + device staging pool (each host page crosses the link once)
+        ws = torch.empty(D.prefill_workspace_size(B, Hkv, page, bt.shape[1]), dtype=torch.uint8, device="cuda")
     D.prefill_attention(qd, out, kv.kg, kv.vg, kv.kh.dp, kv.vh.dp, kv.bt, sl, B, T, Hq, Hkv, d, page, bt.shape[1],
-                        cfg=cfg)
+                        cfg=cfg, workspace=ws, workspace_bytes=ws.numel() if ws is not None else 0)
     torch.cuda.synchronize()
     ref = Kx.paged_prefill_attention(q, kg, vg, kh, vh, bt, Ls, page)
     return from_dev(out), ref, n_host
@@ -43,10 +46,11 @@ CASES = [  # (seq lens, T, Hkv, Hq, page, host fraction)
 ]
 
 
+@pytest.mark.parametrize("stage", [True, False])
 @pytest.mark.parametrize("Ls,T,Hkv,Hq,page,frac", CASES)
-def test_prefill_parity(D, Ls, T, Hkv, Hq, page, frac):
+def test_prefill_parity(D, Ls, T, Hkv, Hq, page, frac, stage):
     from tests.gpu_util import assert_close
-    got, ref, _ = run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed=700 + T)
+    got, ref, _ = run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed=700 + T, stage=stage)
     assert_close(Kx.bf16_to_f64(got), ref)
 
 
@@ -58,12 +62,14 @@ def test_prefill_score_ranges(D, kind):
 
 
 def test_prefill_r_invariance_and_stages_bitwise(D):
-    """The same logical KV with 0 / 50 / 100 % of its pages on the host, and any ring depth, gives
-    bitwise the same output (tiles are consumed in key order whatever their tier)."""
+    """The same logical KV with 0 / 50 / 100 % of its pages on the host, any ring depth, host pages
+    streamed through the staging pool or read directly, any streamer count: bitwise the same output
+    (tiles are consumed newest keys first whatever their tier or path)."""
     base, _, _ = run_prefill(D, [700, 260], 120, 2, 16, 64, 0.0, seed=21)
-    for frac, st in ((0.5, 0), (1.0, 0), (0.5, 2), (0.0, 3)):
-        got, _, _ = run_prefill(D, [700, 260], 120, 2, 16, 64, frac, seed=21, stages=st)
-        assert np.array_equal(got, base), (frac, st)
+    for frac, st, stage, nh in ((0.5, 0, True, 0), (1.0, 0, True, 1), (0.5, 2, False, 0), (0.0, 3, True, 0),
+                                (1.0, 0, False, 0), (0.5, 0, True, 7)):
+        got, _, _ = run_prefill(D, [700, 260], 120, 2, 16, 64, frac, seed=21, stages=st, stage=stage, n_cta_host=nh)
+        assert np.array_equal(got, base), (frac, st, stage, nh)
 
 
 def test_prefill_errors(D):
