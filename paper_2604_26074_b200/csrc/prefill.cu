@@ -8,8 +8,8 @@
 // CTA reads each tile once for all of them. Warps 0-7 each own 16 query rows (FlashAttention-2
 // style, mma.sync m16n8k16 -> fp32: S = Q K^T in bf16 with K rows via ldmatrix, online softmax in
 // the exp2 domain in registers, O += P V in fp16 with P re-used from the S accumulators as the A
-// operand and V via ldmatrix.trans converted bf16 -> fp16 in registers (exact for |v| <= 65504,
-// saturating beyond; reading R20 of DESIGN.md)); warp 8 lane 0 streams 64-token K and V tiles of the CTA's causal key range
+// operand and V via ldmatrix.trans, the V tile converted bf16 -> fp16 in shared memory once per
+// CTA by a convert warp (exact for |v| <= 65504, saturating beyond; reading R20 of DESIGN.md)); warp 8 lane 0 streams 64-token K and V tiles of the CTA's causal key range
 // [0, kmax) into a ring of shared-memory stages with 1-D bulk copies (cp.async.bulk), each tile from
 // the tier its page's block-table entry names (bit 31: host pool over the link, else HBM).
 // Tiles are consumed in key order: the reduction order of a row depends on (seq_len, T) only, never
@@ -29,7 +29,7 @@ namespace pf {
 
 constexpr int kD = 128;
 constexpr int kConsumers = 8;
-constexpr int kThreads = (kConsumers + 1) * 32;
+constexpr int kThreads = (kConsumers + 2) * 32;  // + producer warp + V-convert warp
 constexpr int kRows = kConsumers * 16;  // query rows per CTA
 constexpr int kTile = 64;               // keys per stage
 constexpr int kTileBytes = kTile * kD * 2;
@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
+  uint64_t* vready = empty + kMaxStages;  // V tile of the slot converted to fp16 in place
   unsigned char* ring = smem + 1024;  // [stages][K tile | V tile]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumers);
+      mbar_init(&vready[s], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
@@ -266,6 +268,25 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
         bulk_g2s(dst + kTileBytes, vsrc, kTileBytes, &full[s]);
         if (++s == S) { s = 0; ph ^= 1u; }
       }
+    }
+    return;
+  }
+
+  if (warp == kConsumers + 1) {  // ---- V tiles bf16 -> fp16 in place, once per CTA (P V runs in fp16)
+    int s = 0;
+    uint32_t ph = 0;
+    for (int i = 0; i < ntiles; ++i) {
+      mbar_wait(&full[s], ph);
+      uint4* v = reinterpret_cast<uint4*>(ring + (size_t)s * 2 * kTileBytes + kTileBytes);
+#pragma unroll 4
+      for (int c = lane; c < kTileBytes / 16; c += 32) {
+        uint4 u = v[c];
+        u.x = bf2_to_h2(u.x); u.y = bf2_to_h2(u.y); u.z = bf2_to_h2(u.z); u.w = bf2_to_h2(u.w);
+        v[c] = u;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&vready[s]);
+      if (++s == S) { s = 0; ph ^= 1u; }
     }
     return;
   }
@@ -369,7 +390,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
       for (int i = 0; i < kD / 8; ++i) {
         o[i][0] *= al0; o[i][1] *= al0; o[i][2] *= al1; o[i][3] *= al1;
       }
-      // ---- O += P V : V rows [key][d] through ldmatrix.trans (B operand, k = keys)
+      // ---- O += P V : V rows [key][d] (fp16 after the convert warp) through ldmatrix.trans
+      mbar_wait(&vready[s], ph);
 #pragma unroll
       for (int kk = 0; kk < kTile / 16; ++kk) {
 #pragma unroll
@@ -377,8 +399,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
           const int mtx = lane >> 3;
           uint32_t b0, b1, b2, b3;
           ldsm_x4_t(vb + pg_off(16 * kk + ((mtx & 1) << 3) + (lane & 7), i + (mtx >> 1)), b0, b1, b2, b3);
-          mma_f16(o[i], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], bf2_to_h2(b0), bf2_to_h2(b1));
-          mma_f16(o[i + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], bf2_to_h2(b2), bf2_to_h2(b3));
+          mma_f16(o[i], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b0, b1);
+          mma_f16(o[i + 1], pa[kk][0], pa[kk][1], pa[kk][2], pa[kk][3], b2, b3);
         }
       }
     }
