@@ -291,7 +291,8 @@ def make_llama(a, hw, world, rank, dak):
     budget = int(168e9 * layers / cfg.__class__().n_layers)
     y_req, R = dak.global_offload_bytes(w_bytes, kv_bytes, budget)
     eng = DakLlama(cfg, batch, context, hw, tp_rank=rank, tp_size=tp_size, comm=comm, mode=dak.PLAN_EXACT,
-                   y_req=y_req, pdl=not a.no_pdl, congestion_control=not a.no_cc, seed=1234 + rank)
+                   y_req=y_req, pdl=not a.no_pdl, congestion_control=not a.no_cc, seed=1234 + rank,
+                   chunk_pages=a.chunk_pages, nvls=a.nvls and world > 1)
     wl = dict(workload="llama3-70b-tp8-b%d-ctx%d" % (batch, context), model_shape="Llama-3-70B (TP%d shard)" % tp_size,
               batch=batch, context=context, layers=layers, layers_model=80,
               extrapolation="x%d per token step" % (80 // layers) if layers != 80 else None,
@@ -325,6 +326,8 @@ def main():
     ap.add_argument("--context", type=int, default=64)
     ap.add_argument("--no-pdl", action="store_true")
     ap.add_argument("--no-cc", action="store_true")
+    ap.add_argument("--chunk-pages", type=int, default=0, help="split-KV chunk in pages (0: the engine's rule)")
+    ap.add_argument("--nvls", action="store_true", help="Llama TP (>= 2 ranks): NVLS combine instead of ncclAllReduce")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--l2-prefetch-mb", type=float, default=0.0, help="L2 warm-up of the next linear (0: off)")
@@ -365,14 +368,14 @@ def main():
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
                      evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
-                     seed=1234 + rank)
+                     seed=1234 + rank, chunk_pages=a.chunk_pages)
         if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
             tot = sum(o["total_bytes"] for o in eng.plan_ops)
             eng.close()
             eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                          congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
                          evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
-                     seed=1234 + rank)
+                     seed=1234 + rank, chunk_pages=a.chunk_pages)
     nb = eng.bytes_per_step()
     stream = torch.cuda.Stream()
     g = eng.capture(stream)

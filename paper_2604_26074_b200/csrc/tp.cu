@@ -274,7 +274,12 @@ dak_status dak_allreduce_residual(void* comm, void* partial, void* x, int32_t ro
     tp::Nccl* n;
     dak_status st = tp::nccl(&n);
     if (st != DAK_OK) return st;
-    DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+    int world = 1;  // a one-rank communicator has nothing to exchange: no collective launch
+    DAK_NCCL_TRY(n, n->comm_count((ncclComm_t)comm, &world));
+    if (world > 1)
+      DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+    else
+      comm = nullptr;  // PDL stays allowed below (no NCCL kernel in between)
   }
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -351,7 +356,12 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
     tp::Nccl* n;
     dak_status st = tp::nccl(&n);
     if (st != DAK_OK) return st;
-    DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+    int world = 1;  // a one-rank communicator has nothing to exchange: no collective launch
+    DAK_NCCL_TRY(n, n->comm_count((ncclComm_t)comm, &world));
+    if (world > 1)
+      DAK_NCCL_TRY(n, n->all_reduce(partial, partial, (size_t)rows * cols, ncclBfloat16, ncclSum, (ncclComm_t)comm, s));
+    else
+      comm = nullptr;  // PDL stays allowed below (no NCCL kernel in between)
   }
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

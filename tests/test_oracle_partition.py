@@ -103,3 +103,64 @@ def test_attention_page_placement():
     assert Pt.host_pages_prefix(10, 0.0, 4) == 0
     assert Pt.host_pages_prefix(10, 1.0, 4) == 10
     assert Pt.batch_split_host_requests(8, 0.25) == 2
+
+
+def test_kv_place_chunk_major_pins():
+    """oracle.partition.kv_place_chunk_major (reading R15) against the per-request reading it
+    refines and invariants it must keep: when every request has the same chunk count and the host
+    units are a multiple of B, each request's host pages equal host_pages_prefix(ratio = units per
+    request / chunks); host pages always form a per-request prefix, at most one chunk apart between
+    requests (chunk-major = oldest first across requests), pool indices are a permutation, and
+    host_tokens counts exactly the cached tokens on host pages."""
+    import numpy as np
+    from fractions import Fraction
+    g = np.random.default_rng(77)
+    for _ in range(300):
+        B = int(g.integers(1, 7))
+        page = int(g.choice([16, 64]))
+        cp = int(g.integers(1, 4))
+        L = int(g.integers(1, 900))
+        pages = -(-L // page)
+        chunks = -(-pages // cp)
+        k = int(g.integers(0, chunks + 1))
+        table, nh, ng, ht = Pt.kv_place_chunk_major([L] * B, page, pages + 1, cp, k * B)
+        for b in range(B):
+            host = [(e & 0x80000000) != 0 for e in table[b]]
+            assert sum(host) == Pt.host_pages_prefix(pages, Fraction(k, chunks) if chunks else 0, cp)
+    for _ in range(300):
+        B = int(g.integers(1, 7))
+        page, cp = 16, int(g.integers(1, 4))
+        Ls = [int(g.integers(0, 300)) for _ in range(B)]
+        max_pages = max(1, max(-(-L // page) for L in Ls))
+        n_chunks = [-(-(-(-L // page)) // cp) for L in Ls]
+        hu = int(g.integers(0, sum(n_chunks) + 1))
+        table, nh, ng, ht = Pt.kv_place_chunk_major(Ls, page, max_pages, cp, hu)
+        hc = []
+        tok = 0
+        for b in range(B):
+            host = [(e & 0x80000000) != 0 for e in table[b]]
+            hp = sum(host)
+            assert host == [True] * hp + [False] * (max_pages - hp)  # prefix
+            hc.append(-(-hp // cp))
+            tok += min(hp * page, Ls[b])
+        assert sum(hc) == hu and ht == tok
+        full = [c for c, n in zip(hc, n_chunks) if c < n]  # requests not entirely on the host
+        if full:
+            assert max(full) - min(full) <= 1
+        idx_h = sorted(e & 0x7FFFFFFF for row in table for e in row if e & 0x80000000)
+        idx_g = sorted(e for row in table for e in row if not e & 0x80000000)
+        assert idx_h == list(range(nh)) and idx_g == list(range(ng))
+
+
+def test_linear_splitk_items_cover_rows():
+    """oracle.partition.linear_splitk_items: every row of each tier is owned by exactly `splits`
+    CTAs of that tier, in blocks of `block` rows (the last short), host tier first."""
+    for M, h, S in ((7168, 1024, 2), (1280, 128, 13), (1000, 0, 3), (300, 300, 4), (129, 1, 5)):
+        items = Pt.linear_splitk_items(M, h, S, 128)
+        cover = [0] * M
+        for tier, a, b in items:
+            assert (tier == "host") == (b <= h) and b - a <= 128 and a < b
+            for r in range(a, b):
+                cover[r] += 1
+        assert cover == [S] * M
+        assert [t for t, _, _ in items] == sorted([t for t, _, _ in items], key=lambda t: t != "host")
