@@ -315,7 +315,7 @@ typedef struct {
                                                       /* > 1 adds one split-K reduce launch     */
   int32_t host_gate;                                  /* split-K with congestion control: host   */
                                                       /* item CTAs streaming at once (0: no cap) */
-  int32_t reserved;
+  int32_t kblock;                                     /* split-K: rows per item (0: not split)   */
 } dak_linear_launch_info;
 
 dak_status dak_linear_query(const dak_linear_args* args, dak_linear_launch_info* info);
@@ -326,8 +326,8 @@ size_t dak_linear_workspace_size(const dak_linear_args* args);
 /* Row ownership of CTA `cta` (0 <= cta < grid): tier (0 HBM, 1 host) and [row_begin,row_end)
  * in global row numbering. Host CTAs split [0,h), HBM CTAs split [h,M), each into contiguous
  * ranges whose sizes differ by at most one row (8-row units on the tcgen05 path).
- * Split-K plans (ksplit > 1): CTA j of a tier owns the K split j % ksplit of the 128-row block
- * j / ksplit of that tier. N > 512 CTA groups: the group's rows. Pure query. */
+ * Split-K plans (ksplit > 1): CTA j of a tier owns the K split j % ksplit of the kblock-row block
+ * j / ksplit of that tier (dak_linear_launch_info.kblock). N > 512 CTA groups: the group's rows. Pure query. */
 dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t* tier, int64_t* row_begin, int64_t* row_end);
 
 /* Enqueue the split GEMV / skinny GEMM. */

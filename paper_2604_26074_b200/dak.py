@@ -71,7 +71,7 @@ class dak_linear_launch_info(C.Structure):
                 ("stages_hbm", C.c_int32), ("window_host", C.c_int32), ("smem_bytes", C.c_int32), ("path", C.c_int32),
                 ("rows_per_cta_host_max", C.c_int64), ("rows_per_cta_hbm_max", C.c_int64),
                 ("hbm_bytes", C.c_int64), ("host_bytes", C.c_int64), ("cluster", C.c_int32), ("ksplit", C.c_int32),
-                ("host_gate", C.c_int32), ("reserved", C.c_int32)]
+                ("host_gate", C.c_int32), ("kblock", C.c_int32)]
 
 
 def _sig(name, res, args):

@@ -453,12 +453,12 @@ def test_linear_large_m_r_invariance_bitwise(D, torch, M, K, N):
 @pytest.mark.parametrize("M,K,N,h", [(7168, 8192, 64, 1024), (1280, 4096, 32, 128)])
 def test_linear_cta_rows_split_k_match_oracle(D, torch, M, K, N, h):
     """dak_linear_cta_rows on split-K plans: CTA j of a tier owns K split j % S of that tier's
-    128-row block j // S (the oracle's rule, oracle/partition.py linear_splitk_items)."""
+    kblock-row block j // S (the oracle's rule, oracle/partition.py linear_splitk_items)."""
     from oracle import partition as Pt
     a = D.linear_args(16, 16, M, K, h, 64, N, 16, 16)
     a.workspace, a.workspace_bytes = 256, 1 << 40
     info = D.linear_query(a)
     assert info["ksplit"] > 1
-    ref = Pt.linear_splitk_items(M, h, info["ksplit"], 128)
+    ref = Pt.linear_splitk_items(M, h, info["ksplit"], info["kblock"])
     got = [D.linear_cta_rows(a, c) for c in range(info["grid"])]
     assert got == ref
