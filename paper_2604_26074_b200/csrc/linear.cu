@@ -1571,35 +1571,10 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     // form at the Llama TP8 b64 shapes; 256-row items (one instruction per 256 rows) were slower
     // (4 deeper stages instead of 6: profiles/r01/splitk_sweep.txt)
     if (ksplit > 1 && N <= 128 && M % 4 == 0 && (force_swap || !c.force_path)) swap = N <= 64 ? 2 : 1;  // 2: M = 64
-    if (swap) {
-      // item geometry of the swapped form from (M, K, SM count) only (never h): the weight rows of an
-      // item are the MMA's N side, any multiple of 16 up to 256. A CTA's stream is latency-bound
-      // (its weight bytes in flight / memory latency), so choose (kblock, S) maximising the weight
-      // bytes in flight over the whole grid -- items x min(ring slots x stage bytes, item bytes) --
-      // with every item in ONE wave (one block of reserve for the tier split). Llama TP8 b64:
-      // [gate; up] 7168 x 8192 -> 256-row blocks x 5 splits (140 CTAs, 160 KB each in flight) instead
-      // of 128 x 2 (112 CTAs, 128 KB).
-      const long long xb = (N <= 64 ? 64 : 128) * 128;
-      long long best = 0;
-      for (int kb = 64; kb <= 256; kb += 16) {
-        const long long wst = (long long)kb * 128;
-        const long long slots = std::min<long long>(kMaxStages, (kSmemBudget - 2048 - 16384) / (wst + xb));
-        for (long long s0 = 1; s0 <= std::min<long long>(16, C); ++s0) {
-          const long long b2 = ceil_div(C, s0), s2 = ceil_div(C, b2);
-          if (s2 < 2 || b2 < 2) continue;  // split-K form only; >= 2 chunks per split keep the ring busy
-          if ((ceil_div(M, kb) + 1) * s2 > nsm) continue;
-          const long long score = ceil_div(M, kb) * s2 * std::min(slots * wst, b2 * wst);
-          if (score > best) {
-            best = score;
-            kblock = kb;
-            ksplit = (int)s2;
-            k64_split = (int)b2;
-          }
-        }
-      }
-      n_host = (int)(ceil_div(h, kblock) * ksplit);
-      n_hbm = (int)(ceil_div(M - h, kblock) * ksplit);
-    }
+    // (kblock, S) alternatives chasing more weight bytes in flight per SM -- 176..256-row items over
+    // 120-141 CTAs -- were measured slower than 128-row items (Llama TP8 b64 step 0.989 vs 0.883 ms,
+    // profiles/r02/notes.md): the swapped form is paced per stage by the MMA / commit cycle, not by
+    // bytes in flight.
   }
   if (force_swap && !swap) return fail(DAK_EUNSUPPORTED, "dak_linear: swapped tcgen05 form needs N <= 128, M %% 4 == 0 and a split-K workspace");
   const long long rmax_host = ksplit > 1 ? std::min<long long>(h, kblock)
