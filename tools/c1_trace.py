@@ -25,6 +25,7 @@ def main():
     kc = int(sys.argv[1]) if len(sys.argv) > 1 else 512
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 48
     extra = dict(kv.split("=") for kv in sys.argv[3:])
+    pf_mb = float(extra.pop("pf_mb", 0))  # L2 warm-up of the NEXT launch's weights (dak_linear_args.l2_prefetch)
     cfg = dict(pdl=1, congestion_control=1, **{k: int(v) for k, v in extra.items()})
     M = K = 4096
     N = 1
@@ -33,7 +34,9 @@ def main():
     h = plan[0]["host_units"] * 16
     copies = 24
     hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
-    args = [dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg)
+    pf = int(pf_mb * (1 << 20)) // 16 * 16
+    args = [dak.linear_args(hosts[i % copies][1] if h else None, hbm[i % copies], M, K, h, kc, N, x, y, cfg=cfg,
+                            l2_prefetch=hbm[(i + 1) % copies] if pf else None, l2_prefetch_bytes=pf)
             for i in range(n)]
     info = dak.linear_query(args[0])
     s = torch.cuda.Stream()
@@ -82,7 +85,7 @@ def main():
         prev_end = end.max()
         rows.append(r)
     med = {k: round(float(np.median([r[k] for r in rows[4:] if r[k] is not None])), 3) for k in rows[4]}
-    print(json.dumps(dict(kc=kc, h=h, grid=info["grid"], n_cta_host=info["n_cta_host"], stages=info["stages_hbm"],
+    print(json.dumps(dict(kc=kc, h=h, pf_mb=pf_mb, grid=info["grid"], n_cta_host=info["n_cta_host"], stages=info["stages_hbm"],
                           smem=info["smem_bytes"], path=info["path"], us_per_launch_events=round(float(np.median(ts)), 3),
                           gbs=round(M * K * 2 / (np.median(ts) * 1e-6) / 1e9, 1), medians_us=med)))
     for i, h_ in enumerate(hosts):
