@@ -90,11 +90,80 @@ def time_cfg(M, K, N, h, kc, launches=64, reps=10, ln=False, stats=False, swiglu
                                                                         "smem_bytes", "path", "ws")}, cfg=cfg)
 
 
+def time_chain(layers=8, N=8, two_per_sm=False, stages=0, kc_override=0):
+    """OPT-30B layer linears (qkv, o, fc1, fc2) x layers chained with PDL in one graph, host share r*;
+    two_per_sm: two CTAs per SM per op (rows halved, ring <= 113 KB) so the next op's CTAs can take
+    a slot while this op's last CTAs drain."""
+    H, F = 7168, 28672
+    shapes = [(3 * H, H), (H, H), (F, H), (H, F)] * layers
+    sms = dak.device_sms()
+    args, keep = [], []
+    x = torch.randn(N, F, device="cuda").to(torch.bfloat16)
+    y = torch.empty(N, F, device="cuda", dtype=torch.bfloat16)
+    for (M, K) in shapes:
+        h = 16 * max(1, round(M * 0.0066 / 16))
+        nh = 2
+        nhbm = (2 * sms - nh) if two_per_sm else 0
+        rows = -(-(M - h) // (nhbm or (sms - nh)))
+        kc = kc_override or dak.choose_kc(rows, K)
+        W = torch.randn((M - h) * K, device="cuda").to(torch.bfloat16)
+        hp, dp = dak.host_alloc(h * K * 2)
+        keep += [W, hp]
+        cfg = dict(pdl=1, congestion_control=1, n_cta_host=nh, n_cta_hbm=nhbm, stages=stages)
+        args.append(dak.linear_args(dp, W, M, K, h, kc, N, x, y, cfg=cfg))
+    info = [dak.linear_query(a) for a in args[:4]]
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for a in args:
+            dak.linear(a, s)
+        s.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for a in args:
+                dak.linear(a, s)
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ts = []
+    for _ in range(5):
+        e0.record(s)
+        with torch.cuda.stream(s):
+            g.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.median(ts))
+    nbytes = sum(M * K * 2 for M, K in shapes)
+    for hp in keep[1::2]:
+        dak.host_free(hp)
+    return dict(two_per_sm=two_per_sm, stages=stages, ms=round(t * 1e3, 4), gbs=round(nbytes / t / 1e9, 1),
+                info=[{k: i[k] for k in ("grid", "smem_bytes", "stages_hbm")} for i in info])
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--exp", default="")
     a = ap.parse_args()
+    if a.exp == "chain":  # OPT layer chain: one CTA per SM (default) vs two per SM with shallower rings
+        print(json.dumps(time_chain()), flush=True)
+        for st in (2, 3, 4):
+            try:
+                print(json.dumps(time_chain(two_per_sm=True, stages=st)), flush=True)
+            except Exception as e:  # noqa: BLE001
+                print(json.dumps(dict(two_per_sm=True, stages=st, error=str(e))), flush=True)
+        return
+    if a.exp == "n16":  # OPT-30B shapes at N = 16: mma.sync (path 2) vs tcgen05 (3, split-K when few rows) vs swapped (4)
+        for (M, K) in ((21504, 7168), (7168, 7168), (28672, 7168), (7168, 28672)):
+            h = 16 * max(1, round(M * 0.0066 / 16))
+            for path in (2, 3, 4):
+                kc = 64 if path >= 3 else dak.choose_kc(-(-(M - h) // 146), K)
+                try:
+                    r = time_cfg(M, K, 16, h, kc, pdl=1, n_cta_host=2, congestion_control=1, force_path=path, ws=True)
+                except Exception as e:  # noqa: BLE001
+                    r = dict(M=M, K=K, path=path, error=str(e))
+                print(json.dumps(r), flush=True)
+        return
     if a.exp == "sk":  # tcgen05 split-K at the Llama TP8 shard shapes, b64 (kc from env KCS, default 64)
         for (M, K) in ((1280, 8192), (8192, 1024), (7168, 8192), (8192, 3584)):
             for kc in [int(v) for v in os.environ.get("KCS", "64").split(",")]:
