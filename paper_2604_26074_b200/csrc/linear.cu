@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.h"
 
@@ -85,6 +86,7 @@ struct __align__(64) Params {
   int ln_rms;       // 1: RMSNorm (no mean subtraction, no bias)
   float* stats_out;  // epilogue row statistics (count, mean, M2) of this CTA's outputs (nullable)
   unsigned long long* trace;  // dak_trace_enable slot (nullable)
+  int exp_flags;    // EXPERIMENT (DAK_EXP_NOMMA): 1 = swapped kernel skips the MMAs (memory pipeline only)
 };
 
 // Row range of CTA j of n in a tier of R rows, in units of g rows (sizes differ by <= one unit).
@@ -780,6 +782,13 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* v) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
@@ -1229,7 +1238,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     for (int i = 0; i < nchunks; ++i) {
       mbar_wait(&full[s], ph);
       tc_fence_after();
-      if (leader) {
+      if (leader && (p.exp_flags & 1)) {
+        mbar_arrive(&empty[s]);
+      } else if (leader) {
         const uint32_t ws = wr + (uint32_t)s * wstage, xs = xr + (uint32_t)s * p.x_stage_bytes;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -1241,42 +1252,56 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     }
     if (leader) umma_commit(done);
     __syncwarp();
-  } else if (warp >= 4 && warp < 8) {  // epilogue: warp q <-> TMEM lanes 32q.. = batch rows
-    if (threadIdx.x == 128) {
-      uint32_t ok = 0;
-      while (!ok) {
-        asm volatile(
-            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-            : "=r"(ok)
-            : "r"(su32(done)), "r"(0u)
-            : "memory");
-        if (!ok) __nanosleep(256);
-      }
+  }
+  // ---- epilogue (every warp): TMEM -> SMEM tile -> coalesced fp32 partial part[ks][n][row0..row0+R)
+  if (threadIdx.x == 0) {
+    uint32_t ok = 0;
+    while (!ok) {
+      asm volatile(
+          "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+          : "=r"(ok)
+          : "r"(su32(done)), "r"(0u)
+          : "memory");
+      if (!ok) __nanosleep(128);
     }
-    asm volatile("bar.sync 2, 128;" ::: "memory");
-    tc_fence_after();
-    grid_dep_wait();  // the partial buffer may still be read by the previous kernel's consumer
-    const int q = warp & 3;
-    // M = 128: TMEM lane 32q + l holds batch row 32q + l. M = 64 (measured, tools/umma_m64_layout.cu):
-    // batch row r sits in lane 32 (r / 16) + r % 16, i.e. lanes 0..15 of each warp quadrant
-    const int n = p.swap == 2 ? (lane < 16 ? 16 * q + lane : 1 << 30) : 32 * q + lane;
-    float* dst = p.part + ((size_t)ks * N + n) * p.M + row0;
+  }
+  __syncthreads();  // every MMA has completed, so every ring stage has landed and been read: the ring is free
+  tc_fence_after();
+  grid_dep_wait();  // partials / y / split-K counters may still be in use by the previous kernel
+  const int RN = (R + 15) & ~15;
+  const int pitch = RN + 4;  // floats; +16 B per row: 2-way bank conflicts at most on the tile stores
+  float* tile = reinterpret_cast<float*>(wring);
+  {
+    // warp w reads TMEM lane quadrant q = w & 3 (tcgen05.ld lane restriction) and half of the
+    // 16-column groups. M = 128: TMEM lane 32q + l holds batch row 32q + l. M = 64 (measured,
+    // tools/umma_m64_layout.cu): batch row r sits in lane 32 (r / 16) + r % 16.
+    const int q = warp & 3, half = (warp >> 2) & 1;
+    const int n = p.swap == 2 ? (lane < 16 ? 16 * q + lane : -1) : 32 * q + lane;
+    const int G = RN / 16, g0 = half ? G / 2 : 0, g1 = warp >= 8 ? 0 : (half ? G : G / 2);  // warp 8: idle
 #pragma unroll 1
-    for (int c0 = 0; c0 < R; c0 += 8) {
-      uint32_t v[8];
-      tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
+    for (int g = g0; g < g1; ++g) {
+      uint32_t v[16];
+      tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(16 * g), v);
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (n < N) {
-        if (c0 + 8 <= R) {
-          float4* d4 = reinterpret_cast<float4*>(dst + c0);
-          d4[0] = make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
-          d4[1] = make_float4(__uint_as_float(v[4]), __uint_as_float(v[5]), __uint_as_float(v[6]), __uint_as_float(v[7]));
-        } else {
-          for (int e = 0; e < R - c0; ++e) dst[c0 + e] = __uint_as_float(v[e]);
-        }
+      if (n >= 0 && n < N) {
+        float4* d4 = reinterpret_cast<float4*>(tile + (size_t)n * pitch + 16 * g);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          d4[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]), __uint_as_float(v[4 * e + 2]),
+                              __uint_as_float(v[4 * e + 3]));
       }
     }
-    tc_fence_before();
+  }
+  tc_fence_before();
+  __syncthreads();
+  const int R4 = R >> 2;  // R % 4 == 0 (M % 4 == 0, h % 8 == 0, kblock % 8 == 0)
+  if (!(p.exp_flags & 2)) {
+    float* dst = p.part + (size_t)ks * N * p.M + row0;
+    for (int i = threadIdx.x; i < N * R4; i += kThreads) {
+      const int nn = i / R4, m4 = i - nn * R4;
+      __stcg(reinterpret_cast<float4*>(dst + (size_t)nn * p.M) + m4,
+             *reinterpret_cast<const float4*>(tile + (size_t)nn * pitch + 4 * m4));
+    }
   }
   __syncthreads();
   if (threadIdx.x == 32 && p.trace) tstamp(p.trace, 3);
@@ -1560,11 +1585,18 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       bks = ceil_div(C, S);
       S = ceil_div(C, bks);
     }
+    if (getenv("DAK_EXP_KBLOCK")) {  // EXPERIMENT: item rows and split count override
+      kblock = atoi(getenv("DAK_EXP_KBLOCK"));
+      S = std::min<long long>(std::min<long long>(16, C), nsm / ceil_div(M, kblock));
+      if (getenv("DAK_EXP_S")) S = atoi(getenv("DAK_EXP_S"));
+      bks = ceil_div(C, S);
+      S = ceil_div(C, bks);
+    }
     if (S > 1 && ceil_div(M, nsm) < 128) {  // from M and the SM count only (never h: r-invariance)
       ksplit = (int)S;
       k64_split = (int)bks;
-      n_host = (int)(ceil_div(h, 128) * S);
-      n_hbm = (int)(ceil_div(M - h, 128) * S);
+      n_host = (int)(ceil_div(h, kblock) * S);
+      n_hbm = (int)(ceil_div(M - h, kblock) * S);
     }
     // swapped operands (N <= 128, same items): the batch is the MMA's M = 128 side, the item's 128
     // weight rows its N side (umma_swap_kernel). Measured 5-12% faster than the weight-rows-as-M
@@ -1672,6 +1704,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   if (a->stats_out && !aligned16(a->stats_out)) return fail(DAK_EINVAL, "dak_linear: stats_out must be 16-byte aligned");
   p.stats_out = a->stats_out;
+  p.exp_flags = getenv("DAK_EXP_FLAGS") ? atoi(getenv("DAK_EXP_FLAGS")) : 0;  // EXPERIMENT: 1 no MMA, 2 no epilogue, 4 no reduce
   const int W2 = (path == 1 && kc / 8 > 32) ? kc / 8 / 32 : 1;
   // MMA path: one partial slot per k-warp when they fit in 48 KB (one barrier), else serial rounds
   p.red_slots = (path == 2 && wk > 1 && (long long)wk * rmax * N * 4 <= 48 * 1024) ? wk : 1;
@@ -2052,7 +2085,7 @@ dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool d
   if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
   const int S = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;
   if (ksplit_out) *ksplit_out = S;
-  if (S > 1 && !defer_reduce) {
+  if (S > 1 && !defer_reduce && !(pl.p.exp_flags & 4)) {
     const int vec = args->M % 4 == 0 && pl.p.ldy % 4 == 0 && ((uintptr_t)pl.p.y & 7) == 0 &&
                     ((uintptr_t)pl.p.residual & 7) == 0 && ((uintptr_t)pl.p.bias & 7) == 0;
     const long long per_row = vec ? args->M / 4 : args->M;
@@ -2060,7 +2093,8 @@ dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool d
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = args->cfg.pdl ? 1 : 0;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)std::min<long long>(ceil_div_ll(per_row, 256), 64), (unsigned)args->N);
+    const long long gx = std::min<long long>(ceil_div_ll(per_row, 256), 64);
+    cfg.gridDim = dim3((unsigned)gx, (unsigned)args->N);
     cfg.blockDim = dim3(256);
     cfg.stream = (cudaStream_t)stream;
     cfg.attrs = attr;

@@ -235,7 +235,7 @@ class _DecodeEngine:
             need = dak.linear_workspace_size(ha)
             if need:
                 if getattr(self, "head_ws", None) is None or self.head_ws.numel() < need:
-                    self.head_ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+                    self.head_ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
                 ha.workspace, ha.workspace_bytes = self.head_ws.data_ptr(), self.head_ws.numel()
         return ha
 
@@ -352,7 +352,7 @@ class DakOPT(_DecodeEngine):
         self.h = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
         self.logits = torch.empty((B, c.vocab), dtype=torch.bfloat16, device="cuda")
         self.layer_args = [self._layer_args(l) for l in range(c.n_layers)]
-        self.scratch = torch.empty(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
+        self.scratch = torch.zeros(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
         for a in self.layer_args:
             a.scratch, a.scratch_bytes = self.scratch.data_ptr(), self.scratch.numel()
         # fused pre-norm: the residual stream's row statistics travel embed -> FC2 -> FC2 ... -> head

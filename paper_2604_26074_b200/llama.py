@@ -101,7 +101,7 @@ class DakLlama(_DecodeEngine):
         self.hnorm = torch.empty((B, c.hidden), dtype=torch.bfloat16, device="cuda")
         self.logits = torch.empty((B, self.dims["vocab"]), dtype=torch.bfloat16, device="cuda")
         self.layer_args = [self._layer_args(l) for l in range(c.n_layers)]
-        self.scratch = torch.empty(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
+        self.scratch = torch.zeros(dak.layer_scratch_size(self.layer_args[0]), dtype=torch.uint8, device="cuda")
         self.stats = torch.zeros((1024, B, 4), dtype=torch.float32, device="cuda")
         parts = 1
         for a in self.layer_args:

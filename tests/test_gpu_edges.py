@@ -33,7 +33,7 @@ def _lin(D, torch, M, K, N, h, kc, **cfg):
     wsb = None
     ws = D.linear_workspace_size(a) if cfg.get("force_path") == 3 else 0
     if ws:
-        wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
+        wsb = torch.zeros(ws, dtype=torch.uint8, device="cuda")
         a.workspace, a.workspace_bytes = wsb.data_ptr(), ws
     D.linear(a)
     torch.cuda.synchronize()

@@ -356,7 +356,7 @@ def test_linear_tcgen05_split_k(D, torch, M, K, N, h, fp):
     a = sl.args(xd, y, N, bias=bd, residual=rd, force_path=fp)
     ws = D.linear_workspace_size(a)
     assert ws > 0
-    wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
+    wsb = torch.zeros(ws, dtype=torch.uint8, device="cuda")
     a.workspace, a.workspace_bytes = wsb.data_ptr(), ws
     D.linear(a)
     torch.cuda.synchronize()
@@ -377,7 +377,7 @@ def test_linear_tcgen05_split_k_r_invariance_integer_exact(D, torch, fp):
         a = sl.args(xd, y, N, force_path=fp)
         ws = D.linear_workspace_size(a)
         assert ws > 0
-        wsb = torch.empty(ws, dtype=torch.uint8, device="cuda")
+        wsb = torch.zeros(ws, dtype=torch.uint8, device="cuda")
         a.workspace, a.workspace_bytes = wsb.data_ptr(), ws
         D.linear(a)
         torch.cuda.synchronize()
@@ -402,7 +402,7 @@ def _run_cfg(D, torch, W, x, h, kc, **cfg):
         need = D.linear_workspace_size(a)
         a.workspace, a.workspace_bytes = None, 0
         if need:
-            wsb = torch.empty(need, dtype=torch.uint8, device="cuda")
+            wsb = torch.zeros(need, dtype=torch.uint8, device="cuda")
             a.workspace, a.workspace_bytes = wsb.data_ptr(), need
     info = D.linear_query(a)
     D.linear(a)
@@ -462,3 +462,30 @@ def test_linear_cta_rows_split_k_match_oracle(D, torch, M, K, N, h):
     ref = Pt.linear_splitk_items(M, h, info["ksplit"], info["kblock"])
     got = [D.linear_cta_rows(a, c) for c in range(info["grid"])]
     assert got == ref
+
+
+def test_linear_split_k_shared_workspace_reuse(D, torch):
+    """One split-K workspace serves a chain of swapped-operand ops with different split counts,
+    launched back to back without a host sync (each op's partials are written after its dependency
+    wait and reduced before the next op runs): every output bit-exact (integer inputs) vs the oracle."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    shapes = [(1280, 8192, 64, 0), (8192, 1024, 64, 256), (7168, 4096, 64, 0), (1024, 2048, 48, 128)]
+    runs = []
+    for i, (M, K, N, h) in enumerate(shapes):
+        W, x, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(32, i), kind="int")
+        sl = SplitLinear(D, W, h, 64)
+        xd = to_dev(x)
+        y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+        a = sl.args(xd, y, N, force_path=4)
+        runs.append((W, x, sl, xd, y, a))
+    need = max(D.linear_workspace_size(r[5]) for r in runs)
+    wsb = torch.zeros(need, dtype=torch.uint8, device="cuda")
+    for r in runs:
+        r[5].workspace, r[5].workspace_bytes = wsb.data_ptr(), need
+        assert D.linear_query(r[5])["ksplit"] > 1
+    for _ in range(3):
+        for r in runs:
+            D.linear(r[5])
+    torch.cuda.synchronize()
+    for W, x, sl, xd, y, a in runs:
+        assert np.array_equal(Kx.bf16_to_f64(from_dev(y)), Kx.round_to_bf16(Kx.linear(W, x)))

@@ -40,7 +40,7 @@ def linear_case(name, M, K, N, h, kc, **cfg):
     a.workspace, a.workspace_bytes = None, 0
     ws = None
     if need:
-        ws = torch.empty(need, dtype=torch.uint8, device="cuda")
+        ws = torch.zeros(need, dtype=torch.uint8, device="cuda")
         a.workspace, a.workspace_bytes = ws.data_ptr(), need
     info = dak.linear_query(a)
     torch.cuda.synchronize()
