@@ -400,55 +400,82 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
                                   pg_off((L - 1) % p.page, j)) = v;
         __syncwarp();
       }
-      for (int sub = 0; sub < tt && tile0 + sub < t1; sub += 16) {
-        const int tok0 = tile0 + sub;
-        const uint32_t kbase = kslot + sub * (kD * 2);
-        const uint32_t vbase = kslot + tile_bytes + sub * (kD * 2);
-        // ---- S^T = K . Q^T   [16 tokens x 8 heads]   (row t of the tile: swizzle phase t & 7)
-        float sc[4] = {0.f, 0.f, 0.f, 0.f};
+      // The tile's (up to two) 16-token sub-tiles are processed together: their S^T = K . Q^T chains
+      // interleave, ONE online-softmax update (max, rescale of O) covers the whole tile, then
+      // O^T += V^T . P^T for both. P enters the tensor core as bf16 hi + lo parts (p = hi + lo to
+      // ~16 significant bits; V stays bf16: no per-tile conversion of V), l sums the same hi + lo.
+      const int nsub = (min(tt, t1 - tile0) + 15) >> 4;  // sub-tiles holding a valid token (1 or 2)
+      float sc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks) {
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4(kbase + pg_off(lane & 15, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
-          mma_bf16(sc, a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+      for (int ks = 0; ks < kD / 16; ++ks) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (u < nsub) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4(kslot + u * 16 * (kD * 2) + pg_off(lane & 15, 2 * ks + (lane >> 4)), a0, a1, a2, a3);
+            mma_bf16(sc[u], a0, a1, a2, a3, qb[ks][0], qb[ks][1]);
+          }
         }
-        // ---- scale, mask, online softmax (exp2 domain), per head column
-        const bool v0 = tok0 + gq < t1, v1 = tok0 + gq + 8 < t1;
-        const float s0 = v0 ? sc[0] * p.scale_log2 : -INFINITY;
-        const float s1 = v0 ? sc[1] * p.scale_log2 : -INFINITY;
-        const float s2 = v1 ? sc[2] * p.scale_log2 : -INFINITY;
-        const float s3 = v1 ? sc[3] * p.scale_log2 : -INFINITY;
-        float mx0 = fmaxf(s0, s2), mx1 = fmaxf(s1, s3);
+      }
+      // ---- scale, mask, online softmax (exp2 domain), per head column, once per tile
+      float sv[2][4];
+      float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
-          mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      for (int u = 0; u < 2; ++u) {
+        const int tok0 = tile0 + 16 * u;
+        const bool v0 = u < nsub && tok0 + gq < t1, v1 = u < nsub && tok0 + gq + 8 < t1;
+        sv[u][0] = v0 ? sc[u][0] * p.scale_log2 : -INFINITY;
+        sv[u][1] = v0 ? sc[u][1] * p.scale_log2 : -INFINITY;
+        sv[u][2] = v1 ? sc[u][2] * p.scale_log2 : -INFINITY;
+        sv[u][3] = v1 ? sc[u][3] * p.scale_log2 : -INFINITY;
+        mx0 = fmaxf(mx0, fmaxf(sv[u][0], sv[u][2]));
+        mx1 = fmaxf(mx1, fmaxf(sv[u][1], sv[u][3]));
+      }
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+        mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+      }
+      const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: the tile has a valid token
+      const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
+      m[0] = mn0;
+      m[1] = mn1;
+      uint32_t ph[2][2], pl[2][2];  // [sub][rows gq | gq + 8] bf16x2 (head 2cq, 2cq + 1): hi and lo parts
+      float ls0 = 0.f, ls1 = 0.f;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const float e0 = exp2f(sv[u][2 * r] - mn0), e1 = exp2f(sv[u][2 * r + 1] - mn1);
+          const uint32_t hi = pack_bf16(e0, e1);
+          const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xffff0000u);
+          const uint32_t lo = pack_bf16(e0 - h0, e1 - h1);
+          ph[u][r] = hi;
+          pl[u][r] = lo;
+          ls0 += h0 + __uint_as_float(lo << 16);
+          ls1 += h1 + __uint_as_float(lo & 0xffff0000u);
         }
-        const float mn0 = fmaxf(m[0], mx0), mn1 = fmaxf(m[1], mx1);  // finite: tile has a valid token
-        const float al0 = exp2f(m[0] - mn0), al1 = exp2f(m[1] - mn1);
-        m[0] = mn0;
-        m[1] = mn1;
-        // P in fp16 for the P V product (11-bit significand for p in [0, 1]; bf16's 8 bits move o by up
-        // to ~1% of |V| when a few keys dominate); l sums the same rounded weights
-        const uint32_t h01 = pack_f16(exp2f(s0 - mn0), exp2f(s1 - mn1));
-        const uint32_t h23 = pack_f16(exp2f(s2 - mn0), exp2f(s3 - mn1));
-        const float2 f01 = __half22float2(*reinterpret_cast<const __half2*>(&h01));
-        const float2 f23 = __half22float2(*reinterpret_cast<const __half2*>(&h23));
-        l[0] = l[0] * al0 + (f01.x + f23.x);
-        l[1] = l[1] * al1 + (f01.y + f23.y);
+      }
+      l[0] = l[0] * al0 + ls0;
+      l[1] = l[1] * al1 + ls1;
 #pragma unroll
-        for (int i = 0; i < kD / 16; ++i) {
-          o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
-        }
-        // ---- P^T as B operand: transpose the two 8x8 blocks of P (tokens x heads)
-        const uint32_t b0 = movm_t(h01);
-        const uint32_t b1 = movm_t(h23);
-        // ---- O^T[d x heads] += V^T . P^T
+      for (int i = 0; i < kD / 16; ++i) {
+        o[i][0] *= al0; o[i][1] *= al1; o[i][2] *= al0; o[i][3] *= al1;
+      }
+      // ---- O^T[d x heads] += V^T . P^T  (P^T as the B operand: transposed 8x8 blocks of P)
 #pragma unroll
-        for (int i = 0; i < kD / 16; ++i) {
-          uint32_t a0, a1, a2, a3;
-          ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
-          mma_f16(o[i], bf2_to_h2(a0), bf2_to_h2(a1), bf2_to_h2(a2), bf2_to_h2(a3), b0, b1);
+      for (int u = 0; u < 2; ++u) {
+        if (u < nsub) {
+          const uint32_t bh0 = movm_t(ph[u][0]), bh1 = movm_t(ph[u][1]);
+          const uint32_t bl0 = movm_t(pl[u][0]), bl1 = movm_t(pl[u][1]);
+          const uint32_t vbase = kslot + tile_bytes + u * 16 * (kD * 2);
+#pragma unroll
+          for (int i = 0; i < kD / 16; ++i) {
+            uint32_t a0, a1, a2, a3;
+            ldsm_x4_t(vbase + pg_off((lane & 7) + ((lane >> 4) << 3), 2 * i + ((lane >> 3) & 1)), a0, a1, a2, a3);
+            mma_bf16(o[i], a0, a1, a2, a3, bh0, bh1);
+            mma_bf16(o[i], a0, a1, a2, a3, bl0, bl1);
+          }
         }
       }
       __syncwarp();

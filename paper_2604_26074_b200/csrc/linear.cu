@@ -1505,7 +1505,16 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   // default: tensor cores for every N -- mma.sync (path 2) up to N = 16; tcgen05 (path 3) beyond,
   // where mma.sync becomes issue-bound, when its operand constraints hold
   int path = c.force_path ? c.force_path : 2;
-  if (!c.force_path && N > 16 && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster at N > 512: W multicast groups
+  // 9..16 columns: tcgen05 too when every CTA owns >= 128 rows (one M = 128 tile, no split-K) --
+  // mma.sync's two n8 tiles per k-step become issue-bound there (OPT-30B qkv / fc1 / head at b16)
+  bool tc_n16 = false;
+  if (!c.force_path && N > 8 && N <= 16 && kc == 64) {
+    int sm = 0;
+    dak_status st = device_sms(&sm);
+    if (st != DAK_OK) return st;
+    tc_n16 = M >= 128LL * sm;
+  }
+  if (!c.force_path && (N > 16 || tc_n16) && kc == 64 && (c.cluster <= 1 || N > 512) && h % 8 == 0)  // cluster at N > 512: W multicast groups
     path = 3;
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   const bool force_swap = path == 4;  // force_path 4: tcgen05 with swapped operands (split-K decode form)

@@ -140,11 +140,13 @@ class _DecodeEngine:
                 self.head = op
             else:
                 self.layers[o["layer"]][self.ROLE_KEY[o["role"]]] = op
-            # KC = 64 above 16 batch columns (the tcgen05 path's canonical SWIZZLE_128B operands);
-            # else the widest KC whose stage holds the CTA's rows (dak_linear_choose_kc)
+            # KC = 64 where the tcgen05 path runs (its canonical SWIZZLE_128B operands): above 16
+            # batch columns, and at 9..16 for ops with >= 128 rows per SM (dak_linear picks tcgen05
+            # there); else the widest KC whose stage holds the CTA's rows (dak_linear_choose_kc)
             n_host = min(self.n_cta_host, op.h) if op.h > 0 else 0
             rows = max(-(-op.h // max(n_host, 1)) if op.h else 0, -(-(op.M - op.h) // (self.sms - n_host)))
-            op.kc = 64 if self.B > 16 else dak.choose_kc(rows, op.K)
+            tc = self.B > 16 or (self.B > 8 and op.M >= 128 * self.sms)
+            op.kc = 64 if tc else dak.choose_kc(rows, op.K)
         return plan
 
     def linear_ops(self):
