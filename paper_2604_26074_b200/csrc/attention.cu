@@ -200,22 +200,38 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   }
   grid_dep_launch();
   const int n_pairs = p.B * p.max_chunks;
-  // CTA roles (one tier per SM). Auto: one host CTA per 4 host units (request, kv head,
-  // chunk) -- host CTAs are bound by the link latency, so a few keep more bytes in flight -- capped
-  // at 16 (congestion control), none when the block table names no host chunk.
+  // CTA roles (one tier per SM): given, or chosen below from the block table (auto)
   int n_host = p.n_host, n_hbm = p.n_hbm, host_inflight = p.host_inflight;
-  if (p.auto_host) {
+  // ---- schedule inputs, loaded ONCE with independent loads (two dependent rounds in all: seq_lens,
+  // then the first block-table entry of every (request, chunk) pair); pref[i] holds the pair's flags
+  // (bit 0: the chunk exists, bit 1: its first page is on the host) until the scan overwrites it
+  for (int b = threadIdx.x; b < p.B; b += kThreads) s_len[b] = p.seq_lens[b];
+  __syncthreads();
+  {
     int cnt = 0;
+#pragma unroll 4
     for (int i = threadIdx.x; i < n_pairs; i += kThreads) {
-      const int b = i / p.max_chunks, c = i % p.max_chunks;
-      const int npg = (p.seq_lens[b] + p.page - 1) / p.page;
-      if (c * p.chunk_pages < npg)
-        cnt += ((uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages] & kHostBit) != 0;
+      const int b = i / p.max_chunks, c = i - b * p.max_chunks;
+      const int npg = (s_len[b] + p.page - 1) / p.page;
+      int f = 0;
+      if (c * p.chunk_pages < npg) {
+        const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages];
+        f = 1 | ((e & kHostBit) ? 2 : 0);
+        cnt += f >> 1;
+      }
+      pref[i] = f;
     }
+    if (p.auto_host) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if (lane == 0) warp_tot[warp] = cnt;
+      for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+      if (lane == 0) warp_tot[warp] = cnt;
+    }
     __syncthreads();
+  }
+  if (p.auto_host) {
+    // one host CTA per 4 host units (request, kv head, chunk) -- host CTAs are bound by the link
+    // latency, so a few keep more bytes in flight -- capped at 16 (congestion control),
+    // none when the block table names no host chunk
     int hu = 0;
     for (int w = 0; w < kWarps; ++w) hu += warp_tot[w];
     __syncthreads();
@@ -231,21 +247,16 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   // written by earlier steps: the schedule and those tiles do not wait for the previous kernel
   // (griddepcontrol.wait). q and the tile holding the new token (position seq_len - 1, written by
   // the KV-append kernel just before) are read only after it (ABI contract in dak.h).
-  // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c; tier = bit 31 of the chunk's first page
-  {  // flags -> exclusive prefix over tier-matching pairs (block-wide, fixed order)
+  // ---- schedule: pairs (b, c) linearised p = b*max_chunks + c, tier-matching ones ranked (exclusive
+  // prefix over the flags in SMEM, block-wide, fixed order)
+  {
     int carry = 0;
     for (int base = 0; base < n_pairs; base += kThreads) {
       const int i = base + threadIdx.x;
       int f = 0;
       if (i < n_pairs) {
-        const int b = i / p.max_chunks, c = i % p.max_chunks;
-        const int L = p.seq_lens[b];
-        if (c == 0) s_len[b] = L;
-        const int npg = (L + p.page - 1) / p.page;
-        if (c * p.chunk_pages < npg) {
-          const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages];
-          f = ((e & kHostBit) != 0) == host;
-        }
+        const int fl = pref[i];
+        f = (fl & 1) && (((fl >> 1) & 1) != 0) == host;
       }
       int v = f;
 #pragma unroll

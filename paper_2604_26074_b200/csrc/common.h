@@ -47,6 +47,10 @@ dak_status rope_kv_append_part(void* qkv, int64_t row_stride, int32_t B, int32_t
                                const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
                                int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
                                void* stream, const float* part, int32_t S);
+// one rank: x += bf16(sum_s part[s]) (the row-parallel linear's split-K partials, reduced here instead
+// of by its reduce kernel), y_norm = RMSNorm(x)
+dak_status residual_rmsnorm_part(const float* part, int32_t S, void* x, int32_t rows, int32_t cols, const void* norm_w,
+                                 float eps, void* y_norm, int32_t pdl, void* stream);
 dak_status silu_mul_part(const void* gu, void* out, int32_t rows, int32_t F, int32_t pdl, void* stream,
                          const float* part, int32_t S);
 

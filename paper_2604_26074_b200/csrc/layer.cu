@@ -479,9 +479,18 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   at.cfg.pdl = pdl;
   at.q_row_stride = qkv_cols;
   if ((st = dak_attention(&at, strm)) != DAK_OK) return st;
+  // one-rank communicator, unfused combine: a split-K row-parallel linear leaves its fp32 partials
+  // to the residual + RMSNorm kernel (no reduce launch; same arithmetic)
+  int world = 1;
+  if (tp && (st = dak_comm_size(a->comm, &world)) != DAK_OK) return st;
+  const bool part_combine = tp && world == 1 && !nv && !fuse;
+  int o_split = 1;
   // o projection: residual + statistics in the epilogue (1 rank), or partial -> all-reduce -> residual
   int o_parts = 1;
-  {
+  if (part_combine) {
+    dak_linear_args l = lin_args(a->o, H, (long long)Hq * d, B, attn, partial, nullptr, DAK_ACT_NONE, a->cfg);
+    if ((st = linear_enqueue(&l, strm, true, &o_split)) != DAK_OK) return st;
+  } else {
     dak_linear_args l = lin_args(a->o, H, (long long)Hq * d, B, attn, tp ? partial : a->x, tp ? nullptr : a->x,
                                  DAK_ACT_NONE, a->cfg);
     if (!tp && fuse) {
@@ -497,6 +506,9 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
   const bool norm2_done = tp && !fuse;
   if (norm2_done && nv) {
     if ((st = dak_nvls_residual_rmsnorm(a->nvls, 0, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, strm)) != DAK_OK) return st;
+  } else if (norm2_done && o_split > 1) {
+    if ((st = residual_rmsnorm_part((const float*)ws, o_split, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
+      return st;
   } else if (norm2_done) {
     if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->ln2_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)
       return st;
@@ -517,8 +529,13 @@ static dak_status llama_layer(const dak_layer_args* a, const Scratch& s, dak_str
     else if ((st = silu_mul_part(gu, f2, B, F, pdl, strm, up_split > 1 ? (const float*)ws : nullptr, up_split)) != DAK_OK)
       return st;
     if (!tp && fuse) l.stats_out = a->stats_out;
-    if ((st = dak_linear(&l, strm)) != DAK_OK) return st;
-    if (nv) {  // NVLS: one kernel (the next layer's RMSNorm 1 too when given)
+    int down_split = 1;
+    if ((st = linear_enqueue(&l, strm, part_combine && a->next_ln_w, &down_split)) != DAK_OK) return st;
+    if (part_combine && a->next_ln_w && down_split > 1) {
+      if ((st = residual_rmsnorm_part((const float*)ws, down_split, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, pdl, strm)) !=
+          DAK_OK)
+        return st;
+    } else if (nv) {  // NVLS: one kernel (the next layer's RMSNorm 1 too when given)
       if ((st = dak_nvls_residual_rmsnorm(a->nvls, 0, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, strm)) != DAK_OK) return st;
     } else if (tp && !fuse && a->next_ln_w) {  // the next layer's RMSNorm 1 in the same combine kernel
       if ((st = dak_allreduce_residual_rmsnorm(a->comm, partial, a->x, B, H, a->next_ln_w, a->ln_eps, hbuf, pdl, strm)) != DAK_OK)

@@ -158,10 +158,30 @@ __global__ void __launch_bounds__(kThreads) residual_stats_vec_kernel(const __nv
 // launch of its own). 8 columns per 16-byte chunk, chunks held in registers; y may alias partial
 // (each thread reads its own chunks before the first barrier and writes only those).
 constexpr int kVec = 8;  // 16-byte chunks per thread (cols <= 256 * 64)
+// part != nullptr (one rank): the row-parallel linear's split-K partials are reduced here instead of
+// by its reduce kernel -- partial = bf16(sum_s part[s][r][c]) in split order, the arithmetic of
+// splitk_reduce_kernel without bias / activation -- so the combine costs no extra launch.
+__device__ __forceinline__ uint4 sum_parts8(const float* part, long long plane, int S, long long off) {
+  float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
+  float4 b = __ldcg(reinterpret_cast<const float4*>(part + off + 4));
+  for (int s = 1; s < S; ++s) {
+    const float4 c = __ldcg(reinterpret_cast<const float4*>(part + s * plane + off));
+    const float4 d = __ldcg(reinterpret_cast<const float4*>(part + s * plane + off + 4));
+    a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+    b.x += d.x; b.y += d.y; b.z += d.z; b.w += d.w;
+  }
+  uint4 o;
+  __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
+  oh[0] = __floats2bfloat162_rn(a.x, a.y);
+  oh[1] = __floats2bfloat162_rn(a.z, a.w);
+  oh[2] = __floats2bfloat162_rn(b.x, b.y);
+  oh[3] = __floats2bfloat162_rn(b.z, b.w);
+  return o;
+}
 __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_bfloat16* partial,
                                                                     __nv_bfloat16* __restrict__ x, int cols,
                                                                     const __nv_bfloat16* __restrict__ w, float eps,
-                                                                    __nv_bfloat16* y) {
+                                                                    __nv_bfloat16* y, const float* part, int S, int rows) {
   __shared__ float red[kThreads / 32];
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -169,13 +189,14 @@ __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_b
   const long long base = (long long)blockIdx.x * nc;
   uint4* xr = reinterpret_cast<uint4*>(x) + base;
   const uint4* pr = reinterpret_cast<const uint4*>(partial) + base;
+  const long long plane = (long long)rows * cols;
   float f[kVec][8];
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < kVec; ++i) {
     const int c = threadIdx.x + i * kThreads;
     if (c < nc) {
-      const uint4 a = xr[c], b = pr[c];
+      const uint4 a = xr[c], b = part ? sum_parts8(part, plane, S, (base + c) * 8) : pr[c];
       const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
       const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&b);
       uint4 o;
@@ -373,8 +394,31 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_rmsnorm_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
-                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm));
+                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm,
+                                  (const float*)nullptr, 1, (int)rows));
   return DAK_OK;
 }
 
 }  // extern "C"
+
+// One rank: x += bf16(sum_s part[s]) (split-K partials of the row-parallel linear, reduced here),
+// y = RMSNorm(x) -- dak_allreduce_residual_rmsnorm with the reduce kernel folded in.
+dak_status dak::residual_rmsnorm_part(const float* part, int32_t S, void* x, int32_t rows, int32_t cols,
+                                      const void* norm_w, float eps, void* y_norm, int32_t pdl, void* stream) {
+  if (!part || S < 1 || !x || !norm_w || !y_norm || rows <= 0 || cols <= 0 || cols % 8 ||
+      cols > tp::kThreads * 8 * tp::kVec || !aligned16(part) || !aligned16(x) || !aligned16(norm_w) || !aligned16(y_norm))
+    return fail(DAK_EINVAL, "residual_rmsnorm_part: bad arguments");
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(rows);
+  cfg.blockDim = dim3(tp::kThreads);
+  cfg.stream = (cudaStream_t)stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_rmsnorm_kernel, (const __nv_bfloat16*)nullptr, (__nv_bfloat16*)x,
+                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm, part, (int)S,
+                                  (int)rows));
+  return DAK_OK;
+}

@@ -103,25 +103,29 @@ def test_rope_kv_append_matches_oracle():
             assert np.array_equal(rowv, qkv.reshape(B, Hq + 2 * Hkv, d)[b, Hq + Hkv + gkv])
 
 
-def test_llama_tp8_shard_shapes_b64():
-    """One layer at the per-GPU shapes of Llama-3-70B under TP8 (hidden 8192, 8 q heads / 1 kv head,
-    FFN 3584, batch 64 -> N = 64 GEMV columns, GQA group 8), host share forced, vs the oracle."""
+@pytest.mark.parametrize("L,use_comm", [(1, False), (2, True)])
+def test_llama_tp8_shard_shapes_b64(L, use_comm):
+    """Llama-3-70B layers at the per-GPU shapes of TP8 (hidden 8192, 8 q heads / 1 kv head, FFN 3584,
+    batch 64 -> N = 64 GEMV columns, GQA group 8), host share forced, vs the oracle. With a one-rank
+    communicator (the bench's path) the o / down split-K partials are reduced inside the residual +
+    RMSNorm combine kernel (no reduce launch)."""
     import torch
     from paper_2604_26074_b200 import dak
     from paper_2604_26074_b200.engine import HW
     from paper_2604_26074_b200.llama import DakLlama, LlamaConfig
     from tests.test_oracle_llama import make_llama_params
-    L, H, F, V, nh, nkv, d, B, ctx = 1, 8192, 3584, 256, 8, 1, 128, 64, 80
+    H, F, V, nh, nkv, d, B, ctx = 8192, 3584, 256, 8, 1, 128, 64, 80
     g = synth.rng(7070)
     p = make_llama_params(g, L, H, F, V, nh, nkv, d)
     cfg = LlamaConfig(n_layers=L, hidden=H, n_heads=nh, n_kv_heads=nkv, ffn=F, vocab=V, name="llama-tp8-shard")
     hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
     total = (H * (nh + 2 * nkv) * d + nh * d * H + 3 * F * H) * 2 + V * H * 2
-    eng = DakLlama(cfg, B, ctx, hw, mode=dak.PLAN_EXACT, y_req=int(0.05 * total), page_size=64, chunk_pages=1,
-                   weights=_dev(p, torch))
+    comm = dak.comm_init(dak.comm_unique_id(), 0, 1) if use_comm else None
+    eng = DakLlama(cfg, B, ctx, hw, mode=dak.PLAN_EXACT, y_req=int(0.05 * L * total), page_size=64, chunk_pages=1,
+                   weights=_dev(p, torch), comm=comm)
     assert sum(op.h for op in eng.linear_ops()) > 0
-    Kc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)]]
-    Vc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)]]
+    Kc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
+    Vc = [[synth.normal_bf16(g, (ctx - 1, nkv, d)) for _ in range(B)] for _ in range(L)]
     eng.load_kv(Kc, Vc)
     tokens = (np.arange(B) * 7) % V
     eng.tokens.copy_(torch.from_numpy(tokens.astype(np.int32)))
@@ -134,6 +138,8 @@ def test_llama_tp8_shard_shapes_b64():
     from tests.gpu_util import assert_close
     assert_close(got, ref, rtol=3e-2)
     eng.close()
+    if comm:
+        dak.comm_destroy(comm)
 
 
 def test_rmsnorm_and_silu_mul_kernels():
