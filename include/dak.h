@@ -193,6 +193,20 @@ dak_status dak_kv_place(int32_t B, const int32_t* seq_lens, int32_t page_size, i
                         int64_t host_units, int32_t* block_table, int32_t* n_host_pages, int32_t* n_hbm_pages,
                         int64_t* host_tokens);
 
+/* a4 across decode steps (reading R23): the requests grew to
+ * seq_lens and the planner gave the op host_units; every block-table entry takes the tier of
+ * dak_kv_place's chunk-major placement for these lengths and units. An entry keeps its pool slot when
+ * its tier is unchanged; an entry whose tier changes takes the lowest slot of the destination pool
+ * (host_pool_pages / hbm_pool_pages pages) that old_table does not reference -- so slots freed here
+ * are reused only by a later call, and every copy reads a slot nothing writes. Outputs: new_table
+ * [B * max_pages] (caller host array, != old_table) and moves [n_moves][2] (old entry, new entry)
+ * in (request, page) order, for dak_kv_migrate. Pure host computation.
+ * Errors: DAK_EINVAL (bad sizes, old slot outside its pool, more than max_moves moves),
+ * DAK_ECAPACITY (a destination pool has no free slot). */
+dak_status dak_kv_replace(int32_t B, const int32_t* seq_lens, int32_t page_size, int32_t max_pages, int32_t chunk_pages,
+                          int64_t host_units, int32_t host_pool_pages, int32_t hbm_pool_pages, const int32_t* old_table,
+                          int32_t* new_table, int32_t* moves, int32_t max_moves, int32_t* n_moves);
+
 /* =============================================================================================
  * 2. Host tier memory (SMs stream host data straight into SMEM; no HBM staging)
  * ============================================================================================= */
@@ -390,6 +404,14 @@ dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_strid
                          const int32_t* positions, int32_t B, int32_t Hkv, int32_t d, int32_t page_size,
                          int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,
                          dak_stream_t stream);
+
+/* Carry out dak_kv_replace's moves on one layer's pools: page (all Hkv heads, K and V, DAK-PG
+ * layout) of entry moves[2i] copied to entry moves[2i+1]. moves: device int32 [n_moves][2]. Pools as
+ * of dak_attention_args, host pools pinned + mapped. Async on stream (graph-capturable); the
+ * caller orders it after the step that last read the old table and before the first step that
+ * reads the new one. Errors: DAK_EINVAL. */
+dak_status dak_kv_migrate(const int32_t* moves, int32_t n_moves, int32_t Hkv, int32_t page_size, int32_t d, void* k_hbm,
+                          void* v_hbm, void* k_host, void* v_host, dak_stream_t stream);
 
 /* Llama decode KV write with rotary positions (BASELINE configs[2] model): for every request b,
  * rotate q (in place, all Hq heads) and k of the new token at positions[b] (rotate-half pairs

@@ -166,6 +166,60 @@ def kv_place_chunk_major(seq_lens, page_size: int, max_pages: int, chunk_pages: 
     return table, ih, ig, host_tokens
 
 
+def kv_host_units_keep_ratio(h0: int, n0: int, n_new: int) -> int:
+    """Host units of an attention op whose chunk count grew from n0 to n_new while it keeps the
+    planner's ratio x = h0 / n0 (P:L466 per-op ratio x_i; reading R23): round-half-up(x * n_new), the
+    unit rounding of reading R6, in exact rationals, at most n_new."""
+    if n0 == 0:
+        return 0
+    return min(n_new, round_half_up(Fraction(h0, n0) * n_new))
+
+
+def kv_replace(old_table, seq_lens, page_size: int, max_pages: int, chunk_pages: int, host_units: int,
+               host_pool_pages: int, hbm_pool_pages: int):
+    """KV placement across decode steps (reading R23 of DESIGN.md). As the
+    requests grow, the planner is re-run for the new context and the attention op gets new host
+    units; the tier of every block-table entry is then the chunk-major placement of
+    kv_place_chunk_major for the NEW lengths and host units (P:L321-323 oldest rows on the host).
+    A page keeps its pool slot when its tier does not change; a page whose tier changes takes the
+    lowest slot of the destination pool that the OLD table does not reference (slots freed by this
+    re-placement are reused only by the next one, so every copy reads a slot nobody writes).
+
+    Written as the enumeration it describes. Returns (new table [B][max_pages] of uint32, moves as
+    (request, page, old entry, new entry) in (request, page) order). Raises ValueError when a pool
+    runs out of free slots."""
+    HOST = 0x80000000
+    fresh, _, _, _ = kv_place_chunk_major(seq_lens, page_size, max_pages, chunk_pages, host_units)
+    B = len(seq_lens)
+    used_h = set()
+    used_g = set()
+    for b in range(B):
+        for p in range(max_pages):
+            e = int(old_table[b][p])
+            if e & HOST:
+                used_h.add(e & 0x7FFFFFFF)
+            else:
+                used_g.add(e)
+    free_h = [i for i in range(host_pool_pages) if i not in used_h]
+    free_g = [i for i in range(hbm_pool_pages) if i not in used_g]
+    new = [[0] * max_pages for _ in range(B)]
+    moves = []
+    for b in range(B):
+        for p in range(max_pages):
+            old = int(old_table[b][p])
+            want_host = bool(fresh[b][p] & HOST)
+            if bool(old & HOST) == want_host:
+                new[b][p] = old
+                continue
+            pool = free_h if want_host else free_g
+            if not pool:
+                raise ValueError("no free slot in the destination pool")
+            slot = pool.pop(0)
+            new[b][p] = (slot | HOST) if want_host else slot
+            moves.append((b, p, old, new[b][p]))
+    return new, moves
+
+
 def linear_splitk_items(M: int, h: int, splits: int, block: int = 128):
     """Row ownership of a split-K dak_linear launch: every tier is cut into blocks
     of `block` rows (the last may be short) and every block into `splits` K ranges; CTA j of a tier

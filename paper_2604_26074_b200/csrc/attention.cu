@@ -614,6 +614,24 @@ __global__ void pack_pages_kernel(const uint4* __restrict__ src, long long n_blo
   }
 }
 
+// KV re-placement across decode steps (dak_kv_replace's moves): copy whole pages (all kv heads,
+// K and V) from their old slot to their new slot. The DAK-PG layout is the same in both pools, so a
+// page moves as raw 16-byte words. moves[2i] = old entry, moves[2i+1] = new entry (bit 31: host).
+__global__ void migrate_pages_kernel(const int* __restrict__ moves, int n, long long page_u4, uint4* k_hbm,
+                                     uint4* v_hbm, uint4* k_host, uint4* v_host) {
+  const long long total = (long long)n * 2 * page_u4;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long m = i / (2 * page_u4);
+    const long long r = i - m * 2 * page_u4;
+    const bool is_v = r >= page_u4;
+    const long long w = is_v ? r - page_u4 : r;
+    const uint32_t src = (uint32_t)moves[2 * m], dst = (uint32_t)moves[2 * m + 1];
+    const uint4* sp = (src & kHostBit) ? (is_v ? v_host : k_host) : (is_v ? v_hbm : k_hbm);
+    uint4* dp = (dst & kHostBit) ? (is_v ? v_host : k_host) : (is_v ? v_hbm : k_hbm);
+    dp[(long long)(dst & ~kHostBit) * page_u4 + w] = sp[(long long)(src & ~kHostBit) * page_u4 + w];
+  }
+}
+
 // append one token's K and V rows per (request, kv head) at position pos[b] (decode KV write)
 __global__ void append_kernel(const uint4* __restrict__ k_new, const uint4* __restrict__ v_new, long long stride16,
                               const int* block_table, const int* pos, int B, int Hkv, int page, int max_pages,
@@ -884,6 +902,22 @@ dak_status dak_kv_append(const void* k_new, const void* v_new, int64_t row_strid
   DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, attn::append_kernel, (const uint4*)k_new, (const uint4*)v_new, stride / 8,
                                   block_table, positions, B, Hkv, page_size, max_pages, (uint4*)k_hbm, (uint4*)v_hbm,
                                   (uint4*)k_host, (uint4*)v_host, trace_slot(DAK_KIND_APPEND, B, Hkv, (n + 255) / 256)));
+  return DAK_OK;
+}
+
+dak_status dak_kv_migrate(const int32_t* moves, int32_t n_moves, int32_t Hkv, int32_t page_size, int32_t d, void* k_hbm,
+                          void* v_hbm, void* k_host, void* v_host, dak_stream_t stream) {
+  if (n_moves < 0 || (n_moves > 0 && !moves) || Hkv <= 0 || page_size <= 0 || d <= 0 || (d * 2) % 16)
+    return fail(DAK_EINVAL, "dak_kv_migrate: bad arguments");
+  if (n_moves == 0) return DAK_OK;
+  if (!aligned16(k_hbm) || !aligned16(v_hbm) || !aligned16(k_host) || !aligned16(v_host))
+    return fail(DAK_EINVAL, "dak_kv_migrate: pools must be 16-byte aligned");
+  const long long page_u4 = (long long)Hkv * page_size * d * 2 / 16;
+  const long long total = (long long)n_moves * 2 * page_u4;
+  const unsigned grid = (unsigned)std::min<long long>((total + 255) / 256, 4096);
+  attn::migrate_pages_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(moves, n_moves, page_u4, (uint4*)k_hbm, (uint4*)v_hbm,
+                                                                       (uint4*)k_host, (uint4*)v_host);
+  DAK_CUDA_TRY(cudaGetLastError());
   return DAK_OK;
 }
 

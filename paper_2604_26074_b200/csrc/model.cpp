@@ -6,6 +6,8 @@
 //   dak_kv_place             -- the KV byte partition of one attention op: oldest split-KV chunks
 //                               on the host, chunk-major across requests (
 //                               DESIGN.md readings R7, R15)
+//   dak_kv_replace           -- that partition moved along as the requests grow across decode
+//                               steps (reading R23)
 // Compiled with -ffp-contract=off: every double below is one IEEE rounding in the written order,
 // so the T_i values are bit-identical to the oracle's definition (oracle/models.py decode_ops),
 // which the CPU tests check. The oracle is never linked or called from here.
@@ -160,6 +162,60 @@ dak_status dak_kv_place(int32_t B, const int32_t* seq_lens, int32_t page_size, i
   if (n_host_pages) *n_host_pages = ih;
   if (n_hbm_pages) *n_hbm_pages = ig;
   if (host_tokens) *host_tokens = ht;
+  return DAK_OK;
+}
+
+dak_status dak_kv_replace(int32_t B, const int32_t* seq_lens, int32_t page_size, int32_t max_pages, int32_t chunk_pages,
+                          int64_t host_units, int32_t host_pool_pages, int32_t hbm_pool_pages, const int32_t* old_table,
+                          int32_t* new_table, int32_t* moves, int32_t max_moves, int32_t* n_moves) {
+  if (B <= 0 || !seq_lens || page_size <= 0 || max_pages <= 0 || chunk_pages <= 0 || host_units < 0 ||
+      host_pool_pages < 0 || hbm_pool_pages < 0 || !old_table || !new_table || max_moves < 0 || (max_moves && !moves) ||
+      !n_moves || old_table == new_table)
+    return dak::fail(DAK_EINVAL, "dak_kv_replace: bad arguments");
+  const int64_t E = (int64_t)B * max_pages;
+  // tiers of the fresh chunk-major placement for the new lengths and host units
+  std::vector<int32_t> fresh((size_t)E);
+  dak_status st = dak_kv_place(B, seq_lens, page_size, max_pages, chunk_pages, host_units, fresh.data(), nullptr, nullptr,
+                               nullptr);
+  if (st != DAK_OK) return st;
+  // free slots: those the old table does not reference, ascending
+  std::vector<char> used_h((size_t)host_pool_pages, 0), used_g((size_t)hbm_pool_pages, 0);
+  for (int64_t i = 0; i < E; ++i) {
+    const uint32_t e = (uint32_t)old_table[i];
+    const uint32_t slot = e & 0x7FFFFFFFu;
+    if (e & 0x80000000u) {
+      if (slot >= (uint32_t)host_pool_pages) return dak::fail(DAK_EINVAL, "dak_kv_replace: old host slot %u >= pool", slot);
+      used_h[slot] = 1;
+    } else {
+      if (slot >= (uint32_t)hbm_pool_pages) return dak::fail(DAK_EINVAL, "dak_kv_replace: old HBM slot %u >= pool", slot);
+      used_g[slot] = 1;
+    }
+  }
+  int32_t next_h = 0, next_g = 0, nm = 0;
+  for (int64_t i = 0; i < E; ++i) {
+    const uint32_t old = (uint32_t)old_table[i];
+    const bool want_host = ((uint32_t)fresh[(size_t)i] & 0x80000000u) != 0;
+    if (((old & 0x80000000u) != 0) == want_host) {
+      new_table[i] = (int32_t)old;
+      continue;
+    }
+    uint32_t ne;
+    if (want_host) {
+      while (next_h < host_pool_pages && used_h[(size_t)next_h]) ++next_h;
+      if (next_h >= host_pool_pages) return dak::fail(DAK_ECAPACITY, "dak_kv_replace: host pool of %d pages is full", host_pool_pages);
+      ne = (uint32_t)next_h++ | 0x80000000u;
+    } else {
+      while (next_g < hbm_pool_pages && used_g[(size_t)next_g]) ++next_g;
+      if (next_g >= hbm_pool_pages) return dak::fail(DAK_ECAPACITY, "dak_kv_replace: HBM pool of %d pages is full", hbm_pool_pages);
+      ne = (uint32_t)next_g++;
+    }
+    new_table[i] = (int32_t)ne;
+    if (nm >= max_moves) return dak::fail(DAK_EINVAL, "dak_kv_replace: more than max_moves = %d moves", max_moves);
+    moves[2 * nm] = (int32_t)old;
+    moves[2 * nm + 1] = (int32_t)ne;
+    ++nm;
+  }
+  *n_moves = nm;
   return DAK_OK;
 }
 

@@ -224,7 +224,12 @@ _sig("dak_decode_ops", C.c_int32, [C.POINTER(dak_model), C.c_int32, C.c_int64, C
 _sig("dak_kv_place", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32, C.c_int64,
                                  C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                  C.POINTER(C.c_int64)])
-EXPORTED += ["dak_global_offload_bytes", "dak_decode_ops", "dak_kv_place"]
+_sig("dak_kv_replace", C.c_int32, [C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int32, C.c_int32, C.c_int64,
+                                   C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                   C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)])
+_sig("dak_kv_migrate", C.c_int32, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p])
+EXPORTED += ["dak_global_offload_bytes", "dak_decode_ops", "dak_kv_place", "dak_kv_replace", "dak_kv_migrate"]
 
 
 def global_offload_bytes(weight_bytes: int, kv_bytes: int, hbm_budget_bytes: int, host_capacity_bytes: int = -1):
@@ -264,6 +269,28 @@ def kv_place(seq_lens, page_size: int, max_pages: int, chunk_pages: int, host_un
     _check(lib.dak_kv_place(B, sl, int(page_size), int(max_pages), int(chunk_pages), int(host_units),
                             bt.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(nh), C.byref(ng), C.byref(ht)))
     return bt, nh.value, ng.value, ht.value
+
+
+def kv_replace(old_table, seq_lens, page_size: int, max_pages: int, chunk_pages: int, host_units: int,
+               host_pool_pages: int, hbm_pool_pages: int):
+    """dak_kv_replace -> (new block table numpy int32 [B, max_pages], moves numpy int32 [n, 2])."""
+    import numpy as np
+    B = len(seq_lens)
+    sl = (C.c_int32 * B)(*[int(x) for x in seq_lens])
+    old = np.ascontiguousarray(np.asarray(old_table).astype(np.uint32).view(np.int32).reshape(B, max_pages))
+    new = np.zeros((B, max_pages), dtype=np.int32)
+    mv = np.zeros((B * max_pages, 2), dtype=np.int32)
+    n = C.c_int32()
+    P = C.POINTER(C.c_int32)
+    _check(lib.dak_kv_replace(B, sl, int(page_size), int(max_pages), int(chunk_pages), int(host_units),
+                              int(host_pool_pages), int(hbm_pool_pages), old.ctypes.data_as(P), new.ctypes.data_as(P),
+                              mv.ctypes.data_as(P), B * max_pages, C.byref(n)))
+    return new, mv[:n.value].copy()
+
+
+def kv_migrate(moves, n_moves, Hkv, page_size, d, k_hbm, v_hbm, k_host, v_host, stream=None):
+    _check(lib.dak_kv_migrate(_ptr(moves), int(n_moves), int(Hkv), int(page_size), int(d), _ptr(k_hbm), _ptr(v_hbm),
+                              _ptr(k_host), _ptr(v_host), _stream(stream)))
 
 
 # ------------------------------------------------------------------------------------- host tier

@@ -89,8 +89,12 @@ class _DecodeEngine:
     ROLE_KEY = dict(qkv="qkv", q="q", k="k", v="v", o="o", up="up", gate_up="up", down="down")
 
     def _init_common(self, batch, context, hw, unit_rows, page_size, chunk_pages, max_context, n_kv_local,
-                     pdl, congestion_control, n_cta_host, seed, evict_first=True):
+                     pdl, congestion_control, n_cta_host, seed, evict_first=True, kv_replan=False):
         self.B, self.context, self.hw = batch, context, hw
+        self.cur_len = context  # tokens every request holds for the next step (host mirror of seq_lens)
+        # KV placement across decode steps (reading R23): pools sized for any placement, re-placed as
+        # the requests grow (advance -> replan)
+        self.kv_replan = bool(kv_replan)
         self.page, self.unit_rows = page_size, unit_rows
         self.max_context = max(context, max_context or context)
         self.pages_per_req = -(-self.max_context // page_size)
@@ -127,9 +131,11 @@ class _DecodeEngine:
         self.layers = [dict() for _ in range(n_layers)]
         self.attn_host_chunks = [0] * n_layers
         self.head = None
+        self.attn_units = [0] * n_layers
         for o, p in zip(ops, plan):
             if o["role"] == "attn":
                 self.attn_host_chunks[o["layer"]] = p["host_units"]
+                self.attn_units[o["layer"]] = o["n_units"]
                 continue
             name = "head" if o["role"] == "head" else f"L{o['layer']}.{o['role']}"
             op = LinearOp(name, o["M"], o["K"])
@@ -187,10 +193,13 @@ class _DecodeEngine:
         tier pools (prompt KV drawn N(0, 1) in HBM, host pools zeroed then packed by load_kv)."""
         B, ppr = self.B, self.pages_per_req
         page_elems = n_kv_local * self.page * head_dim
-        self.block_tables, self.kv, self.kv_host_tokens = [], [], []
+        self.block_tables, self.kv, self.kv_host_tokens, self.block_tables_np = [], [], [], []
         for l in range(len(self.layers)):
             bt, Ph, Pg, ht = dak.kv_place([self.context] * B, self.page, ppr, self.chunk_pages,
                                           self.attn_host_chunks[l])
+            self.block_tables_np.append(bt)
+            if self.kv_replan:  # room for every page in either pool (placements change as requests grow)
+                Ph, Pg = B * ppr, B * ppr
             kg = torch.zeros(max(Pg, 1) * page_elems, dtype=torch.bfloat16, device="cuda")
             vg = torch.zeros_like(kg)
             kh = self._alloc_host(max(Ph, 1) * page_elems * 2)
@@ -243,12 +252,46 @@ class _DecodeEngine:
 
     # ------------------------------------------------------------------ step
     def advance(self, stream=None):
-        """Move every request to the next position (after a step appended its token's KV)."""
+        """Move every request to the next position (after a step appended its token's KV). With
+        kv_replan, a step that opens a new split-KV chunk first re-places the KV (replan)."""
         if int(self.positions.max()) + 1 >= self.max_context:
             raise ValueError("decode past max_context")
         with torch.cuda.stream(stream or torch.cuda.current_stream()):
             self.positions.add_(1)
             self.seq_lens.add_(1)
+        self.cur_len += 1
+        if self.kv_replan and (self.cur_len - 1) % (self.chunk_pages * self.page) == 0:
+            self.replan(stream)
+
+    def replan(self, stream=None):
+        """KV placement across decode steps (reading R23 of DESIGN.md): every
+        attention op keeps the host ratio the planner gave it, x = host units / units at planning
+        (per-op ratio x_i), as its chunk count grows: host units = round-half-up(x * units),
+        the R6 rounding. dak_kv_replace gives the new block table (chunk-major oldest chunks on the
+        host, pages keep their slot unless their tier changes) and the page moves, dak_kv_migrate
+        copies the moved pages on the device, then the table the captured graph reads is rewritten
+        in place (stream-ordered before the next replay)."""
+        if not self.kv_replan:
+            raise ValueError("replan needs kv_replan=True (pools sized for any placement)")
+        B, ppr, cp, page = self.B, self.pages_per_req, self.chunk_pages, self.page
+        L = self.cur_len
+        n_new = B * (-(-(-(-L // page)) // cp))
+        s = stream or torch.cuda.current_stream()
+        keep = []
+        with torch.cuda.stream(s):
+            for l, (kg, vg, kh, vh, Ph, Pg) in enumerate(self.kv):
+                h0, n0 = self.attn_host_chunks[l], self.attn_units[l]
+                hu = min(n_new, (2 * h0 * n_new + n0) // (2 * n0)) if n0 else 0
+                new, moves = dak.kv_replace(self.block_tables_np[l], [L] * B, page, ppr, cp, hu, Ph, Pg)
+                if len(moves):
+                    mv = torch.from_numpy(moves).cuda()
+                    keep.append(mv)
+                    dak.kv_migrate(mv, len(moves), self.n_kv_local, page, self.head_dim, kg, vg, kh[1], vh[1], s)
+                self.block_tables[l].copy_(torch.from_numpy(new))
+                self.block_tables_np[l] = new
+                hp = ((new.view(np.uint32) & dak.HOST_BIT) != 0).sum(axis=1)
+                self.kv_host_tokens[l] = int(np.minimum(hp * page, L).sum())
+        s.synchronize()
 
     def capture(self, stream: torch.cuda.Stream):
         with torch.cuda.stream(stream):
@@ -269,7 +312,7 @@ class _DecodeEngine:
         tok = 2 * self.n_kv_local * self.head_dim * 2
         for ht in self.kv_host_tokens:
             host += tok * ht
-            hbm += tok * (self.B * self.context - ht)
+            hbm += tok * (self.B * self.cur_len - ht)
         return dict(hbm=hbm, host=host, total=hbm + host)
 
     def close(self):
@@ -291,11 +334,11 @@ class DakOPT(_DecodeEngine):
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
                  host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
                  evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
-                 max_context: int | None = None):
+                 max_context: int | None = None, kv_replan: bool = False):
         self.cfg = cfg
         self.n_kv_local, self.head_dim = cfg.n_kv_heads, cfg.head_dim
         self._init_common(batch, context, hw, unit_rows, page_size, chunk_pages, max_context, cfg.n_kv_heads,
-                          pdl, congestion_control, n_cta_host, seed, evict_first)
+                          pdl, congestion_control, n_cta_host, seed, evict_first, kv_replan)
         self.l2_prefetch = int(l2_prefetch)
         self.fuse_norm = bool(fuse_norm)
         # one [q; k; v] projection per layer (one launch reading x once; reading R18); the paper's

@@ -249,6 +249,31 @@ def test_kv_place_bit_exact_vs_oracle(D):
         D.kv_place([64, 64], 64, 1, 1, 3)  # 3 host units > 2 chunks
 
 
+def test_kv_replace_bit_exact_vs_oracle(D):
+    """dak_kv_replace (KV placement across decode steps, reading R23) equals oracle/partition.py
+    kv_replace bit for bit -- new block table and the (old entry, new entry) moves in order -- on
+    random growing batches; a full destination pool is DAK_ECAPACITY."""
+    from oracle import partition as Pt
+    from tests.test_oracle_partition import _random_replace_case
+    g = np.random.default_rng(47)
+    for trial in range(400):
+        B, page, cp, Ls0, Ls1, max_pages, hu0, hu1 = _random_replace_case(g)
+        old, nh0, ng0, _ = Pt.kv_place_chunk_major(Ls0, page, max_pages, cp, hu0)
+        cap_h = nh0 + int(g.integers(0, B * max_pages + 1))
+        cap_g = B * max_pages
+        try:
+            ref_new, ref_moves = Pt.kv_replace(old, Ls1, page, max_pages, cp, hu1, cap_h, cap_g)
+        except ValueError:
+            with pytest.raises(D.DakError) as e:
+                D.kv_replace(old, Ls1, page, max_pages, cp, hu1, cap_h, cap_g)
+            assert e.value.code == "ECAPACITY"
+            continue
+        new, moves = D.kv_replace(old, Ls1, page, max_pages, cp, hu1, cap_h, cap_g)
+        assert np.array_equal(new.view(np.uint32), np.array(ref_new, dtype=np.uint32)), trial
+        ref_mv = np.array([(s, d) for _, _, s, d in ref_moves], dtype=np.uint32).reshape(-1, 2)
+        assert np.array_equal(moves.view(np.uint32), ref_mv), trial
+
+
 def test_kv_place_matches_planned_bytes_when_chunks_are_full(D):
     """With contexts that fill whole chunks, the placed host bytes equal the planner's host bytes
     for the attention op exactly (units are then uniform: reading R15's mean unit is exact)."""

@@ -102,6 +102,64 @@ def test_engine_multistep_decode_matches_oracle(frac):
     eng.close()
 
 
+def test_engine_kv_replan_across_steps_matches_oracle():
+    """KV placement across decode steps (reading R23): with kv_replan the engine re-places the KV
+    each time the requests open a new split-KV chunk -- the attention ops keep the planner's host
+    ratio, dak_kv_replace moves the next-oldest chunks to the host, dak_kv_migrate copies those pages
+    on the device, the captured graph reads the rewritten tables. Every step's logits match the
+    oracle's multi-step decode, and the block tables after each re-placement equal the oracle's
+    chain (kv_place_chunk_major, then kv_replace with kv_host_units_keep_ratio) bit for bit."""
+    import torch
+    from oracle import partition as Pt
+    from paper_2604_26074_b200 import dak
+    from paper_2604_26074_b200.engine import DakOPT, OPTConfig, HW
+    L, H, F, V, heads, maxpos, B, prompt, steps, page = 2, 256, 512, 1000, 2, 256, 3, 40, 12, 16
+    g = np.random.default_rng(78)
+    p = make_params(g, L, H, F, V, maxpos)
+    cfg = OPTConfig(n_layers=L, hidden=H, n_heads=heads, ffn=F, vocab=V, max_pos=maxpos, name="opt-tiny")
+    hw = HW(hbm_bps=6555.5e9, link_bps=51.5e9)
+    total = (4 * H * H + 2 * F * H) * 2 * L + V * H * 2
+    eng = DakOPT(cfg, B, prompt + 1, hw, mode=dak.PLAN_EXACT, y_req=int(0.45 * total), page_size=page, chunk_pages=1,
+                 weights=_engine_weights(p, L, torch), max_context=prompt + steps + 1, kv_replan=True)
+    assert min(eng.attn_host_chunks) > 0
+    Kc = [[synth.normal_bf16(g, (prompt, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    Vc = [[synth.normal_bf16(g, (prompt, heads, H // heads)) for _ in range(B)] for _ in range(L)]
+    eng.load_kv(Kc, Vc)
+    ppr = eng.pages_per_req
+    ref_tables = [Pt.kv_place_chunk_major([prompt + 1] * B, page, ppr, 1, eng.attn_host_chunks[l])[0] for l in range(L)]
+    n0 = [eng.attn_units[l] for l in range(L)]
+    toks = [np.array([3 + 11 * s, 500 + 7 * s, 900 - 5 * s]) for s in range(steps)]
+    s_ = torch.cuda.Stream()
+    eng.tokens.copy_(torch.from_numpy(toks[0].astype(np.int32)))
+    eng.capture(s_)
+    got, replans = [], 0
+    for s in range(steps):
+        eng.tokens.copy_(torch.from_numpy(toks[s].astype(np.int32)))
+        eng.graph.replay()
+        torch.cuda.synchronize()
+        got.append(Kx.bf16_to_f64(eng.logits.view(torch.int16).cpu().numpy().view(np.uint16)))
+        if s + 1 < steps:
+            eng.advance()
+            torch.cuda.synchronize()
+            Lc = prompt + s + 2
+            if (Lc - 1) % page == 0:  # a new chunk opened: the engine re-placed
+                replans += 1
+                n_new = B * (-(-Lc // page))
+                for l in range(L):
+                    hu = Pt.kv_host_units_keep_ratio(eng.attn_host_chunks[l], n0[l], n_new)
+                    ref_tables[l], _ = Pt.kv_replace(ref_tables[l], [Lc] * B, page, ppr, 1, hu, B * ppr, B * ppr)
+                    dev = eng.block_tables[l].cpu().numpy().view(np.uint32)
+                    assert np.array_equal(dev, np.array(ref_tables[l], dtype=np.uint32)), (s, l)
+    assert replans >= 1
+    host_pages = sum(int(((np.array(t, dtype=np.uint32) & 0x80000000) != 0).sum()) for t in ref_tables)
+    assert host_pages > sum(eng.attn_host_chunks)  # the KV moved to the host as it grew
+    ref = Ly.opt_decode_steps(toks, prompt, p, Kc, Vc, heads)
+    from tests.gpu_util import assert_close
+    for s in range(steps):
+        assert_close(got[s], ref[s], rtol=3e-2)
+    eng.close()
+
+
 @pytest.mark.parametrize("fused_qkv,ctx,max_ctx,frac", [(True, 70, None, 0.3), (False, 63, 67, 0.3), (True, 200, 260, 0.6)])
 def test_engine_plan_and_placement_match_oracle(fused_qkv, ctx, max_ctx, frac):
     """The engine's op list (dak_decode_ops), ratios (dak_plan_ratios) and KV placement

@@ -152,6 +152,88 @@ def test_kv_place_chunk_major_pins():
         assert idx_h == list(range(nh)) and idx_g == list(range(ng))
 
 
+def _random_replace_case(g):
+    """A decode-step re-placement: B requests grow from Ls0 to Ls1 tokens, host units old -> new."""
+    B = int(g.integers(1, 6))
+    page = int(g.choice([16, 64]))
+    cp = int(g.integers(1, 4))
+    Ls0 = [int(g.integers(1, 400)) for _ in range(B)]
+    Ls1 = [L + int(g.integers(0, 200)) for L in Ls0]
+    max_pages = max(-(-L // page) for L in Ls1) + int(g.integers(0, 2))
+    ch0 = sum(-(-(-(-L // page)) // cp) for L in Ls0)
+    ch1 = sum(-(-(-(-L // page)) // cp) for L in Ls1)
+    hu0 = int(g.integers(0, ch0 + 1))
+    hu1 = int(g.integers(0, ch1 + 1))
+    return B, page, cp, Ls0, Ls1, max_pages, hu0, hu1
+
+
+def test_kv_replace_pins():
+    """oracle.partition.kv_replace (reading R23: KV placement across decode steps) against what it
+    must keep: (1) every entry's tier is the fresh chunk-major placement's for the new lengths and
+    host units; (2) an entry whose tier is unchanged keeps its slot, and the moves are exactly the
+    tier changes; (3) no two entries share a slot of a pool, and every move writes a slot the OLD
+    table did not use (copies never overwrite live data); (4) replaying the moves on simulated pools
+    leaves every cached page's content readable through the new table; (5) unchanged lengths and
+    units give no moves. Plus a worked example by hand."""
+    import numpy as np
+    HOST = 0x80000000
+    # worked example: 2 requests of 128 / 200 tokens, page 64, 1-page chunks, 1 host unit (request
+    # 0's page 0); they grow to 192 / 256 tokens and get 4 host units = chunks 0 and 1 of both
+    # requests. Old HBM slots: request 0 pages 1-4 -> 0-3, request 1 pages 0-4 -> 4-8. Free host
+    # slots 1, 2, 3, ... go to (0, 1), (1, 0), (1, 1) in (request, page) order.
+    t0, _, _, _ = Pt.kv_place_chunk_major([128, 200], 64, 5, 1, 1)
+    new, moves = Pt.kv_replace(t0, [192, 256], 64, 5, 1, 4, 10, 10)
+    assert new == [[HOST | 0, HOST | 1, 1, 2, 3], [HOST | 2, HOST | 3, 6, 7, 8]]
+    assert moves == [(0, 1, 0, HOST | 1), (1, 0, 4, HOST | 2), (1, 1, 5, HOST | 3)]
+    g = np.random.default_rng(91)
+    for _ in range(300):
+        B, page, cp, Ls0, Ls1, max_pages, hu0, hu1 = _random_replace_case(g)
+        old, nh0, ng0, _ = Pt.kv_place_chunk_major(Ls0, page, max_pages, cp, hu0)
+        cap_h, cap_g = B * max_pages, B * max_pages
+        new, moves = Pt.kv_replace(old, Ls1, page, max_pages, cp, hu1, cap_h, cap_g)
+        fresh, _, _, _ = Pt.kv_place_chunk_major(Ls1, page, max_pages, cp, hu1)
+        changed = []
+        for b in range(B):
+            for p in range(max_pages):
+                assert bool(new[b][p] & HOST) == bool(fresh[b][p] & HOST)          # (1)
+                if bool(old[b][p] & HOST) == bool(new[b][p] & HOST):
+                    assert new[b][p] == old[b][p]                                  # (2)
+                else:
+                    changed.append((b, p, old[b][p], new[b][p]))
+        assert changed == moves                                                    # (2)
+        flat = [e for row in new for e in row]
+        assert len(set(flat)) == len(flat)                                         # (3)
+        old_used = {e for row in old for e in row}
+        assert all(dst not in old_used for _, _, _, dst in moves)                  # (3)
+        pools = {}                                                                 # (4)
+        for b in range(B):
+            for p in range(max_pages):
+                pools[old[b][p]] = (b, p)
+        for _, _, src, dst in moves:
+            pools[dst] = pools[src]
+        for b in range(B):
+            for p in range(-(-Ls0[b] // page)):
+                assert pools[new[b][p]] == (b, p)
+        same, moves2 = Pt.kv_replace(old, Ls0, page, max_pages, cp, hu0, cap_h, cap_g)
+        assert same == old and moves2 == []                                        # (5)
+    with pytest.raises(ValueError):  # the host pool is full
+        Pt.kv_replace(t0, [192, 256], 64, 5, 1, 4, 2, 10)
+
+
+def test_kv_host_units_keep_ratio_pins():
+    """round-half-up of x * n in exact rationals (reading R23 with R6's rounding): exact halves go up,
+    the ratio is kept exactly when n scales by an integer, never more than n units, 0 of 0."""
+    assert Pt.kv_host_units_keep_ratio(1, 4, 6) == 2        # 1.5 -> 2
+    assert Pt.kv_host_units_keep_ratio(1, 4, 5) == 1        # 1.25 -> 1
+    assert Pt.kv_host_units_keep_ratio(3, 8, 12) == 5       # 4.5 -> 5
+    assert Pt.kv_host_units_keep_ratio(0, 7, 100) == 0
+    assert Pt.kv_host_units_keep_ratio(7, 7, 9) == 9
+    assert Pt.kv_host_units_keep_ratio(0, 0, 5) == 0
+    for h0 in range(0, 9):
+        for k in range(1, 5):
+            assert Pt.kv_host_units_keep_ratio(h0, 8, 8 * k) == h0 * k
+
+
 def test_linear_splitk_items_cover_rows():
     """oracle.partition.linear_splitk_items: every row of each tier is owned by exactly `splits`
     CTAs of that tier, in blocks of `block` rows (the last short), host tier first."""
