@@ -254,7 +254,7 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------------------------------------
-def make_llama(a, hw, world, rank, dak):
+def make_llama(a, hw, world, rank, dak, cal_kw=None):
     """BASELINE configs[2]: Llama-3-70B decode, batch 64, 64k context, TP8. Weights + KV of one rank
     (17.6 GB + 171.8 GB) exceed HBM, so the global ratio is forced by capacity (EXACT mode)
     against an HBM budget of 168 GB (12 GB kept for workspace); the default run is an 8-layer subset
@@ -292,7 +292,7 @@ def make_llama(a, hw, world, rank, dak):
     y_req, R = dak.global_offload_bytes(w_bytes, kv_bytes, budget)
     eng = DakLlama(cfg, batch, context, hw, tp_rank=rank, tp_size=tp_size, comm=comm, mode=dak.PLAN_EXACT,
                    y_req=y_req, pdl=not a.no_pdl, congestion_control=not a.no_cc, seed=1234 + rank,
-                   chunk_pages=a.chunk_pages, nvls=a.nvls and world > 1)
+                   chunk_pages=a.chunk_pages, nvls=a.nvls and world > 1, **(cal_kw or {}))
     wl = dict(workload="llama3-70b-tp8-b%d-ctx%d" % (batch, context), model_shape="Llama-3-70B (TP%d shard)" % tp_size,
               batch=batch, context=context, layers=layers, layers_model=80,
               extrapolation="x%d per token step" % (80 // layers) if layers != 80 else None,
@@ -330,6 +330,8 @@ def main():
     ap.add_argument("--nvls", action="store_true", help="Llama TP (>= 2 ranks): NVLS combine instead of ncclAllReduce")
     ap.add_argument("--ratio", type=float, default=None, help="force global offload ratio R (EXACT mode)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--calibrate", action="store_true",
+                    help="run dak_calibrate (P:L533-535) first: planner rates and congestion control from the sweep")
     ap.add_argument("--l2-prefetch-mb", type=float, default=0.0, help="L2 warm-up of the next linear (0: off)")
     ap.add_argument("--no-evict-first", action="store_true")
     ap.add_argument("--no-fuse-norm", action="store_true", help="LayerNorm kernels instead of the fused pre-norm")
@@ -359,23 +361,36 @@ def main():
     ph, pl, plan_src = planner_rates(hbm_gbs, link_gbs)
     hw = HW(hbm_bps=(a.plan_hbm_gbs or ph) * 1e9, link_bps=(a.plan_link_gbs or pl) * 1e9,
             host_latency_s=a.plan_host_latency_us * 1e-6)
+    cal = None
+    if a.calibrate:  # the online calibration sweep, before any decode kernel
+        hbm_buf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda")
+        hp, dp = dak.host_alloc(256 << 20, numa_node=dak.device_numa_node())
+        try:
+            cal, _ = dak.calibrate(hbm_buf, hbm_buf.numel(), dp, 256 << 20)
+        finally:
+            dak.host_free(hp)
+        del hbm_buf
+        torch.cuda.empty_cache()
+        hw = HW.from_calibration(cal)
+        plan_src = "dak_calibrate"
+    cal_kw = dict(n_cta_host=max(1, cal["n_cta_host"]), host_inflight_kb=int(cal["host_inflight_bytes"] // 1024)) if cal else {}
     llama = a.workload == "llama3-70b-tp8"
     if llama:
-        eng, cfg, wl = make_llama(a, hw, world, rank, dak)
+        eng, cfg, wl = make_llama(a, hw, world, rank, dak, cal_kw)
     else:
         layers = a.layers or 48
         cfg = OPT_30B if layers == 48 else OPTConfig(n_layers=layers)
         eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_BALANCED, y_req=0, pdl=not a.no_pdl,
                      congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
                      evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
-                     seed=1234 + rank, chunk_pages=a.chunk_pages)
+                     seed=1234 + rank, chunk_pages=a.chunk_pages, **cal_kw)
         if a.ratio is not None:  # forced global ratio: EXACT mode at y_req = R * sum C_i
             tot = sum(o["total_bytes"] for o in eng.plan_ops)
             eng.close()
             eng = DakOPT(cfg, a.batch, a.context, hw, mode=dak.PLAN_EXACT, y_req=int(a.ratio * tot), pdl=not a.no_pdl,
                          congestion_control=not a.no_cc, l2_prefetch=int(a.l2_prefetch_mb * (1 << 20)),
                          evict_first=not a.no_evict_first, fuse_norm=not a.no_fuse_norm,
-                     seed=1234 + rank, chunk_pages=a.chunk_pages)
+                         seed=1234 + rank, chunk_pages=a.chunk_pages, **cal_kw)
     nb = eng.bytes_per_step()
     stream = torch.cuda.Stream()
     g = eng.capture(stream)
@@ -497,6 +512,8 @@ def main():
                             execution="per-op kernels (dak_layer, PDL, CUDA graph)",
                             parallelism="dp%d replicas (weak scaling, no collective)" % world)),
                 tokens_per_s=round(tok_s, 2), roofline=roofline, e2e=e2e, clocks=clocks, per_rank=per_rank,
+                **({"calibration": dict(cal, hbm_gbs=round(cal["hbm_bps"] / 1e9, 1), link_gbs=round(cal["link_bps"] / 1e9, 2),
+                                        host_latency_us=round(cal["host_latency_s"] * 1e6, 3))} if cal else {}),
                 **({"tokens_per_s_full_model_extrapolated": round(tok_s * cfg.n_layers / 80, 2)}
                    if llama and cfg.n_layers != 80 else {}),
                 gpu_launches=eng.kernels_per_step() * a.steps)

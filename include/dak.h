@@ -223,6 +223,60 @@ dak_status dak_host_free(void* host_ptr);
 dak_status dak_device_numa_node(int32_t* node);
 
 /* =============================================================================================
+ * 2b. Congestion-control calibration (§3.3; SURVEY §8(f) rank 4 "online calibration")
+ * ============================================================================================= */
+
+/* Sweep of the calibration: n_host[i] host CTAs x window[j] x chunk_bytes host bytes in flight per
+ * host CTA. Steady-state probe runs last duration_us; every sweep point times dak_linear (N = 8,
+ * K = 7168, op_mb MiB of weights at the balanced ratio) end to end, median of reps chains of 8.
+ * tolerance in [0, 1): the choice is the cheapest point within that fraction of the fastest. */
+typedef struct {
+  int32_t n_host[8];
+  int32_t n_n_host;
+  int32_t window[8];
+  int32_t n_window;
+  int32_t chunk_bytes;
+  int32_t duration_us;
+  int32_t reps;
+  int32_t op_mb;      /* weight bytes of the end-to-end probe GEMV in MiB (0: 384) */
+  double tolerance;
+} dak_calib_opts;
+
+/* Calibrated operating point: the launch configuration (dak_launch_cfg.n_cta_host and
+ * host_inflight_kb = host_inflight_bytes / 1024) and the machine model of the planner (dak_hw:
+ * hbm_bps = B_g and link_bps = B_h measured CONCURRENTLY at that point, host_latency_s = tau: one
+ * chunk in flight, minus its transfer time at link_bps). hbm_alone_bps: every SM on HBM. */
+typedef struct {
+  int32_t n_cta_host;
+  int32_t window;
+  int64_t host_inflight_bytes;
+  double hbm_bps;
+  double link_bps;
+  double hbm_alone_bps;
+  double host_latency_s;
+} dak_calib_result;
+
+/* The choice (pure): table[i][j] = {HBM B/s, host B/s} of the end-to-end probe op at point
+ * (n_host[i], window[j]) (each tier's bytes / the op's time): among the points whose aggregate (HBM +
+ * host, summed in that order) is >= (1 - tolerance) x the best ("the exact SM allocation to the host
+ * that maximizes end-to-end throughput"), the fewest host CTAs, then the smallest window
+ * ("exactly enough SMs ... and avoid congestion"); ties: the first index. Errors: DAK_EINVAL. */
+dak_status dak_calib_select(const double* table, int32_t n_n_host, int32_t n_window, const int32_t* n_host,
+                            const int32_t* window, double tolerance, int32_t* best_i, int32_t* best_j);
+
+/* The "lightweight parameter-sweeping profiler executed prior to kernel launch": measures
+ * B_g (every SM on HBM), the saturated link rate and the link latency with steady-state probes (the
+ * decode kernels' bulk-copy load path without the math, one CTA per SM), then times the split GEMV
+ * at the balanced ratio r = B_h / (B_g + B_h) over opts' grid, on
+ * hbm_buf (device; >= op_mb MiB + 1 MiB, and well above the 126 MB L2) and host_buf (pinned +
+ * mapped; >= 16 chunks and the probe GEMV's host rows, ~1% of op_mb), fills *out and, when table !=
+ * NULL, table[n_n_host][n_window][2] (each tier's bytes / the GEMV's time, B/s).
+ * SETUP-TIME call: blocking, on an internal stream, not graph-capturable; allocates a small device
+ * buffer. Errors: DAK_EINVAL (bad options / buffers), DAK_ECUDA. */
+dak_status dak_calibrate(const void* hbm_buf, size_t hbm_bytes, const void* host_buf, size_t host_bytes,
+                         const dak_calib_opts* opts, dak_calib_result* out, double* table);
+
+/* =============================================================================================
  * 3. Split-source linear: y = act(x W^T + bias) + residual   (§3.1)
  *    W [M,K] is split along M: rows [0,h) in host memory, rows [h,M) in HBM (R7/R14).
  * ============================================================================================= */
@@ -269,7 +323,9 @@ typedef struct {
                               /* N > 512 (tcgen05 groups of ceil(N/512) CTAs over the same rows): */
                               /* >= 2 makes each group one cluster whose rank 0 multicasts every  */
                               /* weight tile to the group: one HBM / link fetch per tile (Table 1)*/
-  int32_t reserved;
+  int32_t host_inflight_kb;   /* congestion control: host bytes in flight over all host CTAs, in KB */
+                              /* (0: the built-in defaults, 256 KB linear / 512 KB attention;     */
+                              /* dak_calibrate's host_inflight_bytes / 1024)                        */
 } dak_launch_cfg;
 
 typedef struct {

@@ -166,6 +166,24 @@ def kv_place_chunk_major(seq_lens, page_size: int, max_pages: int, chunk_pages: 
     return table, ih, ig, host_tokens
 
 
+def calib_choice(table, n_host, window, tolerance: float):
+    """Congestion-control operating point from the calibration sweep (reading R24 of
+    DESIGN.md): table[i][j] = (HBM B/s, host B/s) of a split op run end to end at the balanced ratio
+    r* with n_host[i] host CTAs and window[j] requests in flight per host CTA (bytes of each tier /
+    the op's time). Its aggregate HBM + host (summed in that order, IEEE double) is the op's
+    end-to-end throughput ("the exact SM allocation to the host that maximizes end-to-end
+    throughput"); among the points within `tolerance` of the best -- aggregate >=
+    best * (1 - tolerance) -- the fewest host CTAs, then the smallest window ("provisions exactly
+    enough SMs ... and avoid congestion"); ties: the first index. Returns (i, j)."""
+    agg = [[float(table[i][j][0]) + float(table[i][j][1]) for j in range(len(window))] for i in range(len(n_host))]
+    best = max(max(row) for row in agg)
+    thr = best * (1.0 - tolerance)
+    cands = [(n_host[i], window[j], i, j) for i in range(len(n_host)) for j in range(len(window)) if agg[i][j] >= thr]
+    n_min = min(c[0] for c in cands)
+    w_min = min(c[1] for c in cands if c[0] == n_min)
+    return next((c[2], c[3]) for c in cands if c[0] == n_min and c[1] == w_min)
+
+
 def kv_host_units_keep_ratio(h0: int, n0: int, n_new: int) -> int:
     """Host units of an attention op whose chunk count grew from n0 to n_new while it keeps the
     planner's ratio x = h0 / n0 (P:L466 per-op ratio x_i; reading R23): round-half-up(x * n_new), the

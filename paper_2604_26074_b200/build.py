@@ -40,6 +40,7 @@ SOURCES = [
     ("layer.cu", []),
     ("tp.cu", []),
     ("nvls.cu", ["-I", NCCL_INC]),
+    ("calib.cu", []),
 ]
 
 

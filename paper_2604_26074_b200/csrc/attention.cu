@@ -62,6 +62,7 @@ struct Params {
   int max_slots;      // ring slots per warp cap (<= kMaxSlots)
   int host_window;    // host CTAs: max in-flight tiles per warp (0: none)
   int host_inflight;  // host CTAs: max in-flight bytes per CTA (congestion control; 0: none)
+  int host_budget;    // host bytes in flight over all host CTAs (auto host-CTA count)
   int off_pairs;
   const uint4* k_new;  // fused append: new token rows (16-byte units), nullptr: off
   const uint4* v_new;
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
     hu *= p.Hkv;
     n_host = hu ? min(min(16, (hu + 3) / 4), (int)gridDim.x - 1) : 0;
     n_hbm = (int)gridDim.x - n_host;
-    if (host_inflight > 0 && n_host > 0) host_inflight = max(2 * 16 * kD * 2, (512 * 1024) / n_host);
+    if (host_inflight > 0 && n_host > 0) host_inflight = max(2 * 16 * kD * 2, p.host_budget / n_host);
   }
   const bool host = cta < n_host;
   const int my_j = host ? cta : cta - n_host;
@@ -777,7 +778,9 @@ static dak_status make_plan(const dak_attention_args* a, Plan* out, bool need_pt
   int n_host = c.n_cta_host > 0 ? c.n_cta_host : (a->k_host ? 1 : 0);
   if (!a->k_host) n_host = 0;
   p.host_window = c.window > 0 ? c.window : 0;
-  p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, (512 * 1024) / std::max(1, n_host)) : 0;
+  // congestion budget: host bytes in flight over all host CTAs (dak_calibrate, else 512 KB)
+  p.host_budget = c.host_inflight_kb > 0 ? c.host_inflight_kb * 1024 : 512 * 1024;
+  p.host_inflight = (c.window <= 0 && c.congestion_control) ? (int)std::max<long long>(2 * 16 * kD * 2, p.host_budget / std::max(1, n_host)) : 0;
   int n_hbm = c.n_cta_hbm;
   if (n_hbm <= 0) {
     if (g_sms <= 0) {

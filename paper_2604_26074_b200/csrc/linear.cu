@@ -1764,7 +1764,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
     if (c.window > 0) window = std::min(c.window, p.stages_host);
     else if (c.congestion_control) {
       const long long hstage = std::max<long long>(1, rmax_host * kc * 2);
-      window = (int)std::min<long long>(p.stages_host, std::max<long long>(1, ceil_div(256 * 1024, hstage * n_stream_host)));
+      const long long budget = c.host_inflight_kb > 0 ? (long long)c.host_inflight_kb * 1024 : 256 * 1024;  // dak_calibrate
+      window = (int)std::min<long long>(p.stages_host, std::max<long long>(1, ceil_div(budget, hstage * n_stream_host)));
     }
   }
   p.window = std::max(1, window);

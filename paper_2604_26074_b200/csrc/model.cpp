@@ -8,6 +8,8 @@
 //                               DESIGN.md readings R7, R15)
 //   dak_kv_replace           -- that partition moved along as the requests grow across decode
 //                               steps (reading R23)
+//   dak_calib_select         -- the choice of the congestion-control operating point from the
+//                               calibration sweep (reading R24)
 // Compiled with -ffp-contract=off: every double below is one IEEE rounding in the written order,
 // so the T_i values are bit-identical to the oracle's definition (oracle/models.py decode_ops),
 // which the CPU tests check. The oracle is never linked or called from here.
@@ -216,6 +218,30 @@ dak_status dak_kv_replace(int32_t B, const int32_t* seq_lens, int32_t page_size,
     ++nm;
   }
   *n_moves = nm;
+  return DAK_OK;
+}
+
+dak_status dak_calib_select(const double* table, int32_t n_n_host, int32_t n_window, const int32_t* n_host,
+                            const int32_t* window, double tolerance, int32_t* best_i, int32_t* best_j) {
+  if (!table || n_n_host <= 0 || n_window <= 0 || !n_host || !window || !best_i || !best_j ||
+      !(tolerance >= 0.0 && tolerance < 1.0))
+    return dak::fail(DAK_EINVAL, "dak_calib_select: bad arguments");
+  const int64_t n = (int64_t)n_n_host * n_window;
+  double best = -1.0;
+  for (int64_t k = 0; k < n; ++k) best = std::max(best, table[2 * k] + table[2 * k + 1]);
+  const double thr = best * (1.0 - tolerance);
+  int32_t bi = -1, bj = -1;
+  for (int32_t i = 0; i < n_n_host; ++i)
+    for (int32_t j = 0; j < n_window; ++j) {
+      const int64_t k = (int64_t)i * n_window + j;
+      if (table[2 * k] + table[2 * k + 1] < thr) continue;
+      if (bi < 0 || n_host[i] < n_host[bi] || (n_host[i] == n_host[bi] && window[j] < window[bj])) {
+        bi = i;
+        bj = j;
+      }
+    }
+  *best_i = bi;
+  *best_j = bj;
   return DAK_OK;
 }
 

@@ -52,7 +52,7 @@ class dak_op_plan(C.Structure):
 class dak_launch_cfg(C.Structure):
     _fields_ = [("n_cta_host", C.c_int32), ("n_cta_hbm", C.c_int32), ("window", C.c_int32), ("stages", C.c_int32),
                 ("congestion_control", C.c_int32), ("pdl", C.c_int32), ("force_path", C.c_int32),
-                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("reserved", C.c_int32)]
+                ("l2_policy", C.c_int32), ("cluster", C.c_int32), ("host_inflight_kb", C.c_int32)]
 
 
 class dak_linear_args(C.Structure):
@@ -291,6 +291,59 @@ def kv_replace(old_table, seq_lens, page_size: int, max_pages: int, chunk_pages:
 def kv_migrate(moves, n_moves, Hkv, page_size, d, k_hbm, v_hbm, k_host, v_host, stream=None):
     _check(lib.dak_kv_migrate(_ptr(moves), int(n_moves), int(Hkv), int(page_size), int(d), _ptr(k_hbm), _ptr(v_hbm),
                               _ptr(k_host), _ptr(v_host), _stream(stream)))
+
+
+# ------------------------------------------------------------------------------------- calibration
+class dak_calib_opts(C.Structure):
+    _fields_ = [("n_host", C.c_int32 * 8), ("n_n_host", C.c_int32), ("window", C.c_int32 * 8), ("n_window", C.c_int32),
+                ("chunk_bytes", C.c_int32), ("duration_us", C.c_int32), ("reps", C.c_int32), ("op_mb", C.c_int32),
+                ("tolerance", C.c_double)]
+
+
+class dak_calib_result(C.Structure):
+    _fields_ = [("n_cta_host", C.c_int32), ("window", C.c_int32), ("host_inflight_bytes", C.c_int64),
+                ("hbm_bps", C.c_double), ("link_bps", C.c_double), ("hbm_alone_bps", C.c_double),
+                ("host_latency_s", C.c_double)]
+
+
+_sig("dak_calib_select", C.c_int32, [C.POINTER(C.c_double), C.c_int32, C.c_int32, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32), C.c_double, C.POINTER(C.c_int32), C.POINTER(C.c_int32)])
+_sig("dak_calibrate", C.c_int32, [C.c_void_p, C.c_size_t, C.c_void_p, C.c_size_t, C.POINTER(dak_calib_opts),
+                                  C.POINTER(dak_calib_result), C.POINTER(C.c_double)])
+EXPORTED += ["dak_calib_select", "dak_calibrate"]
+
+
+def calib_select(table, n_host, window, tolerance: float):
+    """dak_calib_select: table [len(n_host)][len(window)][2] (HBM, host B/s) -> (i, j) of the choice."""
+    import numpy as np
+    t = np.ascontiguousarray(np.asarray(table, dtype=np.float64))
+    ni, nw = len(n_host), len(window)
+    hs = (C.c_int32 * ni)(*[int(v) for v in n_host])
+    ws = (C.c_int32 * nw)(*[int(v) for v in window])
+    bi, bj = C.c_int32(), C.c_int32()
+    _check(lib.dak_calib_select(t.ctypes.data_as(C.POINTER(C.c_double)), ni, nw, hs, ws, float(tolerance),
+                                C.byref(bi), C.byref(bj)))
+    return bi.value, bj.value
+
+
+def calibrate(hbm_buf, hbm_bytes: int, host_dev_ptr, host_bytes: int, n_host=(1, 2, 4, 8, 16),
+              window=(1, 2, 4, 6, 8), chunk_bytes: int = 16384, duration_us: int = 300, reps: int = 3,
+              tolerance: float = 0.005, op_mb: int = 384):
+    """dak_calibrate -> (result dict, table numpy [len(n_host), len(window), 2])."""
+    import numpy as np
+    o = dak_calib_opts()
+    o.n_n_host, o.n_window = len(n_host), len(window)
+    for i, v in enumerate(n_host):
+        o.n_host[i] = int(v)
+    for j, v in enumerate(window):
+        o.window[j] = int(v)
+    o.chunk_bytes, o.duration_us, o.reps, o.tolerance = int(chunk_bytes), int(duration_us), int(reps), float(tolerance)
+    o.op_mb = int(op_mb)
+    r = dak_calib_result()
+    tab = np.zeros((len(n_host), len(window), 2), dtype=np.float64)
+    _check(lib.dak_calibrate(_ptr(hbm_buf), int(hbm_bytes), _ptr(host_dev_ptr), int(host_bytes), C.byref(o), C.byref(r),
+                             tab.ctypes.data_as(C.POINTER(C.c_double))))
+    return {f: getattr(r, f) for f, _ in dak_calib_result._fields_}, tab
 
 
 # ------------------------------------------------------------------------------------- host tier

@@ -52,6 +52,13 @@ class HW:
     host_latency_s: float = 0.0  # latency-aware planner extension (dak_hw.host_latency_s)
     host_capacity_bytes: int = -1
 
+    @classmethod
+    def from_calibration(cls, cal: dict, peak_flops: float = 1.3554e15):
+        """The planner's machine model measured by dak_calibrate: B_g and B_h at the
+        chosen congestion-control point (concurrent rates), tau = the link latency."""
+        return cls(hbm_bps=cal["hbm_bps"], link_bps=cal["link_bps"], peak_flops=peak_flops,
+                   host_latency_s=cal["host_latency_s"])
+
     def as_dict(self):
         return dict(hbm_bps=self.hbm_bps, link_bps=self.link_bps,
                     host_dram_bps=self.host_dram_bps or self.link_bps, host_capacity_bytes=self.host_capacity_bytes,
@@ -89,7 +96,8 @@ class _DecodeEngine:
     ROLE_KEY = dict(qkv="qkv", q="q", k="k", v="v", o="o", up="up", gate_up="up", down="down")
 
     def _init_common(self, batch, context, hw, unit_rows, page_size, chunk_pages, max_context, n_kv_local,
-                     pdl, congestion_control, n_cta_host, seed, evict_first=True, kv_replan=False):
+                     pdl, congestion_control, n_cta_host, seed, evict_first=True, kv_replan=False,
+                     host_inflight_kb=0):
         self.B, self.context, self.hw = batch, context, hw
         self.cur_len = context  # tokens every request holds for the next step (host mirror of seq_lens)
         # KV placement across decode steps (reading R23): pools sized for any placement, re-placed as
@@ -105,8 +113,10 @@ class _DecodeEngine:
         self.chunks_per_req = -(-self.pages_per_req // chunk_pages)
         self.pdl = int(pdl)
         self.n_cta_host = n_cta_host
+        # congestion control: host CTAs and host bytes in flight (dak_calibrate's choice when given;
+        # 0 = the library's defaults)
         self.launch = dict(pdl=self.pdl, congestion_control=int(congestion_control), n_cta_host=n_cta_host,
-                           l2_policy=0 if evict_first else 1)
+                           l2_policy=0 if evict_first else 1, host_inflight_kb=int(host_inflight_kb))
         # attention: host CTAs chosen by the library from the block table (dak_attention auto mode)
         self.attn_launch = dict(self.launch, n_cta_host=0)
         self.sms = dak.device_sms()
@@ -334,11 +344,11 @@ class DakOPT(_DecodeEngine):
                  pdl: bool = True, congestion_control: bool = True, weights: dict | None = None,
                  host_override: dict | None = None, n_cta_host: int = 2, l2_prefetch: int = 0,
                  evict_first: bool = True, fuse_norm: bool = True, fused_qkv: bool = True,
-                 max_context: int | None = None, kv_replan: bool = False):
+                 max_context: int | None = None, kv_replan: bool = False, host_inflight_kb: int = 0):
         self.cfg = cfg
         self.n_kv_local, self.head_dim = cfg.n_kv_heads, cfg.head_dim
         self._init_common(batch, context, hw, unit_rows, page_size, chunk_pages, max_context, cfg.n_kv_heads,
-                          pdl, congestion_control, n_cta_host, seed, evict_first, kv_replan)
+                          pdl, congestion_control, n_cta_host, seed, evict_first, kv_replan, host_inflight_kb)
         self.l2_prefetch = int(l2_prefetch)
         self.fuse_norm = bool(fuse_norm)
         # one [q; k; v] projection per layer (one launch reading x once; reading R18); the paper's

@@ -45,7 +45,7 @@ class DakLlama(_DecodeEngine):
                  comm=None, mode: int = dak.PLAN_BALANCED, y_req: int = 0, unit_rows: int = 16, page_size: int = 64,
                  chunk_pages: int = 0, seed: int = 0, pdl: bool = True, congestion_control: bool = True,
                  weights: dict | None = None, n_cta_host: int = 2, fuse_norm: bool | None = None,
-                 nvls: bool = False):
+                 nvls: bool = False, host_inflight_kb: int = 0):
         self.cfg = cfg
         self.rank, self.world, self.comm = tp_rank, tp_size, comm
         # operand transforms fused into the linears only at small batch: above 16 columns every CTA
@@ -54,7 +54,7 @@ class DakLlama(_DecodeEngine):
         self.dims = tp.local_dims(cfg.n_heads, cfg.n_kv_heads, cfg.ffn, cfg.vocab, tp_size)
         self.n_kv_local, self.head_dim = self.dims["n_kv"], cfg.head_dim
         self._init_common(batch, context, hw, unit_rows, page_size, chunk_pages, None, self.dims["n_kv"], pdl,
-                          congestion_control, n_cta_host, seed + 7919 * tp_rank)
+                          congestion_control, n_cta_host, seed + 7919 * tp_rank, host_inflight_kb=host_inflight_kb)
         self._plan(mode, y_req)
         self._allocate(weights)
         self._kv_pools(self.dims["n_kv"], cfg.head_dim)

@@ -274,6 +274,25 @@ def test_kv_replace_bit_exact_vs_oracle(D):
         assert np.array_equal(moves.view(np.uint32), ref_mv), trial
 
 
+def test_calib_select_bit_exact_vs_oracle(D):
+    """dak_calib_select (the calibration's choice, reading R24) equals oracle/partition.py
+    calib_choice on random sweeps, with integer-valued rates (exact ties) and real-valued ones."""
+    from oracle import partition as Pt
+    g = np.random.default_rng(53)
+    for trial in range(500):
+        ni, nw = int(g.integers(1, 9)), int(g.integers(1, 9))
+        n_host = [int(v) for v in g.integers(1, 20, ni)]
+        window = [int(v) for v in g.integers(1, 9, nw)]
+        if trial % 2:
+            tab = g.integers(0, 5, (ni, nw, 2)).astype(np.float64) * 1e9
+        else:
+            tab = np.stack([g.uniform(5e12, 7e12, (ni, nw)), g.uniform(1e10, 6e10, (ni, nw))], axis=-1)
+        tol = float(g.choice([0.0, 0.005, 0.02, 0.1]))
+        assert D.calib_select(tab, n_host, window, tol) == Pt.calib_choice(tab.tolist(), n_host, window, tol), trial
+    with pytest.raises(D.DakError):
+        D.calib_select(np.zeros((1, 1, 2)), [1], [1], 1.5)
+
+
 def test_kv_place_matches_planned_bytes_when_chunks_are_full(D):
     """With contexts that fill whole chunks, the placed host bytes equal the planner's host bytes
     for the attention op exactly (units are then uniform: reading R15's mean unit is exact)."""

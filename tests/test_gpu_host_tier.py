@@ -70,3 +70,25 @@ def test_attention_auto_host_ctas_bitwise(D, Ls, frac, cp):
     for nh in (1, 3):
         got, _, _ = run_attn(D, torch, Ls, 2, 8, 64, cp, frac, seed=71, n_cta_host=nh)
         assert np.array_equal(got, auto)
+
+
+def test_calibrate_sweep_and_choice(D):
+    """dak_calibrate (the parameter-sweeping profiler run before the kernels): on the
+    B200's PCIe link the probe measures an HBM rate near the copy peak with every SM on HBM, a link
+    rate of tens of GB/s that rises with the bytes in flight, a positive link latency, and its choice
+    is dak_calib_select's over the table it returns."""
+    import torch
+    hbm = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    hp, dp = D.host_alloc(64 << 20)
+    try:
+        n_host, window = (1, 2, 4), (1, 2, 4, 8)
+        res, tab = D.calibrate(hbm, hbm.numel(), dp, 64 << 20, n_host=n_host, window=window, duration_us=200, reps=3)
+    finally:
+        D.host_free(hp)
+    assert 3e12 < res["hbm_alone_bps"] < 9e12
+    assert 1e10 < res["link_bps"] < 1e11 and 3e12 < res["hbm_bps"] < 9e12
+    assert 0 < res["host_latency_s"] < 50e-6
+    i, j = D.calib_select(tab, n_host, window, 0.005)
+    assert (res["n_cta_host"], res["window"]) == (n_host[i], window[j])
+    assert res["host_inflight_bytes"] == n_host[i] * window[j] * 16384
+    assert tab[0, -1].sum() > tab[0, 0].sum()  # one host CTA: more requests in flight, a faster op

@@ -234,6 +234,30 @@ def test_kv_host_units_keep_ratio_pins():
             assert Pt.kv_host_units_keep_ratio(h0, 8, 8 * k) == h0 * k
 
 
+def test_calib_choice_pins():
+    """oracle.partition.calib_choice (reading R24) on an end-to-end sweep shaped like the paper's
+    Fig. 6: a balanced split op of C bytes at r* = B_h / (B_g + B_h) takes
+    max(HBM part / B_g(n, w), host part / B_h(n, w)); B_h rises with host SMs x window until the link
+    saturates, B_g degrades past 8 requests in flight (the GH200 congestion). The choice is the
+    cheapest point within the tolerance of the fastest; exact ties go to the first index."""
+    n_host, window = [1, 2, 4, 8, 16], [1, 2, 4, 8]
+    Bg, Bh = 6500.0, 50.0
+    r = Bh / (Bg + Bh)
+    bh = lambda n, w: min(Bh, 7.0 * n * w)
+    bg = lambda n, w: Bg - (0.0 if n * w <= 8 else 30.0 * (n * w - 8))
+    t = lambda n, w: max((1 - r) / bg(n, w), r / bh(n, w))  # per byte of the op
+    tab = [[((1 - r) / t(n, w), r / t(n, w)) for w in window] for n in n_host]
+    i, j = Pt.calib_choice(tab, n_host, window, 0.0)
+    assert (n_host[i], window[j]) == (1, 8)     # 8 in flight saturate the link, no congestion
+    i, j = Pt.calib_choice(tab, n_host, window, 0.2)
+    assert (n_host[i], window[j]) == (1, 8)     # everything below 8 in flight loses > 20%
+    i, j = Pt.calib_choice(tab, n_host, window, 0.5)
+    assert (n_host[i], window[j]) == (1, 4)     # 28 of 50 GB/s: the op at 3668 of 6550 is within 50%
+    tab2 = [[(100.0, 0.0), (100.0, 0.0)], [(100.0, 0.0), (100.0, 0.0)]]
+    assert Pt.calib_choice(tab2, [2, 2], [3, 3], 0.0) == (0, 0)    # ties: first index
+    assert Pt.calib_choice([[(1.0, 1.0), (2.0, 0.0)]], [4], [8, 2], 0.0) == (0, 1)  # smaller window value
+
+
 def test_linear_splitk_items_cover_rows():
     """oracle.partition.linear_splitk_items: every row of each tier is owned by exactly `splits`
     CTAs of that tier, in blocks of `block` rows (the last short), host tier first."""
