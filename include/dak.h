@@ -403,6 +403,20 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
 /* Enqueue the split GEMV / skinny GEMM. */
 dak_status dak_linear(const dak_linear_args* args, dak_stream_t stream);
 
+/* A chain of split GEMVs in ONE persistent launch (one CTA per SM): each CTA walks the ops in
+ * order with the row partition, arithmetic and epilogue of dak_linear's mma.sync path (outputs
+ * bitwise equal to launching each op alone with cfg.force_path = 2 and the same kc / n_cta_host),
+ * while its producer streams the next ops' weight stages into the same SMEM ring -- no per-op
+ * drain and restart. An op whose x / residual / y overlaps an earlier op's buffers (x of op i = y of
+ * op i-1 in a decode chain) reads x only after every CTA finished op i-1 (per-op counters in
+ * `workspace`). Limits: 1 <= n_ops <= 16; every op has the same N (1..16) and kc; plain GEMV ops (no
+ * ln_w / x_swiglu / stats_out / cluster; bias, ReLU, residual allowed); ops[0].cfg.pdl applies to
+ * the launch; each op's n_cta_host / window / congestion_control / host_inflight_kb apply to it.
+ * workspace: device, >= 4 * n_ops bytes, 16-byte aligned, ZERO-FILLED before the first call (each
+ * call leaves it zeroed). Errors: DAK_EINVAL, DAK_EUNSUPPORTED, DAK_ECUDA. */
+dak_status dak_linear_chain(const dak_linear_args* ops, int32_t n_ops, void* workspace, size_t workspace_bytes,
+                            dak_stream_t stream);
+
 /* =============================================================================================
  * 4. Split paged GQA decode attention  (P:L631 SplitK_FlashAttn; P:L386 decode attention)
  *    o[b, h] = softmax(scale * K_b q[b,h]) V_b over the tokens [0, seq_len[b]) of request b,

@@ -41,6 +41,7 @@ SOURCES = [
     ("tp.cu", []),
     ("nvls.cu", ["-I", NCCL_INC]),
     ("calib.cu", []),
+    ("chain.cu", []),
 ]
 
 

@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
         if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
       }
-      grid_dep_wait();  // x is produced by the previous kernel
+      if (!(p.exp_flags & 16)) grid_dep_wait();  // x is produced by the previous kernel (EXPERIMENT 16: independent)
       tstamp(p.trace, 1);
       for (int i = 0; i < pro; ++i) load_x(i, i);
       int s = pro == slots ? 0 : pro;
@@ -679,7 +679,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   }
 
   // ================================ epilogue: bias, activation, residual, bf16 RNE store
-  grid_dep_wait();  // residual / y may belong to the previous kernel
+  if (!(p.exp_flags & 16)) grid_dep_wait();  // residual / y may belong to the previous kernel
   const int RN = PATH == 1 ? NN : N;
   // bias / residual of this thread's first two items are fetched before the reduction barrier
   float pre_b[2] = {0.f, 0.f}, pre_r[2] = {0.f, 0.f};

@@ -409,6 +409,16 @@ def linear(args: dak_linear_args, stream=None):
     _check(lib.dak_linear(C.byref(args), _stream(stream)))
 
 
+_sig("dak_linear_chain", C.c_int32, [C.POINTER(dak_linear_args), C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p])
+EXPORTED += ["dak_linear_chain"]
+
+
+def linear_chain(ops: list, workspace, workspace_bytes: int, stream=None):
+    """dak_linear_chain: the ops (dak_linear_args) in one persistent launch; workspace zero-filled."""
+    arr = (dak_linear_args * len(ops))(*ops)
+    _check(lib.dak_linear_chain(arr, len(ops), _ptr(workspace), int(workspace_bytes), _stream(stream)))
+
+
 def linear_workspace_size(args: dak_linear_args) -> int:
     return int(lib.dak_linear_workspace_size(C.byref(args)))
 

@@ -489,3 +489,44 @@ def test_linear_split_k_shared_workspace_reuse(D, torch):
     torch.cuda.synchronize()
     for W, x, sl, xd, y, a in runs:
         assert np.array_equal(Kx.bf16_to_f64(from_dev(y)), Kx.round_to_bf16(Kx.linear(W, x)))
+
+
+@pytest.mark.parametrize("N,kc,h", [(1, 512, 32), (1, 256, 0), (8, 256, 48), (16, 128, 64)])
+def test_linear_chain_bitwise_vs_single_launches(D, torch, N, kc, h):
+    """dak_linear_chain (persistent multi-op launch): a DEPENDENT chain of C1-shaped GEMVs (x of op i
+    = y of op i-1, 4096 x 4096, host rows at the planner's share) and an independent tail of other
+    shapes with bias / ReLU / residual give outputs bitwise equal to the ops launched one by one
+    through dak_linear (mma.sync path, same kc and host CTAs); integer inputs are exact against the
+    oracle. Run twice on one workspace (it must be left zeroed)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    M = K = 4096
+    g = synth.rng(90 + N)
+    Ws = [synth.linear_inputs(M, K, N, seed=synth.seed_for(40, i), kind="int")[0] for i in range(3)]
+    x0 = synth.linear_inputs(M, K, N, seed=synth.seed_for(41, N), kind="int")[1]
+    sls = [SplitLinear(D, W, h, kc) for W in Ws]
+    bufs = [to_dev(x0)] + [torch.zeros((N, M), dtype=torch.int16, device="cuda") for _ in range(3)]
+    # tail: independent ops of other shapes (same N, kc) with bias / ReLU / residual
+    W2, x2, b2 = synth.linear_inputs(1024, 2048, N, seed=synth.seed_for(42, N), bias=True)
+    res2 = synth.normal_bf16(g, (N, 1024), 1.0)
+    sl2 = SplitLinear(D, W2, 16 if h else 0, kc)
+    x2d, b2d, r2d = to_dev(x2), to_dev(b2), to_dev(res2)
+    y2 = torch.zeros((N, 1024), dtype=torch.int16, device="cuda")
+    cfg = dict(force_path=2, n_cta_host=2, congestion_control=1, pdl=1)
+    ops = [sls[i].args(bufs[i], bufs[i + 1], N, **cfg) for i in range(3)]
+    ops.append(sl2.args(x2d, y2, N, bias=b2d, residual=r2d, act=D.ACT_RELU, **cfg))
+    ref = []
+    for a, out in zip(ops, bufs[1:] + [y2]):
+        D.linear(a)
+        torch.cuda.synchronize()
+        ref.append(from_dev(out).copy())
+    for b in bufs[1:] + [y2]:
+        b.zero_()
+    ws = torch.zeros(64, dtype=torch.uint8, device="cuda")
+    for _ in range(2):
+        D.linear_chain(ops, ws, ws.numel())
+        torch.cuda.synchronize()
+        for r_, out in zip(ref, bufs[1:] + [y2]):
+            assert np.array_equal(from_dev(out), r_)
+        assert int(ws.view(torch.int32).abs().sum()) == 0
+    y1 = Kx.round_to_bf16(Kx.linear(Ws[0], x0))
+    assert np.array_equal(Kx.bf16_to_f64(ref[0]), y1)

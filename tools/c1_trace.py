@@ -26,12 +26,15 @@ def main():
     n = int(sys.argv[2]) if len(sys.argv) > 2 else 48
     extra = dict(kv.split("=") for kv in sys.argv[3:])
     pf_mb = float(extra.pop("pf_mb", 0))  # L2 warm-up of the NEXT launch's weights (dak_linear_args.l2_prefetch)
+    tau_us = float(extra.pop("tau_us", 0))  # latency-aware planner: host link latency (dak_hw.host_latency_s)
+    h_force = int(extra.pop("h", -1))       # host rows override (-1: the planner's)
     cfg = dict(pdl=1, congestion_control=1, **{k: int(v) for k, v in extra.items()})
     M = K = 4096
     N = 1
-    plan, _ = dak.plan_ratios(dict(hbm_bps=6542.1e9, link_bps=51.5e9), [dict(n_units=M // 16, unit_bytes=16 * K * 2,
-                              total_bytes=M * K * 2, T=0.0)], 0, dak.PLAN_BALANCED)
-    h = plan[0]["host_units"] * 16
+    plan, _ = dak.plan_ratios(dict(hbm_bps=6542.1e9, link_bps=51.5e9, host_latency_s=tau_us * 1e-6),
+                              [dict(n_units=M // 16, unit_bytes=16 * K * 2, total_bytes=M * K * 2, T=0.0)], 0,
+                              dak.PLAN_BALANCED)
+    h = plan[0]["host_units"] * 16 if h_force < 0 else h_force
     copies = 24
     hbm, hosts, x, y = setup(M, K, N, h, kc, copies)
     pf = int(pf_mb * (1 << 20)) // 16 * 16
@@ -85,7 +88,7 @@ def main():
         prev_end = end.max()
         rows.append(r)
     med = {k: round(float(np.median([r[k] for r in rows[4:] if r[k] is not None])), 3) for k in rows[4]}
-    print(json.dumps(dict(kc=kc, h=h, pf_mb=pf_mb, grid=info["grid"], n_cta_host=info["n_cta_host"], stages=info["stages_hbm"],
+    print(json.dumps(dict(kc=kc, h=h, tau_us=tau_us, pf_mb=pf_mb, grid=info["grid"], n_cta_host=info["n_cta_host"], stages=info["stages_hbm"],
                           smem=info["smem_bytes"], path=info["path"], us_per_launch_events=round(float(np.median(ts)), 3),
                           gbs=round(M * K * 2 / (np.median(ts) * 1e-6) / 1e9, 1), medians_us=med)))
     for i, h_ in enumerate(hosts):
