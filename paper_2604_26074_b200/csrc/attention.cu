@@ -682,8 +682,24 @@ __global__ void __launch_bounds__(64) rope_append_kernel(__nv_bfloat16* qkv, lon
   if (part) {
     const long long cols = (long long)H3 * kD, split = (long long)B * cols;
     const float* pr = part + (long long)b * cols + (long long)hh * kD;
-    float a1 = pr[i], a2 = pr[i + kD / 2];
-    for (int sp = 1; sp < S; ++sp) {
+    // all S partials are loaded before the (fixed-order) sum: one L2 round trip, not S
+    float v1[16], v2[16];
+#pragma unroll
+    for (int sp = 0; sp < 16; ++sp) {
+      if (sp < S) {
+        v1[sp] = __ldcg(pr + sp * split + i);
+        v2[sp] = __ldcg(pr + sp * split + i + kD / 2);
+      }
+    }
+    float a1 = v1[0], a2 = v2[0];
+#pragma unroll
+    for (int sp = 1; sp < 16; ++sp) {
+      if (sp < S) {
+        a1 += v1[sp];
+        a2 += v2[sp];
+      }
+    }
+    for (int sp = 16; sp < S; ++sp) {  // (more than 16 splits: the rest one by one, same order)
       a1 += pr[sp * split + i];
       a2 += pr[sp * split + i + kD / 2];
     }
