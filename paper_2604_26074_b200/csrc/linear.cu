@@ -22,7 +22,6 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "common.h"
 
@@ -86,7 +85,6 @@ struct __align__(64) Params {
   int ln_rms;       // 1: RMSNorm (no mean subtraction, no bias)
   float* stats_out;  // epilogue row statistics (count, mean, M2) of this CTA's outputs (nullable)
   unsigned long long* trace;  // dak_trace_enable slot (nullable)
-  int exp_flags;    // EXPERIMENT (DAK_EXP_NOMMA): 1 = swapped kernel skips the MMAs (memory pipeline only)
 };
 
 // Row range of CTA j of n in a tier of R rows, in units of g rows (sizes differ by <= one unit).
@@ -364,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
         bulk_g2s(smem + p.off_ln, p.ln_w, kb, lnbar);
         if (p.ln_b) bulk_g2s(smem + p.off_ln + kb, p.ln_b, kb, lnbar);
       }
-      if (!(p.exp_flags & 16)) grid_dep_wait();  // x is produced by the previous kernel (EXPERIMENT 16: independent)
+      grid_dep_wait();  // x is produced by the previous kernel
       tstamp(p.trace, 1);
       for (int i = 0; i < pro; ++i) load_x(i, i);
       int s = pro == slots ? 0 : pro;
@@ -679,7 +677,7 @@ __global__ void __launch_bounds__(kThreads, 1) split_linear_kernel(const __grid_
   }
 
   // ================================ epilogue: bias, activation, residual, bf16 RNE store
-  if (!(p.exp_flags & 16)) grid_dep_wait();  // residual / y may belong to the previous kernel
+  grid_dep_wait();  // residual / y may belong to the previous kernel
   const int RN = PATH == 1 ? NN : N;
   // bias / residual of this thread's first two items are fetched before the reduction barrier
   float pre_b[2] = {0.f, 0.f}, pre_r[2] = {0.f, 0.f};
@@ -1238,9 +1236,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
     for (int i = 0; i < nchunks; ++i) {
       mbar_wait(&full[s], ph);
       tc_fence_after();
-      if (leader && (p.exp_flags & 1)) {
-        mbar_arrive(&empty[s]);
-      } else if (leader) {
+      if (leader) {
         const uint32_t ws = wr + (uint32_t)s * wstage, xs = xr + (uint32_t)s * p.x_stage_bytes;
 #pragma unroll
         for (int k = 0; k < 4; ++k)
@@ -1267,7 +1263,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
   }
   __syncthreads();  // every MMA has completed, so every ring stage has landed and been read: the ring is free
   tc_fence_after();
-  grid_dep_wait();  // partials / y / split-K counters may still be in use by the previous kernel
+  grid_dep_wait();  // the partial buffer may still be read by the previous kernel
   const int RN = (R + 15) & ~15;
   const int pitch = RN + 4;  // floats; +16 B per row: 2-way bank conflicts at most on the tile stores
   float* tile = reinterpret_cast<float*>(wring);
@@ -1295,7 +1291,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_swap_kernel(const __grid_con
   tc_fence_before();
   __syncthreads();
   const int R4 = R >> 2;  // R % 4 == 0 (M % 4 == 0, h % 8 == 0, kblock % 8 == 0)
-  if (!(p.exp_flags & 2)) {
+  {
     float* dst = p.part + (size_t)ks * N * p.M + row0;
     for (int i = threadIdx.x; i < N * R4; i += kThreads) {
       const int nn = i / R4, m4 = i - nn * R4;
@@ -1594,13 +1590,6 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
       bks = ceil_div(C, S);
       S = ceil_div(C, bks);
     }
-    if (getenv("DAK_EXP_KBLOCK")) {  // EXPERIMENT: item rows and split count override
-      kblock = atoi(getenv("DAK_EXP_KBLOCK"));
-      S = std::min<long long>(std::min<long long>(16, C), nsm / ceil_div(M, kblock));
-      if (getenv("DAK_EXP_S")) S = atoi(getenv("DAK_EXP_S"));
-      bks = ceil_div(C, S);
-      S = ceil_div(C, bks);
-    }
     if (S > 1 && ceil_div(M, nsm) < 128) {  // from M and the SM count only (never h: r-invariance)
       ksplit = (int)S;
       k64_split = (int)bks;
@@ -1713,7 +1702,6 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   }
   if (a->stats_out && !aligned16(a->stats_out)) return fail(DAK_EINVAL, "dak_linear: stats_out must be 16-byte aligned");
   p.stats_out = a->stats_out;
-  p.exp_flags = getenv("DAK_EXP_FLAGS") ? atoi(getenv("DAK_EXP_FLAGS")) : 0;  // EXPERIMENT: 1 no MMA, 2 no epilogue, 4 no reduce
   const int W2 = (path == 1 && kc / 8 > 32) ? kc / 8 / 32 : 1;
   // MMA path: one partial slot per k-warp when they fit in 48 KB (one barrier), else serial rounds
   p.red_slots = (path == 2 && wk > 1 && (long long)wk * rmax * N * 4 <= 48 * 1024) ? wk : 1;
@@ -2095,7 +2083,7 @@ dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool d
   if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
   const int S = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;
   if (ksplit_out) *ksplit_out = S;
-  if (S > 1 && !defer_reduce && !(pl.p.exp_flags & 4)) {
+  if (S > 1 && !defer_reduce) {
     const int vec = args->M % 4 == 0 && pl.p.ldy % 4 == 0 && ((uintptr_t)pl.p.y & 7) == 0 &&
                     ((uintptr_t)pl.p.residual & 7) == 0 && ((uintptr_t)pl.p.bias & 7) == 0;
     const long long per_row = vec ? args->M / 4 : args->M;
