@@ -13,9 +13,10 @@ done
 for r in 0.05 0.1 0.2 0.4; do
   python bench.py --batch 8 --ratio $r --steps 3 --warmup 3 --no-cpu-baseline >> $OUT/c2_sweep.jsonl 2>> $OUT/c2_sweep.err
 done
-python - <<'PY'
+python - "$R" <<'PY'
 import json
-for l in open("gpurun_out/r02/c2_sweep.jsonl"):
+import sys
+for l in open("gpurun_out/%s/c2_sweep.jsonl" % sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/r02/c2_sweep.jsonl"):
     d = json.loads(l)
     c, rf = d["config"], d["roofline"]
     print(c["batch"], c["plan"], "r=%.4f" % c["host_ratio"], "%.3f ms" % d["ms_per_step"], "%.0f GB/s" % d["value"],
