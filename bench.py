@@ -459,7 +459,10 @@ def main():
     lin_bytes = sum(op.M * op.K * 2 + eng.B * (op.K + op.M) * 2 for op in ops)  # algorithmic, per step
     lin_time = prof["linear_s"]
     lin_achieved = lin_bytes / lin_time / 1e9
-    peak = hbm_gbs + link_gbs
+    # peak: the split roofline at the linears' own host ratio, EB(r) = 1 / max((1 - r)/B_g, r/B_l)
+    # (= B_g + B_l at r*, B_l / r for a capacity-forced, link-bound plan)
+    r_lin = sum(op.h * op.K * 2 for op in ops) / max(1, sum(op.M * op.K * 2 for op in ops))
+    peak = 1.0 / max((1.0 - r_lin) / hbm_gbs, r_lin / link_gbs) if r_lin > 0 else hbm_gbs
     # traffic: DRAM read+write bytes per dak_linear launch of THIS workload from the committed ncu
     # capture (profiles/r*/linear_traffic_<workload>.json, tools/summarize_profiles.py)
     wl_name = wl["workload"] if llama else "opt-30b-decode-b%d-ctx%d" % (eng.B, a.context)
@@ -476,9 +479,10 @@ def main():
                     kernel="dak_linear (split GEMV / skinny GEMM), timed inside the captured decode step: per-launch "
                            "timeline increments from the library's globaltimer trace, summed over the step's %d "
                            "linear launches" % len(ops),
-                    peak_source="%s HBM copy %.1f GB/s (MEASURED_PEAKS.json hbm_gbs) + measured host link %.1f GB/s"
-                                % (peak_src, hbm_gbs, link_gbs),
-                    step_frac=round(value / world / peak, 4),
+                    peak_source="EB(r) = 1/max((1-r)/B_g, r/B_l) at the linears' host ratio r = %.5f: B_g = %s HBM copy "
+                                "%.1f GB/s (MEASURED_PEAKS.json hbm_gbs), B_l = measured host link %.1f GB/s"
+                                % (r_lin, peak_src, hbm_gbs, link_gbs),
+                    frac_of_copy_plus_link=round(lin_achieved / (hbm_gbs + link_gbs), 4),
                     # read-only streams exceed the copy figure: the calibrated bulk-read ring peak
                     # (profiles/r01/calib_loadpath.jsonl, 148 SMs x 4 x 32 KB) as a second denominator
                     read_peak=round(READ_PEAK_GBS + link_gbs, 1),

@@ -33,8 +33,8 @@ def family(name):
     return re.sub(r"\(.*", "", name).replace("void ", "").split("::")[-1]
 
 
-def main(rnd="r02", csv_name="launches_opt.csv", workload="opt-30b-decode-b8-ctx64"):
-    out_dir = os.path.join(ROOT, "profiles", rnd)
+def main(rnd="r02", csv_name="launches_opt.csv", workload="opt-30b-decode-b8-ctx64", out_rnd=None):
+    out_dir = os.path.join(ROOT, "profiles", out_rnd or rnd)
     os.makedirs(out_dir, exist_ok=True)
     src = os.path.join(ROOT, "gpurun_out", rnd, csv_name)
     per = launch_table(src)
