@@ -23,15 +23,15 @@ def main():
     tau_us = float(extra.pop("tau_us", 0))
     h_force = int(extra.pop("h", -1))
     indep = int(extra.pop("indep", 0))  # 1: independent ops (one x, a y per op): steady-state operator throughput
+    M = K = int(extra.pop("M", 4096))
+    N = int(extra.pop("N", 1))
     cfg = dict(pdl=1, congestion_control=1, force_path=2, **{k: int(v) for k, v in extra.items()})
-    M = K = 4096
-    N = 1
     Bg, Bl = 6542.1e9, 51.5e9
     plan, _ = dak.plan_ratios(dict(hbm_bps=Bg, link_bps=Bl, host_latency_s=tau_us * 1e-6),
                               [dict(n_units=M // 16, unit_bytes=16 * K * 2, total_bytes=M * K * 2, T=0.0)], 0,
                               dak.PLAN_BALANCED)
     h = plan[0]["host_units"] * 16 if h_force < 0 else h_force
-    hbm = [torch.randn((M - h) * K, device="cuda").to(torch.bfloat16) for _ in range(L)]
+    hbm = [torch.empty((M - h) * K, device="cuda", dtype=torch.bfloat16).normal_() for _ in range(L)]
     hosts = [dak.host_alloc(max(h * K * 2, 16)) for _ in range(L)]
     xs = [torch.randn(N, K, device="cuda").to(torch.bfloat16) * 0.01, torch.zeros(N, K, device="cuda", dtype=torch.bfloat16)]
     ys = [torch.zeros(N, M, device="cuda", dtype=torch.bfloat16) for _ in range(L)]
