@@ -33,7 +33,7 @@ def run_attn(D, torch, Ls, Hkv, Hq, page, chunk_pages, frac, seed, paper_mode=Fa
     a = D.attention_args(qd, out, kv.kg, kv.vg, kv.kh.dp, kv.vh.dp, kv.bt, sl, B, Hq, Hkv, d, page, bt.shape[1],
                          chunk_pages, cfg=cfg)
     ws_bytes = D.attention_workspace_size(a)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device="cuda")
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
     D.attention(a)
     torch.cuda.synchronize()
@@ -122,7 +122,7 @@ def test_kv_append(D, torch):
     qd = to_dev(q)  # keep a reference: the workspace allocated below must not reuse q's memory
     a = D.attention_args(qd, out, kv.kg, kv.vg, kv.kh.dp, kv.vh.dp, kv.bt, sl, B, Hq, Hkv, d, page,
                          bt.shape[1], 1)
-    ws = torch.empty(D.attention_workspace_size(a), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(D.attention_workspace_size(a), dtype=torch.uint8, device="cuda")
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     D.attention(a)
     torch.cuda.synchronize()
@@ -159,7 +159,7 @@ def test_attention_fused_kv_append(D, torch, Ls, cp):
     a = D.attention_args(qd, out, kv.kg, kv.vg, kv.kh.dp, kv.vh.dp, kv.bt, sl, B, Hq, Hkv, d, page, bt.shape[1], cp,
                          k_new=qkvd.data_ptr() + Hq * d * 2, v_new=qkvd.data_ptr() + (Hq + Hkv) * d * 2,
                          kv_new_stride=(Hq + 2 * Hkv) * d)
-    ws = torch.empty(max(D.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(D.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     D.attention(a)
     torch.cuda.synchronize()

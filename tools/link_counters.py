@@ -69,7 +69,7 @@ def attention_case(name, B, L, Hq, Hkv, frac, page=64, cp=16):
     btd = torch.from_numpy(bt).cuda()
     a = dak.attention_args(q, out, kg, vg, kh[1], vh[1], btd, sl, B, Hq, Hkv, d, page, pages, cp,
                            cfg=dict(pdl=1, congestion_control=1, n_cta_host=0))
-    ws = torch.empty(max(dak.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(dak.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
     torch.cuda.synchronize()
     dak.attention(a)

@@ -43,7 +43,7 @@ host_units = B * (hp // cp) * Hkv
 nh = nh_arg or 0  # 0: auto (chosen in-kernel from the block table)
 a = dak.attention_args(q, out, kg, vg, kh[1], vh[1], btd, sl, B, Hq, Hkv, d, page, pages, cp,
                        cfg=dict(pdl=1, congestion_control=1, n_cta_host=nh))
-ws = torch.empty(max(dak.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
+ws = torch.zeros(max(dak.attention_workspace_size(a), 16), dtype=torch.uint8, device="cuda")
 a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
 for _ in range(3):
     dak.attention(a)

@@ -100,7 +100,7 @@ def c4():
                 nh = 0  # auto: the library picks the host CTAs from the block table
                 a = dak.attention_args(q, out, kg, vg, kh[1], vh[1], btd, sl, B, Hq, Hkv, d, page, pages, cp,
                                        cfg=dict(pdl=1, congestion_control=cc, n_cta_host=nh))
-                ws = torch.empty(dak.attention_workspace_size(a), dtype=torch.uint8, device="cuda")
+                ws = torch.zeros(dak.attention_workspace_size(a), dtype=torch.uint8, device="cuda")
                 a.workspace, a.workspace_bytes = ws.data_ptr(), ws.numel()
                 s = torch.cuda.Stream()
                 with torch.cuda.stream(s):
