@@ -22,20 +22,17 @@
 #include <vector>
 
 #include "common.h"
+#include "ptx.cuh"
 
 namespace dak {
 namespace cal {
+
+using namespace ptx;
 
 constexpr int kHbmStages = 6;
 constexpr int kMaxSlots = 16;
 constexpr int kSmem = 227 * 1024;
 
-__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
   uint32_t done;
   asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"

@@ -1,5 +1,5 @@
 // Inline-PTX helpers for sm_100a (mbarrier, bulk copy, ldmatrix/movmatrix, mma.sync, PDL,
-// gpu-scope acquire/release). Header-only; used by the persistent decode-step kernel.
+// gpu-scope acquire/release). Header-only; shared by the kernels of every translation unit.
 #pragma once
 #include <cuda_bf16.h>
 #include <stdint.h>
@@ -109,6 +109,26 @@ __device__ __forceinline__ uint32_t kc_swz(long long r_tier, int sl) {
 // DAK-PG: byte offset of 16-byte chunk j of token row t in a page with d = 128 (row pitch 256 B)
 __device__ __forceinline__ uint32_t pg_off(int t, int j) {
   return (uint32_t)(t * 256 + ((((j >> 3) << 3) | ((j & 7) ^ (t & 7))) << 4));
+}
+
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void mma_f16(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                        uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// bf16x2 -> f16x2: exact for |v| in [2^-14, 65504] (bf16's 8-bit significand fits fp16's 11 bits)
+__device__ __forceinline__ uint32_t bf2_to_h2(uint32_t r) {
+  return pack_f16(__uint_as_float(r << 16), __uint_as_float(r & 0xffff0000u));
 }
 
 }  // namespace ptx
