@@ -194,8 +194,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         op_rows(o, cta, &h_, &rb, &re, &Rt);
         if (re <= rb) continue;
         if (oi > 0 && o.dep) {
-          while (ld_acquire(p.done + (oi - 1)) < grid) {  // acquire polls: one L2 round trip per check
-          }
+          // acquire polls (one L2 round trip per check); bounded: a CTA that never arrives is a bug
+          // and traps (a kernel error) instead of hanging the device
+          for (long long it = 0; ld_acquire(p.done + (oi - 1)) < grid; ++it)
+            if (it > (1LL << 26)) asm volatile("trap;");
           fence_proxy_async();  // other CTAs' generic y stores -> this CTA's async-proxy x loads
         }
         ostamp(p.trace, oi, 1);
@@ -234,7 +236,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
         // every CTA passed every wait once all have finished the last op: zero the counters for
         // the next call (CTA 0 waits for the others here, at the very end of the chain)
         const int last = p.n_ops - 1;
-        while (ld_acquire(p.done + last) < grid) __nanosleep(64);
+        for (long long it = 0; ld_acquire(p.done + last) < grid; ++it) {
+          __nanosleep(64);
+          if (it > (1LL << 24)) asm volatile("trap;");
+        }
         for (int i = 0; i < p.n_ops; ++i) p.done[i] = 0;
         __threadfence();
       }
