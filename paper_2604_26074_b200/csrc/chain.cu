@@ -83,13 +83,6 @@ __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
                : "memory");
   return done != 0;
 }
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* tmap, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-          "r"(su32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
 __device__ __forceinline__ void bulk_g2s_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
@@ -205,13 +198,13 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(const __grid_constan
           const int b = xi & 1;
           if (xi >= 2) mbar_wait(&xempty[b], (uint32_t)(((xi >> 1) - 1) & 1));
           mbar_expect_tx(&xfull[b], (uint32_t)(p.N * o.K * 2));
-          tma_3d(xring + (size_t)b * p.xres_bytes, &o.xmap, 0, 0, 0, &xfull[b]);
+          tma_3d(xring + (size_t)b * p.xres_bytes, reinterpret_cast<uint64_t>(&o.xmap), 0, 0, 0, &xfull[b]);
           ++xi;
         } else {
           for (int c = 0; c < o.nchunks; ++c, ++g) {
             while (*w_issued <= g) __nanosleep(20);
             const int s = (int)(g % stages);
-            tma_3d(xring + (size_t)s * p.x_stage_bytes, &o.xmap, 0, 0, c * (kc >> 6), &full[s]);
+            tma_3d(xring + (size_t)s * p.x_stage_bytes, reinterpret_cast<uint64_t>(&o.xmap), 0, 0, c * (kc >> 6), &full[s]);
           }
         }
       }

@@ -364,6 +364,370 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   }
 }
 
+
+// ================================================================================================
+// tcgen05 form (5th-gen tensor cores, TMEM accumulators). Same work split, producer, host staging
+// and newest-keys-first order as prefill_attention_kernel; the contractions run as
+//   S[128 rows x 64 keys]  = Q[128 x 128 d] . K_tile^T     (8 x M128 N64 K16, TMEM columns 64 (j&1))
+//   O[128 rows x 128 d]   += P[128 x 64 keys] . V_tile     (fp16 operands: 4 x M128 N128 K16)
+// with every operand a canonical K-major SWIZZLE_128B tile: Q written once by all threads; the K
+// tile de-interleaved from DAK-PG (row = [d 0..63 | d 64..127], chunks already swizzled by row & 7)
+// into two 64-column blocks, V transposed to V^T [128 d][64 keys] by four transform warps; P written
+// by the softmax warps. Softmax: one thread per query row (TMEM lane = row), exp2 domain, LAZY
+// rescaling (the row's reference max moves only when the tile max exceeds it by more than 8, then
+// O is rescaled in TMEM; P <= 2^8), P in fp16 and V^T converted bf16 -> fp16 by the transform
+// (reading R20, as the mma.sync form), l summed from the fp32 P.
+// Warps: 0 producer, 1 MMA issuer (one elected lane), 2-5 transform, 6-9 softmax + epilogue.
+constexpr int kUThreads = 10 * 32;
+constexpr int kUOffQ = 1024;                       // Q: 2 blocks x 16 KB
+constexpr int kUOffRaw = kUOffQ + 32768;           // raw ring: 2 stages x (K 16 KB | V 16 KB)
+constexpr int kUOffKc = kUOffRaw + 2 * 2 * kTileBytes;  // Kc: 2 buffers x 2 blocks x 8 KB
+constexpr int kUOffVt = kUOffKc + 2 * kTileBytes;  // V^T: 2 buffers x 16 KB ([128 d][128 B])
+constexpr int kUOffP = kUOffVt + 2 * kTileBytes;   // P (fp16): 2 buffers x 16 KB
+constexpr int kUSmem = kUOffP + 2 * 16384 + 1024;  // + alignment slack
+
+__global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* full = bars;          // [2] raw tile landed (producer)
+  uint64_t* empty = bars + 2;     // [2] raw tile transformed (4 transform warps)
+  uint64_t* kv_full = bars + 4;   // [2] Kc / V^T of the buffer ready (4 transform warps)
+  uint64_t* s_full = bars + 6;    // [2] S of the buffer computed (MMA commit)
+  uint64_t* p_full = bars + 8;    // [2] P of the buffer written, O rescaled (4 softmax warps)
+  uint64_t* pv_done = bars + 10;  // [2] P V of the buffer's tile complete (MMA commit)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 256);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int page_bytes = p.page * kD * 2;
+  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer: as prefill_attention_kernel
+    unsigned char* ring = smem + kUOffRaw;
+    if (threadIdx.x == 0) {
+      for (int s2 = 0; s2 < 2; ++s2) mbar_init(&full[s2], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const int n_items_max = p.max_pages * p.B * p.Hkv;
+    int k = 0, mine = 0;
+    auto next_mine = [&](int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {
+      for (; k < n_items_max; ++k) {
+        const int pg = p.max_pages - 1 - k / (p.B * p.Hkv);
+        const int b2 = (k / p.Hkv) % p.B, g2 = k % p.Hkv;
+        const int filled = (p.seq_lens[b2] + p.page - 1) / p.page;
+        if (pg >= filled) continue;
+        const uint32_t e = (uint32_t)p.block_table[(long long)b2 * p.max_pages + pg];
+        if (!(e & kHostBit)) continue;
+        if ((mine++ % p.n_stream) == (int)blockIdx.x) {
+          b_ = b2; g_ = g2; pg_ = pg; e_ = e;
+          ++k;
+          return true;
+        }
+      }
+      return false;
+    };
+    const int SS = (2 * 2 * kTileBytes) / (2 * page_bytes) > 0 ? (2 * 2 * kTileBytes) / (2 * page_bytes) : 1;
+    int qb[2], qg[2], qp[2];
+    int issued = 0, done = 0;
+    auto issue = [&](int slot) -> bool {
+      int b_, g_, pg_;
+      uint32_t e_;
+      if (!next_mine(b_, g_, pg_, e_)) return false;
+      const long long off = ((long long)(e_ & ~kHostBit) * p.Hkv + g_) * page_bytes;
+      unsigned char* dst = ring + (size_t)slot * 2 * page_bytes;
+      mbar_expect_tx(&full[slot], 2u * page_bytes);
+      bulk_g2s(dst, p.k_host + off, page_bytes, &full[slot]);
+      bulk_g2s(dst + page_bytes, p.v_host + off, page_bytes, &full[slot]);
+      qb[slot] = b_; qg[slot] = g_; qp[slot] = pg_;
+      ++issued;
+      return true;
+    };
+    for (int sl = 0; sl < SS && sl < 2 && issue(sl); ++sl) {}
+    const int SSn = SS < 2 ? SS : 2;
+    while (done < issued) {
+      const int sl = done % SSn;
+      mbar_wait(&full[sl], (uint32_t)((done / SSn) & 1));
+      const long long so = (((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl]) * page_bytes;
+      unsigned char* src = ring + (size_t)sl * 2 * page_bytes;
+      bulk_s2g(p.k_stage + so, src, page_bytes);
+      bulk_s2g(p.v_stage + so, src + page_bytes, page_bytes);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      int* f = p.flags + ((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl];
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+      ++done;
+      issue(sl);
+    }
+    return;
+  }
+  const int cta = (int)blockIdx.x - p.n_stream;
+  const int bg = cta / p.blocks_per_bg, blk = cta % p.blocks_per_bg;
+  const int b = bg / p.Hkv, g = bg % p.Hkv;
+  const int L = p.seq_lens[b];
+  const int rows = p.T * p.G;
+  const int r0 = blk * kRows;
+  const int r_last = min(rows, r0 + kRows) - 1;
+  const int kmax = L - p.T + r_last / p.G + 1;
+  const int nt = (kmax + kTile - 1) / kTile;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 12; ++i) {
+      const int which = i >> 1;  // full, empty, kv_full, s_full, p_full, pv_done
+      mbar_init(&bars[i], which == 1 || which == 2 || which == 4 ? 4u : 1u);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    tstamp(p.trace, 0);
+  }
+  if (warp == 1) {  // TMEM: S0 [0, 64), S1 [64, 128), O [128, 256)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  // ---- Q (all threads): row r = (token r / G, head r % G) of the block, two 64-column blocks
+  for (int idx = threadIdx.x; idx < kRows * 16; idx += kUThreads) {
+    const int r = idx >> 4, j16 = idx & 15;
+    const int gr = r0 + r;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (gr < rows) {
+      const int i = gr / p.G, hh = gr % p.G;
+      v = reinterpret_cast<const uint4*>(p.q + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD)[j16];
+    }
+    const int blkq = j16 >> 3, c = j16 & 7;
+    *reinterpret_cast<uint4*>(smem + kUOffQ + blkq * 16384 + r * 128 + ((c ^ (r & 7)) << 4)) = v;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {  // ---- producer: raw K / V tiles (DAK-PG), newest keys first
+    if (lane == 0) {
+      const int* bt = p.block_table + (long long)b * p.max_pages;
+      for (int t = 0; t < nt; ++t) {
+        const int s2 = t & 1;
+        if (t >= 2) mbar_wait(&empty[s2], (uint32_t)(((t >> 1) - 1) & 1));
+        const int key0 = (nt - 1 - t) * kTile;
+        const int pg = key0 / p.page;
+        const uint32_t e = (uint32_t)bt[pg];
+        const bool host = (e & kHostBit) != 0;
+        const long long in_page = (long long)(key0 % p.page) * kD * 2;
+        const char* ksrc = (host ? p.k_host : p.k_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
+        const char* vsrc = (host ? p.v_host : p.v_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
+        if (host && p.n_stream > 0) {
+          const long long so = (((long long)b * p.Hkv + g) * p.max_pages + pg) * page_bytes + in_page;
+          const int* f = p.flags + ((long long)b * p.Hkv + g) * p.max_pages + pg;
+          int ready = 0;
+          for (int it = 0; it < (1 << 22) && !ready; ++it) {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
+            if (!ready) __nanosleep(64);
+          }
+          if (ready) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            ksrc = p.k_stage + so;
+            vsrc = p.v_stage + so;
+          }
+        }
+        unsigned char* dst = smem + kUOffRaw + (size_t)s2 * 2 * kTileBytes;
+        mbar_expect_tx(&full[s2], 2u * kTileBytes);
+        bulk_g2s(dst, ksrc, kTileBytes, &full[s2]);
+        bulk_g2s(dst + kTileBytes, vsrc, kTileBytes, &full[s2]);
+      }
+    }
+  } else if (warp == 1) {  // ---- MMA issuer
+    const uint32_t id_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t id_o = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // f16 x f16 -> f32
+    const uint32_t q_u = su32(smem + kUOffQ), kc_u = su32(smem + kUOffKc), vt_u = su32(smem + kUOffVt),
+                   p_u = su32(smem + kUOffP);
+    uint32_t leader;
+    asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+    auto issue_s = [&](int t) {  // S[t & 1] = Q . Kc[t & 1]^T
+      const int bb = t & 1;
+      mbar_wait(&kv_full[bb], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      if (leader) {
+#pragma unroll
+        for (int ks = 0; ks < kD / 16; ++ks)
+          umma_bf16(tmem + (uint32_t)(bb * 64), umma_desc_sw128(q_u + (ks >> 2) * 16384 + (ks & 3) * 32),
+                    umma_desc_sw128(kc_u + bb * kTileBytes + (ks >> 2) * 8192 + (ks & 3) * 32), id_s, ks != 0);
+        umma_commit(&s_full[bb]);
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    if (nt > 1) issue_s(1);
+    for (int t = 0; t < nt; ++t) {
+      const int bb = t & 1;
+      mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      if (leader) {  // O += P V (fp16 operands)
+#pragma unroll
+        for (int ks = 0; ks < kTile / 16; ++ks)
+          umma_bf16(tmem + 128u, umma_desc_sw128(p_u + bb * 16384 + ks * 32),
+                    umma_desc_sw128(vt_u + bb * kTileBytes + ks * 32), id_o, (t | ks) != 0);
+        umma_commit(&pv_done[bb]);  // frees Kc / V^T / P of the buffer; O of tile t is complete
+      }
+      __syncwarp();
+      if (t + 2 < nt) issue_s(t + 2);
+    }
+  } else if (warp >= 2 && warp <= 5) {  // ---- transform: raw DAK-PG tile -> Kc (2 blocks), V^T
+    const int tt = threadIdx.x - 64;  // 0..127
+    for (int t = 0; t < nt; ++t) {
+      const int bb = t & 1;
+      mbar_wait(&full[bb], (uint32_t)((t >> 1) & 1));
+      if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));  // buffer bb read by tile t - 2
+      const unsigned char* rk = smem + kUOffRaw + (size_t)bb * 2 * kTileBytes;
+      const unsigned char* rv = rk + kTileBytes;
+      unsigned char* kc = smem + kUOffKc + bb * kTileBytes;
+      unsigned char* vt = smem + kUOffVt + bb * kTileBytes;
+      // K: 16 lanes per key row, stored chunk j16 -> block j16 >> 3 (the swizzle is the same)
+      for (int idx = tt; idx < kTile * 16; idx += 128) {
+        const int key = idx >> 4, j16 = idx & 15;
+        const uint4 u = *reinterpret_cast<const uint4*>(rk + key * 256 + j16 * 16);
+        *reinterpret_cast<uint4*>(kc + (j16 >> 3) * 8192 + key * 128 + (j16 & 7) * 16) = u;
+      }
+      // V^T: lane = key (32 consecutive keys per warp: the swizzled 16-byte reads of one logical d
+      // chunk, and the 2-byte writes of one d row, spread over all banks), logical d chunks dc of
+      // this warp's half
+      {
+        const int tw = warp - 2;  // 0..3
+        const int key = (tw & 1) * 32 + lane;
+        for (int dc = (tw >> 1) * 8; dc < (tw >> 1) * 8 + 8; ++dc) {
+          const int j16 = (dc & 8) | ((dc & 7) ^ (key & 7));  // stored position of logical chunk dc
+          const uint4 w = *reinterpret_cast<const uint4*>(rv + key * 256 + j16 * 16);
+          const uint32_t wv[4] = {bf2_to_h2(w.x), bf2_to_h2(w.y), bf2_to_h2(w.z), bf2_to_h2(w.w)};  // fp16 (R20)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int d = dc * 8 + e;
+            const unsigned short h = (unsigned short)((wv[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
+            *reinterpret_cast<unsigned short*>(vt + d * 128 + (((key >> 3) ^ (d & 7)) << 4) + (key & 7) * 2) = h;
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&empty[bb]);
+        mbar_arrive(&kv_full[bb]);
+      }
+    }
+  } else {  // ---- softmax warps 6..9: thread = query row (TMEM lane)
+    const int q4 = warp & 3;
+    const int r = 32 * q4 + lane;  // row of the block
+    const int gr = r0 + r;
+    const int lim = gr < rows ? L - p.T + gr / p.G + 1 : 0;  // keys [0, lim) visible
+    const int lim_w = __reduce_min_sync(0xffffffffu, (unsigned)lim);  // tiles below it need no mask
+    const uint32_t lane_base = (uint32_t)(32 * q4) << 16;
+    float m = -INFINITY, l = 0.f;
+    unsigned char* pbase = smem + kUOffP;
+    for (int t = 0; t < nt; ++t) {
+      const int bb = t & 1;
+      const int key0 = (nt - 1 - t) * kTile;
+      mbar_wait(&s_full[bb], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      float sv[kTile];
+      {
+        uint32_t v[kTile];
+#pragma unroll
+        for (int c0 = 0; c0 < kTile; c0 += 16) tmem_ld16(tmem + lane_base + (uint32_t)(bb * 64 + c0), v + c0);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < kTile; ++c) {
+          asm volatile("" : "+r"(v[c]));  // keep every use after the wait
+          sv[c] = __uint_as_float(v[c]);
+        }
+      }
+      if (key0 + kTile > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
+#pragma unroll
+        for (int c = 0; c < kTile; ++c) sv[c] = key0 + c < lim ? sv[c] : -INFINITY;
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < kTile; ++c) mx = fmaxf(mx, sv[c]);
+      mx *= p.scale_log2;  // scale > 0: max of the scaled logits
+      // lazy reference max: move it (and rescale O, l) only when the tile max exceeds it by > 8
+      const bool move = mx > m + 8.f;
+      const float m_new = move ? mx : m;
+      const float alpha = move ? exp2f(m - m_new) : 1.f;  // exp2(-inf) = 0 for a row's first keys
+      if (t > 0 && __any_sync(0xffffffffu, move && m != -INFINITY)) {
+        // O of tile t - 1 must be complete before it is rescaled in TMEM
+        mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < kD; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+          tmem_st16(tmem + lane_base + 128u + (uint32_t)c0, v);
+        }
+        tmem_wait_st();
+      }
+      l *= alpha;
+      m = m_new;
+      const float ref = m == -INFINITY ? 0.f : m;
+      // P buffer bb is free once the P V of tile t - 2 has completed
+      if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));
+      unsigned char* ph = pbase + bb * 16384;
+      float l2 = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < kTile / 8; ++c8) {
+        uint32_t hw[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = ex2_ftz(fmaf(sv[c8 * 8 + 2 * e], p.scale_log2, -ref));
+          const float p1 = ex2_ftz(fmaf(sv[c8 * 8 + 2 * e + 1], p.scale_log2, -ref));
+          hw[e] = pack_f16(p0, p1);
+          l += p0;
+          l2 += p1;
+        }
+        const int off = r * 128 + ((c8 ^ (r & 7)) << 4);
+        *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      }
+      l += l2;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[bb]);
+    }
+    // ---- epilogue: O / l -> bf16
+    mbar_wait(&pv_done[(nt - 1) & 1], (uint32_t)(((nt - 1) >> 1) & 1));
+    tc_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* dst = nullptr;
+    if (gr < rows) {
+      const int i = gr / p.G, hh = gr % p.G;
+      dst = p.out + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD;
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < kD; c0 += 16) {
+      uint32_t v[16];
+      tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v);
+      tmem_wait_ld();
+      if (dst) {
+        uint4 o0, o1;
+        o0.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
+        o0.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
+        o0.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
+        o0.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
+        o1.x = pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv);
+        o1.y = pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv);
+        o1.z = pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv);
+        o1.w = pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv);
+        reinterpret_cast<uint4*>(dst + c0)[0] = o0;
+        reinterpret_cast<uint4*>(dst + c0)[1] = o1;
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tstamp(p.trace, 3);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
 }  // namespace pf
 }  // namespace dak
 
@@ -436,12 +800,17 @@ dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stre
   if (!attr) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(pf::prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       1024 + pf::kMaxStages * 2 * pf::kTileBytes + 1024));
+    DAK_CUDA_TRY(cudaFuncSetAttribute(pf::prefill_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kUSmem));
     attr = true;
   }
+  const bool umma = args->cfg.force_path != 2;  // tcgen05 by default; force_path 2: the mma.sync form
   if (p.n_stream > 0)  // staged-page flags start lowered (a memset node under graph capture)
     DAK_CUDA_TRY(cudaMemsetAsync(p.flags, 0, (size_t)args->B * args->Hkv * args->max_pages * 4, (cudaStream_t)stream));
   p.trace = trace_slot(DAK_KIND_PREFILL, args->B, args->T, grid);
-  pf::prefill_attention_kernel<<<grid, pf::kThreads, smem, (cudaStream_t)stream>>>(p);
+  if (umma)
+    pf::prefill_umma_kernel<<<grid, pf::kUThreads, pf::kUSmem, (cudaStream_t)stream>>>(p);
+  else
+    pf::prefill_attention_kernel<<<grid, pf::kThreads, smem, (cudaStream_t)stream>>>(p);
   DAK_CUDA_TRY(cudaGetLastError());
   return DAK_OK;
 }
