@@ -15,6 +15,7 @@
 // Tiles are consumed in key order: the reduction order of a row depends on (seq_len, T) only, never
 // on the tier split (bitwise r-invariant). DAK-PG pages (include/dak.h): row t's 16-byte chunks are
 // swizzled by t & 7, so both ldmatrix forms are bank-conflict free.
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -38,6 +39,7 @@ constexpr int kTile = 64;               // keys per stage
 constexpr int kTileBytes = kTile * kD * 2;
 constexpr int kMaxStages = 6;
 constexpr uint32_t kHostBit = 0x80000000u;
+constexpr int kListBytes = kThreads * 8 + 128;  // streamer scan list + per-warp counts
 
 struct Params {
   const __nv_bfloat16* q;
@@ -60,6 +62,9 @@ struct Params {
   int* flags;  // [B][Hkv][max_pages]
   float scale_log2;
   unsigned long long* trace;
+  // tcgen05 form: K pools [0 HBM, 1 host, 2 staging], V pools [3, 4, 5] as 3-D tensors (64 elements,
+  // 2 row halves, pool rows), box (64, 1, 64), no swizzle (DAK-PG rows are swizzled already)
+  alignas(64) CUtensorMap kvmap[6];
 };
 
 __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
@@ -74,7 +79,89 @@ __device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Params p) {
+// ---- host-tier streamer CTAs (blockIdx < n_stream; an SM reads one tier): every host page
+// (b, g, page) of the batch is read ONCE over the link into the device staging pool, in the order
+// the compute CTAs consume them -- (b, g) in grid order, newest page first within each -- so the
+// first waves' pages arrive at the full link rate; each page's flag is raised with a release store.
+// The scan over (b, g, page) runs on all threads, one item per thread per round, compacted in
+// order through `list` (blockDim entries); the host items are dealt round-robin over the streamers
+// and thread 0 keeps `slots` pages (K + V, 2 * page bytes each, in `ring`) in flight.
+__device__ void stream_host_pages(const Params& p, unsigned char* ring, int slots, uint64_t* full, uint2* list) {
+  const int nth = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* wsum = reinterpret_cast<int*>(list + nth);  // [32] per-warp host-item counts
+  const int page_bytes = p.page * kD * 2;
+  if (tid == 0) {
+    for (int s = 0; s < slots; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int n_items = p.max_pages * p.B * p.Hkv;
+  int seen = 0;                    // host items before this round (all threads)
+  int issued = 0, done = 0;        // thread 0
+  int qb[4], qg[4], qp[4];         // thread 0: the item in each slot
+  auto complete = [&]() {          // thread 0: oldest slot landed -> staging pool, flag up
+    const int sl = done % slots;
+    mbar_wait(&full[sl], (uint32_t)((done / slots) & 1));
+    const long long so = (((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl]) * page_bytes;
+    const unsigned char* src = ring + (size_t)sl * 2 * page_bytes;
+    bulk_s2g(p.k_stage + so, src, page_bytes);
+    bulk_s2g(p.v_stage + so, src + page_bytes, page_bytes);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    int* f = p.flags + ((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl];
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+    ++done;
+  };
+  for (int k0 = 0; k0 < n_items; k0 += nth) {
+    const int k = k0 + tid;
+    uint32_t e = 0;
+    bool host = false;
+    if (k < n_items) {
+      const int pg = p.max_pages - 1 - k % p.max_pages;
+      const int b2 = k / p.max_pages / p.Hkv;
+      if (pg < (p.seq_lens[b2] + p.page - 1) / p.page) {
+        e = (uint32_t)p.block_table[(long long)b2 * p.max_pages + pg];
+        host = (e & kHostBit) != 0;
+      }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, host);
+    if (lane == 0) wsum[warp] = __popc(bal);
+    __syncthreads();
+    int off = 0, total = 0;
+    for (int w = 0; w < (nth >> 5); ++w) {
+      off += w < warp ? wsum[w] : 0;
+      total += wsum[w];
+    }
+    if (host) list[off + __popc(bal & ((1u << lane) - 1u))] = make_uint2((uint32_t)k, e);
+    __syncthreads();
+    if (tid == 0) {
+      for (int j = 0; j < total; ++j) {
+        if ((seen + j) % p.n_stream != (int)blockIdx.x) continue;
+        if (issued - done == slots) complete();
+        const int kk = (int)list[j].x;
+        const uint32_t ee = list[j].y;
+        const int sl = issued % slots;
+        const int bg2 = kk / p.max_pages, g2 = bg2 % p.Hkv;
+        const long long hoff = ((long long)(ee & ~kHostBit) * p.Hkv + g2) * page_bytes;
+        unsigned char* dst = ring + (size_t)sl * 2 * page_bytes;
+        mbar_expect_tx(&full[sl], 2u * page_bytes);
+        bulk_g2s(dst, p.k_host + hoff, page_bytes, &full[sl]);
+        bulk_g2s(dst + page_bytes, p.v_host + hoff, page_bytes, &full[sl]);
+        qb[sl] = bg2 / p.Hkv;
+        qg[sl] = g2;
+        qp[sl] = p.max_pages - 1 - kk % p.max_pages;
+        ++issued;
+      }
+    }
+    seen += total;
+    __syncthreads();  // list / wsum reused
+  }
+  if (tid == 0)
+    while (done < issued) complete();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
@@ -85,65 +172,9 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = p.stages;
   const int page_bytes = p.page * kD * 2;
-  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer (an SM reads one tier)
-    if (threadIdx.x == 0) {
-      for (int s = 0; s < kMaxStages; ++s) mbar_init(&full[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    // items: host pages (b, g, page), newest page first (the compute CTAs consume keys newest first);
-    // this CTA takes items n_stream apart. A slot holds one page of K and one of V.
-    const int n_items_max = p.max_pages * p.B * p.Hkv;
-    auto item = [&](int k, int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {  // k-th item of the scan
-      const int pg = p.max_pages - 1 - k / (p.B * p.Hkv);
-      const int b2 = (k / p.Hkv) % p.B, g2 = k % p.Hkv;
-      const int filled = (p.seq_lens[b2] + p.page - 1) / p.page;
-      if (pg >= filled) return false;
-      e_ = (uint32_t)p.block_table[(long long)b2 * p.max_pages + pg];
-      if (!(e_ & kHostBit)) return false;
-      b_ = b2; g_ = g2; pg_ = pg;
-      return true;
-    };
-    // my items, in scan order
-    int k = 0, mine = 0;
-    auto next_mine = [&](int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {
-      for (; k < n_items_max; ++k)
-        if (item(k, b_, g_, pg_, e_) && (mine++ % p.n_stream) == (int)blockIdx.x) { ++k; return true; }
-      return false;
-    };
-    int qb[kMaxStages], qg[kMaxStages], qp[kMaxStages];
-    int issued = 0, done = 0;
-    auto issue = [&](int slot) -> bool {
-      int b_, g_, pg_;
-      uint32_t e_;
-      if (!next_mine(b_, g_, pg_, e_)) return false;
-      const long long off = ((long long)(e_ & ~kHostBit) * p.Hkv + g_) * page_bytes;
-      unsigned char* dst = ring + (size_t)slot * 2 * kTileBytes * (p.page / kTile);
-      mbar_expect_tx(&full[slot], 2u * page_bytes);
-      bulk_g2s(dst, p.k_host + off, page_bytes, &full[slot]);
-      bulk_g2s(dst + page_bytes, p.v_host + off, page_bytes, &full[slot]);
-      qb[slot] = b_; qg[slot] = g_; qp[slot] = pg_;
-      ++issued;
-      return true;
-    };
-    const int SS = S * kTile / p.page > 0 ? S * kTile / p.page : 1;  // page slots in the ring
-    for (int sl = 0; sl < SS && issue(sl); ++sl) {}
-    while (done < issued) {
-      const int sl = done % SS;
-      mbar_wait(&full[sl], (uint32_t)((done / SS) & 1));
-      const long long so = (((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl]) * page_bytes;
-      unsigned char* src = ring + (size_t)sl * 2 * kTileBytes * (p.page / kTile);
-      bulk_s2g(p.k_stage + so, src, page_bytes);
-      bulk_s2g(p.v_stage + so, src + page_bytes, page_bytes);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      int* f = p.flags + ((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl];
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
-      ++done;
-      issue(sl);
-    }
+  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer
+    const int slots = min(4, S * kTileBytes / page_bytes);  // ring: S stages of 2 tiles
+    stream_host_pages(p, ring, slots, full, reinterpret_cast<uint2*>(ring + (size_t)S * 2 * kTileBytes));
     return;
   }
   const int cta = (int)blockIdx.x - p.n_stream;
@@ -366,98 +397,46 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const Pa
 
 
 // ================================================================================================
-// tcgen05 form (5th-gen tensor cores, TMEM accumulators). Same work split, producer, host staging
-// and newest-keys-first order as prefill_attention_kernel; the contractions run as
-//   S[128 rows x 64 keys]  = Q[128 x 128 d] . K_tile^T     (8 x M128 N64 K16, TMEM columns 64 (j&1))
-//   O[128 rows x 128 d]   += P[128 x 64 keys] . V_tile     (fp16 operands: 4 x M128 N128 K16)
-// with every operand a canonical K-major SWIZZLE_128B tile: Q written once by all threads; the K
-// tile de-interleaved from DAK-PG (row = [d 0..63 | d 64..127], chunks already swizzled by row & 7)
-// into two 64-column blocks, V transposed to V^T [128 d][64 keys] by four transform warps; P written
-// by the softmax warps. Softmax: one thread per query row (TMEM lane = row), exp2 domain, LAZY
-// rescaling (the row's reference max moves only when the tile max exceeds it by more than 8, then
-// O is rescaled in TMEM; P <= 2^8), P in fp16 and V^T converted bf16 -> fp16 by the transform
-// (reading R20, as the mma.sync form), l summed from the fp32 P.
-// Warps: 0 producer, 1 MMA issuer (one elected lane), 2-5 transform, 6-9 softmax + epilogue.
+// tcgen05 form (5th-gen tensor cores, TMEM accumulators). Same work split, host staging and
+// newest-keys-first order as prefill_attention_kernel; the contractions run as
+//   S[128 rows x 64 keys]  = Q[128 x 128 d] . K_tile^T   (8 x M128 N64 K16, TMEM columns 64 (t & 1))
+//   O[128 rows x 128 d]   += P[128 x 64 keys] . V_tile   (fp16 operands: 4 x M128 N128 K16, columns 128..255)
+// The K / V tiles come straight from the DAK-PG pages by TMA into canonical SWIZZLE_128B operands:
+// a DAK-PG row is [d 0..63 | d 64..127] with the 16-byte chunks of each half already XOR-swizzled by
+// row & 7, so a 3-D tensor map (64 elements, 2 halves, rows) with box (64, 1, 64) copies one half of
+// 64 rows verbatim into an 8 KB block that IS the 128-byte-swizzled layout: K blocks are the K-major
+// B operand of S (rows = keys), V blocks the MN-major B operand of P V (rows = keys, N = d; LBO =
+// the 8 KB block stride, SBO = 1 KB per 8 keys). No transpose; V is converted bf16 -> fp16 in
+// place (reading R20, as the mma.sync form) by 4 convert warps while S runs.
+// Softmax: one thread per query row (TMEM lane = row), exp2 domain, LAZY rescaling (the row's
+// reference max moves only when the tile max exceeds it by more than 8, then O is rescaled in
+// TMEM; P <= 2^8), P in fp16, l summed from the fp32 P. S buffer t & 1 is released (s_free) as soon
+// as the softmax warps have it in registers, so S(t + 2) overlaps softmax(t) and softmax(t + 1).
+// Warps: 0 producer (one lane), 1 MMA issuer (one elected lane), 2-5 V convert, 6-9 softmax + epilogue.
 constexpr int kUThreads = 10 * 32;
-constexpr int kUOffQ = 1024;                       // Q: 2 blocks x 16 KB
-constexpr int kUOffRaw = kUOffQ + 32768;           // raw ring: 2 stages x (K 16 KB | V 16 KB)
-constexpr int kUOffKc = kUOffRaw + 2 * 2 * kTileBytes;  // Kc: 2 buffers x 2 blocks x 8 KB
-constexpr int kUOffVt = kUOffKc + 2 * kTileBytes;  // V^T: 2 buffers x 16 KB ([128 d][128 B])
-constexpr int kUOffP = kUOffVt + 2 * kTileBytes;   // P (fp16): 2 buffers x 16 KB
-constexpr int kUSmem = kUOffP + 2 * 16384 + 1024;  // + alignment slack
+constexpr int kUStages = 4;
+constexpr int kUOffQ = 1024;                                 // Q: 2 blocks x 16 KB
+constexpr int kUOffStage = kUOffQ + 32768;                   // stages: [K0 | K1 | V0 | V1] x 8 KB
+constexpr int kUOffP = kUOffStage + kUStages * 2 * kTileBytes;  // P (fp16): 2 buffers x 16 KB
+constexpr int kUSmem = kUOffP + 2 * 16384 + 1024;            // + alignment slack
 
-__global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params p) {
+__global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* full = bars;          // [2] raw tile landed (producer)
-  uint64_t* empty = bars + 2;     // [2] raw tile transformed (4 transform warps)
-  uint64_t* kv_full = bars + 4;   // [2] Kc / V^T of the buffer ready (4 transform warps)
-  uint64_t* s_full = bars + 6;    // [2] S of the buffer computed (MMA commit)
-  uint64_t* p_full = bars + 8;    // [2] P of the buffer written, O rescaled (4 softmax warps)
-  uint64_t* pv_done = bars + 10;  // [2] P V of the buffer's tile complete (MMA commit)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 256);
+  uint64_t* full = bars;                   // [kUStages] K / V tile landed (TMA tx)
+  uint64_t* empty = bars + kUStages;       // [kUStages] P V of the stage's tile done (MMA commit)
+  uint64_t* vconv = bars + 2 * kUStages;   // [kUStages] V converted to fp16 (4 convert warps)
+  uint64_t* s_full = bars + 3 * kUStages;  // [2] S computed (MMA commit)
+  uint64_t* s_free = s_full + 2;           // [2] S read into registers (4 softmax warps)
+  uint64_t* p_full = s_full + 4;           // [2] P written, O rescaled (4 softmax warps)
+  uint64_t* pv_done = s_full + 6;          // [2] P V of the buffer's tile complete (MMA commit)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
-  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer: as prefill_attention_kernel
-    unsigned char* ring = smem + kUOffRaw;
-    if (threadIdx.x == 0) {
-      for (int s2 = 0; s2 < 2; ++s2) mbar_init(&full[s2], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    const int n_items_max = p.max_pages * p.B * p.Hkv;
-    int k = 0, mine = 0;
-    auto next_mine = [&](int& b_, int& g_, int& pg_, uint32_t& e_) -> bool {
-      for (; k < n_items_max; ++k) {
-        const int pg = p.max_pages - 1 - k / (p.B * p.Hkv);
-        const int b2 = (k / p.Hkv) % p.B, g2 = k % p.Hkv;
-        const int filled = (p.seq_lens[b2] + p.page - 1) / p.page;
-        if (pg >= filled) continue;
-        const uint32_t e = (uint32_t)p.block_table[(long long)b2 * p.max_pages + pg];
-        if (!(e & kHostBit)) continue;
-        if ((mine++ % p.n_stream) == (int)blockIdx.x) {
-          b_ = b2; g_ = g2; pg_ = pg; e_ = e;
-          ++k;
-          return true;
-        }
-      }
-      return false;
-    };
-    const int SS = (2 * 2 * kTileBytes) / (2 * page_bytes) > 0 ? (2 * 2 * kTileBytes) / (2 * page_bytes) : 1;
-    int qb[2], qg[2], qp[2];
-    int issued = 0, done = 0;
-    auto issue = [&](int slot) -> bool {
-      int b_, g_, pg_;
-      uint32_t e_;
-      if (!next_mine(b_, g_, pg_, e_)) return false;
-      const long long off = ((long long)(e_ & ~kHostBit) * p.Hkv + g_) * page_bytes;
-      unsigned char* dst = ring + (size_t)slot * 2 * page_bytes;
-      mbar_expect_tx(&full[slot], 2u * page_bytes);
-      bulk_g2s(dst, p.k_host + off, page_bytes, &full[slot]);
-      bulk_g2s(dst + page_bytes, p.v_host + off, page_bytes, &full[slot]);
-      qb[slot] = b_; qg[slot] = g_; qp[slot] = pg_;
-      ++issued;
-      return true;
-    };
-    for (int sl = 0; sl < SS && sl < 2 && issue(sl); ++sl) {}
-    const int SSn = SS < 2 ? SS : 2;
-    while (done < issued) {
-      const int sl = done % SSn;
-      mbar_wait(&full[sl], (uint32_t)((done / SSn) & 1));
-      const long long so = (((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl]) * page_bytes;
-      unsigned char* src = ring + (size_t)sl * 2 * page_bytes;
-      bulk_s2g(p.k_stage + so, src, page_bytes);
-      bulk_s2g(p.v_stage + so, src + page_bytes, page_bytes);
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      int* f = p.flags + ((long long)qb[sl] * p.Hkv + qg[sl]) * p.max_pages + qp[sl];
-      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
-      ++done;
-      issue(sl);
-    }
+  if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer
+    const int slots = min(4, kUStages * kTileBytes / page_bytes);  // the stage area
+    stream_host_pages(p, smem + kUOffStage, slots, full, reinterpret_cast<uint2*>(smem + kUOffP));
     return;
   }
   const int cta = (int)blockIdx.x - p.n_stream;
@@ -471,9 +450,16 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params
   const int nt = (kmax + kTile - 1) / kTile;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 12; ++i) {
-      const int which = i >> 1;  // full, empty, kv_full, s_full, p_full, pv_done
-      mbar_init(&bars[i], which == 1 || which == 2 || which == 4 ? 4u : 1u);
+    for (int i = 0; i < kUStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&vconv[i], 4);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
+      mbar_init(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
@@ -482,6 +468,8 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
+  if (warp == 0 && lane == 0)
+    for (int i = 0; i < 6; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.kvmap[i])) : "memory");
   // ---- Q (all threads): row r = (token r / G, head r % G) of the block, two 64-column blocks
   for (int idx = threadIdx.x; idx < kRows * 16; idx += kUThreads) {
     const int r = idx >> 4, j16 = idx & 15;
@@ -500,115 +488,122 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params
   tc_fence_after();
   const uint32_t tmem = *tslot;
 
-  if (warp == 0) {  // ---- producer: raw K / V tiles (DAK-PG), newest keys first
-    if (lane == 0) {
-      const int* bt = p.block_table + (long long)b * p.max_pages;
-      for (int t = 0; t < nt; ++t) {
-        const int s2 = t & 1;
-        if (t >= 2) mbar_wait(&empty[s2], (uint32_t)(((t >> 1) - 1) & 1));
-        const int key0 = (nt - 1 - t) * kTile;
-        const int pg = key0 / p.page;
-        const uint32_t e = (uint32_t)bt[pg];
-        const bool host = (e & kHostBit) != 0;
-        const long long in_page = (long long)(key0 % p.page) * kD * 2;
-        const char* ksrc = (host ? p.k_host : p.k_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
-        const char* vsrc = (host ? p.v_host : p.v_hbm) + ((long long)(e & ~kHostBit) * p.Hkv + g) * page_bytes + in_page;
-        if (host && p.n_stream > 0) {
-          const long long so = (((long long)b * p.Hkv + g) * p.max_pages + pg) * page_bytes + in_page;
-          const int* f = p.flags + ((long long)b * p.Hkv + g) * p.max_pages + pg;
-          int ready = 0;
-          for (int it = 0; it < (1 << 22) && !ready; ++it) {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(ready) : "l"(f) : "memory");
-            if (!ready) __nanosleep(64);
+  if (warp == 0) {  // ---- producer: K / V tiles by TMA, newest keys first (lane 0 issues)
+    const int* bt = p.block_table + (long long)b * p.max_pages;
+    const int* fl = p.flags + ((long long)b * p.Hkv + g) * p.max_pages;
+    int ready_until = -1;  // staged host tiles up to here are known to have their flag up
+    for (int t = 0; t < nt; ++t) {
+      const int s2 = t % kUStages;
+      const int key0 = (nt - 1 - t) * kTile;
+      const int pg = key0 / p.page;
+      const uint32_t e = (uint32_t)bt[pg];
+      const bool host = (e & kHostBit) != 0;
+      int tier = host ? 1 : 0;
+      // pool row of the tile's first key: (page * Hkv + g) * page + key in page
+      long long row = ((long long)(e & ~kHostBit) * p.Hkv + g) * p.page + key0 % p.page;
+      if (host && p.n_stream > 0) {
+        if (t > ready_until) {
+          // the warp polls the flags of tiles t .. t + 31 at once (acquire), until tile t's is up
+          // (bounded: after it, tile t is read over the link directly -- the same bits)
+          const int tl = t + lane;
+          bool mine = true;  // tiles past the end or in HBM count as ready
+          if (tl < nt) {
+            const int pgl = (nt - 1 - tl) * kTile / p.page;
+            if ((uint32_t)bt[pgl] & kHostBit) {
+              int f = 0;
+              asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(fl + pgl) : "memory");
+              mine = f != 0;
+            }
           }
-          if (ready) {
+          uint32_t mask = __ballot_sync(0xffffffffu, mine);
+          for (int it = 0; it < (1 << 22) && !(mask & 1u); ++it) {
+            __nanosleep(64);
+            int f = 1;
+            if (lane == 0) asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(fl + pg) : "memory");
+            mask = __ballot_sync(0xffffffffu, lane == 0 && f != 0);
+          }
+          if (mask & 1u) {
+            ready_until = t + (~mask ? __ffs(~mask) - 1 : 32) - 1;
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            ksrc = p.k_stage + so;
-            vsrc = p.v_stage + so;
           }
         }
-        unsigned char* dst = smem + kUOffRaw + (size_t)s2 * 2 * kTileBytes;
-        mbar_expect_tx(&full[s2], 2u * kTileBytes);
-        bulk_g2s(dst, ksrc, kTileBytes, &full[s2]);
-        bulk_g2s(dst + kTileBytes, vsrc, kTileBytes, &full[s2]);
+        if (t <= ready_until) {
+          tier = 2;
+          row = (((long long)b * p.Hkv + g) * p.max_pages + pg) * p.page + key0 % p.page;
+        }
       }
+      if (lane == 0) {
+        if (t >= kUStages) mbar_wait(&empty[s2], (uint32_t)((t / kUStages - 1) & 1));
+        unsigned char* dst = smem + kUOffStage + (size_t)s2 * 2 * kTileBytes;
+        const uint64_t km = reinterpret_cast<uint64_t>(&p.kvmap[tier]), vm = reinterpret_cast<uint64_t>(&p.kvmap[3 + tier]);
+        mbar_expect_tx(&full[s2], 2u * kTileBytes);
+        tma_3d(dst, km, 0, 0, (int)row, &full[s2]);
+        tma_3d(dst + 8192, km, 0, 1, (int)row, &full[s2]);
+        tma_3d(dst + 16384, vm, 0, 0, (int)row, &full[s2]);
+        tma_3d(dst + 24576, vm, 0, 1, (int)row, &full[s2]);
+      }
+      __syncwarp();
     }
   } else if (warp == 1) {  // ---- MMA issuer
+    // instruction descriptors: f32 accumulate, M = 128; S: bf16 x bf16, N = 64, both K-major;
+    // P V: f16 x f16, N = 128, B (V) MN-major (bit 16)
     const uint32_t id_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const uint32_t id_o = (1u << 4) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);  // f16 x f16 -> f32
-    const uint32_t q_u = su32(smem + kUOffQ), kc_u = su32(smem + kUOffKc), vt_u = su32(smem + kUOffVt),
-                   p_u = su32(smem + kUOffP);
+    const uint32_t id_o = (1u << 4) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    const uint32_t q_u = su32(smem + kUOffQ), st_u = su32(smem + kUOffStage), p_u = su32(smem + kUOffP);
     uint32_t leader;
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
-    auto issue_s = [&](int t) {  // S[t & 1] = Q . Kc[t & 1]^T
-      const int bb = t & 1;
-      mbar_wait(&kv_full[bb], (uint32_t)((t >> 1) & 1));
+    auto issue_s = [&](int t) {  // S[t & 1] = Q . K_t^T
+      const int s2 = t % kUStages;
+      mbar_wait(&full[s2], (uint32_t)((t / kUStages) & 1));
       tc_fence_after();
       if (leader) {
+        const uint32_t kb = st_u + (uint32_t)s2 * 2 * kTileBytes;
 #pragma unroll
         for (int ks = 0; ks < kD / 16; ++ks)
-          umma_bf16(tmem + (uint32_t)(bb * 64), umma_desc_sw128(q_u + (ks >> 2) * 16384 + (ks & 3) * 32),
-                    umma_desc_sw128(kc_u + bb * kTileBytes + (ks >> 2) * 8192 + (ks & 3) * 32), id_s, ks != 0);
-        umma_commit(&s_full[bb]);
+          umma_bf16(tmem + (uint32_t)((t & 1) * 64), umma_desc_sw128(q_u + (ks >> 2) * 16384 + (ks & 3) * 32),
+                    umma_desc_sw128(kb + (ks >> 2) * 8192 + (ks & 3) * 32), id_s, ks != 0);
+        umma_commit(&s_full[t & 1]);
       }
       __syncwarp();
     };
     issue_s(0);
     if (nt > 1) issue_s(1);
     for (int t = 0; t < nt; ++t) {
-      const int bb = t & 1;
+      const int bb = t & 1, s2 = t % kUStages;
+      if (t + 2 < nt) {  // S buffer bb is free once softmax(t) has read it
+        mbar_wait(&s_free[bb], (uint32_t)((t >> 1) & 1));
+        issue_s(t + 2);
+      }
       mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));
+      mbar_wait(&vconv[s2], (uint32_t)((t / kUStages) & 1));
       tc_fence_after();
-      if (leader) {  // O += P V (fp16 operands)
+      if (leader) {  // O += P V
+        const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
 #pragma unroll
         for (int ks = 0; ks < kTile / 16; ++ks)
           umma_bf16(tmem + 128u, umma_desc_sw128(p_u + bb * 16384 + ks * 32),
-                    umma_desc_sw128(vt_u + bb * kTileBytes + ks * 32), id_o, (t | ks) != 0);
-        umma_commit(&pv_done[bb]);  // frees Kc / V^T / P of the buffer; O of tile t is complete
+                    umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | ks) != 0);
+        umma_commit(&empty[s2]);    // K / V stage free
+        umma_commit(&pv_done[bb]);  // P buffer free; O of tile t complete
       }
       __syncwarp();
-      if (t + 2 < nt) issue_s(t + 2);
     }
-  } else if (warp >= 2 && warp <= 5) {  // ---- transform: raw DAK-PG tile -> Kc (2 blocks), V^T
+  } else if (warp >= 2 && warp <= 5) {  // ---- V: bf16 -> fp16 in place (16 KB per tile)
     const int tt = threadIdx.x - 64;  // 0..127
     for (int t = 0; t < nt; ++t) {
-      const int bb = t & 1;
-      mbar_wait(&full[bb], (uint32_t)((t >> 1) & 1));
-      if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));  // buffer bb read by tile t - 2
-      const unsigned char* rk = smem + kUOffRaw + (size_t)bb * 2 * kTileBytes;
-      const unsigned char* rv = rk + kTileBytes;
-      unsigned char* kc = smem + kUOffKc + bb * kTileBytes;
-      unsigned char* vt = smem + kUOffVt + bb * kTileBytes;
-      // K: 16 lanes per key row, stored chunk j16 -> block j16 >> 3 (the swizzle is the same)
-      for (int idx = tt; idx < kTile * 16; idx += 128) {
-        const int key = idx >> 4, j16 = idx & 15;
-        const uint4 u = *reinterpret_cast<const uint4*>(rk + key * 256 + j16 * 16);
-        *reinterpret_cast<uint4*>(kc + (j16 >> 3) * 8192 + key * 128 + (j16 & 7) * 16) = u;
-      }
-      // V^T: lane = key (32 consecutive keys per warp: the swizzled 16-byte reads of one logical d
-      // chunk, and the 2-byte writes of one d row, spread over all banks), logical d chunks dc of
-      // this warp's half
-      {
-        const int tw = warp - 2;  // 0..3
-        const int key = (tw & 1) * 32 + lane;
-        for (int dc = (tw >> 1) * 8; dc < (tw >> 1) * 8 + 8; ++dc) {
-          const int j16 = (dc & 8) | ((dc & 7) ^ (key & 7));  // stored position of logical chunk dc
-          const uint4 w = *reinterpret_cast<const uint4*>(rv + key * 256 + j16 * 16);
-          const uint32_t wv[4] = {bf2_to_h2(w.x), bf2_to_h2(w.y), bf2_to_h2(w.z), bf2_to_h2(w.w)};  // fp16 (R20)
+      const int s2 = t % kUStages;
+      mbar_wait(&full[s2], (uint32_t)((t / kUStages) & 1));
+      unsigned char* v = smem + kUOffStage + (size_t)s2 * 2 * kTileBytes + 16384;
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int d = dc * 8 + e;
-            const unsigned short h = (unsigned short)((wv[e >> 1] >> ((e & 1) * 16)) & 0xffffu);
-            *reinterpret_cast<unsigned short*>(vt + d * 128 + (((key >> 3) ^ (d & 7)) << 4) + (key & 7) * 2) = h;
-          }
-        }
+      for (int i = 0; i < 8; ++i) {
+        uint4* w = reinterpret_cast<uint4*>(v) + tt + 128 * i;
+        uint4 u = *w;
+        u.x = bf2_to_h2(u.x); u.y = bf2_to_h2(u.y); u.z = bf2_to_h2(u.z); u.w = bf2_to_h2(u.w);
+        *w = u;
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&empty[bb]);
-        mbar_arrive(&kv_full[bb]);
-      }
+      if (lane == 0) mbar_arrive(&vconv[s2]);
     }
   } else {  // ---- softmax warps 6..9: thread = query row (TMEM lane)
     const int q4 = warp & 3;
@@ -636,6 +631,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params
           sv[c] = __uint_as_float(v[c]);
         }
       }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[bb]);
       if (key0 + kTile > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
 #pragma unroll
         for (int c = 0; c < kTile; ++c) sv[c] = key0 + c < lim ? sv[c] : -INFINITY;
@@ -733,6 +731,32 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const Params
 
 using namespace dak;
 
+// A K or V pool (HBM, host or staging) as a 3-D bf16 tensor: 64 elements (128 B), 2 row halves
+// (stride 128 B), rows (stride 256 B; the pool's extent is not known here, so the row count is a
+// bound, 2^30, that every in-range row index satisfies).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static dak_status encode_kv_map(CUtensorMap* m, const void* base) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qr;
+    void* f = nullptr;
+    DAK_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &qr));
+    if (qr != cudaDriverEntryPointSuccess || !f) return fail(DAK_ECUDA, "dak_prefill_attention: cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)f;
+  }
+  const cuuint64_t dims[3] = {64, 2, 1ull << 30};
+  const cuuint64_t strides[2] = {128, 256};
+  const cuuint32_t box[3] = {64, 1, (cuuint32_t)pf::kTile};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DAK_ECUDA, "dak_prefill_attention: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DAK_OK;
+}
+
 extern "C" {
 
 static dak_status prefill_plan(const dak_prefill_args* a, pf::Params* p, int* grid, int* smem) {
@@ -775,11 +799,24 @@ static dak_status prefill_plan(const dak_prefill_args* a, pf::Params* p, int* gr
     q.k_stage = (char*)a->workspace + flag_bytes;
     q.v_stage = q.k_stage + stage_bytes;
   }
+  if (q.n_stream > 0) {  // a streamer slot holds one page of K and of V in the kernel's stage ring
+    const long long ring = a->cfg.force_path == 2 ? (long long)q.stages * 2 * pf::kTileBytes : (long long)pf::kUStages * 2 * pf::kTileBytes;
+    if (2LL * a->page_size * pf::kD * 2 > ring)
+      return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: page_size %d too large for host staging (ring %lld B)", a->page_size, ring);
+  }
   const long long g = (long long)a->B * a->Hkv * q.blocks_per_bg + q.n_stream;
   if (g > 0x7fffffffLL) return fail(DAK_EUNSUPPORTED, "dak_prefill_attention: grid too large");
+  if (a->cfg.force_path != 2) {
+    const void* base[6] = {a->k_hbm, a->k_host, q.k_stage, a->v_hbm, a->v_host, q.v_stage};
+    for (int i = 0; i < 6; ++i) {
+      const void* ptr = base[i] ? base[i] : (a->k_hbm ? a->k_hbm : a->k_host);  // unused tier: any valid pointer
+      const dak_status st = encode_kv_map(&q.kvmap[i], ptr);
+      if (st != DAK_OK) return st;
+    }
+  }
   *p = q;
   *grid = (int)g;
-  *smem = 1024 + q.stages * 2 * pf::kTileBytes + 1024;
+  *smem = 1024 + q.stages * 2 * pf::kTileBytes + pf::kListBytes + 1024;
   return DAK_OK;
 }
 
@@ -799,7 +836,7 @@ dak_status dak_prefill_attention(const dak_prefill_args* args, dak_stream_t stre
   static bool attr = false;
   if (!attr) {
     DAK_CUDA_TRY(cudaFuncSetAttribute(pf::prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      1024 + pf::kMaxStages * 2 * pf::kTileBytes + 1024));
+                                      1024 + pf::kMaxStages * 2 * pf::kTileBytes + pf::kListBytes + 1024));
     DAK_CUDA_TRY(cudaFuncSetAttribute(pf::prefill_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pf::kUSmem));
     attr = true;
   }
