@@ -408,17 +408,24 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // B operand of S (rows = keys), V blocks the MN-major B operand of P V (rows = keys, N = d; LBO =
 // the 8 KB block stride, SBO = 1 KB per 8 keys). No transpose; V is converted bf16 -> fp16 in
 // place (reading R20, as the mma.sync form) by 4 convert warps while S runs.
-// Softmax: one thread per query row (TMEM lane = row), exp2 domain, LAZY rescaling (the row's
-// reference max moves only when the tile max exceeds it by more than 8, then O is rescaled in
-// TMEM; P <= 2^8), P in fp16, l summed from the fp32 P. S buffer t & 1 is released (s_free) as soon
-// as the softmax warps have it in registers, so S(t + 2) overlaps softmax(t) and softmax(t + 1).
-// Warps: 0 producer (one lane), 1 MMA issuer (one elected lane), 2-5 V convert, 6-9 softmax + epilogue.
-constexpr int kUThreads = 10 * 32;
+// Softmax: 8 warps, two per TMEM lane quadrant; thread = (query row, key half h of every tile).
+// Each half keeps its OWN running max m_h, sum l_h and accumulator O_h (TMEM columns 128 (1 + h)):
+// O_h += P[:, half h] V[half h, :], so the two warps of a row never synchronise per tile (each
+// hides the other's latencies on the SM sub-partition) and are merged once in the epilogue,
+// O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_h = 2^(m_h - max m) (the log-sum-exp merge the
+// split decode attention's combine kernel uses). exp2 domain, LAZY rescaling (m_h moves only when the
+// tile max exceeds it by more than 8, then O_h is rescaled in TMEM; P <= 2^8), P in fp16, l_h summed
+// from the fp32 P. Software-pipelined: the TMEM loads of S(t + 1) are in flight while tile t's
+// exponentials run on the MUFU; S buffer t & 1 is released (s_free) as soon as it is in registers,
+// so S(t + 2) overlaps softmax(t) and softmax(t + 1). Warps: 0 producer (one lane issues), 1 MMA
+// issuer (one elected lane), 2-5 V convert, 6-13 softmax + epilogue.
+constexpr int kUThreads = 14 * 32;
 constexpr int kUStages = 4;
 constexpr int kUOffQ = 1024;                                 // Q: 2 blocks x 16 KB
 constexpr int kUOffStage = kUOffQ + 32768;                   // stages: [K0 | K1 | V0 | V1] x 8 KB
 constexpr int kUOffP = kUOffStage + kUStages * 2 * kTileBytes;  // P (fp16): 2 buffers x 16 KB
-constexpr int kUSmem = kUOffP + 2 * 16384 + 1024;            // + alignment slack
+constexpr int kUOffX = kUOffP + 2 * 16384;                   // epilogue exchange: m, l per half
+constexpr int kUSmem = kUOffX + 2048 + 1024;                 // + alignment slack
 
 __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -428,9 +435,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
   uint64_t* empty = bars + kUStages;       // [kUStages] P V of the stage's tile done (MMA commit)
   uint64_t* vconv = bars + 2 * kUStages;   // [kUStages] V converted to fp16 (4 convert warps)
   uint64_t* s_full = bars + 3 * kUStages;  // [2] S computed (MMA commit)
-  uint64_t* s_free = s_full + 2;           // [2] S read into registers (4 softmax warps)
-  uint64_t* p_full = s_full + 4;           // [2] P written, O rescaled (4 softmax warps)
-  uint64_t* pv_done = s_full + 6;          // [2] P V of the buffer's tile complete (MMA commit)
+  uint64_t* s_free = s_full + 2;           // [2] S read into registers (8 softmax warps)
+  uint64_t* p_full = s_full + 4;           // [2 buffers][2 key halves] P written, O_h rescaled (4 warps)
+  uint64_t* pv_done = s_full + 8;          // [2] P V of the buffer's tile complete (MMA commit)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
@@ -457,15 +464,16 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&s_free[i], 8);
+      mbar_init(&p_full[2 * i], 4);
+      mbar_init(&p_full[2 * i + 1], 4);
       mbar_init(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
   }
-  if (warp == 1) {  // TMEM: S0 [0, 64), S1 [64, 128), O [128, 256)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot)) : "memory");
+  if (warp == 1) {  // TMEM: S0 [0, 64), S1 [64, 128), O_0 [128, 256), O_1 [256, 384)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == 0 && lane == 0)
@@ -574,17 +582,23 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
         mbar_wait(&s_free[bb], (uint32_t)((t >> 1) & 1));
         issue_s(t + 2);
       }
-      mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));
       mbar_wait(&vconv[s2], (uint32_t)((t / kUStages) & 1));
-      tc_fence_after();
-      if (leader) {  // O += P V
-        const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
+      const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
 #pragma unroll
-        for (int ks = 0; ks < kTile / 16; ++ks)
-          umma_bf16(tmem + 128u, umma_desc_sw128(p_u + bb * 16384 + ks * 32),
-                    umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | ks) != 0);
+      for (int h = 0; h < 2; ++h) {  // O_h += P[:, keys of half h] V[keys of half h, :]
+        mbar_wait(&p_full[2 * bb + h], (uint32_t)((t >> 1) & 1));
+        tc_fence_after();
+        if (leader) {
+#pragma unroll
+          for (int ks = 2 * h; ks < 2 * h + 2; ++ks)
+            umma_bf16(tmem + 128u + 128u * h, umma_desc_sw128(p_u + bb * 16384 + ks * 32),
+                      umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | (ks & 1)) != 0);
+        }
+        __syncwarp();
+      }
+      if (leader) {
         umma_commit(&empty[s2]);    // K / V stage free
-        umma_commit(&pv_done[bb]);  // P buffer free; O of tile t complete
+        umma_commit(&pv_done[bb]);  // P buffer free; O_0, O_1 of tile t complete
       }
       __syncwarp();
     }
@@ -605,115 +619,143 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       __syncwarp();
       if (lane == 0) mbar_arrive(&vconv[s2]);
     }
-  } else {  // ---- softmax warps 6..9: thread = query row (TMEM lane)
-    const int q4 = warp & 3;
-    const int r = 32 * q4 + lane;  // row of the block
+  } else {  // ---- softmax warps 6..13: thread = (query row, key half h); own m, l and O_h
+    const int q4 = warp & 3, h = (warp - 6) >> 2;
+    const int r = 32 * q4 + lane;  // row of the block (TMEM lane)
     const int gr = r0 + r;
     const int lim = gr < rows ? L - p.T + gr / p.G + 1 : 0;  // keys [0, lim) visible
     const int lim_w = __reduce_min_sync(0xffffffffu, (unsigned)lim);  // tiles below it need no mask
     const uint32_t lane_base = (uint32_t)(32 * q4) << 16;
+    const uint32_t o_h = tmem + lane_base + 128u + 128u * (uint32_t)h;  // this half's O accumulator
     float m = -INFINITY, l = 0.f;
+    const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
     unsigned char* pbase = smem + kUOffP;
-    for (int t = 0; t < nt; ++t) {
-      const int bb = t & 1;
-      const int key0 = (nt - 1 - t) * kTile;
-      mbar_wait(&s_full[bb], (uint32_t)((t >> 1) & 1));
+    auto load_s = [&](int t, uint32_t (&v)[32]) {  // issue the TMEM loads of S(t), this half (async)
+      mbar_wait(&s_full[t & 1], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
-      float sv[kTile];
-      {
-        uint32_t v[kTile];
+      tmem_ld16(tmem + lane_base + (uint32_t)((t & 1) * 64 + 32 * h), v);
+      tmem_ld16(tmem + lane_base + (uint32_t)((t & 1) * 64 + 32 * h + 16), v + 16);
+    };
+    auto landed_s = [&](int t, uint32_t (&v)[32]) {  // S(t) in registers: release its TMEM buffer
+      tmem_wait_ld();
 #pragma unroll
-        for (int c0 = 0; c0 < kTile; c0 += 16) tmem_ld16(tmem + lane_base + (uint32_t)(bb * 64 + c0), v + c0);
-        tmem_wait_ld();
-#pragma unroll
-        for (int c = 0; c < kTile; ++c) {
-          asm volatile("" : "+r"(v[c]));  // keep every use after the wait
-          sv[c] = __uint_as_float(v[c]);
-        }
-      }
+      for (int c = 0; c < 32; ++c) asm volatile("" : "+r"(v[c]));  // keep every use after the wait
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[bb]);
-      if (key0 + kTile > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
+      if (lane == 0) mbar_arrive(&s_free[t & 1]);
+    };
+    // tile t from registers `cur` while the TMEM loads of S(t + 1) land in `nxt`
+    auto step = [&](int t, uint32_t (&cur)[32], uint32_t (&nxt)[32]) {
+      const int bb = t & 1;
+      const int key0 = (nt - 1 - t) * kTile + 32 * h;
+      if (t + 1 < nt) load_s(t + 1, nxt);
+      float* sv = reinterpret_cast<float*>(cur);
+      if (key0 + 32 > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
 #pragma unroll
-        for (int c = 0; c < kTile; ++c) sv[c] = key0 + c < lim ? sv[c] : -INFINITY;
+        for (int c = 0; c < 32; ++c) sv[c] = key0 + c < lim ? sv[c] : -INFINITY;
       }
-      float mx = -INFINITY;
+      float mq[4];  // 4 independent max chains
 #pragma unroll
-      for (int c = 0; c < kTile; ++c) mx = fmaxf(mx, sv[c]);
-      mx *= p.scale_log2;  // scale > 0: max of the scaled logits
-      // lazy reference max: move it (and rescale O, l) only when the tile max exceeds it by > 8
+      for (int j = 0; j < 4; ++j) {
+        mq[j] = fmax3(sv[8 * j], sv[8 * j + 1], sv[8 * j + 2]);
+        mq[j] = fmax3(mq[j], sv[8 * j + 3], sv[8 * j + 4]);
+        mq[j] = fmax3(mq[j], sv[8 * j + 5], sv[8 * j + 6]);
+        mq[j] = fmaxf(mq[j], sv[8 * j + 7]);
+      }
+      const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * p.scale_log2;  // scale > 0
+      // lazy reference max: move it (and rescale O_h, l) only when the tile max exceeds it by > 8
       const bool move = mx > m + 8.f;
-      const float m_new = move ? mx : m;
-      const float alpha = move ? exp2f(m - m_new) : 1.f;  // exp2(-inf) = 0 for a row's first keys
-      if (t > 0 && __any_sync(0xffffffffu, move && m != -INFINITY)) {
-        // O of tile t - 1 must be complete before it is rescaled in TMEM
-        mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
-        tc_fence_after();
+      if (__any_sync(0xffffffffu, move)) {
+        const float m_new = move ? mx : m;
+        const float alpha = m == -INFINITY ? 0.f : ex2_ftz(m - m_new);  // 1 for rows that keep m
+        if (t > 0 && __any_sync(0xffffffffu, move && m != -INFINITY)) {
+          // O_h of tile t - 1 must be complete before it is rescaled in TMEM
+          mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+          tc_fence_after();
 #pragma unroll 1
-        for (int c0 = 0; c0 < kD; c0 += 16) {
-          uint32_t v[16];
-          tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v);
-          tmem_wait_ld();
+          for (int c0 = 0; c0 < kD; c0 += 16) {
+            uint32_t v[16];
+            tmem_ld16(o_h + (uint32_t)c0, v);
+            tmem_wait_ld();
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-          tmem_st16(tmem + lane_base + 128u + (uint32_t)c0, v);
+            for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
+            tmem_st16(o_h + (uint32_t)c0, v);
+          }
+          tmem_wait_st();
         }
-        tmem_wait_st();
+        l *= alpha;
+        m = m_new;
       }
-      l *= alpha;
-      m = m_new;
       const float ref = m == -INFINITY ? 0.f : m;
+      const float2 nref2 = make_float2(-ref, -ref);
       // P buffer bb is free once the P V of tile t - 2 has completed
       if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));
       unsigned char* ph = pbase + bb * 16384;
-      float l2 = 0.f;
+      float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int c8 = 0; c8 < kTile / 8; ++c8) {
+      for (int c8 = 0; c8 < 4; ++c8) {
         uint32_t hw[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = ex2_ftz(fmaf(sv[c8 * 8 + 2 * e], p.scale_log2, -ref));
-          const float p1 = ex2_ftz(fmaf(sv[c8 * 8 + 2 * e + 1], p.scale_log2, -ref));
-          hw[e] = pack_f16(p0, p1);
-          l += p0;
-          l2 += p1;
+          float2 x = ffma2(make_float2(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]), sc2, nref2);
+          x.x = ex2_ftz(x.x);
+          x.y = ex2_ftz(x.y);
+          hw[e] = pack_f16(x.x, x.y);
+          l2 = fadd2(l2, x);
         }
-        const int off = r * 128 + ((c8 ^ (r & 7)) << 4);
+        const int c = 4 * h + c8;  // 16-byte chunk of the P row
+        const int off = r * 128 + ((c ^ (r & 7)) << 4);
         *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
       }
-      l += l2;
+      l += l2.x + l2.y;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[bb]);
+      if (lane == 0) mbar_arrive(&p_full[2 * bb + h]);
+      if (t + 1 < nt) landed_s(t + 1, nxt);
+    };
+    uint32_t sa[32], sb[32];
+    load_s(0, sa);
+    landed_s(0, sa);
+    for (int t = 0; t < nt; t += 2) {
+      step(t, sa, sb);
+      if (t + 1 < nt) step(t + 1, sb, sa);
     }
-    // ---- epilogue: O / l -> bf16
+    // ---- epilogue: merge the halves, O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_h = 2^(m_h - M);
+    // this warp writes d [64 h, 64 h + 64)
+    float* xch = reinterpret_cast<float*>(smem + kUOffX);  // [m | l][2 halves][128 rows]
+    xch[h * 128 + r] = m;
+    xch[256 + h * 128 + r] = l;
+    asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
+    const float m0 = h ? xch[r] : m, m1 = h ? m : xch[128 + r];
+    const float l0 = h ? xch[256 + r] : l, l1 = h ? l : xch[384 + r];
+    const float M = fmaxf(m0, m1);
+    const float a0 = m0 == -INFINITY ? 0.f : ex2_ftz(m0 - M), a1 = m1 == -INFINITY ? 0.f : ex2_ftz(m1 - M);
+    const float lt = a0 * l0 + a1 * l1;
+    const float inv = lt > 0.f ? 1.f / lt : 0.f;
+    const float s0 = a0 * inv, s1 = a1 * inv;
     mbar_wait(&pv_done[(nt - 1) & 1], (uint32_t)(((nt - 1) >> 1) & 1));
     tc_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
     __nv_bfloat16* dst = nullptr;
     if (gr < rows) {
       const int i = gr / p.G, hh = gr % p.G;
       dst = p.out + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD;
     }
 #pragma unroll 1
-    for (int c0 = 0; c0 < kD; c0 += 16) {
-      uint32_t v[16];
-      tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v);
+    for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 16) {
+      uint32_t v0[16], v1[16];
+      tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v0);
+      tmem_ld16(tmem + lane_base + 256u + (uint32_t)c0, v1);
       tmem_wait_ld();
       if (dst) {
-        uint4 o0, o1;
-        o0.x = pack_bf16(__uint_as_float(v[0]) * inv, __uint_as_float(v[1]) * inv);
-        o0.y = pack_bf16(__uint_as_float(v[2]) * inv, __uint_as_float(v[3]) * inv);
-        o0.z = pack_bf16(__uint_as_float(v[4]) * inv, __uint_as_float(v[5]) * inv);
-        o0.w = pack_bf16(__uint_as_float(v[6]) * inv, __uint_as_float(v[7]) * inv);
-        o1.x = pack_bf16(__uint_as_float(v[8]) * inv, __uint_as_float(v[9]) * inv);
-        o1.y = pack_bf16(__uint_as_float(v[10]) * inv, __uint_as_float(v[11]) * inv);
-        o1.z = pack_bf16(__uint_as_float(v[12]) * inv, __uint_as_float(v[13]) * inv);
-        o1.w = pack_bf16(__uint_as_float(v[14]) * inv, __uint_as_float(v[15]) * inv);
-        reinterpret_cast<uint4*>(dst + c0)[0] = o0;
-        reinterpret_cast<uint4*>(dst + c0)[1] = o1;
+        float o[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = __uint_as_float(v0[e]) * s0 + __uint_as_float(v1[e]) * s1;
+        uint4 w0, w1;
+        w0.x = pack_bf16(o[0], o[1]); w0.y = pack_bf16(o[2], o[3]); w0.z = pack_bf16(o[4], o[5]); w0.w = pack_bf16(o[6], o[7]);
+        w1.x = pack_bf16(o[8], o[9]); w1.y = pack_bf16(o[10], o[11]); w1.z = pack_bf16(o[12], o[13]); w1.w = pack_bf16(o[14], o[15]);
+        reinterpret_cast<uint4*>(dst + c0)[0] = w0;
+        reinterpret_cast<uint4*>(dst + c0)[1] = w1;
       }
     }
     tc_fence_before();
@@ -722,7 +764,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
   if (threadIdx.x == 0) tstamp(p.trace, 3);
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 

@@ -135,6 +135,29 @@ __device__ __forceinline__ float ex2_ftz(float x) {  // MUFU.EX2; ex2(-inf) = 0
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {  // FMNMX3 (sm_100)
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// packed fp32 pair arithmetic (FFMA2 / FADD2, sm_100)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long d;
+  asm("fma.rn.ftz.f32x2 %0, %1, %2, %3;"
+      : "=l"(d)
+      : "l"(((unsigned long long)__float_as_uint(a.y) << 32) | __float_as_uint(a.x)),
+        "l"(((unsigned long long)__float_as_uint(b.y) << 32) | __float_as_uint(b.x)),
+        "l"(((unsigned long long)__float_as_uint(c.y) << 32) | __float_as_uint(c.x)));
+  return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long d;
+  asm("add.rn.ftz.f32x2 %0, %1, %2;"
+      : "=l"(d)
+      : "l"(((unsigned long long)__float_as_uint(a.y) << 32) | __float_as_uint(a.x)),
+        "l"(((unsigned long long)__float_as_uint(b.y) << 32) | __float_as_uint(b.x)));
+  return make_float2(__uint_as_float((uint32_t)d), __uint_as_float((uint32_t)(d >> 32)));
+}
 __device__ __forceinline__ uint32_t pack_f16(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
