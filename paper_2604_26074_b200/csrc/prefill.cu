@@ -399,15 +399,20 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // ================================================================================================
 // tcgen05 form (5th-gen tensor cores, TMEM accumulators). Same work split, host staging and
 // newest-keys-first order as prefill_attention_kernel; the contractions run as
-//   S[128 rows x 64 keys]  = Q[128 x 128 d] . K_tile^T   (8 x M128 N64 K16, TMEM columns 64 (t & 1))
-//   O[128 rows x 128 d]   += P[128 x 64 keys] . V_tile   (fp16 operands: 4 x M128 N128 K16, columns 128..255)
+//   S[128 rows x 64 keys]  = Q[128 x 128 d] . K_tile^T   (8 x M128 N64 K16; A = Q from TMEM)
+//   O_h[128 rows x 128 d] += P[128 x 32 keys] . V_half   (fp16: 2 x M128 N128 K16 per half; A = P from TMEM)
+// Q (stored once) and P (written by the softmax warps with tcgen05.st) are A operands in tensor
+// memory, so shared memory carries only the K / V tiles: the TMA writes (32 KB per tile), the V
+// fp16 conversion (16 + 16 KB) and the tensor core's K / V reads (32 KB) -- with Q and P there too
+// it moved 160 KB per tile, more than the MMAs' 512 cycles at ~128 B/clk.
 // The K / V tiles come straight from the DAK-PG pages by TMA into canonical SWIZZLE_128B operands:
 // a DAK-PG row is [d 0..63 | d 64..127] with the 16-byte chunks of each half already XOR-swizzled by
 // row & 7, so a 3-D tensor map (64 elements, 2 halves, rows) with box (64, 1, 64) copies one half of
 // 64 rows verbatim into an 8 KB block that IS the 128-byte-swizzled layout: K blocks are the K-major
 // B operand of S (rows = keys), V blocks the MN-major B operand of P V (rows = keys, N = d; LBO =
 // the 8 KB block stride, SBO = 1 KB per 8 keys). No transpose; V is converted bf16 -> fp16 in
-// place (reading R20, as the mma.sync form) by 4 convert warps while S runs.
+// place (reading R20, as the mma.sync form; tcgen05 kind::f16 takes one type for A and B) by 4
+// convert warps while S runs.
 // Softmax: 8 warps, two per TMEM lane quadrant; thread = (query row, key half h of every tile).
 // Each half keeps its OWN running max m_h, sum l_h and accumulator O_h (TMEM columns 128 (1 + h)):
 // O_h += P[:, half h] V[half h, :], so the two warps of a row never synchronise per tile (each
@@ -420,12 +425,13 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // so S(t + 2) overlaps softmax(t) and softmax(t + 1). Warps: 0 producer (one lane issues), 1 MMA
 // issuer (one elected lane), 2-5 V convert, 6-13 softmax + epilogue.
 constexpr int kUThreads = 14 * 32;
-constexpr int kUStages = 4;
-constexpr int kUOffQ = 1024;                                 // Q: 2 blocks x 16 KB
-constexpr int kUOffStage = kUOffQ + 32768;                   // stages: [K0 | K1 | V0 | V1] x 8 KB
-constexpr int kUOffP = kUOffStage + kUStages * 2 * kTileBytes;  // P (fp16): 2 buffers x 16 KB
-constexpr int kUOffX = kUOffP + 2 * 16384;                   // epilogue exchange: m, l per half
-constexpr int kUSmem = kUOffX + 2048 + 1024;                 // + alignment slack
+constexpr int kUStages = 6;
+constexpr int kUOffStage = 1024;                             // stages: [K0 | K1 | V0 | V1] x 8 KB
+constexpr int kUOffX = kUOffStage + kUStages * 2 * kTileBytes;  // epilogue m / l exchange; streamer list
+constexpr int kUSmem = kUOffX + 4096 + 1024;                 // + alignment slack
+// TMEM columns: S(t & 1) at 64 (t & 1), O_h at 128 (1 + h), Q (A operand, bf16 pairs) at 384,
+// P(t & 1) (A operand, fp16 pairs) at 448 + 32 (t & 1)
+constexpr uint32_t kTmO = 128, kTmQ = 384, kTmP = 448;
 
 __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid_constant__ Params p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -443,11 +449,12 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
   const int page_bytes = p.page * kD * 2;
   if ((int)blockIdx.x < p.n_stream) {  // ---- host-tier streamer
     const int slots = min(4, kUStages * kTileBytes / page_bytes);  // the stage area
-    stream_host_pages(p, smem + kUOffStage, slots, full, reinterpret_cast<uint2*>(smem + kUOffP));
+    stream_host_pages(p, smem + kUOffStage, slots, full, reinterpret_cast<uint2*>(smem + kUOffX));
     return;
   }
   const int cta = (int)blockIdx.x - p.n_stream;
-  const int bg = cta / p.blocks_per_bg, blk = cta % p.blocks_per_bg;
+  const int bg = cta / p.blocks_per_bg;
+  const int blk = p.blocks_per_bg - 1 - cta % p.blocks_per_bg;  // longest causal ranges first (smaller tail)
   const int b = bg / p.Hkv, g = bg % p.Hkv;
   const int L = p.seq_lens[b];
   const int rows = p.T * p.G;
@@ -472,29 +479,40 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     tstamp(p.trace, 0);
   }
-  if (warp == 1) {  // TMEM: S0 [0, 64), S1 [64, 128), O_0 [128, 256), O_1 [256, 384)
+  if (warp == 1) {  // TMEM: all 512 columns (see kTmO / kTmQ / kTmP)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot)) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (warp == 0 && lane == 0)
     for (int i = 0; i < 6; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&p.kvmap[i])) : "memory");
-  // ---- Q (all threads): row r = (token r / G, head r % G) of the block, two 64-column blocks
-  for (int idx = threadIdx.x; idx < kRows * 16; idx += kUThreads) {
-    const int r = idx >> 4, j16 = idx & 15;
-    const int gr = r0 + r;
-    uint4 v = make_uint4(0u, 0u, 0u, 0u);
-    if (gr < rows) {
-      const int i = gr / p.G, hh = gr % p.G;
-      v = reinterpret_cast<const uint4*>(p.q + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD)[j16];
-    }
-    const int blkq = j16 >> 3, c = j16 & 7;
-    *reinterpret_cast<uint4*>(smem + kUOffQ + blkq * 16384 + r * 128 + ((c ^ (r & 7)) << 4)) = v;
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tslot;
+  if (warp >= 6) {  // ---- Q -> TMEM (A operand of S): thread = row, warp half h = d [64 h, 64 h + 64)
+    const int q4 = warp & 3, h = (warp - 6) >> 2;
+    const int r = 32 * q4 + lane, gr = r0 + r;
+    uint32_t v[32];
+    if (gr < rows) {
+      const int i = gr / p.G, hh = gr % p.G;
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD + 64 * h);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 u = src[j];
+        v[4 * j] = u.x; v[4 * j + 1] = u.y; v[4 * j + 2] = u.z; v[4 * j + 3] = u.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0u;
+    }
+    const uint32_t qa = tmem + ((uint32_t)(32 * q4) << 16) + kTmQ + 32u * (uint32_t)h;
+    tmem_st16(qa, v);
+    tmem_st16(qa + 16u, v + 16);
+    tmem_wait_st();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   if (warp == 0) {  // ---- producer: K / V tiles by TMA, newest keys first (lane 0 issues)
     const int* bt = p.block_table + (long long)b * p.max_pages;
@@ -557,7 +575,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     // P V: f16 x f16, N = 128, B (V) MN-major (bit 16)
     const uint32_t id_s = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
     const uint32_t id_o = (1u << 4) | (1u << 16) | ((uint32_t)(128 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
-    const uint32_t q_u = su32(smem + kUOffQ), st_u = su32(smem + kUOffStage), p_u = su32(smem + kUOffP);
+    const uint32_t st_u = su32(smem + kUOffStage);
     uint32_t leader;
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
     auto issue_s = [&](int t) {  // S[t & 1] = Q . K_t^T
@@ -567,9 +585,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       if (leader) {
         const uint32_t kb = st_u + (uint32_t)s2 * 2 * kTileBytes;
 #pragma unroll
-        for (int ks = 0; ks < kD / 16; ++ks)
-          umma_bf16(tmem + (uint32_t)((t & 1) * 64), umma_desc_sw128(q_u + (ks >> 2) * 16384 + (ks & 3) * 32),
-                    umma_desc_sw128(kb + (ks >> 2) * 8192 + (ks & 3) * 32), id_s, ks != 0);
+        for (int ks = 0; ks < kD / 16; ++ks)  // A = Q from TMEM: 8 columns (16 bf16) per K step
+          umma_ts(tmem + (uint32_t)((t & 1) * 64), tmem + kTmQ + 8u * ks,
+                  umma_desc_sw128(kb + (ks >> 2) * 8192 + (ks & 3) * 32), id_s, ks != 0);
         umma_commit(&s_full[t & 1]);
       }
       __syncwarp();
@@ -590,9 +608,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
         tc_fence_after();
         if (leader) {
 #pragma unroll
-          for (int ks = 2 * h; ks < 2 * h + 2; ++ks)
-            umma_bf16(tmem + 128u + 128u * h, umma_desc_sw128(p_u + bb * 16384 + ks * 32),
-                      umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | (ks & 1)) != 0);
+          for (int ks = 2 * h; ks < 2 * h + 2; ++ks)  // A = P from TMEM
+            umma_ts(tmem + kTmO + 128u * h, tmem + kTmP + 32u * bb + 8u * ks,
+                    umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | (ks & 1)) != 0);
         }
         __syncwarp();
       }
@@ -626,10 +644,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     const int lim = gr < rows ? L - p.T + gr / p.G + 1 : 0;  // keys [0, lim) visible
     const int lim_w = __reduce_min_sync(0xffffffffu, (unsigned)lim);  // tiles below it need no mask
     const uint32_t lane_base = (uint32_t)(32 * q4) << 16;
-    const uint32_t o_h = tmem + lane_base + 128u + 128u * (uint32_t)h;  // this half's O accumulator
+    const uint32_t o_h = tmem + lane_base + kTmO + 128u * (uint32_t)h;  // this half's O accumulator
     float m = -INFINITY, l = 0.f;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    unsigned char* pbase = smem + kUOffP;
     auto load_s = [&](int t, uint32_t (&v)[32]) {  // issue the TMEM loads of S(t), this half (async)
       mbar_wait(&s_full[t & 1], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
@@ -690,25 +707,19 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       const float2 nref2 = make_float2(-ref, -ref);
       // P buffer bb is free once the P V of tile t - 2 has completed
       if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));
-      unsigned char* ph = pbase + bb * 16384;
       float2 l2 = make_float2(0.f, 0.f);
+      uint32_t pw[16];  // P of this half as fp16 pairs -> TMEM (A operand of P V)
 #pragma unroll
-      for (int c8 = 0; c8 < 4; ++c8) {
-        uint32_t hw[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          float2 x = ffma2(make_float2(sv[c8 * 8 + 2 * e], sv[c8 * 8 + 2 * e + 1]), sc2, nref2);
-          x.x = ex2_ftz(x.x);
-          x.y = ex2_ftz(x.y);
-          hw[e] = pack_f16(x.x, x.y);
-          l2 = fadd2(l2, x);
-        }
-        const int c = 4 * h + c8;  // 16-byte chunk of the P row
-        const int off = r * 128 + ((c ^ (r & 7)) << 4);
-        *reinterpret_cast<uint4*>(ph + off) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+      for (int e = 0; e < 16; ++e) {
+        float2 x = ffma2(make_float2(sv[2 * e], sv[2 * e + 1]), sc2, nref2);
+        x.x = ex2_ftz(x.x);
+        x.y = ex2_ftz(x.y);
+        pw[e] = pack_f16(x.x, x.y);
+        l2 = fadd2(l2, x);
       }
+      tmem_st16(tmem + lane_base + kTmP + 32u * (uint32_t)bb + 16u * (uint32_t)h, pw);
       l += l2.x + l2.y;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tmem_wait_st();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[2 * bb + h]);
@@ -744,8 +755,8 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
 #pragma unroll 1
     for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 16) {
       uint32_t v0[16], v1[16];
-      tmem_ld16(tmem + lane_base + 128u + (uint32_t)c0, v0);
-      tmem_ld16(tmem + lane_base + 256u + (uint32_t)c0, v1);
+      tmem_ld16(tmem + lane_base + kTmO + (uint32_t)c0, v0);
+      tmem_ld16(tmem + lane_base + kTmO + 128u + (uint32_t)c0, v1);
       tmem_wait_ld();
       if (dst) {
         float o[16];
