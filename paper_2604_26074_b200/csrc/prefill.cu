@@ -413,17 +413,18 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // the 8 KB block stride, SBO = 1 KB per 8 keys). No transpose; V is converted bf16 -> fp16 in
 // place (reading R20, as the mma.sync form; tcgen05 kind::f16 takes one type for A and B) by 4
 // convert warps while S runs.
-// Softmax: 8 warps, two per TMEM lane quadrant; thread = (query row, key half h of every tile).
-// Each half keeps its OWN running max m_h, sum l_h and accumulator O_h (TMEM columns 128 (1 + h)):
-// O_h += P[:, half h] V[half h, :], so the two warps of a row never synchronise per tile (each
-// hides the other's latencies on the SM sub-partition) and are merged once in the epilogue,
-// O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_h = 2^(m_h - max m) (the log-sum-exp merge the
-// split decode attention's combine kernel uses). exp2 domain, LAZY rescaling (m_h moves only when the
-// tile max exceeds it by more than 8, then O_h is rescaled in TMEM; P <= 2^8), P in fp16, l_h summed
-// from the fp32 P. Software-pipelined: the TMEM loads of S(t + 1) are in flight while tile t's
-// exponentials run on the MUFU; S buffer t & 1 is released (s_free) as soon as it is in registers,
-// so S(t + 2) overlaps softmax(t) and softmax(t + 1). Warps: 0 producer (one lane issues), 1 MMA
-// issuer (one elected lane), 2-5 V convert, 6-13 softmax + epilogue.
+// Softmax: 8 warps, two per TMEM lane quadrant (thread = query row); warp parity c takes the tiles
+// t = c mod 2 and keeps its OWN running max m_c, sum l_c and accumulator O_c (TMEM columns
+// 128 (1 + c); P V of tile t accumulates into O_(t & 1)), so the two warps of a row never
+// synchronise per tile and run half a period apart on their SM sub-partition (one's exponentials
+// overlap the other's TMEM loads, barrier waits and stores -- the ping-pong FA4 gets from two
+// query tiles). Merged once in the epilogue: O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1),
+// a_c = 2^(m_c - max m) (the log-sum-exp merge the split decode attention's combine kernel uses).
+// exp2 domain, LAZY rescaling (m_c moves only when the tile max exceeds it by more than 8, then O_c
+// is rescaled in TMEM; P <= 2^8), P in fp16 (tcgen05.st into TMEM), l_c summed from the fp32 P.
+// S buffer c is released (s_free) as soon as it is in registers, so S(t + 2) overlaps softmax(t).
+// Warps: 0 producer (one lane issues), 1 MMA issuer (one elected lane), 2-5 V convert, 6-13
+// softmax + epilogue.
 constexpr int kUThreads = 14 * 32;
 constexpr int kUStages = 6;
 constexpr int kUOffStage = 1024;                             // stages: [K0 | K1 | V0 | V1] x 8 KB
@@ -442,8 +443,8 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
   uint64_t* vconv = bars + 2 * kUStages;   // [kUStages] V converted to fp16 (4 convert warps)
   uint64_t* s_full = bars + 3 * kUStages;  // [2] S computed (MMA commit)
   uint64_t* s_free = s_full + 2;           // [2] S read into registers (8 softmax warps)
-  uint64_t* p_full = s_full + 4;           // [2 buffers][2 key halves] P written, O_h rescaled (4 warps)
-  uint64_t* pv_done = s_full + 8;          // [2] P V of the buffer's tile complete (MMA commit)
+  uint64_t* p_full = s_full + 4;           // [2] P(t) of parity t & 1 written, O rescaled (4 warps)
+  uint64_t* pv_done = s_full + 6;          // [2] P V of the parity's latest tile complete (MMA commit)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
@@ -471,9 +472,8 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 8);
-      mbar_init(&p_full[2 * i], 4);
-      mbar_init(&p_full[2 * i + 1], 4);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -601,22 +601,16 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
         issue_s(t + 2);
       }
       mbar_wait(&vconv[s2], (uint32_t)((t / kUStages) & 1));
-      const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
+      mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));
+      tc_fence_after();
+      if (leader) {  // O_bb += P(t) V(t): the tiles of parity bb accumulate in their own O
+        const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // O_h += P[:, keys of half h] V[keys of half h, :]
-        mbar_wait(&p_full[2 * bb + h], (uint32_t)((t >> 1) & 1));
-        tc_fence_after();
-        if (leader) {
-#pragma unroll
-          for (int ks = 2 * h; ks < 2 * h + 2; ++ks)  // A = P from TMEM
-            umma_ts(tmem + kTmO + 128u * h, tmem + kTmP + 32u * bb + 8u * ks,
-                    umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, (t | (ks & 1)) != 0);
-        }
-        __syncwarp();
-      }
-      if (leader) {
+        for (int ks = 0; ks < kTile / 16; ++ks)  // A = P from TMEM: 8 columns (16 fp16) per K step
+          umma_ts(tmem + kTmO + 128u * bb, tmem + kTmP + 32u * bb + 8u * ks,
+                  umma_desc_sw128_mn(vb + ks * 2048, 8192), id_o, ((t >> 1) | ks) != 0);
         umma_commit(&empty[s2]);    // K / V stage free
-        umma_commit(&pv_done[bb]);  // P buffer free; O_0, O_1 of tile t complete
+        umma_commit(&pv_done[bb]);  // P(t) consumed; O_bb holds tiles <= t of its parity
       }
       __syncwarp();
     }
@@ -637,115 +631,107 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       __syncwarp();
       if (lane == 0) mbar_arrive(&vconv[s2]);
     }
-  } else {  // ---- softmax warps 6..13: thread = (query row, key half h); own m, l and O_h
-    const int q4 = warp & 3, h = (warp - 6) >> 2;
+  } else {  // ---- softmax warps 6..13: thread = query row, warp parity c = the tiles t = c mod 2
+    const int q4 = warp & 3, c = (warp - 6) >> 2;
     const int r = 32 * q4 + lane;  // row of the block (TMEM lane)
     const int gr = r0 + r;
     const int lim = gr < rows ? L - p.T + gr / p.G + 1 : 0;  // keys [0, lim) visible
     const int lim_w = __reduce_min_sync(0xffffffffu, (unsigned)lim);  // tiles below it need no mask
     const uint32_t lane_base = (uint32_t)(32 * q4) << 16;
-    const uint32_t o_h = tmem + lane_base + kTmO + 128u * (uint32_t)h;  // this half's O accumulator
+    const uint32_t o_c = tmem + lane_base + kTmO + 128u * (uint32_t)c;  // this parity's O accumulator
+    const uint32_t s_c = tmem + lane_base + 64u * (uint32_t)c;          // S buffer of this parity
+    const uint32_t p_c = tmem + lane_base + kTmP + 32u * (uint32_t)c;   // P buffer of this parity
     float m = -INFINITY, l = 0.f;
     const float2 sc2 = make_float2(p.scale_log2, p.scale_log2);
-    auto load_s = [&](int t, uint32_t (&v)[32]) {  // issue the TMEM loads of S(t), this half (async)
-      mbar_wait(&s_full[t & 1], (uint32_t)((t >> 1) & 1));
+    for (int t = c, k = 0; t < nt; t += 2, ++k) {  // k: this warp's k-th tile (barrier phase k & 1)
+      const int key0 = (nt - 1 - t) * kTile;
+      mbar_wait(&s_full[c], (uint32_t)(k & 1));
       tc_fence_after();
-      tmem_ld16(tmem + lane_base + (uint32_t)((t & 1) * 64 + 32 * h), v);
-      tmem_ld16(tmem + lane_base + (uint32_t)((t & 1) * 64 + 32 * h + 16), v + 16);
-    };
-    auto landed_s = [&](int t, uint32_t (&v)[32]) {  // S(t) in registers: release its TMEM buffer
+      uint32_t sv_u[kTile];
+#pragma unroll
+      for (int c0 = 0; c0 < kTile; c0 += 16) tmem_ld16(s_c + (uint32_t)c0, sv_u + c0);
       tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < 32; ++c) asm volatile("" : "+r"(v[c]));  // keep every use after the wait
+      for (int j = 0; j < kTile; ++j) asm volatile("" : "+r"(sv_u[j]));  // keep every use after the wait
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[t & 1]);
-    };
-    // tile t from registers `cur` while the TMEM loads of S(t + 1) land in `nxt`
-    auto step = [&](int t, uint32_t (&cur)[32], uint32_t (&nxt)[32]) {
-      const int bb = t & 1;
-      const int key0 = (nt - 1 - t) * kTile + 32 * h;
-      if (t + 1 < nt) load_s(t + 1, nxt);
-      float* sv = reinterpret_cast<float*>(cur);
-      if (key0 + 32 > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
+      if (lane == 0) mbar_arrive(&s_free[c]);  // S(t + 2) may overwrite the buffer
+      float* sv = reinterpret_cast<float*>(sv_u);
+      if (key0 + kTile > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
 #pragma unroll
-        for (int c = 0; c < 32; ++c) sv[c] = key0 + c < lim ? sv[c] : -INFINITY;
+        for (int j = 0; j < kTile; ++j) sv[j] = key0 + j < lim ? sv[j] : -INFINITY;
       }
       float mq[4];  // 4 independent max chains
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        mq[j] = fmax3(sv[8 * j], sv[8 * j + 1], sv[8 * j + 2]);
-        mq[j] = fmax3(mq[j], sv[8 * j + 3], sv[8 * j + 4]);
-        mq[j] = fmax3(mq[j], sv[8 * j + 5], sv[8 * j + 6]);
-        mq[j] = fmaxf(mq[j], sv[8 * j + 7]);
+        const float* x = sv + 16 * j;
+        float a = fmax3(x[0], x[1], x[2]), b2 = fmax3(x[3], x[4], x[5]);
+        a = fmax3(a, x[6], x[7]);
+        b2 = fmax3(b2, x[8], x[9]);
+        a = fmax3(a, x[10], x[11]);
+        b2 = fmax3(b2, x[12], x[13]);
+        mq[j] = fmax3(a, b2, fmaxf(x[14], x[15]));
       }
       const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * p.scale_log2;  // scale > 0
-      // lazy reference max: move it (and rescale O_h, l) only when the tile max exceeds it by > 8
+      // the P V of this parity's previous tile must be complete before its P buffer is rewritten
+      // and before its O is rescaled
+      if (k > 0) mbar_wait(&pv_done[c], (uint32_t)((k - 1) & 1));
+      // lazy reference max: move it (and rescale O, l) only when the tile max exceeds it by > 8
       const bool move = mx > m + 8.f;
       if (__any_sync(0xffffffffu, move)) {
         const float m_new = move ? mx : m;
         const float alpha = m == -INFINITY ? 0.f : ex2_ftz(m - m_new);  // 1 for rows that keep m
-        if (t > 0 && __any_sync(0xffffffffu, move && m != -INFINITY)) {
-          // O_h of tile t - 1 must be complete before it is rescaled in TMEM
-          mbar_wait(&pv_done[(t - 1) & 1], (uint32_t)(((t - 1) >> 1) & 1));
+        if (k > 0 && __any_sync(0xffffffffu, move && m != -INFINITY)) {
           tc_fence_after();
 #pragma unroll 1
           for (int c0 = 0; c0 < kD; c0 += 16) {
             uint32_t v[16];
-            tmem_ld16(o_h + (uint32_t)c0, v);
+            tmem_ld16(o_c + (uint32_t)c0, v);
             tmem_wait_ld();
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) * alpha);
-            tmem_st16(o_h + (uint32_t)c0, v);
+            tmem_st16(o_c + (uint32_t)c0, v);
           }
-          tmem_wait_st();
         }
         l *= alpha;
         m = m_new;
       }
       const float ref = m == -INFINITY ? 0.f : m;
       const float2 nref2 = make_float2(-ref, -ref);
-      // P buffer bb is free once the P V of tile t - 2 has completed
-      if (t >= 2) mbar_wait(&pv_done[bb], (uint32_t)(((t >> 1) - 1) & 1));
-      float2 l2 = make_float2(0.f, 0.f);
-      uint32_t pw[16];  // P of this half as fp16 pairs -> TMEM (A operand of P V)
+      float2 l2 = make_float2(0.f, 0.f), l3 = make_float2(0.f, 0.f);
+      uint32_t pw[kTile / 2];  // P as fp16 pairs -> TMEM (A operand of P V)
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
+      for (int e = 0; e < kTile / 2; ++e) {
         float2 x = ffma2(make_float2(sv[2 * e], sv[2 * e + 1]), sc2, nref2);
         x.x = ex2_ftz(x.x);
         x.y = ex2_ftz(x.y);
         pw[e] = pack_f16(x.x, x.y);
-        l2 = fadd2(l2, x);
+        if (e & 1) l3 = fadd2(l3, x); else l2 = fadd2(l2, x);
       }
-      tmem_st16(tmem + lane_base + kTmP + 32u * (uint32_t)bb + 16u * (uint32_t)h, pw);
-      l += l2.x + l2.y;
+      tmem_st16(p_c, pw);
+      tmem_st16(p_c + 16u, pw + 16);
+      l += (l2.x + l2.y) + (l3.x + l3.y);
       tmem_wait_st();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[2 * bb + h]);
-      if (t + 1 < nt) landed_s(t + 1, nxt);
-    };
-    uint32_t sa[32], sb[32];
-    load_s(0, sa);
-    landed_s(0, sa);
-    for (int t = 0; t < nt; t += 2) {
-      step(t, sa, sb);
-      if (t + 1 < nt) step(t + 1, sb, sa);
+      if (lane == 0) mbar_arrive(&p_full[c]);
     }
-    // ---- epilogue: merge the halves, O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_h = 2^(m_h - M);
-    // this warp writes d [64 h, 64 h + 64)
-    float* xch = reinterpret_cast<float*>(smem + kUOffX);  // [m | l][2 halves][128 rows]
-    xch[h * 128 + r] = m;
-    xch[256 + h * 128 + r] = l;
+    // ---- epilogue: merge the parities, O = (a_0 O_0 + a_1 O_1) / (a_0 l_0 + a_1 l_1), a_c = 2^(m_c - M);
+    // this warp writes d [64 c, 64 c + 64). An O never written (nt == 1: parity 1 has no tile) has
+    // a_c = 0 and is not read.
+    float* xch = reinterpret_cast<float*>(smem + kUOffX);  // [m | l][2 parities][128 rows]
+    xch[c * 128 + r] = m;
+    xch[256 + c * 128 + r] = l;
     asm volatile("bar.sync %0, 64;" ::"r"(1 + q4) : "memory");
-    const float m0 = h ? xch[r] : m, m1 = h ? m : xch[128 + r];
-    const float l0 = h ? xch[256 + r] : l, l1 = h ? l : xch[384 + r];
+    const float m0 = c ? xch[r] : m, m1 = c ? m : xch[128 + r];
+    const float l0 = c ? xch[256 + r] : l, l1 = c ? l : xch[384 + r];
     const float M = fmaxf(m0, m1);
     const float a0 = m0 == -INFINITY ? 0.f : ex2_ftz(m0 - M), a1 = m1 == -INFINITY ? 0.f : ex2_ftz(m1 - M);
     const float lt = a0 * l0 + a1 * l1;
     const float inv = lt > 0.f ? 1.f / lt : 0.f;
     const float s0 = a0 * inv, s1 = a1 * inv;
-    mbar_wait(&pv_done[(nt - 1) & 1], (uint32_t)(((nt - 1) >> 1) & 1));
+    const bool use1 = nt > 1;
+    mbar_wait(&pv_done[(nt - 1) & 1], (uint32_t)(((nt - 1) >> 1) & 1));  // the last P V (covers both parities)
     tc_fence_after();
     __nv_bfloat16* dst = nullptr;
     if (gr < rows) {
@@ -753,7 +739,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       dst = p.out + (((long long)b * p.T + i) * p.Hq + (long long)g * p.G + hh) * kD;
     }
 #pragma unroll 1
-    for (int c0 = 64 * h; c0 < 64 * h + 64; c0 += 16) {
+    for (int c0 = 64 * c; c0 < 64 * c + 64; c0 += 16) {
       uint32_t v0[16], v1[16];
       tmem_ld16(tmem + lane_base + kTmO + (uint32_t)c0, v0);
       tmem_ld16(tmem + lane_base + kTmO + 128u + (uint32_t)c0, v1);
@@ -761,7 +747,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       if (dst) {
         float o[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = __uint_as_float(v0[e]) * s0 + __uint_as_float(v1[e]) * s1;
+        for (int e = 0; e < 16; ++e) o[e] = __uint_as_float(v0[e]) * s0 + (use1 ? __uint_as_float(v1[e]) * s1 : 0.f);
         uint4 w0, w1;
         w0.x = pack_bf16(o[0], o[1]); w0.y = pack_bf16(o[2], o[3]); w0.z = pack_bf16(o[4], o[5]); w0.w = pack_bf16(o[6], o[7]);
         w1.x = pack_bf16(o[8], o[9]); w1.y = pack_bf16(o[10], o[11]); w1.z = pack_bf16(o[12], o[13]); w1.w = pack_bf16(o[14], o[15]);

@@ -54,6 +54,14 @@ def test_prefill_parity(D, Ls, T, Hkv, Hq, page, frac, stage):
     assert_close(Kx.bf16_to_f64(got), ref)
 
 
+@pytest.mark.parametrize("Ls,T,Hkv,Hq,page,frac", CASES[:3] + CASES[4:5])
+def test_prefill_mma_sync_form(D, Ls, T, Hkv, Hq, page, frac):
+    """cfg.force_path = 2 selects the mma.sync (HMMA) form of the kernel: the same parity bar."""
+    from tests.gpu_util import assert_close
+    got, ref, _ = run_prefill(D, Ls, T, Hkv, Hq, page, frac, seed=800 + T, force_path=2)
+    assert_close(Kx.bf16_to_f64(got), ref)
+
+
 @pytest.mark.parametrize("kind", ["wide", "constk", "dominant"])
 def test_prefill_score_ranges(D, kind):
     from tests.gpu_util import assert_close
