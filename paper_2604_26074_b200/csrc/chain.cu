@@ -73,16 +73,6 @@ __device__ __forceinline__ void op_rows(const Op& o, int cta, bool* host, long l
   }
   tier_rows(*R_tier, j, n, rb, re);
 }
-// non-blocking phase test (mbarrier.try_wait may suspend the thread for a system-dependent time,
-// which would stall the producer's other cursor)
-__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
-  uint32_t done;
-  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-               : "=r"(done)
-               : "r"(su32(b)), "r"(parity)
-               : "memory");
-  return done != 0;
-}
 __device__ __forceinline__ void bulk_g2s_ef(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(

@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // it moved 160 KB per tile, more than the MMAs' 512 cycles at ~128 B/clk.
 // The K / V tiles come straight from the DAK-PG pages by TMA into canonical SWIZZLE_128B operands:
 // a DAK-PG row is [d 0..63 | d 64..127] with the 16-byte chunks of each half already XOR-swizzled by
-// row & 7, so a 3-D tensor map (64 elements, 2 halves, rows) with box (64, 1, 64) copies one half of
+// row & 7, so a 3-D tensor map (64 elements, rows, 2 halves) with box (64, 64, 2) copies each half of
 // 64 rows verbatim into an 8 KB block that IS the 128-byte-swizzled layout: K blocks are the K-major
 // B operand of S (rows = keys), V blocks the MN-major B operand of P V (rows = keys, N = d; LBO =
 // the 8 KB block stride, SBO = 1 KB per 8 keys). No transpose; V is converted bf16 -> fp16 in
@@ -518,15 +518,36 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     const int* bt = p.block_table + (long long)b * p.max_pages;
     const int* fl = p.flags + ((long long)b * p.Hkv + g) * p.max_pages;
     int ready_until = -1;  // staged host tiles up to here are known to have their flag up
+    // block-table entries of tiles [w0, w0 + 32) in lane t - w0 (one load per 32 tiles, the next
+    // window's load in flight while this one is used: a dependent global load per tile would pace
+    // the whole pipeline)
+    auto bt_of = [&](int tl) -> uint32_t { return tl < nt ? (uint32_t)bt[(nt - 1 - tl) * kTile / p.page] : 0u; };
+    // lane i of the window also holds tile w0 + i's page, key offset in the page and staging-pool
+    // row, so a tile costs three shuffles (no integer divisions on the producer's critical path)
+    int pg_w = 0, ip_w = 0, rs_w = 0;
+    auto win_geom = [&](int tl) {
+      const int key0 = (nt - 1 - min(tl, nt - 1)) * kTile;
+      pg_w = key0 / p.page;
+      ip_w = key0 - pg_w * p.page;
+      rs_w = (((b * p.Hkv + g) * p.max_pages) + pg_w) * p.page + ip_w;
+    };
+    uint32_t e_win = bt_of(lane), e_next = bt_of(32 + lane);
+    win_geom(lane);
+    int rp_w = (int)(e_win & ~kHostBit) * p.Hkv * p.page + g * p.page + ip_w;  // HBM / host pool row
     for (int t = 0; t < nt; ++t) {
       const int s2 = t % kUStages;
-      const int key0 = (nt - 1 - t) * kTile;
-      const int pg = key0 / p.page;
-      const uint32_t e = (uint32_t)bt[pg];
+      if (t > 0 && (t & 31) == 0) {
+        e_win = e_next;
+        e_next = bt_of(t + 32 + lane);
+        win_geom(t + lane);
+        rp_w = (int)(e_win & ~kHostBit) * p.Hkv * p.page + g * p.page + ip_w;
+      }
+      const uint32_t e = __shfl_sync(0xffffffffu, e_win, t & 31);
       const bool host = (e & kHostBit) != 0;
       int tier = host ? 1 : 0;
-      // pool row of the tile's first key: (page * Hkv + g) * page + key in page
-      long long row = ((long long)(e & ~kHostBit) * p.Hkv + g) * p.page + key0 % p.page;
+      int row = __shfl_sync(0xffffffffu, rp_w, t & 31);  // pool row of the tile's first key
+      const int row_stage = __shfl_sync(0xffffffffu, rs_w, t & 31);
+      const int pg = __shfl_sync(0xffffffffu, pg_w, t & 31);
       if (host && p.n_stream > 0) {
         if (t > ready_until) {
           // the warp polls the flags of tiles t .. t + 31 at once (acquire), until tile t's is up
@@ -535,7 +556,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
           bool mine = true;  // tiles past the end or in HBM count as ready
           if (tl < nt) {
             const int pgl = (nt - 1 - tl) * kTile / p.page;
-            if ((uint32_t)bt[pgl] & kHostBit) {
+            if (bt_of(tl) & kHostBit) {
               int f = 0;
               asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(f) : "l"(fl + pgl) : "memory");
               mine = f != 0;
@@ -555,7 +576,7 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
         }
         if (t <= ready_until) {
           tier = 2;
-          row = (((long long)b * p.Hkv + g) * p.max_pages + pg) * p.page + key0 % p.page;
+          row = row_stage;
         }
       }
       if (lane == 0) {
@@ -563,10 +584,8 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
         unsigned char* dst = smem + kUOffStage + (size_t)s2 * 2 * kTileBytes;
         const uint64_t km = reinterpret_cast<uint64_t>(&p.kvmap[tier]), vm = reinterpret_cast<uint64_t>(&p.kvmap[3 + tier]);
         mbar_expect_tx(&full[s2], 2u * kTileBytes);
-        tma_3d(dst, km, 0, 0, (int)row, &full[s2]);
-        tma_3d(dst + 8192, km, 0, 1, (int)row, &full[s2]);
-        tma_3d(dst + 16384, vm, 0, 0, (int)row, &full[s2]);
-        tma_3d(dst + 24576, vm, 0, 1, (int)row, &full[s2]);
+        tma_3d(dst, km, 0, (int)row, 0, &full[s2]);          // K: [half][64 rows][128 B]
+        tma_3d(dst + 16384, vm, 0, (int)row, 0, &full[s2]);  // V
       }
       __syncwarp();
     }
@@ -770,9 +789,10 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
 
 using namespace dak;
 
-// A K or V pool (HBM, host or staging) as a 3-D bf16 tensor: 64 elements (128 B), 2 row halves
-// (stride 128 B), rows (stride 256 B; the pool's extent is not known here, so the row count is a
-// bound, 2^30, that every in-range row index satisfies).
+// A K or V pool (HBM, host or staging) as a 3-D bf16 tensor: 64 elements (128 B), rows (stride
+// 256 B; the pool's extent is not known here, so the row count is a bound, 2^30, that every
+// in-range row index satisfies), 2 row halves (stride 128 B). A (64, 64, 2) box lands as two 8 KB
+// blocks [half][row][64 elements].
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -785,9 +805,9 @@ static dak_status encode_kv_map(CUtensorMap* m, const void* base) {
     if (qr != cudaDriverEntryPointSuccess || !f) return fail(DAK_ECUDA, "dak_prefill_attention: cuTensorMapEncodeTiled unavailable");
     fn = (EncodeTiledFn)f;
   }
-  const cuuint64_t dims[3] = {64, 2, 1ull << 30};
-  const cuuint64_t strides[2] = {128, 256};
-  const cuuint32_t box[3] = {64, 1, (cuuint32_t)pf::kTile};
+  const cuuint64_t dims[3] = {64, 1ull << 30, 2};
+  const cuuint64_t strides[2] = {256, 128};
+  const cuuint32_t box[3] = {64, (cuuint32_t)pf::kTile, 2};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,

@@ -28,6 +28,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         : "memory");
   }
 }
+// non-blocking probe (test_wait never suspends the thread; try_wait may, and wakes up late)
+__device__ __forceinline__ bool mbar_test(uint64_t* b, uint32_t parity) {
+  uint32_t done;
+  asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+               : "=r"(done)
+               : "r"(su32(b)), "r"(parity)
+               : "memory");
+  return done != 0;
+}
+// spin on the probe: for short, latency-critical waits of warps that own their issue slots
+__device__ __forceinline__ void mbar_spin(uint64_t* b, uint32_t parity) {
+  while (!mbar_test(b, parity)) {
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
