@@ -7,12 +7,12 @@ import sys
 P = "paper_2604_26074_b200/csrc/prefill.cu"
 MARK = "  // PFT-TRACE\n"
 PTS = [  # (anchor line, event, guard)
-    ("        tma_3d(dst + 24576, vm, 0, 1, (int)row, &full[s2]);\n", 0, ""),
+    ("        tma_3d(dst + 16384, vm, 0, (int)row, 0, &full[s2]);  // V\n", 0, ""),
     ("        umma_commit(&s_full[t & 1]);\n", 1, ""),
     ("        if (t >= kUStages) mbar_wait(&empty[s2], (uint32_t)((t / kUStages - 1) & 1));\n", 11, ""),
     ("        umma_commit(&pv_done[bb]);  // P(t) consumed; O_bb holds tiles <= t of its parity\n", 2, ""),
     ("      if (lane == 0) mbar_arrive(&vconv[s2]);\n", 3, "lane == 0 && warp == 2"),
-    ("      if (lane == 0) mbar_arrive(&s_free[c]);  // S(t + 2) may overwrite the buffer\n", 5, "lane == 0 && q4 == 0"),
+    ("      for (int j = 0; j < kTile; ++j) asm volatile(\"\" : \"+r\"(sv_u[j]));  // keep every use after the wait\n", 5, "lane == 0 && q4 == 0"),
     ("      const float mx = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])) * p.scale_log2;  // scale > 0\n", 6, "lane == 0 && q4 == 0"),
     ("      if (k > 0) mbar_wait(&pv_done[c], (uint32_t)((k - 1) & 1));\n", 7, "lane == 0 && q4 == 0"),
     ("      tmem_st16(p_c, pw);\n", 8, "lane == 0 && q4 == 0"),
@@ -20,7 +20,7 @@ PTS = [  # (anchor line, event, guard)
 ]
 PRE = [("      mbar_wait(&s_full[c], (uint32_t)(k & 1));\n", 4, "lane == 0 && q4 == 0"),
        ("        if (t >= kUStages) mbar_wait(&empty[s2], (uint32_t)((t / kUStages - 1) & 1));\n", 10, ""),
-       ("        mbar_wait(&s_free[bb], (uint32_t)((t >> 1) & 1));\n", 12, "leader"),
+       ("      if (t + 2 < nt) issue_s(t + 2);  // first: softmax(t + 2) waits for it\n", 12, "leader"),
        ("      mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));\n", 13, "leader")]
 DEF = ('#define PFT(ev, tt) do { if (p.trace && cta == 0 && (tt) < 64) { long long c_; asm volatile("mov.u64 %0, %%clock64;" : "=l"(c_)); '
        'p.trace[2100 + (tt) * 16 + (ev)] = (unsigned long long)c_; } } while (0)\n')
