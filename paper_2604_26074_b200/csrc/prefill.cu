@@ -422,7 +422,8 @@ __global__ void __launch_bounds__(kThreads, 1) prefill_attention_kernel(const __
 // a_c = 2^(m_c - max m) (the log-sum-exp merge the split decode attention's combine kernel uses).
 // exp2 domain, LAZY rescaling (m_c moves only when the tile max exceeds it by more than 8, then O_c
 // is rescaled in TMEM; P <= 2^8), P in fp16 (tcgen05.st into TMEM), l_c summed from the fp32 P.
-// S buffer c is released (s_free) as soon as it is in registers, so S(t + 2) overlaps softmax(t).
+// The MMA warp waits on two barriers per tile: p_full(t) (softmax(t) has read S(t) and written
+// P(t)) releases S(t + 2), issued first, then P V(t); vconv(t + 2) (tile landed, V converted).
 // Warps: 0 producer (one lane issues), 1 MMA issuer (one elected lane), 2-5 V convert, 6-13
 // softmax + epilogue.
 constexpr int kUThreads = 14 * 32;
@@ -442,7 +443,6 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
   uint64_t* empty = bars + kUStages;       // [kUStages] P V of the stage's tile done (MMA commit)
   uint64_t* vconv = bars + 2 * kUStages;   // [kUStages] V converted to fp16 (4 convert warps)
   uint64_t* s_full = bars + 3 * kUStages;  // [2] S computed (MMA commit)
-  uint64_t* s_free = s_full + 2;           // [2] S read into registers (8 softmax warps)
   uint64_t* p_full = s_full + 4;           // [2] P(t) of parity t & 1 written, O rescaled (4 warps)
   uint64_t* pv_done = s_full + 6;          // [2] P V of the parity's latest tile complete (MMA commit)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
@@ -472,7 +472,6 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
     }
@@ -597,9 +596,9 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     const uint32_t st_u = su32(smem + kUOffStage);
     uint32_t leader;
     asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
-    auto issue_s = [&](int t) {  // S[t & 1] = Q . K_t^T
+    auto issue_s = [&](int t) {  // S[t & 1] = Q . K_t^T (tile t landed and its V converted)
       const int s2 = t % kUStages;
-      mbar_wait(&full[s2], (uint32_t)((t / kUStages) & 1));
+      mbar_wait(&vconv[s2], (uint32_t)((t / kUStages) & 1));
       tc_fence_after();
       if (leader) {
         const uint32_t kb = st_u + (uint32_t)s2 * 2 * kTileBytes;
@@ -615,13 +614,11 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
     if (nt > 1) issue_s(1);
     for (int t = 0; t < nt; ++t) {
       const int bb = t & 1, s2 = t % kUStages;
-      if (t + 2 < nt) {  // S buffer bb is free once softmax(t) has read it
-        mbar_wait(&s_free[bb], (uint32_t)((t >> 1) & 1));
-        issue_s(t + 2);
-      }
-      mbar_wait(&vconv[s2], (uint32_t)((t / kUStages) & 1));
+      // softmax(t) done: S buffer bb has been read (S(t + 2) may overwrite it) and P(t) is written;
+      // V(t) was converted before S(t) was issued
       mbar_wait(&p_full[bb], (uint32_t)((t >> 1) & 1));
       tc_fence_after();
+      if (t + 2 < nt) issue_s(t + 2);  // first: softmax(t + 2) waits for it
       if (leader) {  // O_bb += P(t) V(t): the tiles of parity bb accumulate in their own O
         const uint32_t vb = st_u + (uint32_t)s2 * 2 * kTileBytes + 16384;
 #pragma unroll
@@ -672,9 +669,6 @@ __global__ void __launch_bounds__(kUThreads, 1) prefill_umma_kernel(const __grid
       tmem_wait_ld();
 #pragma unroll
       for (int j = 0; j < kTile; ++j) asm volatile("" : "+r"(sv_u[j]));  // keep every use after the wait
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[c]);  // S(t + 2) may overwrite the buffer
       float* sv = reinterpret_cast<float*>(sv_u);
       if (key0 + kTile > lim_w) {  // the warp's diagonal tiles: mask keys >= lim
 #pragma unroll
