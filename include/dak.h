@@ -56,7 +56,8 @@ dak_status dak_device_sms(int32_t* sms);
 dak_status dak_trace_enable(void* dev_buf, int32_t max_launches);
 int32_t dak_trace_count(void);
 /* kind: 1 linear (a = M, b = K), 2 attention, 3 combine, 4 KV append, 5 LayerNorm, 6 embed,
- * 7 split-K reduce (a = M, b = splits), 8 prefill attention (a = B, b = T). */
+ * 7 split-K reduce (a = M, b = splits), 8 prefill attention (a = B, b = T), 9 residual + RMSNorm
+ * (a = rows, b = cols), 10 silu * up (a = rows, b = F). */
 dak_status dak_trace_launch(int32_t i, int32_t* kind, int64_t* a, int64_t* b, int32_t* grid);
 
 /* =============================================================================================

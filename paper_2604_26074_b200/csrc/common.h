@@ -36,6 +36,8 @@ unsigned long long* trace_slot(int kind, long long a, long long b, int grid);
 #define DAK_KIND_EMBED 6
 #define DAK_KIND_REDUCE 7
 #define DAK_KIND_PREFILL 8
+#define DAK_KIND_RESIDUAL 9
+#define DAK_KIND_SILU 10
 
 // dak_linear with the split-K reduce optionally left to the consumer (dak_layer fuses it into the
 // next kernel): *ksplit_out = K splits of the launch (1: none, y written); with defer_reduce and

@@ -193,12 +193,21 @@ __global__ void silu_mul_kernel(const __nv_bfloat16* __restrict__ gu, __nv_bfloa
     const long long split = (long long)gridDim.y * 2 * F;
     const float* pr = part + (long long)blockIdx.y * 2 * F;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < F / 4; j += gridDim.x * blockDim.x) {
-      float4 a = reinterpret_cast<const float4*>(pr)[j], u = reinterpret_cast<const float4*>(pr + F)[j];
-      for (int sp = 1; sp < S; ++sp) {
-        const float4 ta = reinterpret_cast<const float4*>(pr + sp * split)[j];
-        const float4 tu = reinterpret_cast<const float4*>(pr + sp * split + F)[j];
-        a.x += ta.x; a.y += ta.y; a.z += ta.z; a.w += ta.w;
-        u.x += tu.x; u.y += tu.y; u.z += tu.z; u.w += tu.w;
+      float4 a = __ldcg(reinterpret_cast<const float4*>(pr) + j), u = __ldcg(reinterpret_cast<const float4*>(pr + F) + j);
+      for (int s0 = 1; s0 < S; s0 += 4) {  // up to 4 splits' loads in flight, then summed in split order
+        float4 ta[4], tu[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (s0 + q < S) {
+            ta[q] = __ldcg(reinterpret_cast<const float4*>(pr + (s0 + q) * split) + j);
+            tu[q] = __ldcg(reinterpret_cast<const float4*>(pr + (s0 + q) * split + F) + j);
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (s0 + q < S) {
+            a.x += ta[q].x; a.y += ta[q].y; a.z += ta[q].z; a.w += ta[q].w;
+            u.x += tu[q].x; u.y += tu[q].y; u.z += tu[q].z; u.w += tu[q].w;
+          }
       }
       const float av[4] = {a.x, a.y, a.z, a.w}, uv[4] = {u.x, u.y, u.z, u.w};
       float r[4];
@@ -763,7 +772,7 @@ dak_status dak::silu_mul_part(const void* gu, void* out, int32_t rows, int32_t F
   const __nv_bfloat16* gp = (const __nv_bfloat16*)gu;
   __nv_bfloat16* op = (__nv_bfloat16*)out;
   int f = F;
-  unsigned long long* tr = trace_slot(DAK_KIND_LAYERNORM, rows, F, rows);
+  unsigned long long* tr = trace_slot(DAK_KIND_SILU, rows, F, rows);
   int vec = F % 8 == 0 && aligned16(gu) && aligned16(out);
   int s = S;
   void* args[] = {&gp, &op, &f, &tr, &vec, &part, &s};

@@ -155,50 +155,106 @@ __global__ void __launch_bounds__(kThreads) residual_stats_vec_kernel(const __nv
 
 // x[r] += partial[r] (bf16 RNE), then y[r] = bf16(x[r] * rstd * w) with rstd = 1/sqrt(mean(x^2) + eps)
 // (RMSNorm of the new row: the same arithmetic as dak_rmsnorm, fused so the MLP pre-norm needs no
-// launch of its own). 8 columns per 16-byte chunk, chunks held in registers; y may alias partial
-// (each thread reads its own chunks before the first barrier and writes only those).
-constexpr int kVec = 8;  // 16-byte chunks per thread (cols <= 256 * 64)
+// launch of its own). y may alias partial (each thread reads its own chunks before it writes).
 // part != nullptr (one rank): the row-parallel linear's split-K partials are reduced here instead of
 // by its reduce kernel -- partial = bf16(sum_s part[s][r][c]) in split order, the arithmetic of
 // splitk_reduce_kernel without bias / activation -- so the combine costs no extra launch.
-__device__ __forceinline__ uint4 sum_parts8(const float* part, long long plane, int S, long long off) {
-  float4 a = __ldcg(reinterpret_cast<const float4*>(part + off));
-  float4 b = __ldcg(reinterpret_cast<const float4*>(part + off + 4));
-  for (int s = 1; s < S; ++s) {
-    const float4 c = __ldcg(reinterpret_cast<const float4*>(part + s * plane + off));
-    const float4 d = __ldcg(reinterpret_cast<const float4*>(part + s * plane + off + 4));
-    a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
-    b.x += d.x; b.y += d.y; b.z += d.z; b.w += d.w;
+//
+// A row is split over a cluster of `cpr` CTAs (16-byte chunks [crank * per, ...)), each thread
+// holding V chunks in registers: every load of a thread (x, the S partials) is issued before the
+// first use -- one L2 round trip -- and the norm weight, a parameter, is loaded before the
+// dependency wait. The row's sum of squares: per thread, warp shuffle, warps in order, then the
+// cluster's CTA sums in rank order through distributed shared memory (every CTA adds the same
+// values in the same order: the same rstd). A one-CTA-per-row form spent ~9 us per launch on
+// dependent load round trips over 64 SMs (profiles/r02/step_launches_llama3-70b-tp8-b64-ctx4096.txt).
+constexpr int kVec = 8;    // max 16-byte chunks per thread
+constexpr int kMaxCpr = 8; // max CTAs per row (portable cluster size)
+__device__ __forceinline__ void tstamp(unsigned long long* tr, int k) {
+  if (tr && threadIdx.x == 0 && blockIdx.x < kTraceCtas) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tr[blockIdx.x * 4 + k] = t;
   }
-  uint4 o;
-  __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
-  oh[0] = __floats2bfloat162_rn(a.x, a.y);
-  oh[1] = __floats2bfloat162_rn(a.z, a.w);
-  oh[2] = __floats2bfloat162_rn(b.x, b.y);
-  oh[3] = __floats2bfloat162_rn(b.z, b.w);
-  return o;
 }
+__device__ __forceinline__ void add4(float4& a, const float4 c) {
+  a.x += c.x; a.y += c.y; a.z += c.z; a.w += c.w;
+}
+template <int V>
 __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_bfloat16* partial,
                                                                     __nv_bfloat16* __restrict__ x, int cols,
                                                                     const __nv_bfloat16* __restrict__ w, float eps,
-                                                                    __nv_bfloat16* y, const float* part, int S, int rows) {
+                                                                    __nv_bfloat16* y, const float* part, int S, int rows,
+                                                                    int cpr, unsigned long long* tr) {
   __shared__ float red[kThreads / 32];
+  __shared__ float cta_sum;
+  tstamp(tr, 0);
+  const int nc = cols / 8;
+  const int crank = (int)blockIdx.x % cpr, row = (int)blockIdx.x / cpr;
+  const int per = (nc + cpr - 1) / cpr;
+  const int c0 = crank * per, c1 = min(nc, c0 + per);
+  const long long base = (long long)row * nc;
+  uint4 wv[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {  // parameters: loaded while the producing kernel drains
+    const int c = c0 + threadIdx.x + i * kThreads;
+    if (c < c1) wv[i] = __ldg(reinterpret_cast<const uint4*>(w) + c);
+  }
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const int nc = cols / 8;
-  const long long base = (long long)blockIdx.x * nc;
+  tstamp(tr, 1);
   uint4* xr = reinterpret_cast<uint4*>(x) + base;
-  const uint4* pr = reinterpret_cast<const uint4*>(partial) + base;
+  uint4 xa[V], pb[V];
+  float4 lo[V], hi[V];
   const long long plane = (long long)rows * cols;
-  float f[kVec][8];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {  // every load of the thread first: one round trip
+    const int c = c0 + threadIdx.x + i * kThreads;
+    if (c < c1) {
+      xa[i] = xr[c];
+      if (part) {
+        const float* q = part + (base + c) * 8;
+        lo[i] = __ldcg(reinterpret_cast<const float4*>(q));
+        hi[i] = __ldcg(reinterpret_cast<const float4*>(q + 4));
+      } else {
+        pb[i] = reinterpret_cast<const uint4*>(partial)[base + c];
+      }
+    }
+  }
+  if (part) {
+    for (int s = 1; s < S; ++s) {  // split order; the V chunks' loads of split s are independent
+      float4 l2[V], h2[V];
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const int c = c0 + threadIdx.x + i * kThreads;
+        if (c < c1) {
+          const float* q = part + s * plane + (base + c) * 8;
+          l2[i] = __ldcg(reinterpret_cast<const float4*>(q));
+          h2[i] = __ldcg(reinterpret_cast<const float4*>(q + 4));
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        add4(lo[i], l2[i]);
+        add4(hi[i], h2[i]);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&pb[i]);
+      oh[0] = __floats2bfloat162_rn(lo[i].x, lo[i].y);
+      oh[1] = __floats2bfloat162_rn(lo[i].z, lo[i].w);
+      oh[2] = __floats2bfloat162_rn(hi[i].x, hi[i].y);
+      oh[3] = __floats2bfloat162_rn(hi[i].z, hi[i].w);
+    }
+  }
+  float f[V][8];
   float ss = 0.f;
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    const int c = threadIdx.x + i * kThreads;
-    if (c < nc) {
-      const uint4 a = xr[c], b = part ? sum_parts8(part, plane, S, (base + c) * 8) : pr[c];
-      const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&a);
-      const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&b);
+  for (int i = 0; i < V; ++i) {
+    const int c = c0 + threadIdx.x + i * kThreads;
+    if (c < c1) {
+      const __nv_bfloat162* ah = reinterpret_cast<const __nv_bfloat162*>(&xa[i]);
+      const __nv_bfloat162* bh = reinterpret_cast<const __nv_bfloat162*>(&pb[i]);
       uint4 o;
       __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
@@ -213,15 +269,30 @@ __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_b
       xr[c] = o;
     }
   }
-  const float rstd = rsqrtf(block_sum(ss, red) / (float)cols + eps);
+  const float t = block_sum(ss, red);
+  float total = t;
+  if (cpr > 1) {  // the cluster's CTA sums, in rank order, through distributed shared memory
+    if (threadIdx.x == 0) cta_sum = t;
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    total = 0.f;
+    const uint32_t local = (uint32_t)__cvta_generic_to_shared(&cta_sum);
+    for (int r = 0; r < cpr; ++r) {
+      uint32_t remote;
+      float v;
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(r));
+      asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+      total += v;
+    }
+    // peers may still read our cta_sum: stay resident until every CTA of the cluster has read
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
+  const float rstd = rsqrtf(total / (float)cols + eps);
   uint4* yr = reinterpret_cast<uint4*>(y) + base;
-  const uint4* wv = reinterpret_cast<const uint4*>(w);
 #pragma unroll
-  for (int i = 0; i < kVec; ++i) {
-    const int c = threadIdx.x + i * kThreads;
-    if (c < nc) {
-      const uint4 wu = wv[c];
-      const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&wu);
+  for (int i = 0; i < V; ++i) {
+    const int c = c0 + threadIdx.x + i * kThreads;
+    if (c < c1) {
+      const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&wv[i]);
       uint4 o;
       __nv_bfloat162* oh = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
@@ -232,6 +303,42 @@ __global__ void __launch_bounds__(kThreads) residual_rmsnorm_kernel(const __nv_b
       yr[c] = o;
     }
   }
+  if (cpr > 1) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  tstamp(tr, 3);
+}
+
+// launch: cpr = CTAs per row (a cluster), V = chunks per thread
+static dak_status launch_residual_rmsnorm(const __nv_bfloat16* partial, const float* part, int S, void* x, int rows,
+                                          int cols, const void* w, float eps, void* y, bool pdl, cudaStream_t s) {
+  const int nc = cols / 8;
+  const int cpr = std::min(kMaxCpr, std::max(1, (nc + kThreads - 1) / kThreads));
+  const int per = (nc + cpr - 1) / cpr;
+  const int V = (per + kThreads - 1) / kThreads;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cpr;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(rows * cpr);
+  cfg.blockDim = dim3(kThreads);
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  unsigned long long* tr = trace_slot(DAK_KIND_RESIDUAL, rows, cols, rows * cpr);
+  auto go = [&](auto kern) {
+    return cudaLaunchKernelEx(&cfg, kern, partial, (__nv_bfloat16*)x, cols, (const __nv_bfloat16*)w, eps,
+                              (__nv_bfloat16*)y, part, S, rows, cpr, tr);
+  };
+  cudaError_t e;
+  if (V <= 1) e = go(residual_rmsnorm_kernel<1>);
+  else if (V <= 2) e = go(residual_rmsnorm_kernel<2>);
+  else if (V <= 4) e = go(residual_rmsnorm_kernel<4>);
+  else e = go(residual_rmsnorm_kernel<kVec>);
+  DAK_CUDA_TRY(e);
+  return DAK_OK;
 }
 
 // rank-major gather [world][N][Ml] -> row-major [N][world * Ml] (16-byte chunks; Ml % 8 == 0)
@@ -368,8 +475,9 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
                                           const void* norm_w, float eps, void* y_norm, int32_t pdl, dak_stream_t stream) {
   if (!partial || !x || !norm_w || !y_norm || rows <= 0 || cols <= 0)
     return fail(DAK_EINVAL, "dak_allreduce_residual_rmsnorm: bad arguments");
-  if (cols % 8 || cols > tp::kThreads * 8 * tp::kVec)
-    return fail(DAK_EUNSUPPORTED, "dak_allreduce_residual_rmsnorm: cols must be a multiple of 8, <= %d", tp::kThreads * 8 * tp::kVec);
+  if (cols % 8 || cols > tp::kThreads * 8 * tp::kVec * tp::kMaxCpr)
+    return fail(DAK_EUNSUPPORTED, "dak_allreduce_residual_rmsnorm: cols must be a multiple of 8, <= %d",
+                tp::kThreads * 8 * tp::kVec * tp::kMaxCpr);
   if (!aligned16(partial) || !aligned16(x) || !aligned16(norm_w) || !aligned16(y_norm))
     return fail(DAK_EINVAL, "dak_allreduce_residual_rmsnorm: pointers must be 16-byte aligned");
   cudaStream_t s = (cudaStream_t)stream;
@@ -384,19 +492,8 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
     else
       comm = nullptr;  // PDL stays allowed below (no NCCL kernel in between)
   }
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = (pdl && !comm) ? 1 : 0;  // NCCL kernels are not PDL-aware
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(rows);
-  cfg.blockDim = dim3(tp::kThreads);
-  cfg.stream = s;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_rmsnorm_kernel, (const __nv_bfloat16*)partial, (__nv_bfloat16*)x,
-                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm,
-                                  (const float*)nullptr, 1, (int)rows));
-  return DAK_OK;
+  return tp::launch_residual_rmsnorm((const __nv_bfloat16*)partial, nullptr, 1, x, rows, cols, norm_w, eps, y_norm,
+                                     pdl && !comm, s);  // NCCL kernels are not PDL-aware
 }
 
 }  // extern "C"
@@ -406,19 +503,8 @@ dak_status dak_allreduce_residual_rmsnorm(void* comm, void* partial, void* x, in
 dak_status dak::residual_rmsnorm_part(const float* part, int32_t S, void* x, int32_t rows, int32_t cols,
                                       const void* norm_w, float eps, void* y_norm, int32_t pdl, void* stream) {
   if (!part || S < 1 || !x || !norm_w || !y_norm || rows <= 0 || cols <= 0 || cols % 8 ||
-      cols > tp::kThreads * 8 * tp::kVec || !aligned16(part) || !aligned16(x) || !aligned16(norm_w) || !aligned16(y_norm))
+      cols > tp::kThreads * 8 * tp::kVec * tp::kMaxCpr || !aligned16(part) || !aligned16(x) || !aligned16(norm_w) ||
+      !aligned16(y_norm))
     return fail(DAK_EINVAL, "residual_rmsnorm_part: bad arguments");
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(rows);
-  cfg.blockDim = dim3(tp::kThreads);
-  cfg.stream = (cudaStream_t)stream;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, tp::residual_rmsnorm_kernel, (const __nv_bfloat16*)nullptr, (__nv_bfloat16*)x,
-                                  (int)cols, (const __nv_bfloat16*)norm_w, eps, (__nv_bfloat16*)y_norm, part, (int)S,
-                                  (int)rows));
-  return DAK_OK;
+  return tp::launch_residual_rmsnorm(nullptr, part, S, x, rows, cols, norm_w, eps, y_norm, pdl != 0, (cudaStream_t)stream);
 }

@@ -155,7 +155,8 @@ def version() -> str:
     return lib.dak_version().decode()
 
 
-TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed", 7: "splitk_reduce", 8: "prefill"}
+TRACE_KINDS = {1: "linear", 2: "attention", 3: "combine", 4: "append", 5: "layernorm", 6: "embed", 7: "splitk_reduce", 8: "prefill",
+               9: "residual_norm", 10: "silu_mul"}
 
 
 def trace_enable(dev_buf, max_launches: int):
