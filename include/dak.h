@@ -487,7 +487,9 @@ dak_status dak_kv_migrate(const int32_t* moves, int32_t n_moves, int32_t Hkv, in
 /* Llama decode KV write with rotary positions (BASELINE configs[2] model): for every request b,
  * rotate q (in place, all Hq heads) and k of the new token at positions[b] (rotate-half pairs
  * (i, i + d/2), angle pos / theta^(2i/d)), then write the rotated k and v rows into the pools at
- * positions[b] like dak_kv_append. qkv: [B, row_stride] bf16 rows holding q | k | v. */
+ * positions[b] like dak_kv_append. qkv: [B, row_stride] bf16 rows holding q | k | v.
+ * With pdl = 1, positions and block_table are read before the dependency wait: they must not be
+ * written by the kernel launched just before (they are step inputs). */
 dak_status dak_rope_kv_append(void* qkv, int64_t row_stride, int32_t B, int32_t Hq, int32_t Hkv, int32_t d,
                              const int32_t* positions, float rope_theta, const int32_t* block_table, int32_t page_size,
                              int32_t max_pages, void* k_hbm, void* v_hbm, void* k_host, void* v_host, int32_t pdl,

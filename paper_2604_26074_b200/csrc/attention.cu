@@ -130,16 +130,19 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   // then the first block-table entry of every (request, chunk) pair); pref[i] holds the pair's flags
   // (bit 0: the chunk exists, bit 1: its first page is on the host) until the scan overwrites it
   for (int b = threadIdx.x; b < p.B; b += kThreads) s_len[b] = p.seq_lens[b];
-  __syncthreads();
   {
+    // seq_lens and the first block-table entry of every pair are loaded together (the entry of a
+    // chunk beyond the request's length is read but ignored: c * chunk_pages < max_pages always):
+    // one round trip, not two
     int cnt = 0;
 #pragma unroll 4
     for (int i = threadIdx.x; i < n_pairs; i += kThreads) {
       const int b = i / p.max_chunks, c = i - b * p.max_chunks;
-      const int npg = (s_len[b] + p.page - 1) / p.page;
+      const int L = p.seq_lens[b];
+      const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages];
+      const int npg = (L + p.page - 1) / p.page;
       int f = 0;
       if (c * p.chunk_pages < npg) {
-        const uint32_t e = (uint32_t)p.block_table[(long long)b * p.max_pages + c * p.chunk_pages];
         f = 1 | ((e & kHostBit) ? 2 : 0);
         cnt += f >> 1;
       }
@@ -459,15 +462,18 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
 }
 
 // merge chunk partials: out[b, h, :] = sum_c w_c o_c / sum_c w_c, w_c = 2^(lse_c - max lse).
-// One 512-thread CTA per (b, q head): warp j accumulates chunks c = j, j + 16, ... with a running
-// max (lane = 4 dims, float4 loads, several chunks in flight), then the 16 warp partials are
-// rescaled to the common max and summed in warp order (16 warps: one L2 round trip for 128 chunks).
-// The order depends only on the chunk count (bitwise r-invariant).
-constexpr int kCombineThreads = 512;
-__global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p) {
-  __shared__ float s_red[kCombineThreads / 32];
-  __shared__ float4 s_acc[kCombineThreads / 32][kD / 4];
-  __shared__ float s_den[kCombineThreads / 32];
+// One CTA of W warps per (b, q head): warp j accumulates chunks c = j, j + W, ... with a running
+// max (lane = 4 dims, float4 loads, several chunks in flight), then the W warp partials are
+// rescaled to the common max and summed in warp order. W = 4 when a request has <= 16 chunks (the
+// decode steps' usual split: B * Hq CTAs fit one wave beside the attention kernel's; 16-warp CTAs
+// took two waves at b64, 3.3 us from the attention's end to the last CTA's start), else 16 (one
+// L2 round trip for 128 chunks). The order depends only on the chunk count and max_chunks
+// (bitwise r-invariant).
+template <int W>
+__global__ void __launch_bounds__(W * 32) combine_kernel(const Params p) {
+  __shared__ float s_red[W];
+  __shared__ float4 s_acc[W][kD / 4];
+  __shared__ float s_den[W];
   if (threadIdx.x == 0) tstamp(p.trace2, 0);
   grid_dep_launch();
   grid_dep_wait();
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p
   float m = -INFINITY, den = 0.f;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
-  for (int c = warp; c < nch; c += kCombineThreads / 32) {
+  for (int c = warp; c < nch; c += W) {
     const long long u = base + (long long)c * p.G;
     const float ls = p.part_lse[u];
     const float4 v = reinterpret_cast<const float4*>(p.part_o + u * kD)[lane];
@@ -507,7 +513,7 @@ __global__ void __launch_bounds__(kCombineThreads) combine_kernel(const Params p
   }
   __syncthreads();
   if (threadIdx.x < kD / 4) {
-    const int nw = min(nch, kCombineThreads / 32);  // warps that own a chunk
+    const int nw = min(nch, W);  // warps that own a chunk
     float M = s_red[0];
     for (int w = 1; w < nw; ++w) M = fmaxf(M, s_red[w]);
     float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -595,11 +601,14 @@ __global__ void __launch_bounds__(64) rope_append_kernel(__nv_bfloat16* qkv, lon
                                                          const float* part, int S, int B) {
   if (threadIdx.x == 0) tstamp(tr, 0);
   grid_dep_launch();
-  grid_dep_wait();
   const int H3 = Hq + 2 * Hkv;
   const int b = blockIdx.x / H3, hh = blockIdx.x % H3;
   const int i = threadIdx.x;  // 0 .. 63
+  // positions and the block table are step inputs (not written by the previous kernel): their
+  // loads overlap the dependency wait
   const int ps = pos[b];
+  const uint32_t e = hh >= Hq ? (uint32_t)block_table[(long long)b * max_pages + ps / page] : 0u;
+  grid_dep_wait();
   __nv_bfloat16* v = qkv + (long long)b * stride + (long long)hh * kD;
   float x1, x2;
   if (part) {
@@ -646,7 +655,6 @@ __global__ void __launch_bounds__(64) rope_append_kernel(__nv_bfloat16* qkv, lon
   if (hh >= Hq) {  // k or v head: append at position ps
     const bool is_k = hh < Hq + Hkv;
     const int g = is_k ? hh - Hq : hh - Hq - Hkv;
-    const uint32_t e = (uint32_t)block_table[(long long)b * max_pages + ps / page];
     const long long idx = (long long)(e & ~kHostBit);
     const bool eh = (e & kHostBit) != 0;
     const int t = ps % page;
@@ -800,12 +808,13 @@ dak_status dak_attention(const dak_attention_args* args, dak_stream_t stream) {
   if (!need_combine) return DAK_OK;
   cudaLaunchConfig_t c2{};
   c2.gridDim = dim3(args->B * args->Hq);
-  c2.blockDim = dim3(attn::kCombineThreads);
+  const bool small = pl.p.max_chunks <= 16;
+  c2.blockDim = dim3(small ? 4 * 32 : 16 * 32);
   c2.dynamicSmemBytes = 0;
   c2.stream = (cudaStream_t)stream;
   c2.attrs = attr;
   c2.numAttrs = 1;
-  DAK_CUDA_TRY(cudaLaunchKernelEx(&c2, attn::combine_kernel, pl.p));
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&c2, small ? attn::combine_kernel<4> : attn::combine_kernel<16>, pl.p));
   return DAK_OK;
 }
 
