@@ -167,10 +167,13 @@ def test_rmsnorm_and_silu_mul_kernels():
     assert_bf16_ulps(got2, ref2, floor=1e-6)
 
 
-@pytest.mark.parametrize("rows,cols", [(4, 8192), (3, 520), (2, 16384)])
+@pytest.mark.parametrize("rows,cols", [(4, 8192), (3, 520), (2, 16384), (2, 64), (3, 2056), (3, 5000), (2, 6152),
+                                       (2, 28672), (1, 65536), (1, 131072)])
 def test_allreduce_residual_rmsnorm_kernel(rows, cols):
     """x += partial (bf16 RNE) and y = RMSNorm(x) * w in one kernel (1-rank: no exchange), vs the
-    oracle's residual add + rmsnorm; y aliasing partial (as in the Llama layer) gives the same."""
+    oracle's residual add + rmsnorm; y aliasing partial (as in the Llama layer) gives the same.
+    The column counts cover every launch shape of the kernel: 1, 2, 3, 4 and 8 CTAs per row (a
+    cluster exchanging the row's sum of squares) and 1, 2, 4 and 8 chunks of 8 columns per thread."""
     import torch
     from paper_2604_26074_b200 import dak
     from tests.gpu_util import to_dev, from_dev
