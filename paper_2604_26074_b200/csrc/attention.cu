@@ -117,11 +117,12 @@ __global__ void __launch_bounds__(kThreads, 1) split_attention_kernel(const Para
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int page_bytes = p.page * kD * 2;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kWarps * kMaxSlots; ++s) mbar_init(&full[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    tstamp(p.trace, 0);
-  }
+  // each warp's ring barriers, one per lane, by the warp itself (128 serial inits by one thread
+  // sat on the kernel's pre-wait critical path)
+  if (lane < kMaxSlots) mbar_init(&full[warp * kMaxSlots + lane], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  if (threadIdx.x == 0) tstamp(p.trace, 0);
   grid_dep_launch();
   const int n_pairs = p.B * p.max_chunks;
   // CTA roles (one tier per SM): given, or chosen below from the block table (auto)
