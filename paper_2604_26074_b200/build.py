@@ -35,6 +35,7 @@ SOURCES = [
     ("linear.cu", ["-DDAK_LINEAR_PART=3"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=4"]),
     ("linear.cu", ["-DDAK_LINEAR_PART=5"]),
+    ("linear.cu", ["-DDAK_LINEAR_PART=6"]),
     ("attention.cu", []),
     ("prefill.cu", []),
     ("layer.cu", []),

@@ -47,6 +47,9 @@ constexpr int kSmemBudget = 227 * 1024;
 
 struct __align__(64) Params {
   CUtensorMap xmap;  // x [N, K] viewed as (64 elements, N rows, K/64 atoms), 128-byte swizzle
+  // CTA-pair GEMM: the packed weight tiers [0 HBM, 1 host] as (64 elements, tier rows, K/64 chunks),
+  // no swizzle (DAK-KC rows are stored 128B-swizzled), box (64, 128, 1); rows past the tier zero-fill
+  alignas(64) CUtensorMap wmap[2];
   const char* w_host;
   const char* w_hbm;
   long long M, K, h;
@@ -72,6 +75,8 @@ struct __align__(64) Params {
   int pair;         // tcgen05, N > 512: groups of `pair` CTAs share rows, rank r computes columns [512 r, 512 r + 512)
   int wmc;          // group mode: the group is one cluster and rank 0 multicasts each W tile to all of it
   int swap;         // tcgen05 swapped operands (umma_swap_kernel): batch = MMA M, weight rows = MMA N
+  int pair2;        // CTA-pair kernel (umma_pair_kernel, cta_group::2): 0 off, else batch columns per pair tile
+  int p2_hp, p2_ct; // CTA-pair kernel: host-tier row pairs (256 rows each), batch-column tiles
   int kblock;       // split-K item rows (128, or 256 when swapped)
   int rgran;        // row-partition granule (1; 8 for the tcgen05 path: 8-row swizzle atoms)
   uint32_t tmem_cols;  // tcgen05 path: TMEM columns allocated (power of two >= 32)
@@ -1050,6 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_linear_kernel(const __grid_c
   }
 }
 
+
 #if DAK_LINEAR_PART == 5
 // Swapped-operand tcgen05 split GEMM for decode batches (N <= 128), split K: the batch is the MMA's
 // M side (x box of 128 rows, TMA zero-fills rows >= N) and the weight rows are its N side (up to 256
@@ -1434,6 +1440,8 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (path == 1 && N > 4) return fail(DAK_EUNSUPPORTED, "dak_linear: CUDA-core path supports N <= 4");
   const bool force_swap = path == 4;  // force_path 4: tcgen05 with swapped operands (split-K decode form)
   if (force_swap) path = 3;
+  const bool force_pair = path == 5;  // force_path 5: the CTA-pair (cta_group::2) GEMM
+  if (force_pair) path = 3;
   if (path != 1 && path != 2 && path != 3) return fail(DAK_EINVAL, "dak_linear: bad force_path");
   if (path != 3 && N > kMaxN) return fail(DAK_EUNSUPPORTED, "dak_linear: N=%d > %d needs the tcgen05 path (kc = 64)", N, kMaxN);
   if (path == 3) {  // tcgen05: canonical SWIZZLE_128B K-major operands need KC = 64; plain GEMV only
@@ -1475,7 +1483,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (rg > 1) {  // every CTA owns whole 8-row units
     n_host = (int)std::min<long long>(n_host, ceil_div(h, rg));
     n_hbm = (int)std::min<long long>(n_hbm, ceil_div(M - h, rg));
-    if (h > 0 && h % rg) return fail(DAK_EINVAL, "dak_linear: the tcgen05 path needs h %% 8 == 0");
+    if (h > 0 && h % rg && !force_pair) return fail(DAK_EINVAL, "dak_linear: the tcgen05 path needs h %% 8 == 0");
   }
   if (mc > 1) {
     const int nh2 = n_host ? (int)ceil_div(n_host, mc) * mc : 0;
@@ -1681,6 +1689,63 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   p.off_ln = p.off_x + x_slots * p.x_stage_bytes;
   p.res_offset = p.off_ln + ln_bytes;
 
+  // CTA-pair GEMM (umma_pair_kernel): the compute-bound large-N regime. Auto when every row is in
+  // HBM (h == 0) and N > 256 for a plain GEMM: 7168^2 at N = 512 / 1024 / 2048 / 4096 runs 1.12 /
+  // 1.43 / 1.41 / 1.54x faster than the one-CTA forms (tools/pair_bench.py, ~1.06 PFLOP/s); at
+  // N = 256 the two tie. A host tier keeps the split paths (their weight-tile multicast groups cross
+  // the link once per tile, Table 1); cluster >= 2 asks for them explicitly.
+  const bool plain = !a->ln_w && !a->x_swiglu && !a->stats_out;
+  if (force_pair && !(kc == 64 && plain))
+    return fail(DAK_EUNSUPPORTED, "dak_linear: the CTA-pair GEMM needs kc = 64 and a plain GEMM (no pre-norm / SwiGLU / statistics)");
+  if (path == 3 && kc == 64 && plain &&
+      (force_pair || (!c.force_path && N > 256 && h == 0 && c.cluster <= 1 && c.n_cta_hbm <= 0 && c.n_cta_host <= 0))) {
+    int nsm = 0;
+    dak_status st2 = device_sms(&nsm);
+    if (st2 != DAK_OK) return st2;
+    const int NB = N > 256 ? 512 : 256;  // batch columns per pair tile (two N = 256 instructions above 256)
+    const long long HP = ceil_div(h, 256), GP = ceil_div(M - h, 256), CT = ceil_div(N, NB);
+    const long long base = (HP + GP) * CT;  // pair items without a K split
+    const long long C = K / 64;
+    // K splits from (M, N, K, SM count) only (never h: the summation order of a row does not depend
+    // on the tier split): as many as keep every pair item in one wave; fp32 partials need workspace
+    long long S = a->workspace ? std::max<long long>(1, std::min<long long>(std::min<long long>(16, C), (nsm / 2) / base)) : 1;
+    long long kps = ceil_div(C, S);
+    S = ceil_div(C, kps);
+    if (S > 1) {
+      const size_t need = (size_t)S * N * M * 4;
+      if (a->workspace_bytes < (int64_t)need)
+        return fail(DAK_EINVAL, "dak_linear: split-K workspace %lld < %zu", (long long)a->workspace_bytes, need);
+      if (!aligned16(a->workspace)) return fail(DAK_EINVAL, "dak_linear: workspace must be 16-byte aligned");
+      p.part = (float*)a->workspace;
+    }
+    const int per_stage = 16384 * (1 + NB / 256);
+    p.stages = std::min(kMaxStages, (kSmemBudget - 2048) / per_stage);
+    if (c.stages > 0) p.stages = std::max(2, std::min(p.stages, c.stages));
+    p.pair2 = NB;
+    p.p2_hp = (int)HP;
+    p.p2_ct = (int)CT;
+    p.ksplit = (int)S;
+    p.k64_split = (int)kps;
+    p.n8 = 128;  // x TMA box: 128 rows (this CTA's half of a 256-column block)
+    p.x_stage_bytes = 16384 * (NB / 256);
+    p.swap = 0;
+    p.pair = 1;
+    p.wmc = 0;
+    p.mc = 1;
+    p.host_gate = 0;
+    p.n_host = (int)(2 * HP * CT * S);
+    p.n_hbm = (int)(2 * GP * CT * S);
+    p.kblock = 256;
+    out->p = p;
+    out->path = 3;
+    out->nn = 0;
+    out->bucket = 0;
+    out->grid = p.n_host + p.n_hbm;
+    out->smem = 1024 + p.stages * per_stage + 1024;
+    out->rmax_host = HP ? std::min<long long>(h, 128) : 0;
+    out->rmax_hbm = GP ? std::min<long long>(M - h, 128) : 0;
+    return DAK_OK;
+  }
   out->p = p;
   out->path = path;
   out->nn = path == 1 ? N : nt_eff;
@@ -1715,6 +1780,33 @@ static dak_status encode_xmap(Params* p) {
                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DAK_ECUDA, "dak_linear: cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return DAK_OK;
+}
+// CTA-pair GEMM weight maps: a tier's DAK-KC block [K/64 chunks][R rows][64 elements] (rows stored
+// 128B-swizzled by row & 7) as (64 elements, R rows, K/64 chunks), box (64, 128, 1), no swizzle:
+// a box of 128 rows starting at a multiple of 128 lands as the canonical SWIZZLE_128B operand
+static dak_status encode_wmaps(Params* p) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    DAK_CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) return fail(DAK_ECUDA, "dak_linear: cuTensorMapEncodeTiled unavailable");
+    fn = (EncodeTiledFn)f;
+  }
+  const long long R[2] = {p->M - p->h, p->h};
+  const char* base[2] = {p->w_hbm, p->w_host};
+  for (int t = 0; t < 2; ++t) {
+    if (R[t] <= 0 || !base[t]) continue;
+    const cuuint64_t dims[3] = {64, (cuuint64_t)R[t], (cuuint64_t)(p->K / 64)};
+    const cuuint64_t strides[2] = {128, (cuuint64_t)R[t] * 128};
+    const cuuint32_t box[3] = {64, 128, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = fn(&p->wmap[t], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, (void*)base[t], dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(DAK_ECUDA, "dak_linear: weight tensor map failed (%d)", (int)r);
+  }
   return DAK_OK;
 }
 
@@ -1783,6 +1875,252 @@ static dak_status launch_mma_xf(const Plan& pl, cudaStream_t s, int pdl) {
   return launch_mma<NT, 0>(pl, s, pdl);
 }
 
+#if DAK_LINEAR_PART == 6
+// ================================================================================================
+// CTA-pair tcgen05 GEMM for the compute-bound large-N regime:
+// a cluster of two CTAs on one TPC computes a tile of 256 weight rows x 256 NI batch columns with
+// ONE stream of tcgen05.mma.cta_group::2 instructions (M = 256, N = 256, K = 16) issued by the
+// leader CTA. Each CTA stages ITS 128 weight rows (A) and ITS half of every 256-column x block (B)
+// at the same shared-memory offsets; the tensor cores read both CTAs' operands and each CTA's TMEM
+// receives its 128 rows of D. Measured (tools/umma2_micro.cu): 128 cycles per M = 256 x N = 256 x
+// K = 16 instruction = the full dense rate per SM, where the one-CTA form pays >= 100 cycles per
+// M = 128 instruction; and each SM ingests half the x bytes per FLOP (the bound of the one-CTA form
+// at large N: profiles/r02/s3/f1_large_n_ncu.txt).
+// Items: (tier row pair, batch-column tile, K split), host-tier pairs first (a CTA pair
+// reads one tier); the splits S are fixed by (M, K, N) -- fp32 partials reduced by
+// splitk_reduce_kernel in split order, as the split-K path. Both CTAs' W and x loads are tensor
+// TMAs with .cta_group::2 completing on the LEADER's stage barrier (which expects the pair's bytes);
+// a first version relayed the peer's arrival through a remote mbarrier arrive and ran at ~0.9
+// PFLOP/s instead of ~1.06. Stage release and accumulator completion are tcgen05.commit multicasts
+// to both CTAs.
+constexpr int kPairThreads = 192;  // warp 0 producer, warp 1 MMA issuer (leader) / relay (peer), 2-5 epilogue
+
+__device__ __forceinline__ uint32_t cta_rank_in_cluster() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{ .reg .pred p; setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p; }" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {  // arrive on `bar` in both CTAs
+  asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   su32(bar)),
+               "h"((uint16_t)3)
+               : "memory");
+}
+// 3-D tensor TMA into this CTA's shared memory completing on a barrier of the CTA pair (shared::cluster
+// address, e.g. the leader's via mapa)
+__device__ __forceinline__ void tma_3d_2sm(void* dst, uint64_t tmap, int c0, int c1, int c2, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          su32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+
+template <int NI>  // 256-column MMA instructions per K step: pair tile = 256 rows x 256 NI columns
+__global__ void __launch_bounds__(kPairThreads, 1) umma_pair_kernel(const __grid_constant__ Params p) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);  // [kMaxStages] leader: the pair's stage landed
+  uint64_t* empty = full + kMaxStages;                  // [kMaxStages] the pair's MMAs read the stage
+  uint64_t* done = empty + kMaxStages;                  // accumulators complete
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + 512);
+  const uint32_t rank = cta_rank_in_cluster();
+  const int item = (int)(blockIdx.x >> 1);
+  const int S = p.ksplit > 1 ? p.ksplit : 1;
+  const int CT = p.p2_ct;
+  const int host_items = p.p2_hp * CT * S;
+  const bool host = item < host_items;
+  const int it = host ? item : item - host_items;
+  const int ks = it % S;
+  const int ct = (it / S) % CT;
+  const int rp = it / (S * CT);
+  const long long R_tier = host ? p.h : p.M - p.h;
+  const long long rb = (long long)rp * 256 + 128 * (long long)rank;  // this CTA's first row in its tier
+  const int R = (int)max(0LL, min(128LL, R_tier - rb));
+  const char* wsrc = host ? p.w_host : p.w_hbm;
+  const long long chunk_stride = R_tier * 128;
+  const int C = (int)(p.K / 64);
+  const int kbeg = ks * p.k64_split;
+  const int kend = min(C, kbeg + p.k64_split);
+  const int nch = kend - kbeg;
+  const int slots = p.stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t kW = 16384, kX = 16384 * NI;  // per-stage bytes: 128 rows x 64 K, NI x 128 x rows x 64 K
+  unsigned char* wring = smem + 1024;
+  unsigned char* xring = smem + 1024 + (size_t)slots * kW;
+  const int col0 = ct * 256 * NI;  // the tile's first batch column
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kMaxStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)), "r"(256u * NI)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers and TMEM exist before any remote arrive / MMA
+  tc_fence_after();
+  if (threadIdx.x == 0) tstamp(p.trace, 0);
+  grid_dep_launch();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    if (lane == 0 && nch > 0) {  // producer: this CTA's W rows + its halves of the x blocks per K chunk
+      // both CTAs' loads complete on the LEADER's full barrier (.cta_group::2), which expects the
+      // pair's bytes; rows past the tier are zero-filled by the tensor map
+      const uint64_t xmap = reinterpret_cast<uint64_t>(&p.xmap);
+      const uint64_t wmap = reinterpret_cast<uint64_t>(&p.wmap[host ? 1 : 0]);
+      asm volatile("prefetch.tensormap [%0];" ::"l"(xmap) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(wmap) : "memory");
+      const int pro = min(slots, nch);
+      auto lead_bar = [&](int slot) {
+        uint32_t r;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(su32(&full[slot])), "r"(0));
+        return r;
+      };
+      auto load_w = [&](int slot, int i) {
+        if (rank == 0) mbar_expect_tx(&full[slot], 2u * (kW + kX));
+        tma_3d_2sm(wring + (size_t)slot * kW, wmap, 0, (int)rb, kbeg + i, lead_bar(slot));
+      };
+      auto load_x = [&](int slot, int i) {
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+          tma_3d_2sm(xring + (size_t)slot * kX + j * 16384, xmap, 0, col0 + 256 * j + 128 * (int)rank, kbeg + i,
+                     lead_bar(slot));
+      };
+      for (int i = 0; i < pro; ++i) load_w(i, i);  // weights do not depend on the previous kernel
+      grid_dep_wait();  // x is produced by the previous kernel
+      tstamp(p.trace, 1);
+      for (int i = 0; i < pro; ++i) load_x(i, i);
+      int s = pro == slots ? 0 : pro;
+      uint32_t ph = pro == slots ? 1u : 0u;
+      for (int i = pro; i < nch; ++i) {
+        mbar_spin(&empty[s], ph ^ 1u);
+        load_w(s, i);
+        load_x(s, i);
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {  // MMA issuer: the whole warp walks the ring, one elected lane issues
+      const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+      const uint32_t wr = su32(wring), xr = su32(xring);
+      uint32_t leader;
+      asm volatile("{ .reg .pred P; elect.sync _|P, 0xffffffff; selp.u32 %0, 1, 0, P; }" : "=r"(leader));
+      int s = 0;
+      uint32_t ph = 0;
+      for (int i = 0; i < nch; ++i) {
+        mbar_spin(&full[s], ph);  // both CTAs' operands of stage s landed
+        tc_fence_after();
+        if (leader) {
+          const uint32_t ws = wr + (uint32_t)s * kW, xs = xr + (uint32_t)s * kX;
+#pragma unroll
+          for (int j = 0; j < NI; ++j)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              umma2_bf16(tmem + 256u * j, umma_desc_sw128(ws + k * 32), umma_desc_sw128(xs + j * 16384 + k * 32), idesc,
+                         (i | k) != 0);
+          umma2_commit_both(&empty[s]);  // both CTAs may refill slot s once these MMAs have read it
+        }
+        __syncwarp();
+        if (++s == slots) { s = 0; ph ^= 1u; }
+      }
+      if (leader) umma2_commit_both(done);
+      __syncwarp();
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. = rows of this CTA's 128
+    if (threadIdx.x == 64) {
+      uint32_t ok = 0;
+      while (!ok) {
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok) : "r"(su32(done)), "r"(0u) : "memory");
+        if (!ok) __nanosleep(256);
+      }
+    }
+    asm volatile("bar.sync 2, 128;" ::: "memory");
+    tc_fence_after();
+    grid_dep_wait();  // residual / y may belong to the previous kernel
+    const int q = warp & 3;
+    const int r = 32 * q + lane;
+    const long long m = (host ? 0 : p.h) + rb + r;
+    const bool ok = r < R && nch > 0;
+    const float bias = (ok && p.bias && S == 1) ? __bfloat162float(p.bias[m]) : 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < 256 * NI; c0 += 8) {
+      uint32_t v[8];
+      tmem_ld8(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c0, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!ok) continue;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int n = col0 + c0 + e;
+        if (n >= p.N) continue;
+        const float acc = __uint_as_float(v[e]);
+        if (S > 1) {  // raw fp32 partial; bias / act / residual in splitk_reduce_kernel
+          p.part[((size_t)ks * p.N + n) * p.M + m] = acc;
+        } else {
+          float o = acc + bias;
+          if (p.act == DAK_ACT_RELU) o = fmaxf(o, 0.f);
+          if (p.residual) o += __bfloat162float(p.residual[(long long)n * p.ldy + m]);
+          p.y[(long long)n * p.ldy + m] = __float2bfloat16_rn(o);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // neither CTA leaves while the pair's MMAs / remote arrives may still target it
+  if (threadIdx.x == 32 && p.trace) tstamp(p.trace, 3);
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256u * NI) : "memory");
+  }
+}
+
+template <int NI>
+static dak_status launch_pair_t(const Plan& pl, cudaStream_t stream, int pdl) {
+  auto kern = umma_pair_kernel<NI>;
+  static int smem_set = 0;
+  if (!smem_set) {
+    DAK_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget));
+    smem_set = 1;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(kPairThreads);
+  cfg.dynamicSmemBytes = pl.smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  DAK_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, pl.p));
+  return DAK_OK;
+}
+dak_status launch_part_pair(const Plan& pl, cudaStream_t s, int pdl) {
+  return pl.p.pair2 > 256 ? launch_pair_t<2>(pl, s, pdl) : launch_pair_t<1>(pl, s, pdl);
+}
+#endif
+
 // The kernel instances are spread over several translation units (this file compiled with
 // DAK_LINEAR_PART = 0..4, see build.py) so they compile in parallel; part 0 holds the host code.
 dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl);
@@ -1792,6 +2130,7 @@ dak_status launch_part_nt4(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_nt8(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl);
 dak_status launch_part_swap(const Plan& pl, cudaStream_t s, int pdl);
+dak_status launch_part_pair(const Plan& pl, cudaStream_t s, int pdl);
 #if DAK_LINEAR_PART == 0
 dak_status launch_part_fma(const Plan& pl, cudaStream_t s, int pdl) {
   switch (pl.nn) {
@@ -1878,7 +2217,7 @@ dak_status launch_part_umma(const Plan& pl, cudaStream_t s, int pdl) {
 static dak_status launch(const Plan& pl, cudaStream_t s, int pdl) {
   if (pl.grid == 0) return DAK_OK;
   if (pl.path == 1) return launch_part_fma(pl, s, pdl);
-  if (pl.path == 3) return pl.p.swap ? launch_part_swap(pl, s, pdl) : launch_part_umma(pl, s, pdl);
+  if (pl.path == 3) return pl.p.pair2 ? launch_part_pair(pl, s, pdl) : pl.p.swap ? launch_part_swap(pl, s, pdl) : launch_part_umma(pl, s, pdl);
   switch (pl.nn) {
     case 1: return launch_part_nt1(pl, s, pdl);
     case 2: return launch_part_nt2(pl, s, pdl);
@@ -1972,7 +2311,12 @@ dak_status dak_linear_cta_rows(const dak_linear_args* args, int32_t cta, int32_t
   const long long n = host ? pl.p.n_host : pl.p.n_hbm;
   const long long off = host ? 0 : args->h;
   long long rb, re;
-  if (pl.path == 3 && pl.p.ksplit > 1) {  // split-K: CTA = (row block of kblock rows, K split) item
+  if (pl.p.pair2) {  // CTA-pair GEMM: CTA = (pair item, rank); item = (row pair, column tile, K split)
+    const long long item = j / 2, rank = j % 2;
+    const long long rp = item / ((long long)pl.p.p2_ct * std::max(1, pl.p.ksplit));
+    rb = std::min<long long>(R, rp * 256 + 128 * rank);
+    re = std::min<long long>(R, rb + 128);
+  } else if (pl.path == 3 && pl.p.ksplit > 1) {  // split-K: CTA = (row block of kblock rows, K split) item
     rb = std::min<long long>(R, (j / pl.p.ksplit) * pl.p.kblock);
     re = std::min<long long>(R, rb + pl.p.kblock);
   } else if (pl.p.pair > 1) {  // N > 512: groups of `pair` CTAs share one row range
@@ -1998,6 +2342,7 @@ dak_status dak::linear_enqueue(const dak_linear_args* args, void* stream, bool d
   if (st != DAK_OK) return st;
   if (pl.grid && !(pl.p.y)) return fail(DAK_EINVAL, "dak_linear: y NULL");
   if (pl.grid && (st = lin::encode_xmap(&pl.p)) != DAK_OK) return st;
+  if (pl.grid && pl.p.pair2 && (st = lin::encode_wmaps(&pl.p)) != DAK_OK) return st;
   pl.p.trace = trace_slot(DAK_KIND_LINEAR, args->M, args->K, pl.grid);
   if ((st = lin::launch(pl, (cudaStream_t)stream, args->cfg.pdl)) != DAK_OK) return st;
   const int S = pl.path == 3 && pl.p.ksplit > 1 ? pl.p.ksplit : 1;

@@ -297,7 +297,10 @@ def test_linear_tcgen05_pairs_w_multicast(D, torch, M, K, N, h):
     ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b)
     from tests.gpu_util import assert_close
     assert_close(Kx.bf16_to_f64(ys[1]), ref)
-    assert np.array_equal(ys[0], ys[1])
+    if h > 0:  # (h == 0 without a cluster takes the CTA-pair GEMM: checked against the oracle)
+        assert np.array_equal(ys[0], ys[1])
+    else:
+        assert_close(Kx.bf16_to_f64(ys[0]), ref)
     Wi, xi, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(13, M), kind="int")
     yi = run_linear(D, torch, Wi, xi, h, 64, cluster=2)[0]
     assert np.array_equal(Kx.bf16_to_f64(yi), Kx.round_to_bf16(Kx.split_linear(Wi[:0], Wi, xi)))
@@ -530,3 +533,57 @@ def test_linear_chain_bitwise_vs_single_launches(D, torch, N, kc, h):
         assert int(ws.view(torch.int32).abs().sum()) == 0
     y1 = Kx.round_to_bf16(Kx.linear(Ws[0], x0))
     assert np.array_equal(Kx.bf16_to_f64(ref[0]), y1)
+
+
+def _run_pair(D, torch, W, x, h, bias=None, residual=None, act=0, split=True, **cfg):
+    """One CTA-pair GEMM launch (force_path 5), with the split-K workspace the plan asks for when
+    `split`; returns (y bits, launch info)."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev
+    M, K = W.shape
+    N = x.shape[0]
+    sl = SplitLinear(D, W, h, 64)
+    y = torch.empty((N, M), dtype=torch.int16, device="cuda")
+    # the device copies must outlive the launch (the args hold raw pointers)
+    xd = to_dev(x)
+    bd = to_dev(bias) if bias is not None else None
+    rd = to_dev(residual) if residual is not None else None
+    a = sl.args(xd, y, N, bias=bd, residual=rd, act=act, force_path=5, **cfg)
+    wsb = None
+    if split:
+        a.workspace, a.workspace_bytes = 256, 1 << 40
+        need = D.linear_workspace_size(a)
+        a.workspace, a.workspace_bytes = None, 0
+        if need:
+            wsb = torch.zeros(need, dtype=torch.uint8, device="cuda")
+            a.workspace, a.workspace_bytes = wsb.data_ptr(), need
+    info = D.linear_query(a)
+    D.linear(a)
+    torch.cuda.synchronize()
+    del xd, bd, rd, wsb
+    return from_dev(y), info
+
+
+@pytest.mark.parametrize("M,K,N,h,act,res", [(1024, 1024, 256, 0, 0, False), (700, 2048, 384, 0, 1, True),
+                                             (7168, 512, 1000, 256, 0, False), (300, 256, 520, 40, 0, True),
+                                             (2000, 2048, 130, 0, 0, False), (512, 512, 2048, 128, 1, False),
+                                             (257, 4096, 512, 0, 0, False)])
+def test_linear_cta_pair_gemm(D, torch, M, K, N, h, act, res):
+    """The CTA-pair GEMM (force_path = 5; auto for h == 0 and N > 128): tcgen05.mma.cta_group::2 on
+    256-row x 256/512-column pair tiles, both tiers, ragged M / N, with and without K splits (fp32
+    partials + the reduce kernel), bias / ReLU / residual epilogue -- vs the oracle; integer inputs
+    bitwise exact, and bitwise the same for every tier split h (the splits depend on M, N, K only)."""
+    from tests.gpu_util import assert_close
+    W, x, b = synth.linear_inputs(M, K, N, seed=synth.seed_for(41, M + N), bias=True)
+    r = synth.normal_bf16(synth.rng(M + 3 * N), (N, M), 0.5) if res else None
+    ref = Kx.split_linear(W[:h], W[h:], x, bias_bits=b, act="relu" if act else "none", residual_bits=r)
+    splits = set()
+    for split in (False, True):
+        y, info = _run_pair(D, torch, W, x, h, bias=b, residual=r, act=act, split=split)
+        assert info["path"] == 3 and info["grid"] % 2 == 0
+        splits.add(info["ksplit"])
+        assert_close(Kx.bf16_to_f64(y), ref)
+    Wi, xi, _ = synth.linear_inputs(M, K, N, seed=synth.seed_for(41, M), kind="int")
+    outs = [_run_pair(D, torch, Wi, xi, hh)[0] for hh in sorted({0, h, M // 2, M})]  # any h: no 8-row rule
+    assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(Kx.split_linear(Wi[:0], Wi, xi)))
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
