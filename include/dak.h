@@ -315,7 +315,9 @@ typedef struct {
   int32_t pdl;                /* 1: programmatic dependent launch (weights stream before the   */
                               /*    previous kernel finishes; x/residual read after it)        */
   int32_t force_path;         /* 0 auto, 1 CUDA-core FMA, 2 mma.sync, 3 tcgen05 (kc == 64),     */
-                              /* 4 tcgen05 swapped operands (split-K decode form, N <= 128)     */
+                              /* 4 tcgen05 swapped operands (split-K decode form, N <= 128),    */
+                              /* 5 CTA-pair tcgen05 GEMM (cta_group::2, 256-row pair tiles; auto */
+                              /*   for a plain GEMM with h == 0 and N > 256; plain GEMM only)    */
   int32_t l2_policy;          /* 0: stream weights/KV with the L2 evict_first hint (they are   */
                               /*    read once per step), 1: no hint                              */
   int32_t cluster;            /* dak_linear: CTAs per thread-block cluster sharing ONE fetch of */
