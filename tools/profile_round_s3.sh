@@ -1,7 +1,7 @@
 #!/bin/bash
 # Round-2 session-3 measurement pass (GPU box, one GPU, repo root): GPU tests + smoke, the contract
 # bench line and the reference arm, Llama TP8 lines (64k capacity-forced, 4k all-HBM), the tcgen05
-# prefill sweep, C4 / C5 sweeps, the ncu launch list of one Llama 4k step, and one ncu --set full of
+# prefill sweep, C4 / C5 / Table 1 sweeps, the CTA-pair GEMM bench, the ncu launch list of one Llama 4k step, and one ncu --set full of
 # the prefill kernel.
 set -u
 OUT=gpurun_out/r02c
@@ -17,6 +17,8 @@ timeout 300 python tools/trace_perop.py 8 64 --llama --context 4096 > $OUT/trace
 timeout 600 python tools/prefill_bench.py > $OUT/prefill_bench.jsonl 2> $OUT/prefill_bench.err
 timeout 900 python tools/sweep.py c4 > $OUT/c4.jsonl 2> $OUT/c4.err
 timeout 900 python tools/sweep.py c5 > $OUT/c5.jsonl 2> $OUT/c5.err
+timeout 900 python tools/sweep.py t1 > $OUT/t1.jsonl 2> $OUT/t1.err
+timeout 600 python tools/pair_bench.py > $OUT/pair_bench.jsonl 2> $OUT/pair_bench.err
 KF='regex:linear_kernel|umma_swap|splitk_reduce|split_attention|combine_kernel|embed|append_kernel|norm|residual|silu|rope|row_stats|prefill'
 per() { python -c "import json,sys; d=json.load(open('$1')); print(d['gpu_launches']//d['steps'])"; }
 PERL=$(per $OUT/bench_llama4k.json)
