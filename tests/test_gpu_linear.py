@@ -587,3 +587,45 @@ def test_linear_cta_pair_gemm(D, torch, M, K, N, h, act, res):
     assert np.array_equal(Kx.bf16_to_f64(outs[0]), Kx.round_to_bf16(Kx.split_linear(Wi[:0], Wi, xi)))
     for o in outs[1:]:
         assert np.array_equal(o, outs[0])
+
+
+def test_linear_cta_pair_chain_pdl_and_strided_y(D, torch):
+    """Two CTA-pair GEMMs chained with programmatic dependent launch on one stream, the second
+    reading the first's output as x (its x loads and y / residual accesses come after the dependency
+    wait), the second writing into a wider row-strided y (ldy > M) with a residual -- vs the oracle."""
+    from tests.gpu_util import SplitLinear, to_dev, from_dev, assert_close
+    M1, K1, N = 1024, 768, 320       # y1 [N, M1] becomes x2 (K2 = M1)
+    M2, K2 = 512, 1024
+    g = synth.rng(4711)
+    W1, x1, _ = synth.linear_inputs(M1, K1, N, seed=synth.seed_for(43, 1))
+    W2, _, _ = synth.linear_inputs(M2, K2, N, seed=synth.seed_for(43, 2))
+    ldy = M2 + 64
+    res = synth.normal_bf16(g, (N, ldy), 0.5)
+    sl1, sl2 = SplitLinear(D, W1, 0, 64), SplitLinear(D, W2, 0, 64)
+    x1d = to_dev(x1)
+    y1 = torch.empty((N, M1), dtype=torch.int16, device="cuda")
+    y2 = to_dev(np.zeros((N, ldy), np.uint16))
+    rd = to_dev(res)
+    a1 = sl1.args(x1d, y1, N, pdl=1)
+    a2 = D.linear_args(None, sl2.hbm, M2, K2, 0, 64, N, y1, y2, residual=rd, cfg=dict(pdl=1), ldy=ldy)
+    wss = []
+    for a in (a1, a2):
+        a.workspace, a.workspace_bytes = 256, 1 << 40
+        need = D.linear_workspace_size(a)
+        a.workspace, a.workspace_bytes = None, 0
+        if need:
+            wss.append(torch.zeros(need, dtype=torch.uint8, device="cuda"))
+            a.workspace, a.workspace_bytes = wss[-1].data_ptr(), need
+        assert D.linear_query(a)["kblock"] == 256  # the CTA-pair plan
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            D.linear(a1, s)
+            D.linear(a2, s)
+    torch.cuda.synchronize()
+    y1b = from_dev(y1)
+    assert_close(Kx.bf16_to_f64(y1b), Kx.linear(W1, x1))
+    ref2 = Kx.linear(W2, y1b) + Kx.bf16_to_f64(res)[:, :M2]
+    got2 = from_dev(y2)
+    assert_close(Kx.bf16_to_f64(got2[:, :M2]), ref2)
+    assert np.array_equal(got2[:, M2:], np.zeros((N, ldy - M2), np.uint16))  # columns past M untouched
