@@ -3,14 +3,15 @@
 Default workload (BASELINE.json configs[1]): OPT-30B decode step, batch 8, context 64 (prompt 32 +
 32 decoded), weights split HBM / pinned host memory at the planner's BALANCED ratios
 (every memory-bound op at its turning point B_l/(B_g+B_l)), one CUDA graph per step
-(P:L637). A step = embed -> 48 x (LN, QKV split-GEMM, KV append, split attention + combine,
-O split-GEMM + residual, LN, FC1 split-GEMM + ReLU, FC2 split-GEMM + residual) -> LN -> LM head.
+(P:L637). A step = embed -> 48 x (QKV split-GEMM with the fused pre-norm, split attention with the
+fused KV append, O split-GEMM + residual, FC1 split-GEMM (fused pre-norm) + ReLU, FC2 split-GEMM +
+residual) -> LN -> LM head.
 
 metric: aggregate GB/s = (weight + KV bytes read from HBM and host per step) / step time.
 Also reported: decode tokens/s, per-tier bytes, roofline of the dominant kernel (dak_linear),
 the CPU oracle baseline, clocks, and an end-to-end number with host buffers.
 
-  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload c1]
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload llama3-70b-tp8]
 Under torchrun every rank runs an independent replica (weak scaling, no data-path collective).
 """
 from __future__ import annotations
