@@ -1698,7 +1698,7 @@ static dak_status make_plan(const dak_linear_args* a, Plan* out) {
   if (force_pair && !(kc == 64 && plain))
     return fail(DAK_EUNSUPPORTED, "dak_linear: the CTA-pair GEMM needs kc = 64 and a plain GEMM (no pre-norm / SwiGLU / statistics)");
   if (path == 3 && kc == 64 && plain &&
-      (force_pair || (!c.force_path && N > 256 && h == 0 && c.cluster <= 1 && c.n_cta_hbm <= 0 && c.n_cta_host <= 0))) {
+      (force_pair || (!c.force_path && N > 256 && h == 0 && c.cluster <= 1 && c.n_cta_hbm <= 0))) {
     int nsm = 0;
     dak_status st2 = device_sms(&nsm);
     if (st2 != DAK_OK) return st2;

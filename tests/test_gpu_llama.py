@@ -18,7 +18,8 @@ def _dev(p, torch):
 
 @pytest.mark.parametrize("frac,B,ctx,use_comm,fuse", [(0.0, 3, 70, False, True), (0.3, 2, 150, False, True),
                                                      (0.2, 4, 40, True, True), (0.2, 4, 40, True, False),
-                                                     (0.3, 24, 90, False, None), (0.3, 24, 90, True, None)])
+                                                     (0.3, 24, 90, False, None), (0.3, 24, 90, True, None),
+                                                     (0.0, 300, 70, True, None)])  # B > 256: CTA-pair linears
 def test_llama_step_matches_oracle(frac, B, ctx, use_comm, fuse):
     import torch
     from paper_2604_26074_b200 import dak
